@@ -1,0 +1,148 @@
+/*
+ * vmfilt_b200.h -- C ABI of the B200-native hot path of `vmfilt`
+ * (Kennedy, "vanishing-moment shape filters", arXiv 1912.07133).
+ *
+ * Each entry point replaces one native kernel (or wrapper + kernel) of the
+ * reference package; file:line below are relative to
+ * /root/reference/pkg/src/vmfilt/.  The reference crosses Python -> numba
+ * native code at exactly these points (engine.py:120, engine.py:145); the
+ * matching ctypes binding is shown in INTEGRATION.md.
+ *
+ * Conventions:
+ *   - every array pointer is a DEVICE pointer (cudaMalloc / torch CUDA
+ *     tensor); images are row-major [h][w] with row pitches ldx/ldy in
+ *     ELEMENTS; outputs are caller-allocated and fully written; inputs are
+ *     never modified;
+ *   - work is enqueued on `stream` (a cudaStream_t, NULL = legacy default)
+ *     and is asynchronous; no entry point synchronises the host except
+ *     vmf_detect* when n_det_host != NULL;
+ *   - return codes: VMF_OK, VMF_EVALUE (the reference raises ValueError),
+ *     VMF_ESTABILITY (the reference raises StabilityError, errors.py:32),
+ *     VMF_ECUDA (CUDA launch/runtime failure).  vmf_last_error() gives the
+ *     message of the last failure on the calling thread;
+ *   - results do not depend on launch configuration (chunk count, block
+ *     size): the analogue of tests/test_engine.py:119-128.
+ *   - arithmetic: fp32 loads/stores, fp64 recurrence state and fp64
+ *     accumulation.
+ */
+#ifndef VMFILT_B200_H
+#define VMFILT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { VMF_OK = 0, VMF_EVALUE = 2, VMF_ESTABILITY = 3, VMF_ECUDA = 4 };
+/* input element types */
+enum { VMF_F32 = 0, VMF_U16 = 1 };
+/* stage kinds for vmf_stage */
+enum { VMF_STAGE_FIR = 0, VMF_STAGE_IIR = 1 };
+
+#define VMF_MAX_IIR_ORDER 8    /* polyz.py:494-495 allows K <= 8 */
+#define VMF_MAX_FIR_TAPS 2049   /* taps travel as kernel parameters */
+
+/* A separable stage: FirKernel (design.py:40-77) or ThreePartIIR
+ * (polyz.py:348-405), flattened to plain arrays.  Host pointers. */
+typedef struct vmf_stage {
+  int kind;               /* VMF_STAGE_FIR | VMF_STAGE_IIR               */
+  int n;                  /* FIR: number of taps 2K+1; IIR: order K       */
+  const double *taps;     /* FIR taps h(-K..K) (FirKernel.taps)           */
+  const double *b_plus;   /* IIR b_plus[0..K-1]  (m = 1..K)              */
+  const double *a_plus;   /* IIR a_plus[0..K-1]                          */
+  double b_zero;          /* IIR b_zero                                   */
+  int sign;               /* IIR +1 parity "sym", -1 parity "anti"        */
+} vmf_stage;
+
+const char *vmf_last_error(void);
+int vmf_abi_version(void);
+
+/* Workspace (bytes, device memory) needed by one IIR pass over `lines`
+ * lines of `length` samples of order k. */
+size_t vmf_iir_workspace_bytes(int64_t lines, int64_t length, int k);
+
+/* Three-part IIR along rows: replaces iir_rows (engine.py:137-153) and
+ * _iir_rows_kernel (engine.py:65-102).  Validation identical to
+ * engine.py:139-142: w >= 2K+1 else VMF_EVALUE; all poles strictly inside
+ * the unit circle else VMF_ESTABILITY. */
+int vmf_iir_rows(const void *x, int x_dtype, float *y, int64_t h, int64_t w,
+                 int64_t ldx, int64_t ldy, const double *b_plus,
+                 const double *a_plus, int k, double b_zero, int sign,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/* Three-part IIR along columns: replaces iir_cols (engine.py:156-158)
+ * without the two transposed copies.  Requires h >= 2K+1. */
+int vmf_iir_cols(const void *x, int x_dtype, float *y, int64_t h, int64_t w,
+                 int64_t ldx, int64_t ldy, const double *b_plus,
+                 const double *a_plus, int k, double b_zero, int sign,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/* Centred FIR along rows with replicate edges: replaces conv_rows
+ * (engine.py:112-121) and _conv_rows_kernel (engine.py:35-62).  ntaps odd,
+ * ntaps <= w else VMF_EVALUE (engine.py:115-118). */
+int vmf_conv_rows(const void *x, int x_dtype, float *y, int64_t h, int64_t w,
+                  int64_t ldx, int64_t ldy, const double *taps, int ntaps,
+                  void *stream);
+
+/* FIR along columns: replaces conv_cols (engine.py:124-126). ntaps <= h. */
+int vmf_conv_cols(const void *x, int x_dtype, float *y, int64_t h, int64_t w,
+                  int64_t ldx, int64_t ldy, const double *taps, int ntaps,
+                  void *stream);
+
+/* Laplacian L = lap_scale * (D20 + D02) with the (1,-2,1) stencil of
+ * fir_vm_bank(3)[2] and replicate edges: replaces derivative_field's
+ * D20/D02 pair (engine.py:218-227) and the trace of blob.py:161.
+ * lap_scale = 1 reproduces the reference; sigma^2 gives the scale-normalised
+ * response used by the scale-space NMS. */
+int vmf_laplacian(const float *b, float *l, int64_t h, int64_t w, int64_t ldb,
+                  int64_t ldl, float lap_scale, void *stream);
+
+/* Workspace for vmf_detect3x3 / vmf_blur_lap_detect. */
+size_t vmf_detect_workspace_bytes(int64_t h, int64_t w);
+
+/* Threshold + 3x3 NMS (stage 4; conventions of
+ * blob.py:162-168): a pixel is a detection iff it is strictly greater (or
+ * strictly smaller) than its 8 edge-replicated neighbours and
+ * |L| >= frac * max|L| over the frame.  Detections are written sorted by
+ * (y, x): det_yx[2i] = y, det_yx[2i+1] = x, det_val[i] = L(y, x).
+ * *n_det_dev (device int64) receives the total count (may exceed cap);
+ * *thr_dev (device float, may be NULL) the threshold used.  If n_det_host
+ * is non-NULL the call synchronises `stream` and stores the count there. */
+int vmf_detect3x3(const float *l, int64_t h, int64_t w, int64_t ldl,
+                  float frac, int32_t *det_yx, float *det_val, int64_t cap,
+                  int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host,
+                  void *ws, size_t ws_bytes, void *stream);
+
+/* Whole hot path in one call: B = cols(rows(x, row_stage), col_stage);
+ * L = lap_scale * Laplacian(B); detections as vmf_detect3x3 (frac <= 0
+ * skips detection).  blur_out / lap_out may be NULL (pitch = w).  This is derivative_field + trace + stage 4 fused
+ * (engine.py:205-228, blob.py:158-168). */
+size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w,
+                                           const vmf_stage *row_stage,
+                                           const vmf_stage *col_stage);
+int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w,
+                        int64_t ldx, const vmf_stage *row_stage,
+                        const vmf_stage *col_stage, float lap_scale, float frac,
+                        float *blur_out, float *lap_out, int32_t *det_yx,
+                        float *det_val, int64_t cap, int64_t *n_det_dev,
+                        float *thr_dev, int64_t *n_det_host, void *ws,
+                        size_t ws_bytes, void *stream);
+
+/* Scale-space 3x3x3 NMS over a stack of ns normalised responses
+ * N[s] (each h x w, pitch ldn, planes spaced plane_stride elements):
+ * strict extremum against the 8 in-scale and the 9+9 adjacent-scale
+ * neighbours (one-sided at the first/last scale), |N| >= frac*max|N| over
+ * the whole stack.  Detections sorted by (s, y, x): det_syx[3i..3i+2]. */
+size_t vmf_detect3x3x3_workspace_bytes(int64_t ns, int64_t h, int64_t w);
+int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w,
+                    int64_t ldn, int64_t plane_stride, float frac,
+                    int32_t *det_syx, float *det_val, int64_t cap,
+                    int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host,
+                    void *ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VMFILT_B200_H */

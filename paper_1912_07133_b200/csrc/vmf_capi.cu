@@ -1,0 +1,193 @@
+// vmf_capi.cu -- extern "C" entry points of libvmfilt_b200.so (declared in
+// include/vmfilt_b200.h).  Host-side validation mirrors the reference
+// wrappers (engine.py:105-109, 115-118, 139-142) before anything is launched.
+#include <cstring>
+
+#include "vmf_common.cuh"
+#include "vmf_iir.cuh"
+#include "vmf_stage4.cuh"
+
+namespace vmf {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_status(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(VMF_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return VMF_OK;
+}
+
+static size_t align256(size_t n) { return (n + 255) & ~(size_t)255; }
+
+static int check_stage(const vmf_stage *s, int64_t length, const char *axis) {
+  if (!s) return fail(VMF_EVALUE, "%s stage is NULL", axis);
+  if (s->kind == VMF_STAGE_FIR) {
+    if (!s->taps || s->n < 1 || s->n % 2 == 0)
+      return fail(VMF_EVALUE, "taps must have odd length 2K+1");
+    if (s->n > length)
+      return fail(VMF_EVALUE, "kernel length %d exceeds row length %lld", s->n, (long long)length);
+    return VMF_OK;
+  }
+  if (s->kind == VMF_STAGE_IIR) {
+    if (s->n < 0 || s->n > VMF_MAX_IIR_ORDER)
+      return fail(VMF_EVALUE, "IIR order %d outside 0..%d", s->n, VMF_MAX_IIR_ORDER);
+    if (s->n > 0 && (!s->b_plus || !s->a_plus)) return fail(VMF_EVALUE, "IIR coefficients NULL");
+    if (length < 2 * s->n + 1)
+      return fail(VMF_EVALUE, "row length %lld < 2K+1 = %d", (long long)length, 2 * s->n + 1);
+    if (s->n > 0 && !poles_inside_unit_circle(s->a_plus, s->n))
+      return fail(VMF_ESTABILITY, "recursion has a pole on or outside the unit circle");
+    return VMF_OK;
+  }
+  return fail(VMF_EVALUE, "unsupported stage type %d", s->kind);
+}
+
+static size_t stage_ws(const vmf_stage *s, int64_t lines, int64_t length) {
+  if (s && s->kind == VMF_STAGE_IIR) return iir_workspace_bytes(lines, length, s->n);
+  return 0;
+}
+
+template <int O>
+static int run_stage(const vmf_stage *s, const void *x, int dt, float *y, int64_t h, int64_t w,
+                     int64_t ldx, int64_t ldy, void *ws, size_t wsb, cudaStream_t st) {
+  if (s->kind == VMF_STAGE_FIR) return fir_pass<O>(x, dt, y, h, w, ldx, ldy, s->taps, s->n, st);
+  return iir_pass<O>(x, dt, y, h, w, ldx, ldy, s->b_plus, s->a_plus, s->n, s->b_zero, s->sign,
+                     ws, wsb, st);
+}
+
+}  // namespace vmf
+
+using namespace vmf;
+
+extern "C" {
+
+const char *vmf_last_error(void) { return g_err; }
+int vmf_abi_version(void) { return 1; }
+
+size_t vmf_iir_workspace_bytes(int64_t lines, int64_t length, int k) {
+  return iir_workspace_bytes(lines, length, k);
+}
+
+int vmf_iir_rows(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t ldx,
+                 int64_t ldy, const double *b_plus, const double *a_plus, int k, double b_zero,
+                 int sign, void *ws, size_t ws_bytes, void *stream) {
+  return iir_pass<ROWS>(x, x_dtype, y, h, w, ldx, ldy, b_plus, a_plus, k, b_zero, sign, ws,
+                        ws_bytes, (cudaStream_t)stream);
+}
+
+int vmf_iir_cols(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t ldx,
+                 int64_t ldy, const double *b_plus, const double *a_plus, int k, double b_zero,
+                 int sign, void *ws, size_t ws_bytes, void *stream) {
+  return iir_pass<COLS>(x, x_dtype, y, h, w, ldx, ldy, b_plus, a_plus, k, b_zero, sign, ws,
+                        ws_bytes, (cudaStream_t)stream);
+}
+
+int vmf_conv_rows(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t ldx,
+                  int64_t ldy, const double *taps, int ntaps, void *stream) {
+  return fir_pass<ROWS>(x, x_dtype, y, h, w, ldx, ldy, taps, ntaps, (cudaStream_t)stream);
+}
+
+int vmf_conv_cols(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t ldx,
+                  int64_t ldy, const double *taps, int ntaps, void *stream) {
+  return fir_pass<COLS>(x, x_dtype, y, h, w, ldx, ldy, taps, ntaps, (cudaStream_t)stream);
+}
+
+int vmf_laplacian(const float *b, float *l, int64_t h, int64_t w, int64_t ldb, int64_t ldl,
+                  float lap_scale, void *stream) {
+  if (h < 1 || w < 1) return fail(VMF_EVALUE, "image must be a 2-D array");
+  if (ldb < w || ldl < w) return fail(VMF_EVALUE, "row pitch smaller than width");
+  return laplacian(b, ldb, l, ldl, h, w, lap_scale, nullptr, (cudaStream_t)stream);
+}
+
+size_t vmf_detect_workspace_bytes(int64_t h, int64_t w) { return detect_workspace_bytes(1, h, w); }
+
+int vmf_detect3x3(const float *l, int64_t h, int64_t w, int64_t ldl, float frac, int32_t *det_yx,
+                  float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev,
+                  int64_t *n_det_host, void *ws, size_t ws_bytes, void *stream) {
+  if (h < 1 || w < 1) return fail(VMF_EVALUE, "image must be a 2-D array");
+  if (ldl < w) return fail(VMF_EVALUE, "row pitch smaller than width");
+  return detect(l, ldl, h * ldl, 1, h, w, frac, false, det_yx, 2, det_val, cap, n_det_dev,
+                thr_dev, n_det_host, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t vmf_detect3x3x3_workspace_bytes(int64_t ns, int64_t h, int64_t w) {
+  return detect_workspace_bytes(ns, h, w);
+}
+
+int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ldn,
+                    int64_t plane_stride, float frac, int32_t *det_syx, float *det_val,
+                    int64_t cap, int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host,
+                    void *ws, size_t ws_bytes, void *stream) {
+  if (ns < 1 || h < 1 || w < 1) return fail(VMF_EVALUE, "stack must be 3-D and non-empty");
+  if (ldn < w || plane_stride < h * ldn) return fail(VMF_EVALUE, "bad stack strides");
+  return detect(n, ldn, plane_stride, ns, h, w, frac, false, det_syx, 3, det_val, cap, n_det_dev,
+                thr_dev, n_det_host, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+// workspace: [T row-pass out][B if blur_out NULL][L if lap_out NULL][iir carry][detect]
+size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage,
+                                           const vmf_stage *col_stage) {
+  size_t img = align256((size_t)h * w * sizeof(float));
+  size_t carry = stage_ws(row_stage, h, w);
+  size_t c2 = stage_ws(col_stage, w, h);
+  if (c2 > carry) carry = c2;
+  return 3 * img + align256(carry) + align256(detect_workspace_bytes(1, h, w)) + 256;
+}
+
+int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                        const vmf_stage *row_stage, const vmf_stage *col_stage, float lap_scale,
+                        float frac, float *blur_out, float *lap_out, int32_t *det_yx,
+                        float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev,
+                        int64_t *n_det_host, void *ws, size_t ws_bytes, void *stream) {
+  if (h < 1 || w < 1) return fail(VMF_EVALUE, "image must be a 2-D array");
+  if (ldx < w) return fail(VMF_EVALUE, "row pitch smaller than width");
+  int rc = check_stage(row_stage, w, "row");
+  if (rc) return rc;
+  rc = check_stage(col_stage, h, "column");
+  if (rc) return rc;
+  size_t need = vmf_blur_lap_detect_workspace_bytes(h, w, row_stage, col_stage);
+  if (!ws || ws_bytes < need)
+    return fail(VMF_EVALUE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  size_t img = align256((size_t)h * w * sizeof(float));
+  float *T = (float *)p;
+  p += img;
+  float *B = blur_out ? blur_out : (float *)p;
+  p += img;
+  float *L = lap_out ? lap_out : (float *)p;
+  p += img;
+  size_t carry_b = align256(vmf_blur_lap_detect_workspace_bytes(h, w, row_stage, col_stage) -
+                            3 * img - align256(detect_workspace_bytes(1, h, w)) - 256);
+  void *carry = p;
+  p += carry_b;
+  void *dws = p;
+  size_t dws_b = align256(detect_workspace_bytes(1, h, w));
+  rc = run_stage<ROWS>(row_stage, x, x_dtype, T, h, w, ldx, w, carry, carry_b, st);
+  if (rc) return rc;
+  rc = run_stage<COLS>(col_stage, T, VMF_F32, B, h, w, w, w, carry, carry_b, st);
+  if (rc) return rc;
+  float *absmax = detect_absmax_slot(dws);
+  cudaMemsetAsync(absmax, 0, sizeof(float), st);
+  rc = laplacian(B, w, L, w, h, w, lap_scale, absmax, st);
+  if (rc) return rc;
+  if (frac <= 0.0f) return VMF_OK;
+  return detect(L, w, h * w, 1, h, w, frac, true, det_yx, 2, det_val, cap, n_det_dev, thr_dev,
+                n_det_host, dws, dws_b, st);
+}
+
+}  // extern "C"

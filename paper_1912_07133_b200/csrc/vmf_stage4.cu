@@ -1,0 +1,296 @@
+// vmf_stage4.cu -- Laplacian (stage 3) and threshold + NMS blob extraction
+// (stage 4) with deterministic, order-preserving compaction.
+//
+// Laplacian: L = s * (D20 + D02), D20 = conv_rows(B, (1,-2,1)),
+// D02 = conv_cols(B, (1,-2,1)) with replicate edges (engine.py:218-227,
+// fir_vm_bank(3)[2] from design.py:250-280, trace at blob.py:161).
+//
+// Detection rule (conventions from blob.py:162-168): a
+// pixel is kept iff it is strictly greater (smaller) than all 8
+// edge-replicated neighbours and L >= t (-L >= t), t = frac * max|L|.
+// Border pixels are their own replicated neighbours and never qualify.
+// Scale-space variant: additionally strict against the 3x3 patches of the
+// adjacent scales that exist.
+//
+// Compaction is three short launches (count per CTA, scan, ordered write) so
+// the list comes out sorted by linear index (s, y, x) with no atomics on the
+// data path: deterministic for any launch configuration.
+#include "vmf_common.cuh"
+#include "vmf_stage4.cuh"
+
+namespace vmf {
+
+constexpr int kLapThreads = 256;
+constexpr int kNmsThreads = 256;
+constexpr int kNmsPerThread = 8;
+constexpr int64_t kNmsPerBlock = (int64_t)kNmsThreads * kNmsPerThread;
+
+__device__ __forceinline__ float block_max(float v, float *red) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(kLapThreads) laplacian_kernel(
+    const float *__restrict__ b, int64_t ldb, float *__restrict__ l, int64_t ldl, int64_t h,
+    int64_t w, float scale, float *__restrict__ absmax) {
+  __shared__ float red[kLapThreads / 32];
+  float mx = 0.0f;
+  int64_t n = h * w;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = p / w, j = p - i * w;
+    int64_t iu = i > 0 ? i - 1 : 0, id = i < h - 1 ? i + 1 : h - 1;
+    int64_t jl = j > 0 ? j - 1 : 0, jr = j < w - 1 ? j + 1 : w - 1;
+    double c = (double)b[i * ldb + j];
+    double dx = (double)b[i * ldb + jr] - 2.0 * c + (double)b[i * ldb + jl];
+    double dy = (double)b[id * ldb + j] - 2.0 * c + (double)b[iu * ldb + j];
+    float v = (float)((double)scale * (dx + dy));
+    l[i * ldl + j] = v;
+    mx = fmaxf(mx, fabsf(v));
+  }
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0 && absmax) atomic_max_nonneg(absmax, mx);
+}
+
+// Is linear pixel p (within plane s of ns) a detection?
+__device__ __forceinline__ bool is_det(const float *__restrict__ l, int64_t ld, int64_t plane,
+                                       int64_t ns, int64_t h, int64_t w, int64_t p, float thr,
+                                       float *val) {
+  int64_t hw = h * w;
+  int64_t s = p / hw, q = p - s * hw;
+  int64_t i = q / w, j = q - i * w;
+  if (i <= 0 || j <= 0 || i >= h - 1 || j >= w - 1) return false;
+  const float *P = l + s * plane;
+  float v = P[i * ld + j];
+  if (!(fabsf(v) >= thr)) return false;
+  bool gt = true, lt = true;
+#pragma unroll
+  for (int di = -1; di <= 1; ++di)
+#pragma unroll
+    for (int dj = -1; dj <= 1; ++dj) {
+      if (di == 0 && dj == 0) continue;
+      float u = P[(i + di) * ld + j + dj];
+      gt &= v > u;
+      lt &= v < u;
+    }
+  if (!gt && !lt) return false;
+  for (int64_t t = s - 1; t <= s + 1; t += 2) {
+    if (t < 0 || t >= ns) continue;
+    const float *Q = l + t * plane;
+#pragma unroll
+    for (int di = -1; di <= 1; ++di)
+#pragma unroll
+      for (int dj = -1; dj <= 1; ++dj) {
+        float u = Q[(i + di) * ld + j + dj];
+        gt &= v > u;
+        lt &= v < u;
+      }
+  }
+  *val = v;
+  return (gt && v >= thr) || (lt && -v >= thr);
+}
+
+__global__ void __launch_bounds__(kNmsThreads) nms_count_kernel(
+    const float *__restrict__ l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int64_t w,
+    float frac, const float *__restrict__ absmax, float *thr_out, int *__restrict__ counts) {
+  float thr = frac * *absmax;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && thr_out) *thr_out = thr;
+  int64_t total = ns * h * w;
+  int64_t base = (int64_t)blockIdx.x * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
+  int c = 0;
+  float v;
+#pragma unroll
+  for (int e = 0; e < kNmsPerThread; ++e) {
+    int64_t p = base + e;
+    if (p < total && is_det(l, ld, plane, ns, h, w, p, thr, &v)) ++c;
+  }
+  __shared__ int sc;
+  if (threadIdx.x == 0) sc = 0;
+  __syncthreads();
+  if (c) atomicAdd(&sc, c);
+  __syncthreads();
+  if (threadIdx.x == 0) counts[blockIdx.x] = sc;
+}
+
+// Single CTA: exclusive scan of per-CTA counts, total -> *n_det.
+__global__ void __launch_bounds__(1024) nms_scan_kernel(int *__restrict__ counts, int64_t nb,
+                                                        int64_t *__restrict__ n_det) {
+  __shared__ int64_t part[1024];
+  int64_t per = (nb + blockDim.x - 1) / blockDim.x;
+  int64_t lo = threadIdx.x * per, hi = lo + per < nb ? lo + per : nb;
+  int64_t s = 0;
+  for (int64_t i = lo; i < hi; ++i) s += counts[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      int64_t t = part[i];
+      part[i] = run;
+      run += t;
+    }
+    *n_det = run;
+  }
+  __syncthreads();
+  int64_t run = part[threadIdx.x];
+  for (int64_t i = lo; i < hi; ++i) {
+    int64_t t = counts[i];
+    counts[i] = (int)run;  // offsets fit: detections <= pixels per launch < 2^31
+    run += t;
+  }
+}
+
+__global__ void __launch_bounds__(kNmsThreads) nms_write_kernel(
+    const float *__restrict__ l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int64_t w,
+    float frac, const float *__restrict__ absmax, const int *__restrict__ offsets,
+    int32_t *__restrict__ det_idx, int idx_stride, float *__restrict__ det_val, int64_t cap) {
+  float thr = frac * *absmax;
+  int64_t total = ns * h * w;
+  int64_t base = (int64_t)blockIdx.x * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
+  unsigned flags = 0;
+  float vals[kNmsPerThread];
+#pragma unroll
+  for (int e = 0; e < kNmsPerThread; ++e) {
+    int64_t p = base + e;
+    vals[e] = 0.0f;
+    if (p < total && is_det(l, ld, plane, ns, h, w, p, thr, &vals[e])) flags |= 1u << e;
+  }
+  int c = __popc(flags);
+  // block exclusive scan of c (thread order == pixel order)
+  __shared__ int wsum[kNmsThreads / 32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < kNmsThreads / 32 ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    if (lane < kNmsThreads / 32) wsum[lane] = v;
+  }
+  __syncthreads();
+  int64_t pos = (int64_t)offsets[blockIdx.x] + (wid ? wsum[wid - 1] : 0) + inc - c;
+  int64_t hw = h * w;
+#pragma unroll
+  for (int e = 0; e < kNmsPerThread; ++e) {
+    if (!(flags >> e & 1u)) continue;
+    if (pos < cap) {
+      int64_t p = base + e;
+      int64_t s = p / hw, q = p - s * hw;
+      int64_t i = q / w, j = q - i * w;
+      int32_t *o = det_idx + pos * idx_stride;
+      if (idx_stride == 3) {
+        o[0] = (int32_t)s;
+        o[1] = (int32_t)i;
+        o[2] = (int32_t)j;
+      } else {
+        o[0] = (int32_t)i;
+        o[1] = (int32_t)j;
+      }
+      det_val[pos] = vals[e];
+    }
+    ++pos;
+  }
+}
+
+__global__ void absmax_kernel(const float *__restrict__ l, int64_t ld, int64_t plane,
+                              int64_t ns, int64_t h, int64_t w, float *__restrict__ absmax) {
+  __shared__ float red[32];
+  float mx = 0.0f;
+  int64_t total = ns * h * w, hw = h * w;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = p / hw, q = p - s * hw;
+    int64_t i = q / w, j = q - i * w;
+    mx = fmaxf(mx, fabsf(l[s * plane + i * ld + j]));
+  }
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0) atomic_max_nonneg(absmax, mx);
+}
+
+// ---------------------------------------------------------------------------
+// host
+// ---------------------------------------------------------------------------
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int laplacian(const float *b, int64_t ldb, float *l, int64_t ldl, int64_t h, int64_t w,
+              float scale, float *absmax, cudaStream_t st) {
+  int64_t n = h * w;
+  int64_t nb = cdiv(n, kLapThreads);
+  int64_t cap = (int64_t)sm_count() * 8;
+  laplacian_kernel<<<(int)(nb < cap ? nb : cap), kLapThreads, 0, st>>>(b, ldb, l, ldl, h, w,
+                                                                        scale, absmax);
+  return cuda_status("laplacian");
+}
+
+size_t detect_workspace_bytes(int64_t ns, int64_t h, int64_t w) {
+  int64_t nb = cdiv(ns * h * w, kNmsPerBlock);
+  return 256 + 256 + (size_t)nb * sizeof(int) + 256;
+}
+
+// ws layout: [0,256) absmax float; [256,512) scratch; [512, ...) counts
+int detect(const float *l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int64_t w,
+           float frac, bool have_absmax, int32_t *det_idx, int idx_stride, float *det_val,
+           int64_t cap, int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host, void *ws,
+           size_t ws_bytes, cudaStream_t st) {
+  size_t need = detect_workspace_bytes(ns, h, w);
+  if (!ws || ws_bytes < need)
+    return fail(VMF_EVALUE, "detect workspace too small: %zu < %zu bytes", ws_bytes, need);
+  if (!n_det_dev) return fail(VMF_EVALUE, "n_det_dev must not be NULL");
+  if (cap > 0 && (!det_idx || !det_val)) return fail(VMF_EVALUE, "detection buffers are NULL");
+  char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float *absmax = (float *)base;
+  int *counts = (int *)(base + 512);
+  if (!have_absmax) {
+    cudaMemsetAsync(absmax, 0, sizeof(float), st);
+    absmax_kernel<<<sm_count() * 4, 256, 0, st>>>(l, ld, plane, ns, h, w, absmax);
+  }
+  int64_t nb = cdiv(ns * h * w, kNmsPerBlock);
+  if (nb > 0x7fffffff) return fail(VMF_EVALUE, "frame stack too large");
+  nms_count_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
+                                                         thr_dev, counts);
+  nms_scan_kernel<<<1, 1024, 0, st>>>(counts, nb, n_det_dev);
+  nms_write_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
+                                                         counts, det_idx, idx_stride, det_val,
+                                                         cap);
+  int rc = cuda_status("detect");
+  if (rc) return rc;
+  if (n_det_host) {
+    cudaMemcpyAsync(n_det_host, n_det_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return cuda_status("detect readback");
+  }
+  return VMF_OK;
+}
+
+float *detect_absmax_slot(void *ws) {
+  return (float *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+}
+
+}  // namespace vmf

@@ -1,0 +1,173 @@
+"""Fused hot path: blur (rows, columns) -> Laplacian -> threshold + NMS.
+
+This is the north-star pipeline (BASELINE.json): stage 1/2 blur, stage 3
+Laplacian L = D20 + D02 (engine.py:215-227, blob.py:161) and stage 4
+detection.  The reference has no Laplacian + 3x3-NMS detector; the rule is
+the restatement of SURVEY.md §8(d) (conventions from blob.py:162-168):
+
+* single scale: keep (y, x) iff L(y, x) is strictly greater (smaller) than
+  its 8 edge-replicated neighbours and L >= t (-L >= t), t = frac * max|L|;
+* scale space (config 3): N_s = sigma_s^2 L_s; strict against the 8
+  in-scale and 9 + 9 adjacent-scale neighbours (one-sided at the ends);
+  t = frac * max over the whole stack of |N|.
+
+Detections come back sorted by (y, x) (and scale first for the stack).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import (_as_image, _dptr, _fir_checks, _iir_checks, _pitch, _ptr, _sign, _stream,
+                     _workspace)
+from .filters import is_fir, is_iir
+
+__all__ = ["Detections", "make_stage", "blur_laplacian_detect", "scale_space_detect"]
+
+
+@dataclass
+class Detections:
+    """Blob list.  `s` is the scale index (scale-space detection only)."""
+
+    y: object
+    x: object
+    value: object
+    threshold: float
+    count: int            # total number of detections found
+    overflow: bool        # True if count > capacity (list truncated)
+    s: object = None
+
+    def __len__(self):
+        return int(len(self.y))
+
+    def as_set(self):
+        ys = np.asarray(_np(self.y)).tolist()
+        xs = np.asarray(_np(self.x)).tolist()
+        if self.s is None:
+            return set(zip(ys, xs))
+        return set(zip(np.asarray(_np(self.s)).tolist(), ys, xs))
+
+
+def _np(t):
+    return t.cpu().numpy() if isinstance(t, torch.Tensor) else t
+
+
+class _Stage:
+    """A vmf_stage plus the ctypes arrays it points into (kept alive)."""
+
+    def __init__(self, stage):
+        self.src = stage
+        self.s = _lib.VmfStage()
+        if is_fir(stage):
+            self._taps = _dptr(stage.taps)
+            self.s.kind, self.s.n = _lib.VMF_STAGE_FIR, len(stage.taps)
+            self.s.taps = C.cast(self._taps, C.POINTER(C.c_double))
+        elif is_iir(stage):
+            self._b, self._a = _dptr(stage.b_plus), _dptr(stage.a_plus)
+            self.s.kind, self.s.n = _lib.VMF_STAGE_IIR, len(stage.a_plus)
+            self.s.b_plus = C.cast(self._b, C.POINTER(C.c_double))
+            self.s.a_plus = C.cast(self._a, C.POINTER(C.c_double))
+            self.s.b_zero, self.s.sign = float(stage.b_zero), _sign(stage)
+        else:
+            raise TypeError(f"unsupported stage type {type(stage).__name__}")
+
+    def check(self, length: int):
+        if is_fir(self.src):
+            _fir_checks(self.src, length)
+        else:
+            _iir_checks(self.src, length)
+
+
+def make_stage(stage) -> _Stage:
+    return _Stage(stage)
+
+
+def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out, cap, sync):
+    h, w = x.shape
+    row.check(w)
+    col.check(h)
+    L = _lib.lib()
+    nbytes = L.vmf_blur_lap_detect_workspace_bytes(h, w, C.byref(row.s), C.byref(col.s))
+    ws = _workspace(nbytes)
+    dev = x.device
+    cap = int(cap)
+    det_yx = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
+    det_val = torch.empty((max(cap, 1),), dtype=torch.float32, device=dev)
+    scal = torch.zeros(2, dtype=torch.int64, device=dev)  # [n_det, thr(float bits)]
+    n_host = C.c_int64(0)
+    _lib.check(L.vmf_blur_lap_detect(
+        _ptr(x), code, h, w, _pitch(x), C.byref(row.s), C.byref(col.s), float(lap_scale),
+        float(frac), _ptr(blur_out) if blur_out is not None else None,
+        _ptr(lap_out) if lap_out is not None else None, _ptr(det_yx), _ptr(det_val), cap,
+        _ptr(scal), scal.data_ptr() + 8, C.byref(n_host) if sync else None, _ptr(ws),
+        ws.numel(), _stream()))
+    return det_yx, det_val, scal, n_host.value
+
+
+def blur_laplacian_detect(img, lpf, frac: float = 0.5, col_stage=None, lap_scale: float = 1.0,
+                          cap: int = 1 << 18, return_fields: bool = False):
+    """Whole north-star path in one native call (vmf_blur_lap_detect).
+
+    img: 2-D numpy array / torch tensor (fp32 or uint16).  lpf: the blur
+    stage (FirKernel or ThreePartIIR; `col_stage` defaults to the same).
+    Returns Detections (numpy if img was numpy) and, with return_fields,
+    (blur, laplacian) as well."""
+    x, kind, code = _as_image(img)
+    h, w = x.shape
+    row, col = _Stage(lpf), _Stage(col_stage if col_stage is not None else lpf)
+    blur = lap = None
+    if return_fields:
+        blur = torch.empty((h, w), dtype=torch.float32, device=x.device)
+        lap = torch.empty((h, w), dtype=torch.float32, device=x.device)
+    det_yx, det_val, scal, n = _fused(x, code, row, col, lap_scale, frac, blur, lap, cap, True)
+    thr = float(scal[1:2].view(torch.float32)[0].item()) if frac > 0 else float("nan")
+    m = min(n, cap)
+    yx, val = det_yx[:m], det_val[:m]
+    if kind == "numpy":
+        yx, val = yx.cpu().numpy(), val.cpu().numpy()
+        if return_fields:
+            blur, lap = blur.cpu().numpy(), lap.cpu().numpy()
+    dets = Detections(yx[:, 0], yx[:, 1], val, thr, n, n > cap)
+    if return_fields:
+        return dets, blur, lap
+    return dets
+
+
+def scale_space_detect(img, stages, sigmas, frac: float = 0.5, cap: int = 1 << 18,
+                       return_stack: bool = False):
+    """Config-3 scale sweep: per scale the fused blur + Laplacian with
+    lap_scale = sigma^2 into one stack, then 3x3x3 NMS over the stack."""
+    if len(stages) != len(sigmas) or not stages:
+        raise ValueError("need one stage per sigma")
+    x, kind, code = _as_image(img)
+    h, w = x.shape
+    ns = len(stages)
+    stack = torch.empty((ns, h, w), dtype=torch.float32, device=x.device)
+    for s, (st, sg) in enumerate(zip(stages, sigmas)):
+        stg = _Stage(st)
+        _fused(x, code, stg, stg, float(sg) ** 2, 0.0, None, stack[s], 0, False)
+    L = _lib.lib()
+    nbytes = L.vmf_detect3x3x3_workspace_bytes(ns, h, w)
+    ws = _workspace(nbytes)
+    cap = int(cap)
+    det = torch.empty((max(cap, 1), 3), dtype=torch.int32, device=x.device)
+    val = torch.empty((max(cap, 1),), dtype=torch.float32, device=x.device)
+    scal = torch.zeros(2, dtype=torch.int64, device=x.device)
+    n_host = C.c_int64(0)
+    _lib.check(L.vmf_detect3x3x3(_ptr(stack), ns, h, w, w, h * w, float(frac), _ptr(det),
+                                 _ptr(val), cap, _ptr(scal), scal.data_ptr() + 8,
+                                 C.byref(n_host), _ptr(ws), ws.numel(), _stream()))
+    n = n_host.value
+    thr = float(scal[1:2].view(torch.float32)[0].item())
+    m = min(n, cap)
+    d, v = det[:m], val[:m]
+    if kind == "numpy":
+        d, v = d.cpu().numpy(), v.cpu().numpy()
+    dets = Detections(d[:, 1], d[:, 2], v, thr, n, n > cap, s=d[:, 0])
+    if return_stack:
+        return dets, (stack.cpu().numpy() if kind == "numpy" else stack)
+    return dets

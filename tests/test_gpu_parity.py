@@ -1,0 +1,229 @@
+"""GPU parity against the CPU oracle (pinned to the reference by
+tests/test_oracle.py).  Every call goes through the C ABI
+(libvmfilt_b200.so) via the drop-in engine / detect API."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1912_07133_b200 import filters as F
+from paper_1912_07133_b200 import synth
+from tests.parity import TOL_REL, compare_blobs, max_rel_err
+
+pytestmark = pytest.mark.gpu
+
+# fp32 output of an fp64-state pass: error is a few fp32 ulps of the output
+PASS_TOL = 4e-6
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1912_07133_b200 import _lib
+
+    _lib.lib()
+
+
+def _E():
+    from paper_1912_07133_b200 import engine
+
+    return engine
+
+
+def _D():
+    from paper_1912_07133_b200 import detect
+
+    return detect
+
+
+def _f32(x):
+    """The GPU consumes fp32; the oracle consumes the same values in fp64."""
+    return np.asarray(x, dtype=np.float32)
+
+
+@pytest.mark.parametrize("op", ["iir_rows", "iir_cols", "conv_rows", "conv_cols"])
+def test_single_pass_matches_oracle(golden, cat, op):
+    E = _E()
+    n = 0
+    for key in [k for k in golden if k.startswith(op + "/")]:
+        _, fname, iname = key.split("/")
+        x = _f32(golden[f"in/{iname}"])
+        got = getattr(E, op)(x, cat[fname])
+        want = getattr(O, op)(x, cat[fname])
+        assert got.dtype == np.float32 and got.shape == want.shape
+        assert max_rel_err(got, want) < PASS_TOL, key
+        n += 1
+    assert n > 10
+
+
+def test_u16_input_path(golden, cat):
+    E = _E()
+    x = golden["in/u16"].astype(np.uint16)
+    for name in ("rp4", "bw6", "g1.5_k8"):
+        for op in ("apply_rows", "apply_cols"):
+            got = getattr(E, op)(x, cat[name])
+            want = getattr(O, op)(x.astype(np.float64), cat[name])
+            assert max_rel_err(got, want) < PASS_TOL, (name, op)
+
+
+def test_torch_in_torch_out(cat):
+    E = _E()
+    x = torch.rand(64, 80, device="cuda")
+    y = E.apply_rows(x, cat["rp4"])
+    assert isinstance(y, torch.Tensor) and y.is_cuda and y.dtype == torch.float32
+    want = O.iir_rows(x.cpu().numpy(), cat["rp4"])
+    assert max_rel_err(y.cpu().numpy(), want) < PASS_TOL
+
+
+def test_constant_image_invariance_everywhere(cat):
+    # tests/test_engine.py:49-53 / test_acceptance.py:175-183
+    E = _E()
+    x = np.full((40, 61), 3.7, np.float32)
+    for name in ("rp4", "rp32", "bw48", "blunt4", "bwapp6", "g4_k16", "sg3.2"):
+        f = cat[name]
+        if min(x.shape) < (len(f.taps) if F.is_fir(f) else 2 * f.k + 1):
+            continue
+        y = E.apply_cols(E.apply_rows(x, f), f)
+        assert np.abs(y - 3.7).max() <= 2e-6 * 3.7, name
+
+
+def test_impulse_response_and_long_lines(cat):
+    E = _E()
+    for n in (101, 4099):  # 4099: many chunks plus a folded tail
+        x = np.zeros((3, n), np.float32)
+        x[1, n // 2] = 1.0
+        for name in ("rp2", "rp32", "bw48"):
+            got = E.iir_rows(x, cat[name])
+            want = O.iir_rows(x, cat[name])
+            assert np.abs(got - want).max() < 1e-7 * max(1, np.abs(want).max()), (name, n)
+            got = E.iir_cols(np.ascontiguousarray(x.T), cat[name])
+            assert np.abs(got.T - want).max() < 1e-7 * max(1, np.abs(want).max()), (name, n)
+
+
+def test_all_orders_and_lengths(cat):
+    # K = 1..4 (and K=0), line lengths around the chunk size and 2K+1
+    E = _E()
+    rng = np.random.default_rng(3)
+    fs = [F.ThreePartIIR((0.2,), (-0.6,), 0.2, "sym"), cat["rp4_k2"], cat["rp4"], cat["rp4_k4"],
+          F.ThreePartIIR((), (), 1.0, "sym"), F.ThreePartIIR((0.1, -0.05), (-0.9, 0.2), 0.0, "anti")]
+    for f in fs:
+        for n in sorted({2 * f.k + 1, 63, 64, 65, 64 + f.k - 1, 127, 128, 129, 300}):
+            if n < 2 * f.k + 1:
+                continue
+            x = rng.standard_normal((5, n)).astype(np.float32)
+            assert max_rel_err(E.iir_rows(x, f), O.iir_rows(x, f)) < PASS_TOL, (f, n)
+            xt = np.ascontiguousarray(x.T)
+            try:
+                got = E.iir_cols(xt, f)
+            except ValueError as e:
+                raise AssertionError((f, n, xt.shape, xt.strides, str(e)))
+            assert max_rel_err(got, O.iir_cols(xt, f)) < PASS_TOL, (f, n)
+
+
+def test_step_inputs_match_transposed_form_reference(cat):
+    # tests/test_engine.py:69-116: the steady-state initialisation
+    E = _E()
+    f = cat["rp4"]
+    for lo, hi in ((2.0, 5.0), (4.0, -1.0), (0.0, 1.0)):
+        x = np.array([[lo] * 25 + [hi] * 25] * 2, np.float32)
+        got = E.iir_rows(x, f)
+        want = O.iir_rows(x, f)
+        assert np.abs(got - want).max() < 1e-5
+
+
+def test_errors_mirror_reference(cat):
+    E = _E()
+    from paper_1912_07133_b200.errors import StabilityError
+
+    bad = F.ThreePartIIR((0.5,), (-1.5,), 0.2, "sym")
+    with pytest.raises(StabilityError):
+        E.iir_rows(np.zeros((4, 16), np.float32), bad)
+    with pytest.raises(ValueError):
+        E.iir_rows(np.zeros((2, 6), np.float32), cat["rp4"])
+    with pytest.raises(ValueError):
+        E.conv_rows(np.zeros((4, 10), np.float32), cat["g4_k16"])
+    with pytest.raises(ValueError):
+        E.apply_rows(np.zeros((4,), np.float32), cat["rp4"])
+    with pytest.raises(TypeError):
+        E.apply_rows(np.zeros((4, 16), np.float32), object())
+
+
+def test_run_to_run_determinism(cat):
+    E = _E()
+    x = torch.randn(300, 500, device="cuda")
+    a = E.apply_cols(E.apply_rows(x, cat["rp8"]), cat["rp8"])
+    b = E.apply_cols(E.apply_rows(x, cat["rp8"]), cat["rp8"])
+    assert torch.equal(a, b)
+
+
+def test_derivative_field(cat, golden):
+    E = _E()
+    x = _f32(golden["in/rand"])
+    fld = E.derivative_field(x, cat["rp4"], 3)
+    B = O.blur(x, cat["rp4"])
+    d1 = F.FirKernel(F.VM_BANK3[1], "anti", 1)
+    d2 = F.FirKernel(F.VM_BANK3[2], "sym", 2)
+    assert max_rel_err(fld[(2, 0)], O.conv_rows(B, d2)) < 1e-4
+    assert max_rel_err(fld[(1, 1)], O.conv_cols(O.conv_rows(B, d1), d1)) < 1e-4
+    assert set(fld.images) == {(0, 0), (1, 0), (0, 1), (2, 0), (1, 1), (0, 2)}
+
+
+# ---------------------------------------------------------------------------
+# the five BASELINE configs (full pipeline through vmf_blur_lap_detect)
+# ---------------------------------------------------------------------------
+def _check_pipeline(x, stage, frac=0.5, lap_scale=1.0, label=""):
+    D = _D()
+    dets, blur, lap = D.blur_laplacian_detect(x, stage, frac=frac, lap_scale=lap_scale,
+                                              return_fields=True)
+    B, L, (ys, xs, vs, thr) = O.pipeline(x, stage, frac=frac, lap_scale=lap_scale)
+    eb, el = max_rel_err(blur, B), max_rel_err(lap, L)
+    assert eb < TOL_REL, (label, "blur", eb)
+    assert el < TOL_REL, (label, "laplacian", el)
+    exempt, bad = compare_blobs(dets.as_set(), set(zip(ys.tolist(), xs.tolist())), L, thr)
+    assert not bad, (label, bad[:10])
+    assert not dets.overflow
+    return dict(blur_err=eb, lap_err=el, n_ref=len(ys), n_gpu=dets.count, exempt=exempt)
+
+
+def test_config1_repeated_pole(cat):
+    x = synth.config1_frame()
+    for name in ("rp4", "rp4_k2"):
+        _check_pipeline(x, cat[name], label=f"config1/{name}")
+
+
+def test_config2_fir(cat):
+    x = synth.config2_frame()
+    r = {}
+    for name in ("sg3.2", "g4_k16"):
+        r[name] = _check_pipeline(x, cat[name], label=f"config2/{name}")
+    assert r["sg3.2"]["n_gpu"] > 0 and r["g4_k16"]["n_gpu"] > 0
+
+
+@pytest.mark.parametrize("family", ["iir", "fir"])
+def test_config3_scale_space(cat, family):
+    D = _D()
+    x = synth.config3_frame(2048)  # quarter-area instance; the 4096^2 run is in bench
+    spec = synth.CONFIG_STAGES[3]
+    stages = [cat[n] for n in spec[family]]
+    sig = spec["sigmas"]
+    dets, stack = D.scale_space_detect(x, stages, sig, frac=0.5, return_stack=True)
+    N = np.stack([O.laplacian(O.blur(x, s)) * (g * g) for s, g in zip(stages, sig)])
+    for i in range(len(sig)):
+        e = max_rel_err(stack[i], N[i])
+        assert e < TOL_REL, (family, sig[i], e)
+    ss, ys, xs, vs, thr = O.detect3x3x3(N, 0.5)
+    exempt, bad = compare_blobs(dets.as_set(), set(zip(ss.tolist(), ys.tolist(), xs.tolist())),
+                                N, thr, stack=True)
+    assert not bad, bad[:10]
+
+
+def test_config4_u16_stream(cat):
+    frames = synth.config4_stream(n_frames=3)
+    for f in frames:
+        _check_pipeline(f, cat["rp6"], label="config4")
+
+
+def test_config5_coarse_scale(cat):
+    x = synth.config5_frame(4096)  # quarter-area instance of the 8192^2 frame
+    _check_pipeline(x, cat["bw48"], label="config5/bw48")
+    _check_pipeline(x, cat["sg38.4"], label="config5/sg38.4")
