@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py -- north-star benchmark of the B200-native vmfilt hot path.
+
+Workload (BASELINE.json configs[2], the 4096^2 case the north-star target is
+stated on): one 4096x4096 fp32 frame (2000 Gaussian blobs, s log-uniform
+[2,32], A uniform [0.5,1.5], N(0, 0.05^2) noise; seeded synthetic, see
+paper_1912_07133_b200/synth.py).  One STEP = the repeated-pole IIR scale
+sweep sigma in {2,4,8,16,32}: per scale the fused path blur(rows) ->
+blur(cols) -> Laplacian -> threshold (0.5 max|L|) + 3x3 NMS, i.e. five
+passes of the hot path over the frame.  metric = Mpixel/s per scale
+(frame pixels x scales / time).  The FIR family of the same sweep is timed
+separately and reported in `per_scale` (IIR vs FIR, BASELINE.json metric).
+
+Timing: W untimed warm-up steps; then K steps, each preceded by an L2 flush
+(a 256 MiB memset, outside the events) and bracketed by CUDA events on the
+launch stream; barrier + synchronize on both sides; max over ranks.
+`value` = frame pixels x scales x ranks / time (weak scaling: every rank
+processes its own frame; no data-path collective).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+SIGMAS = [2.0, 4.0, 8.0, 16.0, 32.0]
+IIR = ["rp2", "rp4", "rp8", "rp16", "rp32"]
+FIR = ["g2_k8", "g4_k16", "g8_k32", "g16_k64", "g32_k128"]
+METRIC = "Mpixel/s per scale (IIR vs FIR) and achieved HBM GB/s vs B200 peak, 1 GPU"
+UNIT = "Mpixel/s"
+FLUSH_BYTES = 256 << 20
+# algorithmic bytes per pixel per launch: fp32 read + write
+ALGO_BYTES_PER_PX = {
+    "iir_apply": 8, "iir_carry": 4, "iir_rows_fused": 8, "iir_cols_fused": 8,
+    "fir_rows": 8, "fir_cols": 8, "laplacian": 8, "nms_count": 4, "nms_write": 4,
+    "absmax": 4,
+}
+PATH_BYTES_PER_PX = 16  # fused path: read x, write T, read T, write L
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# nvidia-smi clock sampling during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index: int):
+        self.dev = dev_index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20", "-i", str(self.dev)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        busy = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (one process per GPU; weak scaling, no data collective)
+# ---------------------------------------------------------------------------
+def dist_init(backend):
+    import torch.distributed as dist
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, local, ws
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v, ws, device):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(v)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port (test infrastructure) as baseline / reference arm
+# ---------------------------------------------------------------------------
+def cpu_time_sweep(frame, stages, reps):
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    O.pipeline(frame[:256, :256], stages[0])  # warm
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for st in stages:
+            O.pipeline(frame, st, frac=0.5)
+        times.append(time.perf_counter() - t0)
+    return times, threads
+
+
+def run_reference(args):
+    rank, local, ws = dist_init("gloo")
+    if rank != 0:
+        return
+    from paper_1912_07133_b200 import filters, synth
+
+    frame = synth.config3_frame(args.size)
+    cat = filters.catalog()
+    stages = [cat[n] for n in IIR]
+    mpx = frame.size / 1e6
+    for _ in range(args.warmup):
+        cpu_time_sweep(frame, stages[:1], 1)
+    times, threads = cpu_time_sweep(frame, stages, args.steps)
+    t = sum(times)
+    value = mpx * len(stages) * args.steps / t
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config3 {args.size}x{args.size} fp32, repeated-pole IIR "
+                               "sweep sigma 2..32, blur+Laplacian+3x3 NMS per scale",
+                   "frame": [args.size, args.size], "scales": len(stages)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"full {args.size}^2 frame x 5 IIR scales per step, "
+                                   f"{args.steps} steps (oracle/vmf_oracle.c restatement of "
+                                   "engine.py:35-102 + numpy-equivalent stage 4)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank, local, ws = dist_init("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1912_07133_b200 import _lib, detect, filters, synth
+
+    cat = filters.catalog()
+    frame = synth.config3_frame(args.size)
+    h, w = frame.shape
+    mpx = h * w / 1e6
+    x = torch.from_numpy(frame).to(dev)
+    iir = [detect.make_stage(cat[n]) for n in IIR]
+    fir = [detect.make_stage(cat[n]) for n in FIR]
+    lap = torch.empty((h, w), dtype=torch.float32, device=dev)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def one_scale(stg):
+        detect._fused(x, _lib.VMF_F32, stg, stg, 1.0, 0.5, None, lap, 1 << 18, False)
+
+    def step(stages):
+        for stg in stages:
+            one_scale(stg)
+
+    def timed(fn, n, flush_between=True):
+        evs = []
+        for _ in range(n):
+            if flush_between:
+                flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        step(iir)
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    n0 = _lib.launch_count()
+    ms = timed(lambda: step(iir), args.steps)
+    launches = _lib.launch_count() - n0
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = max_over_ranks(ms, ws, dev)
+    ms_step = ms / args.steps
+    value = mpx * len(iir) * ws * args.steps / (ms / 1e3)
+
+    # per-scale IIR vs FIR (BASELINE metric), flushed, 3 reps each
+    per_scale = {"iir": {}, "fir": {}}
+    for fam, stages in (("iir", iir), ("fir", fir)):
+        for sg, stg in zip(SIGMAS, stages):
+            one_scale(stg)
+            t = timed(lambda: one_scale(stg), 3) / 3
+            per_scale[fam][f"{sg:g}"] = round(mpx / (t / 1e3), 1)
+
+    # in-situ kernel timing over the same timed steps (events per launch)
+    _lib.profile_begin()
+    timed(lambda: step(iir), args.steps)
+    prof = _lib.profile_end()
+    clk = clocks.stop()
+    hbm, peak_kind = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_n) = dom
+    per_launch_ms = dom_ms / dom_n
+    algo = ALGO_BYTES_PER_PX.get(dom_name, 8) * h * w
+    achieved = algo / (per_launch_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(dom_name)
+    except Exception:
+        pass
+    path_gbs = PATH_BYTES_PER_PX * h * w * len(iir) / (ms_step / 1e3) / 1e9
+
+    # end to end through the public API: pinned host frame -> device ->
+    # 5 scales -> detections back to the host, every step
+    host = torch.from_numpy(frame).pin_memory()
+    stages_obj = [cat[n] for n in IIR]
+    detect.detect_sweep(host, stages_obj)
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(args.steps):
+        res = detect.detect_sweep(host, stages_obj)
+        d2h += sum(len(r) * 12 + 8 for r in res)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
+    barrier(ws)
+    e2e = mpx * len(iir) * ws * args.steps / e2e_s
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        times, threads = cpu_time_sweep(frame, [cat["rp4"]], 3)
+        cpu = {"value": round(mpx / statistics.median(times), 2), "unit": UNIT, "cores": threads,
+               "kind": "port",
+               "sample": f"full {h}x{w} frame, sigma=4 repeated-pole scale, median of 3 "
+                         "(oracle/vmf_oracle.c: fp64 restatement of engine.py:35-102 + stage 4)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config3 {h}x{w} fp32, repeated-pole IIR sweep sigma "
+                                   "2..32, fused blur+Laplacian+3x3 NMS per scale",
+                       "frame": [h, w], "scales": len(iir), "parallelism": f"replicas x{ws}",
+                       "l2": "flushed (256 MiB memset) before every timed step"},
+            "per_scale": per_scale,
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1),
+                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": traffic,
+                         "algo_bytes_per_launch": algo, "avg_launch_ms": round(per_launch_ms, 5)},
+            "path_roofline": {"bytes_per_px": PATH_BYTES_PER_PX, "achieved": round(path_gbs, 1),
+                              "peak": hbm, "frac": round(path_gbs / hbm, 4), "unit": "GB/s"},
+            "kernels": {k: {"avg_ms": round(v[0] / v[1], 5), "launches": v[1]}
+                        for k, v in prof.items()},
+            "e2e": {"value": round(e2e, 1), "unit": UNIT,
+                    "h2d_bytes_per_step": int(frame.nbytes),
+                    "d2h_bytes_per_step": int(d2h / args.steps)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

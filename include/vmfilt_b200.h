@@ -142,6 +142,17 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w,
                     int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host,
                     void *ws, size_t ws_bytes, void *stream);
 
+/* Launch accounting / in-situ kernel timing (used by bench.py).
+ * vmf_launch_count: kernels launched by this library since load.
+ * vmf_profile_begin: start bracketing every launch with CUDA events on its
+ * stream.  vmf_profile_end: wait for them and write, per kernel id,
+ * the summed duration (ms) and launch count; returns the number of ids. */
+long long vmf_launch_count(void);
+int vmf_num_kernel_ids(void);
+const char *vmf_kernel_name(int id);
+void vmf_profile_begin(void);
+int vmf_profile_end(double *ms, long long *counts, int n);
+
 #ifdef __cplusplus
 }
 #endif

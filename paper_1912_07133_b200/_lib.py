@@ -55,6 +55,11 @@ _PROTOS = {
     "vmf_detect3x3x3_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "vmf_detect3x3x3": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, C.c_float, _vp, _vp,
                                   _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "vmf_launch_count": (C.c_longlong, []),
+    "vmf_num_kernel_ids": (C.c_int, []),
+    "vmf_kernel_name": (C.c_char_p, [C.c_int]),
+    "vmf_profile_begin": (None, []),
+    "vmf_profile_end": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int]),
     "vmf_blur_lap_detect_workspace_bytes": (_sz, [_i64, _i64, C.POINTER(VmfStage),
                                                   C.POINTER(VmfStage)]),
     "vmf_blur_lap_detect": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, C.POINTER(VmfStage),
@@ -97,3 +102,21 @@ def check(rc: int) -> None:
     if rc == VMF_ESTABILITY:
         raise StabilityError(msg)
     raise RuntimeError(f"CUDA failure: {msg}")
+
+
+def launch_count() -> int:
+    return int(lib().vmf_launch_count())
+
+
+def profile_begin() -> None:
+    lib().vmf_profile_begin()
+
+
+def profile_end() -> dict:
+    """-> {kernel name: (total_ms, launches)} for kernels that ran."""
+    L = lib()
+    n = L.vmf_num_kernel_ids()
+    ms = (C.c_double * n)()
+    cnt = (C.c_longlong * n)()
+    L.vmf_profile_end(ms, cnt, n)
+    return {L.vmf_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(n) if cnt[i]}

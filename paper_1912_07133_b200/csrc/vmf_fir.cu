@@ -12,6 +12,7 @@
 // from L2/HBM once per tile instead of (2k+1) times.
 #include "vmf_common.cuh"
 #include "vmf_iir.cuh"
+#include "vmf_prof.cuh"
 
 namespace vmf {
 
@@ -103,6 +104,7 @@ static int launch_fir(const T *x, int64_t ldx, float *y, int64_t ldy, int64_t h,
     cudaFuncSetAttribute(fir_rows_kernel<MAXT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     dim3 grid((unsigned)cdiv(w, kFirRowTile), (unsigned)(h < 65535 ? h : 65535));
+    Launch g(K_FIR_ROWS, st);
     fir_rows_kernel<MAXT, T><<<grid, kFirRowTile, smem, st>>>(x, ldx, y, ldy, h, w, tp);
   } else {
     size_t smem = (size_t)(ntaps + (kFirColTileH + 2 * k) * kFirColTileW) * sizeof(double);
@@ -110,6 +112,7 @@ static int launch_fir(const T *x, int64_t ldx, float *y, int64_t ldy, int64_t h,
     cudaFuncSetAttribute(fir_cols_kernel<MAXT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     dim3 grid((unsigned)cdiv(w, kFirColTileW), (unsigned)cdiv(h, kFirColTileH));
+    Launch g(K_FIR_COLS, st);
     fir_cols_kernel<MAXT, T><<<grid, 256, smem, st>>>(x, ldx, y, ldy, h, w, tp);
   }
   return cuda_status("fir pass");

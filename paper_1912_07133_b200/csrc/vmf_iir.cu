@@ -28,6 +28,7 @@
 
 #include "vmf_common.cuh"
 #include "vmf_iir.cuh"
+#include "vmf_prof.cuh"
 
 namespace vmf {
 
@@ -318,8 +319,14 @@ static int launch_iir(const T *x, int64_t ldx, float *y, int64_t ldy, const IirP
                       double *carry, cudaStream_t st) {
   int64_t work = p.C * p.M;
   int nb = (int)cdiv(work, 128);
-  iir_carry_kernel<K, O, T><<<nb, 128, 0, st>>>(x, ldx, p, carry);
-  iir_scan_kernel<K, O, T><<<(int)cdiv(p.M, 128), 128, 0, st>>>(x, ldx, p, carry);
+  {
+    Launch g(K_IIR_CARRY, st);
+    iir_carry_kernel<K, O, T><<<nb, 128, 0, st>>>(x, ldx, p, carry);
+  }
+  {
+    Launch g(K_IIR_SCAN, st);
+    iir_scan_kernel<K, O, T><<<(int)cdiv(p.M, 128), 128, 0, st>>>(x, ldx, p, carry);
+  }
   size_t smem = (size_t)(p.L + K) * kIirApplyThreads * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
@@ -327,8 +334,11 @@ static int launch_iir(const T *x, int64_t ldx, float *y, int64_t ldy, const IirP
                          200 * 1024);
     attr_set = true;
   }
-  iir_apply_kernel<K, O, T><<<(int)cdiv(work, kIirApplyThreads), kIirApplyThreads, smem, st>>>(
-      x, ldx, y, ldy, p, carry);
+  {
+    Launch g(K_IIR_APPLY, st);
+    iir_apply_kernel<K, O, T><<<(int)cdiv(work, kIirApplyThreads), kIirApplyThreads, smem, st>>>(
+        x, ldx, y, ldy, p, carry);
+  }
   return cuda_status("iir pass");
 }
 
@@ -393,6 +403,7 @@ int iir_pass(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t
   if (rc) return rc;
   if (k == 0) {
     int64_t n = h * w;
+    Launch g(K_IIR_SCALE, st);
     if (x_dtype == VMF_F32)
       scale_kernel<<<(int)cdiv(n, 256), 256, 0, st>>>((const float *)x, ldx, y, ldy, h, w, b_zero);
     else

@@ -1,0 +1,97 @@
+// vmf_prof.cu -- see vmf_prof.cuh.
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "vmf_common.cuh"
+#include "vmf_prof.cuh"
+
+namespace vmf {
+
+const char *const kKernelNames[K_NUM_IDS] = {
+    "iir_carry", "iir_scan", "iir_apply", "iir_scale", "fir_rows", "fir_cols",
+    "laplacian", "absmax", "nms_count", "nms_scan", "nms_write", "iir_rows_fused",
+    "iir_cols_fused", "finalize"};
+
+namespace {
+std::atomic<long long> g_launches{0};
+std::mutex g_mu;
+bool g_on = false;
+struct Rec {
+  int id;
+  cudaEvent_t a, b;
+};
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t get_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+Launch::Launch(KernelId id, cudaStream_t st) : slot_(-1), st_(st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_on) return;
+  Rec r{(int)id, get_event(), get_event()};
+  cudaEventRecord(r.a, st);
+  g_recs.push_back(r);
+  slot_ = (int)g_recs.size() - 1;
+}
+
+Launch::~Launch() {
+  if (slot_ < 0) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEventRecord(g_recs[slot_].b, st_);
+}
+
+}  // namespace vmf
+
+extern "C" {
+
+long long vmf_launch_count(void) { return vmf::g_launches.load(); }
+
+int vmf_num_kernel_ids(void) { return vmf::K_NUM_IDS; }
+
+const char *vmf_kernel_name(int id) {
+  return (id >= 0 && id < vmf::K_NUM_IDS) ? vmf::kKernelNames[id] : "";
+}
+
+void vmf_profile_begin(void) {
+  std::lock_guard<std::mutex> lk(vmf::g_mu);
+  for (auto &r : vmf::g_recs) {
+    vmf::g_pool.push_back(r.a);
+    vmf::g_pool.push_back(r.b);
+  }
+  vmf::g_recs.clear();
+  vmf::g_on = true;
+}
+
+// Waits for the recorded events; ms[id] += duration, counts[id] += 1.
+int vmf_profile_end(double *ms, long long *counts, int n) {
+  std::lock_guard<std::mutex> lk(vmf::g_mu);
+  vmf::g_on = false;
+  for (int i = 0; i < n; ++i) {
+    ms[i] = 0.0;
+    counts[i] = 0;
+  }
+  for (auto &r : vmf::g_recs) {
+    cudaEventSynchronize(r.b);
+    float t = 0.0f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.id < n) {
+      ms[r.id] += t;
+      counts[r.id] += 1;
+    }
+  }
+  return vmf::K_NUM_IDS;
+}
+
+}  // extern "C"

@@ -17,6 +17,7 @@
 // data path: deterministic for any launch configuration.
 #include "vmf_common.cuh"
 #include "vmf_stage4.cuh"
+#include "vmf_prof.cuh"
 
 namespace vmf {
 
@@ -244,8 +245,11 @@ int laplacian(const float *b, int64_t ldb, float *l, int64_t ldl, int64_t h, int
   int64_t n = h * w;
   int64_t nb = cdiv(n, kLapThreads);
   int64_t cap = (int64_t)sm_count() * 8;
-  laplacian_kernel<<<(int)(nb < cap ? nb : cap), kLapThreads, 0, st>>>(b, ldb, l, ldl, h, w,
-                                                                        scale, absmax);
+  {
+    Launch g(K_LAPLACIAN, st);
+    laplacian_kernel<<<(int)(nb < cap ? nb : cap), kLapThreads, 0, st>>>(b, ldb, l, ldl, h, w,
+                                                                          scale, absmax);
+  }
   return cuda_status("laplacian");
 }
 
@@ -269,16 +273,26 @@ int detect(const float *l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int
   int *counts = (int *)(base + 512);
   if (!have_absmax) {
     cudaMemsetAsync(absmax, 0, sizeof(float), st);
+    Launch g(K_ABSMAX, st);
     absmax_kernel<<<sm_count() * 4, 256, 0, st>>>(l, ld, plane, ns, h, w, absmax);
   }
   int64_t nb = cdiv(ns * h * w, kNmsPerBlock);
   if (nb > 0x7fffffff) return fail(VMF_EVALUE, "frame stack too large");
-  nms_count_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
-                                                         thr_dev, counts);
-  nms_scan_kernel<<<1, 1024, 0, st>>>(counts, nb, n_det_dev);
-  nms_write_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
-                                                         counts, det_idx, idx_stride, det_val,
-                                                         cap);
+  {
+    Launch g(K_NMS_COUNT, st);
+    nms_count_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
+                                                           thr_dev, counts);
+  }
+  {
+    Launch g(K_NMS_SCAN, st);
+    nms_scan_kernel<<<1, 1024, 0, st>>>(counts, nb, n_det_dev);
+  }
+  {
+    Launch g(K_NMS_WRITE, st);
+    nms_write_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
+                                                           counts, det_idx, idx_stride, det_val,
+                                                           cap);
+  }
   int rc = cuda_status("detect");
   if (rc) return rc;
   if (n_det_host) {

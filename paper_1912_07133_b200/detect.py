@@ -26,7 +26,8 @@ from .engine import (_as_image, _dptr, _fir_checks, _iir_checks, _pitch, _ptr, _
                      _workspace)
 from .filters import is_fir, is_iir
 
-__all__ = ["Detections", "make_stage", "blur_laplacian_detect", "scale_space_detect"]
+__all__ = ["Detections", "make_stage", "blur_laplacian_detect", "detect_sweep",
+           "scale_space_detect"]
 
 
 @dataclass
@@ -135,6 +136,23 @@ def blur_laplacian_detect(img, lpf, frac: float = 0.5, col_stage=None, lap_scale
     if return_fields:
         return dets, blur, lap
     return dets
+
+
+def detect_sweep(img, stages, frac: float = 0.5, lap_scales=None, cap: int = 1 << 18):
+    """One frame through the fused single-scale path once per blur stage
+    (config 3's IIR-vs-FIR scale sweep): the frame is uploaded once, each
+    scale's detections come back to the host.  Returns a list of Detections."""
+    x, kind, code = _as_image(img)
+    out = []
+    for i, st in enumerate(stages):
+        stg = _Stage(st)
+        sc = 1.0 if lap_scales is None else float(lap_scales[i])
+        det_yx, det_val, scal, n = _fused(x, code, stg, stg, sc, frac, None, None, cap, True)
+        m = min(n, cap)
+        thr = float(scal[1:2].view(torch.float32)[0].item())
+        yx, val = det_yx[:m].cpu().numpy(), det_val[:m].cpu().numpy()
+        out.append(Detections(yx[:, 0], yx[:, 1], val, thr, n, n > cap))
+    return out
 
 
 def scale_space_detect(img, stages, sigmas, frac: float = 0.5, cap: int = 1 << 18,
