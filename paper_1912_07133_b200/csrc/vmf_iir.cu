@@ -24,11 +24,13 @@
 //              forward part is parked in shared memory (fp64) and combined
 //              with the backward part on the way back.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "vmf_common.cuh"
 #include "vmf_iir.cuh"
 #include "vmf_prof.cuh"
+#include "vmf_rowpass.cuh"
 
 namespace vmf {
 
@@ -410,6 +412,10 @@ int iir_pass(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t
       scale_kernel<<<(int)cdiv(n, 256), 256, 0, st>>>((const uint16_t *)x, ldx, y, ldy, h, w,
                                                       b_zero);
     return cuda_status("iir scale");
+  }
+  if (O == ROWS && rowpass_supported(w, k) && !getenv("VMF_FORCE_GENERIC")) {
+    if (x_dtype == VMF_F32) return rowpass_run<float>((const float *)x, ldx, y, ldy, p, h, w, st);
+    return rowpass_run<uint16_t>((const uint16_t *)x, ldx, y, ldy, p, h, w, st);
   }
   size_t need = iir_workspace_bytes(lines, length, k);
   if (ws_bytes < need || !ws)

@@ -1,0 +1,30 @@
+// vmf_rowpass.cuh -- single-kernel row pass (vmf_rowpass.cu).
+#pragma once
+#include "vmf_iir.cuh"
+
+namespace vmf {
+
+constexpr int kChunk = 32;          // samples per thread (one chunk)
+constexpr int kRowThreads = 128;    // target threads per CTA (R rows x C chunks)
+constexpr int kRowMaxThreads = 256; // rows up to 8192 samples (C <= 256)
+constexpr int kRowMinBlocks = 2;    // with 256 threads -> <= 128 registers
+constexpr int64_t kRowTileBytes = 40 * 1024;
+
+struct RowParams {
+  double b[VMF_MAX_IIR_ORDER], a[VMF_MAX_IIR_ORDER];
+  double b0, sign, yss;
+  double h[kChunk + 1];  // causal impulse response h[0..32], h[0] = 0
+  double Ty[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // DF-I history transfer over 32 samples
+  double Tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
+  double Tpow[5][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // Ty^(cpl*2^j)
+  int64_t H, W;
+  int C, R, cpl;
+  int vec4;
+};
+
+bool rowpass_supported(int64_t w, int k);
+template <typename T>
+int rowpass_run(const T *x, int64_t ldx, float *y, int64_t ldy, const IirParams &ip, int64_t h,
+                int64_t w, cudaStream_t st);
+
+}  // namespace vmf
