@@ -1,10 +1,12 @@
 // vmf_capi.cu -- extern "C" entry points of libvmfilt_b200.so (declared in
 // include/vmfilt_b200.h).  Host-side validation mirrors the reference
 // wrappers (engine.py:105-109, 115-118, 139-142) before anything is launched.
+#include <cstdlib>
 #include <cstring>
 
 #include "vmf_common.cuh"
 #include "vmf_iir.cuh"
+#include "vmf_colpass.cuh"
 #include "vmf_stage4.cuh"
 
 namespace vmf {
@@ -138,6 +140,11 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ld
                 thr_dev, n_det_host, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+static bool fused_col(const vmf_stage *col_stage, int64_t h, int64_t w) {
+  return col_stage && col_stage->kind == VMF_STAGE_IIR && colpass_supported(h, w, col_stage->n) &&
+         !getenv("VMF_FORCE_GENERIC");
+}
+
 // workspace: [T row-pass out][B if blur_out NULL][L if lap_out NULL][iir carry][detect]
 size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage,
                                            const vmf_stage *col_stage) {
@@ -145,6 +152,10 @@ size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage
   size_t carry = stage_ws(row_stage, h, w);
   size_t c2 = stage_ws(col_stage, w, h);
   if (c2 > carry) carry = c2;
+  if (fused_col(col_stage, h, w)) {
+    size_t c3 = colpass_workspace_bytes(h, w, col_stage->n, 0);
+    if (c3 > carry) carry = c3;
+  }
   return 3 * img + align256(carry) + align256(detect_workspace_bytes(1, h, w)) + 256;
 }
 
@@ -179,6 +190,26 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   size_t dws_b = align256(detect_workspace_bytes(1, h, w));
   rc = run_stage<ROWS>(row_stage, x, x_dtype, T, h, w, ldx, w, carry, carry_b, st);
   if (rc) return rc;
+  if (fused_col(col_stage, h, w) && frac > 0.0f) {
+    // column IIR + Laplacian + NMS in one pass over T (vmf_colpass.cu)
+    IirParams ip;
+    rc = iir_plan(&ip, w, h, col_stage->b_plus, col_stage->a_plus, col_stage->n,
+                  col_stage->b_zero, col_stage->sign);
+    if (rc) return rc;
+    rc = colpass_run(T, w, L, w, ip, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
+                     thr_dev, carry, carry_b, st);
+    if (rc) return rc;
+    if (blur_out) {  // B is not materialised by the fused pass; recompute on request
+      rc = run_stage<COLS>(col_stage, T, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);
+      if (rc) return rc;
+    }
+    if (n_det_host) {
+      cudaMemcpyAsync(n_det_host, n_det_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      return cuda_status("detect readback");
+    }
+    return VMF_OK;
+  }
   rc = run_stage<COLS>(col_stage, T, VMF_F32, B, h, w, w, w, carry, carry_b, st);
   if (rc) return rc;
   float *absmax = detect_absmax_slot(dws);

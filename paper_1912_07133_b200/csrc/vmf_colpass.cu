@@ -1,0 +1,687 @@
+// vmf_colpass.cu -- the fused second pass of the hot path: column IIR
+// (iir_cols, engine.py:156-158 / kernel 65-102) + Laplacian D20 + D02
+// (engine.py:218-227, blob.py:161) + threshold / 3x3 NMS,
+// reading the row-pass output T once more from L2/HBM and writing L plus a
+// short candidate list.  fp64 state, fp64 blur B, L computed from un-rounded
+// B (tools/experiments/park_precision.py: this is what keeps L within 1e-5 of
+// the reference instead of 7e-5).
+//
+// Column chunking is two-level:
+//   bands (256 rows)  : zero-state band carries (colcarry) -> sequential band
+//                       scan per column (colscan) -> true DF-I histories at
+//                       every band edge;
+//   sub-chunks (32)   : inside colapply a CTA (128 columns x one band) gets the
+//                       backward starts of its 8 sub-chunks from a local
+//                       carry + scan, then walks the band top-down: per
+//                       sub-chunk a backward run parked in 32 fp64 registers
+//                       and a forward run producing B, so the forward
+//                       recursion never needs a carry inside the band.
+// Rows are padded to a multiple of 32 with copies of the last row (a steady
+// state fed its own constant stays steady), so every sub-chunk is full.
+//
+// Laplacian/NMS: B rows of a sub-chunk go to shared memory; L lags B by one
+// row and NMS lags L by one row, so only 2 rows of B and L carry over between
+// sub-chunks.  At band edges the 2 rows outside the band are recomputed from
+// the band-edge histories (2 extra recursion steps).  A CTA computes 128
+// columns and owns the 124 inner ones (2-column halo for Lx and the 3x3 NMS).
+//
+// Threshold: t = frac * max|L| is known only at the end, so a CTA keeps the
+// strict extrema with |L| >= frac * (its running max) in shared memory --
+// a superset of the final detections -- and flushes them at the band end;
+// colfinal sorts the survivors of the final threshold by (y, x).  If a buffer
+// overflows, the ordered full-frame NMS of vmf_stage4.cu runs instead.
+#include <cstring>
+
+#include "vmf_colpass.cuh"
+#include "vmf_common.cuh"
+#include "vmf_prof.cuh"
+#include "vmf_stage4.cuh"
+
+namespace vmf {
+
+__device__ __forceinline__ double ldT(const float *T, int64_t ldt, int64_t r, int64_t H,
+                                      int64_t c) {
+  return (double)__ldg(T + (r < H ? r : H - 1) * ldt + c);
+}
+
+// ---------------------------------------------------------------------------
+// 1. band carries: zero-state end histories of every (band, column)
+// ---------------------------------------------------------------------------
+// Z layout: Z[((b * 2 + dir) * K + i) * W + col]
+template <int K>
+__global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__restrict__ T,
+                                                               int64_t ldt, ColParams p,
+                                                               double *__restrict__ Z) {
+  __shared__ double SP[K][kBand / 2], SQ[K][kBand / 2];
+  const int b = blockIdx.y;
+  const int len = b == p.NB - 1 ? p.Blast : kBand;
+  const int half = len / 2;
+  // pair weights: f_i = sum_t h(len-1-i-t) x_t, g_i = sum_t h(t-i) x_t; with
+  // u = x_t + x_t', v = x_t - x_t' (t' = len-1-t): f = P + Q, g = P - Q.
+  for (int q = threadIdx.x; q < K * half; q += blockDim.x) {
+    int i = q / half, t = q % half;
+    int qa = len - 1 - i - t, qb = t - i;
+    double A = qa > 0 ? p.h[qa] : 0.0, B = qb > 0 ? p.h[qb] : 0.0;
+    SP[i][t] = 0.5 * (A + B);
+    SQ[i][t] = 0.5 * (A - B);
+  }
+  __syncthreads();
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= p.W) return;
+  const int64_t r0 = (int64_t)b * kBand;
+  double P[K], Q[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
+#pragma unroll 4
+  for (int t = 0; t < half; ++t) {
+    double xa = ldT(T, ldt, r0 + t, p.H, col);
+    double xb = ldT(T, ldt, r0 + len - 1 - t, p.H, col);
+    double u = xa + xb, v = xa - xb;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      P[i] = fma(SP[i][t], u, P[i]);
+      Q[i] = fma(SQ[i][t], v, Q[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    Z[((int64_t)(b * 2 + 0) * K + i) * p.W + col] = P[i] + Q[i];
+    Z[((int64_t)(b * 2 + 1) * K + i) * p.W + col] = P[i] - Q[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2. band scan per column: Z -> true histories at band edges (in place)
+//    fwd slot b: y+(r0-1 .. r0-K); bwd slot b: y-(r1 .. r1+K-1)
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ T, int64_t ldt,
+                                                      ColParams p, double *__restrict__ Z) {
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= p.W) return;
+  double E[K], X[K], Zv[K];
+  const double x0 = ldT(T, ldt, 0, p.H, col);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    E[i] = p.yss * x0;
+    X[i] = x0;
+  }
+  for (int b = 0; b < p.NB; ++b) {
+    double *slot = Z + (int64_t)(b * 2 + 0) * K * p.W + col;
+#pragma unroll
+    for (int i = 0; i < K; ++i) Zv[i] = slot[i * p.W];
+#pragma unroll
+    for (int i = 0; i < K; ++i) slot[i * p.W] = E[i];
+    if (b < p.NB - 1) {
+      const int64_t r1 = (int64_t)(b + 1) * kBand;
+      double En[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double acc = Zv[i];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fma(p.TxB[0][i * K + j], X[j], acc);
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fma(p.TyB[0][i * K + j], E[j], acc);
+        En[i] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        E[i] = En[i];
+        X[i] = ldT(T, ldt, r1 - 1 - i, p.H, col);
+      }
+    }
+  }
+  const double xl = ldT(T, ldt, p.H - 1, p.H, col);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    E[i] = p.yss * xl;
+    X[i] = xl;
+  }
+  for (int b = p.NB - 1; b >= 0; --b) {
+    double *slot = Z + (int64_t)(b * 2 + 1) * K * p.W + col;
+#pragma unroll
+    for (int i = 0; i < K; ++i) Zv[i] = slot[i * p.W];
+#pragma unroll
+    for (int i = 0; i < K; ++i) slot[i * p.W] = E[i];
+    if (b > 0) {
+      const int tb = b == p.NB - 1 ? 1 : 0;
+      const int64_t r0 = (int64_t)b * kBand;
+      double En[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double acc = Zv[i];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fma(p.TxB[tb][i * K + j], X[j], acc);
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fma(p.TyB[tb][i * K + j], E[j], acc);
+        En[i] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        E[i] = En[i];
+        X[i] = ldT(T, ldt, r0 + i, p.H, col);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3. walk a band: column IIR + Laplacian + NMS candidates
+// ---------------------------------------------------------------------------
+template <int K>
+__device__ __forceinline__ double dfi(const ColParams &p, const double *X, const double *Y) {
+  double s = 0.0;
+#pragma unroll
+  for (int m = 0; m < K; ++m) s = fma(p.b[m], X[m], s);
+#pragma unroll
+  for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Y[m], s);
+  return fma(-p.a[0], Y[0], s);
+}
+
+template <int K>
+__device__ __forceinline__ void push2(double *Y, double y, double *X, double x) {
+#pragma unroll
+  for (int m = K - 1; m > 0; --m) {
+    Y[m] = Y[m - 1];
+    X[m] = X[m - 1];
+  }
+  Y[0] = y;
+  X[0] = x;
+}
+
+template <int K>
+struct ColSmem {
+  double xs[kSub + K][kColThreads];   // x of the sub-chunk (+K rows below), then B in place
+  double bprev[2][kColThreads];       // B of the 2 rows above the sub-chunk
+  double fbs[kBand / kSub][K][kColThreads];  // backward start history per sub-chunk
+  float lcur[kSub + 2][kColThreads];  // L rows [rbase-1, rbase+33)
+  float lprev[2][kColThreads];        // L rows rbase-3, rbase-2
+  int cy[kCandSmem], cx[kCandSmem];
+  float cv[kCandSmem];
+  int ccount;
+  int coverflow;
+  unsigned int cmax;                  // running max |L| of this CTA (float bits)
+};
+
+template <int K>
+__global__ void __launch_bounds__(kColThreads) colapply_kernel(
+    const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, ColParams p,
+    const double *__restrict__ Z, CandState *__restrict__ st, int *__restrict__ gy,
+    int *__restrict__ gx, float *__restrict__ gv, int gcap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ColSmem<K> &S = *reinterpret_cast<ColSmem<K> *>(smem_raw);
+  const int j = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * kColOut;
+  const int64_t col = c0 - kColHalo + j;
+  const int64_t colc = col < 0 ? 0 : (col >= p.W ? p.W - 1 : col);
+  const int b = blockIdx.y;
+  const int64_t r0 = (int64_t)b * kBand;
+  const int len = b == p.NB - 1 ? p.Blast : kBand;
+  const int64_t r1 = r0 + len;
+  const int nsub = len / kSub;
+  const int64_t H = p.H;
+  const bool own_col = j >= kColHalo && j < kColThreads - kColHalo && col < p.W;
+  if (j == 0) {
+    S.ccount = 0;
+    S.coverflow = 0;
+    S.cmax = st->absmax_bits;  // global running max so far: a valid lower bound
+  }
+
+  // ---- fine backward carries of the sub-chunks + reverse scan -------------
+  double Ybot[K], E[K], X[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    Ybot[i] = Z[((int64_t)(b * 2 + 1) * K + i) * p.W + colc];
+    E[i] = Ybot[i];
+    X[i] = ldT(T, ldt, r1 + i, H, colc);
+  }
+  for (int s = nsub - 1; s >= 0; --s) {
+    const int64_t rb = r0 + (int64_t)s * kSub;
+    double zb[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) zb[i] = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < kSub; ++t) {
+      double v = ldT(T, ldt, rb + t, H, colc);
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+        if (t - i > 0) zb[i] = fma(p.h[t - i], v, zb[i]);
+    }
+    double En[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      S.fbs[s][i][j] = E[i];
+      double acc = zb[i];
+#pragma unroll
+      for (int q = 0; q < K; ++q) acc = fma(p.Tx[i * K + q], X[q], acc);
+#pragma unroll
+      for (int q = 0; q < K; ++q) acc = fma(p.Ty[i * K + q], E[q], acc);
+      En[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      E[i] = En[i];
+      X[i] = ldT(T, ldt, rb + i, H, colc);
+    }
+  }
+
+  // ---- walk -------------------------------------------------------------------
+  double Yf[K], Xf[K], Ytop[2];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    Yf[i] = Z[((int64_t)(b * 2 + 0) * K + i) * p.W + colc];
+    int64_t q = r0 - 1 - i;
+    Xf[i] = ldT(T, ldt, q < 0 ? 0 : q, H, colc);
+  }
+  Ytop[0] = Yf[0];
+  Ytop[1] = Yf[1];
+  const double lsc = (double)p.lap_scale;
+
+  for (int s = 0; s < nsub; ++s) {
+    const int64_t rbase = r0 + (int64_t)s * kSub;
+    const bool last = s == nsub - 1;
+    __syncthreads();  // previous sub-chunk's smem reads are done
+#pragma unroll 4
+    for (int t = 0; t < kSub + K; ++t) S.xs[t][j] = ldT(T, ldt, rbase + t, H, colc);
+
+    // backward run, parked in registers
+    double park[kSub];
+    double Yb[K], Xb[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      Yb[i] = S.fbs[s][i][j];
+      Xb[i] = S.xs[kSub + i][j];
+    }
+#pragma unroll
+    for (int t = kSub - 1; t >= 0; --t) {
+      double xv = S.xs[t][j];
+      double y = dfi<K>(p, Xb, Yb);
+      park[t] = p.sign * y;
+      push2<K>(Yb, y, Xb, xv);
+    }
+    if (s == 0) {
+      if (r0 > 0) {  // B at rows r0-1, r0-2 from the band-edge histories
+        double x1 = ldT(T, ldt, r0 - 1, H, colc);
+        double x2 = ldT(T, ldt, r0 >= 2 ? r0 - 2 : 0, H, colc);
+        double ym1 = dfi<K>(p, Xb, Yb);
+        push2<K>(Yb, ym1, Xb, x1);
+        double ym2 = dfi<K>(p, Xb, Yb);
+        S.bprev[1][j] = fma(p.b0, x1, Ytop[0]) + p.sign * ym1;
+        S.bprev[0][j] = fma(p.b0, x2, Ytop[1]) + p.sign * ym2;
+      }
+    }
+    // forward run: B(rbase + t) replaces x in place
+#pragma unroll
+    for (int t = 0; t < kSub; ++t) {
+      double xv = S.xs[t][j];
+      double y = dfi<K>(p, Xf, Yf);
+      S.xs[t][j] = fma(p.b0, xv, y) + park[t];
+      push2<K>(Yf, y, Xf, xv);
+    }
+    if (s == 0 && r0 == 0) {  // replicate edge: B(-1) = B(0)
+      S.bprev[1][j] = S.xs[0][j];
+      S.bprev[0][j] = S.xs[0][j];
+    }
+    if (last) {  // B at rows r1, r1+1 (next band) for L(r1-1), L(r1)
+      double xr1 = S.xs[kSub][j], xr2 = S.xs[kSub + 1][j];
+      double Y2[K], X2[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        Y2[i] = Yf[i];
+        X2[i] = Xf[i];
+      }
+      double y0 = dfi<K>(p, X2, Y2);
+      push2<K>(Y2, y0, X2, xr1);
+      double y1 = dfi<K>(p, X2, Y2);
+      S.xs[kSub][j] = fma(p.b0, xr1, y0) + p.sign * Ybot[0];
+      S.xs[kSub + 1][j] = fma(p.b0, xr2, y1) + p.sign * Ybot[1];
+    }
+    __syncthreads();
+
+    // Laplacian rows [rbase-1, rbase+31) (+2 at the band end)
+    const int nl = last ? kSub + 2 : kSub;
+    const int jl = j > 0 ? j - 1 : 0, jr = j < kColThreads - 1 ? j + 1 : kColThreads - 1;
+    float lmax = 0.0f;
+    for (int q = 0; q < nl; ++q) {
+      const int64_t r = rbase - 1 + q;
+      float lv = 0.0f;
+      if (r >= 0 && r < H && j > 0 && j < kColThreads - 1) {
+        auto Bat = [&](int64_t rr, int jj) -> double {
+          if (rr >= H) rr = H - 1;  // replicate bottom edge
+          int64_t d = rr - rbase;
+          if (d >= 0) return S.xs[d][jj];
+          return S.bprev[d + 2][jj];
+        };
+        double bc = Bat(r, j);
+        double dx = Bat(r, jl) - 2.0 * bc + Bat(r, jr);
+        double dy = Bat(r - 1, j) - 2.0 * bc + Bat(r + 1, j);
+        lv = (float)(lsc * (dx + dy));
+        if (r >= r0 && r < r1 && own_col) {
+          Lout[r * ldl + col] = lv;
+          lmax = fmaxf(lmax, fabsf(lv));
+        }
+      }
+      S.lcur[q][j] = lv;
+    }
+    atomicMax(&S.cmax, __float_as_uint(lmax));
+    __syncthreads();
+
+    // NMS rows [rbase-2, rbase+30) (+2 at the band end), owned rows only
+    const float thr = p.frac * __uint_as_float(S.cmax);
+    const int nn = last ? kSub + 2 : kSub;
+    if (own_col && col >= 1 && col <= p.W - 2) {
+      for (int q = 0; q < nn; ++q) {
+        const int64_t r = rbase - 2 + q;
+        if (r < r0 || r < 1 || r > H - 2) continue;
+        auto Lat = [&](int64_t rr, int jj) -> float {
+          int64_t d = rr - (rbase - 1);
+          if (d >= 0) return S.lcur[d][jj];
+          return S.lprev[d + 2][jj];
+        };
+        float v = Lat(r, j);
+        if (!(fabsf(v) >= thr)) continue;
+        bool gt = true, lt = true;
+#pragma unroll
+        for (int di = -1; di <= 1; ++di)
+#pragma unroll
+          for (int dj = -1; dj <= 1; ++dj) {
+            if (!di && !dj) continue;
+            float u = Lat(r + di, j + dj);
+            gt &= v > u;
+            lt &= v < u;
+          }
+        if (gt || lt) {
+          int k = atomicAdd(&S.ccount, 1);
+          if (k < kCandSmem) {
+            S.cy[k] = (int)r;
+            S.cx[k] = (int)col;
+            S.cv[k] = v;
+          } else {
+            S.coverflow = 1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // carry 2 rows of B and L into the next sub-chunk; compact candidates
+    if (!last) {
+      S.bprev[0][j] = S.xs[kSub - 2][j];
+      S.bprev[1][j] = S.xs[kSub - 1][j];
+      S.lprev[0][j] = S.lcur[kSub - 2][j];
+      S.lprev[1][j] = S.lcur[kSub - 1][j];
+    }
+    if (j == 0 && S.ccount > kCandSmem / 2) {
+      const float t2 = p.frac * __uint_as_float(S.cmax);
+      int n = S.ccount < kCandSmem ? S.ccount : kCandSmem, m = 0;
+      for (int q = 0; q < n; ++q)
+        if (fabsf(S.cv[q]) >= t2) {
+          S.cy[m] = S.cy[q];
+          S.cx[m] = S.cx[q];
+          S.cv[m] = S.cv[q];
+          ++m;
+        }
+      S.ccount = m;
+    }
+  }
+  __syncthreads();
+
+  // ---- flush candidates that survive the best threshold known now ---------
+  __shared__ float thr_end;
+  if (j == 0) {
+    unsigned old = atomicMax(&st->absmax_bits, S.cmax);
+    float m = fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
+    thr_end = p.frac * m;
+    if (S.coverflow) st->overflow = 1;
+  }
+  __syncthreads();
+  const int n = S.ccount < kCandSmem ? S.ccount : kCandSmem;
+  for (int q = j; q < n; q += blockDim.x) {
+    if (!(fabsf(S.cv[q]) >= thr_end)) continue;
+    int k = atomicAdd(&st->count, 1);
+    if (k < gcap) {
+      gy[k] = S.cy[q];
+      gx[k] = S.cx[q];
+      gv[k] = S.cv[q];
+    } else {
+      st->overflow = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 4. final threshold + (y, x) order: one CTA, bitonic sort in shared memory
+// ---------------------------------------------------------------------------
+constexpr int kSortCap = 4096;
+
+__global__ void __launch_bounds__(1024) colfinal_kernel(CandState *__restrict__ st,
+                                                        const int *__restrict__ gy,
+                                                        const int *__restrict__ gx,
+                                                        const float *__restrict__ gv, int gcap,
+                                                        int64_t W, float frac, int32_t *det_yx,
+                                                        float *det_val, int64_t cap,
+                                                        int64_t *n_det, float *thr_out,
+                                                        int *fallback) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  unsigned long long *key = reinterpret_cast<unsigned long long *>(fsm);
+  float *val = reinterpret_cast<float *>(fsm + kSortCap * sizeof(unsigned long long));
+  __shared__ int m;
+  const float thr = frac * __uint_as_float(st->absmax_bits);
+  if (threadIdx.x == 0) {
+    m = 0;
+    if (thr_out) *thr_out = thr;
+  }
+  __syncthreads();
+  const int n = st->count < gcap ? st->count : gcap;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    float v = gv[q];
+    if (!(fabsf(v) >= thr)) continue;
+    int k = atomicAdd(&m, 1);
+    if (k < kSortCap) {
+      key[k] = (unsigned long long)gy[q] * (unsigned long long)W + (unsigned long long)gx[q];
+      val[k] = v;
+    }
+  }
+  __syncthreads();
+  const bool fb = st->overflow || m > kSortCap;
+  if (fb) {
+    if (threadIdx.x == 0) *fallback = 1;
+    return;
+  }
+  if (threadIdx.x == 0) *fallback = 0;
+  int np = 1;
+  while (np < m) np <<= 1;
+  for (int q = m + threadIdx.x; q < np; q += blockDim.x) key[q] = ~0ull;
+  __syncthreads();
+  for (int kk = 2; kk <= np; kk <<= 1)
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        int ix = i ^ jj;
+        if (ix > i) {
+          bool up = (i & kk) == 0;
+          unsigned long long a = key[i], c = key[ix];
+          if ((a > c) == up) {
+            key[i] = c;
+            key[ix] = a;
+            float t = val[i];
+            val[i] = val[ix];
+            val[ix] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int q = threadIdx.x; q < m && q < cap; q += blockDim.x) {
+    det_yx[2 * q] = (int32_t)(key[q] / (unsigned long long)W);
+    det_yx[2 * q + 1] = (int32_t)(key[q] % (unsigned long long)W);
+    det_val[q] = val[q];
+  }
+  if (threadIdx.x == 0) *n_det = m;
+}
+
+// ---------------------------------------------------------------------------
+// host
+// ---------------------------------------------------------------------------
+static void transfer_ld(const double *b, const double *a, int k, int len, double *Ty,
+                        double *Tx) {
+  for (int jj = 0; jj < 2 * k; ++jj) {
+    long double Y[VMF_MAX_IIR_ORDER], X[VMF_MAX_IIR_ORDER];
+    for (int m = 0; m < k; ++m) {
+      Y[m] = (jj == m) ? 1.0L : 0.0L;
+      X[m] = (jj == k + m) ? 1.0L : 0.0L;
+    }
+    for (int n = 0; n < len; ++n) {
+      long double v = 0.0L;
+      for (int m = 0; m < k; ++m) v += (long double)b[m] * X[m] - (long double)a[m] * Y[m];
+      for (int m = k - 1; m > 0; --m) {
+        Y[m] = Y[m - 1];
+        X[m] = X[m - 1];
+      }
+      Y[0] = v;
+      X[0] = 0.0L;
+    }
+    for (int i = 0; i < k; ++i) {
+      if (jj < k)
+        Ty[i * k + jj] = (double)Y[i];
+      else
+        Tx[i * k + (jj - k)] = (double)Y[i];
+    }
+  }
+}
+
+static void impulse_ld(const double *b, const double *a, int k, int n, double *h) {
+  long double Y[VMF_MAX_IIR_ORDER] = {0}, X[VMF_MAX_IIR_ORDER] = {0};
+  for (int q = 0; q < n; ++q) {
+    long double v = 0.0L;
+    for (int m = 0; m < k; ++m) v += (long double)b[m] * X[m] - (long double)a[m] * Y[m];
+    h[q] = (double)v;
+    for (int m = k - 1; m > 0; --m) {
+      Y[m] = Y[m - 1];
+      X[m] = X[m - 1];
+    }
+    Y[0] = v;
+    X[0] = q == 0 ? 1.0L : 0.0L;
+  }
+}
+
+bool colpass_supported(int64_t h, int64_t w, int k) {
+  return k >= 2 && k <= 4 && h >= 2 * kSub && w >= 1;
+}
+
+static void col_geometry(int64_t h, int64_t *Hp, int *NB, int *Blast) {
+  int64_t hp = cdiv(h, kSub) * kSub;
+  int nb = (int)cdiv(hp, kBand);
+  *Hp = hp;
+  *NB = nb;
+  *Blast = (int)(hp - (int64_t)(nb - 1) * kBand);
+}
+
+static int64_t cand_capacity(int64_t h, int64_t w) {
+  int64_t c = h * w / 64;
+  if (c < 65536) c = 65536;
+  return c;
+}
+
+size_t colpass_workspace_bytes(int64_t h, int64_t w, int k, int64_t) {
+  int64_t Hp;
+  int NB, Bl;
+  col_geometry(h, &Hp, &NB, &Bl);
+  int64_t gcap = cand_capacity(h, w);
+  size_t z = (size_t)NB * 2 * k * w * sizeof(double);
+  return 4096 + ((z + 255) & ~(size_t)255) + (size_t)gcap * 12 + 1024 +
+         detect_workspace_bytes(1, h, w);
+}
+
+template <int K>
+static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, const ColParams &p,
+                          int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
+                          float *thr_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
+  char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  CandState *cs = (CandState *)base;
+  int *fallback = (int *)(base + 64);
+  size_t z = (size_t)p.NB * 2 * K * p.W * sizeof(double);
+  double *Z = (double *)(base + 4096);
+  char *q = base + 4096 + ((z + 255) & ~(size_t)255);
+  int64_t gcap = cand_capacity(p.H, p.W);
+  int *gy = (int *)q;
+  int *gx = gy + gcap;
+  float *gv = (float *)(gx + gcap);
+  void *dws = (void *)(((uintptr_t)(gv + gcap) + 255) & ~(uintptr_t)255);
+  size_t dws_b = detect_workspace_bytes(1, p.H, p.W);
+  cudaMemsetAsync(cs, 0, 128, st);
+  {
+    Launch g(K_COL_CARRY, st);
+    dim3 grid((unsigned)cdiv(p.W, kColThreads), (unsigned)p.NB);
+    colcarry_kernel<K><<<grid, kColThreads, 0, st>>>(T, ldt, p, Z);
+  }
+  {
+    Launch g(K_COL_SCAN, st);
+    colscan_kernel<K><<<(unsigned)cdiv(p.W, 128), 128, 0, st>>>(T, ldt, p, Z);
+  }
+  {
+    Launch g(K_IIR_COLS_FUSED, st);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(colapply_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ColSmem<K>));
+      attr = true;
+    }
+    dim3 grid((unsigned)cdiv(p.W, kColOut), (unsigned)p.NB);
+    colapply_kernel<K><<<grid, kColThreads, sizeof(ColSmem<K>), st>>>(T, ldt, L, ldl, p, Z, cs, gy,
+                                                                      gx, gv, (int)gcap);
+  }
+  {
+    Launch g(K_FINALIZE, st);
+    const int fsmem = kSortCap * (int)(sizeof(unsigned long long) + sizeof(float));
+    static bool fattr = false;
+    if (!fattr) {
+      cudaFuncSetAttribute(colfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+      fattr = true;
+    }
+    colfinal_kernel<<<1, 1024, fsmem, st>>>(cs, gy, gx, gv, (int)gcap, p.W, p.frac, det_yx,
+                                            det_val, cap, n_det_dev, thr_dev, fallback);
+  }
+  int rc = cuda_status("column pass");
+  if (rc) return rc;
+  // ordered full-frame NMS, executed only if the candidate path overflowed
+  return detect_if(L, ldl, p.H, p.W, p.frac, (float *)&cs->absmax_bits, fallback, det_yx,
+                   det_val, cap, n_det_dev, thr_dev, dws, dws_b, st);
+}
+
+int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,
+                int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
+                float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
+                size_t ws_bytes, cudaStream_t st) {
+  size_t need = colpass_workspace_bytes(h, w, ip.K, cap);
+  if (!ws || ws_bytes < need)
+    return fail(VMF_EVALUE, "column-pass workspace too small: %zu < %zu bytes", ws_bytes, need);
+  ColParams p;
+  memset(&p, 0, sizeof(p));
+  const int k = ip.K;
+  for (int m = 0; m < k; ++m) {
+    p.b[m] = ip.b[m];
+    p.a[m] = ip.a[m];
+  }
+  p.b0 = ip.b0;
+  p.sign = ip.sign;
+  p.yss = ip.yss;
+  impulse_ld(ip.b, ip.a, k, kHMax, p.h);
+  transfer_ld(ip.b, ip.a, k, kSub, p.Ty, p.Tx);
+  p.H = h;
+  p.W = w;
+  col_geometry(h, &p.Hp, &p.NB, &p.Blast);
+  transfer_ld(ip.b, ip.a, k, kBand, p.TyB[0], p.TxB[0]);
+  transfer_ld(ip.b, ip.a, k, p.Blast, p.TyB[1], p.TxB[1]);
+  p.lap_scale = lap_scale;
+  p.frac = frac;
+  switch (k) {
+    case 2: return launch_colpass<2>(T, ldt, L, ldl, p, det_yx, det_val, cap, n_det_dev, thr_dev,
+                                     ws, ws_bytes, st);
+    case 3: return launch_colpass<3>(T, ldt, L, ldl, p, det_yx, det_val, cap, n_det_dev, thr_dev,
+                                     ws, ws_bytes, st);
+    case 4: return launch_colpass<4>(T, ldt, L, ldl, p, det_yx, det_val, cap, n_det_dev, thr_dev,
+                                     ws, ws_bytes, st);
+  }
+  return fail(VMF_EVALUE, "fused column pass supports K = 2..4, got %d", k);
+}
+
+}  // namespace vmf

@@ -1,0 +1,45 @@
+// vmf_colpass.cuh -- the fused column pass: column IIR + Laplacian + 3x3 NMS
+// (vmf_colpass.cu).
+#pragma once
+#include "vmf_iir.cuh"
+
+namespace vmf {
+
+constexpr int kSub = 32;            // rows per sub-chunk (one recursion run)
+constexpr int kBand = 256;          // rows per band (carry granularity)
+constexpr int kColThreads = 128;    // computed columns per CTA
+constexpr int kColHalo = 2;         // halo columns each side (Laplacian + NMS)
+constexpr int kColOut = kColThreads - 2 * kColHalo;  // 124 output columns per CTA
+constexpr int kCandSmem = 512;      // per-CTA candidate buffer
+constexpr int kHMax = kBand + 2 * VMF_MAX_IIR_ORDER + 2;
+
+struct ColParams {
+  double b[VMF_MAX_IIR_ORDER], a[VMF_MAX_IIR_ORDER];
+  double b0, sign, yss;
+  double h[kHMax];        // causal impulse response, h[0] = 0
+  double Ty[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];   // over one 32-row sub-chunk
+  double Tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
+  double TyB[2][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // over a band / the last band
+  double TxB[2][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
+  int64_t H, W, Hp;       // Hp = H rounded up to 32 (rows >= H replicate row H-1)
+  int NB, Blast;          // bands; rows in the last band (multiple of 32)
+  float lap_scale, frac;
+};
+
+// Device-side bookkeeping shared by the fused column pass and the finaliser.
+struct CandState {
+  unsigned int absmax_bits;  // max |L| (float bits)
+  int count;                 // candidates appended
+  int overflow;              // a CTA buffer or the global list overflowed
+  int pad;
+};
+
+bool colpass_supported(int64_t h, int64_t w, int k);
+size_t colpass_workspace_bytes(int64_t h, int64_t w, int k, int64_t cand_cap);
+// T (fp32, h x w, pitch ldt) -> L (pitch ldl) + detections (sorted by y, x).
+int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,
+                int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
+                float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
+                size_t ws_bytes, cudaStream_t st);
+
+}  // namespace vmf

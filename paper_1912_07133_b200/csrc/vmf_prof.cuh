@@ -22,6 +22,8 @@ enum KernelId {
   K_IIR_ROWS_FUSED,
   K_IIR_COLS_FUSED,
   K_FINALIZE,
+  K_COL_CARRY,
+  K_COL_SCAN,
   K_NUM_IDS
 };
 

@@ -102,7 +102,9 @@ __device__ __forceinline__ bool is_det(const float *__restrict__ l, int64_t ld, 
 
 __global__ void __launch_bounds__(kNmsThreads) nms_count_kernel(
     const float *__restrict__ l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int64_t w,
-    float frac, const float *__restrict__ absmax, float *thr_out, int *__restrict__ counts) {
+    float frac, const float *__restrict__ absmax, float *thr_out, int *__restrict__ counts,
+    const int *gate) {
+  if (gate && !*gate) return;
   float thr = frac * *absmax;
   if (blockIdx.x == 0 && threadIdx.x == 0 && thr_out) *thr_out = thr;
   int64_t total = ns * h * w;
@@ -124,7 +126,9 @@ __global__ void __launch_bounds__(kNmsThreads) nms_count_kernel(
 
 // Single CTA: exclusive scan of per-CTA counts, total -> *n_det.
 __global__ void __launch_bounds__(1024) nms_scan_kernel(int *__restrict__ counts, int64_t nb,
-                                                        int64_t *__restrict__ n_det) {
+                                                        int64_t *__restrict__ n_det,
+                                                        const int *gate) {
+  if (gate && !*gate) return;
   __shared__ int64_t part[1024];
   int64_t per = (nb + blockDim.x - 1) / blockDim.x;
   int64_t lo = threadIdx.x * per, hi = lo + per < nb ? lo + per : nb;
@@ -153,7 +157,9 @@ __global__ void __launch_bounds__(1024) nms_scan_kernel(int *__restrict__ counts
 __global__ void __launch_bounds__(kNmsThreads) nms_write_kernel(
     const float *__restrict__ l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int64_t w,
     float frac, const float *__restrict__ absmax, const int *__restrict__ offsets,
-    int32_t *__restrict__ det_idx, int idx_stride, float *__restrict__ det_val, int64_t cap) {
+    int32_t *__restrict__ det_idx, int idx_stride, float *__restrict__ det_val, int64_t cap,
+    const int *gate) {
+  if (gate && !*gate) return;
   float thr = frac * *absmax;
   int64_t total = ns * h * w;
   int64_t base = (int64_t)blockIdx.x * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
@@ -259,6 +265,30 @@ size_t detect_workspace_bytes(int64_t ns, int64_t h, int64_t w) {
 }
 
 // ws layout: [0,256) absmax float; [256,512) scratch; [512, ...) counts
+static int detect_core(const float *l, int64_t ld, int64_t plane, int64_t ns, int64_t h,
+                       int64_t w, float frac, float *absmax, const int *gate, int32_t *det_idx,
+                       int idx_stride, float *det_val, int64_t cap, int64_t *n_det_dev,
+                       float *thr_dev, int *counts, cudaStream_t st) {
+  int64_t nb = cdiv(ns * h * w, kNmsPerBlock);
+  if (nb > 0x7fffffff) return fail(VMF_EVALUE, "frame stack too large");
+  {
+    Launch g(K_NMS_COUNT, st);
+    nms_count_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
+                                                           thr_dev, counts, gate);
+  }
+  {
+    Launch g(K_NMS_SCAN, st);
+    nms_scan_kernel<<<1, 1024, 0, st>>>(counts, nb, n_det_dev, gate);
+  }
+  {
+    Launch g(K_NMS_WRITE, st);
+    nms_write_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
+                                                           counts, det_idx, idx_stride, det_val,
+                                                           cap, gate);
+  }
+  return cuda_status("detect");
+}
+
 int detect(const float *l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int64_t w,
            float frac, bool have_absmax, int32_t *det_idx, int idx_stride, float *det_val,
            int64_t cap, int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host, void *ws,
@@ -276,24 +306,8 @@ int detect(const float *l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int
     Launch g(K_ABSMAX, st);
     absmax_kernel<<<sm_count() * 4, 256, 0, st>>>(l, ld, plane, ns, h, w, absmax);
   }
-  int64_t nb = cdiv(ns * h * w, kNmsPerBlock);
-  if (nb > 0x7fffffff) return fail(VMF_EVALUE, "frame stack too large");
-  {
-    Launch g(K_NMS_COUNT, st);
-    nms_count_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
-                                                           thr_dev, counts);
-  }
-  {
-    Launch g(K_NMS_SCAN, st);
-    nms_scan_kernel<<<1, 1024, 0, st>>>(counts, nb, n_det_dev);
-  }
-  {
-    Launch g(K_NMS_WRITE, st);
-    nms_write_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
-                                                           counts, det_idx, idx_stride, det_val,
-                                                           cap);
-  }
-  int rc = cuda_status("detect");
+  int rc = detect_core(l, ld, plane, ns, h, w, frac, absmax, nullptr, det_idx, idx_stride,
+                       det_val, cap, n_det_dev, thr_dev, counts, st);
   if (rc) return rc;
   if (n_det_host) {
     cudaMemcpyAsync(n_det_host, n_det_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
@@ -301,6 +315,16 @@ int detect(const float *l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int
     return cuda_status("detect readback");
   }
   return VMF_OK;
+}
+
+int detect_if(const float *l, int64_t ld, int64_t h, int64_t w, float frac, float *absmax,
+              const int *gate, int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
+              float *thr_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
+  size_t need = detect_workspace_bytes(1, h, w);
+  if (!ws || ws_bytes < need) return fail(VMF_EVALUE, "detect workspace too small");
+  char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  return detect_core(l, ld, h * ld, 1, h, w, frac, absmax, gate, det_yx, 2, det_val, cap,
+                     n_det_dev, thr_dev, (int *)(base + 512), st);
 }
 
 float *detect_absmax_slot(void *ws) {

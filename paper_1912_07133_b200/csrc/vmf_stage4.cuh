@@ -10,6 +10,11 @@ size_t detect_workspace_bytes(int64_t ns, int64_t h, int64_t w);
 // absmax lives in the first slot of the detect workspace; callers that
 // already reduced |L| there pass have_absmax = true.
 float *detect_absmax_slot(void *ws);
+// Ordered full-frame NMS whose kernels do nothing unless *gate != 0 (the
+// fallback of the fused column pass); absmax is a device float.
+int detect_if(const float *l, int64_t ld, int64_t h, int64_t w, float frac, float *absmax,
+              const int *gate, int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
+              float *thr_dev, void *ws, size_t ws_bytes, cudaStream_t st);
 int detect(const float *l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int64_t w,
            float frac, bool have_absmax, int32_t *det_idx, int idx_stride, float *det_val,
            int64_t cap, int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host, void *ws,
