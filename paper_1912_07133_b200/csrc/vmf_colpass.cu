@@ -57,11 +57,12 @@ __global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__re
   const int len = b == p.NB - 1 ? p.Blast : kBand;
   const int half = len / 2;
   // pair weights: f_i = sum_t h(len-1-i-t) x_t, g_i = sum_t h(t-i) x_t; with
-  // u = x_t + x_t', v = x_t - x_t' (t' = len-1-t): f = P + Q, g = P - Q.
-  for (int q = threadIdx.x; q < K * half; q += blockDim.x) {
-    int i = q / half, t = q % half;
+  // u = x_t + x_t', v = x_t - x_t' (t' = len-1-t): f = P + Q, g = P - Q, so a
+  // pair of samples costs 2 adds + 2K FMAs instead of 4K FMAs.
+  for (int q = threadIdx.x; q < K * (kBand / 2); q += blockDim.x) {
+    int i = q / (kBand / 2), t = q % (kBand / 2);
     int qa = len - 1 - i - t, qb = t - i;
-    double A = qa > 0 ? p.h[qa] : 0.0, B = qb > 0 ? p.h[qb] : 0.0;
+    double A = (t < half && qa > 0) ? p.h[qa] : 0.0, B = (t < half && qb > 0) ? p.h[qb] : 0.0;
     SP[i][t] = 0.5 * (A + B);
     SQ[i][t] = 0.5 * (A - B);
   }
@@ -72,15 +73,32 @@ __global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__re
   double P[K], Q[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
-#pragma unroll 4
-  for (int t = 0; t < half; ++t) {
-    double xa = ldT(T, ldt, r0 + t, p.H, col);
-    double xb = ldT(T, ldt, r0 + len - 1 - t, p.H, col);
-    double u = xa + xb, v = xa - xb;
+  if (len == kBand) {
+    float xa[kBand / 2], xb[kBand / 2];
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      P[i] = fma(SP[i][t], u, P[i]);
-      Q[i] = fma(SQ[i][t], v, Q[i]);
+    for (int t = 0; t < kBand / 2; ++t) {  // all loads in flight at once
+      xa[t] = __ldg(T + min(r0 + t, p.H - 1) * ldt + col);
+      xb[t] = __ldg(T + min(r0 + kBand - 1 - t, p.H - 1) * ldt + col);
+    }
+#pragma unroll
+    for (int t = 0; t < kBand / 2; ++t) {
+      double a = xa[t], c = xb[t];
+      double u = a + c, v = a - c;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        P[i] = fma(SP[i][t], u, P[i]);
+        Q[i] = fma(SQ[i][t], v, Q[i]);
+      }
+    }
+  } else {
+    for (int t = 0; t < half; ++t) {
+      double a = ldT(T, ldt, r0 + t, p.H, col), c = ldT(T, ldt, r0 + len - 1 - t, p.H, col);
+      double u = a + c, v = a - c;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        P[i] = fma(SP[i][t], u, P[i]);
+        Q[i] = fma(SQ[i][t], v, Q[i]);
+      }
     }
   }
 #pragma unroll
@@ -91,75 +109,112 @@ __global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__re
 }
 
 // ---------------------------------------------------------------------------
-// 2. band scan per column: Z -> true histories at band edges (in place)
-//    fwd slot b: y+(r0-1 .. r0-K); bwd slot b: y-(r1 .. r1+K-1)
+// 2. band scan: one warp per (column, direction), lanes over bands
+//    E_s = d_s + TyB E_{s-1} in scan order (backward = bands bottom-up);
+//    Kogge-Stone with TyB^(cpl 2^l); writes the START history of every band
+//    in place: fwd slot b = y+(r0-1 .. r0-K), bwd slot b = y-(r1 .. r1+K-1).
 // ---------------------------------------------------------------------------
 template <int K>
 __global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ T, int64_t ldt,
                                                       ColParams p, double *__restrict__ Z) {
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= p.W) return;
-  double E[K], X[K], Zv[K];
-  const double x0 = ldT(T, ldt, 0, p.H, col);
+  const int lane = threadIdx.x & 31;
+  const int64_t task = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (task >= 2 * p.W) return;
+  const int64_t col = task >> 1;
+  const int dir = (int)(task & 1);
+  const int NB = p.NB, cpl = p.cpl;
+  const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, col);
+  auto band_of = [&](int sp) { return dir == 0 ? sp : NB - 1 - sp; };
+  // d for scan position sp
+  auto dval = [&](int sp, double *d) {
+    const int b = band_of(sp);
+    double X[K];
+    const int tb = (sp == 0 && (dir == 1 ? NB - 1 : 0) == NB - 1) ? 1 : 0;
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    E[i] = p.yss * x0;
-    X[i] = x0;
-  }
-  for (int b = 0; b < p.NB; ++b) {
-    double *slot = Z + (int64_t)(b * 2 + 0) * K * p.W + col;
+    for (int i = 0; i < K; ++i) {
+      if (sp == 0)
+        X[i] = xe;
+      else if (dir == 0)
+        X[i] = ldT(T, ldt, (int64_t)b * kBand - 1 - i, p.H, col);
+      else
+        X[i] = ldT(T, ldt, (int64_t)(b + 1) * kBand + i, p.H, col);
+    }
 #pragma unroll
-    for (int i = 0; i < K; ++i) Zv[i] = slot[i * p.W];
+    for (int i = 0; i < K; ++i) {
+      double acc = Z[((int64_t)(b * 2 + dir) * K + i) * p.W + col];
 #pragma unroll
-    for (int i = 0; i < K; ++i) slot[i * p.W] = E[i];
-    if (b < p.NB - 1) {
-      const int64_t r1 = (int64_t)(b + 1) * kBand;
-      double En[K];
+      for (int q = 0; q < K; ++q) acc = fma(p.TxB[tb][i * K + q], X[q], acc);
+      if (sp == 0) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc = fma(p.TyB[tb][i * K + q], p.yss * xe, acc);
+      }
+      d[i] = acc;
+    }
+  };
+  double dl[kMaxCpl][K];
+  double A[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) A[i] = 0.0;
+#pragma unroll
+  for (int q = 0; q < kMaxCpl; ++q) {
+    const int sp = lane * cpl + q;
+    if (q < cpl && sp < NB) {
+      dval(sp, dl[q]);
+      double An[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        double acc = Zv[i];
+        double acc = dl[q][i];
 #pragma unroll
-        for (int j = 0; j < K; ++j) acc = fma(p.TxB[0][i * K + j], X[j], acc);
-#pragma unroll
-        for (int j = 0; j < K; ++j) acc = fma(p.TyB[0][i * K + j], E[j], acc);
-        En[i] = acc;
+        for (int m = 0; m < K; ++m) acc = fma(p.TyB[0][i * K + m], A[m], acc);
+        An[i] = acc;
       }
 #pragma unroll
+      for (int i = 0; i < K; ++i) A[i] = An[i];
+    }
+  }
+#pragma unroll
+  for (int lv = 0; lv < 5; ++lv) {
+    const int o = 1 << lv;
+    double B[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) B[i] = __shfl_up_sync(0xffffffffu, A[i], o);
+    if (lane >= o) {
+#pragma unroll
       for (int i = 0; i < K; ++i) {
-        E[i] = En[i];
-        X[i] = ldT(T, ldt, r1 - 1 - i, p.H, col);
+        double acc = A[i];
+#pragma unroll
+        for (int m = 0; m < K; ++m) acc = fma(p.TyBp[lv][i * K + m], B[m], acc);
+        A[i] = acc;
       }
     }
   }
-  const double xl = ldT(T, ldt, p.H - 1, p.H, col);
+  double E[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    E[i] = p.yss * xl;
-    X[i] = xl;
+    double v = __shfl_up_sync(0xffffffffu, A[i], 1);
+    E[i] = lane ? v : p.yss * xe;
   }
-  for (int b = p.NB - 1; b >= 0; --b) {
-    double *slot = Z + (int64_t)(b * 2 + 1) * K * p.W + col;
 #pragma unroll
-    for (int i = 0; i < K; ++i) Zv[i] = slot[i * p.W];
+  for (int q = 0; q < kMaxCpl; ++q) {
+    const int sp = lane * cpl + q;
+    if (q < cpl && sp < NB) {
+      const int b = band_of(sp);
 #pragma unroll
-    for (int i = 0; i < K; ++i) slot[i * p.W] = E[i];
-    if (b > 0) {
-      const int tb = b == p.NB - 1 ? 1 : 0;
-      const int64_t r0 = (int64_t)b * kBand;
-      double En[K];
+      for (int i = 0; i < K; ++i) Z[((int64_t)(b * 2 + dir) * K + i) * p.W + col] = E[i];
+      if (sp == 0) {  // the first band's own end history, from the steady state
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        double acc = Zv[i];
+        for (int i = 0; i < K; ++i) E[i] = dl[q][i];
+      } else {
+        double En[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) acc = fma(p.TxB[tb][i * K + j], X[j], acc);
+        for (int i = 0; i < K; ++i) {
+          double acc = dl[q][i];
 #pragma unroll
-        for (int j = 0; j < K; ++j) acc = fma(p.TyB[tb][i * K + j], E[j], acc);
-        En[i] = acc;
-      }
+          for (int m = 0; m < K; ++m) acc = fma(p.TyB[0][i * K + m], E[m], acc);
+          En[i] = acc;
+        }
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        E[i] = En[i];
-        X[i] = ldT(T, ldt, r0 + i, p.H, col);
+        for (int i = 0; i < K; ++i) E[i] = En[i];
       }
     }
   }
@@ -189,18 +244,20 @@ __device__ __forceinline__ void push2(double *Y, double y, double *X, double x) 
   X[0] = x;
 }
 
+constexpr int kTileRows(int k) { return kBand + 2 * k; }
+constexpr int kRing = kSub + 2;  // L rows [rb-1, rb+33)
+
 template <int K>
 struct ColSmem {
-  double xs[kSub + K][kColThreads];   // x of the sub-chunk (+K rows below), then B in place
-  double bprev[2][kColThreads];       // B of the 2 rows above the sub-chunk
-  double fbs[kBand / kSub][K][kColThreads];  // backward start history per sub-chunk
-  float lcur[kSub + 2][kColThreads];  // L rows [rbase-1, rbase+33)
-  float lprev[2][kColThreads];        // L rows rbase-3, rbase-2
+  float tile[kTileRows(K)][kColThreads];  // T rows r0-K .. r1+K-1 (clamped)
+  float lring[kRing][kColThreads];        // L rows [rb-1, rb-1+34) of the sub-chunk
+  float lprev[2][kColThreads];            // L rows rb-3, rb-2
+  double eb[kColThreads / 32][4][kRing];  // B of lanes 0,1,30,31 per warp, rows rb-1..
   int cy[kCandSmem], cx[kCandSmem];
   float cv[kCandSmem];
   int ccount;
   int coverflow;
-  unsigned int cmax;                  // running max |L| of this CTA (float bits)
+  unsigned int cmax;  // running max |L| of this CTA (float bits)
 };
 
 template <int K>
@@ -210,7 +267,7 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
     int *__restrict__ gx, float *__restrict__ gv, int gcap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ColSmem<K> &S = *reinterpret_cast<ColSmem<K> *>(smem_raw);
-  const int j = threadIdx.x;
+  const int j = threadIdx.x, lane = j & 31, wid = j >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * kColOut;
   const int64_t col = c0 - kColHalo + j;
   const int64_t colc = col < 0 ? 0 : (col >= p.W ? p.W - 1 : col);
@@ -221,161 +278,196 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
   const int nsub = len / kSub;
   const int64_t H = p.H;
   const bool own_col = j >= kColHalo && j < kColThreads - kColHalo && col < p.W;
+  const bool edge = lane == 0 || lane == 31;
+  const int eslot = lane == 0 ? 0 : (lane == 1 ? 1 : (lane == 30 ? 2 : (lane == 31 ? 3 : -1)));
+
+  // ---- stage the band's column tile (async, 4-byte copies: any alignment) --
+  {
+    const int rows = len + 2 * K;
+    for (int tr = 0; tr < rows; ++tr) {
+      int64_t r = r0 - K + tr;
+      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+      unsigned sa = (unsigned)__cvta_generic_to_shared(&S.tile[tr][j]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + colc));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
   if (j == 0) {
     S.ccount = 0;
     S.coverflow = 0;
     S.cmax = st->absmax_bits;  // global running max so far: a valid lower bound
   }
-
-  // ---- fine backward carries of the sub-chunks + reverse scan -------------
-  double Ybot[K], E[K], X[K];
+  double Ybot[K], Yf[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     Ybot[i] = Z[((int64_t)(b * 2 + 1) * K + i) * p.W + colc];
-    E[i] = Ybot[i];
-    X[i] = ldT(T, ldt, r1 + i, H, colc);
+    Yf[i] = Z[((int64_t)(b * 2 + 0) * K + i) * p.W + colc];
   }
-  for (int s = nsub - 1; s >= 0; --s) {
-    const int64_t rb = r0 + (int64_t)s * kSub;
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  auto X_at = [&](int64_t r) -> double { return (double)S.tile[r - (r0 - K)][j]; };
+
+  // ---- backward start of sub-chunk 0 when the band has two ---------------
+  double E0[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) E0[i] = Ybot[i];
+  if (nsub == 2) {
     double zb[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) zb[i] = 0.0;
-#pragma unroll 8
+#pragma unroll
     for (int t = 0; t < kSub; ++t) {
-      double v = ldT(T, ldt, rb + t, H, colc);
+      double v = X_at(r0 + kSub + t);
 #pragma unroll
       for (int i = 0; i < K; ++i)
         if (t - i > 0) zb[i] = fma(p.h[t - i], v, zb[i]);
     }
-    double En[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      S.fbs[s][i][j] = E[i];
       double acc = zb[i];
 #pragma unroll
-      for (int q = 0; q < K; ++q) acc = fma(p.Tx[i * K + q], X[q], acc);
+      for (int q = 0; q < K; ++q) acc = fma(p.Tx[i * K + q], X_at(r1 + q), acc);
 #pragma unroll
-      for (int q = 0; q < K; ++q) acc = fma(p.Ty[i * K + q], E[q], acc);
-      En[i] = acc;
-    }
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      E[i] = En[i];
-      X[i] = ldT(T, ldt, rb + i, H, colc);
+      for (int q = 0; q < K; ++q) acc = fma(p.Ty[i * K + q], Ybot[q], acc);
+      E0[i] = acc;
     }
   }
 
-  // ---- walk -------------------------------------------------------------------
-  double Yf[K], Xf[K], Ytop[2];
+  double Xf[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    Yf[i] = Z[((int64_t)(b * 2 + 0) * K + i) * p.W + colc];
-    int64_t q = r0 - 1 - i;
-    Xf[i] = ldT(T, ldt, q < 0 ? 0 : q, H, colc);
-  }
-  Ytop[0] = Yf[0];
-  Ytop[1] = Yf[1];
+  for (int i = 0; i < K; ++i) Xf[i] = X_at(r0 - 1 - i >= 0 ? r0 - 1 - i : 0);
   const double lsc = (double)p.lap_scale;
+  // sliding state carried across sub-chunks
+  double Bm2 = 0.0, Bm1 = 0.0, Lxm1 = 0.0;
 
   for (int s = 0; s < nsub; ++s) {
-    const int64_t rbase = r0 + (int64_t)s * kSub;
+    const int64_t rb = r0 + (int64_t)s * kSub;
     const bool last = s == nsub - 1;
-    __syncthreads();  // previous sub-chunk's smem reads are done
-#pragma unroll 4
-    for (int t = 0; t < kSub + K; ++t) S.xs[t][j] = ldT(T, ldt, rbase + t, H, colc);
-
     // backward run, parked in registers
     double park[kSub];
-    double Yb[K], Xb[K];
+    {
+      double Yb[K], Xb[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      Yb[i] = S.fbs[s][i][j];
-      Xb[i] = S.xs[kSub + i][j];
-    }
+      for (int i = 0; i < K; ++i) {
+        Yb[i] = last ? Ybot[i] : E0[i];
+        Xb[i] = X_at(rb + kSub + i);
+      }
 #pragma unroll
-    for (int t = kSub - 1; t >= 0; --t) {
-      double xv = S.xs[t][j];
-      double y = dfi<K>(p, Xb, Yb);
-      park[t] = p.sign * y;
-      push2<K>(Yb, y, Xb, xv);
-    }
-    if (s == 0) {
-      if (r0 > 0) {  // B at rows r0-1, r0-2 from the band-edge histories
-        double x1 = ldT(T, ldt, r0 - 1, H, colc);
-        double x2 = ldT(T, ldt, r0 >= 2 ? r0 - 2 : 0, H, colc);
-        double ym1 = dfi<K>(p, Xb, Yb);
-        push2<K>(Yb, ym1, Xb, x1);
-        double ym2 = dfi<K>(p, Xb, Yb);
-        S.bprev[1][j] = fma(p.b0, x1, Ytop[0]) + p.sign * ym1;
-        S.bprev[0][j] = fma(p.b0, x2, Ytop[1]) + p.sign * ym2;
+      for (int t = kSub - 1; t >= 0; --t) {
+        double xv = X_at(rb + t);
+        double y = dfi<K>(p, Xb, Yb);
+        park[t] = p.sign * y;
+        push2<K>(Yb, y, Xb, xv);
+      }
+      if (s == 0) {
+        if (r0 > 0) {  // B at rows r0-2, r0-1 from the band-edge histories
+          double x1 = X_at(r0 - 1), x2 = X_at(r0 - 2);
+          double ym1 = dfi<K>(p, Xb, Yb);
+          push2<K>(Yb, ym1, Xb, x1);
+          double ym2 = dfi<K>(p, Xb, Yb);
+          Bm1 = fma(p.b0, x1, Yf[0]) + p.sign * ym1;
+          Bm2 = fma(p.b0, x2, Yf[1]) + p.sign * ym2;
+        }
       }
     }
-    // forward run: B(rbase + t) replaces x in place
+    // Lx of row r via lane shuffles (warp-edge lanes patched below)
+    auto lx_of = [&](double bc) {
+      double bl = __shfl_up_sync(0xffffffffu, bc, 1);
+      double br = __shfl_down_sync(0xffffffffu, bc, 1);
+      return (bl - 2.0 * bc) + br;
+    };
+    if (s == 0 && r0 > 0) Lxm1 = lx_of(Bm1);
+    if (eslot >= 0) S.eb[wid][eslot][0] = Bm1;  // row rb-1
+    // forward run: B(rb+t); L(rb+t-1) = Lx + Ly as soon as B(rb+t) exists
 #pragma unroll
     for (int t = 0; t < kSub; ++t) {
-      double xv = S.xs[t][j];
+      const int64_t r = rb + t;
+      double xv = X_at(r);
       double y = dfi<K>(p, Xf, Yf);
-      S.xs[t][j] = fma(p.b0, xv, y) + park[t];
+      double Bt = fma(p.b0, xv, y) + park[t];
       push2<K>(Yf, y, Xf, xv);
+      if (r == 0) Bm1 = Bt;  // replicate top edge: B(-1) = B(0)
+      const double lx = lx_of(Bt);
+      // row r-1
+      {
+        const double bnext = (r >= H) ? Bm1 : Bt;  // replicate bottom edge
+        const double ly = (Bm2 - 2.0 * Bm1) + bnext;
+        S.lring[t][j] = (float)(lsc * ((edge ? 0.0 : Lxm1) + ly));
+      }
+      if (eslot >= 0) S.eb[wid][eslot][t + 1] = Bt;
+      Bm2 = Bm1;
+      Bm1 = Bt;
+      Lxm1 = lx;
     }
-    if (s == 0 && r0 == 0) {  // replicate edge: B(-1) = B(0)
-      S.bprev[1][j] = S.xs[0][j];
-      S.bprev[0][j] = S.xs[0][j];
-    }
-    if (last) {  // B at rows r1, r1+1 (next band) for L(r1-1), L(r1)
-      double xr1 = S.xs[kSub][j], xr2 = S.xs[kSub + 1][j];
+    int nl = kSub;  // L rows written to the ring this sub-chunk
+    if (last) {  // B at rows r1, r1+1: L(r1-1), L(r1)
+      double xr1 = X_at(r1), xr2 = X_at(r1 + 1);
+      double y0 = dfi<K>(p, Xf, Yf);
       double Y2[K], X2[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         Y2[i] = Yf[i];
         X2[i] = Xf[i];
       }
-      double y0 = dfi<K>(p, X2, Y2);
       push2<K>(Y2, y0, X2, xr1);
       double y1 = dfi<K>(p, X2, Y2);
-      S.xs[kSub][j] = fma(p.b0, xr1, y0) + p.sign * Ybot[0];
-      S.xs[kSub + 1][j] = fma(p.b0, xr2, y1) + p.sign * Ybot[1];
+      double B1 = fma(p.b0, xr1, y0) + p.sign * Ybot[0];
+      double B2 = fma(p.b0, xr2, y1) + p.sign * Ybot[1];
+      const double lx1 = lx_of(B1);
+      {  // row r1-1
+        const double bnext = (r1 >= H) ? Bm1 : B1;
+        S.lring[kSub][j] = (float)(lsc * ((edge ? 0.0 : Lxm1) + (Bm2 - 2.0 * Bm1) + bnext));
+      }
+      {  // row r1
+        const double bnext = (r1 + 1 >= H) ? B1 : B2;
+        S.lring[kSub + 1][j] = (float)(lsc * ((edge ? 0.0 : lx1) + (Bm1 - 2.0 * B1) + bnext));
+      }
+      if (eslot >= 0) {
+        S.eb[wid][eslot][kSub + 1] = B1;
+      }
+      nl = kSub + 2;
     }
     __syncthreads();
-
-    // Laplacian rows [rbase-1, rbase+31) (+2 at the band end)
-    const int nl = last ? kSub + 2 : kSub;
-    const int jl = j > 0 ? j - 1 : 0, jr = j < kColThreads - 1 ? j + 1 : kColThreads - 1;
+    // patch Lx of warp-edge lanes from the exchanged edge columns
+    if (edge && j > 0 && j < kColThreads - 1) {
+      for (int q = 0; q < nl; ++q) {
+        const int64_t r = rb - 1 + q;
+        if (r < 0 || r >= H) continue;
+        double bl, bc, br;
+        if (lane == 0) {
+          bl = S.eb[wid - 1][3][q];
+          bc = S.eb[wid][0][q];
+          br = S.eb[wid][1][q];
+        } else {
+          bl = S.eb[wid][2][q];
+          bc = S.eb[wid][3][q];
+          br = S.eb[wid + 1][0][q];
+        }
+        S.lring[q][j] += (float)(lsc * ((bl - 2.0 * bc) + br));
+      }
+    }
+    __syncthreads();
+    // L out (owned rows / columns) + running max
     float lmax = 0.0f;
     for (int q = 0; q < nl; ++q) {
-      const int64_t r = rbase - 1 + q;
-      float lv = 0.0f;
-      if (r >= 0 && r < H && j > 0 && j < kColThreads - 1) {
-        auto Bat = [&](int64_t rr, int jj) -> double {
-          if (rr >= H) rr = H - 1;  // replicate bottom edge
-          int64_t d = rr - rbase;
-          if (d >= 0) return S.xs[d][jj];
-          return S.bprev[d + 2][jj];
-        };
-        double bc = Bat(r, j);
-        double dx = Bat(r, jl) - 2.0 * bc + Bat(r, jr);
-        double dy = Bat(r - 1, j) - 2.0 * bc + Bat(r + 1, j);
-        lv = (float)(lsc * (dx + dy));
-        if (r >= r0 && r < r1 && own_col) {
-          Lout[r * ldl + col] = lv;
-          lmax = fmaxf(lmax, fabsf(lv));
-        }
+      const int64_t r = rb - 1 + q;
+      if (r >= r0 && r < r1 && r < H && own_col) {
+        float v = S.lring[q][j];
+        Lout[r * ldl + col] = v;
+        lmax = fmaxf(lmax, fabsf(v));
       }
-      S.lcur[q][j] = lv;
     }
     atomicMax(&S.cmax, __float_as_uint(lmax));
     __syncthreads();
-
-    // NMS rows [rbase-2, rbase+30) (+2 at the band end), owned rows only
+    // NMS rows [rb-2, rb+30) (+2 at the band end), owned rows only
     const float thr = p.frac * __uint_as_float(S.cmax);
-    const int nn = last ? kSub + 2 : kSub;
     if (own_col && col >= 1 && col <= p.W - 2) {
-      for (int q = 0; q < nn; ++q) {
-        const int64_t r = rbase - 2 + q;
+      for (int q = 0; q < nl; ++q) {
+        const int64_t r = rb - 2 + q;
         if (r < r0 || r < 1 || r > H - 2) continue;
         auto Lat = [&](int64_t rr, int jj) -> float {
-          int64_t d = rr - (rbase - 1);
-          if (d >= 0) return S.lcur[d][jj];
+          int64_t d = rr - (rb - 1);
+          if (d >= 0) return S.lring[d][jj];
           return S.lprev[d + 2][jj];
         };
         float v = Lat(r, j);
@@ -403,12 +495,9 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
       }
     }
     __syncthreads();
-    // carry 2 rows of B and L into the next sub-chunk; compact candidates
     if (!last) {
-      S.bprev[0][j] = S.xs[kSub - 2][j];
-      S.bprev[1][j] = S.xs[kSub - 1][j];
-      S.lprev[0][j] = S.lcur[kSub - 2][j];
-      S.lprev[1][j] = S.lcur[kSub - 1][j];
+      S.lprev[0][j] = S.lring[kSub - 2][j];
+      S.lprev[1][j] = S.lring[kSub - 1][j];
     }
     if (j == 0 && S.ccount > kCandSmem / 2) {
       const float t2 = p.frac * __uint_as_float(S.cmax);
@@ -422,8 +511,8 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
         }
       S.ccount = m;
     }
+    __syncthreads();
   }
-  __syncthreads();
 
   // ---- flush candidates that survive the best threshold known now ---------
   __shared__ float thr_end;
@@ -564,7 +653,8 @@ static void impulse_ld(const double *b, const double *a, int k, int n, double *h
 }
 
 bool colpass_supported(int64_t h, int64_t w, int k) {
-  return k >= 2 && k <= 4 && h >= 2 * kSub && w >= 1;
+  return k >= 2 && k <= 4 && h >= 2 * kSub && w >= 1 &&
+         cdiv(cdiv(h, kSub) * kSub, kBand) <= 32 * kMaxCpl;
 }
 
 static void col_geometry(int64_t h, int64_t *Hp, int *NB, int *Blast) {
@@ -615,7 +705,7 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   }
   {
     Launch g(K_COL_SCAN, st);
-    colscan_kernel<K><<<(unsigned)cdiv(p.W, 128), 128, 0, st>>>(T, ldt, p, Z);
+    colscan_kernel<K><<<(unsigned)cdiv(2 * p.W, 4), 128, 0, st>>>(T, ldt, p, Z);
   }
   {
     Launch g(K_IIR_COLS_FUSED, st);
@@ -671,6 +761,12 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirPar
   col_geometry(h, &p.Hp, &p.NB, &p.Blast);
   transfer_ld(ip.b, ip.a, k, kBand, p.TyB[0], p.TxB[0]);
   transfer_ld(ip.b, ip.a, k, p.Blast, p.TyB[1], p.TxB[1]);
+  p.cpl = (p.NB + 31) / 32;
+  if (p.cpl > kMaxCpl) return fail(VMF_EVALUE, "image too tall for the fused column pass");
+  for (int l = 0; l < 5; ++l) {
+    double tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
+    transfer_ld(ip.b, ip.a, k, (p.cpl << l) * kBand, p.TyBp[l], tx);
+  }
   p.lap_scale = lap_scale;
   p.frac = frac;
   switch (k) {

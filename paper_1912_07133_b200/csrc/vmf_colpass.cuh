@@ -6,7 +6,8 @@
 namespace vmf {
 
 constexpr int kSub = 32;            // rows per sub-chunk (one recursion run)
-constexpr int kBand = 256;          // rows per band (carry granularity)
+constexpr int kBand = 64;           // rows per band (carry granularity)
+constexpr int kMaxCpl = 4;          // bands per lane in the band scan (H <= 8192)
 constexpr int kColThreads = 128;    // computed columns per CTA
 constexpr int kColHalo = 2;         // halo columns each side (Laplacian + NMS)
 constexpr int kColOut = kColThreads - 2 * kColHalo;  // 124 output columns per CTA
@@ -21,8 +22,9 @@ struct ColParams {
   double Tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
   double TyB[2][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // over a band / the last band
   double TxB[2][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
+  double TyBp[5][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // TyB^(cpl 2^l)
   int64_t H, W, Hp;       // Hp = H rounded up to 32 (rows >= H replicate row H-1)
-  int NB, Blast;          // bands; rows in the last band (multiple of 32)
+  int NB, Blast, cpl;     // bands; rows in the last band (multiple of 32); bands/lane
   float lap_scale, frac;
 };
 
