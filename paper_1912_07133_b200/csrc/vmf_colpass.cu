@@ -245,19 +245,21 @@ __device__ __forceinline__ void push2(double *Y, double y, double *X, double x) 
 }
 
 constexpr int kTileRows(int k) { return kBand + 2 * k; }
-constexpr int kRing = kSub + 2;  // L rows [rb-1, rb+33)
+constexpr int kEbRows = kBand + 2;  // B of rows r0-1 .. r1
 
 template <int K>
 struct ColSmem {
-  float tile[kTileRows(K)][kColThreads];  // T rows r0-K .. r1+K-1 (clamped)
-  float lring[kRing][kColThreads];        // L rows [rb-1, rb-1+34) of the sub-chunk
-  float lprev[2][kColThreads];            // L rows rb-3, rb-2
-  double eb[kColThreads / 32][4][kRing];  // B of lanes 0,1,30,31 per warp, rows rb-1..
+  // T rows r0-K .. r1+K-1 (clamped).  Column j is private to thread j during
+  // the walk, so L(r) overwrites x(r) in place once x(r) is consumed; after
+  // the walk the tile holds L rows r0-1 .. r1 for the NMS.
+  float tile[kTileRows(K)][kColThreads];
+  double eb[kColThreads / 32][4][kEbRows];  // B of lanes 0,1,30,31 per warp
   int cy[kCandSmem], cx[kCandSmem];
   float cv[kCandSmem];
+  unsigned int eflag[kColThreads / 32][2][kBand / kSub + 1];  // edge-column row flags
   int ccount;
   int coverflow;
-  unsigned int cmax;  // running max |L| of this CTA (float bits)
+  unsigned int cmax;  // max |L| of this CTA (float bits)
 };
 
 template <int K>
@@ -278,25 +280,38 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
   const int nsub = len / kSub;
   const int64_t H = p.H;
   const bool own_col = j >= kColHalo && j < kColThreads - kColHalo && col < p.W;
-  const bool edge = lane == 0 || lane == 31;
+  const bool edge = lane == 0 || lane == 31;  // warp-edge lanes: Lx patched after the walk
   const int eslot = lane == 0 ? 0 : (lane == 1 ? 1 : (lane == 30 ? 2 : (lane == 31 ? 3 : -1)));
+  const int64_t rown_hi = r1 < H ? r1 : H;  // owned rows [r0, rown_hi)
 
-  // ---- stage the band's column tile (async, 4-byte copies: any alignment) --
+  // ---- stage the band's column tile (async 4-byte copies: any alignment) ---
+  float *tcol = &S.tile[0][j];  // tile row tr of this thread's column: tcol[tr * kColThreads]
   {
     const int rows = len + 2 * K;
-    for (int tr = 0; tr < rows; ++tr) {
-      int64_t r = r0 - K + tr;
-      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
-      unsigned sa = (unsigned)__cvta_generic_to_shared(&S.tile[tr][j]);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + colc));
+    const float *src = T + colc;
+    if (r0 >= K && r1 + K <= H) {  // no clamping needed
+      const float *s0 = src + (r0 - K) * ldt;
+      for (int tr = 0; tr < rows; ++tr) {
+        unsigned sa = (unsigned)__cvta_generic_to_shared(tcol + tr * kColThreads);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(s0 + tr * ldt));
+      }
+    } else {
+      for (int tr = 0; tr < rows; ++tr) {
+        int64_t r = r0 - K + tr;
+        r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+        unsigned sa = (unsigned)__cvta_generic_to_shared(tcol + tr * kColThreads);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + r * ldt));
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::);
   }
   if (j == 0) {
     S.ccount = 0;
     S.coverflow = 0;
-    S.cmax = st->absmax_bits;  // global running max so far: a valid lower bound
+    S.cmax = 0u;
   }
+  if (j < (kColThreads / 32) * 2 * (kBand / kSub + 1)) (&S.eflag[0][0][0])[j] = 0u;
+  const float gbound = __uint_as_float(st->absmax_bits);  // global max so far (lower bound)
   double Ybot[K], Yf[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) {
@@ -305,7 +320,8 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
-  auto X_at = [&](int64_t r) -> double { return (double)S.tile[r - (r0 - K)][j]; };
+  // tile row of image row r is r - r0 + K
+#define TX(tr) ((double)tcol[(tr) * kColThreads])
 
   // ---- backward start of sub-chunk 0 when the band has two ---------------
   double E0[K];
@@ -317,7 +333,7 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
     for (int i = 0; i < K; ++i) zb[i] = 0.0;
 #pragma unroll
     for (int t = 0; t < kSub; ++t) {
-      double v = X_at(r0 + kSub + t);
+      double v = TX(K + kSub + t);
 #pragma unroll
       for (int i = 0; i < K; ++i)
         if (t - i > 0) zb[i] = fma(p.h[t - i], v, zb[i]);
@@ -326,7 +342,7 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
     for (int i = 0; i < K; ++i) {
       double acc = zb[i];
 #pragma unroll
-      for (int q = 0; q < K; ++q) acc = fma(p.Tx[i * K + q], X_at(r1 + q), acc);
+      for (int q = 0; q < K; ++q) acc = fma(p.Tx[i * K + q], TX(K + kBand + q), acc);
 #pragma unroll
       for (int q = 0; q < K; ++q) acc = fma(p.Ty[i * K + q], Ybot[q], acc);
       E0[i] = acc;
@@ -335,184 +351,212 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
 
   double Xf[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) Xf[i] = X_at(r0 - 1 - i >= 0 ? r0 - 1 - i : 0);
+  for (int i = 0; i < K; ++i) Xf[i] = TX(K - 1 - i);  // rows r0-1-i (clamped at the top)
   const double lsc = (double)p.lap_scale;
-  // sliding state carried across sub-chunks
-  double Bm2 = 0.0, Bm1 = 0.0, Lxm1 = 0.0;
+  double Bm2 = 0.0, Bm1 = 0.0, Lxm1 = 0.0;  // sliding state (rows r-2, r-1)
+  float tmax = 0.0f;                          // this thread's running max |L|
+  unsigned int masks[kBand / kSub + 1] = {0u, 0u, 0u};  // owned rows over the threshold
+  const bool own_w = own_col && !edge;                  // writes L from the walk
+  auto lx_of = [&](double bc) {  // Lx by lane shuffles; warp-edge lanes patched later
+    double bl = __shfl_up_sync(0xffffffffu, bc, 1);
+    double br = __shfl_down_sync(0xffffffffu, bc, 1);
+    return (bl - 2.0 * bc) + br;
+  };
 
   for (int s = 0; s < nsub; ++s) {
     const int64_t rb = r0 + (int64_t)s * kSub;
+    const int trb = K + s * kSub;  // tile row of rb
     const bool last = s == nsub - 1;
-    // backward run, parked in registers
     double park[kSub];
     {
       double Yb[K], Xb[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         Yb[i] = last ? Ybot[i] : E0[i];
-        Xb[i] = X_at(rb + kSub + i);
+        Xb[i] = TX(trb + kSub + i);
       }
 #pragma unroll
       for (int t = kSub - 1; t >= 0; --t) {
-        double xv = X_at(rb + t);
+        double xv = TX(trb + t);
         double y = dfi<K>(p, Xb, Yb);
-        park[t] = p.sign * y;
+        park[t] = y;
         push2<K>(Yb, y, Xb, xv);
       }
-      if (s == 0) {
-        if (r0 > 0) {  // B at rows r0-2, r0-1 from the band-edge histories
-          double x1 = X_at(r0 - 1), x2 = X_at(r0 - 2);
-          double ym1 = dfi<K>(p, Xb, Yb);
-          push2<K>(Yb, ym1, Xb, x1);
-          double ym2 = dfi<K>(p, Xb, Yb);
-          Bm1 = fma(p.b0, x1, Yf[0]) + p.sign * ym1;
-          Bm2 = fma(p.b0, x2, Yf[1]) + p.sign * ym2;
-        }
+      if (s == 0 && r0 > 0) {  // B at rows r0-2, r0-1 from the band-edge histories
+        double x1 = TX(K - 1), x2 = TX(K - 2);
+        double ym1 = dfi<K>(p, Xb, Yb);
+        push2<K>(Yb, ym1, Xb, x1);
+        double ym2 = dfi<K>(p, Xb, Yb);
+        Bm1 = fma(p.sign, ym1, fma(p.b0, x1, Yf[0]));
+        Bm2 = fma(p.sign, ym2, fma(p.b0, x2, Yf[1]));
+        Lxm1 = lx_of(Bm1);
+        if (eslot >= 0) S.eb[wid][eslot][0] = Bm1;
       }
     }
-    // Lx of row r via lane shuffles (warp-edge lanes patched below)
-    auto lx_of = [&](double bc) {
-      double bl = __shfl_up_sync(0xffffffffu, bc, 1);
-      double br = __shfl_down_sync(0xffffffffu, bc, 1);
-      return (bl - 2.0 * bc) + br;
-    };
-    if (s == 0 && r0 > 0) Lxm1 = lx_of(Bm1);
-    if (eslot >= 0) S.eb[wid][eslot][0] = Bm1;  // row rb-1
+    const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+    const float th = p.frac * fmaxf(wmax, gbound);  // lower bound of the final threshold
+    unsigned int m = 0u;                             // bit t: owned row rb+t-1 flagged
+    float *lo = Lout + (rb - 1) * ldl + col;         // L row rb-1 of this column
     // forward run: B(rb+t); L(rb+t-1) = Lx + Ly as soon as B(rb+t) exists
+    if (rb >= 1 && rb + kSub < H && s > 0) {
+      // interior sub-chunk: every L row written here is owned and in range
 #pragma unroll
-    for (int t = 0; t < kSub; ++t) {
-      const int64_t r = rb + t;
-      double xv = X_at(r);
-      double y = dfi<K>(p, Xf, Yf);
-      double Bt = fma(p.b0, xv, y) + park[t];
-      push2<K>(Yf, y, Xf, xv);
-      if (r == 0) Bm1 = Bt;  // replicate top edge: B(-1) = B(0)
-      const double lx = lx_of(Bt);
-      // row r-1
-      {
-        const double bnext = (r >= H) ? Bm1 : Bt;  // replicate bottom edge
-        const double ly = (Bm2 - 2.0 * Bm1) + bnext;
-        S.lring[t][j] = (float)(lsc * ((edge ? 0.0 : Lxm1) + ly));
+      for (int t = 0; t < kSub; ++t) {
+        double xv = TX(trb + t);
+        double y = dfi<K>(p, Xf, Yf);
+        double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
+        push2<K>(Yf, y, Xf, xv);
+        const double lx = lx_of(Bt);
+        const float v = (float)(lsc * ((edge ? 0.0 : Lxm1) + ((Bm2 - 2.0 * Bm1) + Bt)));
+        tcol[(trb + t - 1) * kColThreads] = v;
+        if (own_w) {
+          lo[t * ldl] = v;
+          const float av = fabsf(v);
+          tmax = fmaxf(tmax, av);
+          m |= (av >= th ? 1u : 0u) << t;
+        }
+        if (eslot >= 0) S.eb[wid][eslot][trb + t - K + 1] = Bt;
+        Bm2 = Bm1;
+        Bm1 = Bt;
+        Lxm1 = lx;
       }
-      if (eslot >= 0) S.eb[wid][eslot][t + 1] = Bt;
-      Bm2 = Bm1;
-      Bm1 = Bt;
-      Lxm1 = lx;
+    } else {
+#pragma unroll
+      for (int t = 0; t < kSub; ++t) {
+        const int64_t r = rb + t;
+        double xv = TX(trb + t);
+        double y = dfi<K>(p, Xf, Yf);
+        double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
+        push2<K>(Yf, y, Xf, xv);
+        if (r == 0) Bm1 = Bt;  // replicate top edge: B(-1) = B(0)
+        const double lx = lx_of(Bt);
+        const double bnext = r >= H ? Bm1 : Bt;  // replicate bottom edge
+        if (r >= 1) {
+          const float v = (float)(lsc * ((edge ? 0.0 : Lxm1) + ((Bm2 - 2.0 * Bm1) + bnext)));
+          tcol[(trb + t - 1) * kColThreads] = v;
+          if (own_w && r - 1 >= r0 && r - 1 < rown_hi) {
+            lo[t * ldl] = v;
+            const float av = fabsf(v);
+            tmax = fmaxf(tmax, av);
+            m |= (av >= th ? 1u : 0u) << t;
+          }
+        }
+        if (eslot >= 0) S.eb[wid][eslot][trb + t - K + 1] = Bt;
+        Bm2 = Bm1;
+        Bm1 = Bt;
+        Lxm1 = lx;
+      }
     }
-    int nl = kSub;  // L rows written to the ring this sub-chunk
-    if (last) {  // B at rows r1, r1+1: L(r1-1), L(r1)
-      double xr1 = X_at(r1), xr2 = X_at(r1 + 1);
+    masks[s] |= m;  // bit t <-> band row 32 s + t - 1
+    if (last) {  // B at rows r1, r1+1 -> L(r1-1), L(r1)
+      const int tr1 = K + len;
+      double xr1 = TX(tr1), xr2 = TX(tr1 + 1);
       double y0 = dfi<K>(p, Xf, Yf);
-      double Y2[K], X2[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        Y2[i] = Yf[i];
-        X2[i] = Xf[i];
-      }
-      push2<K>(Y2, y0, X2, xr1);
-      double y1 = dfi<K>(p, X2, Y2);
-      double B1 = fma(p.b0, xr1, y0) + p.sign * Ybot[0];
-      double B2 = fma(p.b0, xr2, y1) + p.sign * Ybot[1];
+      push2<K>(Yf, y0, Xf, xr1);
+      double y1 = dfi<K>(p, Xf, Yf);
+      double B1 = fma(p.sign, Ybot[0], fma(p.b0, xr1, y0));
+      double B2 = fma(p.sign, Ybot[1], fma(p.b0, xr2, y1));
       const double lx1 = lx_of(B1);
-      {  // row r1-1
-        const double bnext = (r1 >= H) ? Bm1 : B1;
-        S.lring[kSub][j] = (float)(lsc * ((edge ? 0.0 : Lxm1) + (Bm2 - 2.0 * Bm1) + bnext));
-      }
-      {  // row r1
-        const double bnext = (r1 + 1 >= H) ? B1 : B2;
-        S.lring[kSub + 1][j] = (float)(lsc * ((edge ? 0.0 : lx1) + (Bm1 - 2.0 * B1) + bnext));
-      }
-      if (eslot >= 0) {
-        S.eb[wid][eslot][kSub + 1] = B1;
-      }
-      nl = kSub + 2;
-    }
-    __syncthreads();
-    // patch Lx of warp-edge lanes from the exchanged edge columns
-    if (edge && j > 0 && j < kColThreads - 1) {
-      for (int q = 0; q < nl; ++q) {
-        const int64_t r = rb - 1 + q;
-        if (r < 0 || r >= H) continue;
-        double bl, bc, br;
-        if (lane == 0) {
-          bl = S.eb[wid - 1][3][q];
-          bc = S.eb[wid][0][q];
-          br = S.eb[wid][1][q];
-        } else {
-          bl = S.eb[wid][2][q];
-          bc = S.eb[wid][3][q];
-          br = S.eb[wid + 1][0][q];
-        }
-        S.lring[q][j] += (float)(lsc * ((bl - 2.0 * bc) + br));
-      }
-    }
-    __syncthreads();
-    // L out (owned rows / columns) + running max
-    float lmax = 0.0f;
-    for (int q = 0; q < nl; ++q) {
-      const int64_t r = rb - 1 + q;
-      if (r >= r0 && r < r1 && r < H && own_col) {
-        float v = S.lring[q][j];
-        Lout[r * ldl + col] = v;
-        lmax = fmaxf(lmax, fabsf(v));
-      }
-    }
-    atomicMax(&S.cmax, __float_as_uint(lmax));
-    __syncthreads();
-    // NMS rows [rb-2, rb+30) (+2 at the band end), owned rows only
-    const float thr = p.frac * __uint_as_float(S.cmax);
-    if (own_col && col >= 1 && col <= p.W - 2) {
-      for (int q = 0; q < nl; ++q) {
-        const int64_t r = rb - 2 + q;
-        if (r < r0 || r < 1 || r > H - 2) continue;
-        auto Lat = [&](int64_t rr, int jj) -> float {
-          int64_t d = rr - (rb - 1);
-          if (d >= 0) return S.lring[d][jj];
-          return S.lprev[d + 2][jj];
-        };
-        float v = Lat(r, j);
-        if (!(fabsf(v) >= thr)) continue;
-        bool gt = true, lt = true;
-#pragma unroll
-        for (int di = -1; di <= 1; ++di)
-#pragma unroll
-          for (int dj = -1; dj <= 1; ++dj) {
-            if (!di && !dj) continue;
-            float u = Lat(r + di, j + dj);
-            gt &= v > u;
-            lt &= v < u;
-          }
-        if (gt || lt) {
-          int k = atomicAdd(&S.ccount, 1);
-          if (k < kCandSmem) {
-            S.cy[k] = (int)r;
-            S.cx[k] = (int)col;
-            S.cv[k] = v;
-          } else {
-            S.coverflow = 1;
-          }
+      if (r1 - 1 < H) {
+        const float v = (float)(lsc * ((edge ? 0.0 : Lxm1) +
+                                       ((Bm2 - 2.0 * Bm1) + (r1 >= H ? Bm1 : B1))));
+        tcol[(tr1 - 1) * kColThreads] = v;
+        if (own_w) {
+          Lout[(r1 - 1) * ldl + col] = v;
+          const float av = fabsf(v);
+          tmax = fmaxf(tmax, av);
+          masks[nsub] |= (av >= p.frac * fmaxf(tmax, gbound) ? 1u : 0u);  // band row len-1
         }
       }
+      if (r1 < H) {
+        const float v = (float)(lsc * ((edge ? 0.0 : lx1) +
+                                       ((Bm1 - 2.0 * B1) + (r1 + 1 >= H ? B1 : B2))));
+        tcol[tr1 * kColThreads] = v;
+      }
+      if (eslot >= 0) S.eb[wid][eslot][kEbRows - 1] = B1;
     }
-    __syncthreads();
-    if (!last) {
-      S.lprev[0][j] = S.lring[kSub - 2][j];
-      S.lprev[1][j] = S.lring[kSub - 1][j];
-    }
-    if (j == 0 && S.ccount > kCandSmem / 2) {
-      const float t2 = p.frac * __uint_as_float(S.cmax);
-      int n = S.ccount < kCandSmem ? S.ccount : kCandSmem, m = 0;
-      for (int q = 0; q < n; ++q)
-        if (fabsf(S.cv[q]) >= t2) {
-          S.cy[m] = S.cy[q];
-          S.cx[m] = S.cx[q];
-          S.cv[m] = S.cv[q];
-          ++m;
-        }
-      S.ccount = m;
-    }
-    __syncthreads();
   }
+#undef TX
+  __syncthreads();
+
+  // ---- patch Lx of the warp-edge columns (lanes 0 / 31) -------------------
+  // The 2 x (len+2) patches of a warp are spread over its 32 lanes.
+  {
+    const int64_t rlo = r0 > 0 ? r0 - 1 : 0;
+    const int64_t rhi = r1 < H ? r1 : H - 1;
+    const int nr = (int)(rhi - rlo + 1);
+    const float th = p.frac * fmaxf(tmax, gbound);
+    for (int idx = lane; idx < 2 * nr; idx += 32) {
+      const int side = idx & 1;
+      const int64_t r = rlo + (idx >> 1);
+      const int jj = wid * 32 + (side ? 31 : 0);
+      if (jj == 0 || jj == kColThreads - 1) continue;  // CTA halo columns
+      const int q = (int)(r - r0 + 1);
+      double bl, bc, br;
+      if (side == 0) {
+        bl = S.eb[wid - 1][3][q];
+        bc = S.eb[wid][0][q];
+        br = S.eb[wid][1][q];
+      } else {
+        bl = S.eb[wid][2][q];
+        bc = S.eb[wid][3][q];
+        br = S.eb[wid + 1][0][q];
+      }
+      const int tr = (int)(r - r0 + K);
+      const float v = S.tile[tr][jj] + (float)(lsc * ((bl - 2.0 * bc) + br));
+      S.tile[tr][jj] = v;
+      const int64_t cj = c0 - kColHalo + jj;
+      if (cj < p.W && r >= r0 && r < rown_hi) {
+        Lout[r * ldl + cj] = v;
+        tmax = fmaxf(tmax, fabsf(v));
+        if (fabsf(v) >= th) atomicOr(&S.eflag[wid][side][q >> 5], 1u << (q & 31));
+      }
+    }
+  }
+  atomicMax(&S.cmax, __float_as_uint(tmax));
+  __syncthreads();
+  if (lane == 0 || lane == 31) {  // edge columns: flags gathered by the patch
+    const int side = lane == 31;
+#pragma unroll
+    for (int w = 0; w <= kBand / kSub; ++w) masks[w] |= S.eflag[wid][side][w];
+  }
+
+  // ---- strict 3x3 extrema among the flagged rows ----------------------------
+  const float thr = p.frac * fmaxf(__uint_as_float(S.cmax), gbound);
+  if (own_col && col >= 1 && col <= p.W - 2) {
+    // masks[w] bit t <-> band row 32 w + t - 1
+    for (int w = 0; w <= kBand / kSub; ++w) while (masks[w]) {
+      const int q = 32 * w + __ffs((int)masks[w]) - 2;
+      masks[w] &= masks[w] - 1;
+      const int64_t r = r0 + q;
+      if (q < 0) continue;
+      if (r < 1 || r > H - 2) continue;
+      const int tr = (int)(r - (r0 - K));
+      const float v = S.tile[tr][j];
+      if (!(fabsf(v) >= thr)) continue;
+      bool gt = true, lt = true;
+#pragma unroll
+      for (int di = -1; di <= 1; ++di)
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj) {
+          if (!di && !dj) continue;
+          const float u = S.tile[tr + di][j + dj];
+          gt &= v > u;
+          lt &= v < u;
+        }
+      if (gt || lt) {
+        int k = atomicAdd(&S.ccount, 1);
+        if (k < kCandSmem) {
+          S.cy[k] = (int)r;
+          S.cx[k] = (int)col;
+          S.cv[k] = v;
+        } else {
+          S.coverflow = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
 
   // ---- flush candidates that survive the best threshold known now ---------
   __shared__ float thr_end;
