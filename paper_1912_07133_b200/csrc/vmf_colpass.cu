@@ -30,12 +30,14 @@
 // a superset of the final detections -- and flushes them at the band end;
 // colfinal sorts the survivors of the final threshold by (y, x).  If a buffer
 // overflows, the ordered full-frame NMS of vmf_stage4.cu runs instead.
+#include <cstdlib>
 #include <cstring>
 
 #include "vmf_colpass.cuh"
 #include "vmf_common.cuh"
 #include "vmf_prof.cuh"
 #include "vmf_stage4.cuh"
+#include "vmf_tma.cuh"
 
 namespace vmf {
 
@@ -246,13 +248,16 @@ __device__ __forceinline__ void push2(double *Y, double y, double *X, double x) 
 
 constexpr int kTileRows(int k) { return kBand + 2 * k; }
 constexpr int kEbRows = kBand + 2;  // B of rows r0-1 .. r1
+// The TMA box must start at a 16-byte aligned column, so the tile spans 4
+// more columns than the CTA computes: tile column j + 2 <-> thread j.
+constexpr int kTileStride = kColThreads + 4;
 
 template <int K>
 struct ColSmem {
   // T rows r0-K .. r1+K-1 (clamped).  Column j is private to thread j during
   // the walk, so L(r) overwrites x(r) in place once x(r) is consumed; after
   // the walk the tile holds L rows r0-1 .. r1 for the NMS.
-  float tile[kTileRows(K)][kColThreads];
+  float tile[kTileRows(K)][kTileStride];
   double eb[kColThreads / 32][4][kEbRows];  // B of lanes 0,1,30,31 per warp
   int cy[kCandSmem], cx[kCandSmem];
   float cv[kCandSmem];
@@ -263,12 +268,14 @@ struct ColSmem {
 };
 
 template <int K>
-__global__ void __launch_bounds__(kColThreads) colapply_kernel(
+__global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, ColParams p,
     const double *__restrict__ Z, CandState *__restrict__ st, int *__restrict__ gy,
-    int *__restrict__ gx, float *__restrict__ gv, int gcap) {
+    int *__restrict__ gx, float *__restrict__ gv, int gcap,
+    const __grid_constant__ CUtensorMap tmap, int use_tma) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ColSmem<K> &S = *reinterpret_cast<ColSmem<K> *>(smem_raw);
+  // 128-byte aligned base: the tile is a TMA destination
+  ColSmem<K> &S = *reinterpret_cast<ColSmem<K> *>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
   const int j = threadIdx.x, lane = j & 31, wid = j >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * kColOut;
   const int64_t col = c0 - kColHalo + j;
@@ -285,21 +292,30 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
   const int64_t rown_hi = r1 < H ? r1 : H;  // owned rows [r0, rown_hi)
 
   // ---- stage the band's column tile (async 4-byte copies: any alignment) ---
-  float *tcol = &S.tile[0][j];  // tile row tr of this thread's column: tcol[tr * kColThreads]
-  {
+  float *tcol = &S.tile[0][j + 2];  // tile row tr of this thread's column: tcol[tr * kTileStride]
+  __shared__ __align__(8) uint64_t tbar;
+  const bool tma = use_tma && len == kBand && r0 >= K && r1 + K <= H && c0 >= 4 &&
+                   c0 + kColThreads <= p.W;
+  if (tma) {  // one TMA box: rows r0-K .. r1+K-1, columns c0-4 .. c0+127
+    if (j == 0) {
+      mbar_init(&tbar, 1);
+      mbar_expect_tx(&tbar, (unsigned)(kTileRows(K) * kTileStride * sizeof(float)));
+      tma_load_2d(&S.tile[0][0], &tmap, &tbar, (int)(c0 - 4), (int)(r0 - K));
+    }
+  } else {
     const int rows = len + 2 * K;
     const float *src = T + colc;
     if (r0 >= K && r1 + K <= H) {  // no clamping needed
       const float *s0 = src + (r0 - K) * ldt;
       for (int tr = 0; tr < rows; ++tr) {
-        unsigned sa = (unsigned)__cvta_generic_to_shared(tcol + tr * kColThreads);
+        unsigned sa = (unsigned)__cvta_generic_to_shared(tcol + tr * kTileStride);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(s0 + tr * ldt));
       }
     } else {
       for (int tr = 0; tr < rows; ++tr) {
         int64_t r = r0 - K + tr;
         r = r < 0 ? 0 : (r >= H ? H - 1 : r);
-        unsigned sa = (unsigned)__cvta_generic_to_shared(tcol + tr * kColThreads);
+        unsigned sa = (unsigned)__cvta_generic_to_shared(tcol + tr * kTileStride);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + r * ldt));
       }
     }
@@ -318,10 +334,15 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
     Ybot[i] = Z[((int64_t)(b * 2 + 1) * K + i) * p.W + colc];
     Yf[i] = Z[((int64_t)(b * 2 + 0) * K + i) * p.W + colc];
   }
-  asm volatile("cp.async.wait_group 0;\n" ::);
+  if (tma) {
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&tbar, 0);
+  } else {
+    asm volatile("cp.async.wait_group 0;\n" ::);
+  }
   __syncthreads();
   // tile row of image row r is r - r0 + K
-#define TX(tr) ((double)tcol[(tr) * kColThreads])
+#define TX(tr) ((double)tcol[(tr) * kTileStride])
 
   // ---- backward start of sub-chunk 0 when the band has two ---------------
   double E0[K];
@@ -390,61 +411,69 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
         Bm1 = fma(p.sign, ym1, fma(p.b0, x1, Yf[0]));
         Bm2 = fma(p.sign, ym2, fma(p.b0, x2, Yf[1]));
         Lxm1 = lx_of(Bm1);
+        if (edge) Lxm1 = 0.0;
         if (eslot >= 0) S.eb[wid][eslot][0] = Bm1;
       }
     }
     const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
     const float th = p.frac * fmaxf(wmax, gbound);  // lower bound of the final threshold
     unsigned int m = 0u;                             // bit t: owned row rb+t-1 flagged
-    float *lo = Lout + (rb - 1) * ldl + col;         // L row rb-1 of this column
+    const float *xp = tcol + trb * kTileStride;      // x(rb + t) at xp[t * stride]
+    float *lp = tcol + (trb - 1) * kTileStride;      // L(rb + t - 1) at lp[t * stride]
+    float *gp = Lout + (rb - 1) * ldl + col;         // global L(rb - 1)
+    double *ep = &S.eb[wid][eslot < 0 ? 0 : eslot][trb - K + 1];  // B(rb + t) at ep[t]
     // forward run: B(rb+t); L(rb+t-1) = Lx + Ly as soon as B(rb+t) exists
-    if (rb >= 1 && rb + kSub < H && s > 0) {
-      // interior sub-chunk: every L row written here is owned and in range
+    if (rb >= 1 && rb + kSub < H) {
+      // no image edge in reach: L rows rb-1 .. rb+30 are all in range; row
+      // rb-1 is owned unless it belongs to the band above (s == 0)
+      const bool own0 = own_w && s > 0;
 #pragma unroll
       for (int t = 0; t < kSub; ++t) {
-        double xv = TX(trb + t);
+        double xv = (double)xp[t * kTileStride];
         double y = dfi<K>(p, Xf, Yf);
         double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
         push2<K>(Yf, y, Xf, xv);
-        const double lx = lx_of(Bt);
-        const float v = (float)(lsc * ((edge ? 0.0 : Lxm1) + ((Bm2 - 2.0 * Bm1) + Bt)));
-        tcol[(trb + t - 1) * kColThreads] = v;
-        if (own_w) {
-          lo[t * ldl] = v;
+        double lx = lx_of(Bt);
+        const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + Bt)));
+        lp[t * kTileStride] = v;
+        if (t == 0 ? own0 : own_w) {
+          *gp = v;
           const float av = fabsf(v);
           tmax = fmaxf(tmax, av);
           m |= (av >= th ? 1u : 0u) << t;
         }
-        if (eslot >= 0) S.eb[wid][eslot][trb + t - K + 1] = Bt;
+        gp += ldl;
+        if (eslot >= 0) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
-        Lxm1 = lx;
+        Lxm1 = edge ? 0.0 : lx;
       }
     } else {
 #pragma unroll
       for (int t = 0; t < kSub; ++t) {
         const int64_t r = rb + t;
-        double xv = TX(trb + t);
+        double xv = (double)xp[t * kTileStride];
         double y = dfi<K>(p, Xf, Yf);
         double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
         push2<K>(Yf, y, Xf, xv);
         if (r == 0) Bm1 = Bt;  // replicate top edge: B(-1) = B(0)
-        const double lx = lx_of(Bt);
+        double lx = lx_of(Bt);
         const double bnext = r >= H ? Bm1 : Bt;  // replicate bottom edge
         if (r >= 1) {
-          const float v = (float)(lsc * ((edge ? 0.0 : Lxm1) + ((Bm2 - 2.0 * Bm1) + bnext)));
-          tcol[(trb + t - 1) * kColThreads] = v;
+          const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + bnext)));
+          lp[t * kTileStride] = v;
           if (own_w && r - 1 >= r0 && r - 1 < rown_hi) {
-            lo[t * ldl] = v;
+            *gp = v;
             const float av = fabsf(v);
             tmax = fmaxf(tmax, av);
             m |= (av >= th ? 1u : 0u) << t;
           }
         }
-        if (eslot >= 0) S.eb[wid][eslot][trb + t - K + 1] = Bt;
+        gp += ldl;
+        if (eslot >= 0) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
-        Lxm1 = lx;
+        Lxm1 = edge ? 0.0 : lx;
       }
     }
     masks[s] |= m;  // bit t <-> band row 32 s + t - 1
@@ -458,9 +487,8 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
       double B2 = fma(p.sign, Ybot[1], fma(p.b0, xr2, y1));
       const double lx1 = lx_of(B1);
       if (r1 - 1 < H) {
-        const float v = (float)(lsc * ((edge ? 0.0 : Lxm1) +
-                                       ((Bm2 - 2.0 * Bm1) + (r1 >= H ? Bm1 : B1))));
-        tcol[(tr1 - 1) * kColThreads] = v;
+        const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + (r1 >= H ? Bm1 : B1))));
+        tcol[(tr1 - 1) * kTileStride] = v;
         if (own_w) {
           Lout[(r1 - 1) * ldl + col] = v;
           const float av = fabsf(v);
@@ -471,7 +499,7 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
       if (r1 < H) {
         const float v = (float)(lsc * ((edge ? 0.0 : lx1) +
                                        ((Bm1 - 2.0 * B1) + (r1 + 1 >= H ? B1 : B2))));
-        tcol[tr1 * kColThreads] = v;
+        tcol[tr1 * kTileStride] = v;
       }
       if (eslot >= 0) S.eb[wid][eslot][kEbRows - 1] = B1;
     }
@@ -503,8 +531,8 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
         br = S.eb[wid + 1][0][q];
       }
       const int tr = (int)(r - r0 + K);
-      const float v = S.tile[tr][jj] + (float)(lsc * ((bl - 2.0 * bc) + br));
-      S.tile[tr][jj] = v;
+      const float v = S.tile[tr][jj + 2] + (float)(lsc * ((bl - 2.0 * bc) + br));
+      S.tile[tr][jj + 2] = v;
       const int64_t cj = c0 - kColHalo + jj;
       if (cj < p.W && r >= r0 && r < rown_hi) {
         Lout[r * ldl + cj] = v;
@@ -532,7 +560,7 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
       if (q < 0) continue;
       if (r < 1 || r > H - 2) continue;
       const int tr = (int)(r - (r0 - K));
-      const float v = S.tile[tr][j];
+      const float v = S.tile[tr][j + 2];
       if (!(fabsf(v) >= thr)) continue;
       bool gt = true, lt = true;
 #pragma unroll
@@ -540,7 +568,7 @@ __global__ void __launch_bounds__(kColThreads) colapply_kernel(
 #pragma unroll
         for (int dj = -1; dj <= 1; ++dj) {
           if (!di && !dj) continue;
-          const float u = S.tile[tr + di][j + dj];
+          const float u = S.tile[tr + di][j + 2 + dj];
           gt &= v > u;
           lt &= v < u;
         }
@@ -756,12 +784,17 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(colapply_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(ColSmem<K>));
+                           (int)sizeof(ColSmem<K>) + 128);
       attr = true;
     }
     dim3 grid((unsigned)cdiv(p.W, kColOut), (unsigned)p.NB);
-    colapply_kernel<K><<<grid, kColThreads, sizeof(ColSmem<K>), st>>>(T, ldt, L, ldl, p, Z, cs, gy,
-                                                                      gx, gv, (int)gcap);
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    int use_tma = make_tmap_2d_f32(&tmap, T, p.H, p.W, ldt, kTileStride, kTileRows(K)) &&
+                  !getenv("VMF_NO_TMA");
+    cudaGetLastError();
+    colapply_kernel<K><<<grid, kColThreads, sizeof(ColSmem<K>) + 128, st>>>(
+        T, ldt, L, ldl, p, Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma);
   }
   {
     Launch g(K_FINALIZE, st);

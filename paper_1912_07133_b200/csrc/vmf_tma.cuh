@@ -1,0 +1,53 @@
+// vmf_tma.cuh -- TMA (cp.async.bulk.tensor) helpers: host-side tensor-map
+// encoding through the driver entry point (no libcuda link), device-side
+// mbarrier + 2-D tile load.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+namespace vmf {
+
+// 2-D fp32 tensor map over a row-major [rows][cols] image with pitch ld
+// (elements); box = box_cols x box_rows.  Returns false if TMA is unavailable.
+bool make_tmap_2d_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t cols,
+                      int64_t ld, int box_cols, int box_rows);
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::);
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes));
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c, int r) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(r), "r"(b)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+  }
+}
+
+}  // namespace vmf
