@@ -49,7 +49,13 @@ __device__ __forceinline__ double ldT(const float *T, int64_t ldt, int64_t r, in
 // ---------------------------------------------------------------------------
 // 1. band carries: zero-state end histories of every (band, column)
 // ---------------------------------------------------------------------------
-// Z layout: Z[((b * 2 + dir) * K + i) * W + col]
+// Z record per (column, band, dir): 2K doubles at Z + ((col * NB + b) * 2 + dir) * 2K:
+//   [0, K)  zero-state end history of the band (then: true START history)
+//   [K, 2K) the band's edge samples in scan order: fwd = its last K rows
+//           (x(r1-1-i)), bwd = its first K rows (x(r0+i)), as doubles
+__device__ __forceinline__ int64_t zrec(int64_t col, int b, int dir, int NB, int K) {
+  return ((col * NB + b) * 2 + dir) * 2 * K;
+}
 template <int K>
 __global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__restrict__ T,
                                                                int64_t ldt, ColParams p,
@@ -103,10 +109,13 @@ __global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__re
       }
     }
   }
+  double *zf = Z + zrec(col, b, 0, p.NB, K), *zb = Z + zrec(col, b, 1, p.NB, K);
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    Z[((int64_t)(b * 2 + 0) * K + i) * p.W + col] = P[i] + Q[i];
-    Z[((int64_t)(b * 2 + 1) * K + i) * p.W + col] = P[i] - Q[i];
+    zf[i] = P[i] + Q[i];
+    zb[i] = P[i] - Q[i];
+    zf[K + i] = ldT(T, ldt, r0 + len - 1 - i, p.H, col);
+    zb[K + i] = ldT(T, ldt, r0 + i, p.H, col);
   }
 }
 
@@ -127,23 +136,23 @@ __global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ 
   const int NB = p.NB, cpl = p.cpl;
   const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, col);
   auto band_of = [&](int sp) { return dir == 0 ? sp : NB - 1 - sp; };
-  // d for scan position sp
+  // d for scan position sp: Yzs + Tx X_prev (+ Ty E_init for the first band)
   auto dval = [&](int sp, double *d) {
     const int b = band_of(sp);
-    double X[K];
+    const double *rec = Z + zrec(col, b, dir, NB, K);
     const int tb = (sp == 0 && (dir == 1 ? NB - 1 : 0) == NB - 1) ? 1 : 0;
+    double X[K];
+    if (sp == 0) {
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      if (sp == 0)
-        X[i] = xe;
-      else if (dir == 0)
-        X[i] = ldT(T, ldt, (int64_t)b * kBand - 1 - i, p.H, col);
-      else
-        X[i] = ldT(T, ldt, (int64_t)(b + 1) * kBand + i, p.H, col);
+      for (int i = 0; i < K; ++i) X[i] = xe;
+    } else {  // edge samples of the previous band in scan order
+      const double *prv = Z + zrec(col, dir == 0 ? b - 1 : b + 1, dir, NB, K);
+#pragma unroll
+      for (int i = 0; i < K; ++i) X[i] = prv[K + i];
     }
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      double acc = Z[((int64_t)(b * 2 + dir) * K + i) * p.W + col];
+      double acc = rec[i];
 #pragma unroll
       for (int q = 0; q < K; ++q) acc = fma(p.TxB[tb][i * K + q], X[q], acc);
       if (sp == 0) {
@@ -201,8 +210,9 @@ __global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ 
     const int sp = lane * cpl + q;
     if (q < cpl && sp < NB) {
       const int b = band_of(sp);
+      double *rec = Z + zrec(col, b, dir, NB, K);
 #pragma unroll
-      for (int i = 0; i < K; ++i) Z[((int64_t)(b * 2 + dir) * K + i) * p.W + col] = E[i];
+      for (int i = 0; i < K; ++i) rec[i] = E[i];
       if (sp == 0) {  // the first band's own end history, from the steady state
 #pragma unroll
         for (int i = 0; i < K; ++i) E[i] = dl[q][i];
@@ -329,10 +339,13 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   if (j < (kColThreads / 32) * 2 * (kBand / kSub + 1)) (&S.eflag[0][0][0])[j] = 0u;
   const float gbound = __uint_as_float(st->absmax_bits);  // global max so far (lower bound)
   double Ybot[K], Yf[K];
+  {
+    const double *zf = Z + zrec(colc, b, 0, p.NB, K), *zb = Z + zrec(colc, b, 1, p.NB, K);
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    Ybot[i] = Z[((int64_t)(b * 2 + 1) * K + i) * p.W + colc];
-    Yf[i] = Z[((int64_t)(b * 2 + 0) * K + i) * p.W + colc];
+    for (int i = 0; i < K; ++i) {
+      Ybot[i] = zb[i];
+      Yf[i] = zf[i];
+    }
   }
   if (tma) {
     __syncthreads();  // barrier initialised before anyone waits on it
@@ -376,7 +389,8 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   const double lsc = (double)p.lap_scale;
   double Bm2 = 0.0, Bm1 = 0.0, Lxm1 = 0.0;  // sliding state (rows r-2, r-1)
   float tmax = 0.0f;                          // this thread's running max |L|
-  unsigned int masks[kBand / kSub + 1] = {0u, 0u, 0u};  // owned rows over the threshold
+  // owned rows over the threshold: maskN bit t <-> band row 32 N + t - 1
+  unsigned int mask0 = 0u, mask1 = 0u, mask2 = 0u;
   const bool own_w = own_col && !edge;                  // writes L from the walk
   auto lx_of = [&](double bc) {  // Lx by lane shuffles; warp-edge lanes patched later
     double bl = __shfl_up_sync(0xffffffffu, bc, 1);
@@ -476,7 +490,10 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         Lxm1 = edge ? 0.0 : lx;
       }
     }
-    masks[s] |= m;  // bit t <-> band row 32 s + t - 1
+    if (s == 0)
+      mask0 |= m;
+    else
+      mask1 |= m;
     if (last) {  // B at rows r1, r1+1 -> L(r1-1), L(r1)
       const int tr1 = K + len;
       double xr1 = TX(tr1), xr2 = TX(tr1 + 1);
@@ -493,7 +510,11 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
           Lout[(r1 - 1) * ldl + col] = v;
           const float av = fabsf(v);
           tmax = fmaxf(tmax, av);
-          masks[nsub] |= (av >= p.frac * fmaxf(tmax, gbound) ? 1u : 0u);  // band row len-1
+          const unsigned bit = av >= p.frac * fmaxf(tmax, gbound) ? 1u : 0u;  // row len-1
+          if (nsub == 1)
+            mask1 |= bit;
+          else
+            mask2 |= bit;
         }
       }
       if (r1 < H) {
@@ -545,17 +566,19 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   __syncthreads();
   if (lane == 0 || lane == 31) {  // edge columns: flags gathered by the patch
     const int side = lane == 31;
-#pragma unroll
-    for (int w = 0; w <= kBand / kSub; ++w) masks[w] |= S.eflag[wid][side][w];
+    mask0 |= S.eflag[wid][side][0];
+    mask1 |= S.eflag[wid][side][1];
+    mask2 |= S.eflag[wid][side][2];
   }
 
   // ---- strict 3x3 extrema among the flagged rows ----------------------------
   const float thr = p.frac * fmaxf(__uint_as_float(S.cmax), gbound);
   if (own_col && col >= 1 && col <= p.W - 2) {
-    // masks[w] bit t <-> band row 32 w + t - 1
-    for (int w = 0; w <= kBand / kSub; ++w) while (masks[w]) {
-      const int q = 32 * w + __ffs((int)masks[w]) - 2;
-      masks[w] &= masks[w] - 1;
+    for (int w = 0; w <= kBand / kSub; ++w) {
+      unsigned int mk = w == 0 ? mask0 : (w == 1 ? mask1 : mask2);
+      while (mk) {
+      const int q = 32 * w + __ffs((int)mk) - 2;
+      mk &= mk - 1;
       const int64_t r = r0 + q;
       if (q < 0) continue;
       if (r < 1 || r > H - 2) continue;
@@ -582,6 +605,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
           S.coverflow = 1;
         }
       }
+    }
     }
   }
   __syncthreads();
@@ -748,7 +772,7 @@ size_t colpass_workspace_bytes(int64_t h, int64_t w, int k, int64_t) {
   int NB, Bl;
   col_geometry(h, &Hp, &NB, &Bl);
   int64_t gcap = cand_capacity(h, w);
-  size_t z = (size_t)NB * 2 * k * w * sizeof(double);
+  size_t z = (size_t)NB * 2 * 2 * k * w * sizeof(double);
   return 4096 + ((z + 255) & ~(size_t)255) + (size_t)gcap * 12 + 1024 +
          detect_workspace_bytes(1, h, w);
 }
@@ -760,7 +784,7 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   CandState *cs = (CandState *)base;
   int *fallback = (int *)(base + 64);
-  size_t z = (size_t)p.NB * 2 * K * p.W * sizeof(double);
+  size_t z = (size_t)p.NB * 2 * 2 * K * p.W * sizeof(double);
   double *Z = (double *)(base + 4096);
   char *q = base + 4096 + ((z + 255) & ~(size_t)255);
   int64_t gcap = cand_capacity(p.H, p.W);

@@ -107,21 +107,25 @@ __global__ void __launch_bounds__(kNmsThreads) nms_count_kernel(
   if (gate && !*gate) return;
   float thr = frac * *absmax;
   if (blockIdx.x == 0 && threadIdx.x == 0 && thr_out) *thr_out = thr;
-  int64_t total = ns * h * w;
-  int64_t base = (int64_t)blockIdx.x * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
-  int c = 0;
-  float v;
-#pragma unroll
-  for (int e = 0; e < kNmsPerThread; ++e) {
-    int64_t p = base + e;
-    if (p < total && is_det(l, ld, plane, ns, h, w, p, thr, &v)) ++c;
-  }
+  const int64_t total = ns * h * w;
+  const int64_t nranges = (total + kNmsPerBlock - 1) / kNmsPerBlock;
   __shared__ int sc;
-  if (threadIdx.x == 0) sc = 0;
-  __syncthreads();
-  if (c) atomicAdd(&sc, c);
-  __syncthreads();
-  if (threadIdx.x == 0) counts[blockIdx.x] = sc;
+  for (int64_t rg = blockIdx.x; rg < nranges; rg += gridDim.x) {  // grid-stride over ranges
+    int64_t base = rg * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
+    int c = 0;
+    float v;
+#pragma unroll
+    for (int e = 0; e < kNmsPerThread; ++e) {
+      int64_t p = base + e;
+      if (p < total && is_det(l, ld, plane, ns, h, w, p, thr, &v)) ++c;
+    }
+    if (threadIdx.x == 0) sc = 0;
+    __syncthreads();
+    if (c) atomicAdd(&sc, c);
+    __syncthreads();
+    if (threadIdx.x == 0) counts[rg] = sc;
+    __syncthreads();
+  }
 }
 
 // Single CTA: exclusive scan of per-CTA counts, total -> *n_det.
@@ -161,8 +165,11 @@ __global__ void __launch_bounds__(kNmsThreads) nms_write_kernel(
     const int *gate) {
   if (gate && !*gate) return;
   float thr = frac * *absmax;
-  int64_t total = ns * h * w;
-  int64_t base = (int64_t)blockIdx.x * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
+  const int64_t total = ns * h * w;
+  const int64_t nranges = (total + kNmsPerBlock - 1) / kNmsPerBlock;
+  __shared__ int wsum[kNmsThreads / 32];
+  for (int64_t rg = blockIdx.x; rg < nranges; rg += gridDim.x) {  // grid-stride over ranges
+  int64_t base = rg * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
   unsigned flags = 0;
   float vals[kNmsPerThread];
 #pragma unroll
@@ -173,7 +180,6 @@ __global__ void __launch_bounds__(kNmsThreads) nms_write_kernel(
   }
   int c = __popc(flags);
   // block exclusive scan of c (thread order == pixel order)
-  __shared__ int wsum[kNmsThreads / 32];
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int inc = c;
 #pragma unroll
@@ -181,6 +187,7 @@ __global__ void __launch_bounds__(kNmsThreads) nms_write_kernel(
     int t = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += t;
   }
+  __syncthreads();
   if (lane == 31) wsum[wid] = inc;
   __syncthreads();
   if (wid == 0) {
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(kNmsThreads) nms_write_kernel(
     if (lane < kNmsThreads / 32) wsum[lane] = v;
   }
   __syncthreads();
-  int64_t pos = (int64_t)offsets[blockIdx.x] + (wid ? wsum[wid - 1] : 0) + inc - c;
+  int64_t pos = (int64_t)offsets[rg] + (wid ? wsum[wid - 1] : 0) + inc - c;
   int64_t hw = h * w;
 #pragma unroll
   for (int e = 0; e < kNmsPerThread; ++e) {
@@ -214,6 +221,7 @@ __global__ void __launch_bounds__(kNmsThreads) nms_write_kernel(
       det_val[pos] = vals[e];
     }
     ++pos;
+  }
   }
 }
 
@@ -271,9 +279,11 @@ static int detect_core(const float *l, int64_t ld, int64_t plane, int64_t ns, in
                        float *thr_dev, int *counts, cudaStream_t st) {
   int64_t nb = cdiv(ns * h * w, kNmsPerBlock);
   if (nb > 0x7fffffff) return fail(VMF_EVALUE, "frame stack too large");
+  // grid-stride launch: a gated (fallback) launch costs a few hundred idle CTAs
+  const unsigned grid = (unsigned)(nb < (int64_t)sm_count() * 8 ? nb : (int64_t)sm_count() * 8);
   {
     Launch g(K_NMS_COUNT, st);
-    nms_count_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
+    nms_count_kernel<<<grid, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
                                                            thr_dev, counts, gate);
   }
   {
@@ -282,7 +292,7 @@ static int detect_core(const float *l, int64_t ld, int64_t plane, int64_t ns, in
   }
   {
     Launch g(K_NMS_WRITE, st);
-    nms_write_kernel<<<(unsigned)nb, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
+    nms_write_kernel<<<grid, kNmsThreads, 0, st>>>(l, ld, plane, ns, h, w, frac, absmax,
                                                            counts, det_idx, idx_stride, det_val,
                                                            cap, gate);
   }
