@@ -49,44 +49,34 @@ __device__ __forceinline__ double ldT(const float *T, int64_t ldt, int64_t r, in
 // ---------------------------------------------------------------------------
 // 1. band carries: zero-state end histories of every (band, column)
 // ---------------------------------------------------------------------------
-// Z record per (column, band, dir): 2K doubles at Z + ((col * NB + b) * 2 + dir) * 2K:
-//   [0, K)  zero-state end history of the band (then: true START history)
-//   [K, 2K) the band's edge samples in scan order: fwd = its last K rows
-//           (x(r1-1-i)), bwd = its first K rows (x(r0+i)), as doubles
-__device__ __forceinline__ int64_t zrec(int64_t col, int b, int dir, int NB, int K) {
-  return ((col * NB + b) * 2 + dir) * 2 * K;
+// Z layout (coalesced along columns): Z[((b * 2 + dir) * K + i) * W + col]
+__device__ __forceinline__ int64_t zidx(int b, int dir, int i, int K, int64_t W, int64_t col) {
+  return ((int64_t)(b * 2 + dir) * K + i) * W + col;
 }
+
+// f_i = sum_t h(len-1-i-t) x_t, g_i = sum_t h(t-i) x_t over the band.  With
+// u = x_t + x_t', v = x_t - x_t' (t' = len-1-t): f = P + Q, g = P - Q, so a
+// pair of samples costs 2 adds + 2K FMAs instead of 4K FMAs.  The pair
+// weights of a full band are compile-time-indexed kernel parameters.
 template <int K>
 __global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__restrict__ T,
                                                                int64_t ldt, ColParams p,
                                                                double *__restrict__ Z) {
-  __shared__ double SP[K][kBand / 2], SQ[K][kBand / 2];
   const int b = blockIdx.y;
   const int len = b == p.NB - 1 ? p.Blast : kBand;
-  const int half = len / 2;
-  // pair weights: f_i = sum_t h(len-1-i-t) x_t, g_i = sum_t h(t-i) x_t; with
-  // u = x_t + x_t', v = x_t - x_t' (t' = len-1-t): f = P + Q, g = P - Q, so a
-  // pair of samples costs 2 adds + 2K FMAs instead of 4K FMAs.
-  for (int q = threadIdx.x; q < K * (kBand / 2); q += blockDim.x) {
-    int i = q / (kBand / 2), t = q % (kBand / 2);
-    int qa = len - 1 - i - t, qb = t - i;
-    double A = (t < half && qa > 0) ? p.h[qa] : 0.0, B = (t < half && qb > 0) ? p.h[qb] : 0.0;
-    SP[i][t] = 0.5 * (A + B);
-    SQ[i][t] = 0.5 * (A - B);
-  }
-  __syncthreads();
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= p.W) return;
   const int64_t r0 = (int64_t)b * kBand;
-  double P[K], Q[K];
+  double P[2][K], Q[2][K];  // two partial sums each for ILP
 #pragma unroll
-  for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
-  if (len == kBand) {
+  for (int i = 0; i < K; ++i) P[0][i] = P[1][i] = Q[0][i] = Q[1][i] = 0.0;
+  if (len == kBand && r0 + kBand <= p.H) {
+    const float *src = T + r0 * ldt + col;
     float xa[kBand / 2], xb[kBand / 2];
 #pragma unroll
     for (int t = 0; t < kBand / 2; ++t) {  // all loads in flight at once
-      xa[t] = __ldg(T + min(r0 + t, p.H - 1) * ldt + col);
-      xb[t] = __ldg(T + min(r0 + kBand - 1 - t, p.H - 1) * ldt + col);
+      xa[t] = __ldg(src + t * ldt);
+      xb[t] = __ldg(src + (kBand - 1 - t) * ldt);
     }
 #pragma unroll
     for (int t = 0; t < kBand / 2; ++t) {
@@ -94,139 +84,147 @@ __global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__re
       double u = a + c, v = a - c;
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        P[i] = fma(SP[i][t], u, P[i]);
-        Q[i] = fma(SQ[i][t], v, Q[i]);
+        P[t & 1][i] = fma(p.SP[i][t], u, P[t & 1][i]);
+        Q[t & 1][i] = fma(p.SQ[i][t], v, Q[t & 1][i]);
       }
     }
-  } else {
-    for (int t = 0; t < half; ++t) {
-      double a = ldT(T, ldt, r0 + t, p.H, col), c = ldT(T, ldt, r0 + len - 1 - t, p.H, col);
-      double u = a + c, v = a - c;
+  } else {  // last (short or padded) band: direct weights
+    for (int t = 0; t < len; ++t) {
+      double x = ldT(T, ldt, r0 + t, p.H, col);
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        P[i] = fma(SP[i][t], u, P[i]);
-        Q[i] = fma(SQ[i][t], v, Q[i]);
+        int qa = len - 1 - i - t, qb = t - i;
+        if (qa > 0) P[0][i] = fma(p.h[qa], x, P[0][i]);
+        if (qb > 0) Q[0][i] = fma(p.h[qb], x, Q[0][i]);
       }
     }
+    // convert (f, g) into the (P, Q) convention: f = P + Q, g = P - Q
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double f = P[0][i], g = Q[0][i];
+      P[0][i] = 0.5 * (f + g);
+      Q[0][i] = 0.5 * (f - g);
+    }
   }
-  double *zf = Z + zrec(col, b, 0, p.NB, K), *zb = Z + zrec(col, b, 1, p.NB, K);
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    zf[i] = P[i] + Q[i];
-    zb[i] = P[i] - Q[i];
-    zf[K + i] = ldT(T, ldt, r0 + len - 1 - i, p.H, col);
-    zb[K + i] = ldT(T, ldt, r0 + i, p.H, col);
+    const double Pt = P[0][i] + P[1][i], Qt = Q[0][i] + Q[1][i];
+    Z[zidx(b, 0, i, K, p.W, col)] = Pt + Qt;
+    Z[zidx(b, 1, i, K, p.W, col)] = Pt - Qt;
   }
 }
 
 // ---------------------------------------------------------------------------
-// 2. band scan: one warp per (column, direction), lanes over bands
-//    E_s = d_s + TyB E_{s-1} in scan order (backward = bands bottom-up);
-//    Kogge-Stone with TyB^(cpl 2^l); writes the START history of every band
-//    in place: fwd slot b = y+(r0-1 .. r0-K), bwd slot b = y-(r1 .. r1+K-1).
+// 2. band scan.  CTA = 32 columns (lanes, coalesced) x kScanWarps warps; warp
+//    g owns a contiguous group of bands in scan order: local aggregate (zero
+//    start), exclusive combination of the earlier groups' aggregates with
+//    TyB^cpb, then a re-scan from the true carry-in.  Writes the START history
+//    of every band in place: fwd slot b = y+(r0-1 .. r0-K), bwd slot b =
+//    y-(r1 .. r1+K-1).
 // ---------------------------------------------------------------------------
+constexpr int kScanWarps = 16;
+constexpr int kMaxCpb = 8;  // bands per scan warp (NB <= 128)
+
 template <int K>
-__global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ T, int64_t ldt,
-                                                      ColParams p, double *__restrict__ Z) {
-  const int lane = threadIdx.x & 31;
-  const int64_t task = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (task >= 2 * p.W) return;
-  const int64_t col = task >> 1;
-  const int dir = (int)(task & 1);
-  const int NB = p.NB, cpl = p.cpl;
-  const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, col);
-  auto band_of = [&](int sp) { return dir == 0 ? sp : NB - 1 - sp; };
-  // d for scan position sp: Yzs + Tx X_prev (+ Ty E_init for the first band)
+__global__ void __launch_bounds__(32 * kScanWarps) colscan_kernel(const float *__restrict__ T,
+                                                                  int64_t ldt, ColParams p,
+                                                                  double *__restrict__ Z) {
+  __shared__ double agg[kScanWarps][K][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t col = (int64_t)blockIdx.x * 32 + lane;
+  const int dir = blockIdx.y;
+  const int NB = p.NB, cpb = p.cpb;
+  const bool live = col < p.W;
+  const int64_t cc = live ? col : p.W - 1;
+  const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, cc);
+  // d for scan position sp (band b): Yzs + TxB X_prev (+ TyB E_init first)
   auto dval = [&](int sp, double *d) {
-    const int b = band_of(sp);
-    const double *rec = Z + zrec(col, b, dir, NB, K);
-    const int tb = (sp == 0 && (dir == 1 ? NB - 1 : 0) == NB - 1) ? 1 : 0;
+    const int b = dir == 0 ? sp : NB - 1 - sp;
+    const int tb = b == NB - 1 ? 1 : 0;
     double X[K];
-    if (sp == 0) {
 #pragma unroll
-      for (int i = 0; i < K; ++i) X[i] = xe;
-    } else {  // edge samples of the previous band in scan order
-      const double *prv = Z + zrec(col, dir == 0 ? b - 1 : b + 1, dir, NB, K);
-#pragma unroll
-      for (int i = 0; i < K; ++i) X[i] = prv[K + i];
+    for (int i = 0; i < K; ++i) {
+      if (sp == 0)
+        X[i] = xe;
+      else if (dir == 0)
+        X[i] = ldT(T, ldt, (int64_t)b * kBand - 1 - i, p.H, cc);
+      else
+        X[i] = ldT(T, ldt, (int64_t)(b + 1) * kBand + i, p.H, cc);
     }
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      double acc = rec[i];
+      double acc = Z[zidx(b, dir, i, K, p.W, cc)];
 #pragma unroll
-      for (int q = 0; q < K; ++q) acc = fma(p.TxB[tb][i * K + q], X[q], acc);
+      for (int m = 0; m < K; ++m) acc = fma(p.TxB[tb][i * K + m], X[m], acc);
       if (sp == 0) {
 #pragma unroll
-        for (int q = 0; q < K; ++q) acc = fma(p.TyB[tb][i * K + q], p.yss * xe, acc);
+        for (int m = 0; m < K; ++m) acc = fma(p.TyB[tb][i * K + m], p.yss * xe, acc);
       }
       d[i] = acc;
     }
   };
-  double dl[kMaxCpl][K];
+  auto step = [&](const double *TyM, double *E, const double *d) {
+    double En[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double acc = d[i];
+#pragma unroll
+      for (int m = 0; m < K; ++m) acc = fma(TyM[i * K + m], E[m], acc);
+      En[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) E[i] = En[i];
+  };
+  const int s0 = g * cpb, s1 = min(s0 + cpb, NB);
+  // the transfer over a band: band lengths differ only for band NB-1, which
+  // is crossed first in the backward scan and last (never needed) forward
+  const double *TyF = p.TyB[0];
+  double dv[kMaxCpb][K];  // every load of the group issued up front
+#pragma unroll
+  for (int q = 0; q < kMaxCpb; ++q)
+    if (s0 + q < s1) dval(s0 + q, dv[q]);
   double A[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) A[i] = 0.0;
 #pragma unroll
-  for (int q = 0; q < kMaxCpl; ++q) {
-    const int sp = lane * cpl + q;
-    if (q < cpl && sp < NB) {
-      dval(sp, dl[q]);
-      double An[K];
+  for (int q = 0; q < kMaxCpb; ++q)
+    if (s0 + q < s1) step(TyF, A, dv[q]);
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        double acc = dl[q][i];
-#pragma unroll
-        for (int m = 0; m < K; ++m) acc = fma(p.TyB[0][i * K + m], A[m], acc);
-        An[i] = acc;
-      }
-#pragma unroll
-      for (int i = 0; i < K; ++i) A[i] = An[i];
-    }
-  }
-#pragma unroll
-  for (int lv = 0; lv < 5; ++lv) {
-    const int o = 1 << lv;
-    double B[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) B[i] = __shfl_up_sync(0xffffffffu, A[i], o);
-    if (lane >= o) {
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        double acc = A[i];
-#pragma unroll
-        for (int m = 0; m < K; ++m) acc = fma(p.TyBp[lv][i * K + m], B[m], acc);
-        A[i] = acc;
-      }
-    }
-  }
+  for (int i = 0; i < K; ++i) agg[g][i][lane] = A[i];
+  __syncthreads();
+  // carry-in: E = sum_{h < g} TyB^(cpb (g-1-h)) A_h, composed in order
   double E[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    double v = __shfl_up_sync(0xffffffffu, A[i], 1);
-    E[i] = lane ? v : p.yss * xe;
+  for (int i = 0; i < K; ++i) E[i] = 0.0;
+  for (int h = 0; h < g; ++h) {
+    double Ah[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) Ah[i] = agg[h][i][lane];
+    if (h == 0) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) E[i] = Ah[i];
+    } else {
+      step(p.TyBc, E, Ah);
+    }
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) E[i] = p.yss * xe;  // exclusive start of the first band
   }
 #pragma unroll
-  for (int q = 0; q < kMaxCpl; ++q) {
-    const int sp = lane * cpl + q;
-    if (q < cpl && sp < NB) {
-      const int b = band_of(sp);
-      double *rec = Z + zrec(col, b, dir, NB, K);
+  for (int q = 0; q < kMaxCpb; ++q) {
+    const int sp = s0 + q;
+    if (sp < s1) {
+      const int b = dir == 0 ? sp : NB - 1 - sp;
+      if (live) {
 #pragma unroll
-      for (int i = 0; i < K; ++i) rec[i] = E[i];
-      if (sp == 0) {  // the first band's own end history, from the steady state
+        for (int i = 0; i < K; ++i) Z[zidx(b, dir, i, K, p.W, cc)] = E[i];
+      }
+      if (sp == 0) {
 #pragma unroll
-        for (int i = 0; i < K; ++i) E[i] = dl[q][i];
+        for (int i = 0; i < K; ++i) E[i] = dv[q][i];
       } else {
-        double En[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          double acc = dl[q][i];
-#pragma unroll
-          for (int m = 0; m < K; ++m) acc = fma(p.TyB[0][i * K + m], E[m], acc);
-          En[i] = acc;
-        }
-#pragma unroll
-        for (int i = 0; i < K; ++i) E[i] = En[i];
+        step(TyF, E, dv[q]);
       }
     }
   }
@@ -339,13 +337,10 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   if (j < (kColThreads / 32) * 2 * (kBand / kSub + 1)) (&S.eflag[0][0][0])[j] = 0u;
   const float gbound = __uint_as_float(st->absmax_bits);  // global max so far (lower bound)
   double Ybot[K], Yf[K];
-  {
-    const double *zf = Z + zrec(colc, b, 0, p.NB, K), *zb = Z + zrec(colc, b, 1, p.NB, K);
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      Ybot[i] = zb[i];
-      Yf[i] = zf[i];
-    }
+  for (int i = 0; i < K; ++i) {
+    Ybot[i] = Z[zidx(b, 1, i, K, p.W, colc)];
+    Yf[i] = Z[zidx(b, 0, i, K, p.W, colc)];
   }
   if (tma) {
     __syncthreads();  // barrier initialised before anyone waits on it
@@ -637,15 +632,68 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
 // 4. final threshold + (y, x) order: one CTA, bitonic sort in shared memory
 // ---------------------------------------------------------------------------
 constexpr int kSortCap = 4096;
+constexpr int kFinThreads = 1024;
 
-__global__ void __launch_bounds__(1024) colfinal_kernel(CandState *__restrict__ st,
-                                                        const int *__restrict__ gy,
-                                                        const int *__restrict__ gx,
-                                                        const float *__restrict__ gv, int gcap,
-                                                        int64_t W, float frac, int32_t *det_yx,
-                                                        float *det_val, int64_t cap,
-                                                        int64_t *n_det, float *thr_out,
-                                                        int *fallback) {
+// Ordered full-frame NMS by one CTA: the (rare) fallback when a candidate
+// buffer overflowed.  Rows in order, each row compacted with a block scan, so
+// the output is sorted by (y, x) like the fast path.
+__device__ void final_fullscan(const float *__restrict__ L, int64_t ldl, int64_t H, int64_t W,
+                               float thr, int32_t *det_yx, float *det_val, int64_t cap,
+                               int64_t *n_det) {
+  __shared__ int wsum[kFinThreads / 32];
+  __shared__ long long base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t r = 1; r + 1 < H; ++r) {
+    for (int64_t c0 = 0; c0 < W; c0 += kFinThreads) {
+      const int64_t c = c0 + threadIdx.x;
+      bool det = false;
+      float v = 0.0f;
+      if (c >= 1 && c + 1 < W) {
+        v = L[r * ldl + c];
+        if (fabsf(v) >= thr) {
+          bool gt = true, lt = true;
+          for (int di = -1; di <= 1; ++di)
+            for (int dj = -1; dj <= 1; ++dj) {
+              if (!di && !dj) continue;
+              float u = L[(r + di) * ldl + c + dj];
+              gt &= v > u;
+              lt &= v < u;
+            }
+          det = gt || lt;
+        }
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, det);
+      if (lane == 0) wsum[wid] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+      for (int w = 0; w < kFinThreads / 32; ++w) {
+        if (w < wid) before += wsum[w];
+        total += wsum[w];
+      }
+      before += __popc(bal & ((1u << lane) - 1u));
+      if (det) {
+        long long pos = base + before;
+        if (pos < cap) {
+          det_yx[2 * pos] = (int32_t)r;
+          det_yx[2 * pos + 1] = (int32_t)c;
+          det_val[pos] = v;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) base += total;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) *n_det = base;
+}
+
+__global__ void __launch_bounds__(kFinThreads) colfinal_kernel(
+    CandState *__restrict__ st, const int *__restrict__ gy, const int *__restrict__ gx,
+    const float *__restrict__ gv, int gcap, const float *__restrict__ L, int64_t ldl, int64_t H,
+    int64_t W, float frac, int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det,
+    float *thr_out, int force_full) {
   extern __shared__ __align__(16) unsigned char fsm[];
   unsigned long long *key = reinterpret_cast<unsigned long long *>(fsm);
   float *val = reinterpret_cast<float *>(fsm + kSortCap * sizeof(unsigned long long));
@@ -667,12 +715,25 @@ __global__ void __launch_bounds__(1024) colfinal_kernel(CandState *__restrict__ 
     }
   }
   __syncthreads();
-  const bool fb = st->overflow || m > kSortCap;
-  if (fb) {
-    if (threadIdx.x == 0) *fallback = 1;
+  if (force_full || st->overflow || m > kSortCap) {  // buffer overflow: exact, slow path
+    final_fullscan(L, ldl, H, W, thr, det_yx, det_val, cap, n_det);
     return;
   }
-  if (threadIdx.x == 0) *fallback = 0;
+  if (m <= kFinThreads) {
+    // rank sort: keys are distinct (y, x) positions; broadcast smem reads
+    if (threadIdx.x < m) {
+      const unsigned long long mine = key[threadIdx.x];
+      int rank = 0;
+      for (int q = 0; q < m; ++q) rank += key[q] < mine;
+      if (rank < cap) {
+        det_yx[2 * rank] = (int32_t)(mine / (unsigned long long)W);
+        det_yx[2 * rank + 1] = (int32_t)(mine % (unsigned long long)W);
+        det_val[rank] = val[threadIdx.x];
+      }
+    }
+    if (threadIdx.x == 0) *n_det = m;
+    return;
+  }
   int np = 1;
   while (np < m) np <<= 1;
   for (int q = m + threadIdx.x; q < np; q += blockDim.x) key[q] = ~0ull;
@@ -750,7 +811,7 @@ static void impulse_ld(const double *b, const double *a, int k, int n, double *h
 
 bool colpass_supported(int64_t h, int64_t w, int k) {
   return k >= 2 && k <= 4 && h >= 2 * kSub && w >= 1 &&
-         cdiv(cdiv(h, kSub) * kSub, kBand) <= 32 * kMaxCpl;
+         cdiv(cdiv(h, kSub) * kSub, kBand) <= kScanWarps * kMaxCpb;
 }
 
 static void col_geometry(int64_t h, int64_t *Hp, int *NB, int *Blast) {
@@ -772,7 +833,7 @@ size_t colpass_workspace_bytes(int64_t h, int64_t w, int k, int64_t) {
   int NB, Bl;
   col_geometry(h, &Hp, &NB, &Bl);
   int64_t gcap = cand_capacity(h, w);
-  size_t z = (size_t)NB * 2 * 2 * k * w * sizeof(double);
+  size_t z = (size_t)NB * 2 * k * w * sizeof(double);
   return 4096 + ((z + 255) & ~(size_t)255) + (size_t)gcap * 12 + 1024 +
          detect_workspace_bytes(1, h, w);
 }
@@ -784,7 +845,7 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   CandState *cs = (CandState *)base;
   int *fallback = (int *)(base + 64);
-  size_t z = (size_t)p.NB * 2 * 2 * K * p.W * sizeof(double);
+  size_t z = (size_t)p.NB * 2 * K * p.W * sizeof(double);
   double *Z = (double *)(base + 4096);
   char *q = base + 4096 + ((z + 255) & ~(size_t)255);
   int64_t gcap = cand_capacity(p.H, p.W);
@@ -801,7 +862,7 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   }
   {
     Launch g(K_COL_SCAN, st);
-    colscan_kernel<K><<<(unsigned)cdiv(2 * p.W, 4), 128, 0, st>>>(T, ldt, p, Z);
+    colscan_kernel<K><<<dim3((unsigned)cdiv(p.W, 32), 2), 32 * kScanWarps, 0, st>>>(T, ldt, p, Z);
   }
   {
     Launch g(K_IIR_COLS_FUSED, st);
@@ -828,14 +889,11 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
       cudaFuncSetAttribute(colfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
       fattr = true;
     }
-    colfinal_kernel<<<1, 1024, fsmem, st>>>(cs, gy, gx, gv, (int)gcap, p.W, p.frac, det_yx,
-                                            det_val, cap, n_det_dev, thr_dev, fallback);
+    colfinal_kernel<<<1, kFinThreads, fsmem, st>>>(cs, gy, gx, gv, (int)gcap, L, ldl, p.H, p.W,
+                                                   p.frac, det_yx, det_val, cap, n_det_dev,
+                                                   thr_dev, getenv("VMF_FORCE_FULLSCAN") ? 1 : 0);
   }
-  int rc = cuda_status("column pass");
-  if (rc) return rc;
-  // ordered full-frame NMS, executed only if the candidate path overflowed
-  return detect_if(L, ldl, p.H, p.W, p.frac, (float *)&cs->absmax_bits, fallback, det_yx,
-                   det_val, cap, n_det_dev, thr_dev, dws, dws_b, st);
+  return cuda_status("column pass");
 }
 
 int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,
@@ -862,7 +920,19 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirPar
   col_geometry(h, &p.Hp, &p.NB, &p.Blast);
   transfer_ld(ip.b, ip.a, k, kBand, p.TyB[0], p.TxB[0]);
   transfer_ld(ip.b, ip.a, k, p.Blast, p.TyB[1], p.TxB[1]);
+  for (int i = 0; i < k; ++i)
+    for (int t = 0; t < kBand / 2; ++t) {
+      int qa = kBand - 1 - i - t, qb = t - i;
+      double A = qa > 0 ? p.h[qa] : 0.0, B = qb > 0 ? p.h[qb] : 0.0;
+      p.SP[i][t] = 0.5 * (A + B);
+      p.SQ[i][t] = 0.5 * (A - B);
+    }
   p.cpl = (p.NB + 31) / 32;
+  p.cpb = (p.NB + kScanWarps - 1) / kScanWarps;
+  {
+    double tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
+    transfer_ld(ip.b, ip.a, k, p.cpb * kBand, p.TyBc, tx);
+  }
   if (p.cpl > kMaxCpl) return fail(VMF_EVALUE, "image too tall for the fused column pass");
   for (int l = 0; l < 5; ++l) {
     double tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];

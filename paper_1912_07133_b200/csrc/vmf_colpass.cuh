@@ -23,8 +23,10 @@ struct ColParams {
   double TyB[2][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // over a band / the last band
   double TxB[2][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
   double TyBp[5][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // TyB^(cpl 2^l)
+  double SP[4][kBand / 2], SQ[4][kBand / 2];  // folded band-carry weights (K <= 4)
   int64_t H, W, Hp;       // Hp = H rounded up to 32 (rows >= H replicate row H-1)
-  int NB, Blast, cpl;     // bands; rows in the last band (multiple of 32); bands/lane
+  double TyBc[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // TyB^cpb (one scan group)
+  int NB, Blast, cpl, cpb;  // bands; rows in the last band; bands per lane / scan group
   float lap_scale, frac;
 };
 

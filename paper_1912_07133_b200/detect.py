@@ -98,7 +98,7 @@ def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out
     cap = int(cap)
     det_yx = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
     det_val = torch.empty((max(cap, 1),), dtype=torch.float32, device=dev)
-    scal = torch.zeros(2, dtype=torch.int64, device=dev)  # [n_det, thr(float bits)]
+    scal = torch.empty(2, dtype=torch.int64, device=dev)  # [n_det, thr(float bits)], written by the call
     n_host = C.c_int64(0)
     _lib.check(L.vmf_blur_lap_detect(
         _ptr(x), code, h, w, _pitch(x), C.byref(row.s), C.byref(col.s), float(lap_scale),

@@ -227,3 +227,17 @@ def test_config5_coarse_scale(cat):
     x = synth.config5_frame(4096)  # quarter-area instance of the 8192^2 frame
     _check_pipeline(x, cat["bw48"], label="config5/bw48")
     _check_pipeline(x, cat["sg38.4"], label="config5/sg38.4")
+
+
+def test_candidate_overflow_fallback_matches(cat, monkeypatch):
+    """The ordered full-frame NMS used when a candidate buffer overflows
+    (colfinal's fallback) gives the same blob list as the fast path."""
+    D = _D()
+    x = synth.config1_frame()
+    fast = D.blur_laplacian_detect(x, cat["rp4_k2"], frac=0.3)
+    monkeypatch.setenv("VMF_FORCE_FULLSCAN", "1")
+    slow = D.blur_laplacian_detect(x, cat["rp4_k2"], frac=0.3)
+    assert fast.count == slow.count > 0
+    np.testing.assert_array_equal(fast.y, slow.y)
+    np.testing.assert_array_equal(fast.x, slow.x)
+    np.testing.assert_array_equal(fast.value, slow.value)
