@@ -59,24 +59,47 @@ __device__ __forceinline__ int64_t zidx(int b, int dir, int i, int K, int64_t W,
 // pair of samples costs 2 adds + 2K FMAs instead of 4K FMAs.  The pair
 // weights of a full band are compile-time-indexed kernel parameters.
 template <int K>
-__global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__restrict__ T,
-                                                               int64_t ldt, ColParams p,
-                                                               double *__restrict__ Z) {
+__global__ void __launch_bounds__(kColThreads) colcarry_kernel(
+    const float *__restrict__ T, int64_t ldt, ColParams p, double *__restrict__ Z,
+    const __grid_constant__ CUtensorMap tmap, int use_tma) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *tile = reinterpret_cast<float *>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+  __shared__ __align__(8) uint64_t tbar;
   const int b = blockIdx.y;
   const int len = b == p.NB - 1 ? p.Blast : kBand;
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= p.W) return;
+  const int64_t c0 = (int64_t)blockIdx.x * kColThreads;
+  const int64_t col = c0 + threadIdx.x;
   const int64_t r0 = (int64_t)b * kBand;
+  const bool full = len == kBand && r0 + kBand <= p.H;
+  const bool tma = use_tma && full && c0 + kColThreads <= p.W;
+  if (tma) {  // the whole 64 x 128 band tile in one TMA box
+    if (threadIdx.x == 0) {
+      mbar_init(&tbar, 1);
+      mbar_expect_tx(&tbar, (unsigned)(kBand * kColThreads * sizeof(float)));
+      tma_load_2d(tile, &tmap, &tbar, (int)c0, (int)r0);
+    }
+    __syncthreads();
+    mbar_wait(&tbar, 0);
+  }
+  if (col >= p.W) return;
   double P[2][K], Q[2][K];  // two partial sums each for ILP
 #pragma unroll
   for (int i = 0; i < K; ++i) P[0][i] = P[1][i] = Q[0][i] = Q[1][i] = 0.0;
-  if (len == kBand && r0 + kBand <= p.H) {
-    const float *src = T + r0 * ldt + col;
+  if (full) {
     float xa[kBand / 2], xb[kBand / 2];
+    if (tma) {
 #pragma unroll
-    for (int t = 0; t < kBand / 2; ++t) {  // all loads in flight at once
-      xa[t] = __ldg(src + t * ldt);
-      xb[t] = __ldg(src + (kBand - 1 - t) * ldt);
+      for (int t = 0; t < kBand / 2; ++t) {
+        xa[t] = tile[t * kColThreads + threadIdx.x];
+        xb[t] = tile[(kBand - 1 - t) * kColThreads + threadIdx.x];
+      }
+    } else {
+      const float *src = T + r0 * ldt + col;
+#pragma unroll
+      for (int t = 0; t < kBand / 2; ++t) {  // all loads in flight at once
+        xa[t] = __ldg(src + t * ldt);
+        xb[t] = __ldg(src + (kBand - 1 - t) * ldt);
+      }
     }
 #pragma unroll
     for (int t = 0; t < kBand / 2; ++t) {
@@ -122,8 +145,8 @@ __global__ void __launch_bounds__(kColThreads) colcarry_kernel(const float *__re
 //    of every band in place: fwd slot b = y+(r0-1 .. r0-K), bwd slot b =
 //    y-(r1 .. r1+K-1).
 // ---------------------------------------------------------------------------
-constexpr int kScanWarps = 16;
-constexpr int kMaxCpb = 8;  // bands per scan warp (NB <= 128)
+constexpr int kScanWarps = 8;
+constexpr int kMaxCpb = 16;  // bands per scan warp (NB <= 128)
 
 template <int K>
 __global__ void __launch_bounds__(32 * kScanWarps) colscan_kernel(const float *__restrict__ T,
@@ -858,7 +881,17 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   {
     Launch g(K_COL_CARRY, st);
     dim3 grid((unsigned)cdiv(p.W, kColThreads), (unsigned)p.NB);
-    colcarry_kernel<K><<<grid, kColThreads, 0, st>>>(T, ldt, p, Z);
+    CUtensorMap cmap;
+    memset(&cmap, 0, sizeof(cmap));
+    int ctma = make_tmap_2d_f32(&cmap, T, p.H, p.W, ldt, kColThreads, kBand) && !getenv("VMF_NO_TMA");
+    cudaGetLastError();
+    const int csm = kBand * kColThreads * (int)sizeof(float) + 128;
+    static bool cattr = false;
+    if (!cattr) {
+      cudaFuncSetAttribute(colcarry_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
+      cattr = true;
+    }
+    colcarry_kernel<K><<<grid, kColThreads, csm, st>>>(T, ldt, p, Z, cmap, ctma);
   }
   {
     Launch g(K_COL_SCAN, st);
