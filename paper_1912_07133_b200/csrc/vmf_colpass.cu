@@ -49,205 +49,239 @@ __device__ __forceinline__ double ldT(const float *T, int64_t ldt, int64_t r, in
 // ---------------------------------------------------------------------------
 // 1. band carries: zero-state end histories of every (band, column)
 // ---------------------------------------------------------------------------
-// Z layout (coalesced along columns): Z[((b * 2 + dir) * K + i) * W + col]
-__device__ __forceinline__ int64_t zidx(int b, int dir, int i, int K, int64_t W, int64_t col) {
-  return ((int64_t)(b * 2 + dir) * K + i) * W + col;
+// Band records, contiguous over bands for one (column, direction) so the
+// band scan reads and writes them coalesced:
+//   Z + ((col * 2 + dir) * NB + b) * 2K:  [0, K) zero-state end history of the
+//   band (replaced by the band's true START history by the scan), [K, 2K) the
+//   band's edge samples in scan order (fwd: x(r1-1-i), bwd: x(r0+i)).
+__device__ __forceinline__ int64_t zrec(int64_t col, int dir, int b, int NB, int K) {
+  return ((col * 2 + dir) * NB + b) * 2 * K;
 }
 
 // f_i = sum_t h(len-1-i-t) x_t, g_i = sum_t h(t-i) x_t over the band.  With
 // u = x_t + x_t', v = x_t - x_t' (t' = len-1-t): f = P + Q, g = P - Q, so a
 // pair of samples costs 2 adds + 2K FMAs instead of 4K FMAs.  The pair
 // weights of a full band are compile-time-indexed kernel parameters.
+// One CTA = 32 columns x 4 consecutive bands (256 rows), 256 threads: thread
+// (band q, half h, column j) takes half of the 32 sample pairs of band q for
+// column j.  Four consecutive bands of a column make one contiguous run of
+// records, so the record writes are coalesced too.
+constexpr int kCarryCols = 32;
+constexpr int kCarryBands = 4;
+constexpr int kCarryThreads = kCarryCols * kCarryBands * 2;
+
 template <int K>
-__global__ void __launch_bounds__(kColThreads) colcarry_kernel(
+__global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
     const float *__restrict__ T, int64_t ldt, ColParams p, double *__restrict__ Z,
     const __grid_constant__ CUtensorMap tmap, int use_tma) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float *tile = reinterpret_cast<float *>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
   __shared__ __align__(8) uint64_t tbar;
-  const int b = blockIdx.y;
-  const int len = b == p.NB - 1 ? p.Blast : kBand;
-  const int64_t c0 = (int64_t)blockIdx.x * kColThreads;
-  const int64_t col = c0 + threadIdx.x;
-  const int64_t r0 = (int64_t)b * kBand;
-  const bool full = len == kBand && r0 + kBand <= p.H;
-  const bool tma = use_tma && full && c0 + kColThreads <= p.W;
-  if (tma) {  // the whole 64 x 128 band tile in one TMA box
+  __shared__ double part[kCarryBands][2 * K][kCarryCols];
+  const int j = threadIdx.x & (kCarryCols - 1);
+  const int half = (threadIdx.x >> 5) & 1;
+  const int q = threadIdx.x >> 6;  // band within the group
+  const int b = blockIdx.y * kCarryBands + q;
+  const int64_t c0 = (int64_t)blockIdx.x * kCarryCols;
+  const int64_t col = c0 + j;
+  const int64_t g0 = (int64_t)blockIdx.y * kCarryBands * kBand;  // first row of the group
+  const bool tma = use_tma && blockIdx.y * kCarryBands + kCarryBands <= p.NB - 1 &&
+                   g0 + kCarryBands * kBand <= p.H && c0 + kCarryCols <= p.W;
+  if (tma) {  // the whole 256 x 32 tile in one TMA box
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
-      mbar_expect_tx(&tbar, (unsigned)(kBand * kColThreads * sizeof(float)));
-      tma_load_2d(tile, &tmap, &tbar, (int)c0, (int)r0);
+      mbar_expect_tx(&tbar, (unsigned)(kCarryBands * kBand * kCarryCols * sizeof(float)));
+      tma_load_2d(tile, &tmap, &tbar, (int)c0, (int)g0);
     }
     __syncthreads();
     mbar_wait(&tbar, 0);
   }
-  if (col >= p.W) return;
-  double P[2][K], Q[2][K];  // two partial sums each for ILP
+  const bool live = col < p.W && b < p.NB;
+  const int len = b == p.NB - 1 ? p.Blast : kBand;
+  const int64_t r0 = (int64_t)b * kBand;
+  const bool full = live && len == kBand && r0 + kBand <= p.H;
+  double P[K], Q[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) P[0][i] = P[1][i] = Q[0][i] = Q[1][i] = 0.0;
+  for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
   if (full) {
-    float xa[kBand / 2], xb[kBand / 2];
+    constexpr int kHalf = kBand / 4;  // pairs per thread
+    const int t0 = half * kHalf;
+    float xa[kHalf], xb[kHalf];
     if (tma) {
+      const float *tq = tile + q * kBand * kCarryCols + j;
 #pragma unroll
-      for (int t = 0; t < kBand / 2; ++t) {
-        xa[t] = tile[t * kColThreads + threadIdx.x];
-        xb[t] = tile[(kBand - 1 - t) * kColThreads + threadIdx.x];
+      for (int t = 0; t < kHalf; ++t) {
+        xa[t] = tq[(t0 + t) * kCarryCols];
+        xb[t] = tq[(kBand - 1 - t0 - t) * kCarryCols];
       }
     } else {
       const float *src = T + r0 * ldt + col;
 #pragma unroll
-      for (int t = 0; t < kBand / 2; ++t) {  // all loads in flight at once
-        xa[t] = __ldg(src + t * ldt);
-        xb[t] = __ldg(src + (kBand - 1 - t) * ldt);
+      for (int t = 0; t < kHalf; ++t) {
+        xa[t] = __ldg(src + (t0 + t) * ldt);
+        xb[t] = __ldg(src + (kBand - 1 - t0 - t) * ldt);
       }
     }
 #pragma unroll
-    for (int t = 0; t < kBand / 2; ++t) {
+    for (int t = 0; t < kHalf; ++t) {
       double a = xa[t], c = xb[t];
       double u = a + c, v = a - c;
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        P[t & 1][i] = fma(p.SP[i][t], u, P[t & 1][i]);
-        Q[t & 1][i] = fma(p.SQ[i][t], v, Q[t & 1][i]);
+        P[i] = fma(p.SP[i][t0 + t], u, P[i]);
+        Q[i] = fma(p.SQ[i][t0 + t], v, Q[i]);
       }
     }
-  } else {  // last (short or padded) band: direct weights
+  } else if (live && half == 0) {  // last (short or padded) band: direct weights
     for (int t = 0; t < len; ++t) {
       double x = ldT(T, ldt, r0 + t, p.H, col);
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         int qa = len - 1 - i - t, qb = t - i;
-        if (qa > 0) P[0][i] = fma(p.h[qa], x, P[0][i]);
-        if (qb > 0) Q[0][i] = fma(p.h[qb], x, Q[0][i]);
+        if (qa > 0) P[i] = fma(p.h[qa], x, P[i]);
+        if (qb > 0) Q[i] = fma(p.h[qb], x, Q[i]);
       }
     }
-    // convert (f, g) into the (P, Q) convention: f = P + Q, g = P - Q
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      double f = P[0][i], g = Q[0][i];
-      P[0][i] = 0.5 * (f + g);
-      Q[0][i] = 0.5 * (f - g);
+    for (int i = 0; i < K; ++i) {  // (f, g) -> (P, Q): f = P + Q, g = P - Q
+      double f = P[i], g = Q[i];
+      P[i] = 0.5 * (f + g);
+      Q[i] = 0.5 * (f - g);
     }
   }
+  if (half == 1) {
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const double Pt = P[0][i] + P[1][i], Qt = Q[0][i] + Q[1][i];
-    Z[zidx(b, 0, i, K, p.W, col)] = Pt + Qt;
-    Z[zidx(b, 1, i, K, p.W, col)] = Pt - Qt;
+    for (int i = 0; i < K; ++i) {
+      part[q][i][j] = P[i];
+      part[q][K + i][j] = Q[i];
+    }
+  }
+  __syncthreads();
+  if (half == 0 && live) {
+    double *zf = Z + zrec(col, 0, b, p.NB, K), *zb = Z + zrec(col, 1, b, p.NB, K);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const double Pt = P[i] + part[q][i][j], Qt = Q[i] + part[q][K + i][j];
+      zf[i] = Pt + Qt;
+      zb[i] = Pt - Qt;
+      zf[K + i] = ldT(T, ldt, r0 + len - 1 - i, p.H, col);
+      zb[K + i] = ldT(T, ldt, r0 + i, p.H, col);
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// 2. band scan.  CTA = 32 columns (lanes, coalesced) x kScanWarps warps; warp
-//    g owns a contiguous group of bands in scan order: local aggregate (zero
-//    start), exclusive combination of the earlier groups' aggregates with
-//    TyB^cpb, then a re-scan from the true carry-in.  Writes the START history
-//    of every band in place: fwd slot b = y+(r0-1 .. r0-K), bwd slot b =
-//    y-(r1 .. r1+K-1).
+// 2. band scan: one warp per (column, direction), lane l owns bands
+//    [l cpl, (l+1) cpl) in scan order; local scan, Kogge-Stone over lanes with
+//    TyB^(cpl 2^j), re-scan from the carry-in.  Records of one (column, dir)
+//    are contiguous, so every access is coalesced.  Writes the START history
+//    of every band in place: fwd = y+(r0-1 .. r0-K), bwd = y-(r1 .. r1+K-1).
 // ---------------------------------------------------------------------------
-constexpr int kScanWarps = 8;
-constexpr int kMaxCpb = 16;  // bands per scan warp (NB <= 128)
-
 template <int K>
-__global__ void __launch_bounds__(32 * kScanWarps) colscan_kernel(const float *__restrict__ T,
-                                                                  int64_t ldt, ColParams p,
-                                                                  double *__restrict__ Z) {
-  __shared__ double agg[kScanWarps][K][32];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t col = (int64_t)blockIdx.x * 32 + lane;
-  const int dir = blockIdx.y;
-  const int NB = p.NB, cpb = p.cpb;
-  const bool live = col < p.W;
-  const int64_t cc = live ? col : p.W - 1;
-  const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, cc);
-  // d for scan position sp (band b): Yzs + TxB X_prev (+ TyB E_init first)
-  auto dval = [&](int sp, double *d) {
-    const int b = dir == 0 ? sp : NB - 1 - sp;
-    const int tb = b == NB - 1 ? 1 : 0;
-    double X[K];
+__global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ T, int64_t ldt,
+                                                      ColParams p, double *__restrict__ Z) {
+  const int lane = threadIdx.x & 31;
+  const int64_t task = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (task >= 2 * p.W) return;
+  const int64_t col = task >> 1;
+  const int dir = (int)(task & 1);
+  const int NB = p.NB, cpl = p.cpl;
+  const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, col);
+  double *recs = Z + zrec(col, dir, 0, NB, K);
+  auto rec = [&](int sp) {  // record of scan position sp (bands bottom-up backward)
+    return recs + (int64_t)(dir == 0 ? sp : NB - 1 - sp) * 2 * K;
+  };
+  double dl[kMaxCpl][K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      if (sp == 0)
-        X[i] = xe;
-      else if (dir == 0)
-        X[i] = ldT(T, ldt, (int64_t)b * kBand - 1 - i, p.H, cc);
-      else
-        X[i] = ldT(T, ldt, (int64_t)(b + 1) * kBand + i, p.H, cc);
-    }
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      double acc = Z[zidx(b, dir, i, K, p.W, cc)];
-#pragma unroll
-      for (int m = 0; m < K; ++m) acc = fma(p.TxB[tb][i * K + m], X[m], acc);
+  for (int q = 0; q < kMaxCpl; ++q) {  // d_sp = Yzs + TxB X_prev (+ TyB E_init first)
+    const int sp = lane * cpl + q;
+    if (q < cpl && sp < NB) {
+      const double *r = rec(sp);
+      const int b = dir == 0 ? sp : NB - 1 - sp;
+      const int tb = b == NB - 1 ? 1 : 0;
+      double X[K];
       if (sp == 0) {
 #pragma unroll
-        for (int m = 0; m < K; ++m) acc = fma(p.TyB[tb][i * K + m], p.yss * xe, acc);
+        for (int i = 0; i < K; ++i) X[i] = xe;
+      } else {
+        const double *pr = rec(sp - 1);
+#pragma unroll
+        for (int i = 0; i < K; ++i) X[i] = pr[K + i];
       }
-      d[i] = acc;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double acc = r[i];
+#pragma unroll
+        for (int m = 0; m < K; ++m) acc = fma(p.TxB[tb][i * K + m], X[m], acc);
+        if (sp == 0) {
+#pragma unroll
+          for (int m = 0; m < K; ++m) acc = fma(p.TyB[tb][i * K + m], p.yss * xe, acc);
+        }
+        dl[q][i] = acc;
+      }
     }
-  };
-  auto step = [&](const double *TyM, double *E, const double *d) {
-    double En[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      double acc = d[i];
-#pragma unroll
-      for (int m = 0; m < K; ++m) acc = fma(TyM[i * K + m], E[m], acc);
-      En[i] = acc;
-    }
-#pragma unroll
-    for (int i = 0; i < K; ++i) E[i] = En[i];
-  };
-  const int s0 = g * cpb, s1 = min(s0 + cpb, NB);
-  // the transfer over a band: band lengths differ only for band NB-1, which
-  // is crossed first in the backward scan and last (never needed) forward
-  const double *TyF = p.TyB[0];
-  double dv[kMaxCpb][K];  // every load of the group issued up front
-#pragma unroll
-  for (int q = 0; q < kMaxCpb; ++q)
-    if (s0 + q < s1) dval(s0 + q, dv[q]);
+  }
   double A[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) A[i] = 0.0;
 #pragma unroll
-  for (int q = 0; q < kMaxCpb; ++q)
-    if (s0 + q < s1) step(TyF, A, dv[q]);
+  for (int q = 0; q < kMaxCpl; ++q) {
+    if (q < cpl && lane * cpl + q < NB) {
+      double An[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) agg[g][i][lane] = A[i];
-  __syncthreads();
-  // carry-in: E = sum_{h < g} TyB^(cpb (g-1-h)) A_h, composed in order
-  double E[K];
+      for (int i = 0; i < K; ++i) {
+        double acc = dl[q][i];
 #pragma unroll
-  for (int i = 0; i < K; ++i) E[i] = 0.0;
-  for (int h = 0; h < g; ++h) {
-    double Ah[K];
+        for (int m = 0; m < K; ++m) acc = fma(p.TyB[0][i * K + m], A[m], acc);
+        An[i] = acc;
+      }
 #pragma unroll
-    for (int i = 0; i < K; ++i) Ah[i] = agg[h][i][lane];
-    if (h == 0) {
-#pragma unroll
-      for (int i = 0; i < K; ++i) E[i] = Ah[i];
-    } else {
-      step(p.TyBc, E, Ah);
+      for (int i = 0; i < K; ++i) A[i] = An[i];
     }
   }
-  if (g == 0) {
 #pragma unroll
-    for (int i = 0; i < K; ++i) E[i] = p.yss * xe;  // exclusive start of the first band
+  for (int lv = 0; lv < 5; ++lv) {
+    const int o = 1 << lv;
+    double B[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) B[i] = __shfl_up_sync(0xffffffffu, A[i], o);
+    if (lane >= o) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double acc = A[i];
+#pragma unroll
+        for (int m = 0; m < K; ++m) acc = fma(p.TyBp[lv][i * K + m], B[m], acc);
+        A[i] = acc;
+      }
+    }
+  }
+  double E[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double v = __shfl_up_sync(0xffffffffu, A[i], 1);
+    E[i] = lane ? v : p.yss * xe;
   }
 #pragma unroll
-  for (int q = 0; q < kMaxCpb; ++q) {
-    const int sp = s0 + q;
-    if (sp < s1) {
-      const int b = dir == 0 ? sp : NB - 1 - sp;
-      if (live) {
+  for (int q = 0; q < kMaxCpl; ++q) {
+    const int sp = lane * cpl + q;
+    if (q < cpl && sp < NB) {
+      double *r = rec(sp);
 #pragma unroll
-        for (int i = 0; i < K; ++i) Z[zidx(b, dir, i, K, p.W, cc)] = E[i];
-      }
+      for (int i = 0; i < K; ++i) r[i] = E[i];
       if (sp == 0) {
 #pragma unroll
-        for (int i = 0; i < K; ++i) E[i] = dv[q][i];
+        for (int i = 0; i < K; ++i) E[i] = dl[q][i];
       } else {
-        step(TyF, E, dv[q]);
+        double En[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          double acc = dl[q][i];
+#pragma unroll
+          for (int m = 0; m < K; ++m) acc = fma(p.TyB[0][i * K + m], E[m], acc);
+          En[i] = acc;
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) E[i] = En[i];
       }
     }
   }
@@ -360,10 +394,13 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   if (j < (kColThreads / 32) * 2 * (kBand / kSub + 1)) (&S.eflag[0][0][0])[j] = 0u;
   const float gbound = __uint_as_float(st->absmax_bits);  // global max so far (lower bound)
   double Ybot[K], Yf[K];
+  {
+    const double *zf = Z + zrec(colc, 0, b, p.NB, K), *zb = Z + zrec(colc, 1, b, p.NB, K);
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    Ybot[i] = Z[zidx(b, 1, i, K, p.W, colc)];
-    Yf[i] = Z[zidx(b, 0, i, K, p.W, colc)];
+    for (int i = 0; i < K; ++i) {
+      Ybot[i] = zb[i];
+      Yf[i] = zf[i];
+    }
   }
   if (tma) {
     __syncthreads();  // barrier initialised before anyone waits on it
@@ -834,7 +871,7 @@ static void impulse_ld(const double *b, const double *a, int k, int n, double *h
 
 bool colpass_supported(int64_t h, int64_t w, int k) {
   return k >= 2 && k <= 4 && h >= 2 * kSub && w >= 1 &&
-         cdiv(cdiv(h, kSub) * kSub, kBand) <= kScanWarps * kMaxCpb;
+         cdiv(cdiv(h, kSub) * kSub, kBand) <= 32 * kMaxCpl;
 }
 
 static void col_geometry(int64_t h, int64_t *Hp, int *NB, int *Blast) {
@@ -856,7 +893,7 @@ size_t colpass_workspace_bytes(int64_t h, int64_t w, int k, int64_t) {
   int NB, Bl;
   col_geometry(h, &Hp, &NB, &Bl);
   int64_t gcap = cand_capacity(h, w);
-  size_t z = (size_t)NB * 2 * k * w * sizeof(double);
+  size_t z = (size_t)NB * 2 * 2 * k * w * sizeof(double);
   return 4096 + ((z + 255) & ~(size_t)255) + (size_t)gcap * 12 + 1024 +
          detect_workspace_bytes(1, h, w);
 }
@@ -868,7 +905,7 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   CandState *cs = (CandState *)base;
   int *fallback = (int *)(base + 64);
-  size_t z = (size_t)p.NB * 2 * K * p.W * sizeof(double);
+  size_t z = (size_t)p.NB * 2 * 2 * K * p.W * sizeof(double);
   double *Z = (double *)(base + 4096);
   char *q = base + 4096 + ((z + 255) & ~(size_t)255);
   int64_t gcap = cand_capacity(p.H, p.W);
@@ -880,23 +917,25 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   cudaMemsetAsync(cs, 0, 128, st);
   {
     Launch g(K_COL_CARRY, st);
-    dim3 grid((unsigned)cdiv(p.W, kColThreads), (unsigned)p.NB);
+    dim3 grid((unsigned)cdiv(p.W, kCarryCols), (unsigned)cdiv(p.NB, kCarryBands));
     CUtensorMap cmap;
     memset(&cmap, 0, sizeof(cmap));
-    int ctma = make_tmap_2d_f32(&cmap, T, p.H, p.W, ldt, kColThreads, kBand) && !getenv("VMF_NO_TMA");
+    int ctma = make_tmap_2d_f32(&cmap, T, p.H, p.W, ldt, kCarryCols, kCarryBands * kBand) &&
+               !getenv("VMF_NO_TMA");
     cudaGetLastError();
-    const int csm = kBand * kColThreads * (int)sizeof(float) + 128;
+    const int csm = kCarryBands * kBand * kCarryCols * (int)sizeof(float) + 128;
     static bool cattr = false;
     if (!cattr) {
       cudaFuncSetAttribute(colcarry_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
       cattr = true;
     }
-    colcarry_kernel<K><<<grid, kColThreads, csm, st>>>(T, ldt, p, Z, cmap, ctma);
+    colcarry_kernel<K><<<grid, kCarryThreads, csm, st>>>(T, ldt, p, Z, cmap, ctma);
   }
   {
     Launch g(K_COL_SCAN, st);
-    colscan_kernel<K><<<dim3((unsigned)cdiv(p.W, 32), 2), 32 * kScanWarps, 0, st>>>(T, ldt, p, Z);
+    colscan_kernel<K><<<(unsigned)cdiv(2 * p.W, 4), 128, 0, st>>>(T, ldt, p, Z);
   }
+
   {
     Launch g(K_IIR_COLS_FUSED, st);
     static bool attr = false;
@@ -961,11 +1000,7 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirPar
       p.SQ[i][t] = 0.5 * (A - B);
     }
   p.cpl = (p.NB + 31) / 32;
-  p.cpb = (p.NB + kScanWarps - 1) / kScanWarps;
-  {
-    double tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
-    transfer_ld(ip.b, ip.a, k, p.cpb * kBand, p.TyBc, tx);
-  }
+
   if (p.cpl > kMaxCpl) return fail(VMF_EVALUE, "image too tall for the fused column pass");
   for (int l = 0; l < 5; ++l) {
     double tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
