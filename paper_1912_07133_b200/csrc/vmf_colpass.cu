@@ -49,26 +49,20 @@ __device__ __forceinline__ double ldT(const float *T, int64_t ldt, int64_t r, in
 // ---------------------------------------------------------------------------
 // 1. band carries: zero-state end histories of every (band, column)
 // ---------------------------------------------------------------------------
-// Band records, contiguous over bands for one (column, direction) so the
-// band scan reads and writes them coalesced:
-//   Z + ((col * 2 + dir) * NB + b) * 2K:  [0, K) zero-state end history of the
-//   band (replaced by the band's true START history by the scan), [K, 2K) the
-//   band's edge samples in scan order (fwd: x(r1-1-i), bwd: x(r0+i)).
-__device__ __forceinline__ int64_t zrec(int64_t col, int dir, int b, int NB, int K) {
-  return ((col * 2 + dir) * NB + b) * 2 * K;
+// Band records, coalesced along columns:
+//   Z[((dir * NB + b) * 2K + i) * W + col], i in [0, K): zero-state end history
+//   of band b (replaced by its true START history by the scan); i in [K, 2K):
+//   the band's edge samples in scan order (fwd: x(r1-1-i), bwd: x(r0+i)).
+__device__ __forceinline__ int64_t zidx(int dir, int b, int i, int NB, int K, int64_t W,
+                                        int64_t col) {
+  return ((int64_t)(dir * NB + b) * 2 * K + i) * W + col;
 }
 
-// f_i = sum_t h(len-1-i-t) x_t, g_i = sum_t h(t-i) x_t over the band.  With
-// u = x_t + x_t', v = x_t - x_t' (t' = len-1-t): f = P + Q, g = P - Q, so a
-// pair of samples costs 2 adds + 2K FMAs instead of 4K FMAs.  The pair
-// weights of a full band are compile-time-indexed kernel parameters.
-// One CTA = 32 columns x 4 consecutive bands (256 rows), 256 threads: thread
-// (band q, half h, column j) takes half of the 32 sample pairs of band q for
-// column j.  Four consecutive bands of a column make one contiguous run of
-// records, so the record writes are coalesced too.
-constexpr int kCarryCols = 32;
-constexpr int kCarryBands = 4;
-constexpr int kCarryThreads = kCarryCols * kCarryBands * 2;
+// One CTA = 128 columns x one 64-row band (one TMA box), 256 threads:
+// threads j and j + 128 take the two halves of the band's 32 sample pairs of
+// column j; records are written coalesced along columns.
+constexpr int kCarryCols = kColThreads;
+constexpr int kCarryThreads = 2 * kCarryCols;
 
 template <int K>
 __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
@@ -77,42 +71,37 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float *tile = reinterpret_cast<float *>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
   __shared__ __align__(8) uint64_t tbar;
-  __shared__ double part[kCarryBands][2 * K][kCarryCols];
-  const int j = threadIdx.x & (kCarryCols - 1);
-  const int half = (threadIdx.x >> 5) & 1;
-  const int q = threadIdx.x >> 6;  // band within the group
-  const int b = blockIdx.y * kCarryBands + q;
+  __shared__ double part[2 * K][kCarryCols];
+  const int j = threadIdx.x & (kCarryCols - 1), half = threadIdx.x >> 7;
+  const int b = blockIdx.y;
+  const int len = b == p.NB - 1 ? p.Blast : kBand;
   const int64_t c0 = (int64_t)blockIdx.x * kCarryCols;
   const int64_t col = c0 + j;
-  const int64_t g0 = (int64_t)blockIdx.y * kCarryBands * kBand;  // first row of the group
-  const bool tma = use_tma && blockIdx.y * kCarryBands + kCarryBands <= p.NB - 1 &&
-                   g0 + kCarryBands * kBand <= p.H && c0 + kCarryCols <= p.W;
-  if (tma) {  // the whole 256 x 32 tile in one TMA box
+  const int64_t r0 = (int64_t)b * kBand;
+  const bool full = len == kBand && r0 + kBand <= p.H;
+  const bool tma = use_tma && full && c0 + kCarryCols <= p.W;
+  if (tma) {
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
-      mbar_expect_tx(&tbar, (unsigned)(kCarryBands * kBand * kCarryCols * sizeof(float)));
-      tma_load_2d(tile, &tmap, &tbar, (int)c0, (int)g0);
+      mbar_expect_tx(&tbar, (unsigned)(kBand * kCarryCols * sizeof(float)));
+      tma_load_2d(tile, &tmap, &tbar, (int)c0, (int)r0);
     }
     __syncthreads();
     mbar_wait(&tbar, 0);
   }
-  const bool live = col < p.W && b < p.NB;
-  const int len = b == p.NB - 1 ? p.Blast : kBand;
-  const int64_t r0 = (int64_t)b * kBand;
-  const bool full = live && len == kBand && r0 + kBand <= p.H;
+  const bool live = col < p.W;
   double P[K], Q[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
-  if (full) {
+  if (live && full) {
     constexpr int kHalf = kBand / 4;  // pairs per thread
     const int t0 = half * kHalf;
     float xa[kHalf], xb[kHalf];
     if (tma) {
-      const float *tq = tile + q * kBand * kCarryCols + j;
 #pragma unroll
       for (int t = 0; t < kHalf; ++t) {
-        xa[t] = tq[(t0 + t) * kCarryCols];
-        xb[t] = tq[(kBand - 1 - t0 - t) * kCarryCols];
+        xa[t] = tile[(t0 + t) * kCarryCols + j];
+        xb[t] = tile[(kBand - 1 - t0 - t) * kCarryCols + j];
       }
     } else {
       const float *src = T + r0 * ldt + col;
@@ -152,45 +141,62 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
   if (half == 1) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      part[q][i][j] = P[i];
-      part[q][K + i][j] = Q[i];
+      part[i][j] = P[i];
+      part[K + i][j] = Q[i];
     }
   }
   __syncthreads();
   if (half == 0 && live) {
-    double *zf = Z + zrec(col, 0, b, p.NB, K), *zb = Z + zrec(col, 1, b, p.NB, K);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      const double Pt = P[i] + part[q][i][j], Qt = Q[i] + part[q][K + i][j];
-      zf[i] = Pt + Qt;
-      zb[i] = Pt - Qt;
-      zf[K + i] = ldT(T, ldt, r0 + len - 1 - i, p.H, col);
-      zb[K + i] = ldT(T, ldt, r0 + i, p.H, col);
+      const double Pt = P[i] + part[i][j], Qt = Q[i] + part[K + i][j];
+      Z[zidx(0, b, i, p.NB, K, p.W, col)] = Pt + Qt;
+      Z[zidx(1, b, i, p.NB, K, p.W, col)] = Pt - Qt;
+      double ef, eb;
+      if (tma) {  // edge rows are in the staged tile
+        ef = (double)tile[(kBand - 1 - i) * kCarryCols + j];
+        eb = (double)tile[i * kCarryCols + j];
+      } else {
+        ef = ldT(T, ldt, r0 + len - 1 - i, p.H, col);
+        eb = ldT(T, ldt, r0 + i, p.H, col);
+      }
+      Z[zidx(0, b, K + i, p.NB, K, p.W, col)] = ef;
+      Z[zidx(1, b, K + i, p.NB, K, p.W, col)] = eb;
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// 2. band scan: one warp per (column, direction), lane l owns bands
-//    [l cpl, (l+1) cpl) in scan order; local scan, Kogge-Stone over lanes with
-//    TyB^(cpl 2^j), re-scan from the carry-in.  Records of one (column, dir)
-//    are contiguous, so every access is coalesced.  Writes the START history
-//    of every band in place: fwd = y+(r0-1 .. r0-K), bwd = y-(r1 .. r1+K-1).
+// 2. band scan.  CTA = one direction x 16 columns: the records of all bands
+//    are staged in shared memory with coalesced loads, then warp w scans
+//    column w with lanes over bands (cpl bands per lane, Kogge-Stone with
+//    TyB^(cpl 2^j)), and the true START histories go back coalesced:
+//    fwd = y+(r0-1 .. r0-K), bwd = y-(r1 .. r1+K-1).
 // ---------------------------------------------------------------------------
+constexpr int kScanCols = 16;
+
 template <int K>
-__global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ T, int64_t ldt,
-                                                      ColParams p, double *__restrict__ Z) {
-  const int lane = threadIdx.x & 31;
-  const int64_t task = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (task >= 2 * p.W) return;
-  const int64_t col = task >> 1;
-  const int dir = (int)(task & 1);
+__global__ void __launch_bounds__(32 * kScanCols) colscan_kernel(const float *__restrict__ T,
+                                                                 int64_t ldt, ColParams p,
+                                                                 double *__restrict__ Z) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int NB = p.NB, cpl = p.cpl;
+  const int stride = 2 * K * kScanCols + 1;  // doubles per band row (+1 breaks bank aliasing)
+  double *sz = reinterpret_cast<double *>(smem_raw);  // [NB][2K][kScanCols] (+pad)
+  const int dir = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * kScanCols;
+  // coalesced staging: element e = (b, i, c)
+  for (int e = threadIdx.x; e < NB * 2 * K * kScanCols; e += blockDim.x) {
+    const int c = e % kScanCols, bi = e / kScanCols;
+    const int i = bi % (2 * K), b = bi / (2 * K);
+    const int64_t col = c0 + c < p.W ? c0 + c : p.W - 1;
+    sz[b * stride + i * kScanCols + c] = Z[zidx(dir, b, i, NB, K, p.W, col)];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  const int64_t col = c0 + c < p.W ? c0 + c : p.W - 1;
   const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, col);
-  double *recs = Z + zrec(col, dir, 0, NB, K);
-  auto rec = [&](int sp) {  // record of scan position sp (bands bottom-up backward)
-    return recs + (int64_t)(dir == 0 ? sp : NB - 1 - sp) * 2 * K;
-  };
+  auto rec = [&](int sp) { return sz + (dir == 0 ? sp : NB - 1 - sp) * stride + c; };
   double dl[kMaxCpl][K];
 #pragma unroll
   for (int q = 0; q < kMaxCpl; ++q) {  // d_sp = Yzs + TxB X_prev (+ TyB E_init first)
@@ -206,11 +212,11 @@ __global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ 
       } else {
         const double *pr = rec(sp - 1);
 #pragma unroll
-        for (int i = 0; i < K; ++i) X[i] = pr[K + i];
+        for (int i = 0; i < K; ++i) X[i] = pr[(K + i) * kScanCols];
       }
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        double acc = r[i];
+        double acc = r[i * kScanCols];
 #pragma unroll
         for (int m = 0; m < K; ++m) acc = fma(p.TxB[tb][i * K + m], X[m], acc);
         if (sp == 0) {
@@ -261,13 +267,14 @@ __global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ 
     double v = __shfl_up_sync(0xffffffffu, A[i], 1);
     E[i] = lane ? v : p.yss * xe;
   }
+  __syncthreads();  // every warp has read its inputs before results overwrite them
 #pragma unroll
   for (int q = 0; q < kMaxCpl; ++q) {
     const int sp = lane * cpl + q;
     if (q < cpl && sp < NB) {
       double *r = rec(sp);
 #pragma unroll
-      for (int i = 0; i < K; ++i) r[i] = E[i];
+      for (int i = 0; i < K; ++i) r[i * kScanCols] = E[i];
       if (sp == 0) {
 #pragma unroll
         for (int i = 0; i < K; ++i) E[i] = dl[q][i];
@@ -284,6 +291,12 @@ __global__ void __launch_bounds__(128) colscan_kernel(const float *__restrict__ 
         for (int i = 0; i < K; ++i) E[i] = En[i];
       }
     }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NB * K * kScanCols; e += blockDim.x) {
+    const int cc = e % kScanCols, bi = e / kScanCols;
+    const int i = bi % K, b = bi / K;
+    if (c0 + cc < p.W) Z[zidx(dir, b, i, NB, K, p.W, c0 + cc)] = sz[b * stride + i * kScanCols + cc];
   }
 }
 
@@ -394,13 +407,10 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   if (j < (kColThreads / 32) * 2 * (kBand / kSub + 1)) (&S.eflag[0][0][0])[j] = 0u;
   const float gbound = __uint_as_float(st->absmax_bits);  // global max so far (lower bound)
   double Ybot[K], Yf[K];
-  {
-    const double *zf = Z + zrec(colc, 0, b, p.NB, K), *zb = Z + zrec(colc, 1, b, p.NB, K);
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      Ybot[i] = zb[i];
-      Yf[i] = zf[i];
-    }
+  for (int i = 0; i < K; ++i) {
+    Ybot[i] = Z[zidx(1, b, i, p.NB, K, p.W, colc)];
+    Yf[i] = Z[zidx(0, b, i, p.NB, K, p.W, colc)];
   }
   if (tma) {
     __syncthreads();  // barrier initialised before anyone waits on it
@@ -917,13 +927,13 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   cudaMemsetAsync(cs, 0, 128, st);
   {
     Launch g(K_COL_CARRY, st);
-    dim3 grid((unsigned)cdiv(p.W, kCarryCols), (unsigned)cdiv(p.NB, kCarryBands));
+    dim3 grid((unsigned)cdiv(p.W, kCarryCols), (unsigned)p.NB);
     CUtensorMap cmap;
     memset(&cmap, 0, sizeof(cmap));
-    int ctma = make_tmap_2d_f32(&cmap, T, p.H, p.W, ldt, kCarryCols, kCarryBands * kBand) &&
+    int ctma = make_tmap_2d_f32(&cmap, T, p.H, p.W, ldt, kCarryCols, kBand) &&
                !getenv("VMF_NO_TMA");
     cudaGetLastError();
-    const int csm = kCarryBands * kBand * kCarryCols * (int)sizeof(float) + 128;
+    const int csm = kBand * kCarryCols * (int)sizeof(float) + 128;
     static bool cattr = false;
     if (!cattr) {
       cudaFuncSetAttribute(colcarry_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
@@ -933,7 +943,15 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   }
   {
     Launch g(K_COL_SCAN, st);
-    colscan_kernel<K><<<(unsigned)cdiv(2 * p.W, 4), 128, 0, st>>>(T, ldt, p, Z);
+    const int ssm = (int)((size_t)p.NB * (2 * K * kScanCols + 1) * sizeof(double));
+    static bool sattr = false;
+    if (!sattr) {
+      cudaFuncSetAttribute(colscan_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      sattr = true;
+    }
+    colscan_kernel<K><<<dim3((unsigned)cdiv(p.W, kScanCols), 2), 32 * kScanCols, ssm, st>>>(
+        T, ldt, p, Z);
   }
 
   {

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
   float *xs = reinterpret_cast<float *>(smem_raw);
   double *cf = reinterpret_cast<double *>(smem_raw + (size_t)R * rowf * sizeof(float));
   double *cb = cf + (size_t)R * C * K;
+
   const int tid = threadIdx.x;
   const int rr = tid / C, c = tid % C;
   const int64_t row0 = (int64_t)blockIdx.x * R;
@@ -78,26 +79,35 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
   float *xr = xs + rr * rowf;
   const int n0 = c * kChunk;
 
-  // ---- b. zero-state carries ----------------------------------------------
+  // ---- b. zero-state carries (folded sample pairs) -------------------------
   if (active) {
-    double f[K], g[K];
+    double P[K], Q[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) f[i] = g[i] = 0.0;
+    for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
     const float4 *v4 = reinterpret_cast<const float4 *>(xr + sidx(n0));
+    double xv[kChunk];
 #pragma unroll
     for (int q = 0; q < kChunk / 4; ++q) {
       float4 v = v4[q];
-      float e[4] = {v.x, v.y, v.z, v.w};
+      xv[4 * q] = v.x;
+      xv[4 * q + 1] = v.y;
+      xv[4 * q + 2] = v.z;
+      xv[4 * q + 3] = v.w;
+    }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int t = 4 * q + u;
-        double xv = (double)e[u];
+    for (int t = 0; t < kChunk / 2; ++t) {
+      const double u = xv[t] + xv[kChunk - 1 - t], v = xv[t] - xv[kChunk - 1 - t];
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          if (kChunk - 1 - i - t > 0) f[i] = fma(p.h[kChunk - 1 - i - t], xv, f[i]);
-          if (t - i > 0) g[i] = fma(p.h[t - i], xv, g[i]);
-        }
+      for (int i = 0; i < K; ++i) {
+        P[i] = fma(p.SP32[i][t], u, P[i]);
+        Q[i] = fma(p.SQ32[i][t], v, Q[i]);
       }
+    }
+    double f[K], g[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      f[i] = P[i] + Q[i];
+      g[i] = P[i] - Q[i];
     }
     // scan inputs d_c = Yzs_c + Tx X_{c-1} (x history before the chunk in
     // scan order; the steady state of the end sample for the first chunk,
@@ -400,6 +410,13 @@ void rowpass_plan(RowParams *p, const IirParams &ip, int64_t h, int64_t w) {
   // powers are computed directly in long double (no repeated squaring).
   for (int j = 0; j < 5; ++j)
     dfi_transfer_y(ip.b, ip.a, k, (p->cpl << j) * (int)kChunk, p->Tpow[j]);
+  for (int i = 0; i < k && i < VMF_MAX_IIR_ORDER; ++i)
+    for (int t = 0; t < kChunk / 2; ++t) {
+      int qa = kChunk - 1 - i - t, qb = t - i;
+      double A = qa > 0 ? p->h[qa] : 0.0, B = qb > 0 ? p->h[qb] : 0.0;
+      p->SP32[i][t] = 0.5 * (A + B);
+      p->SQ32[i][t] = 0.5 * (A - B);
+    }
   int r = kRowThreads / p->C;
   if (r < 1) r = 1;
   while (r > 1 && (int64_t)r * p->C * kChunk * 5 / 4 * 4 > kRowTileBytes) --r;

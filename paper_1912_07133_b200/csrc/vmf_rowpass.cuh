@@ -17,6 +17,7 @@ struct RowParams {
   double Ty[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // DF-I history transfer over 32 samples
   double Tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
   double Tpow[5][VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // Ty^(cpl*2^j)
+  double SP32[VMF_MAX_IIR_ORDER][kChunk / 2], SQ32[VMF_MAX_IIR_ORDER][kChunk / 2];  // folded
   int64_t H, W;
   int C, R, cpl;
   int vec4;
