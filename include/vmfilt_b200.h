@@ -145,12 +145,17 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w,
 /* Launch accounting / in-situ kernel timing (used by bench.py).
  * vmf_launch_count: kernels launched by this library since load.
  * vmf_profile_begin: start bracketing every launch with CUDA events on its
- * stream.  vmf_profile_end: wait for them and write, per kernel id,
- * the summed duration (ms) and launch count; returns the number of ids. */
+ * stream (record nodes when the stream is being captured into a graph).
+ * vmf_profile_stop: stop bracketing new launches.  vmf_profile_read: wait
+ * for the recorded events and write, per kernel id, the summed duration (ms)
+ * and launch count (the latest replay for graph-captured launches); returns
+ * the number of ids.  vmf_profile_end = stop + read. */
 long long vmf_launch_count(void);
 int vmf_num_kernel_ids(void);
 const char *vmf_kernel_name(int id);
 void vmf_profile_begin(void);
+void vmf_profile_stop(void);
+int vmf_profile_read(double *ms, long long *counts, int n);
 int vmf_profile_end(double *ms, long long *counts, int n);
 
 #ifdef __cplusplus

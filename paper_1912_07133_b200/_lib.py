@@ -59,6 +59,8 @@ _PROTOS = {
     "vmf_num_kernel_ids": (C.c_int, []),
     "vmf_kernel_name": (C.c_char_p, [C.c_int]),
     "vmf_profile_begin": (None, []),
+    "vmf_profile_stop": (None, []),
+    "vmf_profile_read": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int]),
     "vmf_profile_end": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int]),
     "vmf_blur_lap_detect_workspace_bytes": (_sz, [_i64, _i64, C.POINTER(VmfStage),
                                                   C.POINTER(VmfStage)]),
@@ -110,6 +112,20 @@ def launch_count() -> int:
 
 def profile_begin() -> None:
     lib().vmf_profile_begin()
+
+
+def profile_stop() -> None:
+    lib().vmf_profile_stop()
+
+
+def profile_read() -> dict:
+    """-> {kernel name: (total_ms, launches)} of the recorded launches."""
+    L = lib()
+    n = L.vmf_num_kernel_ids()
+    ms = (C.c_double * n)()
+    cnt = (C.c_longlong * n)()
+    L.vmf_profile_read(ms, cnt, n)
+    return {L.vmf_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(n) if cnt[i]}
 
 
 def profile_end() -> dict:

@@ -325,7 +325,7 @@ __device__ __forceinline__ void push2(double *Y, double y, double *X, double x) 
 }
 
 constexpr int kTileRows(int k) { return kBand + 2 * k; }
-constexpr int kEbRows = kBand + 2;  // B of rows r0-1 .. r1
+constexpr int kEbRows = kBand + 4;  // B of rows r0-2 .. r1+1
 // The TMA box must start at a 16-byte aligned column, so the tile spans 4
 // more columns than the CTA computes: tile column j + 2 <-> thread j.
 constexpr int kTileStride = kColThreads + 4;
@@ -339,7 +339,6 @@ struct ColSmem {
   double eb[kColThreads / 32][4][kEbRows];  // B of lanes 0,1,30,31 per warp
   int cy[kCandSmem], cx[kCandSmem];
   float cv[kCandSmem];
-  unsigned int eflag[kColThreads / 32][2][kBand / kSub + 1];  // edge-column row flags
   int ccount;
   int coverflow;
   unsigned int cmax;  // max |L| of this CTA (float bits)
@@ -350,10 +349,12 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, ColParams p,
     const double *__restrict__ Z, CandState *__restrict__ st, int *__restrict__ gy,
     int *__restrict__ gx, float *__restrict__ gv, int gcap,
-    const __grid_constant__ CUtensorMap tmap, int use_tma) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // 128-byte aligned base: the tile is a TMA destination
-  ColSmem<K> &S = *reinterpret_cast<ColSmem<K> *>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+    const __grid_constant__ CUtensorMap tmap, int use_tma, int vec_out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // 128-byte aligned base (the tile is a TMA destination), derived from the
+  // shared array itself so every access stays an LDS / STS
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
+  ColSmem<K> &S = *reinterpret_cast<ColSmem<K> *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
   const int j = threadIdx.x, lane = j & 31, wid = j >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * kColOut;
   const int64_t col = c0 - kColHalo + j;
@@ -365,7 +366,6 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   const int nsub = len / kSub;
   const int64_t H = p.H;
   const bool own_col = j >= kColHalo && j < kColThreads - kColHalo && col < p.W;
-  const bool edge = lane == 0 || lane == 31;  // warp-edge lanes: Lx patched after the walk
   const int eslot = lane == 0 ? 0 : (lane == 1 ? 1 : (lane == 30 ? 2 : (lane == 31 ? 3 : -1)));
   const int64_t rown_hi = r1 < H ? r1 : H;  // owned rows [r0, rown_hi)
 
@@ -404,7 +404,6 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     S.coverflow = 0;
     S.cmax = 0u;
   }
-  if (j < (kColThreads / 32) * 2 * (kBand / kSub + 1)) (&S.eflag[0][0][0])[j] = 0u;
   const float gbound = __uint_as_float(st->absmax_bits);  // global max so far (lower bound)
   double Ybot[K], Yf[K];
 #pragma unroll
@@ -453,16 +452,17 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   for (int i = 0; i < K; ++i) Xf[i] = TX(K - 1 - i);  // rows r0-1-i (clamped at the top)
   const double lsc = (double)p.lap_scale;
   double Bm2 = 0.0, Bm1 = 0.0, Lxm1 = 0.0;  // sliding state (rows r-2, r-1)
-  float tmax = 0.0f;                          // this thread's running max |L|
-  // owned rows over the threshold: maskN bit t <-> band row 32 N + t - 1
-  unsigned int mask0 = 0u, mask1 = 0u, mask2 = 0u;
-  const bool own_w = own_col && !edge;                  // writes L from the walk
-  auto lx_of = [&](double bc) {  // Lx by lane shuffles; warp-edge lanes patched later
+  auto lx_of = [&](double bc) {  // Lx by lane shuffles; warp-edge lanes recomputed later
     double bl = __shfl_up_sync(0xffffffffu, bc, 1);
     double br = __shfl_down_sync(0xffffffffu, bc, 1);
     return (bl - 2.0 * bc) + br;
   };
+  // lanes 0, 1, 30, 31 keep B(r0-2 .. r1+1) for the warp-edge recomputation
+  const bool keep_b = eslot >= 0;
+  double *ebw = &S.eb[wid][keep_b ? eslot : 0][0];  // B(r0 - 2 + q) at ebw[q]
 
+  // The walk leaves L(r0-1 .. r1) in the tile (in place of x); lanes 0 / 31
+  // hold placeholders until the recomputation below.
   for (int s = 0; s < nsub; ++s) {
     const int64_t rb = r0 + (int64_t)s * kSub;
     const int trb = K + s * kSub;  // tile row of rb
@@ -490,75 +490,47 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         Bm1 = fma(p.sign, ym1, fma(p.b0, x1, Yf[0]));
         Bm2 = fma(p.sign, ym2, fma(p.b0, x2, Yf[1]));
         Lxm1 = lx_of(Bm1);
-        if (edge) Lxm1 = 0.0;
-        if (eslot >= 0) S.eb[wid][eslot][0] = Bm1;
+        if (keep_b) {
+          ebw[0] = Bm2;
+          ebw[1] = Bm1;
+        }
       }
     }
-    const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
-    const float th = p.frac * fmaxf(wmax, gbound);  // lower bound of the final threshold
-    unsigned int m = 0u;                             // bit t: owned row rb+t-1 flagged
-    const float *xp = tcol + trb * kTileStride;      // x(rb + t) at xp[t * stride]
-    float *lp = tcol + (trb - 1) * kTileStride;      // L(rb + t - 1) at lp[t * stride]
-    float *gp = Lout + (rb - 1) * ldl + col;         // global L(rb - 1)
-    double *ep = &S.eb[wid][eslot < 0 ? 0 : eslot][trb - K + 1];  // B(rb + t) at ep[t]
+    float *lp = tcol + (trb - 1) * kTileStride;  // L(rb + t - 1) at lp[t * stride]
+    double *ep = ebw + 2 + s * kSub;              // B(rb + t) at ep[t]
     // forward run: B(rb+t); L(rb+t-1) = Lx + Ly as soon as B(rb+t) exists
-    if (rb >= 1 && rb + kSub < H) {
-      // no image edge in reach: L rows rb-1 .. rb+30 are all in range; row
-      // rb-1 is owned unless it belongs to the band above (s == 0)
-      const bool own0 = own_w && s > 0;
+    if (rb >= 1 && rb + kSub < H) {  // no image edge in reach
 #pragma unroll
       for (int t = 0; t < kSub; ++t) {
-        double xv = (double)xp[t * kTileStride];
+        double xv = TX(trb + t);
         double y = dfi<K>(p, Xf, Yf);
         double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
         push2<K>(Yf, y, Xf, xv);
         double lx = lx_of(Bt);
-        const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + Bt)));
-        lp[t * kTileStride] = v;
-        if (t == 0 ? own0 : own_w) {
-          *gp = v;
-          const float av = fabsf(v);
-          tmax = fmaxf(tmax, av);
-          m |= (av >= th ? 1u : 0u) << t;
-        }
-        gp += ldl;
-        if (eslot >= 0) ep[t] = Bt;
+        lp[t * kTileStride] = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + Bt)));
+        if (keep_b) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
-        Lxm1 = edge ? 0.0 : lx;
+        Lxm1 = lx;
       }
     } else {
 #pragma unroll
       for (int t = 0; t < kSub; ++t) {
         const int64_t r = rb + t;
-        double xv = (double)xp[t * kTileStride];
+        double xv = TX(trb + t);
         double y = dfi<K>(p, Xf, Yf);
         double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
         push2<K>(Yf, y, Xf, xv);
         if (r == 0) Bm1 = Bt;  // replicate top edge: B(-1) = B(0)
         double lx = lx_of(Bt);
         const double bnext = r >= H ? Bm1 : Bt;  // replicate bottom edge
-        if (r >= 1) {
-          const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + bnext)));
-          lp[t * kTileStride] = v;
-          if (own_w && r - 1 >= r0 && r - 1 < rown_hi) {
-            *gp = v;
-            const float av = fabsf(v);
-            tmax = fmaxf(tmax, av);
-            m |= (av >= th ? 1u : 0u) << t;
-          }
-        }
-        gp += ldl;
-        if (eslot >= 0) ep[t] = Bt;
+        if (r >= 1) lp[t * kTileStride] = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + bnext)));
+        if (keep_b) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
-        Lxm1 = edge ? 0.0 : lx;
+        Lxm1 = lx;
       }
     }
-    if (s == 0)
-      mask0 |= m;
-    else
-      mask1 |= m;
     if (last) {  // B at rows r1, r1+1 -> L(r1-1), L(r1)
       const int tr1 = K + len;
       double xr1 = TX(tr1), xr2 = TX(tr1 + 1);
@@ -568,88 +540,83 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
       double B1 = fma(p.sign, Ybot[0], fma(p.b0, xr1, y0));
       double B2 = fma(p.sign, Ybot[1], fma(p.b0, xr2, y1));
       const double lx1 = lx_of(B1);
-      if (r1 - 1 < H) {
-        const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + (r1 >= H ? Bm1 : B1))));
-        tcol[(tr1 - 1) * kTileStride] = v;
-        if (own_w) {
-          Lout[(r1 - 1) * ldl + col] = v;
-          const float av = fabsf(v);
-          tmax = fmaxf(tmax, av);
-          const unsigned bit = av >= p.frac * fmaxf(tmax, gbound) ? 1u : 0u;  // row len-1
-          if (nsub == 1)
-            mask1 |= bit;
-          else
-            mask2 |= bit;
-        }
+      if (r1 - 1 < H)
+        tcol[(tr1 - 1) * kTileStride] =
+            (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + (r1 >= H ? Bm1 : B1))));
+      if (r1 < H)
+        tcol[tr1 * kTileStride] = (float)(lsc * (lx1 + ((Bm1 - 2.0 * B1) + (r1 + 1 >= H ? B1 : B2))));
+      if (keep_b) {
+        ebw[len + 2] = B1;
+        ebw[len + 3] = B2;
       }
-      if (r1 < H) {
-        const float v = (float)(lsc * ((edge ? 0.0 : lx1) +
-                                       ((Bm1 - 2.0 * B1) + (r1 + 1 >= H ? B1 : B2))));
-        tcol[tr1 * kTileStride] = v;
-      }
-      if (eslot >= 0) S.eb[wid][eslot][kEbRows - 1] = B1;
     }
   }
 #undef TX
   __syncthreads();
 
-  // ---- patch Lx of the warp-edge columns (lanes 0 / 31) -------------------
-  // The 2 x (len+2) patches of a warp are spread over its 32 lanes.
+  // ---- warp-edge columns (lanes 0 / 31): L recomputed from the kept B ------
+  // The 2 x (rows) recomputations of a warp are spread over its 32 lanes; the
+  // arithmetic is the walk's, so every column gets bit-identical formulas.
   {
     const int64_t rlo = r0 > 0 ? r0 - 1 : 0;
     const int64_t rhi = r1 < H ? r1 : H - 1;
     const int nr = (int)(rhi - rlo + 1);
-    const float th = p.frac * fmaxf(tmax, gbound);
     for (int idx = lane; idx < 2 * nr; idx += 32) {
       const int side = idx & 1;
       const int64_t r = rlo + (idx >> 1);
       const int jj = wid * 32 + (side ? 31 : 0);
       if (jj == 0 || jj == kColThreads - 1) continue;  // CTA halo columns
-      const int q = (int)(r - r0 + 1);
-      double bl, bc, br;
-      if (side == 0) {
-        bl = S.eb[wid - 1][3][q];
-        bc = S.eb[wid][0][q];
-        br = S.eb[wid][1][q];
-      } else {
-        bl = S.eb[wid][2][q];
-        bc = S.eb[wid][3][q];
-        br = S.eb[wid + 1][0][q];
-      }
-      const int tr = (int)(r - r0 + K);
-      const float v = S.tile[tr][jj + 2] + (float)(lsc * ((bl - 2.0 * bc) + br));
-      S.tile[tr][jj + 2] = v;
-      const int64_t cj = c0 - kColHalo + jj;
-      if (cj < p.W && r >= r0 && r < rown_hi) {
-        Lout[r * ldl + cj] = v;
-        tmax = fmaxf(tmax, fabsf(v));
-        if (fabsf(v) >= th) atomicOr(&S.eflag[wid][side][q >> 5], 1u << (q & 31));
-      }
+      const int q = (int)(r - r0 + 2);
+      const int qu = (int)((r > 0 ? r - 1 : 0) - r0 + 2);
+      const int qd = (int)((r + 1 < H ? r + 1 : H - 1) - r0 + 2);
+      const double *bcv = side ? S.eb[wid][3] : S.eb[wid][0];
+      const double bl = side ? S.eb[wid][2][q] : S.eb[wid - 1][3][q];
+      const double br = side ? S.eb[wid + 1][0][q] : S.eb[wid][1][q];
+      const double bc = bcv[q];
+      const double lx = (bl - 2.0 * bc) + br;
+      S.tile[r - r0 + K][jj + 2] = (float)(lsc * (lx + ((bcv[qu] - 2.0 * bc) + bcv[qd])));
     }
   }
-  atomicMax(&S.cmax, __float_as_uint(tmax));
   __syncthreads();
-  if (lane == 0 || lane == 31) {  // edge columns: flags gathered by the patch
-    const int side = lane == 31;
-    mask0 |= S.eflag[wid][side][0];
-    mask1 |= S.eflag[wid][side][1];
-    mask2 |= S.eflag[wid][side][2];
-  }
 
-  // ---- strict 3x3 extrema among the flagged rows ----------------------------
+  // ---- store the owned L block (rows r0 .. r1-1, columns c0 .. c0+123) ----
+  // and this CTA's max |L|
+  float tmax = 0.0f;
+  {
+    const int nrow = (int)(rown_hi - r0);
+    const int ncol = (int)(p.W - c0 < kColOut ? p.W - c0 : kColOut);
+    if (vec_out && ncol == kColOut) {  // 31 float4 per row, one row per warp
+      if (lane < kColOut / 4) {
+        float *dst = Lout + r0 * ldl + c0 + 4 * lane;
+        for (int q = wid; q < nrow; q += kColThreads / 32) {
+          const float4 v = *reinterpret_cast<const float4 *>(&S.tile[q + K][4 + 4 * lane]);
+          *reinterpret_cast<float4 *>(dst + q * ldl) = v;
+          tmax = fmaxf(tmax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+      }
+    } else {
+      for (int q = wid; q < nrow; q += kColThreads / 32)
+        for (int c = lane; c < ncol; c += 32) {
+          const float v = S.tile[q + K][4 + c];
+          Lout[(r0 + q) * ldl + c0 + c] = v;
+          tmax = fmaxf(tmax, fabsf(v));
+        }
+    }
+    tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+    if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
+  }
+  __syncthreads();
+
+  // ---- strict 3x3 extrema over the threshold known so far ------------------
   const float thr = p.frac * fmaxf(__uint_as_float(S.cmax), gbound);
   if (own_col && col >= 1 && col <= p.W - 2) {
-    for (int w = 0; w <= kBand / kSub; ++w) {
-      unsigned int mk = w == 0 ? mask0 : (w == 1 ? mask1 : mask2);
-      while (mk) {
-      const int q = 32 * w + __ffs((int)mk) - 2;
-      mk &= mk - 1;
-      const int64_t r = r0 + q;
-      if (q < 0) continue;
-      if (r < 1 || r > H - 2) continue;
-      const int tr = (int)(r - (r0 - K));
+    const int qlo = r0 >= 1 ? 0 : 1;
+    const int qhi = (int)((rown_hi < H - 1 ? rown_hi : H - 1) - r0);  // rows r0+q <= H-2
+    for (int q = qlo; q < qhi; ++q) {
+      const int tr = q + K;
       const float v = S.tile[tr][j + 2];
       if (!(fabsf(v) >= thr)) continue;
+      const int64_t r = r0 + q;
       bool gt = true, lt = true;
 #pragma unroll
       for (int di = -1; di <= 1; ++di)
@@ -670,7 +637,6 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
           S.coverflow = 1;
         }
       }
-    }
     }
   }
   __syncthreads();
@@ -969,7 +935,8 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
                   !getenv("VMF_NO_TMA");
     cudaGetLastError();
     colapply_kernel<K><<<grid, kColThreads, sizeof(ColSmem<K>) + 128, st>>>(
-        T, ldt, L, ldl, p, Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma);
+        T, ldt, L, ldl, p, Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
+        (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
   }
   {
     Launch g(K_FINALIZE, st);

@@ -34,6 +34,16 @@ cudaEvent_t get_event() {
   cudaEventCreate(&e);
   return e;
 }
+// Inside a stream capture the event becomes a record node of the graph, so a
+// replayed graph is timed launch by launch without host gaps.
+void record(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, st);
+}
 }  // namespace
 
 Launch::Launch(KernelId id, cudaStream_t st) : slot_(-1), st_(st) {
@@ -41,7 +51,7 @@ Launch::Launch(KernelId id, cudaStream_t st) : slot_(-1), st_(st) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_on) return;
   Rec r{(int)id, get_event(), get_event()};
-  cudaEventRecord(r.a, st);
+  record(r.a, st);
   g_recs.push_back(r);
   slot_ = (int)g_recs.size() - 1;
 }
@@ -49,7 +59,7 @@ Launch::Launch(KernelId id, cudaStream_t st) : slot_(-1), st_(st) {
 Launch::~Launch() {
   if (slot_ < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);
-  cudaEventRecord(g_recs[slot_].b, st_);
+  record(g_recs[slot_].b, st_);
 }
 
 }  // namespace vmf
@@ -74,10 +84,14 @@ void vmf_profile_begin(void) {
   vmf::g_on = true;
 }
 
-// Waits for the recorded events; ms[id] += duration, counts[id] += 1.
-int vmf_profile_end(double *ms, long long *counts, int n) {
+void vmf_profile_stop(void) {
   std::lock_guard<std::mutex> lk(vmf::g_mu);
   vmf::g_on = false;
+}
+
+// Waits for the recorded events; ms[id] = summed duration, counts[id] = launches.
+int vmf_profile_read(double *ms, long long *counts, int n) {
+  std::lock_guard<std::mutex> lk(vmf::g_mu);
   for (int i = 0; i < n; ++i) {
     ms[i] = 0.0;
     counts[i] = 0;
@@ -85,13 +99,21 @@ int vmf_profile_end(double *ms, long long *counts, int n) {
   for (auto &r : vmf::g_recs) {
     cudaEventSynchronize(r.b);
     float t = 0.0f;
-    cudaEventElapsedTime(&t, r.a, r.b);
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
     if (r.id < n) {
       ms[r.id] += t;
       counts[r.id] += 1;
     }
   }
   return vmf::K_NUM_IDS;
+}
+
+int vmf_profile_end(double *ms, long long *counts, int n) {
+  vmf_profile_stop();
+  return vmf_profile_read(ms, counts, n);
 }
 
 }  // extern "C"
