@@ -580,50 +580,25 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   __syncthreads();
 
   // ---- store the owned L block (rows r0 .. r1-1, columns c0 .. c0+123) ----
-  // and this CTA's max |L|
-  float tmax = 0.0f;
+  // fused with the strict 3x3 NMS: a warp walks rows, and a pixel is tested
+  // when |L| reaches frac * (running max of the rows seen so far, or the
+  // global max published so far) -- a lower bound of the final threshold, so
+  // the candidates are a superset that the flush and the finaliser filter.
   {
     const int nrow = (int)(rown_hi - r0);
     const int ncol = (int)(p.W - c0 < kColOut ? p.W - c0 : kColOut);
-    if (vec_out && ncol == kColOut) {  // 31 float4 per row, one row per warp
-      if (lane < kColOut / 4) {
-        float *dst = Lout + r0 * ldl + c0 + 4 * lane;
-        for (int q = wid; q < nrow; q += kColThreads / 32) {
-          const float4 v = *reinterpret_cast<const float4 *>(&S.tile[q + K][4 + 4 * lane]);
-          *reinterpret_cast<float4 *>(dst + q * ldl) = v;
-          tmax = fmaxf(tmax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-        }
-      }
-    } else {
-      for (int q = wid; q < nrow; q += kColThreads / 32)
-        for (int c = lane; c < ncol; c += 32) {
-          const float v = S.tile[q + K][4 + c];
-          Lout[(r0 + q) * ldl + c0 + c] = v;
-          tmax = fmaxf(tmax, fabsf(v));
-        }
-    }
-    tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
-    if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
-  }
-  __syncthreads();
-
-  // ---- strict 3x3 extrema over the threshold known so far ------------------
-  const float thr = p.frac * fmaxf(__uint_as_float(S.cmax), gbound);
-  if (own_col && col >= 1 && col <= p.W - 2) {
-    const int qlo = r0 >= 1 ? 0 : 1;
-    const int qhi = (int)((rown_hi < H - 1 ? rown_hi : H - 1) - r0);  // rows r0+q <= H-2
-    for (int q = qlo; q < qhi; ++q) {
-      const int tr = q + K;
-      const float v = S.tile[tr][j + 2];
-      if (!(fabsf(v) >= thr)) continue;
-      const int64_t r = r0 + q;
+    float wrun = gbound;
+    auto test = [&](int q, int c, float v) {  // tile row q + K, tile column 4 + c
+      const int64_t r = r0 + q, cc = c0 + c;
+      if (r < 1 || r > H - 2 || cc < 1 || cc > p.W - 2) return;
+      const int tr = q + K, tc = 4 + c;
       bool gt = true, lt = true;
 #pragma unroll
       for (int di = -1; di <= 1; ++di)
 #pragma unroll
         for (int dj = -1; dj <= 1; ++dj) {
           if (!di && !dj) continue;
-          const float u = S.tile[tr + di][j + 2 + dj];
+          const float u = S.tile[tr + di][tc + dj];
           gt &= v > u;
           lt &= v < u;
         }
@@ -631,13 +606,47 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         int k = atomicAdd(&S.ccount, 1);
         if (k < kCandSmem) {
           S.cy[k] = (int)r;
-          S.cx[k] = (int)col;
+          S.cx[k] = (int)cc;
           S.cv[k] = v;
         } else {
           S.coverflow = 1;
         }
       }
+    };
+    if (vec_out && ncol == kColOut) {  // 31 float4 per row, one row per warp
+      const bool act = lane < kColOut / 4;
+      float *dst = Lout + r0 * ldl + c0 + 4 * lane;
+      for (int q = wid; q < nrow; q += kColThreads / 32) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (act) {
+          v = *reinterpret_cast<const float4 *>(&S.tile[q + K][4 + 4 * lane]);
+          *reinterpret_cast<float4 *>(dst + q * ldl) = v;
+        }
+        const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+        wrun = fmaxf(wrun, __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m4))));
+        const float th = p.frac * wrun;
+        if (m4 >= th) {
+          if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
+          if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
+          if (fabsf(v.z) >= th) test(q, 4 * lane + 2, v.z);
+          if (fabsf(v.w) >= th) test(q, 4 * lane + 3, v.w);
+        }
+      }
+    } else {
+      for (int q = wid; q < nrow; q += kColThreads / 32)
+        for (int cl = 0; cl < ncol; cl += 32) {
+          const int c = cl + lane;
+          float v = 0.0f;
+          if (c < ncol) {
+            v = S.tile[q + K][4 + c];
+            Lout[(r0 + q) * ldl + c0 + c] = v;
+          }
+          const float av = fabsf(v);
+          wrun = fmaxf(wrun, __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(av))));
+          if (c < ncol && av >= p.frac * wrun) test(q, c, v);
+        }
     }
+    if (lane == 0) atomicMax(&S.cmax, __float_as_uint(wrun));
   }
   __syncthreads();
 
