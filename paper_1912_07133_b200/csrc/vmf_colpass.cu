@@ -64,12 +64,49 @@ __device__ __forceinline__ int64_t zidx(int dir, int b, int i, int NB, int K, in
 constexpr int kCarryCols = kColThreads;
 constexpr int kCarryThreads = 2 * kCarryCols;
 
+// Folded zero-state sums of one half of a full band (pairs t0 .. t0+15 of
+// rows (t, 63-t)), from the staged tile or straight from global memory.
+template <int K, int HALF>
+__device__ __forceinline__ void carry_half(const ColParams &p, const float *tile, bool tma,
+                                           const float *src, int64_t ldt, int j, double *P,
+                                           double *Q) {
+  constexpr int kHalf = kBand / 4;  // pairs per thread
+  constexpr int t0 = HALF * kHalf;
+  float xa[kHalf], xb[kHalf];
+  if (tma) {
+#pragma unroll
+    for (int t = 0; t < kHalf; ++t) {
+      xa[t] = tile[(t0 + t) * kCarryCols + j];
+      xb[t] = tile[(kBand - 1 - t0 - t) * kCarryCols + j];
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < kHalf; ++t) {
+      xa[t] = __ldg(src + (t0 + t) * ldt);
+      xb[t] = __ldg(src + (kBand - 1 - t0 - t) * ldt);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kHalf; ++t) {
+    double a = xa[t], c = xb[t];
+    double u = a + c, v = a - c;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      P[i] = fma(p.SP[i][t0 + t], u, P[i]);
+      Q[i] = fma(p.SQ[i][t0 + t], v, Q[i]);
+    }
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
     const float *__restrict__ T, int64_t ldt, ColParams p, double *__restrict__ Z,
     const __grid_constant__ CUtensorMap tmap, int use_tma) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float *tile = reinterpret_cast<float *>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // 128-byte aligned TMA destination, derived from the shared array itself so
+  // the reads stay LDS
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
+  float *tile = reinterpret_cast<float *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
   __shared__ __align__(8) uint64_t tbar;
   __shared__ double part[2 * K][kCarryCols];
   const int j = threadIdx.x & (kCarryCols - 1), half = threadIdx.x >> 7;
@@ -94,33 +131,12 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
 #pragma unroll
   for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
   if (live && full) {
-    constexpr int kHalf = kBand / 4;  // pairs per thread
-    const int t0 = half * kHalf;
-    float xa[kHalf], xb[kHalf];
-    if (tma) {
-#pragma unroll
-      for (int t = 0; t < kHalf; ++t) {
-        xa[t] = tile[(t0 + t) * kCarryCols + j];
-        xb[t] = tile[(kBand - 1 - t0 - t) * kCarryCols + j];
-      }
-    } else {
-      const float *src = T + r0 * ldt + col;
-#pragma unroll
-      for (int t = 0; t < kHalf; ++t) {
-        xa[t] = __ldg(src + (t0 + t) * ldt);
-        xb[t] = __ldg(src + (kBand - 1 - t0 - t) * ldt);
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < kHalf; ++t) {
-      double a = xa[t], c = xb[t];
-      double u = a + c, v = a - c;
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        P[i] = fma(p.SP[i][t0 + t], u, P[i]);
-        Q[i] = fma(p.SQ[i][t0 + t], v, Q[i]);
-      }
-    }
+    // warp-uniform split so the weight indices are compile-time (the
+    // coefficients stay constant-bank operands of the DFMAs)
+    if (half == 0)
+      carry_half<K, 0>(p, tile, tma, T + r0 * ldt + col, ldt, j, P, Q);
+    else
+      carry_half<K, 1>(p, tile, tma, T + r0 * ldt + col, ldt, j, P, Q);
   } else if (live && half == 0) {  // last (short or padded) band: direct weights
     for (int t = 0; t < len; ++t) {
       double x = ldT(T, ldt, r0 + t, p.H, col);
@@ -173,24 +189,40 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
 //    TyB^(cpl 2^j)), and the true START histories go back coalesced:
 //    fwd = y+(r0-1 .. r0-K), bwd = y-(r1 .. r1+K-1).
 // ---------------------------------------------------------------------------
-constexpr int kScanCols = 16;
+constexpr int kScanCols = 4;
 
 template <int K>
-__global__ void __launch_bounds__(32 * kScanCols) colscan_kernel(const float *__restrict__ T,
+__global__ void __launch_bounds__(32 * kScanCols, 48 / kScanCols) colscan_kernel(const float *__restrict__ T,
                                                                  int64_t ldt, ColParams p,
                                                                  double *__restrict__ Z) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int NB = p.NB, cpl = p.cpl;
-  const int stride = 2 * K * kScanCols + 1;  // doubles per band row (+1 breaks bank aliasing)
+  const int stride = 2 * K * kScanCols + 2;  // doubles per band row (+2: 16-byte aligned rows)
   double *sz = reinterpret_cast<double *>(smem_raw);  // [NB][2K][kScanCols] (+pad)
   const int dir = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * kScanCols;
-  // coalesced staging: element e = (b, i, c)
-  for (int e = threadIdx.x; e < NB * 2 * K * kScanCols; e += blockDim.x) {
-    const int c = e % kScanCols, bi = e / kScanCols;
-    const int i = bi % (2 * K), b = bi / (2 * K);
-    const int64_t col = c0 + c < p.W ? c0 + c : p.W - 1;
-    sz[b * stride + i * kScanCols + c] = Z[zidx(dir, b, i, NB, K, p.W, col)];
+  // staging with asynchronous 16-byte copies (two columns each), all in
+  // flight at once: element pair e = (b, i, c/2)
+  {
+    constexpr int kPairs = kScanCols / 2;
+    const bool full = c0 + kScanCols <= p.W && p.W % 2 == 0;
+    for (int e = threadIdx.x; e < NB * 2 * K * kPairs; e += blockDim.x) {
+      const int c = 2 * (e % kPairs), bi = e / kPairs;
+      const int i = bi % (2 * K), b = bi / (2 * K);
+      double *dst = sz + b * stride + i * kScanCols + c;
+      if (full) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                     "l"(Z + zidx(dir, b, i, NB, K, p.W, c0 + c)));
+      } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t col = c0 + c + u < p.W ? c0 + c + u : p.W - 1;
+          dst[u] = Z[zidx(dir, b, i, NB, K, p.W, col)];
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
@@ -918,7 +950,7 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   }
   {
     Launch g(K_COL_SCAN, st);
-    const int ssm = (int)((size_t)p.NB * (2 * K * kScanCols + 1) * sizeof(double));
+    const int ssm = (int)((size_t)p.NB * (2 * K * kScanCols + 2) * sizeof(double));
     static bool sattr = false;
     if (!sattr) {
       cudaFuncSetAttribute(colscan_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
