@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
       mbar_expect_tx(&tbar, (unsigned)(kBand * kCarryCols * sizeof(float)));
-      tma_load_2d(tile, &tmap, &tbar, (int)c0, (int)r0);
+      tma_load_2d_hint(tile, &tmap, &tbar, (int)c0, (int)r0, l2_policy_evict_last());
     }
     __syncthreads();
     mbar_wait(&tbar, 0);
@@ -410,7 +410,8 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     if (j == 0) {
       mbar_init(&tbar, 1);
       mbar_expect_tx(&tbar, (unsigned)(kTileRows(K) * kTileStride * sizeof(float)));
-      tma_load_2d(&S.tile[0][0], &tmap, &tbar, (int)(c0 - 4), (int)(r0 - K));
+      tma_load_2d_hint(&S.tile[0][0], &tmap, &tbar, (int)(c0 - 4), (int)(r0 - K),
+                       l2_policy_evict_first());  // last use of T
     }
   } else {
     const int rows = len + 2 * K;
@@ -647,12 +648,13 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     };
     if (vec_out && ncol == kColOut) {  // 31 float4 per row, one row per warp
       const bool act = lane < kColOut / 4;
+      const uint64_t lpol = l2_policy_evict_first();  // L streams out
       float *dst = Lout + r0 * ldl + c0 + 4 * lane;
       for (int q = wid; q < nrow; q += kColThreads / 32) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (act) {
           v = *reinterpret_cast<const float4 *>(&S.tile[q + K][4 + 4 * lane]);
-          *reinterpret_cast<float4 *>(dst + q * ldl) = v;
+          st_v4_hint(dst + q * ldl, v, lpol);
         }
         const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
         wrun = fmaxf(wrun, __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m4))));

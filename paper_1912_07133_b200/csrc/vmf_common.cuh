@@ -27,6 +27,32 @@ int cuda_status(const char *what);  // VMF_OK or VMF_ECUDA after a launch
 __device__ __forceinline__ double ld64(const float *p) { return (double)__ldg(p); }
 __device__ __forceinline__ double ld64(const uint16_t *p) { return (double)__ldg(p); }
 
+// ---------------------------------------------------------------------------
+// device: L2 residency hints.  The intermediate T (row-pass output) is read
+// twice by the column pass, so it is written and first read with
+// evict_last; the frame X and the final L stream through with evict_first.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_v4_hint(float *addr, float4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(addr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16_hint(void *smem_dst, const void *src, uint64_t policy) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),
+               "l"(src), "l"(policy));
+}
+
 // Element n of line `line` for a pass along rows (line = row) or columns
 // (line = column).
 template <int O, typename T>

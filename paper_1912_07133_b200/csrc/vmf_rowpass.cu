@@ -58,12 +58,10 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
 
   // ---- a. load ------------------------------------------------------------
   if (sizeof(T) == 4 && p.vec4) {
+    const uint64_t pol = l2_policy_evict_first();  // the frame is read once
     for (int r = 0; r < nrows; ++r)
-      for (int n = 4 * tid; n < W; n += 4 * blockDim.x) {
-        const T *src = x + (row0 + r) * ldx + n;
-        unsigned sa = (unsigned)__cvta_generic_to_shared(xs + r * rowf + sidx(n));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
-      }
+      for (int n = 4 * tid; n < W; n += 4 * blockDim.x)
+        cp_async16_hint(xs + r * rowf + sidx(n), x + (row0 + r) * ldx + n, pol);
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
   } else {
     for (int r = 0; r < nrows; ++r)
@@ -306,10 +304,11 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
 
   // ---- e. store --------------------------------------------------------------
   if (p.vec4) {
+    const uint64_t pol = l2_policy_evict_last();  // T is read again by the column pass
     for (int r = 0; r < nrows; ++r)
       for (int n = 4 * tid; n < W; n += 4 * blockDim.x)
-        *reinterpret_cast<float4 *>(y + (row0 + r) * ldy + n) =
-            *reinterpret_cast<const float4 *>(xs + r * rowf + sidx(n));
+        st_v4_hint(y + (row0 + r) * ldy + n, *reinterpret_cast<const float4 *>(xs + r * rowf + sidx(n)),
+                   pol);
   } else {
     for (int r = 0; r < nrows; ++r)
       for (int n = tid; n < W; n += blockDim.x) y[(row0 + r) * ldy + n] = xs[r * rowf + sidx(n)];

@@ -37,6 +37,19 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
       : "memory");
 }
 
+// Same load with an L2 eviction-priority policy (see l2_policy_* in
+// vmf_common.cuh).
+__device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                                 int c, int r, uint64_t policy) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(r), "r"(b), "l"(policy)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   unsigned done = 0;
