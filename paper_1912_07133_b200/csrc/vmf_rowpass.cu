@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
 #pragma unroll
     for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
     const float4 *v4 = reinterpret_cast<const float4 *>(xr + sidx(n0));
-    double xv[kChunk];
+    float xv[kChunk];  // fp32 copies; the pair sums are formed in fp64
 #pragma unroll
     for (int q = 0; q < kChunk / 4; ++q) {
       float4 v = v4[q];
@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
     }
 #pragma unroll
     for (int t = 0; t < kChunk / 2; ++t) {
-      const double u = xv[t] + xv[kChunk - 1 - t], v = xv[t] - xv[kChunk - 1 - t];
+      const double xa = xv[t], xb = xv[kChunk - 1 - t];
+      const double u = xa + xb, v = xa - xb;
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         P[i] = fma(p.SP32[i][t], u, P[i]);

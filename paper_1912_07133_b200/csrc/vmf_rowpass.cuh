@@ -7,7 +7,7 @@ namespace vmf {
 constexpr int kChunk = 32;          // samples per thread (one chunk)
 constexpr int kRowThreads = 128;    // target threads per CTA (R rows x C chunks)
 constexpr int kRowMaxThreads = 256; // rows up to 8192 samples (C <= 256)
-constexpr int kRowMinBlocks = 2;    // with 256 threads -> <= 128 registers
+constexpr int kRowMinBlocks = 3;    // with 256 threads -> <= 85 registers
 constexpr int64_t kRowTileBytes = 40 * 1024;
 
 struct RowParams {
