@@ -24,22 +24,275 @@
 //                recursion writes out(n) in place of x(n).
 //   e. store   : coalesced copy of the R rows to the output.
 // fp64 state and accumulation throughout; fp32 in and out.
+#include <cstdlib>
 #include <cstring>
 
 #include "vmf_common.cuh"
 #include "vmf_iir.cuh"
 #include "vmf_prof.cuh"
 #include "vmf_rowpass.cuh"
+#include "vmf_tma.cuh"
 
 namespace vmf {
 
+// ---------------------------------------------------------------------------
+// shared-memory row layouts
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ int sidx(int n) { return n + 4 * (n >> 5); }
+
+// Padded layout (cp.async staging): a 4-float pad after every 32 samples, so
+// thread c reading chunk c with 16-byte loads is bank-conflict free.
+struct PadRow {
+  float *xr;
+  __device__ float4 ld4(int c, int q) const {
+    return *reinterpret_cast<const float4 *>(xr + 36 * c + 4 * q);
+  }
+  __device__ void st4(int c, int q, float4 v) const {
+    *reinterpret_cast<float4 *>(xr + 36 * c + 4 * q) = v;
+  }
+  __device__ float ld(int n) const { return xr[sidx(n)]; }
+};
+
+// TMA SWIZZLE_128B layout of a [C][32] fp32 box: 16-byte unit q of chunk c
+// sits at unit q ^ (c & 7) of the chunk's 128 bytes (1024-byte aligned base),
+// which is again conflict free for per-chunk 16-byte loads.
+struct SwzRow {
+  char *base;
+  __device__ int off(int c, int q) const { return c * 128 + ((q ^ (c & 7)) << 4); }
+  __device__ float4 ld4(int c, int q) const {
+    return *reinterpret_cast<const float4 *>(base + off(c, q));
+  }
+  __device__ void st4(int c, int q, float4 v) const {
+    *reinterpret_cast<float4 *>(base + off(c, q)) = v;
+  }
+  __device__ float ld(int n) const {
+    return *reinterpret_cast<const float *>(base + off(n >> 5, (n >> 2) & 7) + 4 * (n & 3));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// the three phases of one row (thread = chunk c of row rr)
+// ---------------------------------------------------------------------------
+// b. zero-state chunk carries (folded sample pairs) -> scan inputs d_c =
+//    Yzs_c + Tx X_{c-1} in cf / cb (x history before the chunk in scan
+//    order; the first chunk adds Ty E_{-1}, E_{-1} = yss * end sample).
+template <int K, class Row>
+__device__ __forceinline__ void row_carry(const RowParams &p, const Row &xr, int c, int C, int Wp,
+                                          double *cfr, double *cbr) {
+  double P[K], Q[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
+  float xv[kChunk];  // fp32 copies; the pair sums are formed in fp64
+#pragma unroll
+  for (int q = 0; q < kChunk / 4; ++q) {
+    float4 v = xr.ld4(c, q);
+    xv[4 * q] = v.x;
+    xv[4 * q + 1] = v.y;
+    xv[4 * q + 2] = v.z;
+    xv[4 * q + 3] = v.w;
+  }
+#pragma unroll
+  for (int t = 0; t < kChunk / 2; ++t) {
+    const double xa = xv[t], xb = xv[kChunk - 1 - t];
+    const double u = xa + xb, v = xa - xb;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      P[i] = fma(p.SP32[i][t], u, P[i]);
+      Q[i] = fma(p.SQ32[i][t], v, Q[i]);
+    }
+  }
+  const int n0 = c * kChunk;
+  double Xf[K], Xb[K];
+  const double x0 = (double)xr.ld(0), xl = (double)xr.ld(Wp - 1);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    Xf[i] = c > 0 ? (double)xr.ld(n0 - 1 - i) : x0;
+    Xb[i] = c < C - 1 ? (double)xr.ld(n0 + kChunk + i) : xl;
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double df = P[i] + Q[i], db = P[i] - Q[i];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      df = fma(p.Tx[i * K + j], Xf[j], df);
+      db = fma(p.Tx[i * K + j], Xb[j], db);
+    }
+    if (c == 0) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) df = fma(p.Ty[i * K + j], p.yss * x0, df);
+    }
+    if (c == C - 1) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) db = fma(p.Ty[i * K + j], p.yss * xl, db);
+    }
+    cfr[c * K + i] = df;
+    cbr[c * K + i] = db;
+  }
+}
+
+// c. scan of one (row, direction) by one warp: E_c = d_c + Ty E_{c-1}
+//    (c in scan order; the backward direction scans chunks from the right
+//    end).  Lane l owns cpl consecutive chunks: local sequential scan,
+//    Kogge-Stone across lanes with Ty^(cpl*2^j), then a sequential re-scan
+//    from the carry-in.  Leaves the END history of every chunk in cc.
+template <int K>
+__device__ __forceinline__ void row_scan(const RowParams &p, double *cc, int dir, int C, int lane) {
+  const int cpl = p.cpl;
+  const bool live = lane * cpl < C;
+  auto dval = [&](int sp, double *d) {
+    const int ch = dir == 0 ? sp : C - 1 - sp;
+#pragma unroll
+    for (int i = 0; i < K; ++i) d[i] = cc[ch * K + i];
+  };
+  double A[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) A[i] = 0.0;
+  if (live) {
+    for (int q = 0; q < cpl; ++q) {
+      double d[K], An[K];
+      dval(lane * cpl + q, d);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double acc = d[i];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fma(p.Ty[i * K + j], A[j], acc);
+        An[i] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) A[i] = An[i];
+    }
+  }
+  // inclusive Kogge-Stone over lanes: A_l += Ty^(cpl*o) A_{l-o}
+#pragma unroll
+  for (int lv = 0; lv < 5; ++lv) {
+    const int o = 1 << lv;
+    double B[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) B[i] = __shfl_up_sync(0xffffffffu, A[i], o);
+    if (lane >= o) {
+      const double *M = p.Tpow[lv];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double acc = A[i];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fma(M[i * K + j], B[j], acc);
+        A[i] = acc;
+      }
+    }
+  }
+  // carry-in = inclusive value of the previous lane
+  double E[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double v = __shfl_up_sync(0xffffffffu, A[i], 1);
+    E[i] = lane ? v : 0.0;
+  }
+  if (live) {
+    for (int q = 0; q < cpl; ++q) {
+      const int sp = lane * cpl + q;
+      const int ch = dir == 0 ? sp : C - 1 - sp;
+      double d[K], En[K];
+      dval(sp, d);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double acc = d[i];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fma(p.Ty[i * K + j], E[j], acc);
+        En[i] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        E[i] = En[i];
+        cc[ch * K + i] = En[i];
+      }
+    }
+  }
+}
+
+// d. apply, backward half: DF-I recursion from the true history, sign*y-
+//    parked in 32 fp32 registers (its rounding is smoothed away by the column
+//    pass, tools/experiments/park_precision.py); also returns the forward
+//    start history.  Reads only x.
+template <int K, class Row>
+__device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row &xr, int c, int C,
+                                              int Wp, const double *cfr, const double *cbr,
+                                              float *park, double *Xf, double *Yf) {
+  const int n0 = c * kChunk;
+  double Xb[K], Yb[K];
+  const double xl = (double)xr.ld(Wp - 1), x0 = (double)xr.ld(0);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    int qb = n0 + kChunk + i;
+    Xb[i] = (double)xr.ld(qb > Wp - 1 ? Wp - 1 : qb);
+    Yb[i] = c < C - 1 ? cbr[(c + 1) * K + i] : p.yss * xl;
+    int qf = n0 - 1 - i;
+    Xf[i] = (double)xr.ld(qf < 0 ? 0 : qf);
+    Yf[i] = c > 0 ? cfr[(c - 1) * K + i] : p.yss * x0;
+  }
+#pragma unroll
+  for (int q = kChunk / 4 - 1; q >= 0; --q) {
+    float4 v = xr.ld4(c, q);
+    float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 3; u >= 0; --u) {
+      double xv = (double)e[u];
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < K; ++m) s = fma(p.b[m], Xb[m], s);
+#pragma unroll
+      for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yb[m], s);
+      s = fma(-p.a[0], Yb[0], s);
+      park[4 * q + u] = (float)(p.sign * s);
+#pragma unroll
+      for (int m = K - 1; m > 0; --m) {
+        Yb[m] = Yb[m - 1];
+        Xb[m] = Xb[m - 1];
+      }
+      Yb[0] = s;
+      Xb[0] = xv;
+    }
+  }
+}
+
+// d. apply, forward half: out(n) = b0 x + y+ + parked sign*y-, in place.
+template <int K, class Row>
+__device__ __forceinline__ void row_apply_fwd(const RowParams &p, const Row &xr, int c,
+                                              const float *park, double *Xf, double *Yf) {
+#pragma unroll
+  for (int q = 0; q < kChunk / 4; ++q) {
+    float4 v = xr.ld4(c, q);
+    float e[4] = {v.x, v.y, v.z, v.w};
+    float o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double xv = (double)e[u];
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < K; ++m) s = fma(p.b[m], Xf[m], s);
+#pragma unroll
+      for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yf[m], s);
+      s = fma(-p.a[0], Yf[0], s);
+      o[u] = (float)(fma(p.b0, xv, s) + (double)park[4 * q + u]);
+#pragma unroll
+      for (int m = K - 1; m > 0; --m) {
+        Yf[m] = Yf[m - 1];
+        Xf[m] = Xf[m - 1];
+      }
+      Yf[0] = s;
+      Xf[0] = xv;
+    }
+    xr.st4(c, q, make_float4(o[0], o[1], o[2], o[3]));
+  }
+}
 
 template <typename T>
 __device__ __forceinline__ float ldf(const T *p) {
   return (float)__ldg(p);
 }
 
+// ---------------------------------------------------------------------------
+// kernel 1: one CTA = R whole rows, staged with cp.async (any width / dtype)
+// ---------------------------------------------------------------------------
 template <int K, typename T>
 __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(const T *__restrict__ x, int64_t ldx,
                                                               float *__restrict__ y, int64_t ldy,
@@ -69,238 +322,31 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
         xs[r * rowf + sidx(n)] = ldf(x + (row0 + r) * ldx + n);
   }
   __syncthreads();
-  for (int r = 0; r < nrows; ++r)  // replicate x[W-1] into the padding
+  // Each row is padded to C*32 samples with copies of x[W-1]: a steady state
+  // fed a constant stays steady, so the backward recursion may start at the
+  // padded end in the steady state of x[W-1].
+  for (int r = 0; r < nrows; ++r)
     for (int n = W + tid; n < Wp; n += blockDim.x) xs[r * rowf + sidx(n)] = xs[r * rowf + sidx(W - 1)];
   __syncthreads();
 
   const bool active = rr < nrows;
-  float *xr = xs + rr * rowf;
-  const int n0 = c * kChunk;
-
-  // ---- b. zero-state carries (folded sample pairs) -------------------------
-  if (active) {
-    double P[K], Q[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0;
-    const float4 *v4 = reinterpret_cast<const float4 *>(xr + sidx(n0));
-    float xv[kChunk];  // fp32 copies; the pair sums are formed in fp64
-#pragma unroll
-    for (int q = 0; q < kChunk / 4; ++q) {
-      float4 v = v4[q];
-      xv[4 * q] = v.x;
-      xv[4 * q + 1] = v.y;
-      xv[4 * q + 2] = v.z;
-      xv[4 * q + 3] = v.w;
-    }
-#pragma unroll
-    for (int t = 0; t < kChunk / 2; ++t) {
-      const double xa = xv[t], xb = xv[kChunk - 1 - t];
-      const double u = xa + xb, v = xa - xb;
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        P[i] = fma(p.SP32[i][t], u, P[i]);
-        Q[i] = fma(p.SQ32[i][t], v, Q[i]);
-      }
-    }
-    double f[K], g[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      f[i] = P[i] + Q[i];
-      g[i] = P[i] - Q[i];
-    }
-    // scan inputs d_c = Yzs_c + Tx X_{c-1} (x history before the chunk in
-    // scan order; the steady state of the end sample for the first chunk,
-    // plus Ty E_{-1} with E_{-1} = yss * that sample)
-    double Xf[K], Xb[K];
-    const double x0 = (double)xr[sidx(0)], xl = (double)xr[sidx(Wp - 1)];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      Xf[i] = c > 0 ? (double)xr[sidx(n0 - 1 - i)] : x0;
-      Xb[i] = c < C - 1 ? (double)xr[sidx(n0 + kChunk + i)] : xl;
-    }
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      double df = f[i], db = g[i];
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        df = fma(p.Tx[i * K + j], Xf[j], df);
-        db = fma(p.Tx[i * K + j], Xb[j], db);
-      }
-      if (c == 0) {
-#pragma unroll
-        for (int j = 0; j < K; ++j) df = fma(p.Ty[i * K + j], p.yss * x0, df);
-      }
-      if (c == C - 1) {
-#pragma unroll
-        for (int j = 0; j < K; ++j) db = fma(p.Ty[i * K + j], p.yss * xl, db);
-      }
-      cf[(rr * C + c) * K + i] = df;
-      cb[(rr * C + c) * K + i] = db;
-    }
-  }
+  const PadRow xr{xs + rr * rowf};
+  if (active) row_carry<K>(p, xr, c, C, Wp, cf + rr * C * K, cb + rr * C * K);
   __syncthreads();
-
-  // ---- c. scan: one warp per (row, direction) ------------------------------
-  // E_c = d_c + Ty E_{c-1},  d_c = Yzs_c + Tx X_{c-1}  (c in scan order; the
-  // backward direction scans chunks from the right end).  Lane l owns cpl
-  // consecutive chunks: local sequential scan, Kogge-Stone across lanes
-  // with Ty^(cpl*2^j), then a sequential re-scan from the carry-in.
   {
     const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int cpl = p.cpl;
     for (int task = warp; task < 2 * nrows; task += nwarps) {
       const int r = task >> 1, dir = task & 1;
-      double *cc = (dir == 0 ? cf : cb) + r * C * K;
-      const bool live = lane * cpl < C;
-      auto dval = [&](int sp, double *d) {
-        const int ch = dir == 0 ? sp : C - 1 - sp;
-#pragma unroll
-        for (int i = 0; i < K; ++i) d[i] = cc[ch * K + i];
-      };
-      double A[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) A[i] = 0.0;
-      if (live) {
-        for (int q = 0; q < cpl; ++q) {
-          double d[K], An[K];
-          dval(lane * cpl + q, d);
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            double acc = d[i];
-#pragma unroll
-            for (int j = 0; j < K; ++j) acc = fma(p.Ty[i * K + j], A[j], acc);
-            An[i] = acc;
-          }
-#pragma unroll
-          for (int i = 0; i < K; ++i) A[i] = An[i];
-        }
-      }
-      // inclusive Kogge-Stone over lanes: A_l += Ty^(cpl*o) A_{l-o}
-#pragma unroll
-      for (int lv = 0; lv < 5; ++lv) {
-        const int o = 1 << lv;
-        double B[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) B[i] = __shfl_up_sync(0xffffffffu, A[i], o);
-        if (lane >= o) {
-          const double *M = p.Tpow[lv];
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            double acc = A[i];
-#pragma unroll
-            for (int j = 0; j < K; ++j) acc = fma(M[i * K + j], B[j], acc);
-            A[i] = acc;
-          }
-        }
-      }
-      // carry-in = inclusive value of the previous lane
-      double E[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        double v = __shfl_up_sync(0xffffffffu, A[i], 1);
-        E[i] = lane ? v : 0.0;
-      }
-      if (live) {
-        for (int q = 0; q < cpl; ++q) {
-          const int sp = lane * cpl + q;
-          const int ch = dir == 0 ? sp : C - 1 - sp;
-          double d[K], En[K];
-          dval(sp, d);
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            double acc = d[i];
-#pragma unroll
-            for (int j = 0; j < K; ++j) acc = fma(p.Ty[i * K + j], E[j], acc);
-            En[i] = acc;
-          }
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            E[i] = En[i];
-            cc[ch * K + i] = En[i];  // END history of chunk ch (scan order)
-          }
-        }
-      }
+      row_scan<K>(p, (dir == 0 ? cf : cb) + r * C * K, dir, C, lane);
       __syncwarp();
     }
   }
   __syncthreads();
-
-  // ---- d. apply -------------------------------------------------------------
-  // Backward first (reads only x, parks sign*y- in registers), then a barrier,
-  // then the forward recursion overwrites x(n) with out(n) in place.
   float park[kChunk];
-  float4 *v4 = reinterpret_cast<float4 *>(xr + sidx(n0));
-  if (active) {
-    double Xb[K], Yb[K];
-    const double xl = (double)xr[sidx(Wp - 1)];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      int qb = n0 + kChunk + i;
-      Xb[i] = (double)xr[sidx(qb > Wp - 1 ? Wp - 1 : qb)];
-      Yb[i] = c < C - 1 ? cb[(rr * C + c + 1) * K + i] : p.yss * xl;
-    }
-#pragma unroll
-    for (int q = kChunk / 4 - 1; q >= 0; --q) {
-      float4 v = v4[q];
-      float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int u = 3; u >= 0; --u) {
-        double xv = (double)e[u];
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m < K; ++m) s = fma(p.b[m], Xb[m], s);
-#pragma unroll
-        for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yb[m], s);
-        s = fma(-p.a[0], Yb[0], s);
-        park[4 * q + u] = (float)(p.sign * s);
-#pragma unroll
-        for (int m = K - 1; m > 0; --m) {
-          Yb[m] = Yb[m - 1];
-          Xb[m] = Xb[m - 1];
-        }
-        Yb[0] = s;
-        Xb[0] = xv;
-      }
-    }
-  }
   double Xf[K], Yf[K];
-  if (active) {
-    const double x0 = (double)xr[sidx(0)];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      int qf = n0 - 1 - i;
-      Xf[i] = (double)xr[sidx(qf < 0 ? 0 : qf)];
-      Yf[i] = c > 0 ? cf[(rr * C + c - 1) * K + i] : p.yss * x0;
-    }
-  }
+  if (active) row_apply_bwd<K>(p, xr, c, C, Wp, cf + rr * C * K, cb + rr * C * K, park, Xf, Yf);
   __syncthreads();  // every halo read before any chunk is overwritten
-  if (active) {
-#pragma unroll
-    for (int q = 0; q < kChunk / 4; ++q) {
-      float4 v = v4[q];
-      float e[4] = {v.x, v.y, v.z, v.w};
-      float o[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        double xv = (double)e[u];
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m < K; ++m) s = fma(p.b[m], Xf[m], s);
-#pragma unroll
-        for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yf[m], s);
-        s = fma(-p.a[0], Yf[0], s);
-        o[u] = (float)(fma(p.b0, xv, s) + (double)park[4 * q + u]);
-#pragma unroll
-        for (int m = K - 1; m > 0; --m) {
-          Yf[m] = Yf[m - 1];
-          Xf[m] = Xf[m - 1];
-        }
-        Yf[0] = s;
-        Xf[0] = xv;
-      }
-      v4[q] = make_float4(o[0], o[1], o[2], o[3]);
-    }
-  }
+  if (active) row_apply_fwd<K>(p, xr, c, park, Xf, Yf);
   __syncthreads();
 
   // ---- e. store --------------------------------------------------------------
@@ -314,6 +360,71 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
     for (int r = 0; r < nrows; ++r)
       for (int n = tid; n < W; n += blockDim.x) y[(row0 + r) * ldy + n] = xs[r * rowf + sidx(n)];
   }
+}
+
+// ---------------------------------------------------------------------------
+// kernel 2 (fp32, W = 32 C): persistent, one row per step, TMA in and out.
+// The row is one SWIZZLE_128B box [C][32]; the box of the next row is loaded
+// while the current one is computed, and the result leaves with a TMA store
+// from the same buffer (two buffers, one mbarrier each).
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_tma_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+    RowParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int C = p.C, Wp = C * kChunk;
+  const int rowb = Wp * (int)sizeof(float);
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
+  char *buf0 = reinterpret_cast<char *>(smem_raw) + ((1024u - (sbase & 1023u)) & 1023u);
+  double *cf = reinterpret_cast<double *>(buf0 + 2 * rowb);
+  double *cb = cf + C * K;
+  const int c = threadIdx.x;
+  const int64_t H = p.H;
+  const int rows_per = (int)((H + gridDim.x - 1) / gridDim.x);
+  const int64_t rlo = (int64_t)blockIdx.x * rows_per;
+  const int64_t rhi = rlo + rows_per < H ? rlo + rows_per : H;
+  if (rlo >= rhi) return;
+  if (c == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_expect_tx(&bar[0], (unsigned)rowb);
+    tma_load_3d_hint(buf0, &xmap, &bar[0], 0, 0, (int)rlo, l2_policy_evict_first());
+  }
+  __syncthreads();
+  int b = 0;
+  unsigned phases = 0u;
+  for (int64_t r = rlo; r < rhi; ++r, b ^= 1) {
+    const SwzRow xr{buf0 + b * rowb};
+    mbar_wait(&bar[b], (phases >> b) & 1u);
+    phases ^= 1u << b;
+    row_carry<K>(p, xr, c, C, Wp, cf, cb);
+    __syncthreads();
+    if (c == 0 && r + 1 < rhi) {
+      // buffer b^1 last held row r-1, whose TMA store was issued a full step
+      // ago: wait until it has been read out, then refill with row r+1
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      mbar_expect_tx(&bar[b ^ 1], (unsigned)rowb);
+      tma_load_3d_hint(buf0 + (b ^ 1) * rowb, &xmap, &bar[b ^ 1], 0, 0, (int)(r + 1),
+                       l2_policy_evict_first());
+    }
+    for (int task = c >> 5; task < 2; task += (int)(blockDim.x >> 5))
+      row_scan<K>(p, task == 0 ? cf : cb, task, C, c & 31);
+    __syncthreads();
+    float park[kChunk];
+    double Xf[K], Yf[K];
+    row_apply_bwd<K>(p, xr, c, C, Wp, cf, cb, park, Xf, Yf);
+    __syncthreads();  // every halo read (and cf / cb) before chunks are overwritten
+    row_apply_fwd<K>(p, xr, c, park, Xf, Yf);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
+    __syncthreads();
+    if (c == 0) {
+      tma_store_3d_hint(&ymap, buf0 + b * rowb, 0, 0, (int)r, l2_policy_evict_last());
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  }
+  if (c == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -447,11 +558,55 @@ static int launch_rowpass(const T *x, int64_t ldx, float *y, int64_t ldy, RowPar
   return cuda_status("row pass");
 }
 
+// Persistent TMA variant: fp32, w = 32 C exactly (no padding), aligned pitches.
+template <int K>
+static int launch_rowpass_tma(const CUtensorMap &xm, const CUtensorMap &ym, RowParams p,
+                              cudaStream_t st) {
+  const size_t smem = 1024 + 2 * (size_t)p.C * kChunk * sizeof(float) +
+                      2 * (size_t)p.C * K * sizeof(double);
+  static int slots = 0;  // resident CTAs over the device
+  if (!slots) {
+    cudaFuncSetAttribute(rowpass_tma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    int occ = 0, dev = 0, nsm = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_tma_kernel<K>, kRowThreads, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    slots = (occ > 0 ? occ : 1) * nsm;
+  }
+  // equal row counts per CTA
+  const int64_t per = cdiv(p.H, slots);
+  const int grid = (int)cdiv(p.H, per);
+  Launch g(K_IIR_ROWS_FUSED, st);
+  rowpass_tma_kernel<K><<<grid, p.C, smem, st>>>(xm, ym, p);
+  return cuda_status("row pass");
+}
+
 template <typename T>
 int rowpass_run(const T *x, int64_t ldx, float *y, int64_t ldy, const IirParams &ip, int64_t h,
                 int64_t w, cudaStream_t st) {
   RowParams p;
   rowpass_plan(&p, ip, h, w);
+  if (sizeof(T) == 4 && w == (int64_t)p.C * kChunk && p.C >= 32 && !getenv("VMF_ROW_NO_TMA")) {
+    CUtensorMap xm, ym;
+    memset(&xm, 0, sizeof(xm));
+    memset(&ym, 0, sizeof(ym));
+    if (make_tmap_rows_swz_f32(&xm, (const float *)x, h, w, ldx) &&
+        make_tmap_rows_swz_f32(&ym, y, h, w, ldy)) {
+      switch (ip.K) {
+        case 1: return launch_rowpass_tma<1>(xm, ym, p, st);
+        case 2: return launch_rowpass_tma<2>(xm, ym, p, st);
+        case 3: return launch_rowpass_tma<3>(xm, ym, p, st);
+        case 4: return launch_rowpass_tma<4>(xm, ym, p, st);
+        case 5: return launch_rowpass_tma<5>(xm, ym, p, st);
+        case 6: return launch_rowpass_tma<6>(xm, ym, p, st);
+        case 7: return launch_rowpass_tma<7>(xm, ym, p, st);
+        case 8: return launch_rowpass_tma<8>(xm, ym, p, st);
+      }
+    }
+    cudaGetLastError();
+  }
   switch (ip.K) {
     case 1: return launch_rowpass<1, T>(x, ldx, y, ldy, p, st);
     case 2: return launch_rowpass<2, T>(x, ldx, y, ldy, p, st);

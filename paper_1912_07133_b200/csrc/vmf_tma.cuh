@@ -14,6 +14,11 @@ namespace vmf {
 bool make_tmap_2d_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t cols,
                       int64_t ld, int box_cols, int box_rows);
 
+// Rows of a row-major fp32 image as 3-D boxes [chunks][32] with 128-byte
+// swizzle: dims {32, w / 32, rows}; box = one whole row.  w % 32 == 0.
+bool make_tmap_rows_swz_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t w,
+                            int64_t ld);
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
@@ -47,6 +52,29 @@ __device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *m
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(d),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(r), "r"(b), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d_hint(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                                 int c0, int c1, int c2, uint64_t policy) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(b), "l"(policy)
+      : "memory");
+}
+
+// shared -> global tile store (bulk-group completion; the caller commits and
+// waits with cp.async.bulk.commit_group / wait_group).
+__device__ __forceinline__ void tma_store_3d_hint(const CUtensorMap *map, const void *src, int c0,
+                                                  int c1, int c2, uint64_t policy) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(src);
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint"
+      " [%0, {%1, %2, %3}], [%4], %5;\n" ::"l"(reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(s), "l"(policy)
       : "memory");
 }
 
