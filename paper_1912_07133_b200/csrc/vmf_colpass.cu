@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     double br = __shfl_down_sync(0xffffffffu, bc, 1);
     return (bl - 2.0 * bc) + br;
   };
+  float tmax = 0.0f;  // running max |L| of this column (valid columns, non-edge lanes)
   // lanes 0, 1, 30, 31 keep B(r0-2 .. r1+1) for the warp-edge recomputation
   const bool keep_b = eslot >= 0;
   double *ebw = &S.eb[wid][keep_b ? eslot : 0][0];  // B(r0 - 2 + q) at ebw[q]
@@ -540,7 +541,9 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
         push2<K>(Yf, y, Xf, xv);
         double lx = lx_of(Bt);
-        lp[t * kTileStride] = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + Bt)));
+        const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + Bt)));
+        lp[t * kTileStride] = v;
+        tmax = fmaxf(tmax, fabsf(v));
         if (keep_b) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
@@ -557,7 +560,11 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         if (r == 0) Bm1 = Bt;  // replicate top edge: B(-1) = B(0)
         double lx = lx_of(Bt);
         const double bnext = r >= H ? Bm1 : Bt;  // replicate bottom edge
-        if (r >= 1) lp[t * kTileStride] = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + bnext)));
+        if (r >= 1) {
+          const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + bnext)));
+          lp[t * kTileStride] = v;
+          if (r - 1 < H) tmax = fmaxf(tmax, fabsf(v));
+        }
         if (keep_b) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
@@ -573,11 +580,16 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
       double B1 = fma(p.sign, Ybot[0], fma(p.b0, xr1, y0));
       double B2 = fma(p.sign, Ybot[1], fma(p.b0, xr2, y1));
       const double lx1 = lx_of(B1);
-      if (r1 - 1 < H)
-        tcol[(tr1 - 1) * kTileStride] =
-            (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + (r1 >= H ? Bm1 : B1))));
-      if (r1 < H)
-        tcol[tr1 * kTileStride] = (float)(lsc * (lx1 + ((Bm1 - 2.0 * B1) + (r1 + 1 >= H ? B1 : B2))));
+      if (r1 - 1 < H) {
+        const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + (r1 >= H ? Bm1 : B1))));
+        tcol[(tr1 - 1) * kTileStride] = v;
+        tmax = fmaxf(tmax, fabsf(v));
+      }
+      if (r1 < H) {
+        const float v = (float)(lsc * (lx1 + ((Bm1 - 2.0 * B1) + (r1 + 1 >= H ? B1 : B2))));
+        tcol[tr1 * kTileStride] = v;
+        tmax = fmaxf(tmax, fabsf(v));
+      }
       if (keep_b) {
         ebw[len + 2] = B1;
         ebw[len + 3] = B2;
@@ -594,6 +606,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     const int64_t rlo = r0 > 0 ? r0 - 1 : 0;
     const int64_t rhi = r1 < H ? r1 : H - 1;
     const int nr = (int)(rhi - rlo + 1);
+    float pmax = 0.0f;
     for (int idx = lane; idx < 2 * nr; idx += 32) {
       const int side = idx & 1;
       const int64_t r = rlo + (idx >> 1);
@@ -607,20 +620,28 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
       const double br = side ? S.eb[wid + 1][0][q] : S.eb[wid][1][q];
       const double bc = bcv[q];
       const double lx = (bl - 2.0 * bc) + br;
-      S.tile[r - r0 + K][jj + 2] = (float)(lsc * (lx + ((bcv[qu] - 2.0 * bc) + bcv[qd])));
+      const float v = (float)(lsc * (lx + ((bcv[qu] - 2.0 * bc) + bcv[qd])));
+      S.tile[r - r0 + K][jj + 2] = v;
+      const int64_t cj = c0 - kColHalo + jj;
+      if (cj >= 0 && cj < p.W) pmax = fmaxf(pmax, fabsf(v));
     }
+    // the walk values of edge lanes were placeholders; columns outside the
+    // image never count
+    if (lane == 0 || lane == 31 || col < 0 || col >= p.W) tmax = 0.0f;
+    tmax = fmaxf(tmax, pmax);
+    tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+    if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
   }
   __syncthreads();
 
   // ---- store the owned L block (rows r0 .. r1-1, columns c0 .. c0+123) ----
-  // fused with the strict 3x3 NMS: a warp walks rows, and a pixel is tested
-  // when |L| reaches frac * (running max of the rows seen so far, or the
-  // global max published so far) -- a lower bound of the final threshold, so
+  // fused with the strict 3x3 NMS over frac * max(this CTA's max |L|, the
+  // global max published so far): a lower bound of the final threshold, so
   // the candidates are a superset that the flush and the finaliser filter.
   {
     const int nrow = (int)(rown_hi - r0);
     const int ncol = (int)(p.W - c0 < kColOut ? p.W - c0 : kColOut);
-    float wrun = gbound;
+    const float th = p.frac * fmaxf(__uint_as_float(S.cmax), gbound);
     auto test = [&](int q, int c, float v) {  // tile row q + K, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
       if (r < 1 || r > H - 2 || cc < 1 || cc > p.W - 2) return;
@@ -657,8 +678,6 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
           st_v4_hint(dst + q * ldl, v, lpol);
         }
         const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-        wrun = fmaxf(wrun, __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m4))));
-        const float th = p.frac * wrun;
         if (m4 >= th) {
           if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
           if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
@@ -675,12 +694,9 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
             v = S.tile[q + K][4 + c];
             Lout[(r0 + q) * ldl + c0 + c] = v;
           }
-          const float av = fabsf(v);
-          wrun = fmaxf(wrun, __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(av))));
-          if (c < ncol && av >= p.frac * wrun) test(q, c, v);
+          if (c < ncol && fabsf(v) >= th) test(q, c, v);
         }
     }
-    if (lane == 0) atomicMax(&S.cmax, __float_as_uint(wrun));
   }
   __syncthreads();
 
