@@ -101,7 +101,7 @@ __device__ __forceinline__ void carry_half(const ColParams &p, const float *tile
 template <int K>
 __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
     const float *__restrict__ T, int64_t ldt, ColParams p, double *__restrict__ Z,
-    const __grid_constant__ CUtensorMap tmap, int use_tma) {
+    const __grid_constant__ CUtensorMap tmap, int use_tma, CandState *__restrict__ cs) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 128-byte aligned TMA destination, derived from the shared array itself so
   // the reads stay LDS
@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
   const int64_t r0 = (int64_t)b * kBand;
   const bool full = len == kBand && r0 + kBand <= p.H;
   const bool tma = use_tma && full && c0 + kCarryCols <= p.W;
+  pdl_wait();  // T comes from the row pass
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 4) (&cs->absmax_bits)[threadIdx.x] = 0u;
   if (tma) {
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
       Q[i] = 0.5 * (f - g);
     }
   }
+  pdl_trigger();
   if (half == 1) {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
@@ -201,6 +204,7 @@ __global__ void __launch_bounds__(32 * kScanCols, 48 / kScanCols) colscan_kernel
   double *sz = reinterpret_cast<double *>(smem_raw);  // [NB][2K][kScanCols] (+pad)
   const int dir = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * kScanCols;
+  pdl_wait();  // records come from the band carries
   // staging with asynchronous 16-byte copies (two columns each), all in
   // flight at once: element pair e = (b, i, c/2)
   {
@@ -224,6 +228,7 @@ __global__ void __launch_bounds__(32 * kScanCols, 48 / kScanCols) colscan_kernel
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
   }
+  pdl_trigger();
   __syncthreads();
   const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
   const int64_t col = c0 + c < p.W ? c0 + c : p.W - 1;
@@ -437,6 +442,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     S.coverflow = 0;
     S.cmax = 0u;
   }
+  pdl_wait();  // band histories and the CandState come from earlier kernels
   const float gbound = __uint_as_float(st->absmax_bits);  // global max so far (lower bound)
   double Ybot[K], Yf[K];
 #pragma unroll
@@ -597,6 +603,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     }
   }
 #undef TX
+  pdl_trigger();
   __syncthreads();
 
   // ---- warp-edge columns (lanes 0 / 31): L recomputed from the kept B ------
@@ -793,6 +800,7 @@ __global__ void __launch_bounds__(kFinThreads) colfinal_kernel(
   unsigned long long *key = reinterpret_cast<unsigned long long *>(fsm);
   float *val = reinterpret_cast<float *>(fsm + kSortCap * sizeof(unsigned long long));
   __shared__ int m;
+  pdl_wait();
   const float thr = frac * __uint_as_float(st->absmax_bits);
   if (threadIdx.x == 0) {
     m = 0;
@@ -949,7 +957,6 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   float *gv = (float *)(gx + gcap);
   void *dws = (void *)(((uintptr_t)(gv + gcap) + 255) & ~(uintptr_t)255);
   size_t dws_b = detect_workspace_bytes(1, p.H, p.W);
-  cudaMemsetAsync(cs, 0, 128, st);
   {
     Launch g(K_COL_CARRY, st);
     dim3 grid((unsigned)cdiv(p.W, kCarryCols), (unsigned)p.NB);
@@ -964,7 +971,8 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
       cudaFuncSetAttribute(colcarry_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
       cattr = true;
     }
-    colcarry_kernel<K><<<grid, kCarryThreads, csm, st>>>(T, ldt, p, Z, cmap, ctma);
+    launch_pdl(colcarry_kernel<K>, grid, dim3(kCarryThreads), csm, st, T, ldt, p, Z, cmap, ctma,
+               cs);
   }
   {
     Launch g(K_COL_SCAN, st);
@@ -975,8 +983,8 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
                            200 * 1024);
       sattr = true;
     }
-    colscan_kernel<K><<<dim3((unsigned)cdiv(p.W, kScanCols), 2), 32 * kScanCols, ssm, st>>>(
-        T, ldt, p, Z);
+    launch_pdl(colscan_kernel<K>, dim3((unsigned)cdiv(p.W, kScanCols), 2), dim3(32 * kScanCols),
+               ssm, st, T, ldt, p, Z);
   }
 
   {
@@ -993,9 +1001,9 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
     int use_tma = make_tmap_2d_f32(&tmap, T, p.H, p.W, ldt, kTileStride, kTileRows(K)) &&
                   !getenv("VMF_NO_TMA");
     cudaGetLastError();
-    colapply_kernel<K><<<grid, kColThreads, sizeof(ColSmem<K>) + 128, st>>>(
-        T, ldt, L, ldl, p, Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
-        (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
+    launch_pdl(colapply_kernel<K>, grid, dim3(kColThreads), sizeof(ColSmem<K>) + 128, st, T, ldt,
+               L, ldl, p, (const double *)Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
+               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
   }
   {
     Launch g(K_FINALIZE, st);
@@ -1005,9 +1013,10 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
       cudaFuncSetAttribute(colfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
       fattr = true;
     }
-    colfinal_kernel<<<1, kFinThreads, fsmem, st>>>(cs, gy, gx, gv, (int)gcap, L, ldl, p.H, p.W,
-                                                   p.frac, det_yx, det_val, cap, n_det_dev,
-                                                   thr_dev, getenv("VMF_FORCE_FULLSCAN") ? 1 : 0);
+    launch_pdl(colfinal_kernel, dim3(1), dim3(kFinThreads), fsmem, st, cs, (const int *)gy,
+               (const int *)gx, (const float *)gv, (int)gcap, (const float *)L, ldl, p.H, p.W,
+               p.frac, det_yx, det_val, cap, n_det_dev, thr_dev,
+               getenv("VMF_FORCE_FULLSCAN") ? 1 : 0);
   }
   return cuda_status("column pass");
 }

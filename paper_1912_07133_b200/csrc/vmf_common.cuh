@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <utility>
 
 #include "../../include/vmfilt_b200.h"
 
@@ -51,6 +52,34 @@ __device__ __forceinline__ void cp_async16_hint(void *smem_dst, const void *src,
   unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),
                "l"(src), "l"(policy));
+}
+
+// ---------------------------------------------------------------------------
+// programmatic dependent launch: the fused path's kernels are launched with
+// the PDL attribute, so each may be scheduled while its predecessor drains.
+// pdl_wait() blocks until the predecessor grid has completed and its memory
+// is visible (a no-op without the attribute); pdl_trigger() lets the next
+// grid launch once every CTA of this grid has issued it or exited.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+template <typename... Exp, typename... Act>
+inline cudaError_t launch_pdl(void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Act &&...args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
 }
 
 // Element n of line `line` for a pass along rows (line = row) or columns

@@ -420,10 +420,12 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_tma_ker
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
     __syncthreads();
     if (c == 0) {
+      if (r == rlo) pdl_wait();  // T may still be read by the previous scale's column pass
       tma_store_3d_hint(&ymap, buf0 + b * rowb, 0, 0, (int)r, l2_policy_evict_last());
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
   }
+  pdl_trigger();
   if (c == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
@@ -579,7 +581,7 @@ static int launch_rowpass_tma(const CUtensorMap &xm, const CUtensorMap &ym, RowP
   const int64_t per = cdiv(p.H, slots);
   const int grid = (int)cdiv(p.H, per);
   Launch g(K_IIR_ROWS_FUSED, st);
-  rowpass_tma_kernel<K><<<grid, p.C, smem, st>>>(xm, ym, p);
+  launch_pdl(rowpass_tma_kernel<K>, dim3(grid), dim3(p.C), smem, st, xm, ym, p);
   return cuda_status("row pass");
 }
 
