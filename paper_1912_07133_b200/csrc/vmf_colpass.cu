@@ -204,21 +204,28 @@ __global__ void __launch_bounds__(32 * kScanCols, 48 / kScanCols) colscan_kernel
   double *sz = reinterpret_cast<double *>(smem_raw);  // [NB][2K][kScanCols] (+pad)
   const int dir = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * kScanCols;
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  const int64_t col = c0 + c < p.W ? c0 + c : p.W - 1;
   pdl_wait();  // records come from the band carries
+  // the end sample (steady-state start of the first band) is loaded now, so
+  // its latency hides under the staging
+  const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, col);
   // staging with asynchronous 16-byte copies (two columns each), all in
-  // flight at once: element pair e = (b, i, c/2)
+  // flight at once: element pair e = (record row bi = b * 2K + i, c/2)
   {
     constexpr int kPairs = kScanCols / 2;
     const bool full = c0 + kScanCols <= p.W && p.W % 2 == 0;
+    const double *zdir = Z + (int64_t)dir * NB * 2 * K * p.W + c0;
     for (int e = threadIdx.x; e < NB * 2 * K * kPairs; e += blockDim.x) {
       const int c = 2 * (e % kPairs), bi = e / kPairs;
-      const int i = bi % (2 * K), b = bi / (2 * K);
-      double *dst = sz + b * stride + i * kScanCols + c;
+      const int b = bi / (2 * K);
+      double *dst = sz + bi * kScanCols + 2 * b + c;  // = b * stride + i * kScanCols + c
+      const double *src = zdir + (int64_t)bi * p.W + c;
       if (full) {
         const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
-                     "l"(Z + zidx(dir, b, i, NB, K, p.W, c0 + c)));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
       } else {
+        const int i = bi - b * 2 * K;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int64_t col = c0 + c + u < p.W ? c0 + c + u : p.W - 1;
@@ -230,9 +237,6 @@ __global__ void __launch_bounds__(32 * kScanCols, 48 / kScanCols) colscan_kernel
   }
   pdl_trigger();
   __syncthreads();
-  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
-  const int64_t col = c0 + c < p.W ? c0 + c : p.W - 1;
-  const double xe = ldT(T, ldt, dir == 0 ? 0 : p.H - 1, p.H, col);
   auto rec = [&](int sp) { return sz + (dir == 0 ? sp : NB - 1 - sp) * stride + c; };
   double dl[kMaxCpl][K];
 #pragma unroll
@@ -330,10 +334,13 @@ __global__ void __launch_bounds__(32 * kScanCols, 48 / kScanCols) colscan_kernel
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < NB * K * kScanCols; e += blockDim.x) {
-    const int cc = e % kScanCols, bi = e / kScanCols;
-    const int i = bi % K, b = bi / K;
-    if (c0 + cc < p.W) Z[zidx(dir, b, i, NB, K, p.W, c0 + cc)] = sz[b * stride + i * kScanCols + cc];
+  {
+    double *zdir = Z + (int64_t)dir * NB * 2 * K * p.W + c0;
+    for (int e = threadIdx.x; e < NB * K * kScanCols; e += blockDim.x) {
+      const int cc = e % kScanCols, bi = e / kScanCols;
+      const int b = bi / K, i = bi - b * K;
+      if (c0 + cc < p.W) zdir[(int64_t)(b * 2 * K + i) * p.W + cc] = sz[b * stride + i * kScanCols + cc];
+    }
   }
 }
 
