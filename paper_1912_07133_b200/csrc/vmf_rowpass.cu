@@ -210,78 +210,104 @@ __device__ __forceinline__ void row_scan(const RowParams &p, double *cc, int dir
 }
 
 // d. apply, backward half: DF-I recursion from the true history, sign*y-
-//    parked in 32 fp32 registers (its rounding is smoothed away by the column
-//    pass, tools/experiments/park_precision.py); also returns the forward
-//    start history.  Reads only x.
-template <int K, class Row>
-__device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row &xr, int c, int C,
-                                              int Wp, const double *cfr, const double *cbr,
-                                              float *park, double *Xf, double *Yf) {
+//    parked in 32 fp32 registers per row (its rounding is smoothed away by
+//    the column pass, tools/experiments/park_precision.py); also returns the
+//    forward start history.  Reads only x.  NR rows are walked in lockstep so
+//    the scheduler sees NR independent recursion chains.
+template <int K, int NR, class Row>
+__device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row *xr, int c, int C,
+                                              int Wp, double *const *cfr, double *const *cbr,
+                                              float (*park)[kChunk], double (*Xf)[K],
+                                              double (*Yf)[K]) {
   const int n0 = c * kChunk;
-  double Xb[K], Yb[K];
-  const double xl = (double)xr.ld(Wp - 1), x0 = (double)xr.ld(0);
+  double Xb[NR][K], Yb[NR][K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    int qb = n0 + kChunk + i;
-    Xb[i] = (double)xr.ld(qb > Wp - 1 ? Wp - 1 : qb);
-    Yb[i] = c < C - 1 ? cbr[(c + 1) * K + i] : p.yss * xl;
-    int qf = n0 - 1 - i;
-    Xf[i] = (double)xr.ld(qf < 0 ? 0 : qf);
-    Yf[i] = c > 0 ? cfr[(c - 1) * K + i] : p.yss * x0;
+  for (int g = 0; g < NR; ++g) {
+    const double xl = (double)xr[g].ld(Wp - 1), x0 = (double)xr[g].ld(0);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      int qb = n0 + kChunk + i;
+      Xb[g][i] = (double)xr[g].ld(qb > Wp - 1 ? Wp - 1 : qb);
+      Yb[g][i] = c < C - 1 ? cbr[g][(c + 1) * K + i] : p.yss * xl;
+      int qf = n0 - 1 - i;
+      Xf[g][i] = (double)xr[g].ld(qf < 0 ? 0 : qf);
+      Yf[g][i] = c > 0 ? cfr[g][(c - 1) * K + i] : p.yss * x0;
+    }
   }
 #pragma unroll
   for (int q = kChunk / 4 - 1; q >= 0; --q) {
-    float4 v = xr.ld4(c, q);
-    float e[4] = {v.x, v.y, v.z, v.w};
+    float e[NR][4];
+#pragma unroll
+    for (int g = 0; g < NR; ++g) {
+      float4 v = xr[g].ld4(c, q);
+      e[g][0] = v.x;
+      e[g][1] = v.y;
+      e[g][2] = v.z;
+      e[g][3] = v.w;
+    }
 #pragma unroll
     for (int u = 3; u >= 0; --u) {
-      double xv = (double)e[u];
-      double s = 0.0;
 #pragma unroll
-      for (int m = 0; m < K; ++m) s = fma(p.b[m], Xb[m], s);
+      for (int g = 0; g < NR; ++g) {
+        double xv = (double)e[g][u];
+        double s = 0.0;
 #pragma unroll
-      for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yb[m], s);
-      s = fma(-p.a[0], Yb[0], s);
-      park[4 * q + u] = (float)(p.sign * s);
+        for (int m = 0; m < K; ++m) s = fma(p.b[m], Xb[g][m], s);
 #pragma unroll
-      for (int m = K - 1; m > 0; --m) {
-        Yb[m] = Yb[m - 1];
-        Xb[m] = Xb[m - 1];
+        for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yb[g][m], s);
+        s = fma(-p.a[0], Yb[g][0], s);
+        park[g][4 * q + u] = (float)(p.sign * s);
+#pragma unroll
+        for (int m = K - 1; m > 0; --m) {
+          Yb[g][m] = Yb[g][m - 1];
+          Xb[g][m] = Xb[g][m - 1];
+        }
+        Yb[g][0] = s;
+        Xb[g][0] = xv;
       }
-      Yb[0] = s;
-      Xb[0] = xv;
     }
   }
 }
 
 // d. apply, forward half: out(n) = b0 x + y+ + parked sign*y-, in place.
-template <int K, class Row>
-__device__ __forceinline__ void row_apply_fwd(const RowParams &p, const Row &xr, int c,
-                                              const float *park, double *Xf, double *Yf) {
+template <int K, int NR, class Row>
+__device__ __forceinline__ void row_apply_fwd(const RowParams &p, const Row *xr, int c,
+                                              const float (*park)[kChunk], double (*Xf)[K],
+                                              double (*Yf)[K]) {
 #pragma unroll
   for (int q = 0; q < kChunk / 4; ++q) {
-    float4 v = xr.ld4(c, q);
-    float e[4] = {v.x, v.y, v.z, v.w};
-    float o[4];
+    float e[NR][4], o[NR][4];
+#pragma unroll
+    for (int g = 0; g < NR; ++g) {
+      float4 v = xr[g].ld4(c, q);
+      e[g][0] = v.x;
+      e[g][1] = v.y;
+      e[g][2] = v.z;
+      e[g][3] = v.w;
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      double xv = (double)e[u];
-      double s = 0.0;
 #pragma unroll
-      for (int m = 0; m < K; ++m) s = fma(p.b[m], Xf[m], s);
+      for (int g = 0; g < NR; ++g) {
+        double xv = (double)e[g][u];
+        double s = 0.0;
 #pragma unroll
-      for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yf[m], s);
-      s = fma(-p.a[0], Yf[0], s);
-      o[u] = (float)(fma(p.b0, xv, s) + (double)park[4 * q + u]);
+        for (int m = 0; m < K; ++m) s = fma(p.b[m], Xf[g][m], s);
 #pragma unroll
-      for (int m = K - 1; m > 0; --m) {
-        Yf[m] = Yf[m - 1];
-        Xf[m] = Xf[m - 1];
+        for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yf[g][m], s);
+        s = fma(-p.a[0], Yf[g][0], s);
+        o[g][u] = (float)(fma(p.b0, xv, s) + (double)park[g][4 * q + u]);
+#pragma unroll
+        for (int m = K - 1; m > 0; --m) {
+          Yf[g][m] = Yf[g][m - 1];
+          Xf[g][m] = Xf[g][m - 1];
+        }
+        Yf[g][0] = s;
+        Xf[g][0] = xv;
       }
-      Yf[0] = s;
-      Xf[0] = xv;
     }
-    xr.st4(c, q, make_float4(o[0], o[1], o[2], o[3]));
+#pragma unroll
+    for (int g = 0; g < NR; ++g) xr[g].st4(c, q, make_float4(o[g][0], o[g][1], o[g][2], o[g][3]));
   }
 }
 
@@ -342,11 +368,12 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
     }
   }
   __syncthreads();
-  float park[kChunk];
-  double Xf[K], Yf[K];
-  if (active) row_apply_bwd<K>(p, xr, c, C, Wp, cf + rr * C * K, cb + rr * C * K, park, Xf, Yf);
+  float park[1][kChunk];
+  double Xf[1][K], Yf[1][K];
+  double *cfr[1] = {cf + rr * C * K}, *cbr[1] = {cb + rr * C * K};
+  if (active) row_apply_bwd<K, 1>(p, &xr, c, C, Wp, cfr, cbr, park, Xf, Yf);
   __syncthreads();  // every halo read before any chunk is overwritten
-  if (active) row_apply_fwd<K>(p, xr, c, park, Xf, Yf);
+  if (active) row_apply_fwd<K, 1>(p, &xr, c, park, Xf, Yf);
   __syncthreads();
 
   // ---- e. store --------------------------------------------------------------
@@ -363,65 +390,77 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// kernel 2 (fp32, W = 32 C): persistent, one row per step, TMA in and out.
-// The row is one SWIZZLE_128B box [C][32]; the box of the next row is loaded
-// while the current one is computed, and the result leaves with a TMA store
-// from the same buffer (two buffers, one mbarrier each).
+// kernel 2 (fp32, W = 32 C): persistent, NR rows per step, TMA in and out.
+// A step's rows are one SWIZZLE_128B box [NR][C][32]; the box of the next
+// step is loaded while the current one is computed, and the result leaves
+// with a TMA store from the same buffer (two buffers, one mbarrier each).
+// With NR = 2 every thread walks two independent recursions and the four
+// (row, direction) scans keep all four warps busy.
 // ---------------------------------------------------------------------------
-template <int K>
-__global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_tma_kernel(
+template <int K, int NR>
+__global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
     RowParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar[2];
   const int C = p.C, Wp = C * kChunk;
   const int rowb = Wp * (int)sizeof(float);
+  const int stepb = NR * rowb;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
   char *buf0 = reinterpret_cast<char *>(smem_raw) + ((1024u - (sbase & 1023u)) & 1023u);
-  double *cf = reinterpret_cast<double *>(buf0 + 2 * rowb);
-  double *cb = cf + C * K;
+  double *cf = reinterpret_cast<double *>(buf0 + 2 * stepb);  // [NR][C][K]
+  double *cb = cf + NR * C * K;
   const int c = threadIdx.x;
   const int64_t H = p.H;
-  const int rows_per = (int)((H + gridDim.x - 1) / gridDim.x);
-  const int64_t rlo = (int64_t)blockIdx.x * rows_per;
-  const int64_t rhi = rlo + rows_per < H ? rlo + rows_per : H;
+  const int64_t per = p.rows_per;  // multiple of NR
+  const int64_t rlo = (int64_t)blockIdx.x * per;
+  const int64_t rhi = rlo + per < H ? rlo + per : H;
   if (rlo >= rhi) return;
   if (c == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
-    mbar_expect_tx(&bar[0], (unsigned)rowb);
+    mbar_expect_tx(&bar[0], (unsigned)stepb);
     tma_load_3d_hint(buf0, &xmap, &bar[0], 0, 0, (int)rlo, l2_policy_evict_first());
   }
   __syncthreads();
   int b = 0;
   unsigned phases = 0u;
-  for (int64_t r = rlo; r < rhi; ++r, b ^= 1) {
-    const SwzRow xr{buf0 + b * rowb};
+  double *cfr[NR], *cbr[NR];
+#pragma unroll
+  for (int g = 0; g < NR; ++g) {
+    cfr[g] = cf + g * C * K;
+    cbr[g] = cb + g * C * K;
+  }
+  for (int64_t r = rlo; r < rhi; r += NR, b ^= 1) {
+    SwzRow xr[NR];
+#pragma unroll
+    for (int g = 0; g < NR; ++g) xr[g].base = buf0 + b * stepb + g * rowb;
     mbar_wait(&bar[b], (phases >> b) & 1u);
     phases ^= 1u << b;
-    row_carry<K>(p, xr, c, C, Wp, cf, cb);
+#pragma unroll
+    for (int g = 0; g < NR; ++g) row_carry<K>(p, xr[g], c, C, Wp, cfr[g], cbr[g]);
     __syncthreads();
-    if (c == 0 && r + 1 < rhi) {
-      // buffer b^1 last held row r-1, whose TMA store was issued a full step
-      // ago: wait until it has been read out, then refill with row r+1
+    if (c == 0 && r + NR < rhi) {
+      // buffer b^1 last held the previous step, whose TMA store was issued a
+      // full step ago: wait until it has been read out, then refill
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-      mbar_expect_tx(&bar[b ^ 1], (unsigned)rowb);
-      tma_load_3d_hint(buf0 + (b ^ 1) * rowb, &xmap, &bar[b ^ 1], 0, 0, (int)(r + 1),
+      mbar_expect_tx(&bar[b ^ 1], (unsigned)stepb);
+      tma_load_3d_hint(buf0 + (b ^ 1) * stepb, &xmap, &bar[b ^ 1], 0, 0, (int)(r + NR),
                        l2_policy_evict_first());
     }
-    for (int task = c >> 5; task < 2; task += (int)(blockDim.x >> 5))
-      row_scan<K>(p, task == 0 ? cf : cb, task, C, c & 31);
+    for (int task = c >> 5; task < 2 * NR; task += (int)(blockDim.x >> 5))
+      row_scan<K>(p, (task & 1) == 0 ? cfr[task >> 1] : cbr[task >> 1], task & 1, C, c & 31);
     __syncthreads();
-    float park[kChunk];
-    double Xf[K], Yf[K];
-    row_apply_bwd<K>(p, xr, c, C, Wp, cf, cb, park, Xf, Yf);
+    float park[NR][kChunk];
+    double Xf[NR][K], Yf[NR][K];
+    row_apply_bwd<K, NR>(p, xr, c, C, Wp, cfr, cbr, park, Xf, Yf);
     __syncthreads();  // every halo read (and cf / cb) before chunks are overwritten
-    row_apply_fwd<K>(p, xr, c, park, Xf, Yf);
+    row_apply_fwd<K, NR>(p, xr, c, park, Xf, Yf);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
     __syncthreads();
     if (c == 0) {
       if (r == rlo) pdl_wait();  // T may still be read by the previous scale's column pass
-      tma_store_3d_hint(&ymap, buf0 + b * rowb, 0, 0, (int)r, l2_policy_evict_last());
+      tma_store_3d_hint(&ymap, buf0 + b * stepb, 0, 0, (int)r, l2_policy_evict_last());
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
   }
@@ -560,29 +599,48 @@ static int launch_rowpass(const T *x, int64_t ldx, float *y, int64_t ldy, RowPar
   return cuda_status("row pass");
 }
 
-// Persistent TMA variant: fp32, w = 32 C exactly (no padding), aligned pitches.
-template <int K>
+// Persistent TMA variant: fp32, w = 32 C exactly (no padding), aligned
+// pitches; NR = 2 rows per step when the height is even.
+template <int K, int NR>
 static int launch_rowpass_tma(const CUtensorMap &xm, const CUtensorMap &ym, RowParams p,
                               cudaStream_t st) {
-  const size_t smem = 1024 + 2 * (size_t)p.C * kChunk * sizeof(float) +
-                      2 * (size_t)p.C * K * sizeof(double);
+  const size_t smem = 1024 + 2 * (size_t)NR * p.C * kChunk * sizeof(float) +
+                      2 * (size_t)NR * p.C * K * sizeof(double);
   static int slots = 0;  // resident CTAs over the device
   if (!slots) {
-    cudaFuncSetAttribute(rowpass_tma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(rowpass_tma_kernel<K, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     int occ = 0, dev = 0, nsm = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_tma_kernel<K>, kRowThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_tma_kernel<K, NR>, kRowThreads,
+                                                  smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
     slots = (occ > 0 ? occ : 1) * nsm;
   }
-  // equal row counts per CTA
-  const int64_t per = cdiv(p.H, slots);
-  const int grid = (int)cdiv(p.H, per);
+  // equal row counts per CTA (a multiple of NR)
+  p.rows_per = cdiv(cdiv(p.H, slots), NR) * NR;
+  const int grid = (int)cdiv(p.H, p.rows_per);
   Launch g(K_IIR_ROWS_FUSED, st);
-  launch_pdl(rowpass_tma_kernel<K>, dim3(grid), dim3(p.C), smem, st, xm, ym, p);
+  launch_pdl(rowpass_tma_kernel<K, NR>, dim3(grid), dim3(p.C), smem, st, xm, ym, p);
   return cuda_status("row pass");
+}
+
+template <int K>
+static int launch_rowpass_tma_any(const float *x, int64_t ldx, float *y, int64_t ldy,
+                                  const RowParams &p, cudaStream_t st, bool *done) {
+  // NR = 2 (two interleaved rows per thread) needs twice the registers and
+  // shared memory and measured slower on B200 (2 CTAs/SM instead of 5);
+  // VMF_ROW_NR2 selects it for experiments.
+  const int nr = (p.H % 2 == 0 && getenv("VMF_ROW_NR2")) ? 2 : 1;
+  CUtensorMap xm, ym;
+  memset(&xm, 0, sizeof(xm));
+  memset(&ym, 0, sizeof(ym));
+  *done = make_tmap_rows_swz_f32(&xm, x, p.H, p.W, ldx, nr) &&
+          make_tmap_rows_swz_f32(&ym, y, p.H, p.W, ldy, nr);
+  cudaGetLastError();
+  if (!*done) return VMF_OK;
+  return nr == 2 ? launch_rowpass_tma<K, 2>(xm, ym, p, st) : launch_rowpass_tma<K, 1>(xm, ym, p, st);
 }
 
 template <typename T>
@@ -590,24 +648,22 @@ int rowpass_run(const T *x, int64_t ldx, float *y, int64_t ldy, const IirParams 
                 int64_t w, cudaStream_t st) {
   RowParams p;
   rowpass_plan(&p, ip, h, w);
-  if (sizeof(T) == 4 && w == (int64_t)p.C * kChunk && p.C >= 32 && !getenv("VMF_ROW_NO_TMA")) {
-    CUtensorMap xm, ym;
-    memset(&xm, 0, sizeof(xm));
-    memset(&ym, 0, sizeof(ym));
-    if (make_tmap_rows_swz_f32(&xm, (const float *)x, h, w, ldx) &&
-        make_tmap_rows_swz_f32(&ym, y, h, w, ldy)) {
-      switch (ip.K) {
-        case 1: return launch_rowpass_tma<1>(xm, ym, p, st);
-        case 2: return launch_rowpass_tma<2>(xm, ym, p, st);
-        case 3: return launch_rowpass_tma<3>(xm, ym, p, st);
-        case 4: return launch_rowpass_tma<4>(xm, ym, p, st);
-        case 5: return launch_rowpass_tma<5>(xm, ym, p, st);
-        case 6: return launch_rowpass_tma<6>(xm, ym, p, st);
-        case 7: return launch_rowpass_tma<7>(xm, ym, p, st);
-        case 8: return launch_rowpass_tma<8>(xm, ym, p, st);
-      }
+  if (sizeof(T) == 4 && w == (int64_t)p.C * kChunk && p.C >= 32 && p.C <= kRowThreads &&
+      !getenv("VMF_ROW_NO_TMA")) {
+    const float *xf = (const float *)x;
+    bool done = false;
+    int rc = VMF_OK;
+    switch (ip.K) {
+      case 1: rc = launch_rowpass_tma_any<1>(xf, ldx, y, ldy, p, st, &done); break;
+      case 2: rc = launch_rowpass_tma_any<2>(xf, ldx, y, ldy, p, st, &done); break;
+      case 3: rc = launch_rowpass_tma_any<3>(xf, ldx, y, ldy, p, st, &done); break;
+      case 4: rc = launch_rowpass_tma_any<4>(xf, ldx, y, ldy, p, st, &done); break;
+      case 5: rc = launch_rowpass_tma_any<5>(xf, ldx, y, ldy, p, st, &done); break;
+      case 6: rc = launch_rowpass_tma_any<6>(xf, ldx, y, ldy, p, st, &done); break;
+      case 7: rc = launch_rowpass_tma_any<7>(xf, ldx, y, ldy, p, st, &done); break;
+      case 8: rc = launch_rowpass_tma_any<8>(xf, ldx, y, ldy, p, st, &done); break;
     }
-    cudaGetLastError();
+    if (done) return rc;
   }
   switch (ip.K) {
     case 1: return launch_rowpass<1, T>(x, ldx, y, ldy, p, st);

@@ -21,6 +21,7 @@ struct RowParams {
   int64_t H, W;
   int C, R, cpl;
   int vec4;
+  int64_t rows_per;  // TMA variant: rows per CTA
 };
 
 bool rowpass_supported(int64_t w, int k);

@@ -38,13 +38,13 @@ bool make_tmap_2d_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t
 }
 
 bool make_tmap_rows_swz_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t w,
-                            int64_t ld) {
+                            int64_t ld, int nrows) {
   auto fn = encode_fn();
   if (!fn) return false;
   if (((uintptr_t)base & 15) || ((ld * 4) & 15) || (w % 32) || w / 32 > 256) return false;
   cuuint64_t dims[3] = {32, (cuuint64_t)(w / 32), (cuuint64_t)rows};
   cuuint64_t strides[2] = {128, (cuuint64_t)(ld * 4)};
-  cuuint32_t box[3] = {32, (cuuint32_t)(w / 32), 1};
+  cuuint32_t box[3] = {32, (cuuint32_t)(w / 32), (cuuint32_t)nrows};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

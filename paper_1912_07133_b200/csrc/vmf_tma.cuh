@@ -15,9 +15,9 @@ bool make_tmap_2d_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t
                       int64_t ld, int box_cols, int box_rows);
 
 // Rows of a row-major fp32 image as 3-D boxes [chunks][32] with 128-byte
-// swizzle: dims {32, w / 32, rows}; box = one whole row.  w % 32 == 0.
+// swizzle: dims {32, w / 32, rows}; box = nrows whole rows.  w % 32 == 0.
 bool make_tmap_rows_swz_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t w,
-                            int64_t ld);
+                            int64_t ld, int nrows);
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
