@@ -87,7 +87,11 @@ def make_stage(stage) -> _Stage:
     return _Stage(stage)
 
 
-def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out, cap, sync):
+def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out, cap, sync,
+           out=None):
+    """One vmf_blur_lap_detect call.  `out` = preallocated (det_yx [cap, 2],
+    det_val [cap], scal [2]) device tensors; with sync=False nothing waits
+    for the GPU and the count is read from scal[0] later."""
     h, w = x.shape
     row.check(w)
     col.check(h)
@@ -96,9 +100,12 @@ def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out
     ws = _workspace(nbytes)
     dev = x.device
     cap = int(cap)
-    det_yx = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
-    det_val = torch.empty((max(cap, 1),), dtype=torch.float32, device=dev)
-    scal = torch.empty(2, dtype=torch.int64, device=dev)  # [n_det, thr(float bits)], written by the call
+    if out is None:
+        det_yx = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
+        det_val = torch.empty((max(cap, 1),), dtype=torch.float32, device=dev)
+        scal = torch.empty(2, dtype=torch.int64, device=dev)  # [n_det, thr(float bits)]
+    else:
+        det_yx, det_val, scal = out
     n_host = C.c_int64(0)
     _lib.check(L.vmf_blur_lap_detect(
         _ptr(x), code, h, w, _pitch(x), C.byref(row.s), C.byref(col.s), float(lap_scale),
@@ -140,18 +147,35 @@ def blur_laplacian_detect(img, lpf, frac: float = 0.5, col_stage=None, lap_scale
 
 def detect_sweep(img, stages, frac: float = 0.5, lap_scales=None, cap: int = 1 << 18):
     """One frame through the fused single-scale path once per blur stage
-    (config 3's IIR-vs-FIR scale sweep): the frame is uploaded once, each
-    scale's detections come back to the host.  Returns a list of Detections."""
+    (config 3's IIR-vs-FIR scale sweep): the frame is uploaded once, all
+    scales are queued back to back without host synchronisation, and the
+    detections of every scale come back in one device-to-host copy.
+    Returns a list of Detections (numpy arrays)."""
     x, kind, code = _as_image(img)
-    out = []
+    ns = len(stages)
+    if ns == 0:
+        return []
+    dev = x.device
+    cap = max(int(cap), 1)
+    det_yx = torch.empty((ns, cap, 2), dtype=torch.int32, device=dev)
+    det_val = torch.empty((ns, cap), dtype=torch.float32, device=dev)
+    scal = torch.empty((ns, 2), dtype=torch.int64, device=dev)
     for i, st in enumerate(stages):
-        stg = _Stage(st)
+        stg = st if isinstance(st, _Stage) else _Stage(st)
         sc = 1.0 if lap_scales is None else float(lap_scales[i])
-        det_yx, det_val, scal, n = _fused(x, code, stg, stg, sc, frac, None, None, cap, True)
+        _fused(x, code, stg, stg, sc, frac, None, None, cap, False,
+               out=(det_yx[i], det_val[i], scal[i]))
+    head = scal.cpu()                                   # counts + thresholds
+    ns_det = head[:, 0].tolist()
+    thr = head[:, 1:2].contiguous().view(torch.float32)[:, 0].tolist()
+    mmax = min(max(ns_det), cap)
+    yx = det_yx[:, :mmax].cpu().numpy()
+    val = det_val[:, :mmax].cpu().numpy()
+    out = []
+    for i in range(ns):
+        n = int(ns_det[i])
         m = min(n, cap)
-        thr = float(scal[1:2].view(torch.float32)[0].item())
-        yx, val = det_yx[:m].cpu().numpy(), det_val[:m].cpu().numpy()
-        out.append(Detections(yx[:, 0], yx[:, 1], val, thr, n, n > cap))
+        out.append(Detections(yx[i, :m, 0], yx[i, :m, 1], val[i, :m], float(thr[i]), n, n > cap))
     return out
 
 

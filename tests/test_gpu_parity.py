@@ -241,3 +241,20 @@ def test_candidate_overflow_fallback_matches(cat, monkeypatch):
     np.testing.assert_array_equal(fast.y, slow.y)
     np.testing.assert_array_equal(fast.x, slow.x)
     np.testing.assert_array_equal(fast.value, slow.value)
+
+
+def test_detect_sweep_matches_single_scale_calls(cat):
+    """detect_sweep queues every scale without host synchronisation and reads
+    all results back at once; each scale must equal the one-call path."""
+    D = _D()
+    x = synth.config3_frame(1024)
+    names = synth.CONFIG_STAGES[3]["iir"][:3] + ["g4_k16"]
+    sweep = D.detect_sweep(x, [cat[n] for n in names], frac=0.5)
+    assert len(sweep) == len(names)
+    for name, got in zip(names, sweep):
+        ref = D.blur_laplacian_detect(x, cat[name], frac=0.5)
+        assert got.count == ref.count > 0, name
+        assert got.threshold == ref.threshold, name
+        np.testing.assert_array_equal(got.y, ref.y)
+        np.testing.assert_array_equal(got.x, ref.x)
+        np.testing.assert_array_equal(got.value, ref.value)
