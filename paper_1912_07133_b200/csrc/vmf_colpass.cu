@@ -497,11 +497,17 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
 #pragma unroll
   for (int i = 0; i < K; ++i) Xf[i] = TX(K - 1 - i);  // rows r0-1-i (clamped at the top)
   const double lsc = (double)p.lap_scale;
-  double Bm2 = 0.0, Bm1 = 0.0, Lxm1 = 0.0;  // sliding state (rows r-2, r-1)
-  auto lx_of = [&](double bc) {  // Lx by lane shuffles; warp-edge lanes recomputed later
+  // 5-point Laplacian as (left + right) + (up + down) - 4 centre: the
+  // horizontal neighbour sum of row r-1 comes from lane shuffles when B(r-1)
+  // is produced (warp-edge lanes are recomputed after the walk)
+  double Bm2 = 0.0, Bm1 = 0.0, Sxm1 = 0.0;  // sliding state (rows r-2, r-1)
+  auto sx_of = [&](double bc) {
     double bl = __shfl_up_sync(0xffffffffu, bc, 1);
     double br = __shfl_down_sync(0xffffffffu, bc, 1);
-    return (bl - 2.0 * bc) + br;
+    return bl + br;
+  };
+  auto lap = [&](double sx, double bu, double bc, double bd) {
+    return (float)(lsc * fma(-4.0, bc, sx + (bu + bd)));
   };
   float tmax = 0.0f;  // running max |L| of this column (valid columns, non-edge lanes)
   // lanes 0, 1, 30, 31 keep B(r0-2 .. r1+1) for the warp-edge recomputation
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         double ym2 = dfi<K>(p, Xb, Yb);
         Bm1 = fma(p.sign, ym1, fma(p.b0, x1, Yf[0]));
         Bm2 = fma(p.sign, ym2, fma(p.b0, x2, Yf[1]));
-        Lxm1 = lx_of(Bm1);
+        Sxm1 = sx_of(Bm1);
         if (keep_b) {
           ebw[0] = Bm2;
           ebw[1] = Bm1;
@@ -553,14 +559,14 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         double y = dfi<K>(p, Xf, Yf);
         double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
         push2<K>(Yf, y, Xf, xv);
-        double lx = lx_of(Bt);
-        const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + Bt)));
+        const double sx = sx_of(Bt);
+        const float v = lap(Sxm1, Bm2, Bm1, Bt);
         lp[t * kTileStride] = v;
         tmax = fmaxf(tmax, fabsf(v));
         if (keep_b) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
-        Lxm1 = lx;
+        Sxm1 = sx;
       }
     } else {
 #pragma unroll
@@ -571,17 +577,17 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
         push2<K>(Yf, y, Xf, xv);
         if (r == 0) Bm1 = Bt;  // replicate top edge: B(-1) = B(0)
-        double lx = lx_of(Bt);
+        const double sx = sx_of(Bt);
         const double bnext = r >= H ? Bm1 : Bt;  // replicate bottom edge
         if (r >= 1) {
-          const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + bnext)));
+          const float v = lap(Sxm1, Bm2, Bm1, bnext);
           lp[t * kTileStride] = v;
           if (r - 1 < H) tmax = fmaxf(tmax, fabsf(v));
         }
         if (keep_b) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
-        Lxm1 = lx;
+        Sxm1 = sx;
       }
     }
     if (last) {  // B at rows r1, r1+1 -> L(r1-1), L(r1)
@@ -592,14 +598,14 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
       double y1 = dfi<K>(p, Xf, Yf);
       double B1 = fma(p.sign, Ybot[0], fma(p.b0, xr1, y0));
       double B2 = fma(p.sign, Ybot[1], fma(p.b0, xr2, y1));
-      const double lx1 = lx_of(B1);
+      const double sx1 = sx_of(B1);
       if (r1 - 1 < H) {
-        const float v = (float)(lsc * (Lxm1 + ((Bm2 - 2.0 * Bm1) + (r1 >= H ? Bm1 : B1))));
+        const float v = lap(Sxm1, Bm2, Bm1, r1 >= H ? Bm1 : B1);
         tcol[(tr1 - 1) * kTileStride] = v;
         tmax = fmaxf(tmax, fabsf(v));
       }
       if (r1 < H) {
-        const float v = (float)(lsc * (lx1 + ((Bm1 - 2.0 * B1) + (r1 + 1 >= H ? B1 : B2))));
+        const float v = lap(sx1, Bm1, B1, r1 + 1 >= H ? B1 : B2);
         tcol[tr1 * kTileStride] = v;
         tmax = fmaxf(tmax, fabsf(v));
       }
@@ -633,8 +639,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
       const double bl = side ? S.eb[wid][2][q] : S.eb[wid - 1][3][q];
       const double br = side ? S.eb[wid + 1][0][q] : S.eb[wid][1][q];
       const double bc = bcv[q];
-      const double lx = (bl - 2.0 * bc) + br;
-      const float v = (float)(lsc * (lx + ((bcv[qu] - 2.0 * bc) + bcv[qd])));
+      const float v = lap(bl + br, bcv[qu], bc, bcv[qd]);
       S.tile[r - r0 + K][jj + 2] = v;
       const int64_t cj = c0 - kColHalo + jj;
       if (cj >= 0 && cj < p.W) pmax = fmaxf(pmax, fabsf(v));
@@ -647,6 +652,10 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
   }
   __syncthreads();
+  // publish this CTA's max now (later CTAs prune with it) and pick up what
+  // earlier CTAs published since this one started
+  if (j == 0) atomicMax(&st->absmax_bits, S.cmax);
+  const float gnow = fmaxf(gbound, __uint_as_float(*(volatile unsigned *)&st->absmax_bits));
 
   // ---- store the owned L block (rows r0 .. r1-1, columns c0 .. c0+123) ----
   // fused with the strict 3x3 NMS over frac * max(this CTA's max |L|, the
@@ -655,7 +664,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   {
     const int nrow = (int)(rown_hi - r0);
     const int ncol = (int)(p.W - c0 < kColOut ? p.W - c0 : kColOut);
-    const float th = p.frac * fmaxf(__uint_as_float(S.cmax), gbound);
+    const float th = p.frac * fmaxf(__uint_as_float(S.cmax), gnow);
     auto test = [&](int q, int c, float v) {  // tile row q + K, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
       if (r < 1 || r > H - 2 || cc < 1 || cc > p.W - 2) return;
@@ -685,6 +694,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
       const bool act = lane < kColOut / 4;
       const uint64_t lpol = l2_policy_evict_first();  // L streams out
       float *dst = Lout + r0 * ldl + c0 + 4 * lane;
+#pragma unroll 4
       for (int q = wid; q < nrow; q += kColThreads / 32) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (act) {
