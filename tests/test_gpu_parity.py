@@ -156,6 +156,19 @@ def test_run_to_run_determinism(cat):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("name", ["rp4_k2", "rp8"])
+def test_fused_path_determinism_full_frame(cat, name):
+    """Bitwise-identical L and detections over repeated fused calls on a
+    full 4096^2 frame (thousands of CTAs in flight: races would show)."""
+    D = _D()
+    x = torch.as_tensor(synth.config3_frame(4096)).cuda()
+    runs = [D.blur_laplacian_detect(x, cat[name], return_fields=True) for _ in range(3)]
+    for d, _, lap in runs[1:]:
+        assert torch.equal(lap, runs[0][2])
+        assert d.count == runs[0][0].count
+        assert torch.equal(d.y, runs[0][0].y) and torch.equal(d.x, runs[0][0].x)
+
+
 def test_derivative_field(cat, golden):
     E = _E()
     x = _f32(golden["in/rand"])
