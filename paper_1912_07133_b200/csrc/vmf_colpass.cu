@@ -37,6 +37,7 @@
 #include "vmf_common.cuh"
 #include "vmf_prof.cuh"
 #include "vmf_stage4.cuh"
+#include "vmf_dfi.cuh"
 #include "vmf_tma.cuh"
 
 namespace vmf {
@@ -472,16 +473,23 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
 #pragma unroll
   for (int i = 0; i < K; ++i) E0[i] = Ybot[i];
   if (nsub == 2) {
-    double zb[K];
+    double zb[K], zo[K];  // even / odd samples: two independent FMA chains per i
 #pragma unroll
-    for (int i = 0; i < K; ++i) zb[i] = 0.0;
+    for (int i = 0; i < K; ++i) zb[i] = zo[i] = 0.0;
 #pragma unroll
     for (int t = 0; t < kSub; ++t) {
       double v = TX(K + kSub + t);
 #pragma unroll
       for (int i = 0; i < K; ++i)
-        if (t - i > 0) zb[i] = fma(p.h[t - i], v, zb[i]);
+        if (t - i > 0) {
+          if (t & 1)
+            zo[i] = fma(p.h[t - i], v, zo[i]);
+          else
+            zb[i] = fma(p.h[t - i], v, zb[i]);
+        }
     }
+#pragma unroll
+    for (int i = 0; i < K; ++i) zb[i] += zo[i];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       double acc = zb[i];
@@ -500,11 +508,17 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   // 5-point Laplacian as (left + right) + (up + down) - 4 centre: the
   // horizontal neighbour sum of row r-1 comes from lane shuffles when B(r-1)
   // is produced (warp-edge lanes are recomputed after the walk)
-  double Bm2 = 0.0, Bm1 = 0.0, Sxm1 = 0.0;  // sliding state (rows r-2, r-1)
-  auto sx_of = [&](double bc) {
-    double bl = __shfl_up_sync(0xffffffffu, bc, 1);
-    double br = __shfl_down_sync(0xffffffffu, bc, 1);
-    return bl + br;
+  //
+  // Software-pipelined so that no long dependency chain sits inside one
+  // row step: the lane shuffles of B(r) are consumed one step later, the
+  // part of L(r-1) that does not involve B(r) is formed before B(r) exists,
+  // and the recursion itself is the latency-pipelined DfiRun (one fma on the
+  // loop-carried value per row).
+  double Bm2 = 0.0, Bm1 = 0.0;  // B of rows r-2, r-1
+  double blp = 0.0, brp = 0.0;  // shuffles of B(r-1) (left / right neighbour)
+  auto shfl_lr = [&](double bc) {
+    blp = __shfl_up_sync(0xffffffffu, bc, 1);
+    brp = __shfl_down_sync(0xffffffffu, bc, 1);
   };
   auto lap = [&](double sx, double bu, double bc, double bd) {
     return (float)(lsc * fma(-4.0, bc, sx + (bu + bd)));
@@ -516,6 +530,8 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
 
   // The walk leaves L(r0-1 .. r1) in the tile (in place of x); lanes 0 / 31
   // hold placeholders until the recomputation below.
+  DfiRun<K> rf;
+  rf.init(p, Yf, Xf);
   for (int s = 0; s < nsub; ++s) {
     const int64_t rb = r0 + (int64_t)s * kSub;
     const int trb = K + s * kSub;  // tile row of rb
@@ -528,21 +544,17 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         Yb[i] = last ? Ybot[i] : E0[i];
         Xb[i] = TX(trb + kSub + i);
       }
+      DfiRun<K> rb_;
+      rb_.init(p, Yb, Xb);
 #pragma unroll
-      for (int t = kSub - 1; t >= 0; --t) {
-        double xv = TX(trb + t);
-        double y = dfi<K>(p, Xb, Yb);
-        park[t] = y;
-        push2<K>(Yb, y, Xb, xv);
-      }
+      for (int t = kSub - 1; t >= 0; --t) park[t] = p.sign * rb_.step(p, TX(trb + t));  // sign*y-
       if (s == 0 && r0 > 0) {  // B at rows r0-2, r0-1 from the band-edge histories
         double x1 = TX(K - 1), x2 = TX(K - 2);
-        double ym1 = dfi<K>(p, Xb, Yb);
-        push2<K>(Yb, ym1, Xb, x1);
-        double ym2 = dfi<K>(p, Xb, Yb);
+        double ym1 = rb_.step(p, x1);
+        double ym2 = rb_.step(p, x2);
         Bm1 = fma(p.sign, ym1, fma(p.b0, x1, Yf[0]));
         Bm2 = fma(p.sign, ym2, fma(p.b0, x2, Yf[1]));
-        Sxm1 = sx_of(Bm1);
+        shfl_lr(Bm1);
         if (keep_b) {
           ebw[0] = Bm2;
           ebw[1] = Bm1;
@@ -555,52 +567,50 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     if (rb >= 1 && rb + kSub < H) {  // no image edge in reach
 #pragma unroll
       for (int t = 0; t < kSub; ++t) {
-        double xv = TX(trb + t);
-        double y = dfi<K>(p, Xf, Yf);
-        double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
-        push2<K>(Yf, y, Xf, xv);
-        const double sx = sx_of(Bt);
-        const float v = lap(Sxm1, Bm2, Bm1, Bt);
+        const double pre = lsc * fma(-4.0, Bm1, (blp + brp) + Bm2);  // L(r-1) without B(r)
+        const double xv = TX(trb + t);
+        const double ct = fma(p.b0, xv, park[t]);
+        const double Bt = rf.step(p, xv) + ct;
+        shfl_lr(Bt);
+        const float v = (float)fma(lsc, Bt, pre);
         lp[t * kTileStride] = v;
         tmax = fmaxf(tmax, fabsf(v));
         if (keep_b) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
-        Sxm1 = sx;
       }
     } else {
 #pragma unroll
       for (int t = 0; t < kSub; ++t) {
         const int64_t r = rb + t;
-        double xv = TX(trb + t);
-        double y = dfi<K>(p, Xf, Yf);
-        double Bt = fma(p.sign, park[t], fma(p.b0, xv, y));
-        push2<K>(Yf, y, Xf, xv);
+        const double xv = TX(trb + t);
+        const double Bt = rf.step(p, xv) + fma(p.b0, xv, park[t]);
         if (r == 0) Bm1 = Bt;  // replicate top edge: B(-1) = B(0)
-        const double sx = sx_of(Bt);
+        const double sxm1 = blp + brp;
+        shfl_lr(Bt);
         const double bnext = r >= H ? Bm1 : Bt;  // replicate bottom edge
         if (r >= 1) {
-          const float v = lap(Sxm1, Bm2, Bm1, bnext);
+          const float v = (float)fma(lsc, bnext, lsc * fma(-4.0, Bm1, sxm1 + Bm2));
           lp[t * kTileStride] = v;
           if (r - 1 < H) tmax = fmaxf(tmax, fabsf(v));
         }
         if (keep_b) ep[t] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
-        Sxm1 = sx;
       }
     }
     if (last) {  // B at rows r1, r1+1 -> L(r1-1), L(r1)
       const int tr1 = K + len;
       double xr1 = TX(tr1), xr2 = TX(tr1 + 1);
-      double y0 = dfi<K>(p, Xf, Yf);
-      push2<K>(Yf, y0, Xf, xr1);
-      double y1 = dfi<K>(p, Xf, Yf);
+      double y0 = rf.step(p, xr1);
+      double y1 = rf.step(p, xr2);
       double B1 = fma(p.sign, Ybot[0], fma(p.b0, xr1, y0));
       double B2 = fma(p.sign, Ybot[1], fma(p.b0, xr2, y1));
-      const double sx1 = sx_of(B1);
+      const double sxm1 = blp + brp;
+      shfl_lr(B1);
+      const double sx1 = blp + brp;
       if (r1 - 1 < H) {
-        const float v = lap(Sxm1, Bm2, Bm1, r1 >= H ? Bm1 : B1);
+        const float v = lap(sxm1, Bm2, Bm1, r1 >= H ? Bm1 : B1);
         tcol[(tr1 - 1) * kTileStride] = v;
         tmax = fmaxf(tmax, fabsf(v));
       }

@@ -28,6 +28,7 @@
 #include <cstring>
 
 #include "vmf_common.cuh"
+#include "vmf_dfi.cuh"
 #include "vmf_iir.cuh"
 #include "vmf_prof.cuh"
 #include "vmf_rowpass.cuh"
@@ -234,6 +235,9 @@ __device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row *xr,
       Yf[g][i] = c > 0 ? cfr[g][(c - 1) * K + i] : p.yss * x0;
     }
   }
+  DfiRun<K> rb[NR];
+#pragma unroll
+  for (int g = 0; g < NR; ++g) rb[g].init(p, Yb[g], Xb[g]);
 #pragma unroll
   for (int q = kChunk / 4 - 1; q >= 0; --q) {
     float e[NR][4];
@@ -249,21 +253,8 @@ __device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row *xr,
     for (int u = 3; u >= 0; --u) {
 #pragma unroll
       for (int g = 0; g < NR; ++g) {
-        double xv = (double)e[g][u];
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m < K; ++m) s = fma(p.b[m], Xb[g][m], s);
-#pragma unroll
-        for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yb[g][m], s);
-        s = fma(-p.a[0], Yb[g][0], s);
+        const double s = rb[g].step(p, (double)e[g][u]);
         park[g][4 * q + u] = (float)(p.sign * s);
-#pragma unroll
-        for (int m = K - 1; m > 0; --m) {
-          Yb[g][m] = Yb[g][m - 1];
-          Xb[g][m] = Xb[g][m - 1];
-        }
-        Yb[g][0] = s;
-        Xb[g][0] = xv;
       }
     }
   }
@@ -274,6 +265,9 @@ template <int K, int NR, class Row>
 __device__ __forceinline__ void row_apply_fwd(const RowParams &p, const Row *xr, int c,
                                               const float (*park)[kChunk], double (*Xf)[K],
                                               double (*Yf)[K]) {
+  DfiRun<K> rf[NR];
+#pragma unroll
+  for (int g = 0; g < NR; ++g) rf[g].init(p, Yf[g], Xf[g]);
 #pragma unroll
   for (int q = 0; q < kChunk / 4; ++q) {
     float e[NR][4], o[NR][4];
@@ -289,21 +283,9 @@ __device__ __forceinline__ void row_apply_fwd(const RowParams &p, const Row *xr,
     for (int u = 0; u < 4; ++u) {
 #pragma unroll
       for (int g = 0; g < NR; ++g) {
-        double xv = (double)e[g][u];
-        double s = 0.0;
-#pragma unroll
-        for (int m = 0; m < K; ++m) s = fma(p.b[m], Xf[g][m], s);
-#pragma unroll
-        for (int m = K - 1; m >= 1; --m) s = fma(-p.a[m], Yf[g][m], s);
-        s = fma(-p.a[0], Yf[g][0], s);
+        const double xv = (double)e[g][u];
+        const double s = rf[g].step(p, xv);
         o[g][u] = (float)(fma(p.b0, xv, s) + (double)park[g][4 * q + u]);
-#pragma unroll
-        for (int m = K - 1; m > 0; --m) {
-          Yf[g][m] = Yf[g][m - 1];
-          Xf[g][m] = Xf[g][m - 1];
-        }
-        Yf[g][0] = s;
-        Xf[g][0] = xv;
       }
     }
 #pragma unroll
@@ -389,6 +371,22 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
   }
 }
 
+#ifdef VMF_PHASE_PROF
+__device__ unsigned long long g_row_phase[8];
+#define PH(i)                                                        \
+  do {                                                               \
+    if (c == 0) {                                                    \
+      long long t_ = clock64();                                      \
+      atomicAdd(&g_row_phase[i], (unsigned long long)(t_ - ph_t0)); \
+      ph_t0 = t_;                                                    \
+    }                                                                \
+  } while (0)
+#else
+#define PH(i) \
+  do {        \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // kernel 2 (fp32, W = 32 C): persistent, NR rows per step, TMA in and out.
 // A step's rows are one SWIZZLE_128B box [NR][C][32]; the box of the next
@@ -431,15 +429,20 @@ __global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kern
     cfr[g] = cf + g * C * K;
     cbr[g] = cb + g * C * K;
   }
+#ifdef VMF_PHASE_PROF
+  long long ph_t0 = clock64();
+#endif
   for (int64_t r = rlo; r < rhi; r += NR, b ^= 1) {
     SwzRow xr[NR];
 #pragma unroll
     for (int g = 0; g < NR; ++g) xr[g].base = buf0 + b * stepb + g * rowb;
     mbar_wait(&bar[b], (phases >> b) & 1u);
     phases ^= 1u << b;
+    PH(0);
 #pragma unroll
     for (int g = 0; g < NR; ++g) row_carry<K>(p, xr[g], c, C, Wp, cfr[g], cbr[g]);
     __syncthreads();
+    PH(1);
     if (c == 0 && r + NR < rhi) {
       // buffer b^1 last held the previous step, whose TMA store was issued a
       // full step ago: wait until it has been read out, then refill
@@ -451,18 +454,22 @@ __global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kern
     for (int task = c >> 5; task < 2 * NR; task += (int)(blockDim.x >> 5))
       row_scan<K>(p, (task & 1) == 0 ? cfr[task >> 1] : cbr[task >> 1], task & 1, C, c & 31);
     __syncthreads();
+    PH(2);
     float park[NR][kChunk];
     double Xf[NR][K], Yf[NR][K];
     row_apply_bwd<K, NR>(p, xr, c, C, Wp, cfr, cbr, park, Xf, Yf);
     __syncthreads();  // every halo read (and cf / cb) before chunks are overwritten
+    PH(3);
     row_apply_fwd<K, NR>(p, xr, c, park, Xf, Yf);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
     __syncthreads();
+    PH(4);
     if (c == 0) {
       if (r == rlo) pdl_wait();  // T may still be read by the previous scale's column pass
       tma_store_3d_hint(&ymap, buf0 + b * stepb, 0, 0, (int)r, l2_policy_evict_last());
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
+    PH(5);
   }
   pdl_trigger();
   if (c == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
@@ -684,3 +691,14 @@ template int rowpass_run<uint16_t>(const uint16_t *, int64_t, float *, int64_t,
                                    const IirParams &, int64_t, int64_t, cudaStream_t);
 
 }  // namespace vmf
+
+#ifdef VMF_PHASE_PROF
+extern "C" int vmf_debug_row_phases(double *out, int n) {
+  unsigned long long h[8] = {0};
+  cudaMemcpyFromSymbol(h, vmf::g_row_phase, sizeof(h));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(vmf::g_row_phase, z, sizeof(z));
+  for (int i = 0; i < n && i < 8; ++i) out[i] = (double)h[i];
+  return 8;
+}
+#endif
