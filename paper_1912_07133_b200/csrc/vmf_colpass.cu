@@ -827,25 +827,30 @@ __global__ void __launch_bounds__(kFinThreads) colfinal_kernel(
   unsigned long long *key = reinterpret_cast<unsigned long long *>(fsm);
   float *val = reinterpret_cast<float *>(fsm + kSortCap * sizeof(unsigned long long));
   __shared__ int m;
+  // one CTA: let the next kernel (the next scale's row pass, which waits for
+  // this grid before it overwrites anything this kernel reads) start now
+  pdl_trigger();
   pdl_wait();
-  const float thr = frac * __uint_as_float(st->absmax_bits);
+  const CandState cs = *st;
+  const float thr = frac * __uint_as_float(cs.absmax_bits);
   if (threadIdx.x == 0) {
     m = 0;
     if (thr_out) *thr_out = thr;
   }
   __syncthreads();
-  const int n = st->count < gcap ? st->count : gcap;
+  const int n = cs.count < gcap ? cs.count : gcap;
   for (int q = threadIdx.x; q < n; q += blockDim.x) {
-    float v = gv[q];
+    const float v = gv[q];
+    const int yy = gy[q], xx = gx[q];  // loaded together: one round trip
     if (!(fabsf(v) >= thr)) continue;
     int k = atomicAdd(&m, 1);
     if (k < kSortCap) {
-      key[k] = (unsigned long long)gy[q] * (unsigned long long)W + (unsigned long long)gx[q];
+      key[k] = (unsigned long long)yy * (unsigned long long)W + (unsigned long long)xx;
       val[k] = v;
     }
   }
   __syncthreads();
-  if (force_full || st->overflow || m > kSortCap) {  // buffer overflow: exact, slow path
+  if (force_full || cs.overflow || m > kSortCap) {  // buffer overflow: exact, slow path
     final_fullscan(L, ldl, H, W, thr, det_yx, det_val, cap, n_det);
     return;
   }
