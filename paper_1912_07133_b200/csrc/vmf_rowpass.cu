@@ -215,10 +215,10 @@ __device__ __forceinline__ void row_scan(const RowParams &p, double *cc, int dir
 //    the column pass, tools/experiments/park_precision.py); also returns the
 //    forward start history.  Reads only x.  NR rows are walked in lockstep so
 //    the scheduler sees NR independent recursion chains.
-template <int K, int NR, class Row>
+template <int K, int NR, class Row, typename PT>
 __device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row *xr, int c, int C,
                                               int Wp, double *const *cfr, double *const *cbr,
-                                              float (*park)[kChunk], double (*Xf)[K],
+                                              PT (*park)[kChunk], double (*Xf)[K],
                                               double (*Yf)[K]) {
   const int n0 = c * kChunk;
   double Xb[NR][K], Yb[NR][K];
@@ -254,16 +254,16 @@ __device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row *xr,
 #pragma unroll
       for (int g = 0; g < NR; ++g) {
         const double s = rb[g].step(p, (double)e[g][u]);
-        park[g][4 * q + u] = (float)(p.sign * s);
+        park[g][4 * q + u] = (PT)(p.sign * s);
       }
     }
   }
 }
 
 // d. apply, forward half: out(n) = b0 x + y+ + parked sign*y-, in place.
-template <int K, int NR, class Row>
+template <int K, int NR, class Row, typename PT>
 __device__ __forceinline__ void row_apply_fwd(const RowParams &p, const Row *xr, int c,
-                                              const float (*park)[kChunk], double (*Xf)[K],
+                                              const PT (*park)[kChunk], double (*Xf)[K],
                                               double (*Yf)[K]) {
   DfiRun<K> rf[NR];
 #pragma unroll
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
   double *cfr[1] = {cf + rr * C * K}, *cbr[1] = {cb + rr * C * K};
   if (active) row_apply_bwd<K, 1>(p, &xr, c, C, Wp, cfr, cbr, park, Xf, Yf);
   __syncthreads();  // every halo read before any chunk is overwritten
-  if (active) row_apply_fwd<K, 1>(p, &xr, c, park, Xf, Yf);
+  if (active) row_apply_fwd<K, 1>(p, &xr, c, (const float(*)[kChunk])park, Xf, Yf);
   __syncthreads();
 
   // ---- e. store --------------------------------------------------------------
@@ -399,13 +399,13 @@ template <int K, int NR>
 __global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
     RowParams p) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_tma[];
   __shared__ __align__(8) uint64_t bar[2];
   const int C = p.C, Wp = C * kChunk;
   const int rowb = Wp * (int)sizeof(float);
   const int stepb = NR * rowb;
-  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
-  char *buf0 = reinterpret_cast<char *>(smem_raw) + ((1024u - (sbase & 1023u)) & 1023u);
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_tma);
+  char *buf0 = reinterpret_cast<char *>(smem_tma) + ((1024u - (sbase & 1023u)) & 1023u);
   double *cf = reinterpret_cast<double *>(buf0 + 2 * stepb);  // [NR][C][K]
   double *cb = cf + NR * C * K;
   const int c = threadIdx.x;
@@ -455,12 +455,17 @@ __global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kern
       row_scan<K>(p, (task & 1) == 0 ? cfr[task >> 1] : cbr[task >> 1], task & 1, C, c & 31);
     __syncthreads();
     PH(2);
-    float park[NR][kChunk];
+#ifdef VMF_PARK32
+    typedef float ParkT;
+#else
+    typedef double ParkT;  // fp64 park: no F2F pair per sample (the XU pipe is the busy one)
+#endif
+    ParkT park[NR][kChunk];
     double Xf[NR][K], Yf[NR][K];
     row_apply_bwd<K, NR>(p, xr, c, C, Wp, cfr, cbr, park, Xf, Yf);
     __syncthreads();  // every halo read (and cf / cb) before chunks are overwritten
     PH(3);
-    row_apply_fwd<K, NR>(p, xr, c, park, Xf, Yf);
+    row_apply_fwd<K, NR>(p, xr, c, (const ParkT(*)[kChunk])park, Xf, Yf);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
     __syncthreads();
     PH(4);
