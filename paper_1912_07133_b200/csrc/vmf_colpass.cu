@@ -89,8 +89,9 @@ __device__ __forceinline__ void carry_half(const ColParams &p, const float *tile
   }
 #pragma unroll
   for (int t = 0; t < kHalf; ++t) {
-    double a = xa[t], c = xb[t];
-    double u = a + c, v = a - c;
+    // pair sums in fp32 (one conversion per sum; the rounding is that of an
+    // fp32 input)
+    const double u = (double)(xa[t] + xb[t]), v = (double)(xa[t] - xb[t]);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       P[i] = fma(p.SP[i][t0 + t], u, P[i]);

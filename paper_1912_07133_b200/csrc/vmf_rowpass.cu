@@ -94,8 +94,10 @@ __device__ __forceinline__ void row_carry(const RowParams &p, const Row &xr, int
   }
 #pragma unroll
   for (int t = 0; t < kChunk / 2; ++t) {
-    const double xa = xv[t], xb = xv[kChunk - 1 - t];
-    const double u = xa + xb, v = xa - xb;
+    // pair sums in fp32 (one conversion per sum instead of per sample; the
+    // rounding is that of an fp32 input)
+    const double u = (double)(xv[t] + xv[kChunk - 1 - t]);
+    const double v = (double)(xv[t] - xv[kChunk - 1 - t]);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       P[i] = fma(p.SP32[i][t], u, P[i]);
