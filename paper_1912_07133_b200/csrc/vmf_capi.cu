@@ -7,6 +7,7 @@
 #include "vmf_common.cuh"
 #include "vmf_iir.cuh"
 #include "vmf_colpass.cuh"
+#include "vmf_firpass.cuh"
 #include "vmf_stage4.cuh"
 
 namespace vmf {
@@ -145,6 +146,11 @@ static bool fused_col(const vmf_stage *col_stage, int64_t h, int64_t w) {
          !getenv("VMF_FORCE_GENERIC");
 }
 
+static bool fused_fir_col(const vmf_stage *col_stage, int64_t h, int64_t w) {
+  return col_stage && col_stage->kind == VMF_STAGE_FIR &&
+         firpass_supported(h, w, col_stage->n) && !getenv("VMF_FORCE_GENERIC");
+}
+
 // workspace: [T row-pass out][B if blur_out NULL][L if lap_out NULL][iir carry][detect]
 size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage,
                                            const vmf_stage *col_stage) {
@@ -155,6 +161,10 @@ size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage
   if (fused_col(col_stage, h, w)) {
     size_t c3 = colpass_workspace_bytes(h, w, col_stage->n, 0);
     if (c3 > carry) carry = c3;
+  }
+  if (fused_fir_col(col_stage, h, w)) {
+    size_t c4 = firpass_workspace_bytes(h, w);
+    if (c4 > carry) carry = c4;
   }
   return 3 * img + align256(carry) + align256(detect_workspace_bytes(1, h, w)) + 256;
 }
@@ -200,6 +210,22 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
                      thr_dev, carry, carry_b, st);
     if (rc) return rc;
     if (blur_out) {  // B is not materialised by the fused pass; recompute on request
+      rc = run_stage<COLS>(col_stage, T, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);
+      if (rc) return rc;
+    }
+    if (n_det_host) {
+      cudaMemcpyAsync(n_det_host, n_det_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      return cuda_status("detect readback");
+    }
+    return VMF_OK;
+  }
+  if (fused_fir_col(col_stage, h, w) && frac > 0.0f) {
+    // column FIR + Laplacian + NMS in one pass over T (vmf_firpass.cu)
+    rc = firpass_run(T, w, L, w, col_stage->taps, col_stage->n, h, w, lap_scale, frac, det_yx,
+                     det_val, cap, n_det_dev, thr_dev, carry, carry_b, st);
+    if (rc) return rc;
+    if (blur_out) {
       rc = run_stage<COLS>(col_stage, T, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);
       if (rc) return rc;
     }

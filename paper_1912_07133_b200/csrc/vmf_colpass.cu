@@ -974,6 +974,25 @@ size_t colpass_workspace_bytes(int64_t h, int64_t w, int k, int64_t) {
          detect_workspace_bytes(1, h, w);
 }
 
+int64_t colpass_cand_capacity(int64_t h, int64_t w) { return cand_capacity(h, w); }
+
+int colfinal_launch(CandState *cs, const int *gy, const int *gx, const float *gv, int64_t gcap,
+                    const float *L, int64_t ldl, int64_t H, int64_t W, float frac,
+                    int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
+                    float *thr_dev, cudaStream_t st) {
+  Launch g(K_FINALIZE, st);
+  const int fsmem = kSortCap * (int)(sizeof(unsigned long long) + sizeof(float));
+  static bool fattr = false;
+  if (!fattr) {
+    cudaFuncSetAttribute(colfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+    fattr = true;
+  }
+  launch_pdl(colfinal_kernel, dim3(1), dim3(kFinThreads), fsmem, st, cs, gy, gx, gv, (int)gcap, L,
+             ldl, H, W, frac, det_yx, det_val, cap, n_det_dev, thr_dev,
+             getenv("VMF_FORCE_FULLSCAN") ? 1 : 0);
+  return cuda_status("finaliser");
+}
+
 template <int K>
 static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, const ColParams &p,
                           int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
@@ -1038,19 +1057,8 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
                L, ldl, p, (const double *)Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
                (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
   }
-  {
-    Launch g(K_FINALIZE, st);
-    const int fsmem = kSortCap * (int)(sizeof(unsigned long long) + sizeof(float));
-    static bool fattr = false;
-    if (!fattr) {
-      cudaFuncSetAttribute(colfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
-      fattr = true;
-    }
-    launch_pdl(colfinal_kernel, dim3(1), dim3(kFinThreads), fsmem, st, cs, (const int *)gy,
-               (const int *)gx, (const float *)gv, (int)gcap, (const float *)L, ldl, p.H, p.W,
-               p.frac, det_yx, det_val, cap, n_det_dev, thr_dev,
-               getenv("VMF_FORCE_FULLSCAN") ? 1 : 0);
-  }
+  colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, p.H, p.W, p.frac, det_yx, det_val, cap,
+                  n_det_dev, thr_dev, st);
   return cuda_status("column pass");
 }
 

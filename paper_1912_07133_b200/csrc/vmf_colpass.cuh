@@ -39,6 +39,13 @@ struct CandState {
 };
 
 bool colpass_supported(int64_t h, int64_t w, int k);
+// candidate list capacity of the fused column passes (IIR and FIR)
+int64_t colpass_cand_capacity(int64_t h, int64_t w);
+// final threshold + (y, x) order of the candidates a fused column pass appended
+int colfinal_launch(CandState *cs, const int *gy, const int *gx, const float *gv, int64_t gcap,
+                    const float *L, int64_t ldl, int64_t H, int64_t W, float frac,
+                    int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
+                    float *thr_dev, cudaStream_t st);
 size_t colpass_workspace_bytes(int64_t h, int64_t w, int k, int64_t cand_cap);
 // T (fp32, h x w, pitch ldt) -> L (pitch ldl) + detections (sorted by y, x).
 int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,

@@ -10,7 +10,10 @@
 // Tiling: a CTA owns a tile of outputs and stages the input window (tile +
 // 2k halo, edge-clamped) in shared memory once, so each input element is read
 // from L2/HBM once per tile instead of (2k+1) times.
+#include <cstdlib>
+
 #include "vmf_common.cuh"
+#include "vmf_firpass.cuh"
 #include "vmf_iir.cuh"
 #include "vmf_prof.cuh"
 
@@ -140,10 +143,17 @@ int fir_pass(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t
   int64_t length = O == ROWS ? w : h;
   if (ntaps > length)
     return fail(VMF_EVALUE, "kernel length %d exceeds row length %lld", ntaps, (long long)length);
-  if (x_dtype == VMF_F32)
+  // rows up to kFirMaxFast taps: the register-blocked kernel (vmf_firpass.cu)
+  const bool fast = O == ROWS && ntaps <= kFirMaxFast && !getenv("VMF_FIR_GENERIC");
+  if (x_dtype == VMF_F32) {
+    if (fast) return fir_rows_fast<float>((const float *)x, ldx, y, ldy, h, w, taps, ntaps, st);
     return fir_bucket<O>((const float *)x, ldx, y, ldy, h, w, taps, ntaps, st);
-  if (x_dtype == VMF_U16)
+  }
+  if (x_dtype == VMF_U16) {
+    if (fast)
+      return fir_rows_fast<uint16_t>((const uint16_t *)x, ldx, y, ldy, h, w, taps, ntaps, st);
     return fir_bucket<O>((const uint16_t *)x, ldx, y, ldy, h, w, taps, ntaps, st);
+  }
   return fail(VMF_EVALUE, "unsupported dtype");
 }
 

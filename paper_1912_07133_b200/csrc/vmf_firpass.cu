@@ -1,0 +1,350 @@
+// vmf_firpass.cu -- the FIR blur of the hot path on B200 (SURVEY.md §8 a3/a4,
+// north star: "a tiled shared-memory FIR kernel ... for impulse responses up
+// to hundreds of taps" and the fused second pass + Laplacian + NMS).
+//
+//   out(n) = sum_{m=-k..k} taps[k+m] x(clamp(n-m))   (_conv_rows_kernel,
+//   engine.py:35-62; conv_cols engine.py:124-126 for the columns)
+//
+// fp64 accumulation (a 257-tap Gaussian misses the 1e-4 Laplacian tolerance
+// with fp32 accumulation), fp32 in and out.  Both kernels
+// are register-blocked: a thread owns 8 consecutive outputs along the filter
+// direction and slides a 16-value fp64 window over the staged input, so every
+// input read from shared memory feeds 8 DFMAs and every tap (a uniform
+// constant-bank load) feeds 8 DFMAs; the FMA pipe, not the LSU, is the limit.
+//
+// fir_rows_fast_kernel: CTA = 1024 outputs of one row; the input window (1024
+//   + taps, edge-clamped) is staged in shared memory once.
+// firapply_kernel: the column pass fused with the Laplacian and detection:
+//   CTA = 128 computed (124 owned) columns x 32 B rows (28 owned L rows).  The
+//   column window (32 + taps rows x 132 columns, edge-clamped, fp32) is staged
+//   with cp.async; B is kept in fp64 in shared memory (it never rounds to fp32
+//   before the Laplacian), L = lsc (Bl + Br + Bu + Bd - 4 Bc) is formed from it
+//   with replicate edges, and the owned block is stored as float4 rows fused
+//   with the strict 3x3 NMS over frac * max(CTA max, global max so far) -- the
+//   same candidate protocol as the IIR column pass, finished by colfinal.
+#include <cstdlib>
+#include <cstring>
+
+#include "vmf_colpass.cuh"
+#include "vmf_common.cuh"
+#include "vmf_firpass.cuh"
+#include "vmf_prof.cuh"
+
+namespace vmf {
+
+constexpr int kFirTapsPad = kFirMaxFast + 15;  // reversed taps, zero-padded to a multiple of 8
+
+struct FirTapsP {
+  double t[kFirTapsPad];  // t[i] = taps[n-1-i] (i < n), 0 beyond
+  int n, np;              // taps, taps rounded up to a multiple of 8
+};
+
+static void fir_plan(FirTapsP *tp, const double *taps, int ntaps) {
+  memset(tp, 0, sizeof(*tp));
+  for (int i = 0; i < ntaps; ++i) tp->t[i] = taps[ntaps - 1 - i];
+  tp->n = ntaps;
+  tp->np = (ntaps + 7) / 8 * 8;
+}
+
+// acc[j] += sum_i t[i] * w(base + j + i), w(q) read through `ld` (fp32 -> fp64)
+template <class LD>
+__device__ __forceinline__ void fir8(const FirTapsP &tp, LD ld, double *acc) {
+  double xw[16];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) xw[j] = ld(j);
+  for (int mb = 0; mb < tp.np; mb += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xw[8 + j] = ld(mb + 8 + j);
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+      const double tap = tp.t[mb + mm];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = fma(tap, xw[j + mm], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xw[j] = xw[8 + j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// row pass
+// ---------------------------------------------------------------------------
+constexpr int kFrSeg = 1024, kFrThreads = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(kFrThreads) fir_rows_fast_kernel(const T *__restrict__ x,
+                                                                   int64_t ldx,
+                                                                   float *__restrict__ y,
+                                                                   int64_t ldy, int64_t h,
+                                                                   int64_t w, FirTapsP tp,
+                                                                   int vec_out) {
+  extern __shared__ __align__(16) float fwin[];  // [kFrSeg + np + 16]
+  const int k = (tp.n - 1) / 2;
+  const int nwin = kFrSeg + tp.np + 16;
+  const int64_t n0 = (int64_t)blockIdx.x * kFrSeg;
+  const int base = 8 * threadIdx.x;
+  for (int64_t row = blockIdx.y; row < h; row += gridDim.y) {
+    __syncthreads();
+    const T *xr = x + row * ldx;
+    for (int q = threadIdx.x; q < nwin; q += blockDim.x) {
+      int64_t c = n0 - k + q;
+      c = c < 0 ? 0 : (c >= w ? w - 1 : c);
+      fwin[q] = (float)__ldg(xr + c);
+    }
+    __syncthreads();
+    if (n0 + base >= w) continue;
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    const float *wp = fwin + base;
+    fir8(tp, [&](int q) { return (double)wp[q]; }, acc);
+    float *yr = y + row * ldy + n0 + base;
+    if (vec_out && n0 + base + 8 <= w) {
+      reinterpret_cast<float4 *>(yr)[0] = make_float4((float)acc[0], (float)acc[1],
+                                                       (float)acc[2], (float)acc[3]);
+      reinterpret_cast<float4 *>(yr)[1] = make_float4((float)acc[4], (float)acc[5],
+                                                       (float)acc[6], (float)acc[7]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (n0 + base + j < w) yr[j] = (float)acc[j];
+    }
+  }
+}
+
+template <typename T>
+int fir_rows_fast(const T *x, int64_t ldx, float *y, int64_t ldy, int64_t h, int64_t w,
+                  const double *taps, int ntaps, cudaStream_t st) {
+  FirTapsP tp;
+  fir_plan(&tp, taps, ntaps);
+  const size_t smem = (size_t)(kFrSeg + tp.np + 16) * sizeof(float);
+  const int vec = (ldy % 4 == 0) && ((uintptr_t)y % 16 == 0);
+  dim3 grid((unsigned)cdiv(w, kFrSeg), (unsigned)(h < 65535 ? h : 65535));
+  Launch g(K_FIR_ROWS, st);
+  fir_rows_fast_kernel<T><<<grid, kFrThreads, smem, st>>>(x, ldx, y, ldy, h, w, tp, vec);
+  return cuda_status("fir row pass");
+}
+
+template int fir_rows_fast<float>(const float *, int64_t, float *, int64_t, int64_t, int64_t,
+                                  const double *, int, cudaStream_t);
+template int fir_rows_fast<uint16_t>(const uint16_t *, int64_t, float *, int64_t, int64_t,
+                                     int64_t, const double *, int, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// fused column pass
+// ---------------------------------------------------------------------------
+constexpr int kFcCols = 128;                // computed columns (c0-2 .. c0+125)
+constexpr int kFcOut = kFcCols - 4;         // owned columns
+constexpr int kFcGroups = 4;                // row groups of 8 B rows
+constexpr int kFcThreads = kFcCols * kFcGroups;
+constexpr int kFcRB = 8 * kFcGroups;        // B rows r0-2 .. r0+29
+constexpr int kFcOwn = kFcRB - 4;           // owned L rows r0 .. r0+27
+constexpr int kFcLR = kFcRB - 2;            // L rows r0-1 .. r0+28
+constexpr int kFcStride = kFcCols + 4;      // tile columns c0-4 .. c0+127
+constexpr int kFcCand = 256;
+
+static size_t fc_region_bytes(int np) {
+  const size_t win = (size_t)(kFcRB + np + 8) * kFcStride * sizeof(float);
+  const size_t bl = (size_t)kFcRB * kFcCols * sizeof(double) +
+                    (size_t)kFcLR * kFcStride * sizeof(float);
+  return (win > bl ? win : bl + 0);
+}
+
+struct FcSmall {
+  int cy[kFcCand], cx[kFcCand];
+  float cv[kFcCand];
+  int ccount, coverflow;
+  unsigned cmax;
+};
+
+__global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
+    const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, int64_t H,
+    int64_t W, FirTapsP tp, float lap_scale, float frac, CandState *__restrict__ st,
+    int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv, int gcap, int vec_out) {
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  __shared__ FcSmall S;
+  float *win = reinterpret_cast<float *>(fsm_raw);  // [kFcRB + np + 8][kFcStride]
+  double *Bs = reinterpret_cast<double *>(fsm_raw);  // [kFcRB][kFcCols] (after the window)
+  float *Ls = reinterpret_cast<float *>(fsm_raw + (size_t)kFcRB * kFcCols * sizeof(double));
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int j = tid & (kFcCols - 1), g = tid / kFcCols;
+  const int k = (tp.n - 1) / 2;
+  const int64_t c0 = (int64_t)blockIdx.x * kFcOut;
+  const int64_t r0 = (int64_t)blockIdx.y * kFcOwn;
+  const int64_t rB0 = r0 - 2;  // image row of B tile row 0
+  const int wrows = kFcRB + tp.np + 8;
+  if (tid == 0) {
+    S.ccount = 0;
+    S.coverflow = 0;
+    S.cmax = 0u;
+  }
+  pdl_wait();
+  // ---- stage the column window: row w <-> image row rB0 - k + w, column
+  //      cc <-> image column c0 - 4 + cc, both edge-clamped ----------------
+  for (int idx = tid; idx < wrows * kFcStride; idx += kFcThreads) {
+    const int wr = idx / kFcStride, cc = idx - wr * kFcStride;
+    int64_t r = rB0 - k + wr, c = c0 - 4 + cc;
+    r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+    c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(win + idx);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + c));
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // ---- B rows 8g .. 8g+7 of column j (tile column j + 2) -------------------
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  {
+    const float *wp = win + (8 * g) * kFcStride + j + 2;
+    fir8(tp, [&](int q) { return (double)wp[q * kFcStride]; }, acc);
+  }
+  __syncthreads();  // the window is dead: B and L reuse its space
+#pragma unroll
+  for (int q = 0; q < 8; ++q) Bs[(8 * g + q) * kFcCols + j] = acc[q];
+  __syncthreads();
+  // ---- L rows r0-1 .. r0+28, columns 1 .. 126 (replicate edges) ----------
+  const double lsc = (double)lap_scale;
+  float tmax = 0.0f;
+  for (int idx = tid; idx < kFcLR * kFcCols; idx += kFcThreads) {
+    const int lr = idx / kFcCols, jj = idx - lr * kFcCols;
+    const int64_t r = r0 - 1 + lr, c = c0 - 2 + jj;
+    if (jj == 0 || jj == kFcCols - 1 || r < 0 || r >= H) continue;
+    const int64_t ru = r > 0 ? r - 1 : 0, rd = r + 1 < H ? r + 1 : H - 1;
+    const double *bc = Bs + (r - rB0) * kFcCols + jj;
+    // columns outside the image were filtered from clamped inputs, so they
+    // already hold the replicated edge column
+    const double bl = bc[-1], br = bc[1];
+    const double bu = Bs[(ru - rB0) * kFcCols + jj], bd = Bs[(rd - rB0) * kFcCols + jj];
+    const float v = (float)(lsc * fma(-4.0, bc[0], (bl + br) + (bu + bd)));
+    Ls[lr * kFcStride + jj + 2] = v;
+    if (c >= 0 && c < W) tmax = fmaxf(tmax, fabsf(v));
+  }
+  tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+  if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
+  pdl_trigger();
+  __syncthreads();
+  if (tid == 0) atomicMax(&st->absmax_bits, S.cmax);
+  const float gnow = __uint_as_float(*(volatile unsigned *)&st->absmax_bits);
+  // ---- owned block out (float4 rows) + strict 3x3 NMS ---------------------
+  {
+    const int nrow = (int)(H - r0 < kFcOwn ? H - r0 : kFcOwn);
+    const int ncol = (int)(W - c0 < kFcOut ? W - c0 : kFcOut);
+    const float th = frac * fmaxf(__uint_as_float(S.cmax), gnow);
+    auto test = [&](int q, int c, float v) {  // L tile row q + 1, tile column 4 + c
+      const int64_t r = r0 + q, cc = c0 + c;
+      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return;
+      const float *lp = Ls + (q + 1) * kFcStride + 4 + c;
+      bool gt = true, lt = true;
+#pragma unroll
+      for (int di = -1; di <= 1; ++di)
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj) {
+          if (!di && !dj) continue;
+          const float u = lp[di * kFcStride + dj];
+          gt &= v > u;
+          lt &= v < u;
+        }
+      if (gt || lt) {
+        int kk = atomicAdd(&S.ccount, 1);
+        if (kk < kFcCand) {
+          S.cy[kk] = (int)r;
+          S.cx[kk] = (int)cc;
+          S.cv[kk] = v;
+        } else {
+          S.coverflow = 1;
+        }
+      }
+    };
+    if (vec_out && ncol == kFcOut) {
+      if (lane < kFcOut / 4) {
+        float *dst = Lout + r0 * ldl + c0 + 4 * lane;
+        for (int q = wid; q < nrow; q += kFcThreads / 32) {
+          const float4 v = *reinterpret_cast<const float4 *>(Ls + (q + 1) * kFcStride + 4 + 4 * lane);
+          *reinterpret_cast<float4 *>(dst + q * ldl) = v;
+          const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+          if (m4 >= th) {
+            if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
+            if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
+            if (fabsf(v.z) >= th) test(q, 4 * lane + 2, v.z);
+            if (fabsf(v.w) >= th) test(q, 4 * lane + 3, v.w);
+          }
+        }
+      }
+    } else {
+      for (int q = wid; q < nrow; q += kFcThreads / 32)
+        for (int cl = lane; cl < ncol; cl += 32) {
+          const float v = Ls[(q + 1) * kFcStride + 4 + cl];
+          Lout[(r0 + q) * ldl + c0 + cl] = v;
+          if (fabsf(v) >= th) test(q, cl, v);
+        }
+    }
+  }
+  __syncthreads();
+  // ---- flush the candidates that survive the best threshold known now -----
+  __shared__ float thr_end;
+  if (tid == 0) {
+    unsigned old = atomicMax(&st->absmax_bits, S.cmax);
+    thr_end = frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
+    if (S.coverflow) st->overflow = 1;
+  }
+  __syncthreads();
+  const int n = S.ccount < kFcCand ? S.ccount : kFcCand;
+  for (int q = tid; q < n; q += kFcThreads) {
+    if (!(fabsf(S.cv[q]) >= thr_end)) continue;
+    int kk = atomicAdd(&st->count, 1);
+    if (kk < gcap) {
+      gy[kk] = S.cy[q];
+      gx[kk] = S.cx[q];
+      gv[kk] = S.cv[q];
+    } else {
+      st->overflow = 1;
+    }
+  }
+}
+
+bool firpass_supported(int64_t h, int64_t w, int ntaps) {
+  if (ntaps < 1 || ntaps > kFirMaxFast || h < 4 || w < 4) return false;
+  const int np = (ntaps + 7) / 8 * 8;
+  return fc_region_bytes(np) + sizeof(FcSmall) + 1024 <= 227 * 1024;
+}
+
+size_t firpass_workspace_bytes(int64_t h, int64_t w) {
+  return 4096 + (size_t)colpass_cand_capacity(h, w) * 12 + 256;
+}
+
+int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double *taps, int ntaps,
+                int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
+                float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
+                size_t ws_bytes, cudaStream_t st) {
+  if (!firpass_supported(h, w, ntaps))
+    return fail(VMF_EVALUE, "fused FIR column pass does not support %d taps at %lldx%lld", ntaps,
+                (long long)h, (long long)w);
+  if (!ws || ws_bytes < firpass_workspace_bytes(h, w))
+    return fail(VMF_EVALUE, "FIR column-pass workspace too small");
+  FirTapsP tp;
+  fir_plan(&tp, taps, ntaps);
+  char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  CandState *cs = (CandState *)base;
+  const int64_t gcap = colpass_cand_capacity(h, w);
+  int *gy = (int *)(base + 4096);
+  int *gx = gy + gcap;
+  float *gv = (float *)(gx + gcap);
+  cudaMemsetAsync(cs, 0, sizeof(CandState), st);
+  const size_t smem = fc_region_bytes(tp.np);
+  {
+    Launch g(K_FIR_COLS, st);
+    cudaFuncSetAttribute(firapply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    dim3 grid((unsigned)cdiv(w, kFcOut), (unsigned)cdiv(h, kFcOwn));
+    launch_pdl(firapply_kernel, grid, dim3(kFcThreads), smem, st, T, ldt, L, ldl, h, w, tp,
+               lap_scale, frac, cs, gy, gx, gv, (int)gcap,
+               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
+  }
+  int rc = cuda_status("fir column pass");
+  if (rc) return rc;
+  return colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, h, w, frac, det_yx, det_val, cap,
+                         n_det_dev, thr_dev, st);
+}
+
+}  // namespace vmf

@@ -1,0 +1,25 @@
+// vmf_firpass.cuh -- the FIR hot path: register-blocked row FIR and the fused
+// column FIR + Laplacian + 3x3 NMS (vmf_firpass.cu).
+#pragma once
+#include "vmf_common.cuh"
+
+namespace vmf {
+
+constexpr int kFirMaxFast = 257;  // taps of the fused FIR path (longer: generic kernels)
+
+bool firpass_supported(int64_t h, int64_t w, int ntaps);
+size_t firpass_workspace_bytes(int64_t h, int64_t w);
+
+// row pass: y = conv_rows(x, taps) (fp32 / u16 in, fp32 out, fp64 accumulation)
+template <typename T>
+int fir_rows_fast(const T *x, int64_t ldx, float *y, int64_t ldy, int64_t h, int64_t w,
+                  const double *taps, int ntaps, cudaStream_t st);
+
+// column FIR of T + Laplacian + threshold / 3x3 NMS; L (pitch ldl) and the
+// sorted detections like colpass_run
+int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double *taps, int ntaps,
+                int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
+                float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
+                size_t ws_bytes, cudaStream_t st);
+
+}  // namespace vmf
