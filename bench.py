@@ -277,13 +277,21 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = mpx * len(iir) * ws * args.steps / (ms / 1e3)
 
-    # per-scale IIR vs FIR (BASELINE metric), flushed, 3 reps each
+    # per-scale IIR vs FIR (BASELINE metric): each scale captured as its own
+    # CUDA graph (device time, no host launch overhead), L2 flushed, 5 reps
     per_scale = {"iir": {}, "fir": {}}
     for fam, stages in (("iir", iir), ("fir", fir)):
         for sg, stg in zip(SIGMAS, stages):
             one_scale(stg)
-            t = timed(lambda: one_scale(stg), 3) / 3
+            torch.cuda.synchronize()
+            g1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1):
+                one_scale(stg)
+            g1.replay()
+            torch.cuda.synchronize()
+            t = timed(g1.replay, 5) / 5
             per_scale[fam][f"{sg:g}"] = round(mpx / (t / 1e3), 1)
+            del g1
 
     # in-situ kernel timing over the same timed steps (events per launch)
     # (a second graph of the same step with event record nodes around every
