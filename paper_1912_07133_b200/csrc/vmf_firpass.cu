@@ -133,22 +133,28 @@ template int fir_rows_fast<uint16_t>(const uint16_t *, int64_t, float *, int64_t
 // ---------------------------------------------------------------------------
 // fused column pass
 // ---------------------------------------------------------------------------
-constexpr int kFcCols = 128;                // computed columns (c0-2 .. c0+125)
-constexpr int kFcOut = kFcCols - 4;         // owned columns
-constexpr int kFcGroups = 4;                // row groups of 8 B rows
-constexpr int kFcThreads = kFcCols * kFcGroups;
-constexpr int kFcRB = 8 * kFcGroups;        // B rows r0-2 .. r0+29
-constexpr int kFcOwn = kFcRB - 4;           // owned L rows r0 .. r0+27
-constexpr int kFcLR = kFcRB - 2;            // L rows r0-1 .. r0+28
-constexpr int kFcStride = kFcCols + 4;      // tile columns c0-4 .. c0+127
+// Tile shapes: COLS computed columns (COLS-4 owned), GROUPS groups of 8 B rows
+// (8 GROUPS - 4 owned L rows).  Short FIRs: 128 x 4 (two CTAs per SM); long
+// FIRs: 64 x 16, so the 2k-row halo of the column window is shared by 124 B
+// rows instead of 28 (less re-staging per output).
+template <int COLS, int GROUPS>
+struct FcShape {
+  static constexpr int kCols = COLS, kOut = COLS - 4, kGroups = GROUPS;
+  static constexpr int kThreads = COLS * GROUPS;
+  static constexpr int kRB = 8 * GROUPS;  // B rows r0-2 .. r0+kRB-3
+  static constexpr int kOwn = kRB - 4;    // owned L rows r0 .. r0+kOwn-1
+  static constexpr int kLR = kRB - 2;     // L rows r0-1 .. r0+kOwn
+  static constexpr int kStride = COLS + 4;
+  static size_t region_bytes(int np) {
+    const size_t win = (size_t)(kRB + np + 8) * kStride * sizeof(float);
+    const size_t bl = (size_t)kRB * kCols * sizeof(double) + (size_t)kLR * kStride * sizeof(float);
+    return win > bl ? win : bl;
+  }
+};
+using FcShort = FcShape<128, 4>;
+using FcLong = FcShape<64, 16>;
+constexpr int kFcLongTaps = 64;  // np above this: the long tile
 constexpr int kFcCand = 256;
-
-static size_t fc_region_bytes(int np) {
-  const size_t win = (size_t)(kFcRB + np + 8) * kFcStride * sizeof(float);
-  const size_t bl = (size_t)kFcRB * kFcCols * sizeof(double) +
-                    (size_t)kFcLR * kFcStride * sizeof(float);
-  return (win > bl ? win : bl + 0);
-}
 
 struct FcSmall {
   int cy[kFcCand], cx[kFcCand];
@@ -157,22 +163,23 @@ struct FcSmall {
   unsigned cmax;
 };
 
-__global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
+template <class SH>
+__global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, int64_t H,
     int64_t W, FirTapsP tp, float lap_scale, float frac, CandState *__restrict__ st,
     int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv, int gcap, int vec_out) {
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   __shared__ FcSmall S;
-  float *win = reinterpret_cast<float *>(fsm_raw);  // [kFcRB + np + 8][kFcStride]
-  double *Bs = reinterpret_cast<double *>(fsm_raw);  // [kFcRB][kFcCols] (after the window)
-  float *Ls = reinterpret_cast<float *>(fsm_raw + (size_t)kFcRB * kFcCols * sizeof(double));
+  float *win = reinterpret_cast<float *>(fsm_raw);  // [SH::kRB + np + 8][SH::kStride]
+  double *Bs = reinterpret_cast<double *>(fsm_raw);  // [SH::kRB][SH::kCols] (after the window)
+  float *Ls = reinterpret_cast<float *>(fsm_raw + (size_t)SH::kRB * SH::kCols * sizeof(double));
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int j = tid & (kFcCols - 1), g = tid / kFcCols;
+  const int j = tid & (SH::kCols - 1), g = tid / SH::kCols;
   const int k = (tp.n - 1) / 2;
-  const int64_t c0 = (int64_t)blockIdx.x * kFcOut;
-  const int64_t r0 = (int64_t)blockIdx.y * kFcOwn;
+  const int64_t c0 = (int64_t)blockIdx.x * SH::kOut;
+  const int64_t r0 = (int64_t)blockIdx.y * SH::kOwn;
   const int64_t rB0 = r0 - 2;  // image row of B tile row 0
-  const int wrows = kFcRB + tp.np + 8;
+  const int wrows = SH::kRB + tp.np + 8;
   if (tid == 0) {
     S.ccount = 0;
     S.coverflow = 0;
@@ -181,8 +188,8 @@ __global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
   pdl_wait();
   // ---- stage the column window: row w <-> image row rB0 - k + w, column
   //      cc <-> image column c0 - 4 + cc, both edge-clamped ----------------
-  for (int idx = tid; idx < wrows * kFcStride; idx += kFcThreads) {
-    const int wr = idx / kFcStride, cc = idx - wr * kFcStride;
+  for (int idx = tid; idx < wrows * SH::kStride; idx += SH::kThreads) {
+    const int wr = idx / SH::kStride, cc = idx - wr * SH::kStride;
     int64_t r = rB0 - k + wr, c = c0 - 4 + cc;
     r = r < 0 ? 0 : (r >= H ? H - 1 : r);
     c = c < 0 ? 0 : (c >= W ? W - 1 : c);
@@ -196,28 +203,28 @@ __global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q] = 0.0;
   {
-    const float *wp = win + (8 * g) * kFcStride + j + 2;
-    fir8(tp, [&](int q) { return (double)wp[q * kFcStride]; }, acc);
+    const float *wp = win + (8 * g) * SH::kStride + j + 2;
+    fir8(tp, [&](int q) { return (double)wp[q * SH::kStride]; }, acc);
   }
   __syncthreads();  // the window is dead: B and L reuse its space
 #pragma unroll
-  for (int q = 0; q < 8; ++q) Bs[(8 * g + q) * kFcCols + j] = acc[q];
+  for (int q = 0; q < 8; ++q) Bs[(8 * g + q) * SH::kCols + j] = acc[q];
   __syncthreads();
   // ---- L rows r0-1 .. r0+28, columns 1 .. 126 (replicate edges) ----------
   const double lsc = (double)lap_scale;
   float tmax = 0.0f;
-  for (int idx = tid; idx < kFcLR * kFcCols; idx += kFcThreads) {
-    const int lr = idx / kFcCols, jj = idx - lr * kFcCols;
+  for (int idx = tid; idx < SH::kLR * SH::kCols; idx += SH::kThreads) {
+    const int lr = idx / SH::kCols, jj = idx - lr * SH::kCols;
     const int64_t r = r0 - 1 + lr, c = c0 - 2 + jj;
-    if (jj == 0 || jj == kFcCols - 1 || r < 0 || r >= H) continue;
+    if (jj == 0 || jj == SH::kCols - 1 || r < 0 || r >= H) continue;
     const int64_t ru = r > 0 ? r - 1 : 0, rd = r + 1 < H ? r + 1 : H - 1;
-    const double *bc = Bs + (r - rB0) * kFcCols + jj;
+    const double *bc = Bs + (r - rB0) * SH::kCols + jj;
     // columns outside the image were filtered from clamped inputs, so they
     // already hold the replicated edge column
     const double bl = bc[-1], br = bc[1];
-    const double bu = Bs[(ru - rB0) * kFcCols + jj], bd = Bs[(rd - rB0) * kFcCols + jj];
+    const double bu = Bs[(ru - rB0) * SH::kCols + jj], bd = Bs[(rd - rB0) * SH::kCols + jj];
     const float v = (float)(lsc * fma(-4.0, bc[0], (bl + br) + (bu + bd)));
-    Ls[lr * kFcStride + jj + 2] = v;
+    Ls[lr * SH::kStride + jj + 2] = v;
     if (c >= 0 && c < W) tmax = fmaxf(tmax, fabsf(v));
   }
   tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
@@ -228,20 +235,20 @@ __global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
   const float gnow = __uint_as_float(*(volatile unsigned *)&st->absmax_bits);
   // ---- owned block out (float4 rows) + strict 3x3 NMS ---------------------
   {
-    const int nrow = (int)(H - r0 < kFcOwn ? H - r0 : kFcOwn);
-    const int ncol = (int)(W - c0 < kFcOut ? W - c0 : kFcOut);
+    const int nrow = (int)(H - r0 < SH::kOwn ? H - r0 : SH::kOwn);
+    const int ncol = (int)(W - c0 < SH::kOut ? W - c0 : SH::kOut);
     const float th = frac * fmaxf(__uint_as_float(S.cmax), gnow);
     auto test = [&](int q, int c, float v) {  // L tile row q + 1, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
       if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return;
-      const float *lp = Ls + (q + 1) * kFcStride + 4 + c;
+      const float *lp = Ls + (q + 1) * SH::kStride + 4 + c;
       bool gt = true, lt = true;
 #pragma unroll
       for (int di = -1; di <= 1; ++di)
 #pragma unroll
         for (int dj = -1; dj <= 1; ++dj) {
           if (!di && !dj) continue;
-          const float u = lp[di * kFcStride + dj];
+          const float u = lp[di * SH::kStride + dj];
           gt &= v > u;
           lt &= v < u;
         }
@@ -256,11 +263,11 @@ __global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
         }
       }
     };
-    if (vec_out && ncol == kFcOut) {
-      if (lane < kFcOut / 4) {
+    if (vec_out && ncol == SH::kOut) {
+      if (lane < SH::kOut / 4) {
         float *dst = Lout + r0 * ldl + c0 + 4 * lane;
-        for (int q = wid; q < nrow; q += kFcThreads / 32) {
-          const float4 v = *reinterpret_cast<const float4 *>(Ls + (q + 1) * kFcStride + 4 + 4 * lane);
+        for (int q = wid; q < nrow; q += SH::kThreads / 32) {
+          const float4 v = *reinterpret_cast<const float4 *>(Ls + (q + 1) * SH::kStride + 4 + 4 * lane);
           *reinterpret_cast<float4 *>(dst + q * ldl) = v;
           const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
           if (m4 >= th) {
@@ -272,9 +279,9 @@ __global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
         }
       }
     } else {
-      for (int q = wid; q < nrow; q += kFcThreads / 32)
+      for (int q = wid; q < nrow; q += SH::kThreads / 32)
         for (int cl = lane; cl < ncol; cl += 32) {
-          const float v = Ls[(q + 1) * kFcStride + 4 + cl];
+          const float v = Ls[(q + 1) * SH::kStride + 4 + cl];
           Lout[(r0 + q) * ldl + c0 + cl] = v;
           if (fabsf(v) >= th) test(q, cl, v);
         }
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
   }
   __syncthreads();
   const int n = S.ccount < kFcCand ? S.ccount : kFcCand;
-  for (int q = tid; q < n; q += kFcThreads) {
+  for (int q = tid; q < n; q += SH::kThreads) {
     if (!(fabsf(S.cv[q]) >= thr_end)) continue;
     int kk = atomicAdd(&st->count, 1);
     if (kk < gcap) {
@@ -303,14 +310,35 @@ __global__ void __launch_bounds__(kFcThreads, 1) firapply_kernel(
   }
 }
 
+template <class SH>
+static size_t fc_smem(int np) {
+  return SH::region_bytes(np);
+}
+static size_t fc_smem_any(int np) {
+  return np > kFcLongTaps ? fc_smem<FcLong>(np) : fc_smem<FcShort>(np);
+}
+
 bool firpass_supported(int64_t h, int64_t w, int ntaps) {
   if (ntaps < 1 || ntaps > kFirMaxFast || h < 4 || w < 4) return false;
   const int np = (ntaps + 7) / 8 * 8;
-  return fc_region_bytes(np) + sizeof(FcSmall) + 1024 <= 227 * 1024;
+  return fc_smem_any(np) + sizeof(FcSmall) + 1024 <= 227 * 1024;
 }
 
 size_t firpass_workspace_bytes(int64_t h, int64_t w) {
   return 4096 + (size_t)colpass_cand_capacity(h, w) * 12 + 256;
+}
+
+template <class SH>
+static void launch_firapply(const float *T, int64_t ldt, float *L, int64_t ldl, int64_t h,
+                            int64_t w, const FirTapsP &tp, float lap_scale, float frac,
+                            CandState *cs, int *gy, int *gx, float *gv, int64_t gcap, int vec,
+                            cudaStream_t st) {
+  const size_t smem = fc_smem<SH>(tp.np);
+  cudaFuncSetAttribute(firapply_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  dim3 grid((unsigned)cdiv(w, SH::kOut), (unsigned)cdiv(h, SH::kOwn));
+  launch_pdl(firapply_kernel<SH>, grid, dim3(SH::kThreads), smem, st, T, ldt, L, ldl, h, w, tp,
+             lap_scale, frac, cs, gy, gx, gv, (int)gcap, vec);
 }
 
 int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double *taps, int ntaps,
@@ -331,15 +359,15 @@ int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double
   int *gx = gy + gcap;
   float *gv = (float *)(gx + gcap);
   cudaMemsetAsync(cs, 0, sizeof(CandState), st);
-  const size_t smem = fc_region_bytes(tp.np);
   {
     Launch g(K_FIR_COLS, st);
-    cudaFuncSetAttribute(firapply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    dim3 grid((unsigned)cdiv(w, kFcOut), (unsigned)cdiv(h, kFcOwn));
-    launch_pdl(firapply_kernel, grid, dim3(kFcThreads), smem, st, T, ldt, L, ldl, h, w, tp,
-               lap_scale, frac, cs, gy, gx, gv, (int)gcap,
-               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
+    const int vec = (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0);
+    if (tp.np > kFcLongTaps)
+      launch_firapply<FcLong>(T, ldt, L, ldl, h, w, tp, lap_scale, frac, cs, gy, gx, gv, gcap, vec,
+                              st);
+    else
+      launch_firapply<FcShort>(T, ldt, L, ldl, h, w, tp, lap_scale, frac, cs, gy, gx, gv, gcap,
+                               vec, st);
   }
   int rc = cuda_status("fir column pass");
   if (rc) return rc;
