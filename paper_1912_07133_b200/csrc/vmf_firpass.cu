@@ -29,6 +29,7 @@
 #include "vmf_common.cuh"
 #include "vmf_firpass.cuh"
 #include "vmf_prof.cuh"
+#include "vmf_tma.cuh"
 
 namespace vmf {
 
@@ -167,12 +168,17 @@ template <class SH>
 __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, int64_t H,
     int64_t W, FirTapsP tp, float lap_scale, float frac, CandState *__restrict__ st,
-    int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv, int gcap, int vec_out) {
-  extern __shared__ __align__(16) unsigned char fsm_raw[];
+    int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv, int gcap, int vec_out,
+    const __grid_constant__ CUtensorMap tmap, int tma_rows, int tma_boxes) {
+  extern __shared__ __align__(128) unsigned char fsm_raw[];
   __shared__ FcSmall S;
-  float *win = reinterpret_cast<float *>(fsm_raw);  // [SH::kRB + np + 8][SH::kStride]
-  double *Bs = reinterpret_cast<double *>(fsm_raw);  // [SH::kRB][SH::kCols] (after the window)
-  float *Ls = reinterpret_cast<float *>(fsm_raw + (size_t)SH::kRB * SH::kCols * sizeof(double));
+  __shared__ __align__(8) uint64_t fbar;
+  // 128-byte aligned base (TMA destination), derived from the shared array
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(fsm_raw);
+  unsigned char *fsm = fsm_raw + ((128u - (sbase & 127u)) & 127u);
+  float *win = reinterpret_cast<float *>(fsm);  // [kRB + np + 8][kStride]
+  double *Bs = reinterpret_cast<double *>(fsm);  // [kRB][kCols] (after the window)
+  float *Ls = reinterpret_cast<float *>(fsm + (size_t)SH::kRB * SH::kCols * sizeof(double));
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int j = tid & (SH::kCols - 1), g = tid / SH::kCols;
   const int k = (tp.n - 1) / 2;
@@ -188,15 +194,30 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
   pdl_wait();
   // ---- stage the column window: row w <-> image row rB0 - k + w, column
   //      cc <-> image column c0 - 4 + cc, both edge-clamped ----------------
-  for (int idx = tid; idx < wrows * SH::kStride; idx += SH::kThreads) {
-    const int wr = idx / SH::kStride, cc = idx - wr * SH::kStride;
-    int64_t r = rB0 - k + wr, c = c0 - 4 + cc;
-    r = r < 0 ? 0 : (r >= H ? H - 1 : r);
-    c = c < 0 ? 0 : (c >= W ? W - 1 : c);
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(win + idx);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + c));
+  const int64_t rw0 = rB0 - k;  // image row of window row 0
+  const bool tma = tma_boxes > 0 && rw0 >= 0 && rw0 + (int64_t)tma_boxes * tma_rows <= H &&
+                   c0 >= 4 && c0 - 4 + SH::kStride <= W;
+  if (tma) {  // interior tile: tma_boxes boxes of tma_rows x kStride
+    if (tid == 0) {
+      mbar_init(&fbar, 1);
+      mbar_expect_tx(&fbar, (unsigned)(tma_boxes * tma_rows * SH::kStride * sizeof(float)));
+      for (int bx = 0; bx < tma_boxes; ++bx)
+        tma_load_2d_hint(win + bx * tma_rows * SH::kStride, &tmap, &fbar, (int)(c0 - 4),
+                         (int)(rw0 + bx * tma_rows), l2_policy_evict_first());
+    }
+    __syncthreads();
+    mbar_wait(&fbar, 0);
+  } else {
+    for (int idx = tid; idx < wrows * SH::kStride; idx += SH::kThreads) {
+      const int wr = idx / SH::kStride, cc = idx - wr * SH::kStride;
+      int64_t r = rw0 + wr, c = c0 - 4 + cc;
+      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+      c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(win + idx);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + c));
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
   }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
   __syncthreads();
   // ---- B rows 8g .. 8g+7 of column j (tile column j + 2) -------------------
   double acc[8];
@@ -312,7 +333,11 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
 
 template <class SH>
 static size_t fc_smem(int np) {
-  return SH::region_bytes(np);
+  // + room for the rounded-up TMA boxes and the 128-byte alignment
+  const size_t box = (size_t)(SH::kRB + np + 8 + 8 * ((SH::kRB + np + 8 + 255) / 256)) *
+                     SH::kStride * sizeof(float);
+  const size_t r = SH::region_bytes(np);
+  return (r > box ? r : box) + 128;
 }
 static size_t fc_smem_any(int np) {
   return np > kFcLongTaps ? fc_smem<FcLong>(np) : fc_smem<FcShort>(np);
@@ -328,17 +353,31 @@ size_t firpass_workspace_bytes(int64_t h, int64_t w) {
   return 4096 + (size_t)colpass_cand_capacity(h, w) * 12 + 256;
 }
 
+// window rows staged by TMA: nbox boxes of `rows` (<= 256, a multiple of 8)
+template <class SH>
+static void fc_boxes(int np, int *rows, int *nbox) {
+  const int wrows = SH::kRB + np + 8;
+  *nbox = (wrows + 255) / 256;
+  *rows = ((wrows + *nbox - 1) / *nbox + 7) / 8 * 8;
+}
+
 template <class SH>
 static void launch_firapply(const float *T, int64_t ldt, float *L, int64_t ldl, int64_t h,
                             int64_t w, const FirTapsP &tp, float lap_scale, float frac,
                             CandState *cs, int *gy, int *gx, float *gv, int64_t gcap, int vec,
                             cudaStream_t st) {
   const size_t smem = fc_smem<SH>(tp.np);
+  int rows = 0, nbox = 0;
+  fc_boxes<SH>(tp.np, &rows, &nbox);
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (!make_tmap_2d_f32(&tmap, T, h, w, ldt, SH::kStride, rows) || getenv("VMF_NO_TMA")) nbox = 0;
+  cudaGetLastError();
   cudaFuncSetAttribute(firapply_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   dim3 grid((unsigned)cdiv(w, SH::kOut), (unsigned)cdiv(h, SH::kOwn));
   launch_pdl(firapply_kernel<SH>, grid, dim3(SH::kThreads), smem, st, T, ldt, L, ldl, h, w, tp,
-             lap_scale, frac, cs, gy, gx, gv, (int)gcap, vec);
+             lap_scale, frac, cs, gy, gx, gv, (int)gcap, vec, tmap, rows, nbox);
 }
 
 int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double *taps, int ntaps,
