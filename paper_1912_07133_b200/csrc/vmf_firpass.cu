@@ -153,7 +153,7 @@ struct FcShape {
   }
 };
 using FcShort = FcShape<128, 4>;
-using FcLong = FcShape<64, 16>;
+using FcLong = FcShape<64, 8>;
 constexpr int kFcLongTaps = 64;  // np above this: the long tile
 constexpr int kFcCand = 256;
 
