@@ -200,7 +200,7 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   size_t dws_b = align256(detect_workspace_bytes(1, h, w));
   rc = run_stage<ROWS>(row_stage, x, x_dtype, T, h, w, ldx, w, carry, carry_b, st);
   if (rc) return rc;
-  if (fused_col(col_stage, h, w) && frac > 0.0f) {
+  if (fused_col(col_stage, h, w)) {
     // column IIR + Laplacian + NMS in one pass over T (vmf_colpass.cu)
     IirParams ip;
     rc = iir_plan(&ip, w, h, col_stage->b_plus, col_stage->a_plus, col_stage->n,
@@ -213,14 +213,14 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
       rc = run_stage<COLS>(col_stage, T, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);
       if (rc) return rc;
     }
-    if (n_det_host) {
+    if (n_det_host && frac > 0.0f) {
       cudaMemcpyAsync(n_det_host, n_det_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       return cuda_status("detect readback");
     }
     return VMF_OK;
   }
-  if (fused_fir_col(col_stage, h, w) && frac > 0.0f) {
+  if (fused_fir_col(col_stage, h, w)) {
     // column FIR + Laplacian + NMS in one pass over T (vmf_firpass.cu)
     rc = firpass_run(T, w, L, w, col_stage->taps, col_stage->n, h, w, lap_scale, frac, det_yx,
                      det_val, cap, n_det_dev, thr_dev, carry, carry_b, st);
@@ -229,7 +229,7 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
       rc = run_stage<COLS>(col_stage, T, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);
       if (rc) return rc;
     }
-    if (n_det_host) {
+    if (n_det_host && frac > 0.0f) {
       cudaMemcpyAsync(n_det_host, n_det_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       return cuda_status("detect readback");

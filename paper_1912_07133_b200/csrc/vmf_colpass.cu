@@ -675,7 +675,9 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   {
     const int nrow = (int)(rown_hi - r0);
     const int ncol = (int)(p.W - c0 < kColOut ? p.W - c0 : kColOut);
-    const float th = p.frac * fmaxf(__uint_as_float(S.cmax), gnow);
+    // frac <= 0: L only (scale-space stacks), no candidates
+    const float th = p.frac > 0.0f ? p.frac * fmaxf(__uint_as_float(S.cmax), gnow)
+                                   : __int_as_float(0x7f800000);
     auto test = [&](int q, int c, float v) {  // tile row q + K, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
       if (r < 1 || r > H - 2 || cc < 1 || cc > p.W - 2) return;
@@ -1057,8 +1059,9 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
                L, ldl, p, (const double *)Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
                (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
   }
-  colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, p.H, p.W, p.frac, det_yx, det_val, cap,
-                  n_det_dev, thr_dev, st);
+  if (p.frac > 0.0f)
+    colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, p.H, p.W, p.frac, det_yx, det_val, cap,
+                    n_det_dev, thr_dev, st);
   return cuda_status("column pass");
 }
 

@@ -258,7 +258,9 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
   {
     const int nrow = (int)(H - r0 < SH::kOwn ? H - r0 : SH::kOwn);
     const int ncol = (int)(W - c0 < SH::kOut ? W - c0 : SH::kOut);
-    const float th = frac * fmaxf(__uint_as_float(S.cmax), gnow);
+    // frac <= 0: L only (scale-space stacks), no candidates
+    const float th = frac > 0.0f ? frac * fmaxf(__uint_as_float(S.cmax), gnow)
+                                 : __int_as_float(0x7f800000);
     auto test = [&](int q, int c, float v) {  // L tile row q + 1, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
       if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return;
@@ -410,6 +412,7 @@ int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double
   }
   int rc = cuda_status("fir column pass");
   if (rc) return rc;
+  if (frac <= 0.0f) return VMF_OK;
   return colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, h, w, frac, det_yx, det_val, cap,
                          n_det_dev, thr_dev, st);
 }
