@@ -5,7 +5,7 @@
 
 namespace vmf {
 
-constexpr int kFirMaxFast = 257;  // taps of the fused FIR path (longer: generic kernels)
+constexpr int kFirMaxFast = 385;  // taps of the fast FIR paths (longer: generic kernels)
 
 bool firpass_supported(int64_t h, int64_t w, int ntaps);
 size_t firpass_workspace_bytes(int64_t h, int64_t w);

@@ -27,7 +27,7 @@ from .engine import (_as_image, _dptr, _fir_checks, _iir_checks, _pitch, _ptr, _
 from .filters import is_fir, is_iir
 
 __all__ = ["Detections", "make_stage", "blur_laplacian_detect", "detect_sweep",
-           "scale_space_detect"]
+           "scale_space_detect", "stream_detect"]
 
 
 @dataclass
@@ -213,3 +213,61 @@ def scale_space_detect(img, stages, sigmas, frac: float = 0.5, cap: int = 1 << 1
     if return_stack:
         return dets, (stack.cpu().numpy() if kind == "numpy" else stack)
     return dets
+
+
+def stream_detect(frames, stage, frac: float = 0.5, cap: int = 1 << 16):
+    """Config-4 stream front end: a frame stream (n, h, w) of uint16 or
+    float32 in host memory (pin it for full speed) through the fused
+    single-scale path.  Two device frame buffers: the upload of frame i+1
+    runs on a copy stream while frame i is filtered on the current stream;
+    nothing waits for the host until the end, when every frame's detections
+    come back in one copy.  Returns a list of Detections, one per frame."""
+    if isinstance(frames, np.ndarray):
+        frames = torch.from_numpy(np.ascontiguousarray(frames))
+    if frames.ndim != 3 or frames.shape[0] < 1:
+        raise ValueError("frames must be an (n, h, w) array")
+    if frames.dtype not in (torch.uint16, torch.float32):
+        frames = frames.to(torch.float32)
+    n, h, w = frames.shape
+    dev = torch.device("cuda", torch.cuda.current_device())
+    code = _lib.VMF_U16 if frames.dtype == torch.uint16 else _lib.VMF_F32
+    stg = stage if isinstance(stage, _Stage) else _Stage(stage)
+    cap = max(int(cap), 1)
+    det_yx = torch.empty((n, cap, 2), dtype=torch.int32, device=dev)
+    det_val = torch.empty((n, cap), dtype=torch.float32, device=dev)
+    scal = torch.empty((n, 2), dtype=torch.int64, device=dev)
+    comp = torch.cuda.current_stream()
+    if frames.is_cuda:
+        for i in range(n):
+            _fused(frames[i], code, stg, stg, 1.0, frac, None, None, cap, False,
+                   out=(det_yx[i], det_val[i], scal[i]))
+    else:
+        copy = torch.cuda.Stream()
+        bufs = [torch.empty((h, w), dtype=frames.dtype, device=dev) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        for e in free:
+            e.record(comp)
+        for i in range(n):
+            b = i & 1
+            with torch.cuda.stream(copy):
+                copy.wait_event(free[b])          # frame i-2 has been filtered
+                bufs[b].copy_(frames[i], non_blocking=True)
+                ready[b].record(copy)
+            comp.wait_event(ready[b])
+            _fused(bufs[b], code, stg, stg, 1.0, frac, None, None, cap, False,
+                   out=(det_yx[i], det_val[i], scal[i]))
+            bufs[b].record_stream(comp)
+            free[b].record(comp)
+    head = scal.cpu()
+    counts = head[:, 0].tolist()
+    thr = head[:, 1:2].contiguous().view(torch.float32)[:, 0].tolist()
+    mmax = min(max(counts), cap)
+    yx = det_yx[:, :mmax].cpu().numpy()
+    val = det_val[:, :mmax].cpu().numpy()
+    out = []
+    for i in range(n):
+        c = int(counts[i])
+        m = min(c, cap)
+        out.append(Detections(yx[i, :m, 0], yx[i, :m, 1], val[i, :m], float(thr[i]), c, c > cap))
+    return out

@@ -271,3 +271,27 @@ def test_detect_sweep_matches_single_scale_calls(cat):
         np.testing.assert_array_equal(got.y, ref.y)
         np.testing.assert_array_equal(got.x, ref.x)
         np.testing.assert_array_equal(got.value, ref.value)
+
+
+def test_stream_detect_matches_per_frame(cat):
+    """Config-4 stream front end (double-buffered uploads on a copy stream)
+    gives each frame's single-call result; the first frame is also checked
+    against the oracle pipeline."""
+    D = _D()
+    frames = synth.config4_stream(n_frames=4, size=512)
+    host = torch.from_numpy(frames).pin_memory()
+    got = D.stream_detect(host, cat["rp6"], frac=0.5)
+    assert len(got) == 4
+    for f, g in zip(frames, got):
+        ref = D.blur_laplacian_detect(f, cat["rp6"], frac=0.5)
+        assert g.count == ref.count
+        np.testing.assert_array_equal(g.y, ref.y)
+        np.testing.assert_array_equal(g.x, ref.x)
+        np.testing.assert_array_equal(g.value, ref.value)
+    _check_pipeline(frames[0], cat["rp6"], label="config4/stream")
+
+
+def test_fir_fused_long_taps(cat):
+    """385-tap colored SG (config 5's FIR) on the fused FIR column pass."""
+    x = synth.config5_frame(1024)
+    _check_pipeline(x, cat["sg38.4"], label="config5/sg38.4 fused")
