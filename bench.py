@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config 4 / 5 lines")
     return ap.parse_args()
 
 
@@ -341,6 +342,10 @@ def run_ours(args):
     barrier(ws)
     e2e = mpx * len(iir) * ws * args.steps / e2e_s
 
+    other = None
+    if rank == 0 and ws == 1 and not args.no_extra:
+        other = other_configs(cat, flush, stream)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         times, threads = cpu_time_sweep(frame, [cat["rp4"]], 3)
@@ -375,12 +380,87 @@ def run_ours(args):
             "graph": "each timed step is one CUDA-graph replay of the 5-scale sweep",
             "clocks": clk,
             "cpu_baseline": cpu,
+            "other_configs": other,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def other_configs(cat, flush, stream):
+    """Secondary lines (rank 0, N=1): config 4 (u16 stream, sustained end to
+    end with double-buffered uploads) and config 5 (8192^2, Butterworth IIR vs
+    385-tap SG FIR per scale).  Device-timed values are CUDA-graph replays
+    with L2 flushed before each rep."""
+    import torch
+
+    from paper_1912_07133_b200 import _lib, detect, synth
+
+    out = {}
+
+    def graph_ms(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(reps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        del g
+        return tot / reps
+
+    # config 4: 16 frames of 2048^2 u16 (the config's 64-frame stream, shortened
+    # to bound the bench run), rp6, per-frame threshold + NMS
+    frames = synth.config4_stream(n_frames=16)
+    n4, h4, w4 = frames.shape
+    host = torch.from_numpy(frames).pin_memory()
+    st4 = detect.make_stage(cat["rp6"])
+    detect.stream_detect(host[:2], st4)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = detect.stream_detect(host, st4)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    dframes = host.cuda()
+    x4 = dframes[0]
+    lap4 = torch.empty((h4, w4), dtype=torch.float32, device=x4.device)
+    ms4 = graph_ms(lambda: detect._fused(x4, _lib.VMF_U16, st4, st4, 1.0, 0.5, None, lap4,
+                                         1 << 16, False))
+    mpx4 = h4 * w4 / 1e6
+    out["config4"] = {
+        "workload": f"{n4} frames {h4}x{w4} u16, rp6 blur + Laplacian + 3x3 NMS per frame",
+        "e2e_sustained_mpx_s": round(mpx4 * n4 / e2e_s, 1),
+        "e2e_note": "pinned host frames -> device (copy stream, 2 buffers) -> detections back",
+        "device_mpx_s": round(mpx4 / (ms4 / 1e3), 1),
+        "detections_per_frame": int(statistics.median([r.count for r in res]))}
+    del dframes, x4, lap4
+
+    # config 5: 8192^2 fp32, Butterworth sigma 48 (K=2) vs colored SG 385 taps
+    f5 = synth.config5_frame(8192)
+    x5 = torch.from_numpy(f5).cuda()
+    lap5 = torch.empty_like(x5)
+    c5 = {"workload": "8192x8192 fp32, bw48 IIR vs sg38.4 (385-tap) FIR, fused blur + "
+                      "Laplacian + 3x3 NMS"}
+    for name in ("bw48", "sg38.4"):
+        stg = detect.make_stage(cat[name])
+        ms = graph_ms(lambda: detect._fused(x5, _lib.VMF_F32, stg, stg, 1.0, 0.5, None, lap5,
+                                            1 << 18, False))
+        c5[name + "_mpx_s"] = round(8192 * 8192 / 1e6 / (ms / 1e3), 1)
+    out["config5"] = c5
+    del x5, lap5
+    return out
 
 
 def main():
