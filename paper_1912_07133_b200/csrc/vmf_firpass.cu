@@ -87,10 +87,20 @@ __global__ void __launch_bounds__(kFrThreads) fir_rows_fast_kernel(const T *__re
   for (int64_t row = blockIdx.y; row < h; row += gridDim.y) {
     __syncthreads();
     const T *xr = x + row * ldx;
-    for (int q = threadIdx.x; q < nwin; q += blockDim.x) {
-      int64_t c = n0 - k + q;
-      c = c < 0 ? 0 : (c >= w ? w - 1 : c);
-      fwin[q] = (float)__ldg(xr + c);
+    if (sizeof(T) == 4) {  // asynchronous 4-byte copies: the whole window in flight at once
+      for (int q = threadIdx.x; q < nwin; q += blockDim.x) {
+        int64_t c = n0 - k + q;
+        c = c < 0 ? 0 : (c >= w ? w - 1 : c);
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(fwin + q);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(xr + c));
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+    } else {
+      for (int q = threadIdx.x; q < nwin; q += blockDim.x) {
+        int64_t c = n0 - k + q;
+        c = c < 0 ? 0 : (c >= w ? w - 1 : c);
+        fwin[q] = (float)__ldg(xr + c);
+      }
     }
     __syncthreads();
     if (n0 + base >= w) continue;
