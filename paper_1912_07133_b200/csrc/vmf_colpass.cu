@@ -390,7 +390,7 @@ struct ColSmem {
   unsigned int cmax;  // max |L| of this CTA (float bits)
 };
 
-template <int K>
+template <int K, bool UNIT>  // UNIT: lap_scale == 1 (no scaling multiply)
 __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, ColParams p,
     const double *__restrict__ Z, CandState *__restrict__ st, int *__restrict__ gy,
@@ -566,17 +566,28 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     double *ep = ebw + 2 + s * kSub;              // B(rb + t) at ep[t]
     // forward run: B(rb+t); L(rb+t-1) = Lx + Ly as soon as B(rb+t) exists
     if (rb >= 1 && rb + kSub < H) {  // no image edge in reach
+      // row r = rb + t: the x sample and b0 x + sign y- of the NEXT row are
+      // formed one step early, and q = B(r-2) - 4 B(r-1) at the end of the
+      // previous step, so after B(r) only two additions remain before L(r-1)
+      double xn = TX(trb);
+      double cn = fma(p.b0, xn, park[0]);
+      double q = fma(-4.0, Bm1, Bm2);
 #pragma unroll
       for (int t = 0; t < kSub; ++t) {
-        const double pre = lsc * fma(-4.0, Bm1, (blp + brp) + Bm2);  // L(r-1) without B(r)
-        const double xv = TX(trb + t);
-        const double ct = fma(p.b0, xv, park[t]);
+        const double xv = xn, ct = cn;
+        if (t + 1 < kSub) {
+          xn = TX(trb + t + 1);
+          cn = fma(p.b0, xn, park[t + 1]);
+        }
         const double Bt = rf.step(p, xv) + ct;
+        const double sx = blp + brp;  // shuffled when B(r-1) was produced
         shfl_lr(Bt);
-        const float v = (float)fma(lsc, Bt, pre);
+        const double l = sx + (Bt + q);
+        const float v = UNIT ? (float)l : (float)(lsc * l);
         lp[t * kTileStride] = v;
         tmax = fmaxf(tmax, fabsf(v));
         if (keep_b) ep[t] = Bt;
+        q = fma(-4.0, Bt, Bm1);
         Bm2 = Bm1;
         Bm1 = Bt;
       }
@@ -1045,7 +1056,9 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
     Launch g(K_IIR_COLS_FUSED, st);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(colapply_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(colapply_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ColSmem<K>) + 128);
+      cudaFuncSetAttribute(colapply_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(ColSmem<K>) + 128);
       attr = true;
     }
@@ -1055,7 +1068,7 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
     int use_tma = make_tmap_2d_f32(&tmap, T, p.H, p.W, ldt, kTileStride, kTileRows(K)) &&
                   !getenv("VMF_NO_TMA");
     cudaGetLastError();
-    launch_pdl(colapply_kernel<K>, grid, dim3(kColThreads), sizeof(ColSmem<K>) + 128, st, T, ldt,
+    launch_pdl(p.lap_scale == 1.0f ? colapply_kernel<K, true> : colapply_kernel<K, false>, grid, dim3(kColThreads), sizeof(ColSmem<K>) + 128, st, T, ldt,
                L, ldl, p, (const double *)Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
                (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
   }
