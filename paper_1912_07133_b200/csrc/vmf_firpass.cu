@@ -37,7 +37,7 @@ constexpr int kFirTapsPad = kFirMaxFast + 15;  // reversed taps, zero-padded to 
 
 struct FirTapsP {
   double t[kFirTapsPad];  // t[i] = taps[n-1-i] (i < n), 0 beyond
-  int n, np;              // taps, taps rounded up to a multiple of 8
+  int n, np, n4;          // taps; rounded up to a multiple of 8 (window sizes) and of 4 (loop)
 };
 
 static void fir_plan(FirTapsP *tp, const double *taps, int ntaps) {
@@ -45,6 +45,7 @@ static void fir_plan(FirTapsP *tp, const double *taps, int ntaps) {
   for (int i = 0; i < ntaps; ++i) tp->t[i] = taps[ntaps - 1 - i];
   tp->n = ntaps;
   tp->np = (ntaps + 7) / 8 * 8;
+  tp->n4 = (ntaps + 3) / 4 * 4;
 }
 
 // acc[j] += sum_i t[i] * w(base + j + i), w(q) read through `ld` (fp32 -> fp64)
@@ -53,7 +54,8 @@ __device__ __forceinline__ void fir8(const FirTapsP &tp, LD ld, double *acc) {
   double xw[16];
 #pragma unroll
   for (int j = 0; j < 8; ++j) xw[j] = ld(j);
-  for (int mb = 0; mb < tp.np; mb += 8) {
+  int mb = 0;
+  for (; mb + 8 <= tp.n4; mb += 8) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) xw[8 + j] = ld(mb + 8 + j);
 #pragma unroll
@@ -64,6 +66,16 @@ __device__ __forceinline__ void fir8(const FirTapsP &tp, LD ld, double *acc) {
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) xw[j] = xw[8 + j];
+  }
+  if (mb < tp.n4) {  // a last block of 4 taps (the padding to 8 would waste DFMAs)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xw[8 + j] = ld(mb + 8 + j);
+#pragma unroll
+    for (int mm = 0; mm < 4; ++mm) {
+      const double tap = tp.t[mb + mm];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = fma(tap, xw[j + mm], acc[j]);
+    }
   }
 }
 
