@@ -142,6 +142,28 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w,
                     int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host,
                     void *ws, size_t ws_bytes, void *stream);
 
+/* Hessian blob detector (blob.detect): row stage (IIR or
+ * FIR) then a FIR column stage fused with the derivative bank fir_vm_bank(3)
+ * on the fp64 blur, nd = sigma^4 (D20 D02 - D11^2), trace D20 + D02 and the
+ * stationary-point displacement.  Candidates nd > t1 with the polarity
+ * (+1 dark: trace > 0, -1 bright: trace < 0) are appended unordered:
+ * (cy, cx, cnd, cdx, cdy)[0 .. min(count, cap)), *count_dev = all found.
+ * nd_field / trace_field (pitch ldn) are optional fp32 outputs.
+ * vmf_greedy_nms: greedy suppression within r (d^2 <= r2) in the order
+ * (nd desc, y asc, x asc); order[0 .. *n_kept_dev) = kept candidate indices,
+ * strongest first. */
+size_t vmf_hessian_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage);
+int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                       const vmf_stage *row_stage, const vmf_stage *col_stage, double sigma,
+                       double t1, int polarity, float *nd_field, float *trace_field,
+                       int64_t ldn, int32_t *cy, int32_t *cx, double *cnd, float *cdx,
+                       float *cdy, int64_t cap, int32_t *count_dev, void *ws, size_t ws_bytes,
+                       void *stream);
+size_t vmf_greedy_nms_workspace_bytes(int64_t n, int64_t h, int64_t w, double r2);
+int vmf_greedy_nms(const int32_t *cy, const int32_t *cx, const double *cnd, int64_t n, int64_t h,
+                   int64_t w, double r2, int32_t *order, int32_t *n_kept_dev, void *ws,
+                   size_t ws_bytes, void *stream);
+
 /* Launch accounting / in-situ kernel timing (used by bench.py).
  * vmf_launch_count: kernels launched by this library since load.
  * vmf_profile_begin: start bracketing every launch with CUDA events on its

@@ -203,3 +203,79 @@ def pipeline(x, stage, col_stage=None, frac=0.5, lap_scale=1.0):
     if lap_scale != 1.0:
         L = L * lap_scale
     return B, L, detect3x3(L, frac)
+
+
+# ---------------------------------------------------------------------------
+# Hessian blob detector (blob.py:109-179)
+# ---------------------------------------------------------------------------
+_BANK3 = ((0.0, 1.0, 0.0), (0.5, 0.0, -0.5), (1.0, -2.0, 1.0))  # fir_vm_bank(3), design.py:250
+
+
+class _Taps:
+    def __init__(self, taps):
+        self.taps = tuple(taps)
+
+
+def derivative_field(x, stage, order=3):
+    """engine.derivative_field (engine.py:205-228): blur once, then the
+    minimal-support differentiator bank, conv_rows for d_x then conv_cols for
+    d_y, each with replicate edges; pairs with d_x + d_y >= order skipped."""
+    b = blur(x, stage)
+    out = {}
+    for dx in range(order):
+        for dy in range(order):
+            if dx + dy >= order:
+                continue
+            o = b
+            if dx:
+                o = conv_rows(o, _Taps(_BANK3[dx]))
+            if dy:
+                o = conv_cols(o, _Taps(_BANK3[dy]))
+            out[(dx, dy)] = o
+    return out
+
+
+def hessian_fields(field, sigma):
+    """nd = sigma^4 (D20 D02 - D11^2) (blob.py:109-111), trace D20 + D02, and
+    the displacement dx, dy with NaN where |det| < 1e-12 (blob.py:114-128)."""
+    d10, d01 = field[(1, 0)], field[(0, 1)]
+    d20, d02, d11 = field[(2, 0)], field[(0, 2)], field[(1, 1)]
+    nd = sigma ** 4 * (d20 * d02 - d11 ** 2)
+    det = d20 * d02 - d11 * d11
+    with np.errstate(divide="ignore", invalid="ignore"):
+        dx = (d01 * d11 - d02 * d10) / det
+        dy = (d10 * d11 - d20 * d01) / det
+    bad = np.abs(det) < 1e-12
+    dx[bad] = np.nan
+    dy[bad] = np.nan
+    return nd, d20 + d02, dx, dy
+
+
+def hessian_detect(x, stage, lam, t1, t2=None, polarity="dark"):
+    """blob.detect (blob.py:143-179) with an explicit blur stage: candidates
+    nd > t1 with the trace polarity, visited in lexsort((x, y, -nd)) order,
+    greedy suppression within (lam/2)^2, then the optional t2 displacement
+    filter.  Returns a list of (x, y, dx, dy, nd) tuples, strongest first."""
+    if t1 <= 0:
+        raise ValueError("t1 must be positive")
+    if polarity not in ("dark", "bright"):
+        raise ValueError("polarity must be 'dark' or 'bright'")
+    sigma = lam / 2.0
+    nd, trace, dx, dy = hessian_fields(derivative_field(x, stage, 3), sigma)
+    mask = nd > t1
+    mask &= (trace > 0) if polarity == "dark" else (trace < 0)
+    ys, xs = np.nonzero(mask)
+    if ys.size == 0:
+        return []
+    scores = nd[ys, xs]
+    order = np.lexsort((xs, ys, -scores))
+    kept = []
+    r2 = (lam / 2.0) ** 2
+    for i in order:
+        xx, yy = int(xs[i]), int(ys[i])
+        if any((xx - k[0]) ** 2 + (yy - k[1]) ** 2 <= r2 for k in kept):
+            continue
+        kept.append((xx, yy, float(dx[yy, xx]), float(dy[yy, xx]), float(nd[yy, xx])))
+    if t2 is not None:
+        kept = [k for k in kept if np.hypot(k[2], k[3]) <= t2]
+    return kept

@@ -13,7 +13,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # engine / detect import torch; load them lazily
-    if name in ("engine", "detect"):
+    if name in ("engine", "detect", "blob", "shard"):
         import importlib
 
         return importlib.import_module(f".{name}", __name__)

@@ -8,6 +8,12 @@
 #include "vmf_iir.cuh"
 #include "vmf_colpass.cuh"
 #include "vmf_firpass.cuh"
+
+namespace vmf {
+size_t greedy_nms_workspace_bytes(int64_t n, int64_t h, int64_t w, double r2);
+int greedy_nms(const int *cy, const int *cx, const double *nd, int64_t n, int64_t h, int64_t w,
+               double r2, int *order, int *nkept, void *ws, size_t ws_bytes, cudaStream_t st);
+}  // namespace vmf
 #include "vmf_stage4.cuh"
 
 namespace vmf {
@@ -139,6 +145,56 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ld
   if (ldn < w || plane_stride < h * ldn) return fail(VMF_EVALUE, "bad stack strides");
   return detect(n, ldn, plane_stride, ns, h, w, frac, false, det_syx, 3, det_val, cap, n_det_dev,
                 thr_dev, n_det_host, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t vmf_hessian_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage) {
+  return align256((size_t)h * w * sizeof(float)) + align256(stage_ws(row_stage, h, w)) + 256;
+}
+
+int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                       const vmf_stage *row_stage, const vmf_stage *col_stage, double sigma,
+                       double t1, int polarity, float *nd_field, float *trace_field,
+                       int64_t ldn, int32_t *cy, int32_t *cx, double *cnd, float *cdx,
+                       float *cdy, int64_t cap, int32_t *count_dev, void *ws, size_t ws_bytes,
+                       void *stream) {
+  if (h < 1 || w < 1) return fail(VMF_EVALUE, "image must be a 2-D array");
+  if (ldx < w) return fail(VMF_EVALUE, "row pitch smaller than width");
+  int rc = check_stage(row_stage, w, "row");
+  if (rc) return rc;
+  rc = check_stage(col_stage, h, "column");
+  if (rc) return rc;
+  if (col_stage->kind != VMF_STAGE_FIR || !firpass_supported(h, w, col_stage->n))
+    return fail(VMF_EVALUE, "the fused Hessian detector needs a FIR column stage of <= %d taps",
+                kFirMaxFast);
+  if ((nd_field || trace_field) && ldn < w) return fail(VMF_EVALUE, "field pitch smaller than width");
+  if (!count_dev || (cap > 0 && (!cy || !cx || !cnd || !cdx || !cdy)))
+    return fail(VMF_EVALUE, "candidate outputs missing");
+  size_t need = vmf_hessian_detect_workspace_bytes(h, w, row_stage);
+  if (!ws || ws_bytes < need)
+    return fail(VMF_EVALUE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float *T = (float *)p;
+  p += align256((size_t)h * w * sizeof(float));
+  rc = run_stage<ROWS>(row_stage, x, x_dtype, T, h, w, ldx, w, p,
+                       align256(stage_ws(row_stage, h, w)), st);
+  if (rc) return rc;
+  return hesspass_run(T, w, col_stage->taps, col_stage->n, h, w, sigma, t1, polarity, nd_field,
+                      trace_field, ldn, cy, cx, cnd, cdx, cdy, cap, count_dev, st);
+}
+
+size_t vmf_greedy_nms_workspace_bytes(int64_t n, int64_t h, int64_t w, double r2) {
+  return greedy_nms_workspace_bytes(n, h, w, r2);
+}
+
+int vmf_greedy_nms(const int32_t *cy, const int32_t *cx, const double *cnd, int64_t n, int64_t h,
+                   int64_t w, double r2, int32_t *order, int32_t *n_kept_dev, void *ws,
+                   size_t ws_bytes, void *stream) {
+  if (h < 1 || w < 1) return fail(VMF_EVALUE, "image must be a 2-D array");
+  if (!n_kept_dev || (n > 0 && (!cy || !cx || !cnd || !order)))
+    return fail(VMF_EVALUE, "NMS inputs missing");
+  return greedy_nms(cy, cx, cnd, n, h, w, r2, order, n_kept_dev, ws, ws_bytes,
+                    (cudaStream_t)stream);
 }
 
 static bool fused_col(const vmf_stage *col_stage, int64_t h, int64_t w) {

@@ -186,12 +186,91 @@ struct FcSmall {
   unsigned cmax;
 };
 
+// Hessian detector outputs (MODE 1, blob.py:109-128,158-163)
+struct HessOut {
+  double sigma4, t1;
+  int polarity;           // +1 dark (trace > 0), -1 bright (trace < 0)
+  float *nd_field;        // nullable: sigma^4 (D20 D02 - D11^2), pitch ldn
+  float *trace_field;     // nullable: D20 + D02
+  int64_t ldn;
+  int *cy, *cx;           // candidates: nd > t1 with the polarity
+  double *cnd;
+  float *cdx, *cdy;       // stationary-point displacement (NaN if |det| < 1e-12)
+  int cap;
+  int *count;             // appended candidates (may exceed cap: overflow)
+};
+
+// Owned pixels of a fused FIR tile -> derivative bank fir_vm_bank(3) of B
+// (replicate edges: rows clamped here, columns by the clamped inputs), the
+// scale-normalised Hessian determinant, trace and displacement; candidates
+// appended with one atomic per warp.
 template <class SH>
+__device__ __forceinline__ void hess_tile(const double *Bs, int64_t r0, int64_t c0, int64_t H,
+                                          int64_t W, const HessOut &ho) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t rB0 = r0 - 2;
+  for (int base = 0; base < SH::kOwn * SH::kOut; base += SH::kThreads) {
+    const int idx = base + tid;
+    bool cand = false;
+    int64_t r = 0, c = 0;
+    double nd = 0.0, dxv = 0.0, dyv = 0.0;
+    if (idx < SH::kOwn * SH::kOut) {
+      const int q = idx / SH::kOut, cl = idx - q * SH::kOut;
+      r = r0 + q;
+      c = c0 + cl;
+      if (r < H && c < W) {
+        const int jj = cl + 2;  // B tile column of image column c
+        const int64_t tr = r - rB0;
+        const int64_t tu = (r > 0 ? r - 1 : 0) - rB0, td = (r + 1 < H ? r + 1 : H - 1) - rB0;
+        const double *rc = Bs + tr * SH::kCols + jj, *ru = Bs + tu * SH::kCols + jj,
+                     *rd = Bs + td * SH::kCols + jj;
+        // conv taps in the reference's accumulation order (m ascending)
+        const double d10 = fma(-0.5, rc[-1], 0.5 * rc[1]);
+        const double d01 = fma(-0.5, ru[0], 0.5 * rd[0]);
+        const double d20 = (rc[1] - 2.0 * rc[0]) + rc[-1];
+        const double d02 = (rd[0] - 2.0 * rc[0]) + ru[0];
+        const double d10u = fma(-0.5, ru[-1], 0.5 * ru[1]), d10d = fma(-0.5, rd[-1], 0.5 * rd[1]);
+        const double d11 = fma(-0.5, d10u, 0.5 * d10d);
+        const double det = d20 * d02 - d11 * d11;
+        nd = ho.sigma4 * det;
+        const double tr2 = d20 + d02;
+        if (ho.nd_field) ho.nd_field[r * ho.ldn + c] = (float)nd;
+        if (ho.trace_field) ho.trace_field[r * ho.ldn + c] = (float)tr2;
+        cand = nd > ho.t1 && (ho.polarity > 0 ? tr2 > 0.0 : tr2 < 0.0);
+        if (cand) {
+          if (fabs(det) < 1e-12) {
+            dxv = dyv = __longlong_as_double(0x7ff8000000000000ll);
+          } else {
+            dxv = (d01 * d11 - d02 * d10) / det;
+            dyv = (d10 * d11 - d20 * d01) / det;
+          }
+        }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, cand);
+    if (!bal) continue;
+    int basek = 0;
+    if (lane == 0) basek = atomicAdd(ho.count, __popc(bal));
+    basek = __shfl_sync(0xffffffffu, basek, 0);
+    if (cand) {
+      const int k = basek + __popc(bal & ((1u << lane) - 1u));
+      if (k < ho.cap) {
+        ho.cy[k] = (int)r;
+        ho.cx[k] = (int)c;
+        ho.cnd[k] = nd;
+        ho.cdx[k] = (float)dxv;
+        ho.cdy[k] = (float)dyv;
+      }
+    }
+  }
+}
+
+template <class SH, int MODE>  // MODE 0: Laplacian + 3x3 NMS, 1: Hessian detector
 __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, int64_t H,
     int64_t W, FirTapsP tp, float lap_scale, float frac, CandState *__restrict__ st,
     int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv, int gcap, int vec_out,
-    const __grid_constant__ CUtensorMap tmap, int tma_rows, int tma_boxes) {
+    const __grid_constant__ CUtensorMap tmap, int tma_rows, int tma_boxes, HessOut ho) {
   extern __shared__ __align__(128) unsigned char fsm_raw[];
   __shared__ FcSmall S;
   __shared__ __align__(8) uint64_t fbar;
@@ -253,6 +332,10 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
 #pragma unroll
   for (int q = 0; q < 8; ++q) Bs[(8 * g + q) * SH::kCols + j] = acc[q];
   __syncthreads();
+  if (MODE == 1) {
+    hess_tile<SH>(Bs, r0, c0, H, W, ho);
+    return;
+  }
   // ---- L rows r0-1 .. r0+28, columns 1 .. 126 (replicate edges) ----------
   const double lsc = (double)lap_scale;
   float tmax = 0.0f;
@@ -385,11 +468,14 @@ static void fc_boxes(int np, int *rows, int *nbox) {
   *rows = ((wrows + *nbox - 1) / *nbox + 7) / 8 * 8;
 }
 
-template <class SH>
+template <class SH, int MODE = 0>
 static void launch_firapply(const float *T, int64_t ldt, float *L, int64_t ldl, int64_t h,
                             int64_t w, const FirTapsP &tp, float lap_scale, float frac,
                             CandState *cs, int *gy, int *gx, float *gv, int64_t gcap, int vec,
-                            cudaStream_t st) {
+                            cudaStream_t st, const HessOut *hop = nullptr) {
+  HessOut ho;
+  memset(&ho, 0, sizeof(ho));
+  if (hop) ho = *hop;
   const size_t smem = fc_smem<SH>(tp.np);
   int rows = 0, nbox = 0;
   fc_boxes<SH>(tp.np, &rows, &nbox);
@@ -397,11 +483,11 @@ static void launch_firapply(const float *T, int64_t ldt, float *L, int64_t ldl, 
   memset(&tmap, 0, sizeof(tmap));
   if (!make_tmap_2d_f32(&tmap, T, h, w, ldt, SH::kStride, rows) || getenv("VMF_NO_TMA")) nbox = 0;
   cudaGetLastError();
-  cudaFuncSetAttribute(firapply_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(firapply_kernel<SH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   dim3 grid((unsigned)cdiv(w, SH::kOut), (unsigned)cdiv(h, SH::kOwn));
-  launch_pdl(firapply_kernel<SH>, grid, dim3(SH::kThreads), smem, st, T, ldt, L, ldl, h, w, tp,
-             lap_scale, frac, cs, gy, gx, gv, (int)gcap, vec, tmap, rows, nbox);
+  launch_pdl(firapply_kernel<SH, MODE>, grid, dim3(SH::kThreads), smem, st, T, ldt, L, ldl, h, w,
+             tp, lap_scale, frac, cs, gy, gx, gv, (int)gcap, vec, tmap, rows, nbox, ho);
 }
 
 int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double *taps, int ntaps,
@@ -437,6 +523,42 @@ int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double
   if (frac <= 0.0f) return VMF_OK;
   return colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, h, w, frac, det_yx, det_val, cap,
                          n_det_dev, thr_dev, st);
+}
+
+// Hessian detector candidates from the row-pass output T and a FIR column
+// stage (blob.detect's derivative field, fused; B stays fp64).
+int hesspass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int64_t h,
+                 int64_t w, double sigma, double t1, int polarity, float *nd_field,
+                 float *trace_field, int64_t ldn, int *cy, int *cx, double *cnd, float *cdx,
+                 float *cdy, int64_t cap, int *count, cudaStream_t st) {
+  if (!firpass_supported(h, w, ntaps))
+    return fail(VMF_EVALUE, "Hessian detector: %d-tap column stage unsupported", ntaps);
+  FirTapsP tp;
+  fir_plan(&tp, taps, ntaps);
+  HessOut ho;
+  memset(&ho, 0, sizeof(ho));
+  ho.sigma4 = sigma * sigma * sigma * sigma;
+  ho.t1 = t1;
+  ho.polarity = polarity >= 0 ? 1 : -1;
+  ho.nd_field = nd_field;
+  ho.trace_field = trace_field;
+  ho.ldn = ldn;
+  ho.cy = cy;
+  ho.cx = cx;
+  ho.cnd = cnd;
+  ho.cdx = cdx;
+  ho.cdy = cdy;
+  ho.cap = (int)(cap < 0x7fffffff ? cap : 0x7fffffff);
+  ho.count = count;
+  cudaMemsetAsync(count, 0, sizeof(int), st);
+  Launch g(K_FIR_COLS, st);
+  if (tp.np > kFcLongTaps)
+    launch_firapply<FcLong, 1>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
+                               nullptr, nullptr, 0, 0, st, &ho);
+  else
+    launch_firapply<FcShort, 1>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
+                                nullptr, nullptr, 0, 0, st, &ho);
+  return cuda_status("hessian pass");
 }
 
 }  // namespace vmf

@@ -22,4 +22,10 @@ int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double
                 float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
                 size_t ws_bytes, cudaStream_t st);
 
+// Hessian blob-detector candidates (fused FIR column pass, B in fp64)
+int hesspass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int64_t h,
+                 int64_t w, double sigma, double t1, int polarity, float *nd_field,
+                 float *trace_field, int64_t ldn, int *cy, int *cx, double *cnd, float *cdx,
+                 float *cdy, int64_t cap, int *count, cudaStream_t st);
+
 }  // namespace vmf
