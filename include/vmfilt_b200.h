@@ -159,6 +159,13 @@ int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t
                        int64_t ldn, int32_t *cy, int32_t *cx, double *cnd, float *cdx,
                        float *cdy, int64_t cap, int32_t *count_dev, void *ws, size_t ws_bytes,
                        void *stream);
+/* engine.derivative_field(order=3) for a FIR column stage in one fused
+ * pass: D00 (the blur) D10 D01 D20 D02 D11 of the fp64 blur, fp32, pitch
+ * ldo (any output may be NULL); workspace = vmf_hessian_detect_workspace_bytes. */
+int vmf_derivative_field(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                         const vmf_stage *row_stage, const vmf_stage *col_stage, float *d00,
+                         float *d10, float *d01, float *d20, float *d02, float *d11, int64_t ldo,
+                         void *ws, size_t ws_bytes, void *stream);
 size_t vmf_greedy_nms_workspace_bytes(int64_t n, int64_t h, int64_t w, double r2);
 int vmf_greedy_nms(const int32_t *cy, const int32_t *cx, const double *cnd, int64_t n, int64_t h,
                    int64_t w, double r2, int32_t *order, int32_t *n_kept_dev, void *ws,

@@ -72,6 +72,9 @@ _PROTOS = {
                                      C.POINTER(VmfStage), C.c_double, C.c_double, C.c_int, _vp,
                                      _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _sz,
                                      _vp]),
+    "vmf_derivative_field": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, C.POINTER(VmfStage),
+                                       C.POINTER(VmfStage), _vp, _vp, _vp, _vp, _vp, _vp, _i64,
+                                       _vp, _sz, _vp]),
     "vmf_greedy_nms_workspace_bytes": (_sz, [_i64, _i64, _i64, C.c_double]),
     "vmf_greedy_nms": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, C.c_double, _vp, _vp, _vp,
                                  _sz, _vp]),

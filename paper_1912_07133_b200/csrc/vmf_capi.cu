@@ -183,6 +183,33 @@ int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t
                       trace_field, ldn, cy, cx, cnd, cdx, cdy, cap, count_dev, st);
 }
 
+int vmf_derivative_field(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                         const vmf_stage *row_stage, const vmf_stage *col_stage, float *d00,
+                         float *d10, float *d01, float *d20, float *d02, float *d11, int64_t ldo,
+                         void *ws, size_t ws_bytes, void *stream) {
+  if (h < 1 || w < 1) return fail(VMF_EVALUE, "image must be a 2-D array");
+  if (ldx < w || ldo < w) return fail(VMF_EVALUE, "row pitch smaller than width");
+  int rc = check_stage(row_stage, w, "row");
+  if (rc) return rc;
+  rc = check_stage(col_stage, h, "column");
+  if (rc) return rc;
+  if (col_stage->kind != VMF_STAGE_FIR || !firpass_supported(h, w, col_stage->n))
+    return fail(VMF_EVALUE, "the fused derivative bank needs a FIR column stage of <= %d taps",
+                kFirMaxFast);
+  size_t need = vmf_hessian_detect_workspace_bytes(h, w, row_stage);
+  if (!ws || ws_bytes < need)
+    return fail(VMF_EVALUE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float *T = (float *)p;
+  p += align256((size_t)h * w * sizeof(float));
+  rc = run_stage<ROWS>(row_stage, x, x_dtype, T, h, w, ldx, w, p,
+                       align256(stage_ws(row_stage, h, w)), st);
+  if (rc) return rc;
+  float *outs[6] = {d00, d10, d01, d20, d02, d11};
+  return derivpass_run(T, w, col_stage->taps, col_stage->n, h, w, outs, ldo, st);
+}
+
 size_t vmf_greedy_nms_workspace_bytes(int64_t n, int64_t h, int64_t w, double r2) {
   return greedy_nms_workspace_bytes(n, h, w, r2);
 }

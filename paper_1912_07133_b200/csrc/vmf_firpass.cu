@@ -198,6 +198,7 @@ struct HessOut {
   float *cdx, *cdy;       // stationary-point displacement (NaN if |det| < 1e-12)
   int cap;
   int *count;             // appended candidates (may exceed cap: overflow)
+  float *deriv[6];        // MODE 2: D00 D10 D01 D20 D02 D11 (pitch ldn), any may be null
 };
 
 // Owned pixels of a fused FIR tile -> derivative bank fir_vm_bank(3) of B
@@ -265,7 +266,36 @@ __device__ __forceinline__ void hess_tile(const double *Bs, int64_t r0, int64_t 
   }
 }
 
-template <class SH, int MODE>  // MODE 0: Laplacian + 3x3 NMS, 1: Hessian detector
+// MODE 2: the derivative bank fir_vm_bank(3) of the fp64 blur as fp32 images
+// (engine.derivative_field, engine.py:205-228, in one pass)
+template <class SH>
+__device__ __forceinline__ void deriv_tile(const double *Bs, int64_t r0, int64_t c0, int64_t H,
+                                           int64_t W, const HessOut &ho) {
+  const int64_t rB0 = r0 - 2;
+  for (int idx = threadIdx.x; idx < SH::kOwn * SH::kOut; idx += SH::kThreads) {
+    const int q = idx / SH::kOut, cl = idx - q * SH::kOut;
+    const int64_t r = r0 + q, c = c0 + cl;
+    if (r >= H || c >= W) continue;
+    const int jj = cl + 2;
+    const int64_t tr = r - rB0;
+    const int64_t tu = (r > 0 ? r - 1 : 0) - rB0, td = (r + 1 < H ? r + 1 : H - 1) - rB0;
+    const double *rc = Bs + tr * SH::kCols + jj, *ru = Bs + tu * SH::kCols + jj,
+                 *rd = Bs + td * SH::kCols + jj;
+    const double d10u = fma(-0.5, ru[-1], 0.5 * ru[1]), d10d = fma(-0.5, rd[-1], 0.5 * rd[1]);
+    const double v[6] = {rc[0],
+                         fma(-0.5, rc[-1], 0.5 * rc[1]),
+                         fma(-0.5, ru[0], 0.5 * rd[0]),
+                         (rc[1] - 2.0 * rc[0]) + rc[-1],
+                         (rd[0] - 2.0 * rc[0]) + ru[0],
+                         fma(-0.5, d10u, 0.5 * d10d)};
+    const int64_t o = r * ho.ldn + c;
+#pragma unroll
+    for (int d = 0; d < 6; ++d)
+      if (ho.deriv[d]) ho.deriv[d][o] = (float)v[d];
+  }
+}
+
+template <class SH, int MODE>  // MODE 0: Laplacian + 3x3 NMS, 1: Hessian detector, 2: derivatives
 __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, int64_t H,
     int64_t W, FirTapsP tp, float lap_scale, float frac, CandState *__restrict__ st,
@@ -334,6 +364,10 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
   __syncthreads();
   if (MODE == 1) {
     hess_tile<SH>(Bs, r0, c0, H, W, ho);
+    return;
+  }
+  if (MODE == 2) {
+    deriv_tile<SH>(Bs, r0, c0, H, W, ho);
     return;
   }
   // ---- L rows r0-1 .. r0+28, columns 1 .. 126 (replicate edges) ----------
@@ -559,6 +593,27 @@ int hesspass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int
     launch_firapply<FcShort, 1>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
                                 nullptr, nullptr, 0, 0, st, &ho);
   return cuda_status("hessian pass");
+}
+
+// engine.derivative_field (order 3, FIR blur) in one fused column pass
+int derivpass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int64_t h,
+                  int64_t w, float *const *outs, int64_t ldo, cudaStream_t st) {
+  if (!firpass_supported(h, w, ntaps))
+    return fail(VMF_EVALUE, "fused derivative bank: %d-tap column stage unsupported", ntaps);
+  FirTapsP tp;
+  fir_plan(&tp, taps, ntaps);
+  HessOut ho;
+  memset(&ho, 0, sizeof(ho));
+  ho.ldn = ldo;
+  for (int d = 0; d < 6; ++d) ho.deriv[d] = outs[d];
+  Launch g(K_FIR_COLS, st);
+  if (tp.np > kFcLongTaps)
+    launch_firapply<FcLong, 2>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
+                               nullptr, nullptr, 0, 0, st, &ho);
+  else
+    launch_firapply<FcShort, 2>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
+                                nullptr, nullptr, 0, 0, st, &ho);
+  return cuda_status("derivative pass");
 }
 
 }  // namespace vmf

@@ -28,4 +28,9 @@ int hesspass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int
                  float *trace_field, int64_t ldn, int *cy, int *cx, double *cnd, float *cdx,
                  float *cdy, int64_t cap, int *count, cudaStream_t st);
 
+// derivative bank fir_vm_bank(3) of the (fp64) FIR blur: outs = D00 D10 D01
+// D20 D02 D11 (any may be null), fp32, pitch ldo
+int derivpass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int64_t h,
+                  int64_t w, float *const *outs, int64_t ldo, cudaStream_t st);
+
 }  // namespace vmf

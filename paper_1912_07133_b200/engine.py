@@ -261,6 +261,21 @@ def derivative_field(img, lpf, order: int = 3, sigma: float = 0.0,
     if order not in (1, 3):
         raise ValueError("only order 1 and 3 derivative banks are built in")
     x, kind, code = _as_image(img)
+    h, w = x.shape
+    if order == 3 and not keep_all and is_fir(lpf) and len(lpf.taps) <= 385 and h >= 4 \
+            and w >= 4 and len(lpf.taps) <= min(h, w):
+        # FIR blur: the whole bank in one fused pass on the fp64 blur
+        from .detect import _Stage
+
+        stg = _Stage(lpf)
+        L = _lib.lib()
+        ws = _workspace(L.vmf_hessian_detect_workspace_bytes(h, w, C.byref(stg.s)))
+        outs = [torch.empty((h, w), dtype=torch.float32, device=x.device) for _ in range(6)]
+        _lib.check(L.vmf_derivative_field(
+            _ptr(x), code, h, w, _pitch(x), C.byref(stg.s), C.byref(stg.s),
+            *[_ptr(o) for o in outs], w, _ptr(ws), ws.numel(), _stream()))
+        keys = ((0, 0), (1, 0), (0, 1), (2, 0), (0, 2), (1, 1))
+        return DerivativeField({k: _finish(o, kind) for k, o in zip(keys, outs)}, order, sigma)
     blurred = _apply_dev(_apply_dev(x, code, lpf, False), _lib.VMF_F32, lpf, True)
     bank = [type("Bank", (), {"taps": t})() for t in VM_BANK3[:order]]
     images = {}

@@ -295,3 +295,21 @@ def test_fir_fused_long_taps(cat):
     """385-tap colored SG (config 5's FIR) on the fused FIR column pass."""
     x = synth.config5_frame(1024)
     _check_pipeline(x, cat["sg38.4"], label="config5/sg38.4 fused")
+
+
+def test_derivative_field_fused_fir(cat, golden):
+    """derivative_field with a FIR blur takes the fused pass (all six images
+    from the fp64 blur) and matches the oracle's bank."""
+    E = _E()
+    x = _f32(golden["in/rand"])
+    g = F.gaussian_fir(3.0, 0, 15)
+    fld = E.derivative_field(x, g, 3)
+    B = O.blur(x, g)
+    d1 = F.FirKernel(F.VM_BANK3[1], "anti", 1)
+    d2 = F.FirKernel(F.VM_BANK3[2], "sym", 2)
+    ref = {(0, 0): B, (1, 0): O.conv_rows(B, d1), (0, 1): O.conv_cols(B, d1),
+           (2, 0): O.conv_rows(B, d2), (0, 2): O.conv_cols(B, d2),
+           (1, 1): O.conv_cols(O.conv_rows(B, d1), d1)}
+    assert set(fld.images) == set(ref)
+    for k, v in ref.items():
+        assert max_rel_err(fld[k], v) < 1e-5, k
