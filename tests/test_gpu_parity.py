@@ -313,3 +313,18 @@ def test_derivative_field_fused_fir(cat, golden):
     assert set(fld.images) == set(ref)
     for k, v in ref.items():
         assert max_rel_err(fld[k], v) < 1e-5, k
+
+
+@pytest.mark.parametrize("shape", [(67, 131), (300, 517), (129, 64), (1000, 33), (33, 1000)])
+@pytest.mark.parametrize("name", ["rp4", "rp4_k2", "g2_k8"])
+def test_fused_path_odd_shapes(cat, shape, name):
+    """Odd / ragged shapes through the fused path (row-pass fallback widths,
+    partial bands and column tiles, short images) against the oracle."""
+    rng = np.random.default_rng(hash((shape, name)) & 0xFFFF)
+    h, w = shape
+    x = (0.05 * rng.standard_normal((h, w))).astype(np.float32)
+    for _ in range(6):  # a few blobs so the threshold selects something
+        cy, cx = rng.integers(0, h), rng.integers(0, w)
+        yy, xx = np.ogrid[:h, :w]
+        x += np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / 18.0).astype(np.float32)
+    _check_pipeline(x, cat[name], label=f"{name} {shape}")
