@@ -152,15 +152,16 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w,
  * vmf_greedy_nms: greedy suppression within r (d^2 <= r2) in the order
  * (nd desc, y asc, x asc); order[0 .. *n_kept_dev) = kept candidate indices,
  * strongest first. */
-size_t vmf_hessian_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage);
+size_t vmf_hessian_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage,
+                                          const vmf_stage *col_stage);
 int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
                        const vmf_stage *row_stage, const vmf_stage *col_stage, double sigma,
                        double t1, int polarity, float *nd_field, float *trace_field,
                        int64_t ldn, int32_t *cy, int32_t *cx, double *cnd, float *cdx,
                        float *cdy, int64_t cap, int32_t *count_dev, void *ws, size_t ws_bytes,
                        void *stream);
-/* engine.derivative_field(order=3) for a FIR column stage in one fused
- * pass: D00 (the blur) D10 D01 D20 D02 D11 of the fp64 blur, fp32, pitch
+/* engine.derivative_field(order=3) for a FIR (one fused pass) or IIR
+ * (fp64 blur, then the bank) column stage: D00 (the blur) D10 D01 D20 D02 D11 of the fp64 blur, fp32, pitch
  * ldo (any output may be NULL); workspace = vmf_hessian_detect_workspace_bytes. */
 int vmf_derivative_field(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
                          const vmf_stage *row_stage, const vmf_stage *col_stage, float *d00,

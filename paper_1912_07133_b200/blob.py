@@ -6,11 +6,13 @@ detector (blob.py) as a drop-in.
 keeps the reference's signature, validation and result (a list of Detection,
 strongest first).  The work runs in two native calls:
 
-* vmf_hessian_detect: the row blur, then the column FIR fused with the
-  derivative bank fir_vm_bank(3) on the fp64 blur, the scale-normalised
-  Hessian determinant nd = sigma^4 (D20 D02 - D11^2) (blob.py:109-111), the
-  trace polarity and the stationary-point displacement (blob.py:114-128);
-  candidates nd > t1 are appended with warp-ballot compaction;
+* vmf_hessian_detect: the row blur, then the column stage with the
+  derivative bank fir_vm_bank(3) on the fp64 blur (a FIR column stage in one
+  fused pass; an IIR one through the fused IIR column pass writing the fp64
+  blur), the scale-normalised Hessian determinant nd = sigma^4 (D20 D02 -
+  D11^2) (blob.py:109-111), the trace polarity and the stationary-point
+  displacement (blob.py:114-128); candidates nd > t1 are appended with
+  warp-ballot compaction;
 * vmf_greedy_nms: the greedy lambda/2-radius suppression in lexsort((x, y,
   -nd)) order (blob.py:168-176), computed in parallel rounds that provably
   keep exactly the sequential greedy set.
@@ -18,10 +20,10 @@ strongest first).  The work runs in two native calls:
 Scene helpers (Ellipse, EllipseScene, render_scene, ellipse_grid_scene,
 scene_from_json) restate the reference's synthetic ground-truth scenes
 (blob.py:23-107) so the reference's detector tests run against this module.
-Blur families: "gaussian_fir" (design restated in filters.gaussian_fir) or a
-FirKernel / catalog stage passed as `family`; the fused detector needs a FIR
-column stage (IIR blurs raise ValueError -- they would need the fp64 blur of
-the IIR column pass, not exposed here).
+Blur families: "gaussian_fir" (design restated in filters.gaussian_fir), or
+any FirKernel / ThreePartIIR stage (e.g. a catalog entry) passed as
+`family`; the reference's other family names need its design code
+(repeated_pole_blur etc.), which is not restated here.
 """
 from __future__ import annotations
 
@@ -36,7 +38,7 @@ import torch
 from . import _lib
 from .detect import _Stage
 from .engine import _as_image, _pitch, _ptr, _stream, _workspace
-from .filters import gaussian_fir, is_fir
+from .filters import gaussian_fir
 
 __all__ = ["Ellipse", "EllipseScene", "Detection", "render_scene", "ellipse_grid_scene",
            "scene_from_json", "hessian_det", "displacement", "detect", "calibrate_t1",
@@ -148,20 +150,18 @@ def _blur_for(family, sigma: float):
     if family == "gaussian_fir":
         return gaussian_fir(sigma, 0, math.ceil(5 * sigma))
     if family in ("repeated_pole", "colored_sg", "butterworth"):
-        raise ValueError(f"blur family '{family}' has no fused FIR detector path here; "
-                         "pass a FirKernel stage as `family`")
+        raise ValueError(f"blur family '{family}' needs the reference's design code; pass the "
+                         "stage (FirKernel / ThreePartIIR) as `family`")
     raise ValueError(f"unsupported blur family '{family}'")
 
 
 def _run(img, stage, sigma, t1, polarity, cap, fields):
     x, kind, code = _as_image(img)
     h, w = x.shape
-    if not is_fir(stage):
-        raise ValueError("the fused Hessian detector needs a FIR column stage")
     stg = _Stage(stage)
     L = _lib.lib()
     dev = x.device
-    nbytes = L.vmf_hessian_detect_workspace_bytes(h, w, C.byref(stg.s))
+    nbytes = L.vmf_hessian_detect_workspace_bytes(h, w, C.byref(stg.s), C.byref(stg.s))
     ws = _workspace(nbytes)
     nd_f = tr_f = None
     if fields:

@@ -147,8 +147,38 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ld
                 thr_dev, n_det_host, ws, ws_bytes, (cudaStream_t)stream);
 }
 
-size_t vmf_hessian_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage) {
-  return align256((size_t)h * w * sizeof(float)) + align256(stage_ws(row_stage, h, w)) + 256;
+static bool iir_b64(const vmf_stage *col_stage, int64_t h, int64_t w) {
+  return col_stage && col_stage->kind == VMF_STAGE_IIR && colpass_supported(h, w, col_stage->n);
+}
+
+size_t vmf_hessian_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage,
+                                          const vmf_stage *col_stage) {
+  size_t b = align256((size_t)h * w * sizeof(float)) + align256(stage_ws(row_stage, h, w)) + 256;
+  if (iir_b64(col_stage, h, w))  // fp64 blur + the IIR column-pass workspace
+    b += align256((size_t)h * w * sizeof(double)) +
+         align256(colpass_workspace_bytes(h, w, col_stage->n, 0));
+  return b;
+}
+
+// row stage into T, then the fp64 blur B64 of an IIR column stage
+static int blur64_iir(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                      const vmf_stage *row_stage, const vmf_stage *col_stage, void *ws,
+                      double **b64, cudaStream_t st) {
+  char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float *T = (float *)p;
+  p += align256((size_t)h * w * sizeof(float));
+  const size_t rws = align256(stage_ws(row_stage, h, w));
+  int rc = run_stage<ROWS>(row_stage, x, x_dtype, T, h, w, ldx, w, p, rws, st);
+  if (rc) return rc;
+  p += rws;
+  *b64 = (double *)p;
+  p += align256((size_t)h * w * sizeof(double));
+  IirParams ip;
+  rc = iir_plan(&ip, w, h, col_stage->b_plus, col_stage->a_plus, col_stage->n, col_stage->b_zero,
+                col_stage->sign);
+  if (rc) return rc;
+  return colpass_run(T, w, nullptr, 0, *b64, ip, h, w, 1.0f, 0.0f, nullptr, nullptr, 0, nullptr,
+                     nullptr, p, align256(colpass_workspace_bytes(h, w, col_stage->n, 0)), st);
 }
 
 int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
@@ -163,16 +193,24 @@ int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t
   if (rc) return rc;
   rc = check_stage(col_stage, h, "column");
   if (rc) return rc;
-  if (col_stage->kind != VMF_STAGE_FIR || !firpass_supported(h, w, col_stage->n))
-    return fail(VMF_EVALUE, "the fused Hessian detector needs a FIR column stage of <= %d taps",
-                kFirMaxFast);
+  const bool iir = iir_b64(col_stage, h, w);
+  if (!iir && (col_stage->kind != VMF_STAGE_FIR || !firpass_supported(h, w, col_stage->n)))
+    return fail(VMF_EVALUE, "Hessian detector: column stage unsupported (FIR <= %d taps or "
+                "IIR K = 2..4)", kFirMaxFast);
   if ((nd_field || trace_field) && ldn < w) return fail(VMF_EVALUE, "field pitch smaller than width");
   if (!count_dev || (cap > 0 && (!cy || !cx || !cnd || !cdx || !cdy)))
     return fail(VMF_EVALUE, "candidate outputs missing");
-  size_t need = vmf_hessian_detect_workspace_bytes(h, w, row_stage);
+  size_t need = vmf_hessian_detect_workspace_bytes(h, w, row_stage, col_stage);
   if (!ws || ws_bytes < need)
     return fail(VMF_EVALUE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
   cudaStream_t st = (cudaStream_t)stream;
+  if (iir) {
+    double *b64 = nullptr;
+    rc = blur64_iir(x, x_dtype, h, w, ldx, row_stage, col_stage, ws, &b64, st);
+    if (rc) return rc;
+    return hess_from_b64(b64, h, w, sigma, t1, polarity, nd_field, trace_field, ldn, cy, cx, cnd,
+                         cdx, cdy, cap, count_dev, st);
+  }
   char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   float *T = (float *)p;
   p += align256((size_t)h * w * sizeof(float));
@@ -193,13 +231,21 @@ int vmf_derivative_field(const void *x, int x_dtype, int64_t h, int64_t w, int64
   if (rc) return rc;
   rc = check_stage(col_stage, h, "column");
   if (rc) return rc;
-  if (col_stage->kind != VMF_STAGE_FIR || !firpass_supported(h, w, col_stage->n))
-    return fail(VMF_EVALUE, "the fused derivative bank needs a FIR column stage of <= %d taps",
-                kFirMaxFast);
-  size_t need = vmf_hessian_detect_workspace_bytes(h, w, row_stage);
+  const bool iir = iir_b64(col_stage, h, w);
+  if (!iir && (col_stage->kind != VMF_STAGE_FIR || !firpass_supported(h, w, col_stage->n)))
+    return fail(VMF_EVALUE, "derivative bank: column stage unsupported (FIR <= %d taps or IIR "
+                "K = 2..4)", kFirMaxFast);
+  size_t need = vmf_hessian_detect_workspace_bytes(h, w, row_stage, col_stage);
   if (!ws || ws_bytes < need)
     return fail(VMF_EVALUE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
   cudaStream_t st = (cudaStream_t)stream;
+  if (iir) {
+    double *b64 = nullptr;
+    rc = blur64_iir(x, x_dtype, h, w, ldx, row_stage, col_stage, ws, &b64, st);
+    if (rc) return rc;
+    float *outs[6] = {d00, d10, d01, d20, d02, d11};
+    return deriv_from_b64(b64, h, w, outs, ldo, st);
+  }
   char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   float *T = (float *)p;
   p += align256((size_t)h * w * sizeof(float));
@@ -289,7 +335,7 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
     rc = iir_plan(&ip, w, h, col_stage->b_plus, col_stage->a_plus, col_stage->n,
                   col_stage->b_zero, col_stage->sign);
     if (rc) return rc;
-    rc = colpass_run(T, w, L, w, ip, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
+    rc = colpass_run(T, w, L, w, nullptr, ip, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
                      thr_dev, carry, carry_b, st);
     if (rc) return rc;
     if (blur_out) {  // B is not materialised by the fused pass; recompute on request

@@ -390,12 +390,14 @@ struct ColSmem {
   unsigned int cmax;  // max |L| of this CTA (float bits)
 };
 
-template <int K, bool UNIT>  // UNIT: lap_scale == 1 (no scaling multiply)
+// MODE 0: L + NMS candidates; 1: the same with lap_scale == 1 (no scaling
+// multiply); 2: the fp64 blur B of the owned pixels to b64 (pitch W), no L
+template <int K, int MODE>
 __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, ColParams p,
     const double *__restrict__ Z, CandState *__restrict__ st, int *__restrict__ gy,
     int *__restrict__ gx, float *__restrict__ gv, int gcap,
-    const __grid_constant__ CUtensorMap tmap, int use_tma, int vec_out) {
+    const __grid_constant__ CUtensorMap tmap, int use_tma, int vec_out, double *__restrict__ b64) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 128-byte aligned base (the tile is a TMA destination), derived from the
   // shared array itself so every access stays an LDS / STS
@@ -583,10 +585,11 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         const double sx = blp + brp;  // shuffled when B(r-1) was produced
         shfl_lr(Bt);
         const double l = sx + (Bt + q);
-        const float v = UNIT ? (float)l : (float)(lsc * l);
+        const float v = MODE == 1 ? (float)l : (float)(lsc * l);
         lp[t * kTileStride] = v;
         tmax = fmaxf(tmax, fabsf(v));
         if (keep_b) ep[t] = Bt;
+        if (MODE == 2 && own_col) b64[(rb + t) * p.W + col] = Bt;
         q = fma(-4.0, Bt, Bm1);
         Bm2 = Bm1;
         Bm1 = Bt;
@@ -607,6 +610,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
           if (r - 1 < H) tmax = fmaxf(tmax, fabsf(v));
         }
         if (keep_b) ep[t] = Bt;
+        if (MODE == 2 && own_col && r < H) b64[r * p.W + col] = Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
       }
@@ -638,6 +642,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     }
   }
 #undef TX
+  if (MODE == 2) return;  // B only
   pdl_trigger();
   __syncthreads();
 
@@ -1008,6 +1013,7 @@ int colfinal_launch(CandState *cs, const int *gy, const int *gx, const float *gv
 
 template <int K>
 static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, const ColParams &p,
+                          double *b64,
                           int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
                           float *thr_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
@@ -1056,9 +1062,11 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
     Launch g(K_IIR_COLS_FUSED, st);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(colapply_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(colapply_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(ColSmem<K>) + 128);
-      cudaFuncSetAttribute(colapply_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(colapply_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ColSmem<K>) + 128);
+      cudaFuncSetAttribute(colapply_kernel<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(ColSmem<K>) + 128);
       attr = true;
     }
@@ -1068,17 +1076,20 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
     int use_tma = make_tmap_2d_f32(&tmap, T, p.H, p.W, ldt, kTileStride, kTileRows(K)) &&
                   !getenv("VMF_NO_TMA");
     cudaGetLastError();
-    launch_pdl(p.lap_scale == 1.0f ? colapply_kernel<K, true> : colapply_kernel<K, false>, grid, dim3(kColThreads), sizeof(ColSmem<K>) + 128, st, T, ldt,
-               L, ldl, p, (const double *)Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
-               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
+    auto kern = b64 ? colapply_kernel<K, 2>
+                    : (p.lap_scale == 1.0f ? colapply_kernel<K, 1> : colapply_kernel<K, 0>);
+    launch_pdl(kern, grid, dim3(kColThreads), sizeof(ColSmem<K>) + 128, st, T, ldt, L, ldl, p,
+               (const double *)Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
+               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0), b64);
   }
-  if (p.frac > 0.0f)
+  if (p.frac > 0.0f && !b64)
     colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, p.H, p.W, p.frac, det_yx, det_val, cap,
                     n_det_dev, thr_dev, st);
   return cuda_status("column pass");
 }
 
-int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,
+int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
+                const IirParams &ip,
                 int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
                 float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
                 size_t ws_bytes, cudaStream_t st) {
@@ -1119,11 +1130,11 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirPar
   p.lap_scale = lap_scale;
   p.frac = frac;
   switch (k) {
-    case 2: return launch_colpass<2>(T, ldt, L, ldl, p, det_yx, det_val, cap, n_det_dev, thr_dev,
+    case 2: return launch_colpass<2>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
                                      ws, ws_bytes, st);
-    case 3: return launch_colpass<3>(T, ldt, L, ldl, p, det_yx, det_val, cap, n_det_dev, thr_dev,
+    case 3: return launch_colpass<3>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
                                      ws, ws_bytes, st);
-    case 4: return launch_colpass<4>(T, ldt, L, ldl, p, det_yx, det_val, cap, n_det_dev, thr_dev,
+    case 4: return launch_colpass<4>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
                                      ws, ws_bytes, st);
   }
   return fail(VMF_EVALUE, "fused column pass supports K = 2..4, got %d", k);

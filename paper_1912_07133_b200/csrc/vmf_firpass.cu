@@ -595,6 +595,122 @@ int hesspass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int
   return cuda_status("hessian pass");
 }
 
+// ---------------------------------------------------------------------------
+// the same Hessian / derivative outputs from an fp64 blur in global memory
+// (the IIR column pass's MODE 2 output): one thread per pixel, 3x3
+// neighbourhood with replicate edges
+// ---------------------------------------------------------------------------
+template <int MODE>  // 1: Hessian detector, 2: derivative images
+__global__ void __launch_bounds__(256) b64_kernel(const double *__restrict__ B, int64_t H,
+                                                  int64_t W, HessOut ho) {
+  const int lane = threadIdx.x & 31;
+  const int64_t npx = H * W;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npx;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = base + threadIdx.x;
+    bool cand = false;
+    int64_t r = 0, c = 0;
+    double nd = 0.0, dxv = 0.0, dyv = 0.0;
+    if (idx < npx) {
+      r = idx / W;
+      c = idx - r * W;
+      const int64_t ru = r > 0 ? r - 1 : 0, rd = r + 1 < H ? r + 1 : H - 1;
+      const int64_t cl = c > 0 ? c - 1 : 0, cr = c + 1 < W ? c + 1 : W - 1;
+      const double *pc = B + r * W, *pu = B + ru * W, *pd = B + rd * W;
+      const double b00 = pc[c], bl = pc[cl], br = pc[cr], bu = pu[c], bd = pd[c];
+      const double d10 = fma(-0.5, bl, 0.5 * br);
+      const double d01 = fma(-0.5, bu, 0.5 * bd);
+      const double d20 = (br - 2.0 * b00) + bl;
+      const double d02 = (bd - 2.0 * b00) + bu;
+      const double d10u = fma(-0.5, pu[cl], 0.5 * pu[cr]), d10d = fma(-0.5, pd[cl], 0.5 * pd[cr]);
+      const double d11 = fma(-0.5, d10u, 0.5 * d10d);
+      const int64_t o = r * ho.ldn + c;
+      if (MODE == 2) {
+        const double v[6] = {b00, d10, d01, d20, d02, d11};
+#pragma unroll
+        for (int d = 0; d < 6; ++d)
+          if (ho.deriv[d]) ho.deriv[d][o] = (float)v[d];
+      } else {
+        const double det = d20 * d02 - d11 * d11;
+        nd = ho.sigma4 * det;
+        const double tr2 = d20 + d02;
+        if (ho.nd_field) ho.nd_field[o] = (float)nd;
+        if (ho.trace_field) ho.trace_field[o] = (float)tr2;
+        cand = nd > ho.t1 && (ho.polarity > 0 ? tr2 > 0.0 : tr2 < 0.0);
+        if (cand) {
+          if (fabs(det) < 1e-12) {
+            dxv = dyv = __longlong_as_double(0x7ff8000000000000ll);
+          } else {
+            dxv = (d01 * d11 - d02 * d10) / det;
+            dyv = (d10 * d11 - d20 * d01) / det;
+          }
+        }
+      }
+    }
+    if (MODE != 1) continue;
+    const unsigned bal = __ballot_sync(0xffffffffu, cand);
+    if (!bal) continue;
+    int basek = 0;
+    if (lane == 0) basek = atomicAdd(ho.count, __popc(bal));
+    basek = __shfl_sync(0xffffffffu, basek, 0);
+    if (cand) {
+      const int k = basek + __popc(bal & ((1u << lane) - 1u));
+      if (k < ho.cap) {
+        ho.cy[k] = (int)r;
+        ho.cx[k] = (int)c;
+        ho.cnd[k] = nd;
+        ho.cdx[k] = (float)dxv;
+        ho.cdy[k] = (float)dyv;
+      }
+    }
+  }
+}
+
+static HessOut hess_out(double sigma, double t1, int polarity, float *nd_field, float *trace_field,
+                        int64_t ldn, int *cy, int *cx, double *cnd, float *cdx, float *cdy,
+                        int64_t cap, int *count) {
+  HessOut ho;
+  memset(&ho, 0, sizeof(ho));
+  ho.sigma4 = sigma * sigma * sigma * sigma;
+  ho.t1 = t1;
+  ho.polarity = polarity >= 0 ? 1 : -1;
+  ho.nd_field = nd_field;
+  ho.trace_field = trace_field;
+  ho.ldn = ldn;
+  ho.cy = cy;
+  ho.cx = cx;
+  ho.cnd = cnd;
+  ho.cdx = cdx;
+  ho.cdy = cdy;
+  ho.cap = (int)(cap < 0x7fffffff ? cap : 0x7fffffff);
+  ho.count = count;
+  return ho;
+}
+
+int hess_from_b64(const double *B, int64_t h, int64_t w, double sigma, double t1, int polarity,
+                  float *nd_field, float *trace_field, int64_t ldn, int *cy, int *cx, double *cnd,
+                  float *cdx, float *cdy, int64_t cap, int *count, cudaStream_t st) {
+  HessOut ho = hess_out(sigma, t1, polarity, nd_field, trace_field, ldn, cy, cx, cnd, cdx, cdy,
+                        cap, count);
+  cudaMemsetAsync(count, 0, sizeof(int), st);
+  const int64_t nb = cdiv(h * w, 256);
+  Launch g(K_LAPLACIAN, st);
+  b64_kernel<1><<<(unsigned)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(B, h, w, ho);
+  return cuda_status("hessian (fp64 blur)");
+}
+
+int deriv_from_b64(const double *B, int64_t h, int64_t w, float *const *outs, int64_t ldo,
+                   cudaStream_t st) {
+  HessOut ho;
+  memset(&ho, 0, sizeof(ho));
+  ho.ldn = ldo;
+  for (int d = 0; d < 6; ++d) ho.deriv[d] = outs[d];
+  const int64_t nb = cdiv(h * w, 256);
+  Launch g(K_LAPLACIAN, st);
+  b64_kernel<2><<<(unsigned)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, st>>>(B, h, w, ho);
+  return cuda_status("derivatives (fp64 blur)");
+}
+
 // engine.derivative_field (order 3, FIR blur) in one fused column pass
 int derivpass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int64_t h,
                   int64_t w, float *const *outs, int64_t ldo, cudaStream_t st) {

@@ -33,4 +33,11 @@ int hesspass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int
 int derivpass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int64_t h,
                   int64_t w, float *const *outs, int64_t ldo, cudaStream_t st);
 
+// the same outputs from an fp64 blur B (pitch w) in global memory
+int hess_from_b64(const double *B, int64_t h, int64_t w, double sigma, double t1, int polarity,
+                  float *nd_field, float *trace_field, int64_t ldn, int *cy, int *cx, double *cnd,
+                  float *cdx, float *cdy, int64_t cap, int *count, cudaStream_t st);
+int deriv_from_b64(const double *B, int64_t h, int64_t w, float *const *outs, int64_t ldo,
+                   cudaStream_t st);
+
 }  // namespace vmf

@@ -262,14 +262,18 @@ def derivative_field(img, lpf, order: int = 3, sigma: float = 0.0,
         raise ValueError("only order 1 and 3 derivative banks are built in")
     x, kind, code = _as_image(img)
     h, w = x.shape
-    if order == 3 and not keep_all and is_fir(lpf) and len(lpf.taps) <= 385 and h >= 4 \
-            and w >= 4 and len(lpf.taps) <= min(h, w):
-        # FIR blur: the whole bank in one fused pass on the fp64 blur
+    fir_ok = is_fir(lpf) and len(lpf.taps) <= 385 and h >= 4 and w >= 4 \
+        and len(lpf.taps) <= min(h, w)
+    iir_ok = is_iir(lpf) and 2 <= len(lpf.a_plus) <= 4 and h >= 64 \
+        and -(-(-(-h // 32) * 32) // 64) <= 128 and w >= 2 * len(lpf.a_plus) + 1
+    if order == 3 and not keep_all and (fir_ok or iir_ok):
+        # the whole bank from the fp64 blur: one fused pass for a FIR blur, the
+        # fused IIR column pass writing the fp64 blur for an IIR one
         from .detect import _Stage
 
         stg = _Stage(lpf)
         L = _lib.lib()
-        ws = _workspace(L.vmf_hessian_detect_workspace_bytes(h, w, C.byref(stg.s)))
+        ws = _workspace(L.vmf_hessian_detect_workspace_bytes(h, w, C.byref(stg.s), C.byref(stg.s)))
         outs = [torch.empty((h, w), dtype=torch.float32, device=x.device) for _ in range(6)]
         _lib.check(L.vmf_derivative_field(
             _ptr(x), code, h, w, _pitch(x), C.byref(stg.s), C.byref(stg.s),

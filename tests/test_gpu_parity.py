@@ -297,12 +297,13 @@ def test_fir_fused_long_taps(cat):
     _check_pipeline(x, cat["sg38.4"], label="config5/sg38.4 fused")
 
 
-def test_derivative_field_fused_fir(cat, golden):
+@pytest.mark.parametrize("lpf", ["g3", "rp4"])
+def test_derivative_field_fused(cat, golden, lpf):
     """derivative_field with a FIR blur takes the fused pass (all six images
     from the fp64 blur) and matches the oracle's bank."""
     E = _E()
     x = _f32(golden["in/rand"])
-    g = F.gaussian_fir(3.0, 0, 15)
+    g = F.gaussian_fir(3.0, 0, 15) if lpf == "g3" else cat[lpf]
     fld = E.derivative_field(x, g, 3)
     B = O.blur(x, g)
     d1 = F.FirKernel(F.VM_BANK3[1], "anti", 1)
