@@ -34,6 +34,7 @@
 #include <cstring>
 
 #include "vmf_colpass.cuh"
+#include "plan_cache.hpp"
 #include "vmf_common.cuh"
 #include "vmf_prof.cuh"
 #include "vmf_stage4.cuh"
@@ -1097,39 +1098,51 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
   if (!ws || ws_bytes < need)
     return fail(VMF_EVALUE, "column-pass workspace too small: %zu < %zu bytes", ws_bytes, need);
   ColParams p;
-  memset(&p, 0, sizeof(p));
-  const int k = ip.K;
-  for (int m = 0; m < k; ++m) {
-    p.b[m] = ip.b[m];
-    p.a[m] = ip.a[m];
-  }
-  p.b0 = ip.b0;
-  p.sign = ip.sign;
-  p.yss = ip.yss;
-  impulse_ld(ip.b, ip.a, k, kHMax, p.h);
-  transfer_ld(ip.b, ip.a, k, kSub, p.Ty, p.Tx);
-  p.H = h;
-  p.W = w;
-  col_geometry(h, &p.Hp, &p.NB, &p.Blast);
-  transfer_ld(ip.b, ip.a, k, kBand, p.TyB[0], p.TxB[0]);
-  transfer_ld(ip.b, ip.a, k, p.Blast, p.TyB[1], p.TxB[1]);
-  for (int i = 0; i < k; ++i)
-    for (int t = 0; t < kBand / 2; ++t) {
-      int qa = kBand - 1 - i - t, qb = t - i;
-      double A = qa > 0 ? p.h[qa] : 0.0, B = qb > 0 ? p.h[qb] : 0.0;
-      p.SP[i][t] = 0.5 * (A + B);
-      p.SQ[i][t] = 0.5 * (A - B);
+  static PlanCache<ColParams> cache;
+  std::vector<unsigned char> key;
+  key_add(key, h);
+  key_add(key, w);
+  key_add(key, ip.K);
+  key_add(key, ip.b0);
+  key_add(key, ip.sign);
+  key_add(key, ip.b, sizeof(double) * ip.K);
+  key_add(key, ip.a, sizeof(double) * ip.K);
+  if (!cache.get(key, &p)) {
+    memset(&p, 0, sizeof(p));
+    const int k = ip.K;
+    for (int m = 0; m < k; ++m) {
+      p.b[m] = ip.b[m];
+      p.a[m] = ip.a[m];
     }
-  p.cpl = (p.NB + 31) / 32;
+    p.b0 = ip.b0;
+    p.sign = ip.sign;
+    p.yss = ip.yss;
+    impulse_ld(ip.b, ip.a, k, kHMax, p.h);
+    transfer_ld(ip.b, ip.a, k, kSub, p.Ty, p.Tx);
+    p.H = h;
+    p.W = w;
+    col_geometry(h, &p.Hp, &p.NB, &p.Blast);
+    transfer_ld(ip.b, ip.a, k, kBand, p.TyB[0], p.TxB[0]);
+    transfer_ld(ip.b, ip.a, k, p.Blast, p.TyB[1], p.TxB[1]);
+    for (int i = 0; i < k; ++i)
+      for (int t = 0; t < kBand / 2; ++t) {
+        int qa = kBand - 1 - i - t, qb = t - i;
+        double A = qa > 0 ? p.h[qa] : 0.0, B = qb > 0 ? p.h[qb] : 0.0;
+        p.SP[i][t] = 0.5 * (A + B);
+        p.SQ[i][t] = 0.5 * (A - B);
+      }
+    p.cpl = (p.NB + 31) / 32;
 
-  if (p.cpl > kMaxCpl) return fail(VMF_EVALUE, "image too tall for the fused column pass");
-  for (int l = 0; l < 5; ++l) {
-    double tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
-    transfer_ld(ip.b, ip.a, k, (p.cpl << l) * kBand, p.TyBp[l], tx);
+    if (p.cpl > kMaxCpl) return fail(VMF_EVALUE, "image too tall for the fused column pass");
+    for (int l = 0; l < 5; ++l) {
+      double tx[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];
+      transfer_ld(ip.b, ip.a, k, (p.cpl << l) * kBand, p.TyBp[l], tx);
+    }
+    cache.put(key, p);
   }
   p.lap_scale = lap_scale;
   p.frac = frac;
-  switch (k) {
+  switch (ip.K) {
     case 2: return launch_colpass<2>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
                                      ws, ws_bytes, st);
     case 3: return launch_colpass<3>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
@@ -1137,7 +1150,7 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
     case 4: return launch_colpass<4>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
                                      ws, ws_bytes, st);
   }
-  return fail(VMF_EVALUE, "fused column pass supports K = 2..4, got %d", k);
+  return fail(VMF_EVALUE, "fused column pass supports K = 2..4, got %d", ip.K);
 }
 
 }  // namespace vmf

@@ -29,6 +29,7 @@
 
 #include "vmf_common.cuh"
 #include "vmf_iir.cuh"
+#include "plan_cache.hpp"
 #include "vmf_prof.cuh"
 #include "vmf_rowpass.cuh"
 
@@ -366,6 +367,16 @@ int iir_plan(IirParams *p, int64_t lines, int64_t length, const double *b_plus,
     return fail(VMF_EVALUE, "IIR order %d outside 0..%d", k, VMF_MAX_IIR_ORDER);
   if (length < 2 * k + 1)
     return fail(VMF_EVALUE, "row length %lld < 2K+1 = %d", (long long)length, 2 * k + 1);
+  static PlanCache<IirParams> cache;
+  std::vector<unsigned char> key;
+  key_add(key, lines);
+  key_add(key, length);
+  key_add(key, k);
+  key_add(key, b_zero);
+  key_add(key, sign);
+  key_add(key, b_plus, sizeof(double) * k);
+  key_add(key, a_plus, sizeof(double) * k);
+  if (cache.get(key, p)) return VMF_OK;  // validated when it was stored
   if (k > 0 && !poles_inside_unit_circle(a_plus, k))
     return fail(VMF_ESTABILITY, "recursion has a pole on or outside the unit circle");
   memset(p, 0, sizeof(*p));
@@ -387,6 +398,7 @@ int iir_plan(IirParams *p, int64_t lines, int64_t length, const double *b_plus,
   transfer_matrix(p->b, p->a, k, p->L, &p->T[0][0]);
   transfer_matrix(p->b, p->a, k, p->Llast, &p->T[1][0]);
   impulse(p->b, p->a, k, kIirHmax, p->h);
+  cache.put(key, *p);
   return VMF_OK;
 }
 

@@ -32,6 +32,7 @@
 #include "vmf_iir.cuh"
 #include "vmf_prof.cuh"
 #include "vmf_rowpass.cuh"
+#include "plan_cache.hpp"
 #include "vmf_tma.cuh"
 
 namespace vmf {
@@ -661,7 +662,21 @@ template <typename T>
 int rowpass_run(const T *x, int64_t ldx, float *y, int64_t ldy, const IirParams &ip, int64_t h,
                 int64_t w, cudaStream_t st) {
   RowParams p;
-  rowpass_plan(&p, ip, h, w);
+  {
+    static PlanCache<RowParams> cache;
+    std::vector<unsigned char> key;
+    key_add(key, h);
+    key_add(key, w);
+    key_add(key, ip.K);
+    key_add(key, ip.b0);
+    key_add(key, ip.sign);
+    key_add(key, ip.b, sizeof(double) * ip.K);
+    key_add(key, ip.a, sizeof(double) * ip.K);
+    if (!cache.get(key, &p)) {
+      rowpass_plan(&p, ip, h, w);
+      cache.put(key, p);
+    }
+  }
   if (sizeof(T) == 4 && w == (int64_t)p.C * kChunk && p.C >= 32 && p.C <= kRowThreads &&
       !getenv("VMF_ROW_NO_TMA")) {
     const float *xf = (const float *)x;
