@@ -26,6 +26,7 @@ built library every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -118,10 +119,15 @@ def _pitch(t: torch.Tensor) -> int:
 # ---------------------------------------------------------------------------
 def stability_margin(f) -> float:
     """1 - max |pole|; positive for a usable recursion (engine.py:129-134)."""
-    k = len(f.a_plus)
-    if k == 0:
+    return _margin(tuple(float(v) for v in f.a_plus))
+
+
+@functools.lru_cache(maxsize=256)
+def _margin(a_plus: tuple) -> float:
+    # memoised: the fused paths check both stages on every call
+    if len(a_plus) == 0:
         return 1.0
-    roots = np.roots(np.concatenate(([1.0], np.asarray(f.a_plus, dtype=np.float64))))
+    roots = np.roots(np.concatenate(([1.0], np.asarray(a_plus, dtype=np.float64))))
     return float(1.0 - np.max(np.abs(roots))) if roots.size else 1.0
 
 
