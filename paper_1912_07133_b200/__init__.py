@@ -5,7 +5,7 @@ extraction on hand-written sm_100a CUDA kernels behind a C ABI
 (include/vmfilt_b200.h, libvmfilt_b200.so).  The Python layer mirrors the
 reference's engine API (engine.py) so it is a drop-in.
 """
-from . import filters, synth  # noqa: F401
+from . import design, filters, synth  # noqa: F401
 from .errors import FilterError, StabilityError  # noqa: F401
 
 __version__ = "0.1.0"

@@ -20,10 +20,10 @@ strongest first).  The work runs in two native calls:
 Scene helpers (Ellipse, EllipseScene, render_scene, ellipse_grid_scene,
 scene_from_json) restate the reference's synthetic ground-truth scenes
 (blob.py:23-107) so the reference's detector tests run against this module.
-Blur families: "gaussian_fir" (design restated in filters.gaussian_fir), or
-any FirKernel / ThreePartIIR stage (e.g. a catalog entry) passed as
-`family`; the reference's other family names need its design code
-(repeated_pole_blur etc.), which is not restated here.
+Blur families (blob.py:131-140): "gaussian_fir" (filters.gaussian_fir),
+"repeated_pole" and "butterworth" (the design re-implementation in
+design.py), or any FirKernel / ThreePartIIR stage passed as `family`;
+"colored_sg" needs the reference's design code (pass its FirKernel).
 """
 from __future__ import annotations
 
@@ -35,7 +35,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, design
 from .detect import _Stage
 from .engine import _as_image, _pitch, _ptr, _stream, _workspace
 from .filters import gaussian_fir
@@ -149,9 +149,13 @@ def _blur_for(family, sigma: float):
         return family
     if family == "gaussian_fir":
         return gaussian_fir(sigma, 0, math.ceil(5 * sigma))
-    if family in ("repeated_pole", "colored_sg", "butterworth"):
-        raise ValueError(f"blur family '{family}' needs the reference's design code; pass the "
-                         "stage (FirKernel / ThreePartIIR) as `family`")
+    if family == "repeated_pole":
+        return design.repeated_pole_blur(sigma)
+    if family == "butterworth":
+        return design.butterworth_blur(sigma)
+    if family == "colored_sg":
+        raise ValueError("blur family 'colored_sg' needs the reference's design code; pass the "
+                         "stage (FirKernel) as `family`")
     raise ValueError(f"unsupported blur family '{family}'")
 
 

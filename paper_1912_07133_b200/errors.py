@@ -9,3 +9,19 @@ class FilterError(Exception):
 class StabilityError(FilterError):
     """A recursion was asked to run with poles on or outside the unit circle
     (errors.py:32)."""
+
+
+class SplitError(FilterError):
+    """A denominator cannot be split into forward/backward factors: a root
+    within tolerance of the unit circle, or a non-mirrored root set
+    (errors.py:16)."""
+
+
+class DecompositionError(FilterError):
+    """The three-part numerator system is singular or inconsistent
+    (errors.py:24)."""
+
+
+class DesignError(FilterError):
+    """A filter design's constraint system is unsolvable or ill-conditioned
+    (errors.py:28)."""

@@ -166,3 +166,22 @@ def test_iir_stage_detector_matches_oracle():
     # the IIR path's blur carries the fp32 row-pass intermediate: nd agrees
     # within 1e-4 of the frame's max |nd| (the hot path's parity rule)
     _check(got, ref, nd_frame=1e-4 * float(np.abs(ond).max()), tie_rel=3e-4)
+
+
+@pytest.mark.parametrize("family,lam", [("repeated_pole", 16.0), ("butterworth", 12.0)])
+def test_family_names_use_design(family, lam):
+    """The reference's IIR family names (blob.py:131-140) resolve through the
+    design re-implementation; the detections equal the oracle's with the same
+    designed stage."""
+    B = _B()
+    from paper_1912_07133_b200 import design
+
+    stage = (design.repeated_pole_blur if family == "repeated_pole" else design.butterworth_blur)(
+        lam / 2.0)
+    img = B.render_scene(B.ellipse_grid_scene(2.0))
+    ond, otr, _, _ = O.hessian_fields(O.derivative_field(img, stage), lam / 2.0)
+    t1 = 0.3 * float(ond[otr > 0].max())
+    ref = O.hessian_detect(img, stage, lam, t1)
+    got = B.detect(img, lam, family, t1)
+    assert len(ref) > 0
+    _check(got, ref, nd_frame=1e-4 * float(np.abs(ond).max()), tie_rel=3e-4)
