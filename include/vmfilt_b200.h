@@ -36,8 +36,10 @@ extern "C" {
 #endif
 
 enum { VMF_OK = 0, VMF_EVALUE = 2, VMF_ESTABILITY = 3, VMF_ECUDA = 4 };
-/* input element types */
-enum { VMF_F32 = 0, VMF_U16 = 1 };
+/* input element types of the first (row) pass: fp32, u16 in host order,
+   u8, and big-endian u16 -- the sample bytes of a PGM P5 file with
+   maxval > 255 (pgmio.py:40-45), byte-swapped inside the row pass */
+enum { VMF_F32 = 0, VMF_U16 = 1, VMF_U8 = 2, VMF_U16BE = 3 };
 /* stage kinds for vmf_stage */
 enum { VMF_STAGE_FIR = 0, VMF_STAGE_IIR = 1 };
 

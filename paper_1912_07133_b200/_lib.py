@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvmfilt_b200.so")
 
 VMF_OK, VMF_EVALUE, VMF_ESTABILITY, VMF_ECUDA = 0, 2, 3, 4
-VMF_F32, VMF_U16 = 0, 1
+VMF_F32, VMF_U16, VMF_U8, VMF_U16BE = 0, 1, 2, 3
 VMF_STAGE_FIR, VMF_STAGE_IIR = 0, 1
 MAX_IIR_ORDER = 8
 MAX_FIR_TAPS = 2049

@@ -25,8 +25,36 @@ int cuda_status(const char *what);  // VMF_OK or VMF_ECUDA after a launch
 // ---------------------------------------------------------------------------
 // device: element loads (fp32 / u16 -> fp64) through the read-only path
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double ld64(const float *p) { return (double)__ldg(p); }
-__device__ __forceinline__ double ld64(const uint16_t *p) { return (double)__ldg(p); }
+// Input sample types of the first pass: fp32, u16 (native order), u8 and
+// big-endian u16 (PGM P5 with maxval > 255, read straight from the file
+// bytes; the byte swap is one PRMT in the load).
+struct u16be {
+  uint16_t raw;
+};
+__device__ __forceinline__ float ldf32(const float *p) { return __ldg(p); }
+__device__ __forceinline__ float ldf32(const uint16_t *p) { return (float)__ldg(p); }
+__device__ __forceinline__ float ldf32(const uint8_t *p) { return (float)__ldg(p); }
+__device__ __forceinline__ float ldf32(const u16be *p) {
+  const unsigned r = __ldg(&p->raw);
+  return (float)__byte_perm(r, 0u, 0x3201u);  // bytes 1,0 -> 0,1 (upper half zero)
+}
+template <typename T>
+__device__ __forceinline__ double ld64(const T *p) {
+  return (double)ldf32(p);  // exact for every input type
+}
+
+// Host: call f((const T *)x) with T the sample type of dtype code `code`
+// (VMF_F32 / VMF_U16 / VMF_U8 / VMF_U16BE); VMF_EVALUE for anything else.
+template <class F>
+int with_sample_type(int code, const void *x, F &&f) {
+  switch (code) {
+    case VMF_F32: return f((const float *)x);
+    case VMF_U16: return f((const uint16_t *)x);
+    case VMF_U8: return f((const uint8_t *)x);
+    case VMF_U16BE: return f((const u16be *)x);
+  }
+  return fail(VMF_EVALUE, "unsupported dtype code %d", code);
+}
 
 // ---------------------------------------------------------------------------
 // device: L2 residency hints.  The intermediate T (row-pass output) is read

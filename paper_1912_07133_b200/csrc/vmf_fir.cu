@@ -145,16 +145,10 @@ int fir_pass(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t
     return fail(VMF_EVALUE, "kernel length %d exceeds row length %lld", ntaps, (long long)length);
   // rows up to kFirMaxFast taps: the register-blocked kernel (vmf_firpass.cu)
   const bool fast = O == ROWS && ntaps <= kFirMaxFast && !getenv("VMF_FIR_GENERIC");
-  if (x_dtype == VMF_F32) {
-    if (fast) return fir_rows_fast<float>((const float *)x, ldx, y, ldy, h, w, taps, ntaps, st);
-    return fir_bucket<O>((const float *)x, ldx, y, ldy, h, w, taps, ntaps, st);
-  }
-  if (x_dtype == VMF_U16) {
-    if (fast)
-      return fir_rows_fast<uint16_t>((const uint16_t *)x, ldx, y, ldy, h, w, taps, ntaps, st);
-    return fir_bucket<O>((const uint16_t *)x, ldx, y, ldy, h, w, taps, ntaps, st);
-  }
-  return fail(VMF_EVALUE, "unsupported dtype");
+  return with_sample_type(x_dtype, x, [&](auto xt) {
+    if (fast) return fir_rows_fast(xt, ldx, y, ldy, h, w, taps, ntaps, st);
+    return fir_bucket<O>(xt, ldx, y, ldy, h, w, taps, ntaps, st);
+  });
 }
 
 template int fir_pass<ROWS>(const void *, int, float *, int64_t, int64_t, int64_t, int64_t,

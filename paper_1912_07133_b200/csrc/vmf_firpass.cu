@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kFrThreads) fir_rows_fast_kernel(const T *__re
       for (int q = threadIdx.x; q < nwin; q += blockDim.x) {
         int64_t c = n0 - k + q;
         c = c < 0 ? 0 : (c >= w ? w - 1 : c);
-        fwin[q] = (float)__ldg(xr + c);
+        fwin[q] = ldf32(xr + c);
       }
     }
     __syncthreads();
@@ -149,6 +149,10 @@ int fir_rows_fast(const T *x, int64_t ldx, float *y, int64_t ldy, int64_t h, int
 }
 
 template int fir_rows_fast<float>(const float *, int64_t, float *, int64_t, int64_t, int64_t,
+                                  const double *, int, cudaStream_t);
+template int fir_rows_fast<uint8_t>(const uint8_t *, int64_t, float *, int64_t, int64_t, int64_t,
+                                    const double *, int, cudaStream_t);
+template int fir_rows_fast<u16be>(const u16be *, int64_t, float *, int64_t, int64_t, int64_t,
                                   const double *, int, cudaStream_t);
 template int fir_rows_fast<uint16_t>(const uint16_t *, int64_t, float *, int64_t, int64_t,
                                      int64_t, const double *, int, cudaStream_t);

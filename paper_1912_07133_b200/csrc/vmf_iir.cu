@@ -411,30 +411,27 @@ int iir_pass(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t
   if (ldx < w || ldy < w)
     return fail(VMF_EVALUE, "row pitch smaller than width (ldx=%lld ldy=%lld w=%lld)",
                 (long long)ldx, (long long)ldy, (long long)w);
-  if (x_dtype != VMF_F32 && x_dtype != VMF_U16) return fail(VMF_EVALUE, "unsupported dtype");
+  if (x_dtype < VMF_F32 || x_dtype > VMF_U16BE) return fail(VMF_EVALUE, "unsupported dtype");
   IirParams p;
   int rc = iir_plan(&p, lines, length, b_plus, a_plus, k, b_zero, sign);
   if (rc) return rc;
   if (k == 0) {
     int64_t n = h * w;
     Launch g(K_IIR_SCALE, st);
-    if (x_dtype == VMF_F32)
-      scale_kernel<<<(int)cdiv(n, 256), 256, 0, st>>>((const float *)x, ldx, y, ldy, h, w, b_zero);
-    else
-      scale_kernel<<<(int)cdiv(n, 256), 256, 0, st>>>((const uint16_t *)x, ldx, y, ldy, h, w,
-                                                      b_zero);
-    return cuda_status("iir scale");
+    return with_sample_type(x_dtype, x, [&](auto xt) {
+      scale_kernel<<<(int)cdiv(n, 256), 256, 0, st>>>(xt, ldx, y, ldy, h, w, b_zero);
+      return cuda_status("iir scale");
+    });
   }
-  if (O == ROWS && rowpass_supported(w, k) && !getenv("VMF_FORCE_GENERIC")) {
-    if (x_dtype == VMF_F32) return rowpass_run<float>((const float *)x, ldx, y, ldy, p, h, w, st);
-    return rowpass_run<uint16_t>((const uint16_t *)x, ldx, y, ldy, p, h, w, st);
-  }
+  if (O == ROWS && rowpass_supported(w, k) && !getenv("VMF_FORCE_GENERIC"))
+    return with_sample_type(x_dtype, x,
+                            [&](auto xt) { return rowpass_run(xt, ldx, y, ldy, p, h, w, st); });
   size_t need = iir_workspace_bytes(lines, length, k);
   if (ws_bytes < need || !ws)
     return fail(VMF_EVALUE, "IIR workspace too small: %zu < %zu bytes", ws_bytes, need);
   double *carry = (double *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  if (x_dtype == VMF_F32) return dispatch_k<O>((const float *)x, ldx, y, ldy, p, carry, st);
-  return dispatch_k<O>((const uint16_t *)x, ldx, y, ldy, p, carry, st);
+  return with_sample_type(x_dtype, x,
+                          [&](auto xt) { return dispatch_k<O>(xt, ldx, y, ldy, p, carry, st); });
 }
 
 template int iir_pass<ROWS>(const void *, int, float *, int64_t, int64_t, int64_t, int64_t,

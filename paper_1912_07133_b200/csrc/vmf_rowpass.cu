@@ -296,11 +296,6 @@ __device__ __forceinline__ void row_apply_fwd(const RowParams &p, const Row *xr,
   }
 }
 
-template <typename T>
-__device__ __forceinline__ float ldf(const T *p) {
-  return (float)__ldg(p);
-}
-
 // ---------------------------------------------------------------------------
 // kernel 1: one CTA = R whole rows, staged with cp.async (any width / dtype)
 // ---------------------------------------------------------------------------
@@ -330,7 +325,7 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
   } else {
     for (int r = 0; r < nrows; ++r)
       for (int n = tid; n < W; n += blockDim.x)
-        xs[r * rowf + sidx(n)] = ldf(x + (row0 + r) * ldx + n);
+        xs[r * rowf + sidx(n)] = ldf32(x + (row0 + r) * ldx + n);
   }
   __syncthreads();
   // Each row is padded to C*32 samples with copies of x[W-1]: a steady state
@@ -711,6 +706,10 @@ template int rowpass_run<float>(const float *, int64_t, float *, int64_t, const 
                                 int64_t, int64_t, cudaStream_t);
 template int rowpass_run<uint16_t>(const uint16_t *, int64_t, float *, int64_t,
                                    const IirParams &, int64_t, int64_t, cudaStream_t);
+template int rowpass_run<uint8_t>(const uint8_t *, int64_t, float *, int64_t, const IirParams &,
+                                  int64_t, int64_t, cudaStream_t);
+template int rowpass_run<u16be>(const u16be *, int64_t, float *, int64_t, const IirParams &,
+                                int64_t, int64_t, cudaStream_t);
 
 }  // namespace vmf
 

@@ -27,7 +27,7 @@ from .engine import (_as_image, _dptr, _fir_checks, _iir_checks, _pitch, _ptr, _
 from .filters import is_fir, is_iir
 
 __all__ = ["Detections", "make_stage", "blur_laplacian_detect", "detect_sweep",
-           "scale_space_detect", "stream_detect"]
+           "scale_space_detect", "stream_detect", "pgm_stream_detect"]
 
 
 @dataclass
@@ -216,8 +216,8 @@ def scale_space_detect(img, stages, sigmas, frac: float = 0.5, cap: int = 1 << 1
 
 
 def stream_detect(frames, stage, frac: float = 0.5, cap: int = 1 << 16):
-    """Config-4 stream front end: a frame stream (n, h, w) of uint16 or
-    float32 in host memory (pin it for full speed) through the fused
+    """Config-4 stream front end: a frame stream (n, h, w) of uint16, uint8
+    or float32 in host memory (pin it for full speed) through the fused
     single-scale path.  Two device frame buffers: the upload of frame i+1
     runs on a copy stream while frame i is filtered on the current stream;
     nothing waits for the host until the end, when every frame's detections
@@ -226,48 +226,139 @@ def stream_detect(frames, stage, frac: float = 0.5, cap: int = 1 << 16):
         frames = torch.from_numpy(np.ascontiguousarray(frames))
     if frames.ndim != 3 or frames.shape[0] < 1:
         raise ValueError("frames must be an (n, h, w) array")
-    if frames.dtype not in (torch.uint16, torch.float32):
+    if frames.dtype not in (torch.uint16, torch.uint8, torch.float32):
         frames = frames.to(torch.float32)
     n, h, w = frames.shape
-    dev = torch.device("cuda", torch.cuda.current_device())
-    code = _lib.VMF_U16 if frames.dtype == torch.uint16 else _lib.VMF_F32
+    code = {torch.uint16: _lib.VMF_U16, torch.uint8: _lib.VMF_U8}.get(frames.dtype, _lib.VMF_F32)
     stg = stage if isinstance(stage, _Stage) else _Stage(stage)
-    cap = max(int(cap), 1)
-    det_yx = torch.empty((n, cap, 2), dtype=torch.int32, device=dev)
-    det_val = torch.empty((n, cap), dtype=torch.float32, device=dev)
-    scal = torch.empty((n, 2), dtype=torch.int64, device=dev)
-    comp = torch.cuda.current_stream()
+    res = _StreamResults(n, cap)
     if frames.is_cuda:
         for i in range(n):
-            _fused(frames[i], code, stg, stg, 1.0, frac, None, None, cap, False,
-                   out=(det_yx[i], det_val[i], scal[i]))
-    else:
-        copy = torch.cuda.Stream()
-        bufs = [torch.empty((h, w), dtype=frames.dtype, device=dev) for _ in range(2)]
-        ready = [torch.cuda.Event() for _ in range(2)]
-        free = [torch.cuda.Event() for _ in range(2)]
-        for e in free:
-            e.record(comp)
-        for i in range(n):
-            b = i & 1
-            with torch.cuda.stream(copy):
-                copy.wait_event(free[b])          # frame i-2 has been filtered
-                bufs[b].copy_(frames[i], non_blocking=True)
-                ready[b].record(copy)
-            comp.wait_event(ready[b])
-            _fused(bufs[b], code, stg, stg, 1.0, frac, None, None, cap, False,
-                   out=(det_yx[i], det_val[i], scal[i]))
-            bufs[b].record_stream(comp)
-            free[b].record(comp)
-    head = scal.cpu()
-    counts = head[:, 0].tolist()
-    thr = head[:, 1:2].contiguous().view(torch.float32)[:, 0].tolist()
-    mmax = min(max(counts), cap)
-    yx = det_yx[:, :mmax].cpu().numpy()
-    val = det_val[:, :mmax].cpu().numpy()
-    out = []
+            _fused(frames[i], code, stg, stg, 1.0, frac, None, None, res.cap, False, out=res.out(i))
+        return res.collect()
+    up = _Uploader((h, w), frames.dtype)
     for i in range(n):
-        c = int(counts[i])
-        m = min(c, cap)
-        out.append(Detections(yx[i, :m, 0], yx[i, :m, 1], val[i, :m], float(thr[i]), c, c > cap))
-    return out
+        _fused(up.put(frames[i]), code, stg, stg, 1.0, frac, None, None, res.cap, False,
+               out=res.out(i))
+        up.release()
+    return res.collect()
+
+
+class _StreamResults:
+    """Device-side detection buffers of a frame stream, read back once."""
+
+    def __init__(self, n, cap):
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.n, self.cap = n, max(int(cap), 1)
+        self.det_yx = torch.empty((n, self.cap, 2), dtype=torch.int32, device=dev)
+        self.det_val = torch.empty((n, self.cap), dtype=torch.float32, device=dev)
+        self.scal = torch.empty((n, 2), dtype=torch.int64, device=dev)
+
+    def out(self, i):
+        return self.det_yx[i], self.det_val[i], self.scal[i]
+
+    def collect(self):
+        head = self.scal.cpu()
+        counts = head[:, 0].tolist()
+        thr = head[:, 1:2].contiguous().view(torch.float32)[:, 0].tolist()
+        mmax = min(max(counts), self.cap)
+        yx = self.det_yx[:, :mmax].cpu().numpy()
+        val = self.det_val[:, :mmax].cpu().numpy()
+        out = []
+        for i in range(self.n):
+            c = int(counts[i])
+            m = min(c, self.cap)
+            out.append(Detections(yx[i, :m, 0], yx[i, :m, 1], val[i, :m], float(thr[i]), c,
+                                  c > self.cap))
+        return out
+
+
+class _Uploader:
+    """Two device frame buffers fed on a copy stream: put() enqueues the
+    upload of the next host frame (waiting only for the filter of the frame
+    two back) and makes the current stream wait for it; release() marks the
+    buffer free once the work queued on the current stream is done."""
+
+    def __init__(self, shape, dtype):
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.comp = torch.cuda.current_stream()
+        self.copy = torch.cuda.Stream()
+        self.bufs = [torch.empty(shape, dtype=dtype, device=dev) for _ in range(2)]
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+        for e in self.free:
+            e.record(self.comp)
+        self.i = -1
+
+    def put(self, host, after_copy=None):
+        self.i += 1
+        b = self.i & 1
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.free[b])  # frame i-2 has been filtered
+            self.bufs[b].copy_(host, non_blocking=True)
+            self.ready[b].record(self.copy)
+            if after_copy is not None:
+                after_copy.record(self.copy)
+        self.comp.wait_event(self.ready[b])
+        return self.bufs[b]
+
+    def release(self):
+        b = self.i & 1
+        self.bufs[b].record_stream(self.comp)
+        self.free[b].record(self.comp)
+
+
+def pgm_stream_detect(paths, stage, frac: float = 0.5, cap: int = 1 << 16,
+                      reference_units: bool = True, depth: int = 3):
+    """Config-4 front end from files: binary PGM frames
+    (P5, 16-bit big-endian or 8-bit, all the same size) through the fused
+    single-scale path.  A reader thread readinto()s the raw sample bytes of
+    frame i+depth-1 into a ring of pinned staging buffers while frame i is
+    uploaded and filtered; the byte swap / widening to fp32 happens in the
+    row pass (VMF_U16BE / VMF_U8), so the host never touches a sample.
+    reference_units: scale L by 1/maxval, i.e. the values the reference
+    computes from read_pgm's [0, 1] image.  Returns a list of Detections."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .pgmio import pgm_info, read_pgm_raw
+
+    paths = list(paths)
+    if not paths:
+        return []
+    info0 = pgm_info(paths[0])
+    if not info0.binary:
+        raise ValueError(f"{paths[0]}: pgm_stream_detect needs binary (P5) PGMs")
+    h, w = info0.height, info0.width
+    wide = info0.maxval > 255
+    nbytes = info0.nbytes
+    depth = max(int(depth), 2)
+    ring = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(depth)]
+    ring_free = [torch.cuda.Event() for _ in range(depth)]
+    for e in ring_free:
+        e.record(torch.cuda.current_stream())
+
+    def load(i):
+        slot = i % depth
+        ring_free[slot].synchronize()  # the upload that last used this slot is done
+        _, info = read_pgm_raw(paths[i], out=ring[slot].numpy())
+        if (info.height, info.width, info.maxval > 255) != (h, w, wide):
+            raise ValueError(f"{paths[i]}: frame shape/depth differs from {paths[0]}")
+        return info
+
+    stg = stage if isinstance(stage, _Stage) else _Stage(stage)
+    res = _StreamResults(len(paths), cap)
+    code = _lib.VMF_U16BE if wide else _lib.VMF_U8
+    up = _Uploader((h, w), torch.uint16 if wide else torch.uint8)
+    with ThreadPoolExecutor(max_workers=1) as pool:
+        futs = [pool.submit(load, i) for i in range(min(depth, len(paths)))]
+        for i in range(len(paths)):
+            info = futs[i].result()
+            slot = i % depth
+            host = ring[slot][:nbytes].view(torch.uint16 if wide else torch.uint8).view(h, w)
+            dbuf = up.put(host, after_copy=ring_free[slot])
+            if i + depth < len(paths):
+                futs.append(pool.submit(load, i + depth))
+            scale = 1.0 / info.maxval if reference_units else 1.0
+            _fused(dbuf, code, stg, stg, scale, frac, None, None, res.cap, False, out=res.out(i))
+            up.release()
+    return res.collect()

@@ -55,26 +55,33 @@ def _device() -> torch.device:
 def _as_image(img):
     """Validate like engine.py:105-109 and stage on the GPU.
 
-    Returns (tensor on device, 'numpy'|'torch', vmf dtype code).  uint16
-    stays uint16 (converted to fp32 inside the first pass); everything else
-    becomes float32."""
+    Returns (tensor on device, 'numpy'|'torch', vmf dtype code).  Integer
+    samples stay integer and are converted inside the first pass: uint16
+    (host order), uint8, and big-endian uint16 (numpy '>u2', e.g. PGM P5
+    samples from pgmio.read_pgm_raw; byte-swapped on the GPU).  Everything
+    else becomes float32."""
+    code = None
     if isinstance(img, torch.Tensor):
         t, kind = img, "torch"
     else:
         a = np.asarray(img)
-        if a.dtype != np.uint16:
+        if a.dtype == np.dtype(">u2") and a.dtype.byteorder != "=":
+            code = _lib.VMF_U16BE
+            a = np.ascontiguousarray(a).view(np.uint16)  # the file's bytes, unswapped
+        elif a.dtype not in (np.uint16, np.uint8):
             a = np.asarray(a, dtype=np.float32)
         t, kind = torch.from_numpy(np.ascontiguousarray(a)), "numpy"
     if t.ndim != 2 or t.shape[0] < 1 or t.shape[1] < 1:
         raise ValueError("image must be a 2-D array")
-    if t.dtype not in (torch.float32, torch.uint16):
+    if t.dtype not in (torch.float32, torch.uint16, torch.uint8):
         t = t.to(torch.float32)
     dev = _device()
     if t.device != dev:
         t = t.to(dev, non_blocking=True)
     if t.stride(1) != 1 or t.stride(0) < t.shape[1]:
         t = t.contiguous()
-    code = _lib.VMF_U16 if t.dtype == torch.uint16 else _lib.VMF_F32
+    if code is None:
+        code = {torch.uint16: _lib.VMF_U16, torch.uint8: _lib.VMF_U8}.get(t.dtype, _lib.VMF_F32)
     return t, kind, code
 
 
