@@ -325,22 +325,36 @@ def run_ours(args):
         pass
     path_gbs = PATH_BYTES_PER_PX * h * w * len(iir) / (ms_step / 1e3) / 1e9
 
-    # end to end through the public API: pinned host frame -> device ->
-    # 5 scales -> detections back to the host, every step
+    # end to end through the public API: K frames streamed from pinned host
+    # memory through the 5-scale sweep (detect.stream_sweep): every step's
+    # 64 MiB upload and its detections' readback are inside the timed
+    # region; uploads overlap the previous frame's filtering.
     host = torch.from_numpy(frame).pin_memory()
     stages_obj = [cat[n] for n in IIR]
+    # untimed pass of the same length: readback buffers allocated, PCIe link up to speed
+    detect.stream_sweep([host] * args.steps, stages_obj)
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0 = time.perf_counter()
+    res = detect.stream_sweep([host] * args.steps, stages_obj)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
+    barrier(ws)
+    assert len(res) == args.steps
+    d2h = len(iir) * (16 + 12 * 4096)  # per frame: header + first 4096 detections per scale
+    e2e = mpx * len(iir) * ws * args.steps / e2e_s
+    # the same without overlap: one detect_sweep call per frame (upload,
+    # 5 scales, readback, then the next frame)
     detect.detect_sweep(host, stages_obj)
     torch.cuda.synchronize()
     barrier(ws)
     t0 = time.perf_counter()
-    d2h = 0
     for _ in range(args.steps):
-        res = detect.detect_sweep(host, stages_obj)
-        d2h += sum(len(r) * 12 + 8 for r in res)
+        detect.detect_sweep(host, stages_obj)
     torch.cuda.synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
+    e2e1_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
     barrier(ws)
-    e2e = mpx * len(iir) * ws * args.steps / e2e_s
+    e2e_single = mpx * len(iir) * ws * args.steps / e2e1_s
 
     other = None
     if rank == 0 and ws == 1 and not args.no_extra:
@@ -375,7 +389,10 @@ def run_ours(args):
                         for k, v in prof.items()},
             "e2e": {"value": round(e2e, 1), "unit": UNIT,
                     "h2d_bytes_per_step": int(frame.nbytes),
-                    "d2h_bytes_per_step": int(d2h / args.steps)},
+                    "d2h_bytes_per_step": int(d2h),
+                    "api": "detect.stream_sweep over K pinned frames (uploads overlapped)",
+                    "single_frame_value": round(e2e_single, 1),
+                    "single_frame_api": "detect.detect_sweep per frame (no overlap)"},
             "gpu_launches": int(launches),
             "graph": "each timed step is one CUDA-graph replay of the 5-scale sweep",
             "clocks": clk,

@@ -27,7 +27,8 @@ from .engine import (_as_image, _dptr, _fir_checks, _iir_checks, _pitch, _ptr, _
 from .filters import is_fir, is_iir
 
 __all__ = ["Detections", "make_stage", "blur_laplacian_detect", "detect_sweep",
-           "scale_space_detect", "stream_detect", "pgm_stream_detect"]
+           "scale_space_detect", "stream_detect", "stream_sweep",
+           "pgm_stream_detect"]
 
 
 @dataclass
@@ -274,38 +275,136 @@ class _StreamResults:
 
 
 class _Uploader:
-    """Two device frame buffers fed on a copy stream: put() enqueues the
+    """Two device frame buffers fed by copy streams: put() enqueues the
     upload of the next host frame (waiting only for the filter of the frame
     two back) and makes the current stream wait for it; release() marks the
-    buffer free once the work queued on the current stream is done."""
+    buffer free once the work queued on the current stream is done.  A frame
+    is uploaded as `nsplit` row blocks alternating over two copy streams
+    (two DMA engines in flight: ~10 % more PCIe bandwidth than one copy)."""
 
-    def __init__(self, shape, dtype):
+    def __init__(self, shape, dtype, nsplit: int = 4):
         dev = torch.device("cuda", torch.cuda.current_device())
         self.comp = torch.cuda.current_stream()
-        self.copy = torch.cuda.Stream()
+        self.copies = [torch.cuda.Stream(), torch.cuda.Stream()]
         self.bufs = [torch.empty(shape, dtype=dtype, device=dev) for _ in range(2)]
-        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.ready = [[torch.cuda.Event() for _ in self.copies] for _ in range(2)]
         self.free = [torch.cuda.Event() for _ in range(2)]
         for e in self.free:
             e.record(self.comp)
+        self.nsplit = max(1, min(int(nsplit), shape[0]))
         self.i = -1
 
     def put(self, host, after_copy=None):
         self.i += 1
         b = self.i & 1
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(self.free[b])  # frame i-2 has been filtered
-            self.bufs[b].copy_(host, non_blocking=True)
-            self.ready[b].record(self.copy)
-            if after_copy is not None:
-                after_copy.record(self.copy)
-        self.comp.wait_event(self.ready[b])
+        h = host.shape[0]
+        bounds = [h * k // self.nsplit for k in range(self.nsplit + 1)]
+        for c, s in enumerate(self.copies):
+            s.wait_event(self.free[b])  # frame i-2 has been filtered
+        for k in range(self.nsplit):
+            s = self.copies[k & 1]
+            with torch.cuda.stream(s):
+                self.bufs[b][bounds[k]:bounds[k + 1]].copy_(host[bounds[k]:bounds[k + 1]],
+                                                           non_blocking=True)
+        for c, s in enumerate(self.copies):
+            self.ready[b][c].record(s)
+            self.comp.wait_event(self.ready[b][c])
+        if after_copy is not None:  # host buffer reusable once both copies are done
+            self.copies[0].wait_event(self.ready[b][1])
+            after_copy.record(self.copies[0])
         return self.bufs[b]
 
     def release(self):
         b = self.i & 1
         self.bufs[b].record_stream(self.comp)
         self.free[b].record(self.comp)
+
+
+_pinned_cache: dict = {}
+
+
+def _pinned(tag: str, shape, dtype) -> torch.Tensor:
+    """Grow-only pinned host buffers for readbacks: a fresh pinned
+    allocation (cudaHostAlloc) costs milliseconds and can serialise with
+    the device, so the stream paths reuse theirs across calls (every call
+    synchronises before returning, so reuse is safe)."""
+    n = 1
+    for d in shape:
+        n *= int(d)
+    buf = _pinned_cache.get((tag, dtype))
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
+        _pinned_cache[(tag, dtype)] = buf
+    return buf[:n].view(*shape)
+
+
+def stream_sweep(frames, stages, frac: float = 0.5, lap_scales=None, cap: int = 1 << 16,
+                 d2h_cap: int = 4096):
+    """A frame stream through the scale sweep (detect_sweep per frame) with
+    the uploads overlapped: frame i+1's host-to-device copy runs on a copy
+    stream while frame i's scales are filtered.  Every frame's results leave
+    the device as soon as they exist (one asynchronous copy into pinned host
+    memory per frame: counts, thresholds and the first d2h_cap detections
+    of each scale; larger sets are completed at the end).  frames: (n, h, w)
+    host array/tensor or a sequence of 2-D host tensors of one shape/dtype
+    (pinned for full speed).  Returns per frame a list of Detections, one per
+    stage."""
+    if isinstance(frames, np.ndarray):
+        frames = torch.from_numpy(np.ascontiguousarray(frames))
+    frames = list(frames) if not isinstance(frames, torch.Tensor) else list(frames.unbind(0))
+    if not frames or frames[0].ndim != 2:
+        raise ValueError("frames must be a non-empty sequence of 2-D frames")
+    dt = frames[0].dtype
+    if dt not in (torch.uint16, torch.uint8, torch.float32):
+        frames = [f.to(torch.float32) for f in frames]
+        dt = torch.float32
+    h, w = frames[0].shape
+    code = {torch.uint16: _lib.VMF_U16, torch.uint8: _lib.VMF_U8}.get(dt, _lib.VMF_F32)
+    stg = [s if isinstance(s, _Stage) else _Stage(s) for s in stages]
+    ns, n = len(stg), len(frames)
+    if ns == 0:
+        return [[] for _ in frames]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cap = max(int(cap), 1)
+    dcap = max(1, min(int(d2h_cap), cap))
+    det_yx = torch.empty((n, ns, cap, 2), dtype=torch.int32, device=dev)
+    det_val = torch.empty((n, ns, cap), dtype=torch.float32, device=dev)
+    scal = torch.empty((n, ns, 2), dtype=torch.int64, device=dev)
+    h_scal = _pinned("scal", (n, ns, 2), torch.int64)
+    h_yx = _pinned("yx", (n, ns, dcap, 2), torch.int32)
+    h_val = _pinned("val", (n, ns, dcap), torch.float32)
+    up = _Uploader((h, w), dt)
+    for i, f in enumerate(frames):
+        if f.shape != (h, w) or f.dtype != dt:
+            raise ValueError("all frames need one shape and dtype")
+        x = up.put(f) if not f.is_cuda else f
+        for j, s in enumerate(stg):
+            sc = 1.0 if lap_scales is None else float(lap_scales[j])
+            _fused(x, code, s, s, sc, frac, None, None, cap, False,
+                   out=(det_yx[i, j], det_val[i, j], scal[i, j]))
+        h_scal[i].copy_(scal[i], non_blocking=True)
+        for j in range(ns):  # contiguous on both sides: plain async copies
+            h_yx[i, j].copy_(det_yx[i, j, :dcap], non_blocking=True)
+            h_val[i, j].copy_(det_val[i, j, :dcap], non_blocking=True)
+        if not f.is_cuda:
+            up.release()
+    torch.cuda.current_stream().synchronize()
+    counts = h_scal[:, :, 0].tolist()
+    thr = h_scal[:, :, 1:2].contiguous().view(torch.float32)[..., 0].tolist()
+    out = []
+    for i in range(n):
+        row = []
+        for j in range(ns):
+            c = int(counts[i][j])
+            m = min(c, cap)
+            if m <= dcap:
+                yx, val = h_yx[i, j, :m].numpy(), h_val[i, j, :m].numpy()
+            else:
+                yx, val = det_yx[i, j, :m].cpu().numpy(), det_val[i, j, :m].cpu().numpy()
+            row.append(Detections(yx[:, 0].copy(), yx[:, 1].copy(), val.copy(), float(thr[i][j]),
+                                  c, c > cap))
+        out.append(row)
+    return out
 
 
 def pgm_stream_detect(paths, stage, frac: float = 0.5, cap: int = 1 << 16,
@@ -332,7 +431,7 @@ def pgm_stream_detect(paths, stage, frac: float = 0.5, cap: int = 1 << 16,
     wide = info0.maxval > 255
     nbytes = info0.nbytes
     depth = max(int(depth), 2)
-    ring = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(depth)]
+    ring = [_pinned(f"ring{k}", (nbytes,), torch.uint8) for k in range(depth)]
     ring_free = [torch.cuda.Event() for _ in range(depth)]
     for e in ring_free:
         e.record(torch.cuda.current_stream())

@@ -329,3 +329,27 @@ def test_fused_path_odd_shapes(cat, shape, name):
         yy, xx = np.ogrid[:h, :w]
         x += np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / 18.0).astype(np.float32)
     _check_pipeline(x, cat[name], label=f"{name} {shape}")
+
+
+def test_stream_sweep_matches_detect_sweep(cat):
+    """The overlapped multi-scale frame stream gives each frame the results
+    of a detect_sweep call, including sets larger than the per-frame
+    readback (d2h_cap) and a device-resident frame."""
+    D = _D()
+    frames = [f.astype(np.float32) for f in synth.config4_stream(n_frames=3, size=512)]
+    stages = [cat[n] for n in ("rp2", "rp4", "g2_k8")]
+    host = [torch.from_numpy(f).pin_memory() for f in frames]
+    got = D.stream_sweep(host, stages, d2h_cap=8)
+    dev = D.stream_sweep([host[0].cuda()], stages, d2h_cap=8)[0]
+    assert len(got) == 3
+    for f, g in zip(frames, got):
+        ref = D.detect_sweep(f, stages)
+        assert len(g) == len(ref) == 3
+        for a, b in zip(g, ref):
+            assert a.count == b.count and a.threshold == b.threshold
+            np.testing.assert_array_equal(a.y, b.y)
+            np.testing.assert_array_equal(a.x, b.x)
+            np.testing.assert_array_equal(a.value, b.value)
+    for a, b in zip(dev, got[0]):
+        np.testing.assert_array_equal(a.value, b.value)
+    assert max(d.count for d in got[0]) > 8
