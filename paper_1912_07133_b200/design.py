@@ -18,6 +18,9 @@ Here the same filters are computed without mpmath:
   are known in closed form (the s-plane roots mapped by z = (2+s)/(2-s)), so
   no polynomial root finding is involved; the numerator split is an exact
   rational solve of N = a0 (B+ A- + b0 A+ A- + B- A+).
+* interp_diff / fir_vm_bank -- the moment-matched differentiators
+  (design.py:203-280): integer moment systems, solved exactly over the
+  rationals (the taps are exact fractions, rounded once).
 * blunt_exponential_blur -- K cascaded (z^-1 + 2 + z)/((1-p/z)(1-pz))
   stages (design.py:520-548), A+ = (1 - p/z)^K directly.
 
@@ -35,11 +38,11 @@ from fractions import Fraction
 import numpy as np
 
 from .errors import DecompositionError, DesignError, SplitError
-from .filters import ThreePartIIR
+from .filters import FirKernel, ThreePartIIR
 
 __all__ = ["repeated_pole_blur", "butterworth_blur", "butterworth_cutoff",
            "butterworth_appendix", "blunt_exponential_blur", "blunt_exponential_from_pole",
-           "three_part_from_poles"]
+           "three_part_from_poles", "interp_diff", "fir_vm_bank"]
 
 COND_LIMIT = 1e12        # design.py:37
 UNIT_CIRCLE_TOL = 1e-9   # polyz.py:40
@@ -261,3 +264,70 @@ def blunt_exponential_blur(lam: float, k: int = 3) -> ThreePartIIR:
     if lam < 1:
         raise ValueError("lambda must be >= 1")
     return blunt_exponential_from_pole(math.exp(-1.0 / lam), k)
+
+
+# ---------------------------------------------------------------------------
+# moment-matched FIR differentiators
+# ---------------------------------------------------------------------------
+def _fir_moment_design(d: int, rows, n: int) -> FirKernel:
+    """Taps of parity d % 2 on the delay basis z^s +- z^-s, s = k + delta
+    (s = 0: the unit impulse), with the moment rows
+    sum_m c_m m^l (+-1)^m = d! [l == d at dc] solved exactly
+    (_delay_basis / _fir_from_combo, design.py:203-230)."""
+    delta = d % 2
+    A, rhs = [], []
+    for l, at in rows:
+        row = []
+        for k in range(n):
+            s = k + delta
+            alt = -1 if (at == "pi" and s % 2) else 1
+            if s == 0:
+                row.append(Fraction(1 if l == 0 else 0))
+            else:  # z^s and the mirrored (-1)^delta z^-s: both give s^l (l of parity delta)
+                row.append(Fraction(2 * alt * s ** l))
+        A.append(row)
+        rhs.append(Fraction(math.factorial(d)) if (l == d and at == "dc") else Fraction(0))
+    cond = _cond(A)
+    if not math.isfinite(cond) or cond > COND_LIMIT:
+        raise DesignError(f"ill-conditioned constraint matrix (cond ~ {cond:.3g})")
+    c = _solve_exact(A, rhs)
+    kmax = n - 1 + delta
+    coef = {0: Fraction(0)}
+    for k, ck in enumerate(c):  # coefficient of z^m
+        s = k + delta
+        if s == 0:
+            coef[0] = ck
+        else:
+            coef[s] = ck
+            coef[-s] = -ck if delta else ck
+    taps = tuple(float(coef.get(-m, 0)) for m in range(-kmax, kmax + 1))  # h(m) = c_-m
+    return FirKernel(taps, "anti" if delta else "sym", d)
+
+
+def interp_diff(d: int) -> FirKernel:
+    """Minimal-support central differentiator of order d, exact on
+    polynomials of degree <= d (design.py:233-247)."""
+    if not 0 <= d <= 8:
+        raise ValueError("d must be in 0..8")
+    delta = d % 2
+    n = (d - delta) // 2 + 1
+    return _fir_moment_design(d, [(delta + 2 * j, "dc") for j in range(n)], n)
+
+
+def fir_vm_bank(D: int, l_pi_bar: int = 2, cascade_mode: str = "behind_blur"):
+    """D differentiators d = 0..D-1 with common vanishing moments
+    (design.py:250-280); standalone mode adds l_pi_bar Nyquist rows."""
+    if D % 2 != 1 or not 3 <= D <= 9:
+        raise ValueError("D must be odd, 3 <= D <= 9")
+    if cascade_mode not in ("behind_blur", "standalone"):
+        raise ValueError("cascade_mode must be 'behind_blur' or 'standalone'")
+    l_d = (D - 1) // 2
+    out = []
+    for d in range(D):
+        delta = d % 2
+        l_dc = l_d - delta + 1
+        l_pi = 0 if cascade_mode == "behind_blur" else l_pi_bar
+        rows = [(delta + 2 * j, "dc") for j in range(l_dc)]
+        rows += [(delta + 2 * j, "pi") for j in range(l_pi)]
+        out.append(_fir_moment_design(d, rows, l_dc + l_pi))
+    return out

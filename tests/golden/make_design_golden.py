@@ -5,7 +5,7 @@ Run HERE, where /root/reference exists:   python tests/golden/make_design_golden
 The reference package is imported from a scratch copy (nothing is written
 into /root/reference).  Output: tests/golden/design_golden.json, one entry
 per design call: b_plus, a_plus, b_zero, parity (or the exception the
-reference raised).
+reference raised); for the FIR designs the taps, parity and d of each kernel.
 """
 import json
 import os
@@ -23,6 +23,11 @@ CALLS = (
     + [f"butterworth_blur(8.0, {ld})" for ld in (2, 3)]
     + [f"butterworth_appendix({lam})" for lam in (1.0, 2.0, 4.0, 10.0, 30.0)]
     + [f"blunt_exponential_blur({lam}, {k})" for lam in (1.0, 3.0, 12.0) for k in (1, 2, 3, 4)]
+)
+FIR_CALLS = (
+    [f"interp_diff({d})" for d in range(9)]
+    + [f"fir_vm_bank({D}, {lp}, '{mode}')" for D in (3, 5, 7, 9)
+       for mode, lp in (("behind_blur", 2), ("standalone", 1), ("standalone", 2))]
 )
 
 
@@ -42,6 +47,10 @@ def main():
             continue
         out[call] = {"b_plus": list(f.b_plus), "a_plus": list(f.a_plus), "b_zero": f.b_zero,
                      "parity": f.parity}
+    for call in FIR_CALLS:
+        f = eval("design." + call)
+        ks = f if isinstance(f, list) else [f]
+        out[call] = {"fir": [{"taps": list(k.taps), "parity": k.parity, "d": k.d} for k in ks]}
     with open(os.path.join(HERE, "design_golden.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     print(len(out), "designs")
