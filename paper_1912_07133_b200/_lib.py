@@ -13,6 +13,8 @@ from .errors import StabilityError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvmfilt_b200.so")
+if os.environ.get("VMF_LIB_PATH"):  # A/B builds for experiments (tools/scratch)
+    LIB_PATH = os.environ["VMF_LIB_PATH"]
 
 VMF_OK, VMF_EVALUE, VMF_ESTABILITY, VMF_ECUDA = 0, 2, 3, 4
 VMF_F32, VMF_U16, VMF_U8, VMF_U16BE = 0, 1, 2, 3
