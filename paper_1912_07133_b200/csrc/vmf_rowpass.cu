@@ -393,18 +393,18 @@ __device__ unsigned long long g_row_phase[8];
 // With NR = 2 every thread walks two independent recursions and the four
 // (row, direction) scans keep all four warps busy.
 // ---------------------------------------------------------------------------
-template <int K, int NR>
-__global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kernel(
-    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
-    RowParams p) {
+template <int K, int NR, int NBUF>
+__global__ void __launch_bounds__(kRowThreads, NR == 1 ? (NBUF == 2 ? 5 : 4) : 3)
+    rowpass_tma_kernel(const __grid_constant__ CUtensorMap xmap,
+                       const __grid_constant__ CUtensorMap ymap, RowParams p) {
   extern __shared__ __align__(1024) unsigned char smem_tma[];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[NBUF];
   const int C = p.C, Wp = C * kChunk;
   const int rowb = Wp * (int)sizeof(float);
   const int stepb = NR * rowb;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_tma);
   char *buf0 = reinterpret_cast<char *>(smem_tma) + ((1024u - (sbase & 1023u)) & 1023u);
-  double *cf = reinterpret_cast<double *>(buf0 + 2 * stepb);  // [NR][C][K]
+  double *cf = reinterpret_cast<double *>(buf0 + NBUF * stepb);  // [NR][C][K]
   double *cb = cf + NR * C * K;
   const int c = threadIdx.x;
   const int64_t H = p.H;
@@ -413,10 +413,13 @@ __global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kern
   const int64_t rhi = rlo + per < H ? rlo + per : H;
   if (rlo >= rhi) return;
   if (c == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_expect_tx(&bar[0], (unsigned)stepb);
-    tma_load_3d_hint(buf0, &xmap, &bar[0], 0, 0, (int)rlo, l2_policy_evict_first());
+    for (int q = 0; q < NBUF; ++q) mbar_init(&bar[q], 1);
+    // prologue: the first NBUF-1 steps in flight
+    for (int q = 0; q < NBUF - 1 && rlo + (int64_t)q * NR < rhi; ++q) {
+      mbar_expect_tx(&bar[q], (unsigned)stepb);
+      tma_load_3d_hint(buf0 + q * stepb, &xmap, &bar[q], 0, 0, (int)(rlo + (int64_t)q * NR),
+                       l2_policy_evict_first());
+    }
   }
   __syncthreads();
   int b = 0;
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kern
 #ifdef VMF_PHASE_PROF
   long long ph_t0 = clock64();
 #endif
-  for (int64_t r = rlo; r < rhi; r += NR, b ^= 1) {
+  for (int64_t r = rlo; r < rhi; r += NR, b = (b + 1 == NBUF ? 0 : b + 1)) {
     SwzRow xr[NR];
 #pragma unroll
     for (int g = 0; g < NR; ++g) xr[g].base = buf0 + b * stepb + g * rowb;
@@ -441,12 +444,14 @@ __global__ void __launch_bounds__(kRowThreads, NR == 1 ? 5 : 3) rowpass_tma_kern
     for (int g = 0; g < NR; ++g) row_carry<K>(p, xr[g], c, C, Wp, cfr[g], cbr[g]);
     __syncthreads();
     PH(1);
-    if (c == 0 && r + NR < rhi) {
-      // buffer b^1 last held the previous step, whose TMA store was issued a
+    const int64_t rn = r + (int64_t)(NBUF - 1) * NR;  // the step this refill serves
+    if (c == 0 && rn < rhi) {
+      // buffer bn last held the previous step, whose TMA store was issued a
       // full step ago: wait until it has been read out, then refill
+      const int bn = b == 0 ? NBUF - 1 : b - 1;
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-      mbar_expect_tx(&bar[b ^ 1], (unsigned)stepb);
-      tma_load_3d_hint(buf0 + (b ^ 1) * stepb, &xmap, &bar[b ^ 1], 0, 0, (int)(r + NR),
+      mbar_expect_tx(&bar[bn], (unsigned)stepb);
+      tma_load_3d_hint(buf0 + bn * stepb, &xmap, &bar[bn], 0, 0, (int)rn,
                        l2_policy_evict_first());
     }
     for (int task = c >> 5; task < 2 * NR; task += (int)(blockDim.x >> 5))
@@ -611,18 +616,18 @@ static int launch_rowpass(const T *x, int64_t ldx, float *y, int64_t ldy, RowPar
 
 // Persistent TMA variant: fp32, w = 32 C exactly (no padding), aligned
 // pitches; NR = 2 rows per step when the height is even.
-template <int K, int NR>
+template <int K, int NR, int NBUF>
 static int launch_rowpass_tma(const CUtensorMap &xm, const CUtensorMap &ym, RowParams p,
                               cudaStream_t st) {
-  const size_t smem = 1024 + 2 * (size_t)NR * p.C * kChunk * sizeof(float) +
+  const size_t smem = 1024 + NBUF * (size_t)NR * p.C * kChunk * sizeof(float) +
                       2 * (size_t)NR * p.C * K * sizeof(double);
   static int slots = 0;  // resident CTAs over the device
   if (!slots) {
-    cudaFuncSetAttribute(rowpass_tma_kernel<K, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+    cudaFuncSetAttribute(rowpass_tma_kernel<K, NR, NBUF>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     int occ = 0, dev = 0, nsm = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_tma_kernel<K, NR>, kRowThreads,
-                                                  smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_tma_kernel<K, NR, NBUF>,
+                                                  kRowThreads, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
@@ -632,7 +637,7 @@ static int launch_rowpass_tma(const CUtensorMap &xm, const CUtensorMap &ym, RowP
   p.rows_per = cdiv(cdiv(p.H, slots), NR) * NR;
   const int grid = (int)cdiv(p.H, p.rows_per);
   Launch g(K_IIR_ROWS_FUSED, st);
-  launch_pdl(rowpass_tma_kernel<K, NR>, dim3(grid), dim3(p.C), smem, st, xm, ym, p);
+  launch_pdl(rowpass_tma_kernel<K, NR, NBUF>, dim3(grid), dim3(p.C), smem, st, xm, ym, p);
   return cuda_status("row pass");
 }
 
@@ -650,7 +655,9 @@ static int launch_rowpass_tma_any(const float *x, int64_t ldx, float *y, int64_t
           make_tmap_rows_swz_f32(&ym, y, p.H, p.W, ldy, nr);
   cudaGetLastError();
   if (!*done) return VMF_OK;
-  return nr == 2 ? launch_rowpass_tma<K, 2>(xm, ym, p, st) : launch_rowpass_tma<K, 1>(xm, ym, p, st);
+  if (nr == 2) return launch_rowpass_tma<K, 2, 2>(xm, ym, p, st);
+  static const bool three = getenv("VMF_ROW_NBUF3") != nullptr;  // experiment: prefetch 2 ahead
+  return three ? launch_rowpass_tma<K, 1, 3>(xm, ym, p, st) : launch_rowpass_tma<K, 1, 2>(xm, ym, p, st);
 }
 
 template <typename T>
