@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
 //    TyB^(cpl 2^j)), and the true START histories go back coalesced:
 //    fwd = y+(r0-1 .. r0-K), bwd = y-(r1 .. r1+K-1).
 // ---------------------------------------------------------------------------
-constexpr int kScanCols = 4;
+constexpr int kScanCols = 8;
 
 template <int K>
 __global__ void __launch_bounds__(32 * kScanCols, 48 / kScanCols) colscan_kernel(const float *__restrict__ T,
