@@ -89,7 +89,7 @@ def make_stage(stage) -> _Stage:
 
 
 def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out, cap, sync,
-           out=None):
+           out=None, slot: int = 0):
     """One vmf_blur_lap_detect call.  `out` = preallocated (det_yx [cap, 2],
     det_val [cap], scal [2]) device tensors; with sync=False nothing waits
     for the GPU and the count is read from scal[0] later."""
@@ -98,7 +98,7 @@ def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out
     col.check(h)
     L = _lib.lib()
     nbytes = L.vmf_blur_lap_detect_workspace_bytes(h, w, C.byref(row.s), C.byref(col.s))
-    ws = _workspace(nbytes)
+    ws = _workspace(nbytes, slot)
     dev = x.device
     cap = int(cap)
     if out is None:
@@ -115,6 +115,47 @@ def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out
         _ptr(scal), scal.data_ptr() + 8, C.byref(n_host) if sync else None, _ptr(ws),
         ws.numel(), _stream()))
     return det_yx, det_val, scal, n_host.value
+
+
+SWEEP_STREAMS = 3  # scales in flight in a sweep (measured on B200: 1 -> 0.617 ms, 3 -> 0.532 ms)
+_side_streams: dict = {}
+
+
+def _side(n: int):
+    lst = _side_streams.setdefault(torch.cuda.current_device(), [])
+    while len(lst) < n:
+        lst.append(torch.cuda.Stream())
+    return lst[:n]
+
+
+def _sweep_launch(x, code, stages, frac, lap_scales, cap, outs, laps=None,
+                  conc: int = SWEEP_STREAMS):
+    """Queue one fused single-scale pass per stage.  The scales of a sweep
+    are independent (same frame, own outputs), so with conc > 1 they run on
+    `conc` side streams, each with its own workspace slot, forked from and
+    joined back into the current stream: one scale's latency-bound phases
+    (band scan, finaliser, kernel tails) overlap another's row pass."""
+    ns = len(stages)
+    conc = max(1, min(int(conc), ns))
+
+    def one(i, slot):
+        sc = 1.0 if lap_scales is None else float(lap_scales[i])
+        _fused(x, code, stages[i], stages[i], sc, frac, None, None if laps is None else laps[i],
+               cap, False, out=outs[i], slot=slot)
+
+    if conc == 1:
+        for i in range(ns):
+            one(i, 0)
+        return
+    cur = torch.cuda.current_stream()
+    side = _side(conc)
+    for s in side:
+        s.wait_stream(cur)
+    for i in range(ns):
+        with torch.cuda.stream(side[i % conc]):
+            one(i, 1 + i % conc)
+    for s in side:
+        cur.wait_stream(s)
 
 
 def blur_laplacian_detect(img, lpf, frac: float = 0.5, col_stage=None, lap_scale: float = 1.0,
@@ -148,9 +189,10 @@ def blur_laplacian_detect(img, lpf, frac: float = 0.5, col_stage=None, lap_scale
 
 def detect_sweep(img, stages, frac: float = 0.5, lap_scales=None, cap: int = 1 << 18):
     """One frame through the fused single-scale path once per blur stage
-    (config 3's IIR-vs-FIR scale sweep): the frame is uploaded once, all
-    scales are queued back to back without host synchronisation, and the
-    detections of every scale come back in one device-to-host copy.
+    (config 3's IIR-vs-FIR scale sweep): the frame is uploaded once, the
+    scales are queued without host synchronisation on SWEEP_STREAMS
+    concurrent streams, and the detections of every scale come back in one
+    device-to-host copy.
     Returns a list of Detections (numpy arrays)."""
     x, kind, code = _as_image(img)
     ns = len(stages)
@@ -161,11 +203,9 @@ def detect_sweep(img, stages, frac: float = 0.5, lap_scales=None, cap: int = 1 <
     det_yx = torch.empty((ns, cap, 2), dtype=torch.int32, device=dev)
     det_val = torch.empty((ns, cap), dtype=torch.float32, device=dev)
     scal = torch.empty((ns, 2), dtype=torch.int64, device=dev)
-    for i, st in enumerate(stages):
-        stg = st if isinstance(st, _Stage) else _Stage(st)
-        sc = 1.0 if lap_scales is None else float(lap_scales[i])
-        _fused(x, code, stg, stg, sc, frac, None, None, cap, False,
-               out=(det_yx[i], det_val[i], scal[i]))
+    stg = [st if isinstance(st, _Stage) else _Stage(st) for st in stages]
+    _sweep_launch(x, code, stg, frac, lap_scales, cap,
+                  [(det_yx[i], det_val[i], scal[i]) for i in range(ns)])
     head = scal.cpu()                                   # counts + thresholds
     ns_det = head[:, 0].tolist()
     thr = head[:, 1:2].contiguous().view(torch.float32)[:, 0].tolist()
@@ -190,9 +230,11 @@ def scale_space_detect(img, stages, sigmas, frac: float = 0.5, cap: int = 1 << 1
     h, w = x.shape
     ns = len(stages)
     stack = torch.empty((ns, h, w), dtype=torch.float32, device=x.device)
-    for s, (st, sg) in enumerate(zip(stages, sigmas)):
-        stg = _Stage(st)
-        _fused(x, code, stg, stg, float(sg) ** 2, 0.0, None, stack[s], 0, False)
+    dummy = [(torch.empty((1, 2), dtype=torch.int32, device=x.device),
+              torch.empty(1, dtype=torch.float32, device=x.device),
+              torch.empty(2, dtype=torch.int64, device=x.device)) for _ in range(ns)]
+    _sweep_launch(x, code, [_Stage(st) for st in stages], 0.0, [float(sg) ** 2 for sg in sigmas],
+                  0, dummy, laps=[stack[s] for s in range(ns)])
     L = _lib.lib()
     nbytes = L.vmf_detect3x3x3_workspace_bytes(ns, h, w)
     ws = _workspace(nbytes)
@@ -378,10 +420,8 @@ def stream_sweep(frames, stages, frac: float = 0.5, lap_scales=None, cap: int = 
         if f.shape != (h, w) or f.dtype != dt:
             raise ValueError("all frames need one shape and dtype")
         x = up.put(f) if not f.is_cuda else f
-        for j, s in enumerate(stg):
-            sc = 1.0 if lap_scales is None else float(lap_scales[j])
-            _fused(x, code, s, s, sc, frac, None, None, cap, False,
-                   out=(det_yx[i, j], det_val[i, j], scal[i, j]))
+        _sweep_launch(x, code, stg, frac, lap_scales, cap,
+                      [(det_yx[i, j], det_val[i, j], scal[i, j]) for j in range(ns)])
         h_scal[i].copy_(scal[i], non_blocking=True)
         for j in range(ns):  # contiguous on both sides: plain async copies
             h_yx[i, j].copy_(det_yx[i, j, :dcap], non_blocking=True)

@@ -96,14 +96,15 @@ def _stream() -> int:
 _ws_cache: dict = {}
 
 
-def _workspace(nbytes: int) -> torch.Tensor:
-    """Grow-only scratch buffer per device (caller-owned workspace of the
-    C ABI)."""
+def _workspace(nbytes: int, slot: int = 0) -> torch.Tensor:
+    """Grow-only scratch buffer per device and slot (caller-owned workspace of
+    the C ABI).  Work queued concurrently on different streams uses
+    different slots."""
     dev = _device()
-    buf = _ws_cache.get(dev)
+    buf = _ws_cache.get((dev, slot))
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
-        _ws_cache[dev] = buf
+        _ws_cache[(dev, slot)] = buf
     return buf
 
 
