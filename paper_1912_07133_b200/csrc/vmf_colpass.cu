@@ -545,19 +545,19 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
       double Yb[K], Xb[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        Yb[i] = last ? Ybot[i] : E0[i];
+        Yb[i] = p.sign * (last ? Ybot[i] : E0[i]);  // history of sign * y-
         Xb[i] = TX(trb + kSub + i);
       }
       DfiRun<K> rb_;
-      rb_.init(p, Yb, Xb);
+      rb_.init(p.bwd, Yb, Xb);
 #pragma unroll
-      for (int t = kSub - 1; t >= 0; --t) park[t] = p.sign * rb_.step(p, TX(trb + t));  // sign*y-
+      for (int t = kSub - 1; t >= 0; --t) park[t] = rb_.step(p.bwd, TX(trb + t));  // sign*y-
       if (s == 0 && r0 > 0) {  // B at rows r0-2, r0-1 from the band-edge histories
         double x1 = TX(K - 1), x2 = TX(K - 2);
-        double ym1 = rb_.step(p, x1);
-        double ym2 = rb_.step(p, x2);
-        Bm1 = fma(p.sign, ym1, fma(p.b0, x1, Yf[0]));
-        Bm2 = fma(p.sign, ym2, fma(p.b0, x2, Yf[1]));
+        double ym1 = rb_.step(p.bwd, x1);
+        double ym2 = rb_.step(p.bwd, x2);
+        Bm1 = ym1 + fma(p.b0, x1, Yf[0]);
+        Bm2 = ym2 + fma(p.b0, x2, Yf[1]);
         shfl_lr(Bm1);
         if (keep_b) {
           ebw[0] = Bm2;
@@ -1116,6 +1116,10 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
     }
     p.b0 = ip.b0;
     p.sign = ip.sign;
+    for (int m = 0; m < k; ++m) {
+      p.bwd.b[m] = ip.sign * ip.b[m];
+      p.bwd.a[m] = ip.a[m];
+    }
     p.yss = ip.yss;
     impulse_ld(ip.b, ip.a, k, kHMax, p.h);
     transfer_ld(ip.b, ip.a, k, kSub, p.Ty, p.Tx);

@@ -2,6 +2,7 @@
 // (vmf_colpass.cu).
 #pragma once
 #include "vmf_iir.cuh"
+#include "vmf_dfi.cuh"
 
 namespace vmf {
 
@@ -28,6 +29,7 @@ struct ColParams {
   double TyBc[VMF_MAX_IIR_ORDER * VMF_MAX_IIR_ORDER];  // TyB^cpb (one scan group)
   int NB, Blast, cpl, cpb;  // bands; rows in the last band; bands per lane / scan group
   float lap_scale, frac;
+  DfiCoef bwd;  // b_minus = sign * b, a: the backward run yields sign * y- directly
 };
 
 // Device-side bookkeeping shared by the fused column pass and the finaliser.

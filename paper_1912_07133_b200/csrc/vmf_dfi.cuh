@@ -18,6 +18,14 @@
 
 namespace vmf {
 
+// Coefficients of one recursion direction.  The backward run of the
+// three-part filter uses b_minus = sign * b_plus: folding the sign into the
+// coefficients (and the start history) gives sign * y- bit for bit (a
+// negation is exact) without a multiply per sample.
+struct DfiCoef {
+  double b[VMF_MAX_IIR_ORDER], a[VMF_MAX_IIR_ORDER];
+};
+
 template <int K>
 struct DfiRun {
   double P[K];

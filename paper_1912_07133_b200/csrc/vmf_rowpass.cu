@@ -232,7 +232,7 @@ __device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row *xr,
     for (int i = 0; i < K; ++i) {
       int qb = n0 + kChunk + i;
       Xb[g][i] = (double)xr[g].ld(qb > Wp - 1 ? Wp - 1 : qb);
-      Yb[g][i] = c < C - 1 ? cbr[g][(c + 1) * K + i] : p.yss * xl;
+      Yb[g][i] = p.sign * (c < C - 1 ? cbr[g][(c + 1) * K + i] : p.yss * xl);  // of sign*y-
       int qf = n0 - 1 - i;
       Xf[g][i] = (double)xr[g].ld(qf < 0 ? 0 : qf);
       Yf[g][i] = c > 0 ? cfr[g][(c - 1) * K + i] : p.yss * x0;
@@ -240,7 +240,7 @@ __device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row *xr,
   }
   DfiRun<K> rb[NR];
 #pragma unroll
-  for (int g = 0; g < NR; ++g) rb[g].init(p, Yb[g], Xb[g]);
+  for (int g = 0; g < NR; ++g) rb[g].init(p.bwd, Yb[g], Xb[g]);
 #pragma unroll
   for (int q = kChunk / 4 - 1; q >= 0; --q) {
     float e[NR][4];
@@ -256,8 +256,7 @@ __device__ __forceinline__ void row_apply_bwd(const RowParams &p, const Row *xr,
     for (int u = 3; u >= 0; --u) {
 #pragma unroll
       for (int g = 0; g < NR; ++g) {
-        const double s = rb[g].step(p, (double)e[g][u]);
-        park[g][4 * q + u] = (PT)(p.sign * s);
+        park[g][4 * q + u] = (PT)rb[g].step(p.bwd, (double)e[g][u]);  // sign*y-
       }
     }
   }
@@ -557,6 +556,10 @@ void rowpass_plan(RowParams *p, const IirParams &ip, int64_t h, int64_t w) {
   }
   p->b0 = ip.b0;
   p->sign = ip.sign;
+  for (int m = 0; m < k; ++m) {
+    p->bwd.b[m] = ip.sign * ip.b[m];
+    p->bwd.a[m] = ip.a[m];
+  }
   p->yss = ip.yss;
   impulse_resp(ip.b, ip.a, k, kChunk + 1, p->h);
   dfi_transfer(ip.b, ip.a, k, (int)kChunk, p->Ty, p->Tx);

@@ -1,6 +1,7 @@
 // vmf_rowpass.cuh -- single-kernel row pass (vmf_rowpass.cu).
 #pragma once
 #include "vmf_iir.cuh"
+#include "vmf_dfi.cuh"
 
 namespace vmf {
 
@@ -22,6 +23,7 @@ struct RowParams {
   int C, R, cpl;
   int vec4;
   int64_t rows_per;  // TMA variant: rows per CTA
+  DfiCoef bwd;       // b_minus = sign * b, a: the backward run yields sign * y- directly
 };
 
 bool rowpass_supported(int64_t w, int k);
