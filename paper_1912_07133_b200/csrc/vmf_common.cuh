@@ -38,6 +38,39 @@ __device__ __forceinline__ float ldf32(const u16be *p) {
   const unsigned r = __ldg(&p->raw);
   return (float)__byte_perm(r, 0u, 0x3201u);  // bytes 1,0 -> 0,1 (upper half zero)
 }
+// Eight consecutive samples from a 16-byte (u16) / 8-byte (u8) aligned
+// address with one vector load, widened to fp32 (exact).
+__device__ __forceinline__ void ld8f(const uint16_t *p, float *o) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
+  const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = (float)(w[i] & 0xffffu);
+    o[2 * i + 1] = (float)(w[i] >> 16);
+  }
+}
+__device__ __forceinline__ void ld8f(const u16be *p, float *o) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
+  const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = (float)__byte_perm(w[i], 0u, 0x4401u);      // bytes 1,0 of the first sample
+    o[2 * i + 1] = (float)__byte_perm(w[i], 0u, 0x4423u);  // bytes 3,2 of the second
+  }
+}
+__device__ __forceinline__ void ld8f(const uint8_t *p, float *o) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[i] = (float)((v.x >> (8 * i)) & 0xffu);
+    o[4 + i] = (float)((v.y >> (8 * i)) & 0xffu);
+  }
+}
+__device__ __forceinline__ void ld8f(const float *p, float *o) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = __ldg(p + i);
+}
+
 template <typename T>
 __device__ __forceinline__ double ld64(const T *p) {
   return (double)ldf32(p);  // exact for every input type

@@ -321,6 +321,15 @@ __global__ void __launch_bounds__(kRowMaxThreads, kRowMinBlocks) rowpass_kernel(
       for (int n = 4 * tid; n < W; n += 4 * blockDim.x)
         cp_async16_hint(xs + r * rowf + sidx(n), x + (row0 + r) * ldx + n, pol);
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  } else if (sizeof(T) < 4 && p.vec8) {  // integer samples: 8 per vector load
+    for (int r = 0; r < nrows; ++r)
+      for (int n = 8 * tid; n < W; n += 8 * blockDim.x) {
+        float o[8];
+        ld8f(x + (row0 + r) * ldx + n, o);
+        float *d = xs + r * rowf + sidx(n);  // 8 samples of one 32-chunk: contiguous
+        *reinterpret_cast<float4 *>(d) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4 *>(d + 4) = make_float4(o[4], o[5], o[6], o[7]);
+      }
   } else {
     for (int r = 0; r < nrows; ++r)
       for (int n = tid; n < W; n += blockDim.x)
@@ -611,6 +620,8 @@ static int launch_rowpass(const T *x, int64_t ldx, float *y, int64_t ldy, RowPar
   p.vec4 = (sizeof(T) == 4) && (p.W % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
            ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
   if (sizeof(T) != 4) p.vec4 = (p.W % 4 == 0) && (ldy % 4 == 0) && ((uintptr_t)y % 16 == 0);
+  p.vec8 = (sizeof(T) < 4) && (p.W % 8 == 0) && (ldx % 8 == 0) &&
+           ((uintptr_t)x % (8 * sizeof(T)) == 0);
   int grid = (int)cdiv(p.H, p.R);
   Launch g(K_IIR_ROWS_FUSED, st);
   rowpass_kernel<K, T><<<grid, p.R * p.C, smem, st>>>(x, ldx, y, ldy, p);

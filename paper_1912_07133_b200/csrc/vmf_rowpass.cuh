@@ -21,7 +21,7 @@ struct RowParams {
   double SP32[VMF_MAX_IIR_ORDER][kChunk / 2], SQ32[VMF_MAX_IIR_ORDER][kChunk / 2];  // folded
   int64_t H, W;
   int C, R, cpl;
-  int vec4;
+  int vec4, vec8;  // 16-byte fp32 / 8-sample integer vector loads
   int64_t rows_per;  // TMA variant: rows per CTA
   DfiCoef bwd;       // b_minus = sign * b, a: the backward run yields sign * y- directly
 };
