@@ -138,9 +138,10 @@ def _sweep_launch(x, code, stages, frac, lap_scales, cap, outs, laps=None,
     ns = len(stages)
     conc = max(1, min(int(conc), ns))
 
-    def one(i, slot):
+    def one(i, slot):  # x: one frame for every stage, or a list (one frame per stage)
         sc = 1.0 if lap_scales is None else float(lap_scales[i])
-        _fused(x, code, stages[i], stages[i], sc, frac, None, None if laps is None else laps[i],
+        xi = x[i] if isinstance(x, (list, tuple)) else x
+        _fused(xi, code, stages[i], stages[i], sc, frac, None, None if laps is None else laps[i],
                cap, False, out=outs[i], slot=slot)
 
     if conc == 1:
