@@ -161,9 +161,11 @@ template int fir_rows_fast<uint16_t>(const uint16_t *, int64_t, float *, int64_t
 // fused column pass
 // ---------------------------------------------------------------------------
 // Tile shapes: COLS computed columns (COLS-4 owned), GROUPS groups of 8 B rows
-// (8 GROUPS - 4 owned L rows).  Short FIRs: 128 x 4 (two CTAs per SM); long
-// FIRs: 64 x 16, so the 2k-row halo of the column window is shared by 124 B
-// rows instead of 28 (less re-staging per output).
+// (8 GROUPS - 4 owned L rows).  Short FIRs (<= 64 taps): 64 x 4, 256 threads
+// (more CTAs per SM mix the staging / taps / Laplacian phases: +5 % over
+// 128 x 4 at 33 taps); long FIRs: 64 x 8, so the 2k-row halo of the column
+// window is shared by 60 B rows instead of 28 (64 x 4 measured 8-23 % slower
+// there).
 template <int COLS, int GROUPS>
 struct FcShape {
   static constexpr int kCols = COLS, kOut = COLS - 4, kGroups = GROUPS;
@@ -178,7 +180,7 @@ struct FcShape {
     return win > bl ? win : bl;
   }
 };
-using FcShort = FcShape<128, 4>;
+using FcShort = FcShape<64, 4>;
 using FcLong = FcShape<64, 8>;
 constexpr int kFcLongTaps = 64;  // np above this: the long tile
 constexpr int kFcCand = 256;
