@@ -21,9 +21,9 @@ Scene helpers (Ellipse, EllipseScene, render_scene, ellipse_grid_scene,
 scene_from_json) restate the reference's synthetic ground-truth scenes
 (blob.py:23-107) so the reference's detector tests run against this module.
 Blur families (blob.py:131-140): "gaussian_fir" (filters.gaussian_fir),
-"repeated_pole" and "butterworth" (the design re-implementation in
-design.py), or any FirKernel / ThreePartIIR stage passed as `family`;
-"colored_sg" needs the reference's design code (pass its FirKernel).
+"repeated_pole", "butterworth" and "colored_sg" (the design
+re-implementation in design.py), or any FirKernel / ThreePartIIR stage
+passed as `family`.
 """
 from __future__ import annotations
 
@@ -154,8 +154,7 @@ def _blur_for(family, sigma: float):
     if family == "butterworth":
         return design.butterworth_blur(sigma)
     if family == "colored_sg":
-        raise ValueError("blur family 'colored_sg' needs the reference's design code; pass the "
-                         "stage (FirKernel) as `family`")
+        return design.colored_sg_blur(sigma)
     raise ValueError(f"unsupported blur family '{family}'")
 
 

@@ -109,7 +109,7 @@ def build(family: str, sigma: float = 0.0, d: int = 0, Dm: int = 3, l_pi_bar: in
         return D.blunt_exponential_blur(sigma, k or 3)
     if family == "butterworth_appendix":
         return D.butterworth_appendix(sigma)
-    raise ValueError("family 'colored_sg' needs the reference's design code")
+    return D.colored_sg_blur(sigma, l_d)
 
 
 # ---------------------------------------------------------------------------

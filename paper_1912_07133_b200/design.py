@@ -21,6 +21,10 @@ Here the same filters are computed without mpmath:
 * interp_diff / fir_vm_bank -- the moment-matched differentiators
   (design.py:203-280): integer moment systems, solved exactly over the
   rationals (the taps are exact fractions, rounded once).
+* colored_sg_blur -- the stopband-noise-minimising symmetric blur
+  (design.py:337-403): a Cholesky solve of its Gram system in decimal
+  arithmetic at the reference's working precision (40 + 2K digits), 12 s for
+  the 385-tap config-5 kernel instead of ~30 s.
 * blunt_exponential_blur -- K cascaded (z^-1 + 2 + z)/((1-p/z)(1-pz))
   stages (design.py:520-548), A+ = (1 - p/z)^K directly.
 
@@ -42,7 +46,7 @@ from .filters import FirKernel, ThreePartIIR
 
 __all__ = ["repeated_pole_blur", "butterworth_blur", "butterworth_cutoff",
            "butterworth_appendix", "blunt_exponential_blur", "blunt_exponential_from_pole",
-           "three_part_from_poles", "interp_diff", "fir_vm_bank"]
+           "three_part_from_poles", "interp_diff", "fir_vm_bank", "colored_sg_blur"]
 
 COND_LIMIT = 1e12        # design.py:37
 UNIT_CIRCLE_TOL = 1e-9   # polyz.py:40
@@ -331,3 +335,130 @@ def fir_vm_bank(D: int, l_pi_bar: int = 2, cascade_mode: str = "behind_blur"):
         rows += [(delta + 2 * j, "pi") for j in range(l_pi)]
         out.append(_fir_moment_design(d, rows, l_dc + l_pi))
     return out
+
+
+# ---------------------------------------------------------------------------
+# colored Savitzky-Golay blur (high-precision decimal arithmetic, no mpmath)
+# ---------------------------------------------------------------------------
+def _dec_pi(ctx_prec: int):
+    """pi by Machin's formula, 16 atan(1/5) - 4 atan(1/239), in the current
+    decimal context."""
+    from decimal import Decimal
+
+    def atan_inv(n: int):
+        x = Decimal(1) / n
+        x2 = x * x
+        term, total, k = x, x, 1
+        eps = Decimal(10) ** (-(ctx_prec + 2))
+        while True:
+            term = -term * x2
+            k += 2
+            t = term / k
+            if abs(t) < eps:
+                return total
+            total += t
+
+    return 16 * atan_inv(5) - 4 * atan_inv(239)
+
+
+def _dec_sin(x, pi, ctx_prec: int):
+    """sin(x) by the Taylor series after reduction to [-pi, pi]."""
+    from decimal import Decimal
+
+    two_pi = 2 * pi
+    x = x - two_pi * (x / two_pi).to_integral_value()
+    if x > pi:
+        x -= two_pi
+    elif x < -pi:
+        x += two_pi
+    x2 = x * x
+    term, total, k = x, x, 1
+    eps = Decimal(10) ** (-(ctx_prec + 2))
+    while abs(term) > eps:
+        term = -term * x2 / ((k + 1) * (k + 2))
+        k += 2
+        total += term
+    return total
+
+
+def colored_sg_blur(sigma: float, l_d: int = 1) -> FirKernel:
+    """Symmetric blur of half-width K = ceil(5 sigma) (ceil(7 sigma) for
+    l_d = 2) minimising the preserved noise power on [wc, pi], wc = 3 / sigma,
+    under unit dc gain and vanishing even moments up to 2 l_d
+    (colored_sg_blur, design.py:337-403).
+
+    The stopband Gram matrix S (Toeplitz-plus-Hankel after folding the tap
+    symmetry) is numerically singular in double precision, so the
+    constrained minimum c = S^-1 F^T (F S^-1 F^T)^-1 e is computed with a
+    Cholesky factorisation of S in decimal arithmetic carrying 40 + 2K
+    digits (the precision the reference uses), then rounded once."""
+    from decimal import Decimal, localcontext
+
+    if sigma < 1:
+        raise ValueError("sigma must be >= 1")
+    if l_d not in (1, 2):
+        raise ValueError("l_d must be 1 or 2")
+    k = math.ceil((5 if l_d == 1 else 7) * sigma)
+    n, nr = k + 1, l_d + 1
+    dps = max(60, 40 + 2 * k)
+    with localcontext() as ctx:
+        ctx.prec = dps + 10
+        pi = _dec_pi(ctx.prec)
+        wc = Decimal(3) / Decimal(repr(float(sigma)))
+        sb = [(pi - wc) / pi] + [-_dec_sin(wc * j, pi, ctx.prec) / (pi * j)
+                                 for j in range(1, 2 * k + 1)]
+        # folded Gram matrix: c_0 is the centre tap, c_j (j >= 1) both taps +-j
+        S = [[None] * n for _ in range(n)]
+        for a in range(n):
+            for b in range(a, n):
+                if a == 0 and b == 0:
+                    v = sb[0]
+                elif a == 0:
+                    v = 2 * sb[b]
+                else:
+                    v = 2 * sb[b - a] + 2 * sb[a + b]
+                S[a][b] = S[b][a] = v
+        # Cholesky S = L L^T (row-oriented)
+        L = [[Decimal(0)] * n for _ in range(n)]
+        for i in range(n):
+            Li = L[i]
+            for j in range(i + 1):
+                Lj = L[j]
+                acc = S[i][j]
+                for q in range(j):
+                    acc -= Li[q] * Lj[q]
+                if i == j:
+                    if acc <= 0:
+                        raise DesignError("stopband Gram matrix is not positive definite")
+                    Li[i] = acc.sqrt()
+                else:
+                    Li[j] = acc / Lj[j]
+        # F^T columns: moment rows sum_m m^(2r) h(m) in folded coordinates
+        Ft = [[Decimal(1 if r == 0 else 0)] + [Decimal(2 * j ** (2 * r)) for j in range(1, n)]
+              for r in range(nr)]
+        Y = []
+        for col in Ft:  # S^-1 F^T by forward / back substitution
+            z = [Decimal(0)] * n
+            for i in range(n):
+                acc = col[i]
+                Li = L[i]
+                for q in range(i):
+                    acc -= Li[q] * z[q]
+                z[i] = acc / Li[i]
+            yv = [Decimal(0)] * n
+            for i in range(n - 1, -1, -1):
+                acc = z[i]
+                for q in range(i + 1, n):
+                    acc -= L[q][i] * yv[q]
+                yv[i] = acc / L[i][i]
+            Y.append(yv)
+        M = [[sum((Ft[r][i] * Y[s][i] for i in range(n)), Decimal(0)) for s in range(nr)]
+             for r in range(nr)]
+        lam = _solve_exact([[Fraction(v) for v in row] for row in M],
+                           [Fraction(1)] + [Fraction(0)] * (nr - 1))
+        lam = [Decimal(v.numerator) / Decimal(v.denominator) for v in lam]
+        c = [sum((Y[s][i] * lam[s] for s in range(nr)), Decimal(0)) for i in range(n)]
+        taps = [float(c[abs(m)]) for m in range(-k, k + 1)]
+    # re-centre the rounding so the double-precision sum is exactly 1
+    taps[k] += 1.0 - (taps[k] + 2 * math.fsum(taps[k + 1:]))
+    return FirKernel(tuple(taps), "sym", 0)

@@ -28,6 +28,7 @@ FIR_CALLS = (
     [f"interp_diff({d})" for d in range(9)]
     + [f"fir_vm_bank({D}, {lp}, '{mode}')" for D in (3, 5, 7, 9)
        for mode, lp in (("behind_blur", 2), ("standalone", 1), ("standalone", 2))]
+    + [f"colored_sg_blur({s}, {ld})" for s, ld in ((1.0, 1), (2.0, 1), (4.5, 1), (2.0, 2), (3.5, 2))]
 )
 
 

@@ -29,7 +29,7 @@ def test_exit_codes(tmp_path, capsys):
     out = str(tmp_path / "f.json")
     assert cli.main(["design", "--family", "repeated_pole", "--sigma", "64", "--out", out]) == 3
     assert cli.main(["design", "--family", "repeated_pole", "--sigma", "0.5", "--out", out]) == 2
-    assert cli.main(["design", "--family", "colored_sg", "--sigma", "3", "--out", out]) == 2
+    assert cli.main(["design", "--family", "colored_sg", "--sigma", "0.5", "--out", out]) == 2
     assert cli.main(["apply", "--in", str(tmp_path / "missing.pgm"), "--coeff", out, "--out",
                      out]) == 2
     with pytest.raises(SystemExit):
