@@ -178,6 +178,23 @@ def cpu_time_sweep(frame, stages, reps):
     return times, threads
 
 
+def cpu_stage_times(frame, stage, threads):
+    """One scale through the oracle port, its three stages timed apart
+    (blur, Laplacian, NMS), with `threads` host threads."""
+    from oracle import oracle as O
+
+    O.set_threads(threads)
+    t0 = time.perf_counter()
+    B = O.blur(frame, stage)
+    t1 = time.perf_counter()
+    L = O.laplacian(B)
+    t2 = time.perf_counter()
+    O.detect3x3(L, 0.5)
+    t3 = time.perf_counter()
+    return {"blur_ms": round(1e3 * (t1 - t0), 1), "laplacian_ms": round(1e3 * (t2 - t1), 1),
+            "nms_ms": round(1e3 * (t3 - t2), 1), "threads": threads}
+
+
 def run_reference(args):
     rank, local, ws = dist_init("gloo")
     if rank != 0:
@@ -375,7 +392,9 @@ def run_ours(args):
         cpu = {"value": round(mpx / statistics.median(times), 2), "unit": UNIT, "cores": threads,
                "kind": "port",
                "sample": f"full {h}x{w} frame, sigma=4 repeated-pole scale, median of 3 "
-                         "(oracle/vmf_oracle.c: fp64 restatement of engine.py:35-102 + stage 4)"}
+                         "(oracle/vmf_oracle.c: fp64 restatement of engine.py:35-102 + stage 4)",
+               "stages": cpu_stage_times(frame, cat["rp4"], threads),
+               "stages_1_thread": cpu_stage_times(frame, cat["rp4"], 1)}
 
     if rank == 0:
         line = {
@@ -483,6 +502,42 @@ def other_configs(cat, flush, stream):
                               "(stream_detect's device part), one CUDA graph",
         "detections_per_frame": int(statistics.median([r.count for r in res]))}
     del dframes, x4, lap4, outs4
+
+    # config 3 with the scale-space rule: sigma^2-normalised L of the 5 IIR
+    # scales into one stack, 3x3x3 NMS over it (detect.scale_space_detect's
+    # device part; the per-scale passes on concurrent streams)
+    from paper_1912_07133_b200.engine import _ptr
+
+    f3 = synth.config3_frame(4096)
+    x3 = torch.from_numpy(f3).cuda()
+    sig3 = (2, 4, 8, 16, 32)
+    st3 = [detect.make_stage(cat[f"rp{s}"]) for s in sig3]
+    stack = torch.empty((5, 4096, 4096), dtype=torch.float32, device=x3.device)
+    dummy = [(torch.empty((1, 2), dtype=torch.int32, device=x3.device),
+              torch.empty(1, dtype=torch.float32, device=x3.device),
+              torch.empty(2, dtype=torch.int64, device=x3.device)) for _ in sig3]
+    L3 = _lib.lib()
+    ws3 = torch.empty(L3.vmf_detect3x3x3_workspace_bytes(5, 4096, 4096), dtype=torch.uint8,
+                      device=x3.device)
+    det3 = torch.empty((1 << 18, 3), dtype=torch.int32, device=x3.device)
+    val3 = torch.empty(1 << 18, dtype=torch.float32, device=x3.device)
+    scal3 = torch.zeros(2, dtype=torch.int64, device=x3.device)
+
+    def ss_step():
+        detect._sweep_launch(x3, _lib.VMF_F32, st3, 0.0, [float(s) ** 2 for s in sig3], 0, dummy,
+                             laps=[stack[i] for i in range(5)])
+        _lib.check(L3.vmf_detect3x3x3(_ptr(stack), 5, 4096, 4096, 4096, 4096 * 4096, 0.5,
+                                      _ptr(det3), _ptr(val3), 1 << 18, _ptr(scal3),
+                                      scal3.data_ptr() + 8, None, _ptr(ws3), ws3.numel(),
+                                      torch.cuda.current_stream().cuda_stream))
+
+    ms3 = graph_ms(ss_step)
+    out["config3_scale_space"] = {
+        "workload": "4096x4096 fp32, 5 repeated-pole scales, sigma^2-normalised L stack, "
+                    "3x3x3 NMS at 0.5 max|stack|",
+        "mpx_s_per_scale": round(5 * 4096 * 4096 / 1e6 / (ms3 / 1e3), 1),
+        "ms_per_sweep": round(ms3, 4)}
+    del x3, stack, ws3
 
     # config 5: 8192^2 fp32, Butterworth sigma 48 (K=2) vs colored SG 385 taps
     f5 = synth.config5_frame(8192)

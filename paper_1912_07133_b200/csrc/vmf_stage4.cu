@@ -62,17 +62,13 @@ __global__ void __launch_bounds__(kLapThreads) laplacian_kernel(
   if (threadIdx.x == 0 && absmax) atomic_max_nonneg(absmax, mx);
 }
 
-// Is linear pixel p (within plane s of ns) a detection?
+// Is pixel (s, i, j) a detection?  v = its value (already loaded).
 __device__ __forceinline__ bool is_det(const float *__restrict__ l, int64_t ld, int64_t plane,
-                                       int64_t ns, int64_t h, int64_t w, int64_t p, float thr,
-                                       float *val) {
-  int64_t hw = h * w;
-  int64_t s = p / hw, q = p - s * hw;
-  int64_t i = q / w, j = q - i * w;
+                                       int64_t ns, int64_t h, int64_t w, int64_t s, int64_t i,
+                                       int64_t j, float v, float thr) {
   if (i <= 0 || j <= 0 || i >= h - 1 || j >= w - 1) return false;
-  const float *P = l + s * plane;
-  float v = P[i * ld + j];
   if (!(fabsf(v) >= thr)) return false;
+  const float *P = l + s * plane;
   bool gt = true, lt = true;
 #pragma unroll
   for (int di = -1; di <= 1; ++di)
@@ -96,8 +92,37 @@ __device__ __forceinline__ bool is_det(const float *__restrict__ l, int64_t ld, 
         lt &= v < u;
       }
   }
-  *val = v;
   return (gt && v >= thr) || (lt && -v >= thr);
+}
+
+// Ranges of the compaction: kNmsPerBlock consecutive pixels of one row
+// (rows in (s, i) order, segments left to right), so a range's pixels are
+// contiguous in memory and the output order stays linear (s, i, j).  One
+// division per range, none per pixel.
+struct NmsRange {
+  int64_t s, i, j0;
+};
+__device__ __forceinline__ NmsRange nms_range(int64_t rg, int64_t h, int64_t nseg) {
+  const int64_t row = rg / nseg, seg = rg - row * nseg;
+  NmsRange r;
+  r.s = row / h;
+  r.i = row - r.s * h;
+  r.j0 = seg * kNmsPerBlock;
+  return r;
+}
+
+// 8 consecutive values of a row from column j (vector loads when aligned)
+__device__ __forceinline__ void ld_row8(const float *__restrict__ row, int64_t j, int64_t w,
+                                        float *v) {
+  if (j + 8 <= w && (((uintptr_t)(row + j)) & 15) == 0) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(row + j));
+    const float4 b = __ldg(reinterpret_cast<const float4 *>(row + j + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = j + e < w ? __ldg(row + j + e) : 0.0f;
+  }
 }
 
 __global__ void __launch_bounds__(kNmsThreads) nms_count_kernel(
@@ -107,17 +132,19 @@ __global__ void __launch_bounds__(kNmsThreads) nms_count_kernel(
   if (gate && !*gate) return;
   float thr = frac * *absmax;
   if (blockIdx.x == 0 && threadIdx.x == 0 && thr_out) *thr_out = thr;
-  const int64_t total = ns * h * w;
-  const int64_t nranges = (total + kNmsPerBlock - 1) / kNmsPerBlock;
+  const int64_t nseg = (w + kNmsPerBlock - 1) / kNmsPerBlock;
+  const int64_t nranges = ns * h * nseg;
   __shared__ int sc;
   for (int64_t rg = blockIdx.x; rg < nranges; rg += gridDim.x) {  // grid-stride over ranges
-    int64_t base = rg * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
+    const NmsRange r = nms_range(rg, h, nseg);
+    const int64_t j = r.j0 + (int64_t)threadIdx.x * kNmsPerThread;
     int c = 0;
-    float v;
+    if (j < w) {
+      float v[kNmsPerThread];
+      ld_row8(l + r.s * plane + r.i * ld, j, w, v);
 #pragma unroll
-    for (int e = 0; e < kNmsPerThread; ++e) {
-      int64_t p = base + e;
-      if (p < total && is_det(l, ld, plane, ns, h, w, p, thr, &v)) ++c;
+      for (int e = 0; e < kNmsPerThread; ++e)
+        if (j + e < w && is_det(l, ld, plane, ns, h, w, r.s, r.i, j + e, v[e], thr)) ++c;
     }
     if (threadIdx.x == 0) sc = 0;
     __syncthreads();
@@ -148,6 +175,7 @@ __global__ void __launch_bounds__(1024) nms_scan_kernel(int *__restrict__ counts
       run += t;
     }
     *n_det = run;
+    counts[nb] = (int)run;  // sentinel: range rg is empty iff counts[rg + 1] == counts[rg]
   }
   __syncthreads();
   int64_t run = part[threadIdx.x];
@@ -165,63 +193,62 @@ __global__ void __launch_bounds__(kNmsThreads) nms_write_kernel(
     const int *gate) {
   if (gate && !*gate) return;
   float thr = frac * *absmax;
-  const int64_t total = ns * h * w;
-  const int64_t nranges = (total + kNmsPerBlock - 1) / kNmsPerBlock;
+  const int64_t nseg = (w + kNmsPerBlock - 1) / kNmsPerBlock;
+  const int64_t nranges = ns * h * nseg;
   __shared__ int wsum[kNmsThreads / 32];
   for (int64_t rg = blockIdx.x; rg < nranges; rg += gridDim.x) {  // grid-stride over ranges
-  int64_t base = rg * kNmsPerBlock + (int64_t)threadIdx.x * kNmsPerThread;
-  unsigned flags = 0;
-  float vals[kNmsPerThread];
+    if (offsets[rg + 1] == offsets[rg]) continue;  // no detection in this range (uniform)
+    const NmsRange r = nms_range(rg, h, nseg);
+    const int64_t j = r.j0 + (int64_t)threadIdx.x * kNmsPerThread;
+    unsigned flags = 0;
+    float vals[kNmsPerThread];
+    if (j < w) {
+      ld_row8(l + r.s * plane + r.i * ld, j, w, vals);
 #pragma unroll
-  for (int e = 0; e < kNmsPerThread; ++e) {
-    int64_t p = base + e;
-    vals[e] = 0.0f;
-    if (p < total && is_det(l, ld, plane, ns, h, w, p, thr, &vals[e])) flags |= 1u << e;
-  }
-  int c = __popc(flags);
-  // block exclusive scan of c (thread order == pixel order)
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int inc = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
-  }
-  __syncthreads();
-  if (lane == 31) wsum[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    int v = lane < kNmsThreads / 32 ? wsum[lane] : 0;
+      for (int e = 0; e < kNmsPerThread; ++e)
+        if (j + e < w && is_det(l, ld, plane, ns, h, w, r.s, r.i, j + e, vals[e], thr))
+          flags |= 1u << e;
+    }
+    int c = __popc(flags);
+    // block exclusive scan of c (thread order == pixel order)
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int inc = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += t;
+      int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
     }
-    if (lane < kNmsThreads / 32) wsum[lane] = v;
-  }
-  __syncthreads();
-  int64_t pos = (int64_t)offsets[rg] + (wid ? wsum[wid - 1] : 0) + inc - c;
-  int64_t hw = h * w;
+    __syncthreads();
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < kNmsThreads / 32 ? wsum[lane] : 0;
 #pragma unroll
-  for (int e = 0; e < kNmsPerThread; ++e) {
-    if (!(flags >> e & 1u)) continue;
-    if (pos < cap) {
-      int64_t p = base + e;
-      int64_t s = p / hw, q = p - s * hw;
-      int64_t i = q / w, j = q - i * w;
-      int32_t *o = det_idx + pos * idx_stride;
-      if (idx_stride == 3) {
-        o[0] = (int32_t)s;
-        o[1] = (int32_t)i;
-        o[2] = (int32_t)j;
-      } else {
-        o[0] = (int32_t)i;
-        o[1] = (int32_t)j;
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
       }
-      det_val[pos] = vals[e];
+      if (lane < kNmsThreads / 32) wsum[lane] = v;
     }
-    ++pos;
-  }
+    __syncthreads();
+    int64_t pos = (int64_t)offsets[rg] + (wid ? wsum[wid - 1] : 0) + inc - c;
+#pragma unroll
+    for (int e = 0; e < kNmsPerThread; ++e) {
+      if (!(flags >> e & 1u)) continue;
+      if (pos < cap) {
+        int32_t *o = det_idx + pos * idx_stride;
+        if (idx_stride == 3) {
+          o[0] = (int32_t)r.s;
+          o[1] = (int32_t)r.i;
+          o[2] = (int32_t)(j + e);
+        } else {
+          o[0] = (int32_t)r.i;
+          o[1] = (int32_t)(j + e);
+        }
+        det_val[pos] = vals[e];
+      }
+      ++pos;
+    }
   }
 }
 
@@ -229,12 +256,20 @@ __global__ void absmax_kernel(const float *__restrict__ l, int64_t ld, int64_t p
                               int64_t ns, int64_t h, int64_t w, float *__restrict__ absmax) {
   __shared__ float red[32];
   float mx = 0.0f;
-  int64_t total = ns * h * w, hw = h * w;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    int64_t s = p / hw, q = p - s * hw;
-    int64_t i = q / w, j = q - i * w;
-    mx = fmaxf(mx, fabsf(l[s * plane + i * ld + j]));
+  const int64_t rows = ns * h;
+  const bool vec = (w % 4 == 0) && (ld % 4 == 0) && (plane % 4 == 0) &&
+                   (((uintptr_t)l & 15) == 0);
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t s = row / h, i = row - s * h;
+    const float *R = l + s * plane + i * ld;
+    if (vec) {
+      for (int64_t j = 4 * threadIdx.x; j < w; j += 4 * blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(R + j));
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+    } else {
+      for (int64_t j = threadIdx.x; j < w; j += blockDim.x) mx = fmaxf(mx, fabsf(R[j]));
+    }
   }
   mx = block_max(mx, red);
   if (threadIdx.x == 0) atomic_max_nonneg(absmax, mx);
@@ -267,9 +302,13 @@ int laplacian(const float *b, int64_t ldb, float *l, int64_t ldl, int64_t h, int
   return cuda_status("laplacian");
 }
 
+static int64_t nms_ranges(int64_t ns, int64_t h, int64_t w) {
+  return ns * h * cdiv(w, kNmsPerBlock);
+}
+
 size_t detect_workspace_bytes(int64_t ns, int64_t h, int64_t w) {
-  int64_t nb = cdiv(ns * h * w, kNmsPerBlock);
-  return 256 + 256 + (size_t)nb * sizeof(int) + 256;
+  int64_t nb = nms_ranges(ns, h, w);
+  return 256 + 256 + (size_t)(nb + 1) * sizeof(int) + 256;
 }
 
 // ws layout: [0,256) absmax float; [256,512) scratch; [512, ...) counts
@@ -277,7 +316,7 @@ static int detect_core(const float *l, int64_t ld, int64_t plane, int64_t ns, in
                        int64_t w, float frac, float *absmax, const int *gate, int32_t *det_idx,
                        int idx_stride, float *det_val, int64_t cap, int64_t *n_det_dev,
                        float *thr_dev, int *counts, cudaStream_t st) {
-  int64_t nb = cdiv(ns * h * w, kNmsPerBlock);
+  int64_t nb = nms_ranges(ns, h, w);
   if (nb > 0x7fffffff) return fail(VMF_EVALUE, "frame stack too large");
   // grid-stride launch: a gated (fallback) launch costs a few hundred idle CTAs
   const unsigned grid = (unsigned)(nb < (int64_t)sm_count() * 8 ? nb : (int64_t)sm_count() * 8);
