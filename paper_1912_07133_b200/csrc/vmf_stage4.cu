@@ -45,18 +45,18 @@ __global__ void __launch_bounds__(kLapThreads) laplacian_kernel(
     int64_t w, float scale, float *__restrict__ absmax) {
   __shared__ float red[kLapThreads / 32];
   float mx = 0.0f;
-  int64_t n = h * w;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = p / w, j = p - i * w;
-    int64_t iu = i > 0 ? i - 1 : 0, id = i < h - 1 ? i + 1 : h - 1;
-    int64_t jl = j > 0 ? j - 1 : 0, jr = j < w - 1 ? j + 1 : w - 1;
-    double c = (double)b[i * ldb + j];
-    double dx = (double)b[i * ldb + jr] - 2.0 * c + (double)b[i * ldb + jl];
-    double dy = (double)b[id * ldb + j] - 2.0 * c + (double)b[iu * ldb + j];
-    float v = (float)((double)scale * (dx + dy));
-    l[i * ldl + j] = v;
-    mx = fmaxf(mx, fabsf(v));
+  for (int64_t i = blockIdx.x; i < h; i += gridDim.x) {  // one row per CTA step
+    const int64_t iu = i > 0 ? i - 1 : 0, id = i < h - 1 ? i + 1 : h - 1;
+    const float *bc = b + i * ldb, *bu = b + iu * ldb, *bd = b + id * ldb;
+    for (int64_t j = threadIdx.x; j < w; j += blockDim.x) {
+      const int64_t jl = j > 0 ? j - 1 : 0, jr = j < w - 1 ? j + 1 : w - 1;
+      double c = (double)bc[j];
+      double dx = (double)bc[jr] - 2.0 * c + (double)bc[jl];
+      double dy = (double)bd[j] - 2.0 * c + (double)bu[j];
+      float v = (float)((double)scale * (dx + dy));
+      l[i * ldl + j] = v;
+      mx = fmaxf(mx, fabsf(v));
+    }
   }
   mx = block_max(mx, red);
   if (threadIdx.x == 0 && absmax) atomic_max_nonneg(absmax, mx);
@@ -291,13 +291,11 @@ static int sm_count() {
 
 int laplacian(const float *b, int64_t ldb, float *l, int64_t ldl, int64_t h, int64_t w,
               float scale, float *absmax, cudaStream_t st) {
-  int64_t n = h * w;
-  int64_t nb = cdiv(n, kLapThreads);
   int64_t cap = (int64_t)sm_count() * 8;
   {
     Launch g(K_LAPLACIAN, st);
-    laplacian_kernel<<<(int)(nb < cap ? nb : cap), kLapThreads, 0, st>>>(b, ldb, l, ldl, h, w,
-                                                                          scale, absmax);
+    laplacian_kernel<<<(int)(h < cap ? h : cap), kLapThreads, 0, st>>>(b, ldb, l, ldl, h, w,
+                                                                        scale, absmax);
   }
   return cuda_status("laplacian");
 }
