@@ -64,6 +64,10 @@ int vmf_abi_version(void);
 /* Workspace (bytes, device memory) needed by one IIR pass over `lines`
  * lines of `length` samples of order k. */
 size_t vmf_iir_workspace_bytes(int64_t lines, int64_t length, int k);
+/* workspace of vmf_iir_cols that also admits its fast path (fp32 input,
+   K 2..4: the band-parallel column pass); vmf_iir_workspace_bytes(w, h, k)
+   still works with the generic column kernel */
+size_t vmf_iir_cols_workspace_bytes(int64_t h, int64_t w, int k);
 
 /* Three-part IIR along rows: replaces iir_rows (engine.py:137-153) and
  * _iir_rows_kernel (engine.py:65-102).  Validation identical to

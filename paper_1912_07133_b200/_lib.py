@@ -44,6 +44,7 @@ _PROTOS = {
     "vmf_last_error": (C.c_char_p, []),
     "vmf_abi_version": (C.c_int, []),
     "vmf_iir_workspace_bytes": (_sz, [_i64, _i64, C.c_int]),
+    "vmf_iir_cols_workspace_bytes": (_sz, [_i64, _i64, C.c_int]),
     "vmf_iir_rows": (C.c_int, [_vp, C.c_int, _vp, _i64, _i64, _i64, _i64, _dp, _dp, C.c_int,
                                C.c_double, C.c_int, _vp, _sz, _vp]),
     "vmf_iir_cols": (C.c_int, [_vp, C.c_int, _vp, _i64, _i64, _i64, _i64, _dp, _dp, C.c_int,

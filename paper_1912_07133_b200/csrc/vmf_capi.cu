@@ -91,6 +91,13 @@ size_t vmf_iir_workspace_bytes(int64_t lines, int64_t length, int k) {
   return iir_workspace_bytes(lines, length, k);
 }
 
+size_t vmf_iir_cols_workspace_bytes(int64_t h, int64_t w, int k) {
+  size_t g = iir_workspace_bytes(w, h, k);
+  if (!colpass_supported(h, w, k)) return g;
+  size_t c = colpass_workspace_bytes(h, w, k, 0) + 256;
+  return c > g ? c : g;
+}
+
 int vmf_iir_rows(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t ldx,
                  int64_t ldy, const double *b_plus, const double *a_plus, int k, double b_zero,
                  int sign, void *ws, size_t ws_bytes, void *stream) {

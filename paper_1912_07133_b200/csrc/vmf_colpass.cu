@@ -392,7 +392,8 @@ struct ColSmem {
 };
 
 // MODE 0: L + NMS candidates; 1: the same with lap_scale == 1 (no scaling
-// multiply); 2: the fp64 blur B of the owned pixels to b64 (pitch W), no L
+// multiply); 2: the fp64 blur B of the owned pixels to b64 (pitch W), no L;
+// 3: the blur B rounded to fp32 into Lout (the iir_cols leaf)
 template <int K, int MODE>
 __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, ColParams p,
@@ -591,6 +592,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         tmax = fmaxf(tmax, fabsf(v));
         if (keep_b) ep[t] = Bt;
         if (MODE == 2 && own_col) b64[(rb + t) * p.W + col] = Bt;
+        if (MODE == 3 && own_col) Lout[(rb + t) * ldl + col] = (float)Bt;
         q = fma(-4.0, Bt, Bm1);
         Bm2 = Bm1;
         Bm1 = Bt;
@@ -612,6 +614,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         }
         if (keep_b) ep[t] = Bt;
         if (MODE == 2 && own_col && r < H) b64[r * p.W + col] = Bt;
+        if (MODE == 3 && own_col && r < H) Lout[r * ldl + col] = (float)Bt;
         Bm2 = Bm1;
         Bm1 = Bt;
       }
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     }
   }
 #undef TX
-  if (MODE == 2) return;  // B only
+  if (MODE >= 2) return;  // B only (fp64 to b64, or fp32 to Lout)
   pdl_trigger();
   __syncthreads();
 
@@ -1014,7 +1017,7 @@ int colfinal_launch(CandState *cs, const int *gy, const int *gx, const float *gv
 
 template <int K>
 static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, const ColParams &p,
-                          double *b64,
+                          double *b64, bool blur_only,
                           int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
                           float *thr_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
@@ -1069,6 +1072,8 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
                            (int)sizeof(ColSmem<K>) + 128);
       cudaFuncSetAttribute(colapply_kernel<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(ColSmem<K>) + 128);
+      cudaFuncSetAttribute(colapply_kernel<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(ColSmem<K>) + 128);
       attr = true;
     }
     dim3 grid((unsigned)cdiv(p.W, kColOut), (unsigned)p.NB);
@@ -1077,13 +1082,14 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
     int use_tma = make_tmap_2d_f32(&tmap, T, p.H, p.W, ldt, kTileStride, kTileRows(K)) &&
                   !getenv("VMF_NO_TMA");
     cudaGetLastError();
-    auto kern = b64 ? colapply_kernel<K, 2>
-                    : (p.lap_scale == 1.0f ? colapply_kernel<K, 1> : colapply_kernel<K, 0>);
+    auto kern = blur_only ? colapply_kernel<K, 3>
+                : b64   ? colapply_kernel<K, 2>
+                        : (p.lap_scale == 1.0f ? colapply_kernel<K, 1> : colapply_kernel<K, 0>);
     launch_pdl(kern, grid, dim3(kColThreads), sizeof(ColSmem<K>) + 128, st, T, ldt, L, ldl, p,
                (const double *)Z, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
                (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0), b64);
   }
-  if (p.frac > 0.0f && !b64)
+  if (p.frac > 0.0f && !b64 && !blur_only)
     colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, p.H, p.W, p.frac, det_yx, det_val, cap,
                     n_det_dev, thr_dev, st);
   return cuda_status("column pass");
@@ -1093,7 +1099,7 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
                 const IirParams &ip,
                 int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
                 float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
-                size_t ws_bytes, cudaStream_t st) {
+                size_t ws_bytes, cudaStream_t st, bool blur_only) {
   size_t need = colpass_workspace_bytes(h, w, ip.K, cap);
   if (!ws || ws_bytes < need)
     return fail(VMF_EVALUE, "column-pass workspace too small: %zu < %zu bytes", ws_bytes, need);
@@ -1147,11 +1153,11 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
   p.lap_scale = lap_scale;
   p.frac = frac;
   switch (ip.K) {
-    case 2: return launch_colpass<2>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
+    case 2: return launch_colpass<2>(T, ldt, L, ldl, p, b64, blur_only, det_yx, det_val, cap, n_det_dev, thr_dev,
                                      ws, ws_bytes, st);
-    case 3: return launch_colpass<3>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
+    case 3: return launch_colpass<3>(T, ldt, L, ldl, p, b64, blur_only, det_yx, det_val, cap, n_det_dev, thr_dev,
                                      ws, ws_bytes, st);
-    case 4: return launch_colpass<4>(T, ldt, L, ldl, p, b64, det_yx, det_val, cap, n_det_dev, thr_dev,
+    case 4: return launch_colpass<4>(T, ldt, L, ldl, p, b64, blur_only, det_yx, det_val, cap, n_det_dev, thr_dev,
                                      ws, ws_bytes, st);
   }
   return fail(VMF_EVALUE, "fused column pass supports K = 2..4, got %d", ip.K);

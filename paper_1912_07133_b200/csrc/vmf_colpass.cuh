@@ -50,11 +50,12 @@ int colfinal_launch(CandState *cs, const int *gy, const int *gx, const float *gv
                     float *thr_dev, cudaStream_t st);
 size_t colpass_workspace_bytes(int64_t h, int64_t w, int k, int64_t cand_cap);
 // T (fp32, h x w, pitch ldt) -> L (pitch ldl) + detections (sorted by y, x).
-// b64 != null: only the fp64 blur B (pitch w) is produced (no L / detections)
+// b64 != null: only the fp64 blur B (pitch w) is produced (no L / detections);
+// blur_only: only the blur B, rounded to fp32, into L (the iir_cols leaf)
 int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
                 const IirParams &ip,
                 int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
                 float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
-                size_t ws_bytes, cudaStream_t st);
+                size_t ws_bytes, cudaStream_t st, bool blur_only = false);
 
 }  // namespace vmf

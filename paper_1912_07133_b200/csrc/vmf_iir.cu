@@ -32,6 +32,7 @@
 #include "plan_cache.hpp"
 #include "vmf_prof.cuh"
 #include "vmf_rowpass.cuh"
+#include "vmf_colpass.cuh"
 
 namespace vmf {
 
@@ -426,6 +427,13 @@ int iir_pass(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t
   if (O == ROWS && rowpass_supported(w, k) && !getenv("VMF_FORCE_GENERIC"))
     return with_sample_type(x_dtype, x,
                             [&](auto xt) { return rowpass_run(xt, ldx, y, ldy, p, h, w, st); });
+  // columns, fp32, K 2..4: the band-parallel column pass (carry, scan, walk)
+  // writing the blur -- the fused pipeline's kernels without the Laplacian;
+  // needs its larger workspace (vmf_iir_cols_workspace_bytes)
+  if (O == COLS && x_dtype == VMF_F32 && colpass_supported(h, w, k) &&
+      !getenv("VMF_FORCE_GENERIC") && ws && ws_bytes >= colpass_workspace_bytes(h, w, k, 0) + 256)
+    return colpass_run((const float *)x, ldx, y, ldy, nullptr, p, h, w, 1.0f, 0.0f, nullptr,
+                       nullptr, 0, nullptr, nullptr, ws, ws_bytes, st, true);
   size_t need = iir_workspace_bytes(lines, length, k);
   if (ws_bytes < need || !ws)
     return fail(VMF_EVALUE, "IIR workspace too small: %zu < %zu bytes", ws_bytes, need);

@@ -169,7 +169,8 @@ def _iir_dev(x: torch.Tensor, code: int, f, cols: bool) -> torch.Tensor:
     y = torch.empty((h, w), dtype=torch.float32, device=x.device)
     lines, length = (w, h) if cols else (h, w)
     L = _lib.lib()
-    nbytes = L.vmf_iir_workspace_bytes(lines, length, k)
+    nbytes = (L.vmf_iir_cols_workspace_bytes(h, w, k) if cols
+              else L.vmf_iir_workspace_bytes(lines, length, k))
     ws = _workspace(nbytes)
     fn = L.vmf_iir_cols if cols else L.vmf_iir_rows
     _lib.check(fn(_ptr(x), code, _ptr(y), h, w, _pitch(x), w, _dptr(f.b_plus),
