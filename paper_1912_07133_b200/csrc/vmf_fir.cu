@@ -145,6 +145,11 @@ int fir_pass(const void *x, int x_dtype, float *y, int64_t h, int64_t w, int64_t
     return fail(VMF_EVALUE, "kernel length %d exceeds row length %lld", ntaps, (long long)length);
   // rows up to kFirMaxFast taps: the register-blocked kernel (vmf_firpass.cu)
   const bool fast = O == ROWS && ntaps <= kFirMaxFast && !getenv("VMF_FIR_GENERIC");
+  // fp32 columns: the fused column pass's tiles (window staged once per
+  // 60-row block, 8 outputs per thread) instead of the generic kernel
+  if (O == COLS && x_dtype == VMF_F32 && firpass_supported(h, w, ntaps) &&
+      !getenv("VMF_FIR_GENERIC"))
+    return fir_cols_blur((const float *)x, ldx, y, ldy, taps, ntaps, h, w, st);
   return with_sample_type(x_dtype, x, [&](auto xt) {
     if (fast) return fir_rows_fast(xt, ldx, y, ldy, h, w, taps, ntaps, st);
     return fir_bucket<O>(xt, ldx, y, ldy, h, w, taps, ntaps, st);

@@ -301,7 +301,8 @@ __device__ __forceinline__ void deriv_tile(const double *Bs, int64_t r0, int64_t
   }
 }
 
-template <class SH, int MODE>  // MODE 0: Laplacian + 3x3 NMS, 1: Hessian detector, 2: derivatives
+template <class SH, int MODE>  // MODE 0: Laplacian + 3x3 NMS, 1: Hessian detector, 2: derivatives,
+                               // 3: the blur only (fp32)
 __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, int64_t H,
     int64_t W, FirTapsP tp, float lap_scale, float frac, CandState *__restrict__ st,
@@ -374,6 +375,14 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
   }
   if (MODE == 2) {
     deriv_tile<SH>(Bs, r0, c0, H, W, ho);
+    return;
+  }
+  if (MODE == 3) {  // the conv_cols leaf: the owned blur rows, rounded to fp32
+    for (int idx = tid; idx < SH::kOwn * SH::kOut; idx += SH::kThreads) {
+      const int q = idx / SH::kOut, cl = idx - q * SH::kOut;
+      const int64_t r = r0 + q, c = c0 + cl;
+      if (r < H && c < W) Lout[r * ldl + c] = (float)Bs[(q + 2) * SH::kCols + cl + 2];
+    }
     return;
   }
   // ---- L rows r0-1 .. r0+28, columns 1 .. 126 (replicate edges) ----------
@@ -528,6 +537,23 @@ static void launch_firapply(const float *T, int64_t ldt, float *L, int64_t ldl, 
   dim3 grid((unsigned)cdiv(w, SH::kOut), (unsigned)cdiv(h, SH::kOwn));
   launch_pdl(firapply_kernel<SH, MODE>, grid, dim3(SH::kThreads), smem, st, T, ldt, L, ldl, h, w,
              tp, lap_scale, frac, cs, gy, gx, gv, (int)gcap, vec, tmap, rows, nbox, ho);
+}
+
+int fir_cols_blur(const float *T, int64_t ldt, float *y, int64_t ldy, const double *taps,
+                  int ntaps, int64_t h, int64_t w, cudaStream_t st) {
+  if (!firpass_supported(h, w, ntaps))
+    return fail(VMF_EVALUE, "FIR column tile does not support %d taps at %lldx%lld", ntaps,
+                (long long)h, (long long)w);
+  FirTapsP tp;
+  fir_plan(&tp, taps, ntaps);
+  Launch g(K_FIR_COLS, st);
+  if (tp.np > kFcLongTaps)
+    launch_firapply<FcLong, 3>(T, ldt, y, ldy, h, w, tp, 1.0f, 0.0f, nullptr, nullptr, nullptr,
+                               nullptr, 0, 0, st);
+  else
+    launch_firapply<FcShort, 3>(T, ldt, y, ldy, h, w, tp, 1.0f, 0.0f, nullptr, nullptr, nullptr,
+                                nullptr, 0, 0, st);
+  return cuda_status("fir column blur");
 }
 
 int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double *taps, int ntaps,

@@ -40,4 +40,9 @@ int hess_from_b64(const double *B, int64_t h, int64_t w, double sigma, double t1
 int deriv_from_b64(const double *B, int64_t h, int64_t w, float *const *outs, int64_t ldo,
                    cudaStream_t st);
 
+// the conv_cols leaf on the fused column tiles: y = taps (*) T along columns,
+// fp64 accumulation, fp32 out (firpass_supported shapes)
+int fir_cols_blur(const float *T, int64_t ldt, float *y, int64_t ldy, const double *taps,
+                  int ntaps, int64_t h, int64_t w, cudaStream_t st);
+
 }  // namespace vmf
