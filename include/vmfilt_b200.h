@@ -148,16 +148,22 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w,
                     int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host,
                     void *ws, size_t ws_bytes, void *stream);
 
-/* Hessian blob detector (blob.detect): row stage (IIR or
- * FIR) then a FIR column stage fused with the derivative bank fir_vm_bank(3)
- * on the fp64 blur, nd = sigma^4 (D20 D02 - D11^2), trace D20 + D02 and the
- * stationary-point displacement.  Candidates nd > t1 with the polarity
+/* Hessian blob detector: replaces the field stage of blob.detect
+ * (blob.py:143-166; hessian_det blob.py:109-111, displacement
+ * blob.py:114-128): row stage (IIR or FIR), then the
+ * column stage -- fused with the derivative bank fir_vm_bank(3)
+ * (design.py:250-280) on the fp64 blur for a FIR, or the fused IIR column
+ * pass writing the fp64 blur followed by the bank -- giving
+ * nd = sigma^4 (D20 D02 - D11^2), trace D20 + D02 and the stationary-point
+ * displacement.  Candidates nd > t1 with the polarity
  * (+1 dark: trace > 0, -1 bright: trace < 0) are appended unordered:
  * (cy, cx, cnd, cdx, cdy)[0 .. min(count, cap)), *count_dev = all found.
  * nd_field / trace_field (pitch ldn) are optional fp32 outputs.
- * vmf_greedy_nms: greedy suppression within r (d^2 <= r2) in the order
- * (nd desc, y asc, x asc); order[0 .. *n_kept_dev) = kept candidate indices,
- * strongest first. */
+ * vmf_greedy_nms: replaces the suppression loop of blob.detect
+ * (blob.py:168-176): greedy suppression within r (d^2 <= r2) in the order
+ * (nd desc, y asc, x asc) of lexsort((x, y, -nd)); order[0 .. *n_kept_dev)
+ * = kept candidate indices, strongest first (parallel rounds that keep
+ * exactly the sequential greedy set). */
 size_t vmf_hessian_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *row_stage,
                                           const vmf_stage *col_stage);
 int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
@@ -166,7 +172,7 @@ int vmf_hessian_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t
                        int64_t ldn, int32_t *cy, int32_t *cx, double *cnd, float *cdx,
                        float *cdy, int64_t cap, int32_t *count_dev, void *ws, size_t ws_bytes,
                        void *stream);
-/* engine.derivative_field(order=3) for a FIR (one fused pass) or IIR
+/* engine.derivative_field(order=3) (engine.py:205-228) for a FIR (one fused pass) or IIR
  * (fp64 blur, then the bank) column stage: D00 (the blur) D10 D01 D20 D02 D11 of the fp64 blur, fp32, pitch
  * ldo (any output may be NULL); workspace = vmf_hessian_detect_workspace_bytes. */
 int vmf_derivative_field(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
