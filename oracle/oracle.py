@@ -216,10 +216,12 @@ class _Taps:
         self.taps = tuple(taps)
 
 
-def derivative_field(x, stage, order=3):
+def derivative_field(x, stage, order=3, bank=None):
     """engine.derivative_field (engine.py:205-228): blur once, then the
-    minimal-support differentiator bank, conv_rows for d_x then conv_cols for
-    d_y, each with replicate edges; pairs with d_x + d_y >= order skipped."""
+    minimal-support differentiator bank (taps per derivative order; default
+    fir_vm_bank(3)), conv_rows for d_x then conv_cols for d_y, each with
+    replicate edges; pairs with d_x + d_y >= order skipped."""
+    bank = _BANK3 if bank is None else bank
     b = blur(x, stage)
     out = {}
     for dx in range(order):
@@ -228,9 +230,9 @@ def derivative_field(x, stage, order=3):
                 continue
             o = b
             if dx:
-                o = conv_rows(o, _Taps(_BANK3[dx]))
+                o = conv_rows(o, _Taps(bank[dx]))
             if dy:
-                o = conv_cols(o, _Taps(_BANK3[dy]))
+                o = conv_cols(o, _Taps(bank[dy]))
             out[(dx, dy)] = o
     return out
 

@@ -34,7 +34,7 @@ import torch
 
 from . import _lib
 from .errors import StabilityError
-from .filters import VM_BANK3, is_fir, is_iir
+from .filters import is_fir, is_iir
 
 __all__ = [
     "conv_rows", "conv_cols", "iir_rows", "iir_cols", "apply_rows", "apply_cols",
@@ -269,12 +269,14 @@ class DerivativeField:
 def derivative_field(img, lpf, order: int = 3, sigma: float = 0.0,
                      keep_all: bool = False) -> DerivativeField:
     """Blur once (rows then columns), then apply the minimal-support
-    differentiator bank fir_vm_bank(order) (engine.py:205-228).  Orders 1 and
-    3 are supported (bank taps pinned by the reference's tests)."""
+    differentiator bank fir_vm_bank(order) (engine.py:205-228; the bank from
+    design.fir_vm_bank, bit-identical to the reference's, so orders 3..9 and
+    the reference's ValueError for anything else)."""
     if order % 2 != 1:
         raise ValueError("order must be odd")
-    if order not in (1, 3):
-        raise ValueError("only order 1 and 3 derivative banks are built in")
+    from .design import fir_vm_bank
+
+    bank = fir_vm_bank(order, cascade_mode="behind_blur")
     x, kind, code = _as_image(img)
     h, w = x.shape
     fir_ok = is_fir(lpf) and len(lpf.taps) <= 385 and h >= 4 and w >= 4 \
@@ -296,7 +298,6 @@ def derivative_field(img, lpf, order: int = 3, sigma: float = 0.0,
         keys = ((0, 0), (1, 0), (0, 1), (2, 0), (0, 2), (1, 1))
         return DerivativeField({k: _finish(o, kind) for k, o in zip(keys, outs)}, order, sigma)
     blurred = _apply_dev(_apply_dev(x, code, lpf, False), _lib.VMF_F32, lpf, True)
-    bank = [type("Bank", (), {"taps": t})() for t in VM_BANK3[:order]]
     images = {}
     for dx in range(order):
         for dy in range(order):

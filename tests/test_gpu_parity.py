@@ -353,3 +353,27 @@ def test_stream_sweep_matches_detect_sweep(cat):
     for a, b in zip(dev, got[0]):
         np.testing.assert_array_equal(a.value, b.value)
     assert max(d.count for d in got[0]) > 8
+
+
+def test_derivative_field_order5(cat):
+    """Higher-order bank (fir_vm_bank(5), taps from the reference-generated
+    design golden file) through the unfused path; order 1 is rejected like
+    the reference's fir_vm_bank."""
+    import json
+    import os
+
+    E = _E()
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "design_golden.json")))
+    bank = [k["taps"] for k in g["fir_vm_bank(5, 2, 'behind_blur')"]["fir"]]
+    x = _f32(synth.config1_frame())[:200, :256]
+    st = cat["g2_k8"]
+    got = E.derivative_field(x, st, order=5)
+    ref = O.derivative_field(x, st, order=5, bank=bank)
+    assert set(got.images) == set(ref)
+    for key, r in ref.items():
+        # derivatives of total order >= 4 are differences of the fp32-rounded
+        # blur (the fused order-3 bank works on the fp64 blur): 1e-3 there
+        tol = 1e-4 if sum(key) <= 3 else 1e-3
+        assert max_rel_err(got[key], r) < tol, key
+    with pytest.raises(ValueError):
+        E.derivative_field(x, st, order=1)

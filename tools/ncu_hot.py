@@ -13,6 +13,10 @@ cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sa
        f"regex:{kern}"]
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
+# the page repeats the whole listing per matching launch record: keep the first
+kn = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+if len(kn) > 1:
+    rows = rows[:kn[1]]
 hi = [i for i, r in enumerate(rows) if r and r[0] == "Line No"][0]
 hdr = rows[hi]
 si = hdr.index("Warp Stall Sampling (All Samples)")

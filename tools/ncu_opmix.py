@@ -12,6 +12,10 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
                       "-k", f"regex:{kern}"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
+# the page repeats the whole listing per matching launch record: keep the first
+kn = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+if len(kn) > 1:
+    rows = rows[:kn[1]]
 hi = [i for i, r in enumerate(rows) if "Source" in r and "Instructions Executed" in r][0]
 hdr = rows[hi]
 src, ie = hdr.index("Source"), hdr.index("Instructions Executed")

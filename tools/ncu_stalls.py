@@ -9,6 +9,10 @@ if kern:
     cmd += ["-k", f"regex:{kern}"]
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
+# the page repeats the whole listing per matching launch record: keep the first
+kn = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+if len(kn) > 1:
+    rows = rows[:kn[1]]
 hi = [i for i, r in enumerate(rows) if "Address" in r and "Source" in r][0]
 hdr = rows[hi]
 reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
