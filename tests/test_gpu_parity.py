@@ -377,3 +377,20 @@ def test_derivative_field_order5(cat):
         assert max_rel_err(got[key], r) < tol, key
     with pytest.raises(ValueError):
         E.derivative_field(x, st, order=1)
+
+
+@pytest.mark.parametrize("shape", [(257, 389), (70, 1030), (1024, 131)])
+@pytest.mark.parametrize("name", ["rp4_k2", "rp8", "rp4_k4", "bw6", "g4_k16", "g16_k64"])
+def test_column_leaves_fast_paths(cat, shape, name):
+    """iir_cols / conv_cols on fp32 frames run on the fused pipeline's column
+    kernels in blur-only mode (colapply / firapply MODE 3); odd shapes, both
+    parities of band and tile edges."""
+    E = _E()
+    st = cat[name]
+    if F.is_fir(st) and len(st.taps) > shape[0]:
+        pytest.skip("kernel longer than the column")
+    x = np.random.default_rng(11).standard_normal(shape).astype(np.float32) + 0.5
+    op = "conv_cols" if F.is_fir(st) else "iir_cols"
+    got = getattr(E, op)(x, st)
+    want = getattr(O, op)(x, st)
+    assert max_rel_err(got, want) < PASS_TOL, (name, shape)
