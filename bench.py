@@ -231,7 +231,6 @@ def run_reference(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 def run_ours(args):
-    import numpy as np
     import torch
 
     rank, local, ws = dist_init("nccl")

@@ -2,7 +2,6 @@
 reference's outputs (tests/golden/blob_golden.json) and the oracle; the
 greedy NMS kernel against a direct sequential implementation."""
 import json
-import math
 import os
 
 import numpy as np
