@@ -178,6 +178,25 @@ def cpu_time_sweep(frame, stages, reps):
     return times, threads
 
 
+DFMA_PEAK_T = 16.44  # T fp64 FMA/s: profiles/r1_pipes.txt (tools/microbench/pipes.cu on this pool)
+
+
+def compute_roofline(per_scale):
+    """Per scale, the algorithmic fp64 FMA rate against the measured DFMA
+    peak (SURVEY.md §8(d): IIR 4K+1 = 13 FMA per pixel per pass for K = 3;
+    FIR one FMA per tap per pass; both passes)."""
+    out = {"peak_tfma_s": DFMA_PEAK_T, "peak_source": "profiles/r1_pipes.txt", "iir": {},
+           "fir": {}}
+    for sg, v in per_scale["iir"].items():
+        a = v * 1e6 * 2 * 13 / 1e12
+        out["iir"][sg] = {"tfma_s": round(a, 2), "frac": round(a / DFMA_PEAK_T, 3)}
+    for sg, v in per_scale["fir"].items():
+        taps = 2 * int(4 * float(sg)) + 1  # gaussian_fir(sigma, 0, 4 sigma)
+        a = v * 1e6 * 2 * taps / 1e12
+        out["fir"][sg] = {"taps": taps, "tfma_s": round(a, 2), "frac": round(a / DFMA_PEAK_T, 3)}
+    return out
+
+
 def cpu_stage_times(frame, stage, threads):
     """One scale through the oracle port, its three stages timed apart
     (blur, Laplacian, NMS), with `threads` host threads."""
@@ -412,6 +431,7 @@ def run_ours(args):
                          "algo_bytes_per_launch": algo, "avg_launch_ms": round(per_launch_ms, 5)},
             "path_roofline": {"bytes_per_px": PATH_BYTES_PER_PX, "achieved": round(path_gbs, 1),
                               "peak": hbm, "frac": round(path_gbs / hbm, 4), "unit": "GB/s"},
+            "compute_roofline": compute_roofline(per_scale),
             "kernels": {k: {"avg_ms": round(v[0] / v[1], 5), "launches": v[1]}
                         for k, v in prof.items()},
             "e2e": {"value": round(e2e, 1), "unit": UNIT,
