@@ -142,6 +142,15 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w,
  * neighbours (one-sided at the first/last scale), |N| >= frac*max|N| over
  * the whole stack.  Detections sorted by (s, y, x): det_syx[3i..3i+2]. */
 size_t vmf_detect3x3x3_workspace_bytes(int64_t ns, int64_t h, int64_t w);
+/* The same with the stack maximum supplied (max |n| of a larger stack this
+ * one is a slab of -- the scale-sharded sweep: each rank's
+ * slab carries one halo plane of each neighbour and the all-reduced max):
+ * threshold = frac * *absmax_dev. */
+int vmf_detect3x3x3_absmax(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ldn,
+                           int64_t plane_stride, float frac, const float *absmax_dev,
+                           int32_t *det_syx, float *det_val, int64_t cap, int64_t *n_det_dev,
+                           float *thr_dev, int64_t *n_det_host, void *ws, size_t ws_bytes,
+                           void *stream);
 int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w,
                     int64_t ldn, int64_t plane_stride, float frac,
                     int32_t *det_syx, float *det_val, int64_t cap,

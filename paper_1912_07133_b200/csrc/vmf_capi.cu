@@ -154,6 +154,22 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ld
                 thr_dev, n_det_host, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int vmf_detect3x3x3_absmax(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ldn,
+                           int64_t plane_stride, float frac, const float *absmax_dev,
+                           int32_t *det_syx, float *det_val, int64_t cap, int64_t *n_det_dev,
+                           float *thr_dev, int64_t *n_det_host, void *ws, size_t ws_bytes,
+                           void *stream) {
+  if (ns < 1 || h < 1 || w < 1) return fail(VMF_EVALUE, "stack must be 3-D and non-empty");
+  if (ldn < w || plane_stride < h * ldn) return fail(VMF_EVALUE, "bad stack strides");
+  if (!absmax_dev) return fail(VMF_EVALUE, "absmax_dev must not be NULL");
+  if (!ws || ws_bytes < detect_workspace_bytes(ns, h, w))
+    return fail(VMF_EVALUE, "detect workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(detect_absmax_slot(ws), absmax_dev, sizeof(float), cudaMemcpyDeviceToDevice, st);
+  return detect(n, ldn, plane_stride, ns, h, w, frac, true, det_syx, 3, det_val, cap, n_det_dev,
+                thr_dev, n_det_host, ws, ws_bytes, st);
+}
+
 static bool iir_b64(const vmf_stage *col_stage, int64_t h, int64_t w) {
   return col_stage && col_stage->kind == VMF_STAGE_IIR && colpass_supported(h, w, col_stage->n);
 }

@@ -394,3 +394,20 @@ def test_column_leaves_fast_paths(cat, shape, name):
     got = getattr(E, op)(x, st)
     want = getattr(O, op)(x, st)
     assert max_rel_err(got, want) < PASS_TOL, (name, shape)
+
+
+def test_scale_sharded_detect_single_rank(cat):
+    """shard.scale_space_detect on one rank (no process group) equals the
+    unsharded scale-space detector: same L stack, threshold and blobs (the
+    multi-rank exchange logic is covered on CPU by test_multiproc.py)."""
+    from paper_1912_07133_b200 import shard
+
+    D = _D()
+    x = synth.config3_frame(1024)
+    spec = synth.CONFIG_STAGES[3]
+    stages = [cat[n] for n in spec["iir"]]
+    sig = spec["sigmas"]
+    ref = D.scale_space_detect(x, stages, sig, frac=0.5)
+    got = shard.scale_space_detect(x, stages, sig, frac=0.5)
+    assert got.threshold == ref.threshold and got.count == ref.count
+    assert got.as_set() == ref.as_set()
