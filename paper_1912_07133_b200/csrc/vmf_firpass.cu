@@ -190,6 +190,7 @@ struct FcSmall {
   float cv[kFcCand];
   int ccount, coverflow;
   unsigned cmax;
+  float thr_end;
 };
 
 // Hessian detector outputs (MODE 1, blob.py:109-128,158-163)
@@ -301,62 +302,21 @@ __device__ __forceinline__ void deriv_tile(const double *Bs, int64_t r0, int64_t
   }
 }
 
-template <class SH, int MODE>  // MODE 0: Laplacian + 3x3 NMS, 1: Hessian detector, 2: derivatives,
-                               // 3: the blur only (fp32)
-__global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_kernel(
-    const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, int64_t H,
-    int64_t W, FirTapsP tp, float lap_scale, float frac, CandState *__restrict__ st,
-    int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv, int gcap, int vec_out,
-    const __grid_constant__ CUtensorMap tmap, int tma_rows, int tma_boxes, HessOut ho) {
-  extern __shared__ __align__(128) unsigned char fsm_raw[];
-  __shared__ FcSmall S;
-  __shared__ __align__(8) uint64_t fbar;
-  // 128-byte aligned base (TMA destination), derived from the shared array
-  const unsigned sbase = (unsigned)__cvta_generic_to_shared(fsm_raw);
-  unsigned char *fsm = fsm_raw + ((128u - (sbase & 127u)) & 127u);
-  float *win = reinterpret_cast<float *>(fsm);  // [kRB + np + 8][kStride]
-  double *Bs = reinterpret_cast<double *>(fsm);  // [kRB][kCols] (after the window)
+// One tile of the fused column pass on a staged window `fsm` (B and L reuse
+// the window's space once the taps are done).  Every thread of the CTA calls
+// it; it contains block barriers.
+template <class SH, int MODE>
+__device__ __forceinline__ void fc_tile(
+    unsigned char *fsm, FcSmall &S, int64_t c0, int64_t r0, float *__restrict__ Lout, int64_t ldl,
+    int64_t H, int64_t W, const FirTapsP &tp, float lap_scale, float frac,
+    CandState *__restrict__ st, int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv,
+    int gcap, int vec_out, const HessOut &ho) {
+  const float *win = reinterpret_cast<const float *>(fsm);  // [kRB + np + 8][kStride]
+  double *Bs = reinterpret_cast<double *>(fsm);              // [kRB][kCols]
   float *Ls = reinterpret_cast<float *>(fsm + (size_t)SH::kRB * SH::kCols * sizeof(double));
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int j = tid & (SH::kCols - 1), g = tid / SH::kCols;
-  const int k = (tp.n - 1) / 2;
-  const int64_t c0 = (int64_t)blockIdx.x * SH::kOut;
-  const int64_t r0 = (int64_t)blockIdx.y * SH::kOwn;
   const int64_t rB0 = r0 - 2;  // image row of B tile row 0
-  const int wrows = SH::kRB + tp.np + 8;
-  if (tid == 0) {
-    S.ccount = 0;
-    S.coverflow = 0;
-    S.cmax = 0u;
-  }
-  pdl_wait();
-  // ---- stage the column window: row w <-> image row rB0 - k + w, column
-  //      cc <-> image column c0 - 4 + cc, both edge-clamped ----------------
-  const int64_t rw0 = rB0 - k;  // image row of window row 0
-  const bool tma = tma_boxes > 0 && rw0 >= 0 && rw0 + (int64_t)tma_boxes * tma_rows <= H &&
-                   c0 >= 4 && c0 - 4 + SH::kStride <= W;
-  if (tma) {  // interior tile: tma_boxes boxes of tma_rows x kStride
-    if (tid == 0) {
-      mbar_init(&fbar, 1);
-      mbar_expect_tx(&fbar, (unsigned)(tma_boxes * tma_rows * SH::kStride * sizeof(float)));
-      for (int bx = 0; bx < tma_boxes; ++bx)
-        tma_load_2d_hint(win + bx * tma_rows * SH::kStride, &tmap, &fbar, (int)(c0 - 4),
-                         (int)(rw0 + bx * tma_rows), l2_policy_evict_first());
-    }
-    __syncthreads();
-    mbar_wait(&fbar, 0);
-  } else {
-    for (int idx = tid; idx < wrows * SH::kStride; idx += SH::kThreads) {
-      const int wr = idx / SH::kStride, cc = idx - wr * SH::kStride;
-      int64_t r = rw0 + wr, c = c0 - 4 + cc;
-      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
-      c = c < 0 ? 0 : (c >= W ? W - 1 : c);
-      const unsigned sa = (unsigned)__cvta_generic_to_shared(win + idx);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + c));
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
-  }
-  __syncthreads();
   // ---- B rows 8g .. 8g+7 of column j (tile column j + 2) -------------------
   double acc[8];
 #pragma unroll
@@ -385,22 +345,30 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
     }
     return;
   }
-  // ---- L rows r0-1 .. r0+28, columns 1 .. 126 (replicate edges) ----------
+  // ---- L rows r0-1 .. r0+kOwn (B tile rows 1 .. kRB-2), replicate edges ---
+  // Thread (g, j) forms L at its own 8 B rows: centre and (inside the group)
+  // vertical neighbours from registers, horizontal ones from Bs.  Columns
+  // outside the image were filtered from clamped inputs, so they already
+  // hold the replicated edge column.
   const double lsc = (double)lap_scale;
   float tmax = 0.0f;
-  for (int idx = tid; idx < SH::kLR * SH::kCols; idx += SH::kThreads) {
-    const int lr = idx / SH::kCols, jj = idx - lr * SH::kCols;
-    const int64_t r = r0 - 1 + lr, c = c0 - 2 + jj;
-    if (jj == 0 || jj == SH::kCols - 1 || r < 0 || r >= H) continue;
-    const int64_t ru = r > 0 ? r - 1 : 0, rd = r + 1 < H ? r + 1 : H - 1;
-    const double *bc = Bs + (r - rB0) * SH::kCols + jj;
-    // columns outside the image were filtered from clamped inputs, so they
-    // already hold the replicated edge column
-    const double bl = bc[-1], br = bc[1];
-    const double bu = Bs[(ru - rB0) * SH::kCols + jj], bd = Bs[(rd - rB0) * SH::kCols + jj];
-    const float v = (float)(lsc * fma(-4.0, bc[0], (bl + br) + (bu + bd)));
-    Ls[lr * SH::kStride + jj + 2] = v;
-    if (c >= 0 && c < W) tmax = fmaxf(tmax, fabsf(v));
+  if (j != 0 && j != SH::kCols - 1) {
+    const int64_t c = c0 - 2 + j;
+    const bool cin = c >= 0 && c < W;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int tr = 8 * g + q;
+      if (tr == 0 || tr == SH::kRB - 1) continue;
+      const int64_t r = rB0 + tr;
+      if (r < 0 || r >= H) continue;
+      const double bc = acc[q];
+      const double bu = r == 0 ? bc : (q > 0 ? acc[q - 1] : Bs[(tr - 1) * SH::kCols + j]);
+      const double bd = r + 1 >= H ? bc : (q < 7 ? acc[q + 1] : Bs[(tr + 1) * SH::kCols + j]);
+      const double bl = Bs[tr * SH::kCols + j - 1], br = Bs[tr * SH::kCols + j + 1];
+      const float v = (float)(lsc * fma(-4.0, bc, (bl + br) + (bu + bd)));
+      Ls[(tr - 1) * SH::kStride + j + 2] = v;
+      if (cin) tmax = fmaxf(tmax, fabsf(v));
+    }
   }
   tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
   if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
@@ -466,16 +434,15 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
   }
   __syncthreads();
   // ---- flush the candidates that survive the best threshold known now -----
-  __shared__ float thr_end;
   if (tid == 0) {
     unsigned old = atomicMax(&st->absmax_bits, S.cmax);
-    thr_end = frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
+    S.thr_end = frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
     if (S.coverflow) st->overflow = 1;
   }
   __syncthreads();
   const int n = S.ccount < kFcCand ? S.ccount : kFcCand;
   for (int q = tid; q < n; q += SH::kThreads) {
-    if (!(fabsf(S.cv[q]) >= thr_end)) continue;
+    if (!(fabsf(S.cv[q]) >= S.thr_end)) continue;
     int kk = atomicAdd(&st->count, 1);
     if (kk < gcap) {
       gy[kk] = S.cy[q];
@@ -485,6 +452,69 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
       st->overflow = 1;
     }
   }
+}
+
+// Fused column pass: one CTA per tile (tile = row-band-major over ntx column
+// tiles).  The window of an interior tile is one TMA transfer (tma_boxes
+// boxes), edge tiles are staged with clamped cp.async copies.  (A persistent
+// variant that stages the next tile's window into a second buffer while the
+// current one is filtered measured 2-12 % slower at every tap count: the
+// other resident CTAs already hide the staging, and the second buffer costs
+// occupancy.)
+template <class SH, int MODE>  // MODE 0: Laplacian + 3x3 NMS, 1: Hessian detector, 2: derivatives,
+                               // 3: the blur only (fp32)
+__global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_kernel(
+    const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl, int64_t H,
+    int64_t W, FirTapsP tp, float lap_scale, float frac, CandState *__restrict__ st,
+    int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv, int gcap, int vec_out,
+    const __grid_constant__ CUtensorMap tmap, int tma_rows, int tma_boxes, HessOut ho) {
+  extern __shared__ __align__(128) unsigned char fsm_raw[];
+  __shared__ FcSmall S;
+  __shared__ __align__(8) uint64_t fbar;
+  // 128-byte aligned base (TMA destination), derived from the shared array
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(fsm_raw);
+  unsigned char *fsm = fsm_raw + ((128u - (sbase & 127u)) & 127u);
+  float *win = reinterpret_cast<float *>(fsm);
+  const int tid = threadIdx.x;
+  const int k = (tp.n - 1) / 2;
+  const int wrows = SH::kRB + tp.np + 8;
+  const int64_t c0 = (int64_t)blockIdx.x * SH::kOut;
+  const int64_t r0 = (int64_t)blockIdx.y * SH::kOwn;
+  if (tid == 0) {
+    S.ccount = 0;
+    S.coverflow = 0;
+    S.cmax = 0u;
+  }
+  pdl_wait();
+  // ---- stage the column window: row w <-> image row r0 - 2 - k + w, column
+  //      cc <-> image column c0 - 4 + cc, both edge-clamped ----------------
+  const int64_t rw0 = r0 - 2 - k;
+  const bool tma = tma_boxes > 0 && rw0 >= 0 && rw0 + (int64_t)tma_boxes * tma_rows <= H &&
+                   c0 >= 4 && c0 - 4 + SH::kStride <= W;
+  if (tma) {  // interior tile: tma_boxes boxes of tma_rows x kStride
+    if (tid == 0) {
+      mbar_init(&fbar, 1);
+      mbar_expect_tx(&fbar, (unsigned)(tma_boxes * tma_rows * SH::kStride * sizeof(float)));
+      for (int bx = 0; bx < tma_boxes; ++bx)
+        tma_load_2d_hint(win + bx * tma_rows * SH::kStride, &tmap, &fbar, (int)(c0 - 4),
+                         (int)(rw0 + bx * tma_rows), l2_policy_evict_first());
+    }
+    __syncthreads();
+    mbar_wait(&fbar, 0);
+  } else {
+    for (int idx = tid; idx < wrows * SH::kStride; idx += SH::kThreads) {
+      const int wr = idx / SH::kStride, cc = idx - wr * SH::kStride;
+      int64_t r = rw0 + wr, c = c0 - 4 + cc;
+      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+      c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(win + idx);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + c));
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  }
+  __syncthreads();
+  fc_tile<SH, MODE>(fsm, S, c0, r0, Lout, ldl, H, W, tp, lap_scale, frac, st, gy, gx, gv, gcap,
+                    vec_out, ho);
 }
 
 template <class SH>
