@@ -161,11 +161,11 @@ template int fir_rows_fast<uint16_t>(const uint16_t *, int64_t, float *, int64_t
 // fused column pass
 // ---------------------------------------------------------------------------
 // Tile shapes: COLS computed columns (COLS-4 owned), GROUPS groups of 8 B rows
-// (8 GROUPS - 4 owned L rows).  Short FIRs (<= 64 taps): 64 x 4, 256 threads
-// (more CTAs per SM mix the staging / taps / Laplacian phases: +5 % over
-// 128 x 4 at 33 taps); long FIRs: 64 x 8, so the 2k-row halo of the column
-// window is shared by 60 B rows instead of 28 (64 x 4 measured 8-23 % slower
-// there).
+// (8 GROUPS - 4 owned L rows).  Every tap count uses 64 x 8 (512 threads):
+// the 2k-row halo of the column window is shared by 60 B rows.  Measured per
+// scale on 4096^2 (tools/fir_ab.py): 64 x 4 ties at 33 taps and is 9-23 %
+// slower at 17 and >= 65 taps; 128 x 4, 32 x 8 and 64 x 16 are slower at
+// every tap count.
 template <int COLS, int GROUPS>
 struct FcShape {
   static constexpr int kCols = COLS, kOut = COLS - 4, kGroups = GROUPS;
@@ -180,9 +180,7 @@ struct FcShape {
     return win > bl ? win : bl;
   }
 };
-using FcShort = FcShape<64, 4>;
 using FcLong = FcShape<64, 8>;
-constexpr int kFcLongTaps = 64;  // np above this: the long tile
 constexpr int kFcCand = 256;
 
 struct FcSmall {
@@ -526,7 +524,7 @@ static size_t fc_smem(int np) {
   return (r > box ? r : box) + 128;
 }
 static size_t fc_smem_any(int np) {
-  return np > kFcLongTaps ? fc_smem<FcLong>(np) : fc_smem<FcShort>(np);
+  return fc_smem<FcLong>(np);
 }
 
 bool firpass_supported(int64_t h, int64_t w, int ntaps) {
@@ -577,12 +575,8 @@ int fir_cols_blur(const float *T, int64_t ldt, float *y, int64_t ldy, const doub
   FirTapsP tp;
   fir_plan(&tp, taps, ntaps);
   Launch g(K_FIR_COLS, st);
-  if (tp.np > kFcLongTaps)
-    launch_firapply<FcLong, 3>(T, ldt, y, ldy, h, w, tp, 1.0f, 0.0f, nullptr, nullptr, nullptr,
-                               nullptr, 0, 0, st);
-  else
-    launch_firapply<FcShort, 3>(T, ldt, y, ldy, h, w, tp, 1.0f, 0.0f, nullptr, nullptr, nullptr,
-                                nullptr, 0, 0, st);
+  launch_firapply<FcLong, 3>(T, ldt, y, ldy, h, w, tp, 1.0f, 0.0f, nullptr, nullptr, nullptr,
+                             nullptr, 0, 0, st);
   return cuda_status("fir column blur");
 }
 
@@ -607,12 +601,8 @@ int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double
   {
     Launch g(K_FIR_COLS, st);
     const int vec = (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0);
-    if (tp.np > kFcLongTaps)
-      launch_firapply<FcLong>(T, ldt, L, ldl, h, w, tp, lap_scale, frac, cs, gy, gx, gv, gcap, vec,
-                              st);
-    else
-      launch_firapply<FcShort>(T, ldt, L, ldl, h, w, tp, lap_scale, frac, cs, gy, gx, gv, gcap,
-                               vec, st);
+    launch_firapply<FcLong>(T, ldt, L, ldl, h, w, tp, lap_scale, frac, cs, gy, gx, gv, gcap, vec,
+                            st);
   }
   int rc = cuda_status("fir column pass");
   if (rc) return rc;
@@ -648,12 +638,8 @@ int hesspass_run(const float *T, int64_t ldt, const double *taps, int ntaps, int
   ho.count = count;
   cudaMemsetAsync(count, 0, sizeof(int), st);
   Launch g(K_FIR_COLS, st);
-  if (tp.np > kFcLongTaps)
-    launch_firapply<FcLong, 1>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
-                               nullptr, nullptr, 0, 0, st, &ho);
-  else
-    launch_firapply<FcShort, 1>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
-                                nullptr, nullptr, 0, 0, st, &ho);
+  launch_firapply<FcLong, 1>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
+                             nullptr, nullptr, 0, 0, st, &ho);
   return cuda_status("hessian pass");
 }
 
@@ -785,12 +771,8 @@ int derivpass_run(const float *T, int64_t ldt, const double *taps, int ntaps, in
   ho.ldn = ldo;
   for (int d = 0; d < 6; ++d) ho.deriv[d] = outs[d];
   Launch g(K_FIR_COLS, st);
-  if (tp.np > kFcLongTaps)
-    launch_firapply<FcLong, 2>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
-                               nullptr, nullptr, 0, 0, st, &ho);
-  else
-    launch_firapply<FcShort, 2>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
-                                nullptr, nullptr, 0, 0, st, &ho);
+  launch_firapply<FcLong, 2>(T, ldt, nullptr, 0, h, w, tp, 1.0f, 0.0f, nullptr, nullptr,
+                             nullptr, nullptr, 0, 0, st, &ho);
   return cuda_status("derivative pass");
 }
 
