@@ -90,18 +90,43 @@ __global__ void __launch_bounds__(kFrThreads) fir_rows_fast_kernel(const T *__re
                                                                    float *__restrict__ y,
                                                                    int64_t ldy, int64_t h,
                                                                    int64_t w, FirTapsP tp,
-                                                                   int vec_out) {
-  extern __shared__ __align__(16) float fwin[];  // [kFrSeg + np + 16]
+                                                                   int vec_out, int vec_in) {
+  extern __shared__ __align__(16) float fwin_raw[];  // [kFrSeg + np + 16]
   const int k = (tp.n - 1) / 2;
   const int nwin = kFrSeg + tp.np + 16;
   const int64_t n0 = (int64_t)blockIdx.x * kFrSeg;
   const int base = 8 * threadIdx.x;
+  // window sample q = image column s0 + q at fwin[q]; with s0 a multiple of
+  // 4 (k % 4 == 0: every Gaussian / SG kernel of the configs) the window is
+  // staged in 16-byte units.  fwin stays 16-byte aligned either way: the
+  // 8-output register blocks then read it as LDS.128.
+  const int64_t s0 = n0 - k;
+  const int nv = (nwin + 3) / 4;
+  const bool vec = sizeof(T) == 4 && vec_in && (k & 3) == 0;
+  float *fwin = fwin_raw;
   for (int64_t row = blockIdx.y; row < h; row += gridDim.y) {
     __syncthreads();
     const T *xr = x + row * ldx;
-    if (sizeof(T) == 4) {  // asynchronous 4-byte copies: the whole window in flight at once
+    if (vec) {  // 16-byte asynchronous copies; units crossing an edge are clamped per sample
+      const float *xf = reinterpret_cast<const float *>(xr);
+      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const int64_t g = s0 + 4 * v;
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(fwin_raw + 4 * v);
+        if (g >= 0 && g + 4 <= w) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(xf + g));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int64_t c = g + e < 0 ? 0 : (g + e >= w ? w - 1 : g + e);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa + 4 * e),
+                         "l"(xf + c));
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+    } else if (sizeof(T) == 4) {  // asynchronous 4-byte copies: the whole window in flight at once
       for (int q = threadIdx.x; q < nwin; q += blockDim.x) {
-        int64_t c = n0 - k + q;
+        int64_t c = s0 + q;
         c = c < 0 ? 0 : (c >= w ? w - 1 : c);
         const unsigned sa = (unsigned)__cvta_generic_to_shared(fwin + q);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(xr + c));
@@ -109,7 +134,7 @@ __global__ void __launch_bounds__(kFrThreads) fir_rows_fast_kernel(const T *__re
       asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
     } else {
       for (int q = threadIdx.x; q < nwin; q += blockDim.x) {
-        int64_t c = n0 - k + q;
+        int64_t c = s0 + q;
         c = c < 0 ? 0 : (c >= w ? w - 1 : c);
         fwin[q] = ldf32(xr + c);
       }
@@ -142,9 +167,10 @@ int fir_rows_fast(const T *x, int64_t ldx, float *y, int64_t ldy, int64_t h, int
   fir_plan(&tp, taps, ntaps);
   const size_t smem = (size_t)(kFrSeg + tp.np + 16) * sizeof(float);
   const int vec = (ldy % 4 == 0) && ((uintptr_t)y % 16 == 0);
+  const int vin = (ldx % 4 == 0) && ((uintptr_t)x % 16 == 0);
   dim3 grid((unsigned)cdiv(w, kFrSeg), (unsigned)(h < 65535 ? h : 65535));
   Launch g(K_FIR_ROWS, st);
-  fir_rows_fast_kernel<T><<<grid, kFrThreads, smem, st>>>(x, ldx, y, ldy, h, w, tp, vec);
+  fir_rows_fast_kernel<T><<<grid, kFrThreads, smem, st>>>(x, ldx, y, ldy, h, w, tp, vec, vin);
   return cuda_status("fir row pass");
 }
 
@@ -308,7 +334,7 @@ __device__ __forceinline__ void fc_tile(
     unsigned char *fsm, FcSmall &S, int64_t c0, int64_t r0, float *__restrict__ Lout, int64_t ldl,
     int64_t H, int64_t W, const FirTapsP &tp, float lap_scale, float frac,
     CandState *__restrict__ st, int *__restrict__ gy, int *__restrict__ gx, float *__restrict__ gv,
-    int gcap, int vec_out, const HessOut &ho) {
+    int gcap, int vec_out, const HessOut &ho, float gbound) {
   const float *win = reinterpret_cast<const float *>(fsm);  // [kRB + np + 8][kStride]
   double *Bs = reinterpret_cast<double *>(fsm);              // [kRB][kCols]
   float *Ls = reinterpret_cast<float *>(fsm + (size_t)SH::kRB * SH::kCols * sizeof(double));
@@ -372,14 +398,16 @@ __device__ __forceinline__ void fc_tile(
   if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
   pdl_trigger();
   __syncthreads();
-  if (tid == 0) atomicMax(&st->absmax_bits, S.cmax);
-  const float gnow = __uint_as_float(*(volatile unsigned *)&st->absmax_bits);
+  // publish this tile's max; the previous global max comes back while the
+  // block is stored and only the flush needs it
+  unsigned old = 0u;
+  if (tid == 0) old = atomicMax(&st->absmax_bits, S.cmax);
   // ---- owned block out (float4 rows) + strict 3x3 NMS ---------------------
   {
     const int nrow = (int)(H - r0 < SH::kOwn ? H - r0 : SH::kOwn);
     const int ncol = (int)(W - c0 < SH::kOut ? W - c0 : SH::kOut);
     // frac <= 0: L only (scale-space stacks), no candidates
-    const float th = frac > 0.0f ? frac * fmaxf(__uint_as_float(S.cmax), gnow)
+    const float th = frac > 0.0f ? frac * fmaxf(__uint_as_float(S.cmax), gbound)
                                  : __int_as_float(0x7f800000);
     auto test = [&](int q, int c, float v) {  // L tile row q + 1, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
@@ -433,7 +461,6 @@ __device__ __forceinline__ void fc_tile(
   __syncthreads();
   // ---- flush the candidates that survive the best threshold known now -----
   if (tid == 0) {
-    unsigned old = atomicMax(&st->absmax_bits, S.cmax);
     S.thr_end = frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
     if (S.coverflow) st->overflow = 1;
   }
@@ -484,6 +511,9 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
     S.cmax = 0u;
   }
   pdl_wait();
+  // global max |L| published so far (a lower bound of the final one; read
+  // now so the load hides under the staging and the taps)
+  const float gbound = MODE == 0 ? __uint_as_float(*(volatile unsigned *)&st->absmax_bits) : 0.0f;
   // ---- stage the column window: row w <-> image row r0 - 2 - k + w, column
   //      cc <-> image column c0 - 4 + cc, both edge-clamped ----------------
   const int64_t rw0 = r0 - 2 - k;
@@ -512,7 +542,7 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
   }
   __syncthreads();
   fc_tile<SH, MODE>(fsm, S, c0, r0, Lout, ldl, H, W, tp, lap_scale, frac, st, gy, gx, gv, gcap,
-                    vec_out, ho);
+                    vec_out, ho, gbound);
 }
 
 template <class SH>

@@ -1,6 +1,8 @@
 """GPU parity against the CPU oracle (pinned to the reference by
 tests/test_oracle.py).  Every call goes through the C ABI
 (libvmfilt_b200.so) via the drop-in engine / detect API."""
+import zlib
+
 import numpy as np
 import pytest
 import torch
@@ -321,7 +323,8 @@ def test_derivative_field_fused(cat, golden, lpf):
 def test_fused_path_odd_shapes(cat, shape, name):
     """Odd / ragged shapes through the fused path (row-pass fallback widths,
     partial bands and column tiles, short images) against the oracle."""
-    rng = np.random.default_rng(hash((shape, name)) & 0xFFFF)
+    # seed from the parameters (crc32: str hashes are salted per process)
+    rng = np.random.default_rng(zlib.crc32(repr((shape, name)).encode()) & 0xFFFF)
     h, w = shape
     x = (0.05 * rng.standard_normal((h, w))).astype(np.float32)
     for _ in range(6):  # a few blobs so the threshold selects something
