@@ -712,7 +712,9 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
           gt &= v > u;
           lt &= v < u;
         }
-      if (gt || lt) {
+      // a maximum counts when L >= t, a minimum when -L >= t (|L| >= t alone
+      // would admit a maximum of a negative region)
+      if ((gt && v >= th) || (lt && -v >= th)) {
         int k = atomicAdd(&S.ccount, 1);
         if (k < kCandSmem) {
           S.cy[k] = (int)r;
@@ -813,7 +815,7 @@ __device__ void final_fullscan(const float *__restrict__ L, int64_t ldl, int64_t
               gt &= v > u;
               lt &= v < u;
             }
-          det = gt || lt;
+          det = (gt && v >= thr) || (lt && -v >= thr);
         }
       }
       unsigned bal = __ballot_sync(0xffffffffu, det);

@@ -423,7 +423,9 @@ __device__ __forceinline__ void fc_tile(
           gt &= v > u;
           lt &= v < u;
         }
-      if (gt || lt) {
+      // a maximum counts when L >= t, a minimum when -L >= t (|L| >= t alone
+      // would admit a maximum of a negative region)
+      if ((gt && v >= th) || (lt && -v >= th)) {
         int kk = atomicAdd(&S.ccount, 1);
         if (kk < kFcCand) {
           S.cy[kk] = (int)r;

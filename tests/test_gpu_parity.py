@@ -334,6 +334,23 @@ def test_fused_path_odd_shapes(cat, shape, name):
     _check_pipeline(x, cat[name], label=f"{name} {shape}")
 
 
+@pytest.mark.parametrize("seed", [38610, 43228, 55631, 62877])
+def test_negative_maximum_is_not_a_blob(cat, seed):
+    """A strict local MAXIMUM whose value is negative (a shallow spot inside a
+    dark region) has |L| >= t but is not a blob: the rule is L >= t for
+    maxima and -L >= t for minima.  These seeds (found by
+    tools/repro_odd.py over 65536 inputs) put one at column W-2 of a 1000x33
+    frame."""
+    h, w = 1000, 33
+    rng = np.random.default_rng(seed)
+    x = (0.05 * rng.standard_normal((h, w))).astype(np.float32)
+    for _ in range(6):
+        cy, cx = rng.integers(0, h), rng.integers(0, w)
+        yy, xx = np.ogrid[:h, :w]
+        x += np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / 18.0).astype(np.float32)
+    _check_pipeline(x, cat["rp4"], label=f"rp4 seed {seed}")
+
+
 def test_stream_sweep_matches_detect_sweep(cat):
     """The overlapped multi-scale frame stream gives each frame the results
     of a detect_sweep call, including sets larger than the per-frame
