@@ -16,6 +16,7 @@ Detections come back sorted by (y, x) (and scale first for the stack).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -117,7 +118,9 @@ def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out
     return det_yx, det_val, scal, n_host.value
 
 
-SWEEP_STREAMS = 3  # scales in flight in a sweep (measured on B200: 1 -> 0.617 ms, 3 -> 0.532 ms)
+# scales in flight in a sweep (measured on B200: 1 -> 0.617 ms, 3 -> 0.532 ms);
+# VMF_SWEEP_STREAMS overrides it for experiments
+SWEEP_STREAMS = int(os.environ.get("VMF_SWEEP_STREAMS", "3"))
 _side_streams: dict = {}
 
 
