@@ -399,6 +399,19 @@ def run_ours(args):
     e2e1_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
     barrier(ws)
     e2e_single = mpx * len(iir) * ws * args.steps / e2e1_s
+    # the link the end-to-end number rides on: raw pinned H2D copies of one
+    # frame (device-timed), and the Mpixel/s per scale they alone would allow
+    dbuf = torch.empty_like(x)
+    dbuf.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    ha, hb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ha.record(stream)
+    for _ in range(5):
+        dbuf.copy_(host, non_blocking=True)
+    hb.record(stream)
+    torch.cuda.synchronize()
+    h2d_gbs = 5 * host.numel() * 4 / (ha.elapsed_time(hb) / 1e3) / 1e9
+    del dbuf
 
     other = None
     if rank == 0 and ws == 1 and not args.no_extra:
@@ -439,7 +452,11 @@ def run_ours(args):
                     "d2h_bytes_per_step": int(d2h),
                     "api": "detect.stream_sweep over K pinned frames (uploads overlapped)",
                     "single_frame_value": round(e2e_single, 1),
-                    "single_frame_api": "detect.detect_sweep per frame (no overlap)"},
+                    "single_frame_api": "detect.detect_sweep per frame (no overlap)",
+                    "h2d_gbs": round(h2d_gbs, 1),
+                    "h2d_bound_value": round(h2d_gbs * 1e9 / frame.itemsize * len(iir) / 1e6, 1),
+                    "h2d_note": "raw pinned H2D copy rate of one frame on this box, and the "
+                                "Mpixel/s per scale that upload rate alone allows"},
             "gpu_launches": int(launches),
             "graph": "each timed step is one CUDA-graph replay of the 5-scale sweep "
                      f"({detect.SWEEP_STREAMS} scales in flight on concurrent streams); "
