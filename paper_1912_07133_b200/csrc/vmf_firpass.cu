@@ -37,7 +37,7 @@ constexpr int kFirTapsPad = kFirMaxFast + 15;  // reversed taps, zero-padded to 
 
 struct FirTapsP {
   double t[kFirTapsPad];  // t[i] = taps[n-1-i] (i < n), 0 beyond
-  int n, np, n4;          // taps; rounded up to a multiple of 8 (window sizes) and of 4 (loop)
+  int n, np;              // taps; rounded up to a multiple of 8 (window sizes)
 };
 
 static void fir_plan(FirTapsP *tp, const double *taps, int ntaps) {
@@ -45,7 +45,6 @@ static void fir_plan(FirTapsP *tp, const double *taps, int ntaps) {
   for (int i = 0; i < ntaps; ++i) tp->t[i] = taps[ntaps - 1 - i];
   tp->n = ntaps;
   tp->np = (ntaps + 7) / 8 * 8;
-  tp->n4 = (ntaps + 3) / 4 * 4;
 }
 
 // acc[j] += sum_i t[i] * w(base + j + i), w(q) read through `ld` (fp32 -> fp64)
@@ -54,8 +53,7 @@ __device__ __forceinline__ void fir8(const FirTapsP &tp, LD ld, double *acc) {
   double xw[16];
 #pragma unroll
   for (int j = 0; j < 8; ++j) xw[j] = ld(j);
-  int mb = 0;
-  for (; mb + 8 <= tp.n4; mb += 8) {
+  auto block8 = [&](int mb) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) xw[8 + j] = ld(mb + 8 + j);
 #pragma unroll
@@ -66,8 +64,19 @@ __device__ __forceinline__ void fir8(const FirTapsP &tp, LD ld, double *acc) {
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) xw[j] = xw[8 + j];
-  }
-  if (mb < tp.n4) {  // a last block of 4 taps (the padding to 8 would waste DFMAs)
+  };
+  int mb = 0;
+  for (; mb + 8 <= tp.n; mb += 8) block8(mb);
+  // the last n % 8 taps without padding DFMAs: 2k + 1 taps with k % 4 == 0
+  // (every Gaussian / SG kernel of the configs) leave exactly one, whose
+  // samples are already in the window; 2..4 use a half block; 5..7 one more
+  // full block over the zero-padded taps
+  const int rem = tp.n - mb;
+  if (rem == 1) {
+    const double tap = tp.t[mb];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = fma(tap, xw[j], acc[j]);
+  } else if (rem > 1 && rem <= 4) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) xw[8 + j] = ld(mb + 8 + j);
 #pragma unroll
@@ -76,6 +85,8 @@ __device__ __forceinline__ void fir8(const FirTapsP &tp, LD ld, double *acc) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = fma(tap, xw[j + mm], acc[j]);
     }
+  } else if (rem > 4) {
+    block8(mb);
   }
 }
 
@@ -103,18 +114,22 @@ __global__ void __launch_bounds__(kFrThreads) fir_rows_fast_kernel(const T *__re
   const int64_t s0 = n0 - k;
   const int nv = (nwin + 3) / 4;
   const bool vec = sizeof(T) == 4 && vec_in && (k & 3) == 0;
+  // units entirely inside the row: [vlo, vhi)
+  const int vlo = s0 >= 0 ? 0 : (int)((3 - s0) / 4);
+  const int vhi = (int)((w - s0) / 4 < nv ? (w - s0) / 4 : nv);
   float *fwin = fwin_raw;
   for (int64_t row = blockIdx.y; row < h; row += gridDim.y) {
     __syncthreads();
     const T *xr = x + row * ldx;
     if (vec) {  // 16-byte asynchronous copies; units crossing an edge are clamped per sample
       const float *xf = reinterpret_cast<const float *>(xr);
+      const float *src = xf + s0;  // unit v = samples s0 + 4v .. s0 + 4v + 3
       for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-        const int64_t g = s0 + 4 * v;
         const unsigned sa = (unsigned)__cvta_generic_to_shared(fwin_raw + 4 * v);
-        if (g >= 0 && g + 4 <= w) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(xf + g));
+        if (v >= vlo && v < vhi) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 4 * v));
         } else {
+          const int64_t g = s0 + 4 * v;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int64_t c = g + e < 0 ? 0 : (g + e >= w ? w - 1 : g + e);
