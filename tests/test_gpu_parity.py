@@ -293,6 +293,30 @@ def test_stream_detect_matches_per_frame(cat):
     _check_pipeline(frames[0], cat["rp6"], label="config4/stream")
 
 
+@pytest.mark.parametrize("ntaps", [1, 3, 5, 7, 9, 11, 13, 15, 19, 23, 29, 41, 63, 71, 101])
+def test_fir_every_tap_remainder(ntaps):
+    """The register-blocked FIR runs taps in blocks of 8 and the last n % 8
+    taps separately (1: from the samples already in the window; 2..4: a half
+    block; 5..7: a full block over zero-padded taps), with the row window
+    staged in 16-byte units only when k % 4 == 0: random symmetric kernels of
+    every remainder and both k parities, through the row / column leaves and
+    the fused FIR column pass, against the oracle."""
+    E, D = _E(), _D()
+    rng = np.random.default_rng(ntaps)
+    half = rng.uniform(0.1, 1.0, ntaps // 2 + 1)
+    taps = np.concatenate([half[:0:-1], half])
+    taps /= taps.sum()
+    f = F.FirKernel(tuple(taps.tolist()), "sym", 0)
+    x = rng.standard_normal((131, 1100)).astype(np.float32)
+    assert max_rel_err(E.conv_rows(x, f), O.conv_rows(x, f)) < PASS_TOL, ntaps
+    assert max_rel_err(E.conv_cols(x, f), O.conv_cols(x, f)) < PASS_TOL, ntaps
+    y = (0.05 * rng.standard_normal((301, 517))).astype(np.float32)
+    yy, xx = np.ogrid[:301, :517]
+    for cy, cx in ((40, 60), (150, 300), (280, 500)):
+        y += np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / 18.0).astype(np.float32)
+    _check_pipeline(y, f, label=f"fir {ntaps} taps")
+
+
 def test_fir_fused_long_taps(cat):
     """385-tap colored SG (config 5's FIR) on the fused FIR column pass."""
     x = synth.config5_frame(1024)
