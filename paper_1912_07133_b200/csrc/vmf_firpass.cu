@@ -391,7 +391,28 @@ __device__ __forceinline__ void fc_tile(
   // hold the replicated edge column.
   const double lsc = (double)lap_scale;
   float tmax = 0.0f;
-  if (j != 0 && j != SH::kCols - 1) {
+  // rows r0-1 .. r0+kOwn and their vertical neighbours all inside the image
+  // (every tile but the first and last row band): no per-row edge logic
+  const bool rows_in = rB0 >= 0 && rB0 + SH::kRB <= H;
+  if (j != 0 && j != SH::kCols - 1 && rows_in) {
+    const int64_t c = c0 - 2 + j;
+    const bool cin = c >= 0 && c < W;
+    const double *bcol = Bs + (8 * g) * SH::kCols + j;  // B(tile row 8g, column j)
+    float *lcol = Ls + (8 * g - 1) * SH::kStride + j + 2;
+    float m = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if ((q == 0 && g == 0) || (q == 7 && g == SH::kGroups - 1)) continue;  // tile rows 0, kRB-1
+      const double bc = acc[q];
+      const double bu = q > 0 ? acc[q - 1] : bcol[-SH::kCols];
+      const double bd = q < 7 ? acc[q + 1] : bcol[8 * SH::kCols];
+      const double bl = bcol[q * SH::kCols - 1], br = bcol[q * SH::kCols + 1];
+      const float v = (float)(lsc * fma(-4.0, bc, (bl + br) + (bu + bd)));
+      lcol[q * SH::kStride] = v;
+      m = fmaxf(m, fabsf(v));
+    }
+    if (cin) tmax = m;
+  } else if (j != 0 && j != SH::kCols - 1) {
     const int64_t c = c0 - 2 + j;
     const bool cin = c >= 0 && c < W;
 #pragma unroll
