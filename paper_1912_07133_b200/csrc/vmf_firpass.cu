@@ -473,17 +473,22 @@ __device__ __forceinline__ void fc_tile(
       }
     };
     if (vec_out && ncol == SH::kOut) {
-      if (lane < SH::kOut / 4) {
-        float *dst = Lout + r0 * ldl + c0 + 4 * lane;
-        for (int q = wid; q < nrow; q += SH::kThreads / 32) {
-          const float4 v = *reinterpret_cast<const float4 *>(Ls + (q + 1) * SH::kStride + 4 + 4 * lane);
+      // a row is kOut / 4 float4 (15 for the 64-column tile): with <= 16 a
+      // warp takes two rows per step (half-warps), else one
+      constexpr int kRpw = SH::kOut / 4 <= 16 ? 2 : 1;
+      const int u = kRpw == 2 ? (lane & 15) : lane;
+      if (u < SH::kOut / 4) {
+        float *dst = Lout + r0 * ldl + c0 + 4 * u;
+        for (int q = kRpw * wid + (kRpw == 2 ? lane >> 4 : 0); q < nrow;
+             q += kRpw * (SH::kThreads / 32)) {
+          const float4 v = *reinterpret_cast<const float4 *>(Ls + (q + 1) * SH::kStride + 4 + 4 * u);
           *reinterpret_cast<float4 *>(dst + q * ldl) = v;
           const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
           if (m4 >= th) {
-            if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
-            if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
-            if (fabsf(v.z) >= th) test(q, 4 * lane + 2, v.z);
-            if (fabsf(v.w) >= th) test(q, 4 * lane + 3, v.w);
+            if (fabsf(v.x) >= th) test(q, 4 * u, v.x);
+            if (fabsf(v.y) >= th) test(q, 4 * u + 1, v.y);
+            if (fabsf(v.z) >= th) test(q, 4 * u + 2, v.z);
+            if (fabsf(v.w) >= th) test(q, 4 * u + 3, v.w);
           }
         }
       }
