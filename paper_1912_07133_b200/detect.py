@@ -439,9 +439,13 @@ def stream_sweep(frames, stages, frac: float = 0.5, lap_scales=None, cap: int = 
         _sweep_launch(x, code, stg, frac, lap_scales, cap,
                       [(det_yx[i, j], det_val[i, j], scal[i, j]) for j in range(ns)])
         h_scal[i].copy_(scal[i], non_blocking=True)
-        for j in range(ns):  # contiguous on both sides: plain async copies
-            h_yx[i, j].copy_(det_yx[i, j, :dcap], non_blocking=True)
-            h_val[i, j].copy_(det_val[i, j, :dcap], non_blocking=True)
+        if os.environ.get("VMF_STREAM_PER_SCALE_D2H"):  # A/B: one copy per scale
+            for j in range(ns):
+                h_yx[i, j].copy_(det_yx[i, j, :dcap], non_blocking=True)
+                h_val[i, j].copy_(det_val[i, j, :dcap], non_blocking=True)
+        else:  # all scales in one strided copy each (fewer host-side calls per frame)
+            h_yx[i].copy_(det_yx[i, :, :dcap], non_blocking=True)
+            h_val[i].copy_(det_val[i, :, :dcap], non_blocking=True)
         if not f.is_cuda:
             up.release()
     torch.cuda.current_stream().synchronize()
