@@ -30,6 +30,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
@@ -57,7 +59,29 @@ def parse():
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the config 4 / 5 lines")
+    ap.add_argument("--plumbing-check", action="store_true",
+                    help="CPU/gloo check of the rank launch + max-over-ranks reduction only")
     return ap.parse_args()
+
+
+def self_launch(args) -> bool:
+    """`bench.py --gpus N` outside torchrun (no WORLD_SIZE): re-exec under
+    torch.distributed.run with N ranks on this node (127.0.0.1) and pass its
+    output through.  Returns True when this process was only the launcher."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd)
+    if r.returncode:
+        sys.exit(r.returncode)
+    return True
 
 
 def peaks():
@@ -130,10 +154,12 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # distributed plumbing (one process per GPU; weak scaling, no data collective)
 # ---------------------------------------------------------------------------
-def dist_init(backend):
+def dist_init(backend, expect=None):
     import torch.distributed as dist
 
     ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if expect is not None and ws != expect and not (ws == 1 and expect <= 1):
+        raise SystemExit(f"bench.py: --gpus {expect} but WORLD_SIZE={ws}")
     if ws > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group(backend)
@@ -163,21 +189,6 @@ def max_over_ranks(v, ws, device):
 # ---------------------------------------------------------------------------
 # CPU side: the oracle port (test infrastructure) as baseline / reference arm
 # ---------------------------------------------------------------------------
-def cpu_time_sweep(frame, stages, reps):
-    from oracle import oracle as O
-
-    threads = os.cpu_count() or 1
-    O.set_threads(threads)
-    O.pipeline(frame[:256, :256], stages[0])  # warm
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        for st in stages:
-            O.pipeline(frame, st, frac=0.5)
-        times.append(time.perf_counter() - t0)
-    return times, threads
-
-
 DFMA_PEAK_T = 16.44  # T fp64 FMA/s: profiles/r1_pipes.txt (tools/microbench/pipes.cu on this pool)
 
 
@@ -214,33 +225,118 @@ def cpu_stage_times(frame, stage, threads):
             "nms_ms": round(1e3 * (t3 - t2), 1), "threads": threads}
 
 
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+
+
+def ref_engine():
+    """The reference package itself (vmfilt, pip-installed into baseline/_ref
+    from /root/reference/pkg; numba JIT cache under /tmp), or None when it is
+    not importable on this box."""
+    if not os.path.isdir(os.path.join(REF_DIR, "vmfilt")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/vmfilt_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        from vmfilt import design, engine, polyz  # noqa: F401
+    except Exception:
+        return None
+    return engine, design, polyz
+
+
+def ref_stage(mods, st):
+    """Our catalog stage -> the reference's own coefficient carrier."""
+    engine, design, polyz = mods
+    if hasattr(st, "taps"):
+        return design.FirKernel(tuple(st.taps), st.parity, st.d)
+    return polyz.ThreePartIIR(tuple(st.b_plus), tuple(st.a_plus), st.b_zero, st.parity)
+
+
+def ref_scale(mods, frame, rst, lap):
+    """One scale through the reference's own numba path (SURVEY.md §8(d),
+    BASELINE.md §2): blur = apply_cols(apply_rows(x)) (engine.py:161-174),
+    L = conv_rows(B, bank[2]) + conv_cols(B, bank[2]) (engine.py:205-228),
+    stage 4 = the restated threshold + 3x3 NMS (no reference function)."""
+    from oracle import oracle as O
+
+    engine = mods[0]
+    t0 = time.perf_counter()
+    B = engine.apply_cols(engine.apply_rows(frame, rst), rst)
+    t1 = time.perf_counter()
+    L = engine.conv_rows(B, lap) + engine.conv_cols(B, lap)
+    t2 = time.perf_counter()
+    O.detect3x3(L, 0.5)
+    t3 = time.perf_counter()
+    return t3 - t0, {"blur_ms": round(1e3 * (t1 - t0), 1),
+                     "laplacian_ms": round(1e3 * (t2 - t1), 1),
+                     "nms_ms": round(1e3 * (t3 - t2), 1)}
+
+
+def workload_config(h, w, n_gpus):
+    """The `config` dict of both arms (identical, so the driver can match them)."""
+    return {"workload": f"config3 {h}x{w} fp32, repeated-pole IIR sweep sigma 2..32, "
+                        "blur+Laplacian+3x3 NMS per scale",
+            "frame": [h, w], "scales": len(IIR), "parallelism": f"replicas x{n_gpus}"}
+
+
+DTYPE = "fp32 I/O, f64 recursion state"
+
+
 def run_reference(args):
+    """The reference's own CPU implementation on this host's cores: the
+    reference package's numba kernels (kind "reference") when baseline/_ref
+    imports here, else the C restatement in oracle/ (kind "port").  One step
+    = one scale of the sweep (sigma cycling 2..32) on the full 4096^2 frame:
+    a bounded sample of the 5-scale workload, same metric (Mpixel/s per
+    scale)."""
     rank, local, ws = dist_init("gloo")
     if rank != 0:
         return
     from paper_1912_07133_b200 import filters, synth
 
-    frame = synth.config3_frame(args.size)
+    frame = synth.config3_frame(args.size).astype(np.float64)
     cat = filters.catalog()
     stages = [cat[n] for n in IIR]
     mpx = frame.size / 1e6
-    for _ in range(args.warmup):
-        cpu_time_sweep(frame, stages[:1], 1)
-    times, threads = cpu_time_sweep(frame, stages, args.steps)
-    t = sum(times)
-    value = mpx * len(stages) * args.steps / t
+    threads = os.cpu_count() or 1
+    mods = ref_engine()
+    if mods is not None:
+        engine, design, _ = mods
+        engine.set_threads(threads)
+        threads = engine.max_threads()
+        lap = design.fir_vm_bank(3)[2]  # design hoisted out of the timed region
+        rst = [ref_stage(mods, st) for st in stages]
+
+        def one(i):
+            return ref_scale(mods, frame, rst[i % len(rst)], lap)[0]
+        kind = "reference"
+        what = ("the reference package's numba path (baseline/_ref vmfilt: engine.apply_rows/"
+                "apply_cols + conv_rows/conv_cols Laplacian, engine.py:35-228) + the restated "
+                "3x3 NMS")
+    else:
+        from oracle import oracle as O
+
+        O.set_threads(threads)
+
+        def one(i):
+            t0 = time.perf_counter()
+            O.pipeline(frame, stages[i % len(stages)], frac=0.5)
+            return time.perf_counter() - t0
+        kind = "port"
+        what = "oracle/vmf_oracle.c restatement of engine.py:35-102 + stage 4"
+    for i in range(max(args.warmup, 1)):  # numba JIT + caches
+        one(i)
+    t = sum(one(i) for i in range(args.steps))
+    value = mpx * args.steps / t
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config3 {args.size}x{args.size} fp32, repeated-pole IIR "
-                               "sweep sigma 2..32, blur+Laplacian+3x3 NMS per scale",
-                   "frame": [args.size, args.size], "scales": len(stages)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"full {args.size}^2 frame x 5 IIR scales per step, "
-                                   f"{args.steps} steps (oracle/vmf_oracle.c restatement of "
-                                   "engine.py:35-102 + numpy-equivalent stage 4)"},
+        "config": workload_config(args.size, args.size, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"one scale per step (sigma cycling 2..32) on the full "
+                                   f"{args.size}^2 frame, {args.steps} steps: {what}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -252,7 +348,7 @@ def run_reference(args):
 def run_ours(args):
     import torch
 
-    rank, local, ws = dist_init("nccl")
+    rank, local, ws = dist_init("nccl", expect=args.gpus)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_1912_07133_b200 import _lib, detect, filters, synth
@@ -420,26 +516,28 @@ def run_ours(args):
     if rank == 0 and ws == 1 and not args.no_extra:
         other = other_configs(cat, flush, stream)
 
+    # parity of the benchmarked path at its own size: the sigma=4 scale of the
+    # timed graph's last replay (detections) and of one more launch of the
+    # same sweep with L written out, against the oracle on the same frame
+    parity = None
+    if rank == 0 and not args.no_cpu_baseline:
+        graph.replay()  # outs <- the timed graph's detections
+        torch.cuda.synchronize()
+        parity = bench_parity(frame, cat, x, iir, outs)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        times, threads = cpu_time_sweep(frame, [cat["rp4"]], 3)
-        cpu = {"value": round(mpx / statistics.median(times), 2), "unit": UNIT, "cores": threads,
-               "kind": "port",
-               "sample": f"full {h}x{w} frame, sigma=4 repeated-pole scale, median of 3 "
-                         "(oracle/vmf_oracle.c: fp64 restatement of engine.py:35-102 + stage 4)",
-               "stages": cpu_stage_times(frame, cat["rp4"], threads),
-               "stages_1_thread": cpu_stage_times(frame, cat["rp4"], 1)}
+        cpu = cpu_baseline_rows(frame, cat)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
             "data": "synthetic",
-            "config": {"workload": f"config3 {h}x{w} fp32, repeated-pole IIR sweep sigma "
-                                   "2..32, fused blur+Laplacian+3x3 NMS per scale",
-                       "frame": [h, w], "scales": len(iir), "parallelism": f"replicas x{ws}",
-                       "l2": "flushed (256 MiB memset) before every timed step"},
+            "config": workload_config(h, w, ws),
+            "l2": "flushed (256 MiB memset) before every timed step",
+            "parity": parity,
             "per_scale": per_scale,
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1),
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
@@ -476,6 +574,84 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def bench_parity(frame, cat, x, iir, outs):
+    """Per-scale parity of the benchmarked sweep at 4096^2 (sigma = 4):
+    L within 1e-4 max|L_ref|, blob set equal up to near-ties (tests/parity.py
+    rule), against the oracle restatement on the same frame."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_1912_07133_b200 import _lib, detect
+    from tests.parity import compare_blobs
+
+    i = IIR.index("rp4")
+    h, w = frame.shape
+    cnt = int(outs[i][2][0].item())
+    yx = outs[i][0][:cnt].cpu().numpy()
+    got = set(zip(yx[:, 0].tolist(), yx[:, 1].tolist()))
+    laps = [torch.empty((h, w), dtype=torch.float32, device=x.device) for _ in iir]
+    extra = [(torch.empty_like(o[0]), torch.empty_like(o[1]), torch.empty_like(o[2])) for o in outs]
+    detect._sweep_launch(x, _lib.VMF_F32, iir, 0.5, None, outs[0][1].numel(), extra, laps=laps)
+    torch.cuda.synchronize()
+    O.set_threads(os.cpu_count() or 1)
+    B, L, (ys, xs, vs, thr) = O.pipeline(frame, cat["rp4"], frac=0.5)
+    err = float(np.abs(laps[i].cpu().numpy().astype(np.float64) - L).max() / np.abs(L).max())
+    want = set(zip(ys.tolist(), xs.tolist()))
+    exempt, bad = compare_blobs(got, want, L, thr)
+    return {"scale": "rp4 (sigma 4)", "lap_rel_err": err, "tol": 1e-4,
+            "blob_set_equal": got == want, "blob_set_equal_up_to_near_ties": not bad,
+            "n_blobs_gpu": len(got), "n_blobs_ref": len(want), "n_exempt": exempt,
+            "oracle": "oracle/vmf_oracle.c (bit-identical to the reference's numba kernels on "
+                      "tests/golden)"}
+
+
+def cpu_baseline_rows(frame, cat):
+    """cpu_baseline: the reference's own numba path on one sigma=4 scale of
+    the same frame with all host threads (kind "reference"; falls back to
+    the C port when baseline/_ref does not import), plus its 1-thread time
+    and the C oracle port for comparison."""
+    from oracle import oracle as O
+
+    h, w = frame.shape
+    mpx = h * w / 1e6
+    threads = os.cpu_count() or 1
+    f64 = frame.astype(np.float64)
+    rows = {}
+    O.set_threads(threads)
+    O.pipeline(f64[:256, :256], cat["rp4"])
+    pt = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        O.pipeline(f64, cat["rp4"], frac=0.5)
+        pt.append(time.perf_counter() - t0)
+    port = {"value": round(mpx / statistics.median(pt), 2), "unit": UNIT, "cores": threads,
+            "kind": "port", "sample": "median of 3, full frame, sigma 4 (oracle/vmf_oracle.c)",
+            "stages": cpu_stage_times(f64, cat["rp4"], threads)}
+    mods = ref_engine()
+    if mods is None:
+        port["reference_unavailable"] = "baseline/_ref (vmfilt + numba) does not import here"
+        return port
+    engine, design, _ = mods
+    lap = design.fir_vm_bank(3)[2]
+    rst = ref_stage(mods, cat["rp4"])
+    for nthr in (threads, 1):
+        engine.set_threads(nthr)
+        ref_scale(mods, f64[:512, :512], rst, lap)  # JIT
+        ts, st = [], None
+        for _ in range(3 if nthr > 1 else 1):
+            t, st = ref_scale(mods, f64, rst, lap)
+            ts.append(t)
+        rows[nthr] = (statistics.median(ts), st, engine.max_threads())
+    t, st, used = rows[threads]
+    return {"value": round(mpx / t, 2), "unit": UNIT, "cores": used, "kind": "reference",
+            "sample": f"full {h}x{w} frame, sigma=4 repeated-pole scale, median of 3: the "
+                      "reference package's numba path (baseline/_ref vmfilt engine.apply_rows/"
+                      "apply_cols, conv_rows/conv_cols Laplacian) + the restated 3x3 NMS",
+            "stages": st,
+            "one_thread": {"value": round(mpx / rows[1][0], 2), "stages": rows[1][1]},
+            "port": port}
+
+
 def other_configs(cat, flush, stream):
     """Secondary lines (rank 0, N=1): config 4 (u16 stream, sustained end to
     end with double-buffered uploads) and config 5 (8192^2, Butterworth IIR vs
@@ -508,9 +684,9 @@ def other_configs(cat, flush, stream):
         del g
         return tot / reps
 
-    # config 4: 16 frames of 2048^2 u16 (the config's 64-frame stream, shortened
-    # to bound the bench run), rp6, per-frame threshold + NMS
-    frames = synth.config4_stream(n_frames=16)
+    # config 4: the config's 64-frame stream of 2048^2 u16, rp6, per-frame
+    # threshold + NMS
+    frames = synth.config4_stream(n_frames=64)
     n4, h4, w4 = frames.shape
     host = torch.from_numpy(frames).pin_memory()
     st4 = detect.make_stage(cat["rp6"])
@@ -538,7 +714,7 @@ def other_configs(cat, flush, stream):
         "e2e_note": "pinned host frames -> device (copy stream, 2 buffers) -> detections back",
         "device_mpx_s": round(mpx4 / (ms4 / 1e3), 1),
         "device_stream_mpx_s": round(mpx4 * n4 / (ms4s / 1e3), 1),
-        "device_stream_note": "16 device-resident frames, 3 in flight on concurrent streams "
+        "device_stream_note": f"{n4} device-resident frames, 3 in flight on concurrent streams "
                               "(stream_detect's device part), one CUDA graph",
         "detections_per_frame": int(statistics.median([r.count for r in res]))}
     del dframes, x4, lap4, outs4
@@ -595,9 +771,28 @@ def other_configs(cat, flush, stream):
     return out
 
 
+def plumbing_check(args):
+    """The multi-rank plumbing of run_ours without a GPU: gloo process group,
+    barrier, max over ranks of a rank-dependent value, world == --gpus."""
+    rank, local, ws = dist_init("gloo", expect=args.gpus)
+    barrier(ws)
+    v = max_over_ranks(float(rank + 1), ws, "cpu")
+    barrier(ws)
+    if rank == 0:
+        print(json.dumps({"n_gpus": ws, "max_over_ranks": v}), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if self_launch(args):
+        return
+    if args.plumbing_check:
+        plumbing_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

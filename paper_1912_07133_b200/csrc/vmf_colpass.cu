@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kCarryThreads) colcarry_kernel(
   const bool full = len == kBand && r0 + kBand <= p.H;
   const bool tma = use_tma && full && c0 + kCarryCols <= p.W;
   pdl_wait();  // T comes from the row pass
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 4) (&cs->absmax_bits)[threadIdx.x] = 0u;
+  if (blockIdx.x == 0 && blockIdx.y == 0) cand_reset(cs);
   if (tma) {
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
@@ -387,7 +387,6 @@ struct ColSmem {
   int cy[kCandSmem], cx[kCandSmem];
   float cv[kCandSmem];
   int ccount;
-  int coverflow;
   unsigned int cmax;  // max |L| of this CTA (float bits)
 };
 
@@ -452,7 +451,6 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
   }
   if (j == 0) {
     S.ccount = 0;
-    S.coverflow = 0;
     S.cmax = 0u;
   }
   pdl_wait();  // band histories and the CandState come from earlier kernels
@@ -714,16 +712,8 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         }
       // a maximum counts when L >= t, a minimum when -L >= t (|L| >= t alone
       // would admit a maximum of a negative region)
-      if ((gt && v >= th) || (lt && -v >= th)) {
-        int k = atomicAdd(&S.ccount, 1);
-        if (k < kCandSmem) {
-          S.cy[k] = (int)r;
-          S.cx[k] = (int)cc;
-          S.cv[k] = v;
-        } else {
-          S.coverflow = 1;
-        }
-      }
+      if ((gt && v >= th) || (lt && -v >= th))
+        cand_push(&S.ccount, S.cy, S.cx, S.cv, kCandSmem, st, gy, gx, gv, gcap, (int)r, (int)cc, v);
     };
     if (vec_out && ncol == kColOut) {  // 31 float4 per row, one row per warp
       const bool act = lane < kColOut / 4;
@@ -765,7 +755,6 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     unsigned old = atomicMax(&st->absmax_bits, S.cmax);
     float m = fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
     thr_end = p.frac * m;
-    if (S.coverflow) st->overflow = 1;
   }
   __syncthreads();
   const int n = S.ccount < kCandSmem ? S.ccount : kCandSmem;
@@ -843,72 +832,22 @@ __device__ void final_fullscan(const float *__restrict__ L, int64_t ldl, int64_t
   if (threadIdx.x == 0) *n_det = base;
 }
 
-__global__ void __launch_bounds__(kFinThreads) colfinal_kernel(
-    CandState *__restrict__ st, const int *__restrict__ gy, const int *__restrict__ gx,
-    const float *__restrict__ gv, int gcap, const float *__restrict__ L, int64_t ldl, int64_t H,
-    int64_t W, float frac, int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det,
-    float *thr_out, int force_full) {
-  extern __shared__ __align__(16) unsigned char fsm[];
-  unsigned long long *key = reinterpret_cast<unsigned long long *>(fsm);
-  float *val = reinterpret_cast<float *>(fsm + kSortCap * sizeof(unsigned long long));
-  __shared__ int m;
-  // one CTA: let the next kernel (the next scale's row pass, which waits for
-  // this grid before it overwrites anything this kernel reads) start now
-  pdl_trigger();
-  pdl_wait();
-  const CandState cs = *st;
-  const float thr = frac * __uint_as_float(cs.absmax_bits);
-  if (threadIdx.x == 0) {
-    m = 0;
-    if (thr_out) *thr_out = thr;
-  }
-  __syncthreads();
-  const int n = cs.count < gcap ? cs.count : gcap;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) {
-    const float v = gv[q];
-    const int yy = gy[q], xx = gx[q];  // loaded together: one round trip
-    if (!(fabsf(v) >= thr)) continue;
-    int k = atomicAdd(&m, 1);
-    if (k < kSortCap) {
-      key[k] = (unsigned long long)yy * (unsigned long long)W + (unsigned long long)xx;
-      val[k] = v;
-    }
-  }
-  __syncthreads();
-  if (force_full || cs.overflow || m > kSortCap) {  // buffer overflow: exact, slow path
-    final_fullscan(L, ldl, H, W, thr, det_yx, det_val, cap, n_det);
-    return;
-  }
-  if (m <= kFinThreads) {
-    // rank sort: keys are distinct (y, x) positions; broadcast smem reads
-    if (threadIdx.x < m) {
-      const unsigned long long mine = key[threadIdx.x];
-      int rank = 0;
-      for (int q = 0; q < m; ++q) rank += key[q] < mine;
-      if (rank < cap) {
-        det_yx[2 * rank] = (int32_t)(mine / (unsigned long long)W);
-        det_yx[2 * rank + 1] = (int32_t)(mine % (unsigned long long)W);
-        det_val[rank] = val[threadIdx.x];
-      }
-    }
-    if (threadIdx.x == 0) *n_det = m;
-    return;
-  }
-  int np = 1;
-  while (np < m) np <<= 1;
-  for (int q = m + threadIdx.x; q < np; q += blockDim.x) key[q] = ~0ull;
+// In-place ascending bitonic sort of (key, val) pairs in shared memory; n keys
+// padded with ~0 up to a power of two np (every thread of the CTA calls it).
+__device__ void smem_bitonic(unsigned long long *key, float *val, int n, int np) {
+  for (int q = n + threadIdx.x; q < np; q += blockDim.x) key[q] = ~0ull;
   __syncthreads();
   for (int kk = 2; kk <= np; kk <<= 1)
     for (int jj = kk >> 1; jj > 0; jj >>= 1) {
       for (int i = threadIdx.x; i < np; i += blockDim.x) {
-        int ix = i ^ jj;
+        const int ix = i ^ jj;
         if (ix > i) {
-          bool up = (i & kk) == 0;
-          unsigned long long a = key[i], c = key[ix];
+          const bool up = (i & kk) == 0;
+          const unsigned long long a = key[i], c = key[ix];
           if ((a > c) == up) {
             key[i] = c;
             key[ix] = a;
-            float t = val[i];
+            const float t = val[i];
             val[i] = val[ix];
             val[ix] = t;
           }
@@ -916,12 +855,168 @@ __global__ void __launch_bounds__(kFinThreads) colfinal_kernel(
       }
       __syncthreads();
     }
-  for (int q = threadIdx.x; q < m && q < cap; q += blockDim.x) {
-    det_yx[2 * q] = (int32_t)(key[q] / (unsigned long long)W);
-    det_yx[2 * q + 1] = (int32_t)(key[q] % (unsigned long long)W);
-    det_val[q] = val[q];
+}
+
+__device__ __forceinline__ void write_dets(const unsigned long long *key, const float *val, int n,
+                                           int64_t base, int64_t W, int32_t *det_yx,
+                                           float *det_val, int64_t cap) {
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    const int64_t o = base + q;
+    if (o < cap) {
+      det_yx[2 * o] = (int32_t)(key[q] / (unsigned long long)W);
+      det_yx[2 * o + 1] = (int32_t)(key[q] % (unsigned long long)W);
+      det_val[o] = val[q];
+    }
   }
-  if (threadIdx.x == 0) *n_det = m;
+}
+
+constexpr int kBigCap = 6144;  // keys per CTA of the large-list path (72 KB)
+constexpr unsigned long long kLookAgg = 1ull << 62, kLookPre = 2ull << 62;
+constexpr unsigned long long kLookMask = (1ull << 62) - 1;
+
+// Final threshold + (y, x) order.  Small lists (<= kSortCap candidates, the
+// usual case) are sorted by CTA 0 alone; the other CTAs return at once.
+// Larger lists use all kFinCtas CTAs: CTA b owns the rows [b H / G, (b+1) H / G),
+// collects its survivors (the list is read from L2 by every CTA), learns how
+// many the earlier row ranges hold by a decoupled look-back over the
+// CandState's look[] words, and writes its sorted survivors at that offset --
+// so the output never depends on how the candidates were appended, and the
+// cost grows with the list instead of falling off a one-CTA cliff.  Only an
+// overflow of the global list itself takes the ordered full-frame scan.
+__global__ void __launch_bounds__(kFinThreads) colfinal_kernel(
+    CandState *__restrict__ st, const int *__restrict__ gy, const int *__restrict__ gx,
+    const float *__restrict__ gv, int gcap, const float *__restrict__ L, int64_t ldl, int64_t H,
+    int64_t W, float frac, int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det,
+    float *thr_out, int force_full) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  unsigned long long *key = reinterpret_cast<unsigned long long *>(fsm);
+  __shared__ int m;
+  __shared__ long long prefix;
+  // let the next kernel (the next scale's row pass, which waits for this grid
+  // before it overwrites anything this kernel reads) start now
+  pdl_trigger();
+  pdl_wait();
+  const int count = st->count, overflow = st->overflow;
+  const float thr = frac * __uint_as_float(st->absmax_bits);
+  const int n = count < gcap ? count : gcap;
+  const bool big = n > kSortCap;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && thr_out) *thr_out = thr;
+  if (force_full || overflow) {  // global list overflow: exact, slow path
+    if (blockIdx.x == 0) final_fullscan(L, ldl, H, W, thr, det_yx, det_val, cap, n_det);
+    return;
+  }
+  if (!big && blockIdx.x != 0) return;
+  float *val = reinterpret_cast<float *>(fsm + (big ? kBigCap : kSortCap) * sizeof(unsigned long long));
+  if (threadIdx.x == 0) m = 0;
+  __syncthreads();
+  if (!big) {
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      const float v = gv[q];
+      const int yy = gy[q], xx = gx[q];  // loaded together: one round trip
+      if (!(fabsf(v) >= thr)) continue;
+      const int k = atomicAdd(&m, 1);
+      key[k] = (unsigned long long)yy * (unsigned long long)W + (unsigned long long)xx;
+      val[k] = v;
+    }
+    __syncthreads();
+    const int mm = m;
+    if (mm <= kFinThreads) {
+      // rank sort: keys are distinct (y, x) positions; broadcast smem reads
+      if (threadIdx.x < mm) {
+        const unsigned long long mine = key[threadIdx.x];
+        int rank = 0;
+        for (int q = 0; q < mm; ++q) rank += key[q] < mine;
+        if (rank < cap) {
+          det_yx[2 * rank] = (int32_t)(mine / (unsigned long long)W);
+          det_yx[2 * rank + 1] = (int32_t)(mine % (unsigned long long)W);
+          det_val[rank] = val[threadIdx.x];
+        }
+      }
+    } else {
+      int np = 1;
+      while (np < mm) np <<= 1;
+      smem_bitonic(key, val, mm, np);
+      write_dets(key, val, mm, 0, W, det_yx, det_val, cap);
+    }
+    if (threadIdx.x == 0) *n_det = mm;
+    return;
+  }
+  // ---- large list: row ranges over kFinCtas CTAs ---------------------------
+  const int G = gridDim.x, b = blockIdx.x;
+  const int64_t ylo = H * b / G, yhi = H * (b + 1) / G;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    const int yy = gy[q];
+    if (yy < ylo || yy >= yhi) continue;
+    const float v = gv[q];
+    if (!(fabsf(v) >= thr)) continue;
+    const int k = atomicAdd(&m, 1);
+    if (k < kBigCap) {
+      key[k] = (unsigned long long)yy * (unsigned long long)W + (unsigned long long)gx[q];
+      val[k] = v;
+    }
+  }
+  __syncthreads();
+  const int T = m;
+  if (threadIdx.x == 0) {
+    volatile unsigned long long *look = st->look;
+    if (b == 0) {
+      prefix = 0;
+    } else {
+      look[b] = kLookAgg | (unsigned long long)T;  // own count, before the look-back
+      long long acc = 0;
+      for (int j = b - 1; j >= 0;) {
+        const unsigned long long f = look[j];
+        if (f & kLookPre) {
+          acc += (long long)(f & kLookMask);
+          break;
+        }
+        if (f & kLookAgg) {
+          acc += (long long)(f & kLookMask);
+          --j;
+        }
+        // else: CTA j has not counted yet (spin; it was dispatched earlier)
+      }
+      prefix = acc;
+    }
+    if (b < G - 1)
+      look[b] = kLookPre | (unsigned long long)(prefix + T);
+    else
+      *n_det = prefix + T;
+  }
+  __syncthreads();
+  const long long base = prefix;
+  if (T <= kBigCap) {
+    int np = 1;
+    while (np < T) np <<= 1;
+    smem_bitonic(key, val, T, np);
+    write_dets(key, val, T, base, W, det_yx, det_val, cap);
+    return;
+  }
+  // more survivors in this row range than shared memory holds: one row at a
+  // time (a row has at most W / 2 strict extrema <= kBigCap for W <= 12288)
+  long long off = base;
+  for (int64_t r = ylo; r < yhi; ++r) {
+    __syncthreads();
+    if (threadIdx.x == 0) m = 0;
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      if (gy[q] != r) continue;
+      const float v = gv[q];
+      if (!(fabsf(v) >= thr)) continue;
+      const int k = atomicAdd(&m, 1);
+      if (k < kBigCap) {
+        key[k] = (unsigned long long)r * (unsigned long long)W + (unsigned long long)gx[q];
+        val[k] = v;
+      }
+    }
+    __syncthreads();
+    const int mr = m < kBigCap ? m : kBigCap;
+    int np = 1;
+    while (np < mr) np <<= 1;
+    smem_bitonic(key, val, mr, np);
+    write_dets(key, val, mr, off, W, det_yx, det_val, cap);
+    off += mr;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1005,13 +1100,12 @@ int colfinal_launch(CandState *cs, const int *gy, const int *gx, const float *gv
                     int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
                     float *thr_dev, cudaStream_t st) {
   Launch g(K_FINALIZE, st);
-  const int fsmem = kSortCap * (int)(sizeof(unsigned long long) + sizeof(float));
-  static bool fattr = false;
-  if (!fattr) {
+  const int fsmem = kBigCap * (int)(sizeof(unsigned long long) + sizeof(float));
+  static PerDevice fattr;
+  if (fattr.first()) {
     cudaFuncSetAttribute(colfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
-    fattr = true;
   }
-  launch_pdl(colfinal_kernel, dim3(1), dim3(kFinThreads), fsmem, st, cs, gy, gx, gv, (int)gcap, L,
+  launch_pdl(colfinal_kernel, dim3(kFinCtas), dim3(kFinThreads), fsmem, st, cs, gy, gx, gv, (int)gcap, L,
              ldl, H, W, frac, det_yx, det_val, cap, n_det_dev, thr_dev,
              getenv("VMF_FORCE_FULLSCAN") ? 1 : 0);
   return cuda_status("finaliser");
@@ -1043,10 +1137,9 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
                !getenv("VMF_NO_TMA");
     cudaGetLastError();
     const int csm = kBand * kCarryCols * (int)sizeof(float) + 128;
-    static bool cattr = false;
-    if (!cattr) {
+    static PerDevice cattr;
+    if (cattr.first()) {
       cudaFuncSetAttribute(colcarry_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
-      cattr = true;
     }
     launch_pdl(colcarry_kernel<K>, grid, dim3(kCarryThreads), csm, st, T, ldt, p, Z, cmap, ctma,
                cs);
@@ -1054,11 +1147,10 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
   {
     Launch g(K_COL_SCAN, st);
     const int ssm = (int)((size_t)p.NB * (2 * K * kScanCols + 2) * sizeof(double));
-    static bool sattr = false;
-    if (!sattr) {
+    static PerDevice sattr;
+    if (sattr.first()) {
       cudaFuncSetAttribute(colscan_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
-      sattr = true;
     }
     launch_pdl(colscan_kernel<K>, dim3((unsigned)cdiv(p.W, kScanCols), 2), dim3(32 * kScanCols),
                ssm, st, T, ldt, p, Z);
@@ -1066,8 +1158,8 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
 
   {
     Launch g(K_IIR_COLS_FUSED, st);
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (attr.first()) {
       cudaFuncSetAttribute(colapply_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(ColSmem<K>) + 128);
       cudaFuncSetAttribute(colapply_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1076,7 +1168,6 @@ static int launch_colpass(const float *T, int64_t ldt, float *L, int64_t ldl, co
                            (int)sizeof(ColSmem<K>) + 128);
       cudaFuncSetAttribute(colapply_kernel<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sizeof(ColSmem<K>) + 128);
-      attr = true;
     }
     dim3 grid((unsigned)cdiv(p.W, kColOut), (unsigned)p.NB);
     CUtensorMap tmap;

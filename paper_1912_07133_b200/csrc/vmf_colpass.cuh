@@ -32,13 +32,48 @@ struct ColParams {
   DfiCoef bwd;  // b_minus = sign * b, a: the backward run yields sign * y- directly
 };
 
-// Device-side bookkeeping shared by the fused column pass and the finaliser.
+constexpr int kFinCtas = 128;       // CTAs of the finaliser's large-list path
+
+// Device-side bookkeeping shared by the fused column pass and the finaliser
+// (zeroed by the first kernel of every pass).
 struct CandState {
   unsigned int absmax_bits;  // max |L| (float bits)
   int count;                 // candidates appended
-  int overflow;              // a CTA buffer or the global list overflowed
+  int overflow;              // the global candidate list overflowed
   int pad;
+  // decoupled look-back of the finaliser's large-list path: per CTA
+  // (status << 62) | count, status 1 = own count, 2 = inclusive prefix
+  unsigned long long look[kFinCtas];
 };
+
+// A candidate goes to the CTA's shared buffer, or straight to the global list
+// once that is full (a superset either way: the finaliser applies the final
+// threshold), so a busy tile never forces the ordered full-frame fallback.
+__device__ __forceinline__ void cand_push(int *ccount, int *cy, int *cx, float *cv, int smem_cap,
+                                          CandState *st, int *gy, int *gx, float *gv, int gcap,
+                                          int y, int x, float v) {
+  const int k = atomicAdd(ccount, 1);
+  if (k < smem_cap) {
+    cy[k] = y;
+    cx[k] = x;
+    cv[k] = v;
+    return;
+  }
+  const int g = atomicAdd(&st->count, 1);
+  if (g < gcap) {
+    gy[g] = y;
+    gx[g] = x;
+    gv[g] = v;
+  } else {
+    st->overflow = 1;
+  }
+}
+
+// Zero the CandState (one CTA's threads; after the pass's pdl_wait).
+__device__ __forceinline__ void cand_reset(CandState *st) {
+  unsigned *w = reinterpret_cast<unsigned *>(st);
+  for (int i = threadIdx.x; i < (int)(sizeof(CandState) / 4); i += blockDim.x) w[i] = 0u;
+}
 
 bool colpass_supported(int64_t h, int64_t w, int k);
 // candidate list capacity of the fused column passes (IIR and FIR)

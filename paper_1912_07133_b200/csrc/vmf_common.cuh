@@ -22,6 +22,26 @@ void set_error(const char *fmt, ...);
 int fail(int code, const char *fmt, ...);
 int cuda_status(const char *what);  // VMF_OK or VMF_ECUDA after a launch
 
+// Per-device one-time host setup.  Kernel attributes (the dynamic shared
+// memory opt-in) and occupancy-derived sizes belong to a device, so a
+// process driving several GPUs must set them once per device, not once.
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+struct PerDevice {
+  uint64_t done = 0;  // bit d: device d set up
+  bool first() {
+    const int d = current_device();
+    if (d < 0 || d >= 64) return true;  // (not cached)
+    const uint64_t b = 1ull << d;
+    if (done & b) return false;
+    done |= b;
+    return true;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // device: element loads (fp32 / u16 -> fp64) through the read-only path
 // ---------------------------------------------------------------------------

@@ -227,7 +227,7 @@ constexpr int kFcCand = 256;
 struct FcSmall {
   int cy[kFcCand], cx[kFcCand];
   float cv[kFcCand];
-  int ccount, coverflow;
+  int ccount;
   unsigned cmax;
   float thr_end;
 };
@@ -461,16 +461,8 @@ __device__ __forceinline__ void fc_tile(
         }
       // a maximum counts when L >= t, a minimum when -L >= t (|L| >= t alone
       // would admit a maximum of a negative region)
-      if ((gt && v >= th) || (lt && -v >= th)) {
-        int kk = atomicAdd(&S.ccount, 1);
-        if (kk < kFcCand) {
-          S.cy[kk] = (int)r;
-          S.cx[kk] = (int)cc;
-          S.cv[kk] = v;
-        } else {
-          S.coverflow = 1;
-        }
-      }
+      if ((gt && v >= th) || (lt && -v >= th))
+        cand_push(&S.ccount, S.cy, S.cx, S.cv, kFcCand, st, gy, gx, gv, gcap, (int)r, (int)cc, v);
     };
     if (vec_out && ncol == SH::kOut) {
       // a row is kOut / 4 float4 (15 for the 64-column tile): with <= 16 a
@@ -505,7 +497,6 @@ __device__ __forceinline__ void fc_tile(
   // ---- flush the candidates that survive the best threshold known now -----
   if (tid == 0) {
     S.thr_end = frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
-    if (S.coverflow) st->overflow = 1;
   }
   __syncthreads();
   const int n = S.ccount < kFcCand ? S.ccount : kFcCand;
@@ -550,7 +541,6 @@ __global__ void __launch_bounds__(SH::kThreads, 1024 / SH::kThreads) firapply_ke
   const int64_t r0 = (int64_t)blockIdx.y * SH::kOwn;
   if (tid == 0) {
     S.ccount = 0;
-    S.coverflow = 0;
     S.cmax = 0u;
   }
   pdl_wait();

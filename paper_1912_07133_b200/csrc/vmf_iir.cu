@@ -332,11 +332,10 @@ static int launch_iir(const T *x, int64_t ldx, float *y, int64_t ldy, const IirP
     iir_scan_kernel<K, O, T><<<(int)cdiv(p.M, 128), 128, 0, st>>>(x, ldx, p, carry);
   }
   size_t smem = (size_t)(p.L + K) * kIirApplyThreads * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static PerDevice attr_set;
+  if (attr_set.first()) {
     cudaFuncSetAttribute(iir_apply_kernel<K, O, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    attr_set = true;
   }
   {
     Launch g(K_IIR_APPLY, st);

@@ -24,6 +24,7 @@
 //                recursion writes out(n) in place of x(n).
 //   e. store   : coalesced copy of the R rows to the output.
 // fp64 state and accumulation throughout; fp32 in and out.
+#include <map>
 #include <cstdlib>
 #include <cstring>
 
@@ -611,11 +612,10 @@ template <int K, typename T>
 static int launch_rowpass(const T *x, int64_t ldx, float *y, int64_t ldy, RowParams p,
                           cudaStream_t st) {
   size_t smem = rowpass_smem(p, K);
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(rowpass_kernel<K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    attr = true;
   }
   p.vec4 = (sizeof(T) == 4) && (p.W % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
            ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
@@ -635,14 +635,17 @@ static int launch_rowpass_tma(const CUtensorMap &xm, const CUtensorMap &ym, RowP
                               cudaStream_t st) {
   const size_t smem = 1024 + NBUF * (size_t)NR * p.C * kChunk * sizeof(float) +
                       2 * (size_t)NR * p.C * K * sizeof(double);
-  static int slots = 0;  // resident CTAs over the device
+  // resident CTAs over the device: per device and per shared-memory size
+  // (the width sets the CTA's footprint)
+  static std::map<std::pair<int, size_t>, int> slot_cache;
+  const int dev_now = current_device();
+  int &slots = slot_cache[std::make_pair(dev_now, smem)];
   if (!slots) {
     cudaFuncSetAttribute(rowpass_tma_kernel<K, NR, NBUF>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    int occ = 0, dev = 0, nsm = 148;
+    int occ = 0, dev = dev_now, nsm = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_tma_kernel<K, NR, NBUF>,
                                                   kRowThreads, smem);
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
     slots = (occ > 0 ? occ : 1) * nsm;

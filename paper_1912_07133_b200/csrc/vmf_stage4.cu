@@ -279,10 +279,11 @@ __global__ void absmax_kernel(const float *__restrict__ l, int64_t ld, int64_t p
 // host
 // ---------------------------------------------------------------------------
 static int sm_count() {
-  static int n = 0;
+  static int by_dev[64];
+  const int dev = current_device();
+  int tmp = 0;
+  int &n = dev >= 0 && dev < 64 ? by_dev[dev] : tmp;
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
   }

@@ -57,15 +57,18 @@ def exchange_halos(stack, has_lo: bool, has_hi: bool, rank: int, group=None) -> 
     neighbours' edge planes into the halo slots (batched P2P)."""
     import torch.distributed as dist
 
+    def peer(r):  # P2POp takes a GLOBAL rank; `rank` is the rank within `group`
+        return r if group is None else dist.get_global_rank(group, r)
+
     n = stack.shape[0]
     first, last = (1 if has_lo else 0), n - (2 if has_hi else 1)
     ops = []
     if has_lo:
-        ops.append(dist.P2POp(dist.isend, stack[first].contiguous(), rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, stack[0], rank - 1, group))
+        ops.append(dist.P2POp(dist.isend, stack[first].contiguous(), peer(rank - 1), group))
+        ops.append(dist.P2POp(dist.irecv, stack[0], peer(rank - 1), group))
     if has_hi:
-        ops.append(dist.P2POp(dist.isend, stack[last].contiguous(), rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, stack[n - 1], rank + 1, group))
+        ops.append(dist.P2POp(dist.isend, stack[last].contiguous(), peer(rank + 1), group))
+        ops.append(dist.P2POp(dist.irecv, stack[n - 1], peer(rank + 1), group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
@@ -132,8 +135,11 @@ def scale_space_detect(img, stages, sigmas, frac: float = 0.5, cap: int = 1 << 1
     else:
         mx = torch.zeros(1, dtype=torch.float32, device=dev)
     if world > 1:
-        exchange_halos(stack, has_lo, has_hi, rank, group)
+        # every rank of the group takes part in the all-reduce first, so the
+        # batched P2P below is never the group's first collective (NCCL needs
+        # all ranks in that one; ranks without scales send nothing)
         global_max(mx, group)
+        exchange_halos(stack, has_lo, has_hi, rank, group)
     if not n_own:
         return Detections(np.empty(0, np.int32), np.empty(0, np.int32),
                           np.empty(0, np.float32), float(frac * mx.item()), 0, False,
@@ -141,17 +147,27 @@ def scale_space_detect(img, stages, sigmas, frac: float = 0.5, cap: int = 1 << 1
     L = _lib.lib()
     nsl = stack.shape[0]
     ws = _workspace(L.vmf_detect3x3x3_workspace_bytes(nsl, h, w))
-    det = torch.empty((max(int(cap), 1), 3), dtype=torch.int32, device=dev)
-    val = torch.empty((max(int(cap), 1),), dtype=torch.float32, device=dev)
-    scal = torch.zeros(2, dtype=torch.int64, device=dev)
-    n_host = C.c_int64(0)
-    _lib.check(L.vmf_detect3x3x3_absmax(
-        _ptr(stack), nsl, h, w, w, h * w, float(frac), _ptr(mx), _ptr(det), _ptr(val), int(cap),
-        _ptr(scal), scal.data_ptr() + 8, C.byref(n_host), _ptr(ws), ws.numel(), _stream()))
-    n = n_host.value
+    cap = max(int(cap), 1)
+    # the slab's list also holds the halo planes' detections (sorted first for
+    # the lower halo), so its capacity covers them; a slab list that still
+    # overflows is redone at its exact size, so the own-plane count is exact
+    slab_cap = cap * (1 + int(has_lo) + int(has_hi))
+    while True:
+        det = torch.empty((slab_cap, 3), dtype=torch.int32, device=dev)
+        val = torch.empty((slab_cap,), dtype=torch.float32, device=dev)
+        scal = torch.zeros(2, dtype=torch.int64, device=dev)
+        n_host = C.c_int64(0)
+        _lib.check(L.vmf_detect3x3x3_absmax(
+            _ptr(stack), nsl, h, w, w, h * w, float(frac), _ptr(mx), _ptr(det), _ptr(val),
+            slab_cap, _ptr(scal), scal.data_ptr() + 8, C.byref(n_host), _ptr(ws), ws.numel(),
+            _stream()))
+        n = n_host.value
+        if n <= slab_cap:
+            break
+        slab_cap = n
     thr = float(scal[1:2].view(torch.float32)[0].item())
-    m = min(n, int(cap))
-    d, v = det[:m].cpu().numpy(), val[:m].cpu().numpy()
+    d, v = det[:n].cpu().numpy(), val[:n].cpu().numpy()
     keep, s_glob = own_detections(d[:, 0], lo, has_lo, n_own)
-    return Detections(d[keep, 1], d[keep, 2], v[keep], thr, int(keep.sum()), n > int(cap),
-                      s=s_glob.astype(np.int32))
+    n_mine = int(keep.sum())
+    ys, xs, vs, ss = d[keep, 1][:cap], d[keep, 2][:cap], v[keep][:cap], s_glob[:cap]
+    return Detections(ys, xs, vs, thr, n_mine, n_mine > cap, s=ss.astype(np.int32))

@@ -1,0 +1,138 @@
+"""Parity at the BASELINE.json configs' own sizes, on the exact paths the
+bench times (SURVEY.md §8(d) per-config pipelines):
+
+* config 3: one 4096^2 frame, the IIR (rp2..rp32) and FIR (g2_k8..g32_k128)
+  scale sweeps through detect._sweep_launch with SWEEP_STREAMS scales in
+  flight (bench.py's step) and detect.detect_sweep (the public API), plus the
+  3x3x3 scale-space detector on the sigma^2-normalised stack;
+* config 4: the 64-frame 2048^2 u16 stream through stream_detect, a seeded
+  sample of 8 frames against the oracle (all 64 against per-frame calls);
+* config 5: one 8192^2 frame, Butterworth sigma 48 and the 385-tap SG.
+
+Each scale's L is within 1e-4 of max|L_ref| (north_star) and the blob sets
+agree except near-ties (tests/parity.py)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1912_07133_b200 import synth
+from tests.parity import TOL_REL, compare_blobs, max_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    O.set_threads(O.max_threads())
+
+
+@pytest.fixture(scope="module")
+def frame3():
+    return synth.config3_frame(4096)
+
+
+def _oracle_scale(x, stage, frac=0.5):
+    B, L, (ys, xs, vs, thr) = O.pipeline(x, stage, frac=frac)
+    return L, set(zip(ys.tolist(), xs.tolist())), thr
+
+
+@pytest.mark.parametrize("family", ["iir", "fir"])
+def test_config3_sweep_full_size(cat, frame3, family):
+    """The benchmarked step (5 scales, 3 in flight, one 4096^2 frame) and the
+    public detect_sweep, per scale against the oracle."""
+    from paper_1912_07133_b200 import _lib, detect
+
+    spec = synth.CONFIG_STAGES[3]
+    names = spec[family]
+    x = torch.from_numpy(frame3).cuda()
+    h, w = x.shape
+    stg = [detect.make_stage(cat[n]) for n in names]
+    cap = 1 << 18
+    outs = [(torch.empty((cap, 2), dtype=torch.int32, device=x.device),
+             torch.empty(cap, dtype=torch.float32, device=x.device),
+             torch.empty(2, dtype=torch.int64, device=x.device)) for _ in names]
+    laps = [torch.empty((h, w), dtype=torch.float32, device=x.device) for _ in names]
+    detect._sweep_launch(x, _lib.VMF_F32, stg, 0.5, None, cap, outs, laps=laps)
+    torch.cuda.synchronize()
+    api = detect.detect_sweep(frame3, [cat[n] for n in names], frac=0.5)
+    for i, n in enumerate(names):
+        L, want, thr = _oracle_scale(frame3, cat[n])
+        e = max_rel_err(laps[i].cpu().numpy(), L)
+        assert e < TOL_REL, (n, e)
+        cnt = int(outs[i][2][0].item())
+        yx = outs[i][0][:cnt].cpu().numpy()
+        got = set(zip(yx[:, 0].tolist(), yx[:, 1].tolist()))
+        exempt, bad = compare_blobs(got, want, L, thr)
+        assert not bad, (n, bad[:10])
+        exempt, bad = compare_blobs(api[i].as_set(), want, L, thr)
+        assert not bad, (n, "detect_sweep", bad[:10])
+        assert not api[i].overflow
+
+
+@pytest.mark.parametrize("family", ["iir", "fir"])
+def test_config3_scale_space_full_size(cat, frame3, family):
+    from paper_1912_07133_b200 import detect
+
+    spec = synth.CONFIG_STAGES[3]
+    stages = [cat[n] for n in spec[family]]
+    sig = spec["sigmas"]
+    dets, stack = detect.scale_space_detect(frame3, stages, sig, frac=0.5, return_stack=True)
+    N = np.stack([O.laplacian(O.blur(frame3, s)) * (g * g) for s, g in zip(stages, sig)])
+    for i in range(len(sig)):
+        e = max_rel_err(stack[i], N[i])
+        assert e < TOL_REL, (family, sig[i], e)
+    ss, ys, xs, vs, thr = O.detect3x3x3(N, 0.5)
+    exempt, bad = compare_blobs(dets.as_set(), set(zip(ss.tolist(), ys.tolist(), xs.tolist())),
+                                N, thr, stack=True)
+    assert not bad, bad[:10]
+
+
+def test_config4_stream_64_frames(cat):
+    from paper_1912_07133_b200 import detect
+
+    frames = synth.config4_stream(n_frames=64)
+    host = torch.from_numpy(frames).pin_memory()
+    got = detect.stream_detect(host, cat["rp6"], frac=0.5)
+    assert len(got) == 64
+    for i in range(0, 64, 8):  # seeded sample against the oracle
+        L, want, thr = _oracle_scale(frames[i].astype(np.float64), cat["rp6"])
+        exempt, bad = compare_blobs(got[i].as_set(), want, L, thr)
+        assert not bad, (i, bad[:10])
+    for i in (1, 31, 63):  # and against single-frame calls
+        ref = detect.blur_laplacian_detect(frames[i], cat["rp6"], frac=0.5)
+        assert got[i].as_set() == ref.as_set() and got[i].count == ref.count
+
+
+@pytest.mark.parametrize("name", ["bw48", "sg38.4"])
+def test_config5_full_size(cat, name):
+    from paper_1912_07133_b200 import detect
+
+    x = synth.config5_frame(8192)
+    dets, blur, lap = detect.blur_laplacian_detect(x, cat[name], frac=0.5, return_fields=True)
+    B, L, (ys, xs, vs, thr) = O.pipeline(x, cat[name], frac=0.5)
+    assert max_rel_err(blur, B) < TOL_REL
+    e = max_rel_err(lap, L)
+    assert e < TOL_REL, (name, e)
+    exempt, bad = compare_blobs(dets.as_set(), set(zip(ys.tolist(), xs.tolist())), L, thr)
+    assert not bad, (name, bad[:10])
+
+
+@pytest.mark.parametrize("name", ["rp4", "g4_k16", "rp32"])
+def test_config3_low_threshold_large_list(cat, frame3, name):
+    """frac = 0.05 on the 4096^2 frame: far more than the finaliser's
+    one-CTA sort capacity survive (and many CTAs' shared candidate buffers
+    spill to the global list), so the multi-CTA row-range finaliser with its
+    look-back runs; the blob list still equals the oracle's (sorted by y, x)."""
+    from paper_1912_07133_b200 import detect
+
+    dets = detect.blur_laplacian_detect(frame3, cat[name], frac=0.05)
+    L, want, thr = _oracle_scale(frame3, cat[name], frac=0.05)
+    assert dets.count > 4096, dets.count  # the large-list path
+    assert not dets.overflow
+    ys, xs = np.asarray(dets.y), np.asarray(dets.x)
+    key = ys.astype(np.int64) * frame3.shape[1] + xs
+    assert np.all(np.diff(key) > 0)  # strictly (y, x) ordered
+    exempt, bad = compare_blobs(dets.as_set(), want, L, thr)
+    assert not bad, (name, len(bad), bad[:10])

@@ -61,7 +61,7 @@ def test_units_for_rank_validation():
         units_for_rank(10, 3, 3)
 
 
-def _ss_worker(rank, world, port, q):
+def _ss_worker(rank, world, port, q, sub=None):
     """The scale-sharded 3x3x3 NMS host logic on CPU (gloo): block partition,
     halo exchange, all-reduced maximum, own-plane filtering -- with the
     oracle's NMS standing in for the device kernel."""
@@ -73,6 +73,14 @@ def _ss_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    group = None
+    if sub is not None:  # a non-default group: P2P peers are group ranks -> global ranks
+        group = dist.new_group(sub)
+        if rank not in sub:
+            q.put((rank, None, None))
+            dist.destroy_process_group()
+            return
+        rank, world = dist.get_rank(group), len(sub)
     full = np.random.default_rng(5).standard_normal((5, 24, 20)).astype(np.float32)
     full[2, 10, 10] = 9.0          # a strong extremum in the middle scale
     full[0, 5, 5] = -8.0           # and on the first scale (one-sided in s)
@@ -85,21 +93,21 @@ def _ss_worker(rank, world, port, q):
         mx = slab[int(has_lo):int(has_lo) + n_own].abs().amax().reshape(1)
     else:
         mx = torch.zeros(1)
-    shard.exchange_halos(slab, has_lo, has_hi, rank)
-    shard.global_max(mx)
+    shard.global_max(mx, group)  # first: never a P2P batch as the group's first collective
+    shard.exchange_halos(slab, has_lo, has_hi, rank, group)
     got = []
     if n_own:
         ss, ys, xs, vs, thr = O.detect3x3x3(slab.numpy(), thr=0.5 * float(mx.item()))
         keep, sg = shard.own_detections(ss, lo, has_lo, n_own)
         got = sorted(zip(sg.tolist(), ys[keep].tolist(), xs[keep].tolist()))
     allgot = [None] * world
-    dist.all_gather_object(allgot, got)
+    dist.all_gather_object(allgot, got, group=group)
     q.put((rank, allgot, float(mx.item())))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3, 7])
-def test_scale_sharded_nms_equals_unsharded(world):
+@pytest.mark.parametrize("world,sub", [(2, None), (3, None), (7, None), (4, (1, 2, 3))])
+def test_scale_sharded_nms_equals_unsharded(world, sub):
     import numpy as np
 
     from oracle import oracle as O
@@ -107,7 +115,7 @@ def test_scale_sharded_nms_equals_unsharded(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ss_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ss_worker, args=(r, world, port, q, sub)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(world)]
@@ -120,6 +128,8 @@ def test_scale_sharded_nms_equals_unsharded(world):
     ss, ys, xs, vs, thr = O.detect3x3x3(full.astype(np.float64), frac=0.5)
     want = sorted(zip(ss.tolist(), ys.tolist(), xs.tolist()))
     assert len(want) >= 2
+    res = [r for r in res if r[1] is not None]
+    assert len(res) == (len(sub) if sub else world)
     for rank, allgot, mx in res:
         assert mx == pytest.approx(9.0)
         assert sorted(d for part in allgot for d in part) == want
