@@ -313,6 +313,8 @@ size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage
   if (fused_col(col_stage, h, w)) {
     size_t c3 = colpass_workspace_bytes(h, w, col_stage->n, 0);
     if (c3 > carry) carry = c3;
+    c3 = colpass32_workspace_bytes(h, w, col_stage->n);
+    if (c3 > carry) carry = c3;
   }
   if (fused_fir_col(col_stage, h, w)) {
     size_t c4 = firpass_workspace_bytes(h, w);
@@ -358,8 +360,12 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
     rc = iir_plan(&ip, w, h, col_stage->b_plus, col_stage->a_plus, col_stage->n,
                   col_stage->b_zero, col_stage->sign);
     if (rc) return rc;
-    rc = colpass_run(T, w, L, w, nullptr, ip, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
-                     thr_dev, carry, carry_b, st);
+    if (colpass32_supported(h, w, ip))  // fp32 "Laplacian first" (vmf_colpass32.cu)
+      rc = colpass32_run(T, w, L, w, ip, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
+                         thr_dev, carry, carry_b, st);
+    else
+      rc = colpass_run(T, w, L, w, nullptr, ip, h, w, lap_scale, frac, det_yx, det_val, cap,
+                       n_det_dev, thr_dev, carry, carry_b, st);
     if (rc) return rc;
     if (blur_out) {  // B is not materialised by the fused pass; recompute on request
       rc = run_stage<COLS>(col_stage, T, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);

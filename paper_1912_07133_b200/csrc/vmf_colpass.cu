@@ -90,9 +90,11 @@ __device__ __forceinline__ void carry_half(const ColParams &p, const float *tile
   }
 #pragma unroll
   for (int t = 0; t < kHalf; ++t) {
-    // pair sums in fp32 (one conversion per sum; the rounding is that of an
-    // fp32 input)
-    const double u = (double)(xa[t] + xb[t]), v = (double)(xa[t] - xb[t]);
+    // pair sums in fp64: an fp32 sum would inject an fp32 rounding of |2T|
+    // into every band carry, i.e. B errors of fp32-ulp size, which the
+    // Laplacian amplifies past the 1e-4 tolerance at large sigma
+    const double xa64 = (double)xa[t], xb64 = (double)xb[t];
+    const double u = xa64 + xb64, v = xa64 - xb64;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       P[i] = fma(p.SP[i][t0 + t], u, P[i]);

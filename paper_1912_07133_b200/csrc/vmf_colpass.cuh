@@ -93,4 +93,15 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
                 float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
                 size_t ws_bytes, cudaStream_t st, bool blur_only = false);
 
+// fp32 "Laplacian-first" fused column pass (vmf_colpass32.cu): the detect
+// path's column pass for IIR stages with a modal fp32 realisation (repeated
+// real pole, K = 2..4, or a complex pair, K = 2); L (* lap_scale) +
+// detections, no blur output.
+bool colpass32_supported(int64_t h, int64_t w, const IirParams &ip);
+size_t colpass32_workspace_bytes(int64_t h, int64_t w, int k);
+int colpass32_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,
+                  int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
+                  float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
+                  size_t ws_bytes, cudaStream_t st);
+
 }  // namespace vmf

@@ -1,0 +1,988 @@
+// vmf_colpass32.cu -- the fused second pass in fp32, "Laplacian first":
+// column IIR (iir_cols, engine.py:156-158 / kernel 65-102) + Laplacian
+// D20 + D02 (engine.py:218-227, blob.py:161) + threshold / 3x3 NMS
+// (SURVEY.md §8(d)), reading the row-pass output T and writing L plus a short
+// candidate list.
+//
+// Why fp32 is enough here.  The reference forms B = C(T) (column filter with
+// steady-state starts) and then L = D20(B) + D02(B) with replicate edges; L is
+// ~1e-3 of B at sigma = 32, so any fp32 rounding of B costs ~1e-4 of max|L|.
+// By linearity and shift invariance on the replicate-extended column the
+// same L is
+//     L = C(U) + corrections at rows 0 and H-1,
+//     U = 5-point Laplacian of T (replicate edges; rows past the bottom are
+//         clamped copies, so there U = D20 T(H-1)), steady-state starts from
+//         D20 T of rows 0 / H-1,
+//     L(0)   += sign * sum_{m>=1} h(m) G(m),   G(m) = T(m) - T(m-1),
+//     L(H-1) -=        sum_{m>=1} h(m) G(H-m),
+// and every quantity in it is a difference of T, so fp32 rounding is relative
+// to |L|, not |B|.  The recursion itself must be well conditioned in fp32: the
+// causal part B(z)/A(z) is realised in modal form (a Jordan chain
+// u1 = p u1 + x, u2 = p u2 + u1, ... for the repeated real pole of the
+// repeated-pole blurs; a rotation for the complex pair of the Butterworth
+// blur), y+(n) = c . u(n-1) -- DF-I in fp32 misses the tolerance by 16x at
+// sigma = 32.  tools/experiments/col_lapfirst_chunked.py is the numpy
+// prototype of exactly this chunking (fp32 throughout): its error equals the
+// fp64 column pass's on the same fp32 T at every config scale.
+//
+// Chunking (as the fp64 pass): bands of 64 rows; colcarry32 computes the
+// zero-state end states of both directions of every (band, column) by folded
+// sample pairs, and band partials of the two boundary corrections; colscan32
+// turns them into the true start state of every band (fp64 arithmetic over
+// fp32 records, Kogge-Stone over bands with A^(64 cpl 2^j)) and sums the
+// corrections; colapply32 (128 columns x one band per CTA) walks up (the
+// backward part parked in registers) and down (L produced directly), then
+// stores the owned 124 x 64 block fused with the 3x3 NMS, exactly like the
+// fp64 pass.  L of the halo rows r0-1 / r1 (for the NMS) comes from the band
+// start states through c A^-1.
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+#include <vector>
+
+#include "plan_cache.hpp"
+#include "vmf_colpass.cuh"
+#include "vmf_common.cuh"
+#include "vmf_prof.cuh"
+#include "vmf_tma.cuh"
+
+namespace vmf {
+
+constexpr int kB32 = 64;                 // rows per band
+constexpr int kC32 = 128;                // columns per CTA (carry and apply)
+constexpr int kC32Out = kC32 - 4;        // owned columns per apply CTA
+constexpr int kT32Stride = kC32 + 4;     // apply tile stride: tile col j+2 <-> thread j
+constexpr int kT32Rows = kB32 + 4;       // T rows r0-2 .. r1+1
+constexpr int kL32Rows = kB32 + 2;       // U / L rows r0-1 .. r1
+constexpr int kCarryStride = kC32 + 8;   // carry tile: cols c0-4 .. c0+131
+constexpr int kCarryRows = kB32 + 2;     // T rows r0-1 .. r1
+constexpr int kCand32 = 256;             // per-CTA candidate buffer
+constexpr int kMaxCpl32 = 4;             // bands per lane in the scan (H <= 8192)
+constexpr int kScan32Cols = 8;
+constexpr int kHm32Max = 2048;           // boundary-correction weights h(1..Mh)
+
+// modal realisation: JORDAN (repeated real pole, K = 2..4) or CPAIR (K = 2)
+enum Modal32Kind { M32_JORDAN = 0, M32_CPAIR = 1 };
+
+struct Col32Params {
+  float p, q;               // JORDAN: pole p; CPAIR: p + i q
+  float c[4];               // y+(n) = c . u(n-1)
+  float ci[4];              // c A^-1 (halo rows)
+  float e1;                 // c A^-1 b
+  float b0, sign, lsc, frac;
+  float SP[4][kB32 / 2], SQ[4][kB32 / 2];  // folded band-carry weights
+  double ALp[5][16];        // A^(64 cpl 2^l), row-major K x K
+  double AL[16];            // A^64
+  double Iss[4];            // (I - A)^-1 b: steady state per unit input
+  int64_t H, W;
+  int NB, cpl, K, Mh;       // bands; bands per scan lane; order; correction length
+};
+
+// h(m) = c A^(m-1) b, m = 0..Mh (h(0) = 0): the boundary-correction weights,
+// a kernel parameter of the carry pass only
+struct Hm32 {
+  float h[kHm32Max + 1];
+};
+
+// ---------------------------------------------------------------------------
+// the recursion: u <- A u + b x, y = c . u (before the update)
+// ---------------------------------------------------------------------------
+template <int K, int KIND>
+struct Rec32 {
+  float u[K];
+  __device__ __forceinline__ float out(const float *c) const {
+    float y = c[0] * u[0];
+#pragma unroll
+    for (int i = 1; i < K; ++i) y = fmaf(c[i], u[i], y);
+    return y;
+  }
+  __device__ __forceinline__ float out_from(const float *c, float acc) const {
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc = fmaf(c[i], u[i], acc);
+    return acc;
+  }
+  __device__ __forceinline__ void step(const Col32Params &P, float x) {
+    if (KIND == M32_JORDAN) {
+      u[0] = fmaf(P.p, u[0], x);
+#pragma unroll
+      for (int i = 1; i < K; ++i) u[i] = fmaf(P.p, u[i], u[i - 1]);
+    } else {
+      const float ur = u[0], ui = u[1];
+      u[0] = fmaf(P.p, ur, fmaf(-P.q, ui, x));
+      u[1] = fmaf(P.q, ur, P.p * ui);
+    }
+  }
+};
+
+// U = ((l - c) + (r - c)) + ((u - c) + (d - c)): every term a difference of
+// neighbouring T values (rounding relative to the difference); the same
+// expression everywhere, so the carry and apply passes see bitwise-equal U.
+__device__ __forceinline__ float lap5(float l, float c, float r, float u, float d) {
+  return ((l - c) + (r - c)) + ((u - c) + (d - c));
+}
+
+// Band records, coalesced along columns: R[(b * (2K + 2) + q) * W + col]
+//   q < K: forward zero-state end state (-> forward start state uf(r0-1)),
+//   K <= q < 2K: backward (-> ub(r1)), 2K / 2K+1: the band's partials of the
+//   top / bottom boundary corrections.
+__device__ __forceinline__ int64_t ridx(int b, int q, int K, int64_t W, int64_t col) {
+  return ((int64_t)b * (2 * K + 2) + q) * W + col;
+}
+
+// ---------------------------------------------------------------------------
+// 1. band carries
+// ---------------------------------------------------------------------------
+// One CTA = 128 columns x one band, 256 threads: threads j and j + 128 take the
+// two halves of the band's 32 sample pairs (t, 63 - t) of column j.  The tile
+// holds T rows r0-1 .. r1 (clamped), columns c0-4 .. c0+131 (clamped).
+template <int K>
+__global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
+    const float *__restrict__ T, int64_t ldt, Col32Params p, float *__restrict__ R,
+    const __grid_constant__ Hm32 hm, const __grid_constant__ CUtensorMap tmap, int use_tma,
+    CandState *__restrict__ cs) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
+  float *tile = reinterpret_cast<float *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t tbar;
+  __shared__ float part[2 * K + 2][kC32];
+  const int j = threadIdx.x & (kC32 - 1), half = threadIdx.x >> 7;
+  const int b = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * kC32;
+  const int64_t col = c0 + j;
+  const int64_t r0 = (int64_t)b * kB32;
+  const int64_t H = p.H, W = p.W;
+  const bool tma = use_tma && r0 >= 1 && r0 + kB32 + 1 <= H && c0 >= 4 && c0 + kC32 + 4 <= W;
+  pdl_wait();  // T comes from the row pass
+  if (blockIdx.x == 0 && blockIdx.y == 0) cand_reset(cs);
+  if (tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&tbar, 1);
+      mbar_expect_tx(&tbar, (unsigned)(kCarryRows * kCarryStride * sizeof(float)));
+      tma_load_2d_hint(tile, &tmap, &tbar, (int)(c0 - 4), (int)(r0 - 1), l2_policy_evict_last());
+    }
+    __syncthreads();
+    mbar_wait(&tbar, 0);
+  } else {  // clamped rows / columns (replicate edges; rows past H repeat H-1)
+    for (int e = threadIdx.x; e < kCarryRows * kCarryStride; e += blockDim.x) {
+      const int tr = e / kCarryStride, tc = e - tr * kCarryStride;
+      int64_t r = r0 - 1 + tr, c = c0 - 4 + tc;
+      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+      c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+      tile[e] = __ldg(T + r * ldt + c);
+    }
+    __syncthreads();
+  }
+  // tile row of image row r: r - r0 + 1; tile column of column c0 + j: j + 4
+  const float *tc = tile + j + 4;
+#define TT(tr, dc) tc[(tr) * kCarryStride + (dc)]
+  auto U = [&](int tr) { return lap5(TT(tr, -1), TT(tr, 0), TT(tr, 1), TT(tr - 1, 0), TT(tr + 1, 0)); };
+  float P[K], Q[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0f;
+  // warp-uniform halves, so the weight indices are compile-time constants
+  // (the weights stay constant-bank operands of the FFMAs)
+  auto run = [&](auto HALF) {
+    constexpr int t0 = decltype(HALF)::value * (kB32 / 4);
+#pragma unroll
+    for (int t = 0; t < kB32 / 4; ++t) {
+      const float ua = U(1 + t0 + t), ub = U(kB32 - t0 - t);
+      const float s = ua + ub, d = ua - ub;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        P[i] = fmaf(p.SP[i][t0 + t], s, P[i]);
+        Q[i] = fmaf(p.SQ[i][t0 + t], d, Q[i]);
+      }
+    }
+  };
+  if (half == 0)
+    run(std::integral_constant<int, 0>());
+  else
+    run(std::integral_constant<int, 1>());
+  // boundary-correction partials (bands within Mh rows of the top / bottom):
+  // top = sum h(r) G(r), bottom = sum h(H - r) G(r) over this band's rows
+  // 1 <= r < H, G(r) = T(r) - T(r-1); each half takes 32 rows
+  float pt = 0.0f, pb = 0.0f;
+  const bool top = r0 < p.Mh + 1, bot = r0 + kB32 > H - 1 - p.Mh;
+  if (top || bot) {
+    for (int t = half * (kB32 / 2); t < (half + 1) * (kB32 / 2); ++t) {
+      const int64_t r = r0 + t;
+      if (r < 1 || r >= H) continue;
+      const float g = TT(t + 1, 0) - TT(t, 0);
+      if (top && r <= p.Mh) pt = fmaf(hm.h[r], g, pt);
+      if (bot && H - r <= p.Mh) pb = fmaf(hm.h[H - r], g, pb);
+    }
+  }
+#undef TT
+  pdl_trigger();
+  if (half == 1) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      part[i][j] = P[i];
+      part[K + i][j] = Q[i];
+    }
+    part[2 * K][j] = pt;
+    part[2 * K + 1][j] = pb;
+  }
+  __syncthreads();
+  if (half == 0 && col < W) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const float Pt = P[i] + part[i][j], Qt = Q[i] + part[K + i][j];
+      R[ridx(b, i, K, W, col)] = Pt + Qt;       // forward
+      R[ridx(b, K + i, K, W, col)] = Pt - Qt;   // backward
+    }
+    R[ridx(b, 2 * K, K, W, col)] = pt + part[2 * K][j];
+    R[ridx(b, 2 * K + 1, K, W, col)] = pb + part[2 * K + 1][j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2. band scan.  CTA = one direction x 8 columns; warp = one column, lanes
+//    over bands (cpl each); fp64 arithmetic.  Writes the start state of every
+//    band over its zero-state carry, and (direction 0 / 1) the column's top /
+//    bottom boundary correction into Cc[dir][W].
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(32 * kScan32Cols) colscan32_kernel(
+    const float *__restrict__ T, int64_t ldt, Col32Params p, float *__restrict__ R,
+    float *__restrict__ Cc) {
+  const int NB = p.NB, cpl = p.cpl;
+  const int dir = blockIdx.y;
+  const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
+  const int64_t col = (int64_t)blockIdx.x * kScan32Cols + wc;
+  const bool live = col < p.W;
+  const int64_t cc = live ? col : p.W - 1;
+  pdl_wait();  // records come from the band carries
+  // steady-state input before the first band: D20 T of row 0 (forward) or
+  // H-1 (backward), the same fp32 expression as U's horizontal part
+  const int64_t er = dir == 0 ? 0 : p.H - 1;
+  const int64_t cl = cc > 0 ? cc - 1 : 0, cr = cc + 1 < p.W ? cc + 1 : p.W - 1;
+  const float tl = __ldg(T + er * ldt + cl), tcv = __ldg(T + er * ldt + cc),
+              tr = __ldg(T + er * ldt + cr);
+  const double e = (double)((tl - tcv) + (tr - tcv));
+  // own bands: d = z (zero-state carries), position sp -> band b
+  double dl[kMaxCpl32][K];
+  double corr = 0.0;
+#pragma unroll
+  for (int q = 0; q < kMaxCpl32; ++q) {
+    const int sp = lane * cpl + q;
+    if (q < cpl && sp < NB) {
+      const int b = dir == 0 ? sp : NB - 1 - sp;
+#pragma unroll
+      for (int i = 0; i < K; ++i) dl[q][i] = (double)R[ridx(b, dir * K + i, K, p.W, cc)];
+      corr += (double)R[ridx(b, 2 * K + dir, K, p.W, cc)];
+      if (sp == 0) {  // + A^64 u_ss(e): the steady start enters with the first band
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          double a = 0.0;
+#pragma unroll
+          for (int m = 0; m < K; ++m) a = fma(p.AL[i * K + m], p.Iss[m] * e, a);
+          dl[q][i] += a;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < K; ++i) dl[q][i] = 0.0;
+    }
+  }
+  pdl_trigger();
+  // lane-local inclusive composition of its cpl bands, then Kogge-Stone
+  double A[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) A[i] = 0.0;
+#pragma unroll
+  for (int q = 0; q < kMaxCpl32; ++q) {
+    if (q < cpl && lane * cpl + q < NB) {
+      double An[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double a = dl[q][i];
+#pragma unroll
+        for (int m = 0; m < K; ++m) a = fma(p.AL[i * K + m], A[m], a);
+        An[i] = a;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) A[i] = An[i];
+    }
+  }
+#pragma unroll
+  for (int lv = 0; lv < 5; ++lv) {
+    const int o = 1 << lv;
+    double Bv[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) Bv[i] = __shfl_up_sync(0xffffffffu, A[i], o);
+    if (lane >= o) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double a = A[i];
+#pragma unroll
+        for (int m = 0; m < K; ++m) a = fma(p.ALp[lv][i * K + m], Bv[m], a);
+        A[i] = a;
+      }
+    }
+  }
+  // exclusive: the state entering this lane's first band
+  double E[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const double v = __shfl_up_sync(0xffffffffu, A[i], 1);
+    E[i] = lane ? v : p.Iss[i] * e;
+  }
+  // column sum of the boundary-correction partials (fixed order)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) corr += __shfl_xor_sync(0xffffffffu, corr, o);
+  if (lane == 0 && live) Cc[(int64_t)dir * p.W + col] = (float)corr;
+#pragma unroll
+  for (int q = 0; q < kMaxCpl32; ++q) {
+    const int sp = lane * cpl + q;
+    if (q < cpl && sp < NB) {
+      const int b = dir == 0 ? sp : NB - 1 - sp;
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) R[ridx(b, dir * K + i, K, p.W, col)] = (float)E[i];
+      }
+      if (sp == 0) {
+        // E <- A^64 E_start + z: dl[0] already holds z + A^64 u_ss(e) = the
+        // inclusive state after the first band
+#pragma unroll
+        for (int i = 0; i < K; ++i) E[i] = dl[q][i];
+      } else {
+        double En[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          double a = dl[q][i];
+#pragma unroll
+          for (int m = 0; m < K; ++m) a = fma(p.AL[i * K + m], E[m], a);
+          En[i] = a;
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) E[i] = En[i];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3. walk a band: U, the column recursion in both directions, L, NMS
+// ---------------------------------------------------------------------------
+struct Col32Smem {
+  float tile[kT32Rows][kT32Stride];  // T rows r0-2 .. r1+1, cols c0-4 .. c0+127
+  float lt[kL32Rows][kT32Stride];    // U, then L, rows r0-1 .. r1 (same columns)
+  int cy[kCand32], cx[kCand32];
+  float cv[kCand32];
+  int ccount;
+  unsigned int cmax;
+  float thr_end;
+};
+
+// LSC: multiply by lap_scale (sigma^2 normalisation of the scale-space stack)
+template <int K, int KIND, bool LSC>
+__global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
+    const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl,
+    Col32Params p, const float *__restrict__ R, const float *__restrict__ Cc,
+    CandState *__restrict__ st, int *__restrict__ gy, int *__restrict__ gx,
+    float *__restrict__ gv, int gcap, const __grid_constant__ CUtensorMap tmap, int use_tma,
+    int vec_out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
+  Col32Smem &S = *reinterpret_cast<Col32Smem *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t tbar;
+  const int j = threadIdx.x, lane = j & 31, wid = j >> 5;
+  const int64_t H = p.H, W = p.W;
+  const int64_t c0 = (int64_t)blockIdx.x * kC32Out;
+  const int64_t col = c0 - 2 + j;
+  const int64_t colc = col < 0 ? 0 : (col >= W ? W - 1 : col);
+  const int b = blockIdx.y;
+  const int64_t r0 = (int64_t)b * kB32, r1 = r0 + kB32;
+  const bool tma = use_tma && r0 >= 2 && r1 + 2 <= H && c0 >= 4 && c0 + kC32 <= W;
+  if (tma) {  // one box: rows r0-2 .. r1+1, columns c0-4 .. c0+127
+    if (j == 0) {
+      mbar_init(&tbar, 1);
+      mbar_expect_tx(&tbar, (unsigned)(kT32Rows * kT32Stride * sizeof(float)));
+      tma_load_2d_hint(&S.tile[0][0], &tmap, &tbar, (int)(c0 - 4), (int)(r0 - 2),
+                       l2_policy_evict_first());  // last use of T
+    }
+  } else {  // clamped 4-byte async copies (replicate edges)
+    for (int e = j; e < kT32Rows * kT32Stride; e += kC32) {
+      const int tr = e / kT32Stride, tcn = e - tr * kT32Stride;
+      int64_t r = r0 - 2 + tr, c = c0 - 4 + tcn;
+      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+      c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(&S.tile[tr][tcn]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + c));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  if (j == 0) {
+    S.ccount = 0;
+    S.cmax = 0u;
+  }
+  pdl_wait();  // band start states, corrections and the CandState come from earlier kernels
+  const float gbound = __uint_as_float(st->absmax_bits);  // global max so far (lower bound)
+  Rec32<K, KIND> rb, rf;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    rf.u[i] = R[ridx(b, i, K, W, colc)];
+    rb.u[i] = R[ridx(b, K + i, K, W, colc)];
+  }
+  // boundary corrections of rows 0 and H-1 where this band computes them
+  const float ctop = r0 == 0 ? p.sign * Cc[colc] : 0.0f;
+  const float cbot = (H - 1 >= r0 - 1 && H - 1 <= r1) ? Cc[W + colc] : 0.0f;
+  if (tma) {
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&tbar, 0);
+  } else {
+    asm volatile("cp.async.wait_group 0;\n" ::);
+  }
+  __syncthreads();
+
+  // ---- up: U of rows r1 .. r0-1 into lt, the backward recursion parked ----
+  // T tile row of image row r: r - r0 + 2; lt row: r - r0 + 1
+  const float *tcol = &S.tile[0][j + 2];
+  float *lcol = &S.lt[0][j + 2];
+  float park[kB32];
+  float ym_below, ym_above;
+  {
+    float td = tcol[(kB32 + 3) * kT32Stride];  // T(r1+1)
+    float tcv = tcol[(kB32 + 2) * kT32Stride]; // T(r1)
+    // r = r1 (halo): y-(r1) = c A^-1 ub(r1) - e1 U(r1)
+    {
+      const float tu = tcol[(kB32 + 1) * kT32Stride];
+      const float u = lap5(tcol[(kB32 + 2) * kT32Stride - 1], tcv, tcol[(kB32 + 2) * kT32Stride + 1],
+                           tu, td);
+      lcol[(kB32 + 1) * kT32Stride] = u;
+      ym_below = fmaf(-p.e1, u, rb.out(p.ci));
+      td = tcv;
+      tcv = tu;
+    }
+#pragma unroll
+    for (int t = kB32 - 1; t >= 0; --t) {  // rows r0 + t
+      const float tu = tcol[(t + 1) * kT32Stride];
+      const float u = lap5(tcol[(t + 2) * kT32Stride - 1], tcv, tcol[(t + 2) * kT32Stride + 1], tu, td);
+      lcol[(t + 1) * kT32Stride] = u;
+      park[t] = rb.out(p.c);  // y-(r0 + t)
+      rb.step(p, u);
+      td = tcv;
+      tcv = tu;
+    }
+    ym_above = rb.out(p.c);  // y-(r0 - 1)
+    // U(r0 - 1) for the top halo row
+    const float tu = tcol[0];
+    lcol[0] = lap5(tcol[kT32Stride - 1], tcv, tcol[kT32Stride + 1], tu, td);
+  }
+
+  // ---- down: L of rows r0-1 .. r1 in place of U ----------------------------
+  const float lsc = p.lsc, b0 = p.b0, sg = p.sign;
+  float tmax = 0.0f;
+  {
+    // top halo row r0 - 1: y+(r0-1) = c A^-1 uf(r0-1) - e1 U(r0-1)
+    if (r0 > 0) {
+      const float u = lcol[0];
+      float v = fmaf(-p.e1, u, rf.out_from(p.ci, fmaf(b0, u, sg * ym_above)));
+      if (r0 - 1 == H - 1) v -= cbot;
+      if (LSC) v *= lsc;
+      lcol[0] = v;
+    }
+#pragma unroll
+    for (int t = 0; t < kB32; ++t) {
+      const int64_t r = r0 + t;
+      const float u = lcol[(t + 1) * kT32Stride];
+      float v = rf.out_from(p.c, fmaf(b0, u, sg * park[t]));
+      rf.step(p, u);
+      if (r == 0) v += ctop;
+      if (r == H - 1) v -= cbot;
+      if (LSC) v *= lsc;
+      lcol[(t + 1) * kT32Stride] = v;
+      if (r < H) tmax = fmaxf(tmax, fabsf(v));
+    }
+    // bottom halo row r1: y+(r1) = c . uf(r1-1) (the walk's end state)
+    {
+      const float u = lcol[(kB32 + 1) * kT32Stride];
+      float v = rf.out_from(p.c, fmaf(b0, u, sg * ym_below));
+      if (r1 == H - 1) v -= cbot;
+      if (LSC) v *= lsc;
+      lcol[(kB32 + 1) * kT32Stride] = v;
+    }
+  }
+  pdl_trigger();
+  // columns outside the image and the two halo columns each side never count
+  if (j < 2 || j >= kC32 - 2 || col >= W) tmax = 0.0f;
+  tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+  if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
+  __syncthreads();
+  // publish this CTA's max now (later CTAs prune with it) and pick up what
+  // earlier CTAs published since this one started
+  if (j == 0) atomicMax(&st->absmax_bits, S.cmax);
+  const float gnow = fmaxf(gbound, __uint_as_float(*(volatile unsigned *)&st->absmax_bits));
+
+  // ---- store the owned L block (rows r0 .. min(r1, H)-1, cols c0 .. c0+123)
+  // fused with the strict 3x3 NMS over frac * max(this CTA's max, the global
+  // max so far): a lower bound of the final threshold -> a superset
+  {
+    const int64_t rhi = r1 < H ? r1 : H;
+    const int nrow = (int)(rhi - r0);
+    const int ncol = (int)(W - c0 < kC32Out ? W - c0 : kC32Out);
+    const float th = p.frac > 0.0f ? p.frac * fmaxf(__uint_as_float(S.cmax), gnow)
+                                   : __int_as_float(0x7f800000);
+    auto test = [&](int q, int c, float v) {  // lt row q + 1, lt column 4 + c
+      const int64_t r = r0 + q, cc = c0 + c;
+      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return;
+      const int tr = q + 1, tcn = 4 + c;
+      bool gt = true, lt = true;
+#pragma unroll
+      for (int di = -1; di <= 1; ++di)
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj) {
+          if (!di && !dj) continue;
+          const float w = S.lt[tr + di][tcn + dj];
+          gt &= v > w;
+          lt &= v < w;
+        }
+      // a maximum counts when L >= t, a minimum when -L >= t
+      if ((gt && v >= th) || (lt && -v >= th))
+        cand_push(&S.ccount, S.cy, S.cx, S.cv, kCand32, st, gy, gx, gv, gcap, (int)r, (int)cc, v);
+    };
+    if (vec_out && ncol == kC32Out) {  // 31 float4 per row, one row per warp
+      const bool act = lane < kC32Out / 4;
+      const uint64_t lpol = l2_policy_evict_first();  // L streams out
+      float *dst = Lout + r0 * ldl + c0 + 4 * lane;
+#pragma unroll 4
+      for (int q = wid; q < nrow; q += kC32 / 32) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (act) {
+          v = *reinterpret_cast<const float4 *>(&S.lt[q + 1][4 + 4 * lane]);
+          st_v4_hint(dst + q * ldl, v, lpol);
+        }
+        const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+        if (m4 >= th) {
+          if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
+          if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
+          if (fabsf(v.z) >= th) test(q, 4 * lane + 2, v.z);
+          if (fabsf(v.w) >= th) test(q, 4 * lane + 3, v.w);
+        }
+      }
+    } else {
+      for (int q = wid; q < nrow; q += kC32 / 32)
+        for (int cl = 0; cl < ncol; cl += 32) {
+          const int c = cl + lane;
+          float v = 0.0f;
+          if (c < ncol) {
+            v = S.lt[q + 1][4 + c];
+            Lout[(r0 + q) * ldl + c0 + c] = v;
+          }
+          if (c < ncol && fabsf(v) >= th) test(q, c, v);
+        }
+    }
+  }
+  __syncthreads();
+  // ---- flush candidates that survive the best threshold known now ---------
+  if (j == 0) {
+    const unsigned old = atomicMax(&st->absmax_bits, S.cmax);
+    S.thr_end = p.frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
+  }
+  __syncthreads();
+  const int n = S.ccount < kCand32 ? S.ccount : kCand32;
+  for (int q = j; q < n; q += kC32) {
+    if (!(fabsf(S.cv[q]) >= S.thr_end)) continue;
+    const int k = atomicAdd(&st->count, 1);
+    if (k < gcap) {
+      gy[k] = S.cy[q];
+      gx[k] = S.cx[q];
+      gv[k] = S.cv[q];
+    } else {
+      st->overflow = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host: modal realisation (long double), plan, launches
+// ---------------------------------------------------------------------------
+typedef long double ld;
+
+static void matmul(const ld *A, const ld *B, ld *C, int k) {
+  ld t[16];
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) {
+      ld s = 0;
+      for (int m = 0; m < k; ++m) s += A[i * k + m] * B[m * k + j];
+      t[i * k + j] = s;
+    }
+  memcpy(C, t, sizeof(ld) * k * k);
+}
+
+static void matpow(const ld *A, int64_t n, ld *out, int k) {
+  ld R[16], P[16];
+  for (int i = 0; i < k * k; ++i) R[i] = (i % (k + 1) == 0) ? 1 : 0;
+  memcpy(P, A, sizeof(ld) * k * k);
+  while (n > 0) {
+    if (n & 1) matmul(R, P, R, k);
+    matmul(P, P, P, k);
+    n >>= 1;
+  }
+  memcpy(out, R, sizeof(ld) * k * k);
+}
+
+// solve M x = y (k <= 4), partial pivoting; false if singular
+static bool solve(ld *M, ld *y, int k) {
+  for (int c = 0; c < k; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < k; ++r)
+      if (fabsl(M[r * k + c]) > fabsl(M[piv * k + c])) piv = r;
+    if (fabsl(M[piv * k + c]) < 1e-300L) return false;
+    if (piv != c) {
+      for (int m = 0; m < k; ++m) {
+        ld t = M[c * k + m];
+        M[c * k + m] = M[piv * k + m];
+        M[piv * k + m] = t;
+      }
+      ld t = y[c];
+      y[c] = y[piv];
+      y[piv] = t;
+    }
+    for (int r = 0; r < k; ++r) {
+      if (r == c) continue;
+      const ld f = M[r * k + c] / M[c * k + c];
+      for (int m = 0; m < k; ++m) M[r * k + m] -= f * M[c * k + m];
+      y[r] -= f * y[c];
+    }
+  }
+  for (int c = 0; c < k; ++c) y[c] /= M[c * k + c];
+  return true;
+}
+
+// Causal impulse response of the reference's DF-II recursion (engine.py:79-88)
+static void impulse_ref(const double *b, const double *a, int k, int n, ld *h) {
+  ld s[VMF_MAX_IIR_ORDER] = {0};
+  for (int t = 0; t < n; ++t) {
+    ld y = 0, w = (t == 0) ? 1 : 0;
+    for (int m = 0; m < k; ++m) {
+      y += (ld)b[m] * s[m];
+      w -= (ld)a[m] * s[m];
+    }
+    h[t] = y;
+    for (int m = k - 1; m > 0; --m) s[m] = s[m - 1];
+    s[0] = w;
+  }
+}
+
+struct Modal {
+  int kind, k;
+  ld p, q;
+  ld A[16], bv[4], c[4];
+};
+
+// repeated real pole (a_plus = coefficients of (1 - p w)^k) or, for k = 2, a
+// complex pair; the output vector c matches the first k impulse-response
+// samples and the whole response is verified against the reference's
+// recursion.
+static bool modal_realise(const double *b, const double *a, int k, Modal *M) {
+  if (k < 2 || k > 4) return false;
+  memset(M, 0, sizeof(*M));
+  M->k = k;
+  const ld p = -(ld)a[0] / k;
+  ld binom = 1, maxdev = 0, scale = 0;
+  for (int m = 1; m <= k; ++m) {
+    binom = binom * (k - m + 1) / m;
+    const ld coef = binom * powl(-p, m);
+    maxdev = fmaxl(maxdev, fabsl(coef - (ld)a[m - 1]));
+    scale = fmaxl(scale, fabsl((ld)a[m - 1]));
+  }
+  if (maxdev <= 1e-13L * scale && p > 0 && p < 1) {
+    M->kind = M32_JORDAN;
+    M->p = p;
+    for (int i = 0; i < k; ++i) {
+      M->bv[i] = 1;
+      for (int j2 = 0; j2 < k; ++j2) M->A[i * k + j2] = j2 <= i ? p : 0;
+    }
+  } else if (k == 2 && a[0] * a[0] - 4 * a[1] < 0) {
+    M->kind = M32_CPAIR;
+    M->p = -(ld)a[0] / 2;
+    M->q = sqrtl(4 * (ld)a[1] - (ld)a[0] * a[0]) / 2;
+    M->A[0] = M->p;
+    M->A[1] = -M->q;
+    M->A[2] = M->q;
+    M->A[3] = M->p;
+    M->bv[0] = 1;
+    M->bv[1] = 0;
+  } else {
+    return false;
+  }
+  ld h[256];
+  impulse_ref(b, a, k, 256, h);
+  ld Mx[16], y[4], v[4], t[4];
+  for (int i = 0; i < k; ++i) v[i] = M->bv[i];
+  for (int m = 0; m < k; ++m) {  // row m: (A^m b)^T, matched to h(m + 1)
+    for (int i = 0; i < k; ++i) Mx[m * k + i] = v[i];
+    y[m] = h[m + 1];
+    for (int i = 0; i < k; ++i) {
+      t[i] = 0;
+      for (int jj = 0; jj < k; ++jj) t[i] += M->A[i * k + jj] * v[jj];
+    }
+    memcpy(v, t, sizeof(ld) * k);
+  }
+  if (!solve(Mx, y, k)) return false;
+  for (int i = 0; i < k; ++i) M->c[i] = y[i];
+  // verify h(m) = c A^(m-1) b over 255 samples
+  ld hmax = 0, err = 0;
+  for (int i = 0; i < k; ++i) v[i] = M->bv[i];
+  for (int m = 1; m < 256; ++m) {
+    ld hm = 0;
+    for (int i = 0; i < k; ++i) hm += M->c[i] * v[i];
+    hmax = fmaxl(hmax, fabsl(h[m]));
+    err = fmaxl(err, fabsl(hm - h[m]));
+    for (int i = 0; i < k; ++i) {
+      t[i] = 0;
+      for (int jj = 0; jj < k; ++jj) t[i] += M->A[i * k + jj] * v[jj];
+    }
+    memcpy(v, t, sizeof(ld) * k);
+  }
+  return err <= 1e-12L * hmax;
+}
+
+struct Col32Plan {
+  Col32Params p;
+  Hm32 hm;
+  int kind;
+};
+
+size_t colpass32_workspace_bytes(int64_t h, int64_t w, int k) {
+  const int64_t NB = cdiv(h, kB32);
+  const size_t rec = (size_t)NB * (2 * k + 2) * w * sizeof(float);
+  const int64_t gcap = colpass_cand_capacity(h, w);
+  return 4096 + ((rec + 255) & ~(size_t)255) + ((2 * w * sizeof(float) + 255) & ~(size_t)255) +
+         (size_t)gcap * 12 + 1024;
+}
+
+static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
+  Modal M;
+  if (!modal_realise(ip.b, ip.a, ip.K, &M)) return fail(VMF_EVALUE, "no modal realisation");
+  const int k = ip.K;
+  Col32Params &p = P->p;
+  memset(&p, 0, sizeof(p));
+  P->kind = M.kind;
+  p.K = k;
+  p.p = (float)M.p;
+  p.q = (float)M.q;
+  for (int i = 0; i < k; ++i) p.c[i] = (float)M.c[i];
+  // c A^-1: solve A^T x = c
+  {
+    ld At[16], x[4];
+    for (int i = 0; i < k; ++i)
+      for (int jj = 0; jj < k; ++jj) At[i * k + jj] = M.A[jj * k + i];
+    for (int i = 0; i < k; ++i) x[i] = M.c[i];
+    if (!solve(At, x, k)) return fail(VMF_EVALUE, "singular modal matrix");
+    ld e1 = 0;
+    for (int i = 0; i < k; ++i) {
+      p.ci[i] = (float)x[i];
+      e1 += x[i] * M.bv[i];
+    }
+    p.e1 = (float)e1;
+  }
+  p.b0 = (float)ip.b0;
+  p.sign = (float)ip.sign;
+  p.H = h;
+  p.W = w;
+  p.NB = (int)cdiv(h, kB32);
+  p.cpl = (p.NB + 31) / 32;
+  if (p.cpl > kMaxCpl32) return fail(VMF_EVALUE, "image too tall for the fp32 column pass");
+  // W(t) = A^t b, folded weights
+  ld Wt[kB32][4];
+  {
+    ld v[4], t[4];
+    for (int i = 0; i < k; ++i) v[i] = M.bv[i];
+    for (int tt = 0; tt < kB32; ++tt) {
+      for (int i = 0; i < k; ++i) Wt[tt][i] = v[i];
+      for (int i = 0; i < k; ++i) {
+        t[i] = 0;
+        for (int jj = 0; jj < k; ++jj) t[i] += M.A[i * k + jj] * v[jj];
+      }
+      memcpy(v, t, sizeof(ld) * k);
+    }
+  }
+  for (int i = 0; i < k; ++i)
+    for (int t = 0; t < kB32 / 2; ++t) {
+      p.SP[i][t] = (float)(0.5L * (Wt[t][i] + Wt[kB32 - 1 - t][i]));
+      p.SQ[i][t] = (float)(0.5L * (Wt[kB32 - 1 - t][i] - Wt[t][i]));
+    }
+  ld AL[16];
+  matpow(M.A, kB32, AL, k);
+  for (int i = 0; i < k * k; ++i) p.AL[i] = (double)AL[i];
+  for (int l = 0; l < 5; ++l) {
+    ld X[16];
+    matpow(AL, (int64_t)p.cpl << l, X, k);
+    for (int i = 0; i < k * k; ++i) p.ALp[l][i] = (double)X[i];
+  }
+  {
+    ld IA[16], y[4];
+    for (int i = 0; i < k; ++i) {
+      for (int jj = 0; jj < k; ++jj) IA[i * k + jj] = (i == jj ? 1 : 0) - M.A[i * k + jj];
+      y[i] = M.bv[i];
+    }
+    if (!solve(IA, y, k)) return fail(VMF_EVALUE, "pole on the unit circle");
+    for (int i = 0; i < k; ++i) p.Iss[i] = (double)y[i];
+  }
+  // boundary-correction weights h(m) = c A^(m-1) b until the tail is
+  // negligible (sum of |h| beyond Mh < 1e-9 of the total), at most H-1
+  {
+    std::vector<ld> hv(1, 0);
+    ld v[4], t[4], tot = 0;
+    for (int i = 0; i < k; ++i) v[i] = M.bv[i];
+    const int64_t mmax = h - 1 < kHm32Max ? h - 1 : kHm32Max;
+    for (int64_t m = 1; m <= mmax; ++m) {
+      ld hm = 0;
+      for (int i = 0; i < k; ++i) hm += M.c[i] * v[i];
+      hv.push_back(hm);
+      tot += fabsl(hm);
+      for (int i = 0; i < k; ++i) {
+        t[i] = 0;
+        for (int jj = 0; jj < k; ++jj) t[i] += M.A[i * k + jj] * v[jj];
+      }
+      memcpy(v, t, sizeof(ld) * k);
+    }
+    // the tail beyond what h() holds must be negligible too (else the
+    // caller keeps the fp64 pass)
+    if (mmax == kHm32Max) {
+      ld rest = 0;
+      for (int64_t m = kHm32Max + 1; m <= kHm32Max + 4096 && m < h; ++m) {
+        ld hm = 0;
+        for (int i = 0; i < k; ++i) hm += M.c[i] * v[i];
+        rest += fabsl(hm);
+        for (int i = 0; i < k; ++i) {
+          t[i] = 0;
+          for (int jj = 0; jj < k; ++jj) t[i] += M.A[i * k + jj] * v[jj];
+        }
+        memcpy(v, t, sizeof(ld) * k);
+      }
+      if (rest >= 1e-9L * tot) return fail(VMF_EVALUE, "impulse response too long for h()");
+    }
+    int64_t Mh = (int64_t)hv.size() - 1;
+    ld tail = 0;
+    while (Mh > 1 && tail + fabsl(hv[Mh]) < 1e-9L * tot) tail += fabsl(hv[Mh--]);
+    p.Mh = (int)Mh;
+    memset(&P->hm, 0, sizeof(P->hm));
+    for (int64_t m = 1; m <= Mh; ++m) P->hm.h[m] = (float)hv[m];
+  }
+  return VMF_OK;
+}
+
+template <int K, int KIND>
+static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Col32Plan &P,
+                    int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
+                    float *thr_dev, void *ws, cudaStream_t st) {
+  const Col32Params &p = P.p;
+  const int64_t h = p.H, w = p.W;
+  char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  CandState *cs = (CandState *)base;
+  char *q = base + 4096;
+  float *R = (float *)q;
+  q += ((size_t)p.NB * (2 * K + 2) * w * sizeof(float) + 255) & ~(size_t)255;
+  float *Cc = (float *)q;
+  q += (2 * w * sizeof(float) + 255) & ~(size_t)255;
+  const int64_t gcap = colpass_cand_capacity(h, w);
+  int *gy = (int *)q;
+  int *gx = gy + gcap;
+  float *gv = (float *)(gx + gcap);
+  {
+    Launch g(K_COL_CARRY, st);
+    CUtensorMap cmap;
+    memset(&cmap, 0, sizeof(cmap));
+    const int ctma = make_tmap_2d_f32(&cmap, T, h, w, ldt, kCarryStride, kCarryRows) &&
+                     !getenv("VMF_NO_TMA");
+    cudaGetLastError();
+    const int csm = kCarryRows * kCarryStride * (int)sizeof(float) + 128;
+    static PerDevice attr;
+    if (attr.first())
+      cudaFuncSetAttribute(colcarry32_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
+    launch_pdl(colcarry32_kernel<K>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
+               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs);
+  }
+  {
+    Launch g(K_COL_SCAN, st);
+    launch_pdl(colscan32_kernel<K>, dim3((unsigned)cdiv(w, kScan32Cols), 2),
+               dim3(32 * kScan32Cols), 0, st, T, ldt, p, R, Cc);
+  }
+  {
+    Launch g(K_IIR_COLS_FUSED, st);
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    const int use_tma = make_tmap_2d_f32(&tmap, T, h, w, ldt, kT32Stride, kT32Rows) &&
+                        !getenv("VMF_NO_TMA");
+    cudaGetLastError();
+    const int sm = (int)sizeof(Col32Smem) + 128;
+    static PerDevice attr;
+    if (attr.first()) {
+      cudaFuncSetAttribute(colapply32_kernel<K, KIND, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      cudaFuncSetAttribute(colapply32_kernel<K, KIND, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    }
+    auto kern = p.lsc == 1.0f ? colapply32_kernel<K, KIND, false> : colapply32_kernel<K, KIND, true>;
+    launch_pdl(kern, dim3((unsigned)cdiv(w, kC32Out), (unsigned)p.NB), dim3(kC32), sm, st, T, ldt,
+               L, ldl, p, (const float *)R, (const float *)Cc, cs, gy, gx, gv, (int)gcap, tmap,
+               use_tma, (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
+  }
+  if (p.frac > 0.0f)
+    colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, h, w, p.frac, det_yx, det_val, cap, n_det_dev,
+                    thr_dev, st);
+  return cuda_status("fp32 column pass");
+}
+
+static int get_plan32(int64_t h, int64_t w, const IirParams &ip, Col32Plan *out) {
+  static PlanCache<Col32Plan> cache;
+  std::vector<unsigned char> key;
+  key_add(key, h);
+  key_add(key, w);
+  key_add(key, ip.K);
+  key_add(key, ip.b0);
+  key_add(key, ip.sign);
+  key_add(key, ip.b, sizeof(double) * ip.K);
+  key_add(key, ip.a, sizeof(double) * ip.K);
+  if (cache.get(key, out)) return VMF_OK;
+  const int rc = plan32(out, h, w, ip);
+  if (rc) return rc;
+  cache.put(key, *out);
+  return VMF_OK;
+}
+
+bool colpass32_supported(int64_t h, int64_t w, const IirParams &ip) {
+  if (getenv("VMF_NO_COLPASS32") || h < 64 || w < 1 || cdiv(h, kB32) > 32 * kMaxCpl32) return false;
+  Modal M;
+  if (!modal_realise(ip.b, ip.a, ip.K, &M)) return false;
+  static Col32Plan tmp;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  return get_plan32(h, w, ip, &tmp) == VMF_OK;  // else the caller keeps the fp64 pass
+}
+
+int colpass32_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,
+                  int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
+                  float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  const size_t need = colpass32_workspace_bytes(h, w, ip.K);
+  if (!ws || ws_bytes < need)
+    return fail(VMF_EVALUE, "fp32 column-pass workspace too small: %zu < %zu bytes", ws_bytes,
+                need);
+  static Col32Plan run;  // (large: not on the stack)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  const int rc = get_plan32(h, w, ip, &run);
+  if (rc) return rc;
+  run.p.lsc = lap_scale;
+  run.p.frac = frac;
+  if (run.kind == M32_CPAIR)
+    return launch32<2, M32_CPAIR>(T, ldt, L, ldl, run, det_yx, det_val, cap, n_det_dev, thr_dev,
+                                  ws, st);
+  switch (ip.K) {
+    case 2: return launch32<2, M32_JORDAN>(T, ldt, L, ldl, run, det_yx, det_val, cap, n_det_dev,
+                                           thr_dev, ws, st);
+    case 3: return launch32<3, M32_JORDAN>(T, ldt, L, ldl, run, det_yx, det_val, cap, n_det_dev,
+                                           thr_dev, ws, st);
+    case 4: return launch32<4, M32_JORDAN>(T, ldt, L, ldl, run, det_yx, det_val, cap, n_det_dev,
+                                           thr_dev, ws, st);
+  }
+  return fail(VMF_EVALUE, "fp32 column pass supports K = 2..4, got %d", ip.K);
+}
+
+}  // namespace vmf
