@@ -7,6 +7,7 @@
 #include "vmf_common.cuh"
 #include "vmf_iir.cuh"
 #include "vmf_colpass.cuh"
+#include "vmf_rowlap.cuh"
 #include "vmf_firpass.cuh"
 
 namespace vmf {
@@ -320,7 +321,26 @@ size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage
     size_t c4 = firpass_workspace_bytes(h, w);
     if (c4 > carry) carry = c4;
   }
-  return 3 * img + align256(carry) + align256(detect_workspace_bytes(1, h, w)) + 256;
+  return 3 * img + align256(carry) + align256(detect_workspace_bytes(1, h, w)) + 256 +
+         align256(2 * (size_t)w * sizeof(float));  // the fp32 row pass's virtual rows
+}
+
+// The all-fp32 "Laplacian-first" path (vmf_rowlap.cu + vmf_colpass32.cu V
+// mode): fp32 frames with W = 32 C (C <= 256), 16-byte aligned rows, IIR row
+// and column stages with a modal fp32 realisation.
+static bool lapfirst_ok(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                        const vmf_stage *row, const vmf_stage *col, IirParams *ip) {
+  if (x_dtype != VMF_F32 || !row || !col || row->kind != VMF_STAGE_IIR ||
+      col->kind != VMF_STAGE_IIR || getenv("VMF_FORCE_GENERIC"))
+    return false;
+  if (((uintptr_t)x & 15) || ((ldx * 4) & 15)) return false;
+  if (!rowlap_supported(h, w, row->b_plus, row->a_plus, row->n, row->b_zero, row->sign))
+    return false;
+  if (iir_plan(ip, w, h, col->b_plus, col->a_plus, col->n, col->b_zero, col->sign)) {
+    cudaGetLastError();
+    return false;
+  }
+  return colpass32_supported(h, w, *ip);
 }
 
 int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
@@ -346,12 +366,40 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   p += img;
   float *L = lap_out ? lap_out : (float *)p;
   p += img;
+  const size_t vrows_b = align256(2 * (size_t)w * sizeof(float));
   size_t carry_b = align256(vmf_blur_lap_detect_workspace_bytes(h, w, row_stage, col_stage) -
-                            3 * img - align256(detect_workspace_bytes(1, h, w)) - 256);
+                            3 * img - align256(detect_workspace_bytes(1, h, w)) - 256 - vrows_b);
   void *carry = p;
   p += carry_b;
   void *dws = p;
   size_t dws_b = align256(detect_workspace_bytes(1, h, w));
+  p += dws_b;
+  float *vrows = (float *)p;
+  IirParams ipc;
+  if (lapfirst_ok(x, x_dtype, h, w, ldx, row_stage, col_stage, &ipc)) {
+    // V = R(Lap5 X) into T's slot, then the column pass in V mode
+    rc = rowlap_run((const float *)x, ldx, T, w, vrows, vrows + w, h, w, row_stage->b_plus,
+                    row_stage->a_plus, row_stage->n, row_stage->b_zero, row_stage->sign, st);
+    if (rc) return rc;
+    const Col32VMode vm = {(const float *)x, ldx, vrows, vrows + w, row_stage->b_plus,
+                           row_stage->a_plus, row_stage->n, row_stage->b_zero, row_stage->sign};
+    rc = colpass32_run(T, w, L, w, ipc, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
+                       thr_dev, carry, carry_b, st, &vm);
+    if (rc) return rc;
+    if (blur_out) {  // B on request: T into the (unused) B slot, then the column leaf
+      float *Tb = T + img / sizeof(float);
+      rc = run_stage<ROWS>(row_stage, x, x_dtype, Tb, h, w, ldx, w, carry, carry_b, st);
+      if (rc) return rc;
+      rc = run_stage<COLS>(col_stage, Tb, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);
+      if (rc) return rc;
+    }
+    if (n_det_host && frac > 0.0f) {
+      cudaMemcpyAsync(n_det_host, n_det_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      return cuda_status("detect readback");
+    }
+    return VMF_OK;
+  }
   rc = run_stage<ROWS>(row_stage, x, x_dtype, T, h, w, ldx, w, carry, carry_b, st);
   if (rc) return rc;
   if (fused_col(col_stage, h, w)) {

@@ -97,11 +97,23 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
 // path's column pass for IIR stages with a modal fp32 realisation (repeated
 // real pole, K = 2..4, or a complex pair, K = 2); L (* lap_scale) +
 // detections, no blur output.
+// V mode: the input is V = R(Lap5 X) from the fp32 row pass (vmf_rowlap.cu)
+// instead of T; x = the frame (border partials), vt / vb = its virtual rows,
+// (rb, ra, rk, rb0, rsign) = the ROW stage (the border rows are row-filtered).
+struct Col32VMode {
+  const float *x;
+  int64_t ldx;
+  const float *vt, *vb;
+  const double *rb, *ra;
+  int rk;
+  double rb0;
+  int rsign;
+};
 bool colpass32_supported(int64_t h, int64_t w, const IirParams &ip);
 size_t colpass32_workspace_bytes(int64_t h, int64_t w, int k);
 int colpass32_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,
                   int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
                   float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
-                  size_t ws_bytes, cudaStream_t st);
+                  size_t ws_bytes, cudaStream_t st, const Col32VMode *vmode = nullptr);
 
 }  // namespace vmf

@@ -29,8 +29,8 @@
 // zero-state end states of both directions of every (band, column) by folded
 // sample pairs, and band partials of the two boundary corrections; colscan32
 // turns them into the true start state of every band (fp64 arithmetic over
-// fp32 records, Kogge-Stone over bands with A^(64 cpl 2^j)) and sums the
-// corrections; colapply32 (128 columns x one band per CTA) walks up (the
+// fp32 records, sequential over the bands per column and direction) and
+// sums the corrections; colapply32 (128 columns x one band per CTA) walks up (the
 // backward part parked in registers) and down (L produced directly), then
 // stores the owned 124 x 64 block fused with the 3x3 NMS, exactly like the
 // fp64 pass.  L of the halo rows r0-1 / r1 (for the NMS) comes from the band
@@ -46,6 +46,8 @@
 #include "vmf_common.cuh"
 #include "vmf_prof.cuh"
 #include "vmf_tma.cuh"
+#include "vmf_modal32.cuh"
+#include "vmf_rowlap.cuh"
 
 namespace vmf {
 
@@ -58,12 +60,9 @@ constexpr int kL32Rows = kB32 + 2;       // U / L rows r0-1 .. r1
 constexpr int kCarryStride = kC32 + 8;   // carry tile: cols c0-4 .. c0+131
 constexpr int kCarryRows = kB32 + 2;     // T rows r0-1 .. r1
 constexpr int kCand32 = 256;             // per-CTA candidate buffer
-constexpr int kMaxCpl32 = 4;             // bands per lane in the scan (H <= 8192)
-constexpr int kScan32Cols = 8;
+constexpr int kMaxNB32 = 128;            // bands (H <= 8192: the scan's shared staging)
+constexpr int kScan32Cols = 32;
 constexpr int kHm32Max = 2048;           // boundary-correction weights h(1..Mh)
-
-// modal realisation: JORDAN (repeated real pole, K = 2..4) or CPAIR (K = 2)
-enum Modal32Kind { M32_JORDAN = 0, M32_CPAIR = 1 };
 
 struct Col32Params {
   float p, q;               // JORDAN: pole p; CPAIR: p + i q
@@ -72,11 +71,10 @@ struct Col32Params {
   float e1;                 // c A^-1 b
   float b0, sign, lsc, frac;
   float SP[4][kB32 / 2], SQ[4][kB32 / 2];  // folded band-carry weights
-  double ALp[5][16];        // A^(64 cpl 2^l), row-major K x K
-  double AL[16];            // A^64
+  double AL[16];            // A^64, row-major K x K
   double Iss[4];            // (I - A)^-1 b: steady state per unit input
   int64_t H, W;
-  int NB, cpl, K, Mh;       // bands; bands per scan lane; order; correction length
+  int NB, K, Mh;            // bands; order; boundary-correction length
 };
 
 // h(m) = c A^(m-1) b, m = 0..Mh (h(0) = 0): the boundary-correction weights,
@@ -84,43 +82,6 @@ struct Col32Params {
 struct Hm32 {
   float h[kHm32Max + 1];
 };
-
-// ---------------------------------------------------------------------------
-// the recursion: u <- A u + b x, y = c . u (before the update)
-// ---------------------------------------------------------------------------
-template <int K, int KIND>
-struct Rec32 {
-  float u[K];
-  __device__ __forceinline__ float out(const float *c) const {
-    float y = c[0] * u[0];
-#pragma unroll
-    for (int i = 1; i < K; ++i) y = fmaf(c[i], u[i], y);
-    return y;
-  }
-  __device__ __forceinline__ float out_from(const float *c, float acc) const {
-#pragma unroll
-    for (int i = 0; i < K; ++i) acc = fmaf(c[i], u[i], acc);
-    return acc;
-  }
-  __device__ __forceinline__ void step(const Col32Params &P, float x) {
-    if (KIND == M32_JORDAN) {
-      u[0] = fmaf(P.p, u[0], x);
-#pragma unroll
-      for (int i = 1; i < K; ++i) u[i] = fmaf(P.p, u[i], u[i - 1]);
-    } else {
-      const float ur = u[0], ui = u[1];
-      u[0] = fmaf(P.p, ur, fmaf(-P.q, ui, x));
-      u[1] = fmaf(P.q, ur, P.p * ui);
-    }
-  }
-};
-
-// U = ((l - c) + (r - c)) + ((u - c) + (d - c)): every term a difference of
-// neighbouring T values (rounding relative to the difference); the same
-// expression everywhere, so the carry and apply passes see bitwise-equal U.
-__device__ __forceinline__ float lap5(float l, float c, float r, float u, float d) {
-  return ((l - c) + (r - c)) + ((u - c) + (d - c));
-}
 
 // Band records, coalesced along columns: R[(b * (2K + 2) + q) * W + col]
 //   q < K: forward zero-state end state (-> forward start state uf(r0-1)),
@@ -136,11 +97,13 @@ __device__ __forceinline__ int64_t ridx(int b, int q, int K, int64_t W, int64_t 
 // One CTA = 128 columns x one band, 256 threads: threads j and j + 128 take the
 // two halves of the band's 32 sample pairs (t, 63 - t) of column j.  The tile
 // holds T rows r0-1 .. r1 (clamped), columns c0-4 .. c0+131 (clamped).
-template <int K>
+// VM: the input is V = R(Lap5 X) of the fp32 row pass (U = V itself, no
+// horizontal neighbours); the border partials then come from the frame X.
+template <int K, bool VM>
 __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
     const float *__restrict__ T, int64_t ldt, Col32Params p, float *__restrict__ R,
     const __grid_constant__ Hm32 hm, const __grid_constant__ CUtensorMap tmap, int use_tma,
-    CandState *__restrict__ cs) {
+    CandState *__restrict__ cs, const float *__restrict__ X, int64_t ldx) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
   float *tile = reinterpret_cast<float *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
@@ -176,7 +139,9 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
   // tile row of image row r: r - r0 + 1; tile column of column c0 + j: j + 4
   const float *tc = tile + j + 4;
 #define TT(tr, dc) tc[(tr) * kCarryStride + (dc)]
-  auto U = [&](int tr) { return lap5(TT(tr, -1), TT(tr, 0), TT(tr, 1), TT(tr - 1, 0), TT(tr + 1, 0)); };
+  auto U = [&](int tr) {
+    return VM ? TT(tr, 0) : lap5(TT(tr, -1), TT(tr, 0), TT(tr, 1), TT(tr - 1, 0), TT(tr + 1, 0));
+  };
   float P[K], Q[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0f;
@@ -208,7 +173,13 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
     for (int t = half * (kB32 / 2); t < (half + 1) * (kB32 / 2); ++t) {
       const int64_t r = r0 + t;
       if (r < 1 || r >= H) continue;
-      const float g = TT(t + 1, 0) - TT(t, 0);
+      float g;
+      if (VM) {  // G of the frame (clamped column)
+        const int64_t cc = col < W ? col : W - 1;
+        g = __ldg(X + r * ldx + cc) - __ldg(X + (r - 1) * ldx + cc);
+      } else {
+        g = TT(t + 1, 0) - TT(t, 0);
+      }
       if (top && r <= p.Mh) pt = fmaf(hm.h[r], g, pt);
       if (bot && H - r <= p.Mh) pb = fmaf(hm.h[H - r], g, pb);
     }
@@ -238,127 +209,107 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// 2. band scan.  CTA = one direction x 8 columns; warp = one column, lanes
-//    over bands (cpl each); fp64 arithmetic.  Writes the start state of every
-//    band over its zero-state carry, and (direction 0 / 1) the column's top /
-//    bottom boundary correction into Cc[dir][W].
+// 2. band scan.  CTA = 32 columns, both directions.  The records of its
+//    columns are staged in shared memory with coalesced 16-byte copies; then
+//    one thread per (column, direction) runs the band recursion
+//    u <- A^64 u + z sequentially in fp64 (64 bands: ~1.5k cycles of DFMA
+//    latency), writing each band's start state over its zero-state carry, and
+//    one thread per (column, correction) sums the boundary partials in band
+//    order; the start states go back with coalesced stores.
 // ---------------------------------------------------------------------------
-template <int K>
-__global__ void __launch_bounds__(32 * kScan32Cols) colscan32_kernel(
-    const float *__restrict__ T, int64_t ldt, Col32Params p, float *__restrict__ R,
-    float *__restrict__ Cc) {
-  const int NB = p.NB, cpl = p.cpl;
-  const int dir = blockIdx.y;
-  const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
-  const int64_t col = (int64_t)blockIdx.x * kScan32Cols + wc;
-  const bool live = col < p.W;
-  const int64_t cc = live ? col : p.W - 1;
+template <int K, bool VM>
+__global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict__ T, int64_t ldt,
+                                                       Col32Params p, float *__restrict__ R,
+                                                       float *__restrict__ Cc,
+                                                       const float *__restrict__ Vt,
+                                                       const float *__restrict__ Vb) {
+  extern __shared__ __align__(16) float ss[];  // [NB][2K+2][32]
+  constexpr int Q = 2 * K + 2;
+  const int NB = p.NB;
+  const int64_t W = p.W, H = p.H;
+  const int64_t c0 = (int64_t)blockIdx.x * kScan32Cols;
+  const int tid = threadIdx.x;
+  __shared__ float es[2][kScan32Cols];
   pdl_wait();  // records come from the band carries
-  // steady-state input before the first band: D20 T of row 0 (forward) or
-  // H-1 (backward), the same fp32 expression as U's horizontal part
-  const int64_t er = dir == 0 ? 0 : p.H - 1;
-  const int64_t cl = cc > 0 ? cc - 1 : 0, cr = cc + 1 < p.W ? cc + 1 : p.W - 1;
-  const float tl = __ldg(T + er * ldt + cl), tcv = __ldg(T + er * ldt + cc),
-              tr = __ldg(T + er * ldt + cr);
-  const double e = (double)((tl - tcv) + (tr - tcv));
-  // own bands: d = z (zero-state carries), position sp -> band b
-  double dl[kMaxCpl32][K];
-  double corr = 0.0;
-#pragma unroll
-  for (int q = 0; q < kMaxCpl32; ++q) {
-    const int sp = lane * cpl + q;
-    if (q < cpl && sp < NB) {
-      const int b = dir == 0 ? sp : NB - 1 - sp;
-#pragma unroll
-      for (int i = 0; i < K; ++i) dl[q][i] = (double)R[ridx(b, dir * K + i, K, p.W, cc)];
-      corr += (double)R[ridx(b, 2 * K + dir, K, p.W, cc)];
-      if (sp == 0) {  // + A^64 u_ss(e): the steady start enters with the first band
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          double a = 0.0;
-#pragma unroll
-          for (int m = 0; m < K; ++m) a = fma(p.AL[i * K + m], p.Iss[m] * e, a);
-          dl[q][i] += a;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < K; ++i) dl[q][i] = 0.0;
+  const bool full = c0 + kScan32Cols <= W && (W & 3) == 0;
+  if (full) {
+    for (int e = tid; e < NB * Q * (kScan32Cols / 4); e += blockDim.x) {
+      const int row = e / (kScan32Cols / 4), v = e - row * (kScan32Cols / 4);  // row = b Q + q
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(ss + row * kScan32Cols + 4 * v);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                   "l"(R + (int64_t)row * W + c0 + 4 * v));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  } else {
+    for (int e = tid; e < NB * Q * kScan32Cols; e += blockDim.x) {
+      const int row = e / kScan32Cols, c = e - row * kScan32Cols;
+      const int64_t col = c0 + c < W ? c0 + c : W - 1;
+      ss[e] = R[(int64_t)row * W + col];
     }
   }
+  if (tid < 2 * kScan32Cols && VM) {  // steady-state inputs: the row pass's virtual rows
+    const int dir = tid / kScan32Cols, c = tid - dir * kScan32Cols;
+    const int64_t cc = c0 + c < W ? c0 + c : W - 1;
+    es[dir][c] = dir == 0 ? Vt[cc] : Vb[cc];
+  } else if (tid < 2 * kScan32Cols) {  // steady-state inputs: D20 T of row 0 / H-1
+    const int dir = tid / kScan32Cols, c = tid - dir * kScan32Cols;
+    const int64_t cc = c0 + c < W ? c0 + c : W - 1;
+    const int64_t er = dir == 0 ? 0 : H - 1;
+    const int64_t cl = cc > 0 ? cc - 1 : 0, cr = cc + 1 < W ? cc + 1 : W - 1;
+    const float tl = __ldg(T + er * ldt + cl), tcv = __ldg(T + er * ldt + cc),
+                tr = __ldg(T + er * ldt + cr);
+    es[dir][c] = (tl - tcv) + (tr - tcv);
+  }
+  if (full) asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
   pdl_trigger();
-  // lane-local inclusive composition of its cpl bands, then Kogge-Stone
-  double A[K];
+  if (tid < 2 * kScan32Cols) {
+    const int dir = tid / kScan32Cols, c = tid - dir * kScan32Cols;
+    const double e = (double)es[dir][c];
+    double u[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) A[i] = 0.0;
-#pragma unroll
-  for (int q = 0; q < kMaxCpl32; ++q) {
-    if (q < cpl && lane * cpl + q < NB) {
-      double An[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        double a = dl[q][i];
-#pragma unroll
-        for (int m = 0; m < K; ++m) a = fma(p.AL[i * K + m], A[m], a);
-        An[i] = a;
-      }
-#pragma unroll
-      for (int i = 0; i < K; ++i) A[i] = An[i];
-    }
-  }
-#pragma unroll
-  for (int lv = 0; lv < 5; ++lv) {
-    const int o = 1 << lv;
-    double Bv[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) Bv[i] = __shfl_up_sync(0xffffffffu, A[i], o);
-    if (lane >= o) {
+    for (int i = 0; i < K; ++i) u[i] = p.Iss[i] * e;
+    for (int s = 0; s < NB; ++s) {
+      const int b = dir == 0 ? s : NB - 1 - s;
+      float *rec = ss + (b * Q + dir * K) * kScan32Cols + c;
+      double z[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        double a = A[i];
-#pragma unroll
-        for (int m = 0; m < K; ++m) a = fma(p.ALp[lv][i * K + m], Bv[m], a);
-        A[i] = a;
+        z[i] = (double)rec[i * kScan32Cols];
+        rec[i * kScan32Cols] = (float)u[i];  // start state of band b
       }
+      double un[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double a = z[i];
+#pragma unroll
+        for (int m = 0; m < K; ++m) a = fma(p.AL[i * K + m], u[m], a);
+        un[i] = a;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) u[i] = un[i];
     }
+  } else if (tid < 4 * kScan32Cols) {  // boundary corrections, band order
+    const int which = (tid - 2 * kScan32Cols) / kScan32Cols;
+    const int c = tid - (2 + which) * kScan32Cols;
+    double a = 0.0;
+    for (int b = 0; b < NB; ++b) a += (double)ss[(b * Q + 2 * K + which) * kScan32Cols + c];
+    if (c0 + c < W) Cc[(int64_t)which * W + c0 + c] = (float)a;
   }
-  // exclusive: the state entering this lane's first band
-  double E[K];
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const double v = __shfl_up_sync(0xffffffffu, A[i], 1);
-    E[i] = lane ? v : p.Iss[i] * e;
-  }
-  // column sum of the boundary-correction partials (fixed order)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) corr += __shfl_xor_sync(0xffffffffu, corr, o);
-  if (lane == 0 && live) Cc[(int64_t)dir * p.W + col] = (float)corr;
-#pragma unroll
-  for (int q = 0; q < kMaxCpl32; ++q) {
-    const int sp = lane * cpl + q;
-    if (q < cpl && sp < NB) {
-      const int b = dir == 0 ? sp : NB - 1 - sp;
-      if (live) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) R[ridx(b, dir * K + i, K, p.W, col)] = (float)E[i];
-      }
-      if (sp == 0) {
-        // E <- A^64 E_start + z: dl[0] already holds z + A^64 u_ss(e) = the
-        // inclusive state after the first band
-#pragma unroll
-        for (int i = 0; i < K; ++i) E[i] = dl[q][i];
-      } else {
-        double En[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          double a = dl[q][i];
-#pragma unroll
-          for (int m = 0; m < K; ++m) a = fma(p.AL[i * K + m], E[m], a);
-          En[i] = a;
-        }
-#pragma unroll
-        for (int i = 0; i < K; ++i) E[i] = En[i];
-      }
+  __syncthreads();
+  // start states back over the carries (q < 2K), coalesced
+  if (full) {
+    for (int e = tid; e < NB * 2 * K * (kScan32Cols / 4); e += blockDim.x) {
+      const int r2 = e / (kScan32Cols / 4), v = e - r2 * (kScan32Cols / 4);
+      const int b = r2 / (2 * K), q = r2 - b * 2 * K;
+      const float4 val = *reinterpret_cast<const float4 *>(ss + (b * Q + q) * kScan32Cols + 4 * v);
+      *reinterpret_cast<float4 *>(R + (int64_t)(b * Q + q) * W + c0 + 4 * v) = val;
+    }
+  } else {
+    for (int e = tid; e < NB * 2 * K * kScan32Cols; e += blockDim.x) {
+      const int r2 = e / kScan32Cols, c = e - r2 * kScan32Cols;
+      const int b = r2 / (2 * K), q = r2 - b * 2 * K;
+      if (c0 + c < W) R[(int64_t)(b * Q + q) * W + c0 + c] = ss[(b * Q + q) * kScan32Cols + c];
     }
   }
 }
@@ -377,10 +328,10 @@ struct Col32Smem {
 };
 
 // LSC: multiply by lap_scale (sigma^2 normalisation of the scale-space stack)
-template <int K, int KIND, bool LSC>
+template <int K, int KIND, bool LSC, bool VM>
 __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     const float *__restrict__ T, int64_t ldt, float *__restrict__ Lout, int64_t ldl,
-    Col32Params p, const float *__restrict__ R, const float *__restrict__ Cc,
+    Col32Params p, const float *__restrict__ R, const float *__restrict__ Cc, float ctop_mul,
     CandState *__restrict__ st, int *__restrict__ gy, int *__restrict__ gx,
     float *__restrict__ gv, int gcap, const __grid_constant__ CUtensorMap tmap, int use_tma,
     int vec_out) {
@@ -427,7 +378,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     rb.u[i] = R[ridx(b, K + i, K, W, colc)];
   }
   // boundary corrections of rows 0 and H-1 where this band computes them
-  const float ctop = r0 == 0 ? p.sign * Cc[colc] : 0.0f;
+  const float ctop = r0 == 0 ? ctop_mul * Cc[colc] : 0.0f;
   const float cbot = (H - 1 >= r0 - 1 && H - 1 <= r1) ? Cc[W + colc] : 0.0f;
   if (tma) {
     __syncthreads();  // barrier initialised before anyone waits on it
@@ -449,8 +400,9 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     // r = r1 (halo): y-(r1) = c A^-1 ub(r1) - e1 U(r1)
     {
       const float tu = tcol[(kB32 + 1) * kT32Stride];
-      const float u = lap5(tcol[(kB32 + 2) * kT32Stride - 1], tcv, tcol[(kB32 + 2) * kT32Stride + 1],
-                           tu, td);
+      const float u = VM ? tcv
+                         : lap5(tcol[(kB32 + 2) * kT32Stride - 1], tcv,
+                                tcol[(kB32 + 2) * kT32Stride + 1], tu, td);
       lcol[(kB32 + 1) * kT32Stride] = u;
       ym_below = fmaf(-p.e1, u, rb.out(p.ci));
       td = tcv;
@@ -459,7 +411,9 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
 #pragma unroll
     for (int t = kB32 - 1; t >= 0; --t) {  // rows r0 + t
       const float tu = tcol[(t + 1) * kT32Stride];
-      const float u = lap5(tcol[(t + 2) * kT32Stride - 1], tcv, tcol[(t + 2) * kT32Stride + 1], tu, td);
+      const float u = VM ? tcv
+                         : lap5(tcol[(t + 2) * kT32Stride - 1], tcv, tcol[(t + 2) * kT32Stride + 1],
+                                tu, td);
       lcol[(t + 1) * kT32Stride] = u;
       park[t] = rb.out(p.c);  // y-(r0 + t)
       rb.step(p, u);
@@ -469,7 +423,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     ym_above = rb.out(p.c);  // y-(r0 - 1)
     // U(r0 - 1) for the top halo row
     const float tu = tcol[0];
-    lcol[0] = lap5(tcol[kT32Stride - 1], tcv, tcol[kT32Stride + 1], tu, td);
+    lcol[0] = VM ? tcv : lap5(tcol[kT32Stride - 1], tcv, tcol[kT32Stride + 1], tu, td);
   }
 
   // ---- down: L of rows r0-1 .. r1 in place of U ----------------------------
@@ -599,148 +553,6 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
 // ---------------------------------------------------------------------------
 // host: modal realisation (long double), plan, launches
 // ---------------------------------------------------------------------------
-typedef long double ld;
-
-static void matmul(const ld *A, const ld *B, ld *C, int k) {
-  ld t[16];
-  for (int i = 0; i < k; ++i)
-    for (int j = 0; j < k; ++j) {
-      ld s = 0;
-      for (int m = 0; m < k; ++m) s += A[i * k + m] * B[m * k + j];
-      t[i * k + j] = s;
-    }
-  memcpy(C, t, sizeof(ld) * k * k);
-}
-
-static void matpow(const ld *A, int64_t n, ld *out, int k) {
-  ld R[16], P[16];
-  for (int i = 0; i < k * k; ++i) R[i] = (i % (k + 1) == 0) ? 1 : 0;
-  memcpy(P, A, sizeof(ld) * k * k);
-  while (n > 0) {
-    if (n & 1) matmul(R, P, R, k);
-    matmul(P, P, P, k);
-    n >>= 1;
-  }
-  memcpy(out, R, sizeof(ld) * k * k);
-}
-
-// solve M x = y (k <= 4), partial pivoting; false if singular
-static bool solve(ld *M, ld *y, int k) {
-  for (int c = 0; c < k; ++c) {
-    int piv = c;
-    for (int r = c + 1; r < k; ++r)
-      if (fabsl(M[r * k + c]) > fabsl(M[piv * k + c])) piv = r;
-    if (fabsl(M[piv * k + c]) < 1e-300L) return false;
-    if (piv != c) {
-      for (int m = 0; m < k; ++m) {
-        ld t = M[c * k + m];
-        M[c * k + m] = M[piv * k + m];
-        M[piv * k + m] = t;
-      }
-      ld t = y[c];
-      y[c] = y[piv];
-      y[piv] = t;
-    }
-    for (int r = 0; r < k; ++r) {
-      if (r == c) continue;
-      const ld f = M[r * k + c] / M[c * k + c];
-      for (int m = 0; m < k; ++m) M[r * k + m] -= f * M[c * k + m];
-      y[r] -= f * y[c];
-    }
-  }
-  for (int c = 0; c < k; ++c) y[c] /= M[c * k + c];
-  return true;
-}
-
-// Causal impulse response of the reference's DF-II recursion (engine.py:79-88)
-static void impulse_ref(const double *b, const double *a, int k, int n, ld *h) {
-  ld s[VMF_MAX_IIR_ORDER] = {0};
-  for (int t = 0; t < n; ++t) {
-    ld y = 0, w = (t == 0) ? 1 : 0;
-    for (int m = 0; m < k; ++m) {
-      y += (ld)b[m] * s[m];
-      w -= (ld)a[m] * s[m];
-    }
-    h[t] = y;
-    for (int m = k - 1; m > 0; --m) s[m] = s[m - 1];
-    s[0] = w;
-  }
-}
-
-struct Modal {
-  int kind, k;
-  ld p, q;
-  ld A[16], bv[4], c[4];
-};
-
-// repeated real pole (a_plus = coefficients of (1 - p w)^k) or, for k = 2, a
-// complex pair; the output vector c matches the first k impulse-response
-// samples and the whole response is verified against the reference's
-// recursion.
-static bool modal_realise(const double *b, const double *a, int k, Modal *M) {
-  if (k < 2 || k > 4) return false;
-  memset(M, 0, sizeof(*M));
-  M->k = k;
-  const ld p = -(ld)a[0] / k;
-  ld binom = 1, maxdev = 0, scale = 0;
-  for (int m = 1; m <= k; ++m) {
-    binom = binom * (k - m + 1) / m;
-    const ld coef = binom * powl(-p, m);
-    maxdev = fmaxl(maxdev, fabsl(coef - (ld)a[m - 1]));
-    scale = fmaxl(scale, fabsl((ld)a[m - 1]));
-  }
-  if (maxdev <= 1e-13L * scale && p > 0 && p < 1) {
-    M->kind = M32_JORDAN;
-    M->p = p;
-    for (int i = 0; i < k; ++i) {
-      M->bv[i] = 1;
-      for (int j2 = 0; j2 < k; ++j2) M->A[i * k + j2] = j2 <= i ? p : 0;
-    }
-  } else if (k == 2 && a[0] * a[0] - 4 * a[1] < 0) {
-    M->kind = M32_CPAIR;
-    M->p = -(ld)a[0] / 2;
-    M->q = sqrtl(4 * (ld)a[1] - (ld)a[0] * a[0]) / 2;
-    M->A[0] = M->p;
-    M->A[1] = -M->q;
-    M->A[2] = M->q;
-    M->A[3] = M->p;
-    M->bv[0] = 1;
-    M->bv[1] = 0;
-  } else {
-    return false;
-  }
-  ld h[256];
-  impulse_ref(b, a, k, 256, h);
-  ld Mx[16], y[4], v[4], t[4];
-  for (int i = 0; i < k; ++i) v[i] = M->bv[i];
-  for (int m = 0; m < k; ++m) {  // row m: (A^m b)^T, matched to h(m + 1)
-    for (int i = 0; i < k; ++i) Mx[m * k + i] = v[i];
-    y[m] = h[m + 1];
-    for (int i = 0; i < k; ++i) {
-      t[i] = 0;
-      for (int jj = 0; jj < k; ++jj) t[i] += M->A[i * k + jj] * v[jj];
-    }
-    memcpy(v, t, sizeof(ld) * k);
-  }
-  if (!solve(Mx, y, k)) return false;
-  for (int i = 0; i < k; ++i) M->c[i] = y[i];
-  // verify h(m) = c A^(m-1) b over 255 samples
-  ld hmax = 0, err = 0;
-  for (int i = 0; i < k; ++i) v[i] = M->bv[i];
-  for (int m = 1; m < 256; ++m) {
-    ld hm = 0;
-    for (int i = 0; i < k; ++i) hm += M->c[i] * v[i];
-    hmax = fmaxl(hmax, fabsl(h[m]));
-    err = fmaxl(err, fabsl(hm - h[m]));
-    for (int i = 0; i < k; ++i) {
-      t[i] = 0;
-      for (int jj = 0; jj < k; ++jj) t[i] += M->A[i * k + jj] * v[jj];
-    }
-    memcpy(v, t, sizeof(ld) * k);
-  }
-  return err <= 1e-12L * hmax;
-}
-
 struct Col32Plan {
   Col32Params p;
   Hm32 hm;
@@ -751,8 +563,8 @@ size_t colpass32_workspace_bytes(int64_t h, int64_t w, int k) {
   const int64_t NB = cdiv(h, kB32);
   const size_t rec = (size_t)NB * (2 * k + 2) * w * sizeof(float);
   const int64_t gcap = colpass_cand_capacity(h, w);
-  return 4096 + ((rec + 255) & ~(size_t)255) + ((2 * w * sizeof(float) + 255) & ~(size_t)255) +
-         (size_t)gcap * 12 + 1024;
+  return 4096 + ((rec + 255) & ~(size_t)255) +
+         2 * ((2 * w * sizeof(float) + 255) & ~(size_t)255) + (size_t)gcap * 12 + 1024;
 }
 
 static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
@@ -785,8 +597,7 @@ static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
   p.H = h;
   p.W = w;
   p.NB = (int)cdiv(h, kB32);
-  p.cpl = (p.NB + 31) / 32;
-  if (p.cpl > kMaxCpl32) return fail(VMF_EVALUE, "image too tall for the fp32 column pass");
+  if (p.NB > kMaxNB32) return fail(VMF_EVALUE, "image too tall for the fp32 column pass");
   // W(t) = A^t b, folded weights
   ld Wt[kB32][4];
   {
@@ -809,11 +620,7 @@ static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
   ld AL[16];
   matpow(M.A, kB32, AL, k);
   for (int i = 0; i < k * k; ++i) p.AL[i] = (double)AL[i];
-  for (int l = 0; l < 5; ++l) {
-    ld X[16];
-    matpow(AL, (int64_t)p.cpl << l, X, k);
-    for (int i = 0; i < k * k; ++i) p.ALp[l][i] = (double)X[i];
-  }
+
   {
     ld IA[16], y[4];
     for (int i = 0; i < k; ++i) {
@@ -867,10 +674,10 @@ static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
   return VMF_OK;
 }
 
-template <int K, int KIND>
+template <int K, int KIND, bool VM>
 static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Col32Plan &P,
-                    int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
-                    float *thr_dev, void *ws, cudaStream_t st) {
+                    const Col32VMode &vm, int32_t *det_yx, float *det_val, int64_t cap,
+                    int64_t *n_det_dev, float *thr_dev, void *ws, cudaStream_t st) {
   const Col32Params &p = P.p;
   const int64_t h = p.H, w = p.W;
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
@@ -879,6 +686,8 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
   float *R = (float *)q;
   q += ((size_t)p.NB * (2 * K + 2) * w * sizeof(float) + 255) & ~(size_t)255;
   float *Cc = (float *)q;
+  q += (2 * w * sizeof(float) + 255) & ~(size_t)255;
+  float *Ky = (float *)q;
   q += (2 * w * sizeof(float) + 255) & ~(size_t)255;
   const int64_t gcap = colpass_cand_capacity(h, w);
   int *gy = (int *)q;
@@ -894,14 +703,24 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     const int csm = kCarryRows * kCarryStride * (int)sizeof(float) + 128;
     static PerDevice attr;
     if (attr.first())
-      cudaFuncSetAttribute(colcarry32_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
-    launch_pdl(colcarry32_kernel<K>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
-               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs);
+      cudaFuncSetAttribute(colcarry32_kernel<K, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           csm);
+    launch_pdl(colcarry32_kernel<K, VM>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
+               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs, vm.x, vm.ldx);
   }
   {
     Launch g(K_COL_SCAN, st);
-    launch_pdl(colscan32_kernel<K>, dim3((unsigned)cdiv(w, kScan32Cols), 2),
-               dim3(32 * kScan32Cols), 0, st, T, ldt, p, R, Cc);
+    const int ssm = p.NB * (2 * K + 2) * kScan32Cols * (int)sizeof(float);
+    static PerDevice attr;
+    if (attr.first())
+      cudaFuncSetAttribute(colscan32_kernel<K, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+    launch_pdl(colscan32_kernel<K, VM>, dim3((unsigned)cdiv(w, kScan32Cols)), dim3(256), ssm, st,
+               T, ldt, p, R, Cc, vm.vt, vm.vb);
+  }
+  if (VM) {  // the column direction's border terms, row-filtered: Ky = R_ss(dy)
+    const int rc = rowfix_run(Cc, Ky, h, w, vm.rb, vm.ra, vm.rk, vm.rb0, vm.rsign, p.sign, st);
+    if (rc) return rc;
   }
   {
     Launch g(K_IIR_COLS_FUSED, st);
@@ -913,15 +732,19 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     const int sm = (int)sizeof(Col32Smem) + 128;
     static PerDevice attr;
     if (attr.first()) {
-      cudaFuncSetAttribute(colapply32_kernel<K, KIND, true>,
+      cudaFuncSetAttribute(colapply32_kernel<K, KIND, true, VM>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      cudaFuncSetAttribute(colapply32_kernel<K, KIND, false>,
+      cudaFuncSetAttribute(colapply32_kernel<K, KIND, false, VM>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     }
-    auto kern = p.lsc == 1.0f ? colapply32_kernel<K, KIND, false> : colapply32_kernel<K, KIND, true>;
+    auto kern = p.lsc == 1.0f ? colapply32_kernel<K, KIND, false, VM>
+                              : colapply32_kernel<K, KIND, true, VM>;
+    // border terms of rows 0 / H-1: T mode adds sign * Cc (T is row-filtered
+    // already); V mode adds the row-filtered Ky (sign inside)
     launch_pdl(kern, dim3((unsigned)cdiv(w, kC32Out), (unsigned)p.NB), dim3(kC32), sm, st, T, ldt,
-               L, ldl, p, (const float *)R, (const float *)Cc, cs, gy, gx, gv, (int)gcap, tmap,
-               use_tma, (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
+               L, ldl, p, (const float *)R, (const float *)(VM ? Ky : Cc), VM ? 1.0f : p.sign,
+               cs, gy, gx, gv, (int)gcap, tmap, use_tma,
+               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
   }
   if (p.frac > 0.0f)
     colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, h, w, p.frac, det_yx, det_val, cap, n_det_dev,
@@ -947,7 +770,7 @@ static int get_plan32(int64_t h, int64_t w, const IirParams &ip, Col32Plan *out)
 }
 
 bool colpass32_supported(int64_t h, int64_t w, const IirParams &ip) {
-  if (getenv("VMF_NO_COLPASS32") || h < 64 || w < 1 || cdiv(h, kB32) > 32 * kMaxCpl32) return false;
+  if (getenv("VMF_NO_COLPASS32") || h < 64 || w < 1 || cdiv(h, kB32) > kMaxNB32) return false;
   Modal M;
   if (!modal_realise(ip.b, ip.a, ip.K, &M)) return false;
   static Col32Plan tmp;
@@ -959,7 +782,7 @@ bool colpass32_supported(int64_t h, int64_t w, const IirParams &ip) {
 int colpass32_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirParams &ip,
                   int64_t h, int64_t w, float lap_scale, float frac, int32_t *det_yx,
                   float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
-                  size_t ws_bytes, cudaStream_t st) {
+                  size_t ws_bytes, cudaStream_t st, const Col32VMode *vmode) {
   const size_t need = colpass32_workspace_bytes(h, w, ip.K);
   if (!ws || ws_bytes < need)
     return fail(VMF_EVALUE, "fp32 column-pass workspace too small: %zu < %zu bytes", ws_bytes,
@@ -971,17 +794,20 @@ int colpass32_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirP
   if (rc) return rc;
   run.p.lsc = lap_scale;
   run.p.frac = frac;
-  if (run.kind == M32_CPAIR)
-    return launch32<2, M32_CPAIR>(T, ldt, L, ldl, run, det_yx, det_val, cap, n_det_dev, thr_dev,
-                                  ws, st);
+  const Col32VMode none = {};
+  const Col32VMode &vm = vmode ? *vmode : none;
+#define VMF_L32(KK, KD)                                                                        \
+  (vmode ? launch32<KK, KD, true>(T, ldt, L, ldl, run, vm, det_yx, det_val, cap, n_det_dev,   \
+                                  thr_dev, ws, st)                                             \
+         : launch32<KK, KD, false>(T, ldt, L, ldl, run, vm, det_yx, det_val, cap, n_det_dev,  \
+                                   thr_dev, ws, st))
+  if (run.kind == M32_CPAIR) return VMF_L32(2, M32_CPAIR);
   switch (ip.K) {
-    case 2: return launch32<2, M32_JORDAN>(T, ldt, L, ldl, run, det_yx, det_val, cap, n_det_dev,
-                                           thr_dev, ws, st);
-    case 3: return launch32<3, M32_JORDAN>(T, ldt, L, ldl, run, det_yx, det_val, cap, n_det_dev,
-                                           thr_dev, ws, st);
-    case 4: return launch32<4, M32_JORDAN>(T, ldt, L, ldl, run, det_yx, det_val, cap, n_det_dev,
-                                           thr_dev, ws, st);
+    case 2: return VMF_L32(2, M32_JORDAN);
+    case 3: return VMF_L32(3, M32_JORDAN);
+    case 4: return VMF_L32(4, M32_JORDAN);
   }
+#undef VMF_L32
   return fail(VMF_EVALUE, "fp32 column pass supports K = 2..4, got %d", ip.K);
 }
 

@@ -1,0 +1,620 @@
+// vmf_rowlap.cu -- the first pass of the fp32 "Laplacian-first" path:
+// V = R(U0), U0 = 5-point Laplacian of the input frame X, R the row filter
+// (iir_rows, engine.py:137-155 / kernel 65-102) in fp32 modal form.
+//
+// Why.  The reference computes T = R X, B = C T and L = Lap5_rep(B)
+// (engine.py:205-228, blob.py:161).  On the replicate-extended frame the three
+// operators commute, so L = C R Lap5(X_ext) plus four border terms
+// (tools/experiments/lapfirst_2d.py derives and checks them):
+//   * left / right of the image Lap5(X_ext) is D02 X of column 0 / W-1,
+//     constant along the row: the steady-state starts eL(r), eR(r) of R;
+//   * above / below it is D20 X of row 0 / H-1 (zero past the columns):
+//     the column pass starts from Vt = R0(D20 X(0, .)) / Vb (zero starts);
+//   * L(r, 0) += C[dxl](r), dxl(r) = s sum_m h(m) (X(r, m) - X(r, m-1)) and
+//     L(r, W-1) -= C[dxr](r): folded into V(r, 0) / V(r, W-1) (C is linear);
+//   * L(0, c) += R[dyt](c), L(H-1, c) -= R[dyb](c): column sums of X's first
+//     differences (the column carry pass), row-filtered by rowfix_kernel.
+// Every quantity is then a Laplacian-size difference, so fp32 rounding is
+// relative to |L| and the modal recursion (vmf_modal32.cuh) runs in fp32:
+// the prototype's error is 1e-6 of max|L|, below the fp64 path's 3e-6..1e-5
+// (which rounds T to fp32), at every config scale.
+//
+// Kernel: persistent CTAs own contiguous rows; thread = 32-sample chunk of
+// the row (W = 32 C, C <= 256).  Input rows arrive by TMA (128-byte
+// swizzled [C][32] boxes) into a ring of 4 buffers (rows r-1, r, r+1 and the
+// prefetch of r+2); per row: U0 in registers, zero-state chunk carries by
+// folded pairs, a Kogge-Stone chunk scan per direction (one warp each), the
+// backward walk parked in registers, the forward walk writing V into one of
+// two output buffers that leave by TMA store.
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "plan_cache.hpp"
+#include "vmf_common.cuh"
+#include "vmf_modal32.cuh"
+#include "vmf_prof.cuh"
+#include "vmf_rowlap.cuh"
+#include "vmf_tma.cuh"
+
+namespace vmf {
+
+constexpr int kRChunk = 32;
+constexpr int kRLMaxC = 256;   // W <= 8192
+constexpr int kRLBufs = 4;     // input ring
+constexpr int kRLOut = 2;      // output ring
+
+// TMA SWIZZLE_128B layout of a [C][32] fp32 row (see vmf_rowpass.cu)
+struct SwzRow32 {
+  char *base;
+  __device__ __forceinline__ int off(int c, int q) const { return c * 128 + ((q ^ (c & 7)) << 4); }
+  __device__ __forceinline__ float4 ld4(int c, int q) const {
+    return *reinterpret_cast<const float4 *>(base + off(c, q));
+  }
+  __device__ __forceinline__ void st4(int c, int q, float4 v) const {
+    *reinterpret_cast<float4 *>(base + off(c, q)) = v;
+  }
+  __device__ __forceinline__ float ld(int n) const {
+    return *reinterpret_cast<const float *>(base + off(n >> 5, (n >> 2) & 7) + 4 * (n & 3));
+  }
+};
+
+__device__ __forceinline__ int hidx(int n) { return n + (n >> 5); }  // padded h() copy
+
+// One row through R: U (registers, this thread's chunk) -> V (registers).
+// eL / eR: steady-state inputs left / right of the row; cf / cb: [C][K]
+// scratch; dx[2]: the row's border terms (added to V(0) / subtracted from
+// V(W-1)) -- published in smem by the caller before the first barrier.
+// Contains two block barriers.
+template <int K, int KIND>
+__device__ __forceinline__ void row_filter(const RowLapParams &p, const float (&U)[kRChunk],
+                                           float (&V)[kRChunk], float *cf, float *cb,
+                                           const float *e2, const float *dx2) {
+  const int c = threadIdx.x, C = p.C, lane = c & 31, warp = c >> 5;
+  // zero-state chunk carries: forward end state P + Q, backward start P - Q
+  {
+    float P[K], Q[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0f;
+#pragma unroll
+    for (int t = 0; t < kRChunk / 2; ++t) {
+      const float s = U[t] + U[kRChunk - 1 - t], d = U[t] - U[kRChunk - 1 - t];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        P[i] = fmaf(p.SP[i][t], s, P[i]);
+        Q[i] = fmaf(p.SQ[i][t], d, Q[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      cf[c * K + i] = P[i] + Q[i];
+      cb[c * K + i] = P[i] - Q[i];
+    }
+  }
+  __syncthreads();
+  // chunk scans: task 0 forward (chunks 0..C-1), task 1 backward
+  for (int task = warp; task < 2; task += (int)(blockDim.x >> 5)) {
+    float *cc = task == 0 ? cf : cb;
+    const int cpl = p.cpl;
+    const float e = e2[task];
+    float A[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) A[i] = 0.0f;
+    for (int q = 0; q < cpl; ++q) {
+      const int sp = lane * cpl + q;
+      if (sp >= C) break;
+      const int ch = task == 0 ? sp : C - 1 - sp;
+      float d[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) d[i] = cc[ch * K + i];
+      if (sp == 0) {  // + A^32 u_ss(e): the steady start enters with the first chunk
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int m = 0; m < K; ++m) d[i] = fmaf(p.A32[i * K + m], p.Iss[m] * e, d[i]);
+      }
+      float An[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        float a = d[i];
+#pragma unroll
+        for (int m = 0; m < K; ++m) a = fmaf(p.A32[i * K + m], A[m], a);
+        An[i] = a;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) A[i] = An[i];
+    }
+#pragma unroll
+    for (int lv = 0; lv < 5; ++lv) {
+      const int o = 1 << lv;
+      float Bv[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) Bv[i] = __shfl_up_sync(0xffffffffu, A[i], o);
+      if (lane >= o) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          float a = A[i];
+#pragma unroll
+          for (int m = 0; m < K; ++m) a = fmaf(p.Apow[lv][i * K + m], Bv[m], a);
+          A[i] = a;
+        }
+      }
+    }
+    float E[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const float v = __shfl_up_sync(0xffffffffu, A[i], 1);
+      E[i] = lane ? v : p.Iss[i] * e;
+    }
+    // each chunk's start state over its carry
+    for (int q = 0; q < cpl; ++q) {
+      const int sp = lane * cpl + q;
+      if (sp >= C) break;
+      const int ch = task == 0 ? sp : C - 1 - sp;
+      float d[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        d[i] = cc[ch * K + i];
+        cc[ch * K + i] = E[i];
+      }
+      if (sp == 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int m = 0; m < K; ++m) d[i] = fmaf(p.A32[i * K + m], p.Iss[m] * e, d[i]);
+      }
+      float En[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        float a = d[i];
+#pragma unroll
+        for (int m = 0; m < K; ++m) a = fmaf(p.A32[i * K + m], E[m], a);
+        En[i] = a;
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) E[i] = En[i];
+    }
+  }
+  __syncthreads();
+  // walks: backward parked (b0 U + s y-), forward adds y+
+  float park[kRChunk];
+  {
+    Rec32<K, KIND> rb;
+#pragma unroll
+    for (int i = 0; i < K; ++i) rb.u[i] = cb[c * K + i];
+#pragma unroll
+    for (int t = kRChunk - 1; t >= 0; --t) {
+      park[t] = rb.out_from(p.cs, p.b0 * U[t]);
+      rb.step(p, U[t]);
+    }
+  }
+  {
+    Rec32<K, KIND> rf;
+#pragma unroll
+    for (int i = 0; i < K; ++i) rf.u[i] = cf[c * K + i];
+#pragma unroll
+    for (int t = 0; t < kRChunk; ++t) {
+      V[t] = rf.out_from(p.c, park[t]);
+      rf.step(p, U[t]);
+    }
+  }
+  if (c == 0) V[0] += dx2[0];
+  if (c == C - 1) V[kRChunk - 1] -= dx2[1];
+}
+
+// Border-term partials of this thread's chunk: sum over its samples n >= 1
+// of h(n) G(n) (n <= Mh) and h(W - n) G(n) (W - n <= Mh), G(n) = X(n) - X(n-1),
+// reduced over the CTA in a fixed order into red[0..nwarp) / red[8..).
+__device__ __forceinline__ void dx_partials(const RowLapParams &p, const float *hs,
+                                            const float (&X)[kRChunk], float xl, float *red) {
+  const int c = threadIdx.x, lane = c & 31, warp = c >> 5;
+  const int n0 = c * kRChunk;
+  const int W = (int)p.W, Mh = p.Mh;
+  float pl = 0.0f, pr = 0.0f;
+  if (n0 <= Mh || n0 + kRChunk - 1 >= W - Mh) {
+#pragma unroll
+    for (int t = 0; t < kRChunk; ++t) {
+      const int n = n0 + t;
+      const float g = X[t] - (t ? X[t - 1] : xl);
+      if (n >= 1 && n <= Mh) pl = fmaf(hs[hidx(n)], g, pl);
+      if (n >= 1 && W - n <= Mh) pr = fmaf(hs[hidx(W - n)], g, pr);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pl += __shfl_xor_sync(0xffffffffu, pl, o);
+    pr += __shfl_xor_sync(0xffffffffu, pr, o);
+  }
+  if (lane == 0) {
+    red[warp] = pl;
+    red[8 + warp] = pr;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the row pass
+// ---------------------------------------------------------------------------
+template <int K, int KIND>
+__global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
+    const __grid_constant__ RowLapParams p, const __grid_constant__ HmRow hm,
+    float *__restrict__ Vt, float *__restrict__ Vb) {
+  extern __shared__ __align__(1024) unsigned char smem_rl[];
+  __shared__ __align__(8) uint64_t bar[kRLBufs];
+  __shared__ float red[16], e2[2], dx2[2];
+  const int C = p.C, c = threadIdx.x, nwarp = (int)(blockDim.x >> 5);
+  const int rowb = C * 128;
+  const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_rl);
+  char *xbuf = reinterpret_cast<char *>(smem_rl) + ((1024u - (sb & 1023u)) & 1023u);
+  char *obuf = xbuf + kRLBufs * rowb;
+  float *cf = reinterpret_cast<float *>(obuf + kRLOut * rowb);
+  float *cb = cf + C * K;
+  float *hs = cb + C * K;  // h(0..Mh), padded one per 32
+  const int64_t H = p.H;
+  const int W = (int)p.W;
+  const int64_t rlo = (int64_t)blockIdx.x * p.rows_per;
+  const int64_t rhi = rlo + p.rows_per < H ? rlo + p.rows_per : H;
+  if (rlo >= rhi) return;
+  const int nrows = (int)(rhi - rlo);
+  // logical input row j = clamp(rlo - 1 + j), j = 0 .. nrows + 1, in slot j % 4
+  auto issue = [&](int j) {
+    int64_t r = rlo - 1 + j;
+    r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+    const int s = j % kRLBufs;
+    mbar_expect_tx(&bar[s], (unsigned)rowb);
+    tma_load_3d_hint(xbuf + s * rowb, &xmap, &bar[s], 0, 0, (int)r, l2_policy_evict_first());
+  };
+  if (c == 0) {
+    for (int s = 0; s < kRLBufs; ++s) mbar_init(&bar[s], 1);
+    for (int j = 0; j < 3 && j <= nrows + 1; ++j) issue(j);
+  }
+  for (int n = c; n <= p.Mh; n += blockDim.x) hs[hidx(n)] = hm.h[n];
+  __syncthreads();
+  auto wait_row = [&](int j) { mbar_wait(&bar[j % kRLBufs], (unsigned)((j / kRLBufs) & 1)); };
+  wait_row(0);
+  wait_row(1);
+
+  float U[kRChunk], V[kRChunk], X[kRChunk];
+  auto load_chunk = [&](int j, float (&o)[kRChunk]) {
+    const SwzRow32 r{xbuf + (j % kRLBufs) * rowb};
+#pragma unroll
+    for (int q = 0; q < kRChunk / 4; ++q) {
+      const float4 v = r.ld4(c, q);
+      o[4 * q] = v.x;
+      o[4 * q + 1] = v.y;
+      o[4 * q + 2] = v.z;
+      o[4 * q + 3] = v.w;
+    }
+  };
+  auto halos = [&](int j, const float (&x)[kRChunk], float &xl, float &xr) {
+    const SwzRow32 r{xbuf + (j % kRLBufs) * rowb};
+    xl = c > 0 ? r.ld(c * kRChunk - 1) : x[0];
+    xr = c < C - 1 ? r.ld(c * kRChunk + kRChunk) : x[kRChunk - 1];
+  };
+  // a virtual row above / below the image: Vt / Vb = R0(D20 X) of row 0 /
+  // H-1 (zero starts), with that row's border terms
+  auto virtual_row = [&](int j, float *dst) {
+    float xl, xr;
+    load_chunk(j, X);
+    halos(j, X, xl, xr);
+#pragma unroll
+    for (int t = 0; t < kRChunk; ++t) {
+      const float l = t ? X[t - 1] : xl, r = t < kRChunk - 1 ? X[t + 1] : xr;
+      U[t] = (l - X[t]) + (r - X[t]);
+    }
+    dx_partials(p, hs, X, xl, red);
+    if (c == 0) e2[0] = e2[1] = 0.0f;
+    __syncthreads();
+    if (c == 0) {
+      float a = 0.0f, b = 0.0f;
+      for (int w = 0; w < nwarp; ++w) {
+        a += red[w];
+        b += red[8 + w];
+      }
+      dx2[0] = p.sign * a;
+      dx2[1] = b;
+    }
+    row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
+#pragma unroll
+    for (int q = 0; q < kRChunk / 4; ++q)
+      *reinterpret_cast<float4 *>(dst + c * kRChunk + 4 * q) =
+          make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]);
+    __syncthreads();
+  };
+  if (rlo == 0) virtual_row(1, Vt);
+
+  for (int i = 0; i < nrows; ++i) {
+    const int64_t r = rlo + i;
+    // rows r-1, r, r+1 are logical rows i, i+1, i+2
+    wait_row(i + 2 <= nrows + 1 ? i + 2 : nrows + 1);
+    float xl, xr;
+    load_chunk(i + 1, X);
+    halos(i + 1, X, xl, xr);
+    {
+      float Xu[kRChunk];
+      load_chunk(i, Xu);
+#pragma unroll
+      for (int t = 0; t < kRChunk; ++t) U[t] = Xu[t] - X[t];
+      load_chunk(i + 2, Xu);
+#pragma unroll
+      for (int t = 0; t < kRChunk; ++t) {
+        const float l = t ? X[t - 1] : xl, rr = t < kRChunk - 1 ? X[t + 1] : xr;
+        U[t] = ((l - X[t]) + (rr - X[t])) + (U[t] + (Xu[t] - X[t]));
+      }
+    }
+    dx_partials(p, hs, X, xl, red);
+    if (c == 0 || c == C - 1) {  // D02 X of the end samples: the steady starts
+      const SwzRow32 ru{xbuf + (i % kRLBufs) * rowb}, rd{xbuf + ((i + 2) % kRLBufs) * rowb};
+      const int n = c == 0 ? 0 : W - 1;
+      const float xc = X[c == 0 ? 0 : kRChunk - 1];
+      e2[c == 0 ? 0 : 1] = (ru.ld(n) - xc) + (rd.ld(n) - xc);
+    }
+    if (c == 0) {
+      // the output buffer this row fills was stored two rows ago: drained?
+      asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(kRLOut - 1) : "memory");
+    }
+    __syncthreads();  // X slots of this row read; e2 / red published; obuf free
+    if (c == 0) {
+      if (i + 3 <= nrows + 1) issue(i + 3);  // into the slot of row r-2 (free)
+      float a = 0.0f, b = 0.0f;
+      for (int w = 0; w < nwarp; ++w) {
+        a += red[w];
+        b += red[8 + w];
+      }
+      dx2[0] = p.sign * a;
+      dx2[1] = b;
+    }
+    row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
+    const SwzRow32 ob{obuf + (i % kRLOut) * rowb};
+#pragma unroll
+    for (int q = 0; q < kRChunk / 4; ++q)
+      ob.st4(c, q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]));
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
+    __syncthreads();
+    if (c == 0) {
+      if (i == 0) pdl_wait();  // V may still be read by the previous scale's column pass
+      tma_store_3d_hint(&vmap, obuf + (i % kRLOut) * rowb, 0, 0, (int)r, l2_policy_evict_last());
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  }
+  if (rhi == H) virtual_row(nrows, Vb);
+  pdl_trigger();
+  if (c == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// rowfix: ky = R_ss(dy) for the top (CTA 0) and bottom (CTA 1) border terms
+// of the column direction: dy = s_C * (column sums of h_C(m) G(m)) from the
+// column scan; steady starts at the row's own end values (replicate).
+// ---------------------------------------------------------------------------
+template <int K, int KIND>
+__global__ void __launch_bounds__(kRLMaxC) rowfix_kernel(const __grid_constant__ RowLapParams p,
+                                                         const float *__restrict__ Cc, float sc,
+                                                         float *__restrict__ Ky) {
+  __shared__ float cf[kRLMaxC * 4], cb[kRLMaxC * 4];
+  __shared__ float e2[2], dx2[2];
+  const int c = threadIdx.x, W = (int)p.W;
+  pdl_wait();  // the column sums come from the column scan
+  const float *dy = Cc + (int64_t)blockIdx.x * W;
+  const float s = blockIdx.x == 0 ? sc : 1.0f;  // dyt carries the column stage's sign
+  float U[kRChunk], V[kRChunk];
+#pragma unroll
+  for (int t = 0; t < kRChunk; ++t) U[t] = s * dy[c * kRChunk + t];
+  if (c == 0) {
+    e2[0] = s * dy[0];
+    e2[1] = s * dy[W - 1];
+    dx2[0] = dx2[1] = 0.0f;
+  }
+  pdl_trigger();
+  __syncthreads();
+  row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
+#pragma unroll
+  for (int t = 0; t < kRChunk; ++t) Ky[(int64_t)blockIdx.x * W + c * kRChunk + t] = V[t];
+}
+
+// ---------------------------------------------------------------------------
+// host
+// ---------------------------------------------------------------------------
+static int rl_plan(RowLapPlan *P, int64_t h, int64_t w, const double *b, const double *a, int k,
+                   double b0, int sign) {
+  Modal M;
+  if (!modal_realise(b, a, k, &M)) return fail(VMF_EVALUE, "no modal realisation");
+  RowLapParams &p = P->p;
+  memset(&p, 0, sizeof(p));
+  P->kind = M.kind;
+  p.K = k;
+  p.p = (float)M.p;
+  p.q = (float)M.q;
+  for (int i = 0; i < k; ++i) {
+    p.c[i] = (float)M.c[i];
+    p.cs[i] = (float)(sign * M.c[i]);
+  }
+  p.b0 = (float)b0;
+  p.sign = (float)sign;
+  p.H = h;
+  p.W = w;
+  p.C = (int)(w / kRChunk);
+  p.cpl = (p.C + 31) / 32;
+  ld Wt[kRChunk][4];
+  {
+    ld v[4], t[4];
+    for (int i = 0; i < k; ++i) v[i] = M.bv[i];
+    for (int tt = 0; tt < kRChunk; ++tt) {
+      for (int i = 0; i < k; ++i) Wt[tt][i] = v[i];
+      for (int i = 0; i < k; ++i) {
+        t[i] = 0;
+        for (int jj = 0; jj < k; ++jj) t[i] += M.A[i * k + jj] * v[jj];
+      }
+      memcpy(v, t, sizeof(ld) * k);
+    }
+  }
+  for (int i = 0; i < k; ++i)
+    for (int t = 0; t < kRChunk / 2; ++t) {
+      p.SP[i][t] = (float)(0.5L * (Wt[t][i] + Wt[kRChunk - 1 - t][i]));
+      p.SQ[i][t] = (float)(0.5L * (Wt[kRChunk - 1 - t][i] - Wt[t][i]));
+    }
+  ld A32[16];
+  matpow(M.A, kRChunk, A32, k);
+  for (int i = 0; i < k * k; ++i) p.A32[i] = (float)A32[i];
+  for (int l = 0; l < 5; ++l) {
+    ld X[16];
+    matpow(A32, (int64_t)p.cpl << l, X, k);
+    for (int i = 0; i < k * k; ++i) p.Apow[l][i] = (float)X[i];
+  }
+  {
+    ld IA[16], y[4];
+    for (int i = 0; i < k; ++i) {
+      for (int jj = 0; jj < k; ++jj) IA[i * k + jj] = (i == jj ? 1 : 0) - M.A[i * k + jj];
+      y[i] = M.bv[i];
+    }
+    if (!solve(IA, y, k)) return fail(VMF_EVALUE, "pole on the unit circle");
+    for (int i = 0; i < k; ++i) p.Iss[i] = (float)y[i];
+  }
+  // border weights h(1..Mh) along the row (tail below 1e-9 of sum |h|)
+  {
+    std::vector<ld> hv(1, 0);
+    ld v[4], t[4], tot = 0;
+    for (int i = 0; i < k; ++i) v[i] = M.bv[i];
+    const int64_t mmax = w - 1 < kHmRowMax ? w - 1 : kHmRowMax;
+    for (int64_t m = 1; m <= mmax; ++m) {
+      ld hmv = 0;
+      for (int i = 0; i < k; ++i) hmv += M.c[i] * v[i];
+      hv.push_back(hmv);
+      tot += fabsl(hmv);
+      for (int i = 0; i < k; ++i) {
+        t[i] = 0;
+        for (int jj = 0; jj < k; ++jj) t[i] += M.A[i * k + jj] * v[jj];
+      }
+      memcpy(v, t, sizeof(ld) * k);
+    }
+    if (mmax == kHmRowMax && w - 1 > kHmRowMax) {
+      ld rest = 0;
+      for (int64_t m = kHmRowMax + 1; m < w && m <= kHmRowMax + 4096; ++m) {
+        ld hmv = 0;
+        for (int i = 0; i < k; ++i) hmv += M.c[i] * v[i];
+        rest += fabsl(hmv);
+        for (int i = 0; i < k; ++i) {
+          t[i] = 0;
+          for (int jj = 0; jj < k; ++jj) t[i] += M.A[i * k + jj] * v[jj];
+        }
+        memcpy(v, t, sizeof(ld) * k);
+      }
+      if (rest >= 1e-9L * tot) return fail(VMF_EVALUE, "impulse response too long for h()");
+    }
+    int64_t Mh = (int64_t)hv.size() - 1;
+    ld tail = 0;
+    while (Mh > 1 && tail + fabsl(hv[Mh]) < 1e-9L * tot) tail += fabsl(hv[Mh--]);
+    p.Mh = (int)Mh;
+    memset(&P->hm, 0, sizeof(P->hm));
+    for (int64_t m = 1; m <= Mh; ++m) P->hm.h[m] = (float)hv[m];
+  }
+  return VMF_OK;
+}
+
+int rowlap_get_plan(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
+                    int sign, RowLapPlan *out) {
+  static PlanCache<RowLapPlan> cache;
+  std::vector<unsigned char> key;
+  key_add(key, h);
+  key_add(key, w);
+  key_add(key, k);
+  key_add(key, b0);
+  key_add(key, sign);
+  key_add(key, b, sizeof(double) * k);
+  key_add(key, a, sizeof(double) * k);
+  if (cache.get(key, out)) return VMF_OK;
+  const int rc = rl_plan(out, h, w, b, a, k, b0, sign);
+  if (rc) return rc;
+  cache.put(key, *out);
+  return VMF_OK;
+}
+
+bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
+                      int sign) {
+  if (getenv("VMF_NO_ROWLAP") || h < 2 || w < 64 || w % kRChunk || w / kRChunk > kRLMaxC)
+    return false;
+  static RowLapPlan tmp;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  return rowlap_get_plan(h, w, b, a, k, b0, sign, &tmp) == VMF_OK;
+}
+
+static size_t rl_smem(int C, int k) {
+  return 1024 + (size_t)(kRLBufs + kRLOut) * C * 128 + 2 * (size_t)C * k * sizeof(float) +
+         (size_t)(kHmRowMax + 1 + kHmRowMax / 32 + 2) * sizeof(float);
+}
+
+template <int K, int KIND>
+static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, float *Vt, float *Vb,
+                         RowLapPlan &P, cudaStream_t st) {
+  RowLapParams &p = P.p;
+  CUtensorMap xm, vm;
+  memset(&xm, 0, sizeof(xm));
+  memset(&vm, 0, sizeof(vm));
+  if (!make_tmap_rows_swz_f32(&xm, x, p.H, p.W, ldx, 1) ||
+      !make_tmap_rows_swz_f32(&vm, V, p.H, p.W, ldv, 1)) {
+    cudaGetLastError();
+    return fail(VMF_EVALUE, "row pass: TMA descriptors unavailable");
+  }
+  const size_t smem = rl_smem(p.C, K);
+  static std::map<std::pair<int, size_t>, int> slot_cache;
+  const int dev = current_device();
+  int &slots = slot_cache[std::make_pair(dev, smem)];
+  if (!slots) {
+    cudaFuncSetAttribute(rowlap_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    int occ = 0, nsm = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, p.C, smem);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    slots = (occ > 0 ? occ : 1) * nsm;
+  }
+  p.rows_per = (int)cdiv(p.H, slots);
+  const int grid = (int)cdiv(p.H, p.rows_per);
+  Launch g(K_IIR_ROWS_FUSED, st);
+  launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(p.C), smem, st, xm, vm, p, P.hm, Vt, Vb);
+  return cuda_status("fp32 row pass");
+}
+
+int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *Vt, float *Vb,
+               int64_t h, int64_t w, const double *b, const double *a, int k, double b0, int sign,
+               cudaStream_t st) {
+  static RowLapPlan P;  // (large: not on the stack)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  int rc = rowlap_get_plan(h, w, b, a, k, b0, sign, &P);
+  if (rc) return rc;
+  if (P.kind == M32_CPAIR) return launch_rowlap<2, M32_CPAIR>(x, ldx, V, ldv, Vt, Vb, P, st);
+  switch (k) {
+    case 2: return launch_rowlap<2, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, st);
+    case 3: return launch_rowlap<3, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, st);
+    case 4: return launch_rowlap<4, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, st);
+  }
+  return fail(VMF_EVALUE, "fp32 row pass supports K = 2..4, got %d", k);
+}
+
+int rowfix_run(const float *Cc, float *Ky, int64_t h, int64_t w, const double *b,
+               const double *a, int k, double b0, int sign, float col_sign, cudaStream_t st) {
+  static RowLapPlan P;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  int rc = rowlap_get_plan(h, w, b, a, k, b0, sign, &P);
+  if (rc) return rc;
+  Launch g(K_COL_SCAN, st);
+  auto go = [&](auto kern) {
+    launch_pdl(kern, dim3(2), dim3(P.p.C), 0, st, P.p, Cc, col_sign, Ky);
+  };
+  if (P.kind == M32_CPAIR)
+    go(rowfix_kernel<2, M32_CPAIR>);
+  else if (k == 2)
+    go(rowfix_kernel<2, M32_JORDAN>);
+  else if (k == 3)
+    go(rowfix_kernel<3, M32_JORDAN>);
+  else
+    go(rowfix_kernel<4, M32_JORDAN>);
+  return cuda_status("row fix");
+}
+
+}  // namespace vmf
