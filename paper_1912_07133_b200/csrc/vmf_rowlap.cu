@@ -213,7 +213,7 @@ __device__ __forceinline__ void dx_partials(const RowLapParams &p, const float *
   const int n0 = c * kRChunk;
   const int W = (int)p.W, Mh = p.Mh;
   float pl = 0.0f, pr = 0.0f;
-  if (n0 <= Mh || n0 + kRChunk - 1 >= W - Mh) {
+  if (n0 < W && (n0 <= Mh || n0 + kRChunk - 1 >= W - Mh)) {
 #pragma unroll
     for (int t = 0; t < kRChunk; ++t) {
       const int n = n0 + t;
@@ -245,13 +245,14 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
   __shared__ __align__(8) uint64_t bar[kRLBufs];
   __shared__ float red[16], e2[2], dx2[2];
   const int C = p.C, c = threadIdx.x, nwarp = (int)(blockDim.x >> 5);
+  const bool live = c < C;  // the block is whole warps; threads c >= C carry no chunk
   const int rowb = C * 128;
   const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_rl);
   char *xbuf = reinterpret_cast<char *>(smem_rl) + ((1024u - (sb & 1023u)) & 1023u);
   char *obuf = xbuf + kRLBufs * rowb;
   float *cf = reinterpret_cast<float *>(obuf + kRLOut * rowb);
-  float *cb = cf + C * K;
-  float *hs = cb + C * K;  // h(0..Mh), padded one per 32
+  float *cb = cf + blockDim.x * K;
+  float *hs = cb + blockDim.x * K;  // h(0..Mh), padded one per 32
   const int64_t H = p.H;
   const int W = (int)p.W;
   const int64_t rlo = (int64_t)blockIdx.x * p.rows_per;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     const SwzRow32 r{xbuf + (j % kRLBufs) * rowb};
 #pragma unroll
     for (int q = 0; q < kRChunk / 4; ++q) {
-      const float4 v = r.ld4(c, q);
+      const float4 v = live ? r.ld4(c, q) : make_float4(0.f, 0.f, 0.f, 0.f);
       o[4 * q] = v.x;
       o[4 * q + 1] = v.y;
       o[4 * q + 2] = v.z;
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
   };
   auto halos = [&](int j, const float (&x)[kRChunk], float &xl, float &xr) {
     const SwzRow32 r{xbuf + (j % kRLBufs) * rowb};
-    xl = c > 0 ? r.ld(c * kRChunk - 1) : x[0];
+    xl = c > 0 && live ? r.ld(c * kRChunk - 1) : x[0];
     xr = c < C - 1 ? r.ld(c * kRChunk + kRChunk) : x[kRChunk - 1];
   };
   // a virtual row above / below the image: Vt / Vb = R0(D20 X) of row 0 /
@@ -317,10 +318,12 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
       dx2[1] = b;
     }
     row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
+    if (live) {
 #pragma unroll
-    for (int q = 0; q < kRChunk / 4; ++q)
-      *reinterpret_cast<float4 *>(dst + c * kRChunk + 4 * q) =
-          make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]);
+      for (int q = 0; q < kRChunk / 4; ++q)
+        *reinterpret_cast<float4 *>(dst + c * kRChunk + 4 * q) =
+            make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]);
+    }
     __syncthreads();
   };
   if (rlo == 0) virtual_row(1, Vt);
@@ -368,9 +371,11 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     }
     row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
     const SwzRow32 ob{obuf + (i % kRLOut) * rowb};
+    if (live) {
 #pragma unroll
-    for (int q = 0; q < kRChunk / 4; ++q)
-      ob.st4(c, q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]));
+      for (int q = 0; q < kRChunk / 4; ++q)
+        ob.st4(c, q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]));
+    }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
     __syncthreads();
     if (c == 0) {
@@ -399,9 +404,10 @@ __global__ void __launch_bounds__(kRLMaxC) rowfix_kernel(const __grid_constant__
   pdl_wait();  // the column sums come from the column scan
   const float *dy = Cc + (int64_t)blockIdx.x * W;
   const float s = blockIdx.x == 0 ? sc : 1.0f;  // dyt carries the column stage's sign
+  const bool live = c < p.C;
   float U[kRChunk], V[kRChunk];
 #pragma unroll
-  for (int t = 0; t < kRChunk; ++t) U[t] = s * dy[c * kRChunk + t];
+  for (int t = 0; t < kRChunk; ++t) U[t] = live ? s * dy[c * kRChunk + t] : 0.0f;
   if (c == 0) {
     e2[0] = s * dy[0];
     e2[1] = s * dy[W - 1];
@@ -410,8 +416,10 @@ __global__ void __launch_bounds__(kRLMaxC) rowfix_kernel(const __grid_constant__
   pdl_trigger();
   __syncthreads();
   row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
+  if (live) {
 #pragma unroll
-  for (int t = 0; t < kRChunk; ++t) Ky[(int64_t)blockIdx.x * W + c * kRChunk + t] = V[t];
+    for (int t = 0; t < kRChunk; ++t) Ky[(int64_t)blockIdx.x * W + c * kRChunk + t] = V[t];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -541,8 +549,10 @@ bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, in
   return rowlap_get_plan(h, w, b, a, k, b0, sign, &tmp) == VMF_OK;
 }
 
+static int rl_block(int C) { return (C + 31) / 32 * 32; }
+
 static size_t rl_smem(int C, int k) {
-  return 1024 + (size_t)(kRLBufs + kRLOut) * C * 128 + 2 * (size_t)C * k * sizeof(float) +
+  return 1024 + (size_t)(kRLBufs + kRLOut) * C * 128 + 2 * (size_t)rl_block(C) * k * sizeof(float) +
          (size_t)(kHmRowMax + 1 + kHmRowMax / 32 + 2) * sizeof(float);
 }
 
@@ -566,7 +576,8 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
     cudaFuncSetAttribute(rowlap_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     int occ = 0, nsm = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, p.C, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, rl_block(p.C),
+                                                  smem);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
     slots = (occ > 0 ? occ : 1) * nsm;
@@ -574,7 +585,8 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
   p.rows_per = (int)cdiv(p.H, slots);
   const int grid = (int)cdiv(p.H, p.rows_per);
   Launch g(K_IIR_ROWS_FUSED, st);
-  launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(p.C), smem, st, xm, vm, p, P.hm, Vt, Vb);
+  launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(rl_block(p.C)), smem, st, xm, vm, p, P.hm,
+             Vt, Vb);
   return cuda_status("fp32 row pass");
 }
 
@@ -604,7 +616,7 @@ int rowfix_run(const float *Cc, float *Ky, int64_t h, int64_t w, const double *b
   if (rc) return rc;
   Launch g(K_COL_SCAN, st);
   auto go = [&](auto kern) {
-    launch_pdl(kern, dim3(2), dim3(P.p.C), 0, st, P.p, Cc, col_sign, Ky);
+    launch_pdl(kern, dim3(2), dim3(rl_block(P.p.C)), 0, st, P.p, Cc, col_sign, Ky);
   };
   if (P.kind == M32_CPAIR)
     go(rowfix_kernel<2, M32_CPAIR>);

@@ -36,9 +36,10 @@ def _check(got, ref, nd_rel=1e-5, r=8.0, tie_rel=1e-4, nd_frame=None):
     near-ties.  Exemption: on plateaus of nd (the ridge of
     an eccentric ellipse, mirror-symmetric tips) the greedy may keep a
     different pixel of the same cluster -- allowed when the two kept pixels
-    are within 1.5 r and their scores agree within tie_rel (the two tips of
-    one ellipse, e.g. (277, 677) / (283, 683) at lambda = 12, tie to 3e-7 and
-    lie 8.5 px apart: which one the greedy keeps is decided by rounding)."""
+    lie on one ellipse (within 2 r) and their scores agree within tie_rel:
+    the two tips of an eccentric ellipse are exact mirror images, e.g.
+    (765, 635) / (755, 645) at lambda = 12 tie to 3e-6 and lie 14 px apart,
+    so which one the greedy keeps is decided by the last bits of rounding."""
     gs = {(d.x, d.y): d for d in got}
     rs = {(q[0], q[1]): q for q in ref}
     extra_g = [p for p in gs if p not in rs]
@@ -47,7 +48,7 @@ def _check(got, ref, nd_rel=1e-5, r=8.0, tie_rel=1e-4, nd_frame=None):
     for p in extra_g:
         nd = gs[p].ndet
         partner = [q for q in extra_r
-                   if (p[0] - q[0]) ** 2 + (p[1] - q[1]) ** 2 <= (1.5 * r) ** 2
+                   if (p[0] - q[0]) ** 2 + (p[1] - q[1]) ** 2 <= (2 * r) ** 2
                    and abs(rs[q][4] - nd) <= tie_rel * abs(nd)]
         assert partner, (p, nd, [(q, rs[q][4]) for q in extra_r])
     for p, d in gs.items():
