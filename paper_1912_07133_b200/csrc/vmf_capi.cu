@@ -8,6 +8,7 @@
 #include "vmf_iir.cuh"
 #include "vmf_colpass.cuh"
 #include "vmf_rowlap.cuh"
+#include "vmf_modal32.cuh"
 #include "vmf_firpass.cuh"
 
 namespace vmf {
@@ -334,13 +335,21 @@ static bool lapfirst_ok(const void *x, int x_dtype, int64_t h, int64_t w, int64_
       col->kind != VMF_STAGE_IIR || getenv("VMF_FORCE_GENERIC"))
     return false;
   if (((uintptr_t)x & 15) || ((ldx * 4) & 15)) return false;
-  if (!rowlap_supported(h, w, row->b_plus, row->a_plus, row->n, row->b_zero, row->sign))
+  if (row->n != col->n ||
+      !rowlap_supported(h, w, row->b_plus, row->a_plus, row->n, row->b_zero, row->sign))
     return false;
   if (iir_plan(ip, w, h, col->b_plus, col->a_plus, col->n, col->b_zero, col->sign)) {
     cudaGetLastError();
     return false;
   }
-  return colpass32_supported(h, w, *ip);
+  if (!colpass32_supported(h, w, *ip)) return false;
+  // one realisation kind for both stages (the column scan row-filters the
+  // border rows with the row stage's plan)
+  RowLapPlan rpl;
+  Modal mc;
+  return rowlap_get_plan(h, w, row->b_plus, row->a_plus, row->n, row->b_zero, row->sign, &rpl) ==
+             VMF_OK &&
+         modal_realise(col->b_plus, col->a_plus, col->n, &mc) && mc.kind == rpl.kind;
 }
 
 int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,

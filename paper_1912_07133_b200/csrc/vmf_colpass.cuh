@@ -40,7 +40,7 @@ struct CandState {
   unsigned int absmax_bits;  // max |L| (float bits)
   int count;                 // candidates appended
   int overflow;              // the global candidate list overflowed
-  int pad;
+  int ticket;                // CTAs done (the fp32 column scan's last-CTA step)
   // decoupled look-back of the finaliser's large-list path: per CTA
   // (status << 62) | count, status 1 = own count, 2 = inclusive prefix
   unsigned long long look[kFinCtas];

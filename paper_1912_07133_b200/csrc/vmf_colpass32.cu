@@ -103,7 +103,8 @@ template <int K, bool VM>
 __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
     const float *__restrict__ T, int64_t ldt, Col32Params p, float *__restrict__ R,
     const __grid_constant__ Hm32 hm, const __grid_constant__ CUtensorMap tmap, int use_tma,
-    CandState *__restrict__ cs, const float *__restrict__ X, int64_t ldx) {
+    CandState *__restrict__ cs, const float *__restrict__ X, int64_t ldx,
+    const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
   float *tile = reinterpret_cast<float *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
@@ -118,24 +119,29 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
   const bool tma = use_tma && r0 >= 1 && r0 + kB32 + 1 <= H && c0 >= 4 && c0 + kC32 + 4 <= W;
   pdl_wait();  // T comes from the row pass
   if (blockIdx.x == 0 && blockIdx.y == 0) cand_reset(cs);
-  if (tma) {
-    if (threadIdx.x == 0) {
-      mbar_init(&tbar, 1);
-      mbar_expect_tx(&tbar, (unsigned)(kCarryRows * kCarryStride * sizeof(float)));
-      tma_load_2d_hint(tile, &tmap, &tbar, (int)(c0 - 4), (int)(r0 - 1), l2_policy_evict_last());
+  // tile <- rows r0-1 .. r1, columns c0-4 .. c0+131 of src (TMA box, or
+  // clamped loads: replicate edges, rows past H repeat H-1)
+  auto stage = [&](const CUtensorMap *map, const float *src, int64_t ld, unsigned phase) {
+    if (tma) {
+      if (threadIdx.x == 0) {
+        if (phase == 0) mbar_init(&tbar, 1);
+        mbar_expect_tx(&tbar, (unsigned)(kCarryRows * kCarryStride * sizeof(float)));
+        tma_load_2d_hint(tile, map, &tbar, (int)(c0 - 4), (int)(r0 - 1), l2_policy_evict_last());
+      }
+      __syncthreads();
+      mbar_wait(&tbar, phase);
+    } else {
+      for (int e = threadIdx.x; e < kCarryRows * kCarryStride; e += blockDim.x) {
+        const int tr = e / kCarryStride, tc = e - tr * kCarryStride;
+        int64_t r = r0 - 1 + tr, c = c0 - 4 + tc;
+        r = r < 0 ? 0 : (r >= H ? H - 1 : r);
+        c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+        tile[e] = __ldg(src + r * ld + c);
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    mbar_wait(&tbar, 0);
-  } else {  // clamped rows / columns (replicate edges; rows past H repeat H-1)
-    for (int e = threadIdx.x; e < kCarryRows * kCarryStride; e += blockDim.x) {
-      const int tr = e / kCarryStride, tc = e - tr * kCarryStride;
-      int64_t r = r0 - 1 + tr, c = c0 - 4 + tc;
-      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
-      c = c < 0 ? 0 : (c >= W ? W - 1 : c);
-      tile[e] = __ldg(T + r * ldt + c);
-    }
-    __syncthreads();
-  }
+  };
+  stage(&tmap, T, ldt, 0);
   // tile row of image row r: r - r0 + 1; tile column of column c0 + j: j + 4
   const float *tc = tile + j + 4;
 #define TT(tr, dc) tc[(tr) * kCarryStride + (dc)]
@@ -169,17 +175,15 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
   // 1 <= r < H, G(r) = T(r) - T(r-1); each half takes 32 rows
   float pt = 0.0f, pb = 0.0f;
   const bool top = r0 < p.Mh + 1, bot = r0 + kB32 > H - 1 - p.Mh;
-  if (top || bot) {
+  if (top || bot) {  // (CTA-uniform)
+    if (VM) {  // G of the frame X: the same tile geometry, reloaded
+      __syncthreads();  // every V read done
+      stage(&xmap, X, ldx, 1);
+    }
     for (int t = half * (kB32 / 2); t < (half + 1) * (kB32 / 2); ++t) {
       const int64_t r = r0 + t;
       if (r < 1 || r >= H) continue;
-      float g;
-      if (VM) {  // G of the frame (clamped column)
-        const int64_t cc = col < W ? col : W - 1;
-        g = __ldg(X + r * ldx + cc) - __ldg(X + (r - 1) * ldx + cc);
-      } else {
-        g = TT(t + 1, 0) - TT(t, 0);
-      }
+      const float g = TT(t + 1, 0) - TT(t, 0);
       if (top && r <= p.Mh) pt = fmaf(hm.h[r], g, pt);
       if (bot && H - r <= p.Mh) pb = fmaf(hm.h[H - r], g, pb);
     }
@@ -217,12 +221,19 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
 //    one thread per (column, correction) sums the boundary partials in band
 //    order; the start states go back with coalesced stores.
 // ---------------------------------------------------------------------------
-template <int K, bool VM>
+// V mode: the CTA that finishes last (ticket in the CandState) also turns the
+// column sums of the border partials into Ky = R_ss(dy) with the ROW stage
+// (two single-row filters, vmf_rowlap.cuh), so no extra kernel sits on the
+// chain.
+template <int K, bool VM, int RKIND>
 __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict__ T, int64_t ldt,
                                                        Col32Params p, float *__restrict__ R,
                                                        float *__restrict__ Cc,
                                                        const float *__restrict__ Vt,
-                                                       const float *__restrict__ Vb) {
+                                                       const float *__restrict__ Vb,
+                                                       const __grid_constant__ RowLapParams rp,
+                                                       float *__restrict__ Ky,
+                                                       CandState *__restrict__ cs) {
   extern __shared__ __align__(16) float ss[];  // [NB][2K+2][32]
   constexpr int Q = 2 * K + 2;
   const int NB = p.NB;
@@ -295,6 +306,38 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
     double a = 0.0;
     for (int b = 0; b < NB; ++b) a += (double)ss[(b * Q + 2 * K + which) * kScan32Cols + c];
     if (c0 + c < W) Cc[(int64_t)which * W + c0 + c] = (float)a;
+  }
+  if (VM) {  // publish this CTA's column sums; the last CTA row-filters them
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(&cs->ticket, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      float *cf = ss + NB * Q * kScan32Cols, *cb = cf + 256 * 4;  // past the records
+      __shared__ float e2[2], dx2[2];
+      const bool live = tid < rp.C;
+      for (int which = 0; which < 2; ++which) {
+        const float s = which == 0 ? p.sign : 1.0f;  // dyt carries the column stage's sign
+        const float *dy = Cc + (int64_t)which * W;
+        float U[kRChunk], V[kRChunk];
+#pragma unroll
+        for (int t = 0; t < kRChunk; ++t) U[t] = live ? s * __ldcg(dy + tid * kRChunk + t) : 0.0f;
+        if (tid == 0) {
+          e2[0] = s * __ldcg(dy);
+          e2[1] = s * __ldcg(dy + W - 1);
+          dx2[0] = dx2[1] = 0.0f;
+        }
+        __syncthreads();
+        row_filter<K, RKIND>(rp, U, V, cf, cb, e2, dx2);
+        if (live) {
+#pragma unroll
+          for (int t = 0; t < kRChunk; ++t) Ky[(int64_t)which * W + tid * kRChunk + t] = V[t];
+        }
+        __syncthreads();
+      }
+    }
   }
   __syncthreads();
   // start states back over the carries (q < 2K), coalesced
@@ -403,7 +446,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
       const float u = VM ? tcv
                          : lap5(tcol[(kB32 + 2) * kT32Stride - 1], tcv,
                                 tcol[(kB32 + 2) * kT32Stride + 1], tu, td);
-      lcol[(kB32 + 1) * kT32Stride] = u;
+      if (!VM) lcol[(kB32 + 1) * kT32Stride] = u;
       ym_below = fmaf(-p.e1, u, rb.out(p.ci));
       td = tcv;
       tcv = tu;
@@ -414,7 +457,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
       const float u = VM ? tcv
                          : lap5(tcol[(t + 2) * kT32Stride - 1], tcv, tcol[(t + 2) * kT32Stride + 1],
                                 tu, td);
-      lcol[(t + 1) * kT32Stride] = u;
+      if (!VM) lcol[(t + 1) * kT32Stride] = u;
       park[t] = rb.out(p.c);  // y-(r0 + t)
       rb.step(p, u);
       td = tcv;
@@ -423,7 +466,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     ym_above = rb.out(p.c);  // y-(r0 - 1)
     // U(r0 - 1) for the top halo row
     const float tu = tcol[0];
-    lcol[0] = VM ? tcv : lap5(tcol[kT32Stride - 1], tcv, tcol[kT32Stride + 1], tu, td);
+    if (!VM) lcol[0] = lap5(tcol[kT32Stride - 1], tcv, tcol[kT32Stride + 1], tu, td);
   }
 
   // ---- down: L of rows r0-1 .. r1 in place of U ----------------------------
@@ -431,8 +474,10 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
   float tmax = 0.0f;
   {
     // top halo row r0 - 1: y+(r0-1) = c A^-1 uf(r0-1) - e1 U(r0-1)
+    // U of lt row q: V mode reads V straight from the tile (row q + 1)
+    auto Urow = [&](int q) { return VM ? tcol[(q + 1) * kT32Stride] : lcol[q * kT32Stride]; };
     if (r0 > 0) {
-      const float u = lcol[0];
+      const float u = Urow(0);
       float v = fmaf(-p.e1, u, rf.out_from(p.ci, fmaf(b0, u, sg * ym_above)));
       if (r0 - 1 == H - 1) v -= cbot;
       if (LSC) v *= lsc;
@@ -441,7 +486,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
 #pragma unroll
     for (int t = 0; t < kB32; ++t) {
       const int64_t r = r0 + t;
-      const float u = lcol[(t + 1) * kT32Stride];
+      const float u = Urow(t + 1);
       float v = rf.out_from(p.c, fmaf(b0, u, sg * park[t]));
       rf.step(p, u);
       if (r == 0) v += ctop;
@@ -452,7 +497,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     }
     // bottom halo row r1: y+(r1) = c . uf(r1-1) (the walk's end state)
     {
-      const float u = lcol[(kB32 + 1) * kT32Stride];
+      const float u = Urow(kB32 + 1);
       float v = rf.out_from(p.c, fmaf(b0, u, sg * ym_below));
       if (r1 == H - 1) v -= cbot;
       if (LSC) v *= lsc;
@@ -676,8 +721,9 @@ static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
 
 template <int K, int KIND, bool VM>
 static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Col32Plan &P,
-                    const Col32VMode &vm, int32_t *det_yx, float *det_val, int64_t cap,
-                    int64_t *n_det_dev, float *thr_dev, void *ws, cudaStream_t st) {
+                    const Col32VMode &vm, const RowLapParams &rp, int32_t *det_yx,
+                    float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
+                    cudaStream_t st) {
   const Col32Params &p = P.p;
   const int64_t h = p.H, w = p.W;
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
@@ -705,22 +751,25 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     if (attr.first())
       cudaFuncSetAttribute(colcarry32_kernel<K, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            csm);
+    CUtensorMap xmap;  // the frame, same box (V mode: border partials)
+    memset(&xmap, 0, sizeof(xmap));
+    const int xtma = !VM || make_tmap_2d_f32(&xmap, vm.x, h, w, vm.ldx, kCarryStride, kCarryRows);
+    cudaGetLastError();
     launch_pdl(colcarry32_kernel<K, VM>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
-               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs, vm.x, vm.ldx);
+               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma && xtma, cs, vm.x, vm.ldx,
+               xmap);
   }
   {
     Launch g(K_COL_SCAN, st);
-    const int ssm = p.NB * (2 * K + 2) * kScan32Cols * (int)sizeof(float);
+    // records, then (V mode) the last CTA's row-filter scratch
+    const int ssm = p.NB * (2 * K + 2) * kScan32Cols * (int)sizeof(float) +
+                    (VM ? 2 * 256 * 4 * (int)sizeof(float) : 0);
     static PerDevice attr;
     if (attr.first())
-      cudaFuncSetAttribute(colscan32_kernel<K, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
-    launch_pdl(colscan32_kernel<K, VM>, dim3((unsigned)cdiv(w, kScan32Cols)), dim3(256), ssm, st,
-               T, ldt, p, R, Cc, vm.vt, vm.vb);
-  }
-  if (VM) {  // the column direction's border terms, row-filtered: Ky = R_ss(dy)
-    const int rc = rowfix_run(Cc, Ky, h, w, vm.rb, vm.ra, vm.rk, vm.rb0, vm.rsign, p.sign, st);
-    if (rc) return rc;
+      cudaFuncSetAttribute(colscan32_kernel<K, VM, KIND>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    launch_pdl(colscan32_kernel<K, VM, KIND>, dim3((unsigned)cdiv(w, kScan32Cols)), dim3(256),
+               ssm, st, T, ldt, p, R, Cc, vm.vt, vm.vb, rp, Ky, cs);
   }
   {
     Launch g(K_IIR_COLS_FUSED, st);
@@ -796,11 +845,19 @@ int colpass32_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirP
   run.p.frac = frac;
   const Col32VMode none = {};
   const Col32VMode &vm = vmode ? *vmode : none;
-#define VMF_L32(KK, KD)                                                                        \
-  (vmode ? launch32<KK, KD, true>(T, ldt, L, ldl, run, vm, det_yx, det_val, cap, n_det_dev,   \
-                                  thr_dev, ws, st)                                             \
-         : launch32<KK, KD, false>(T, ldt, L, ldl, run, vm, det_yx, det_val, cap, n_det_dev,  \
-                                   thr_dev, ws, st))
+  static RowLapPlan rplan;  // V mode: the row stage (border rows are row-filtered)
+  memset(&rplan.p, 0, sizeof(rplan.p));
+  if (vmode) {
+    const int rrc = rowlap_get_plan(h, w, vm.rb, vm.ra, vm.rk, vm.rb0, vm.rsign, &rplan);
+    if (rrc) return rrc;
+    if (rplan.kind != run.kind || vm.rk != ip.K)
+      return fail(VMF_EVALUE, "fp32 path: row and column stages need the same realisation");
+  }
+#define VMF_L32(KK, KD)                                                                         \
+  (vmode ? launch32<KK, KD, true>(T, ldt, L, ldl, run, vm, rplan.p, det_yx, det_val, cap,      \
+                                  n_det_dev, thr_dev, ws, st)                                   \
+         : launch32<KK, KD, false>(T, ldt, L, ldl, run, vm, rplan.p, det_yx, det_val, cap,     \
+                                   n_det_dev, thr_dev, ws, st))
   if (run.kind == M32_CPAIR) return VMF_L32(2, M32_CPAIR);
   switch (ip.K) {
     case 2: return VMF_L32(2, M32_JORDAN);

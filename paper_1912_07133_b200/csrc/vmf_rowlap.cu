@@ -41,7 +41,6 @@
 
 namespace vmf {
 
-constexpr int kRChunk = 32;
 constexpr int kRLMaxC = 256;   // W <= 8192
 constexpr int kRLBufs = 4;     // input ring
 constexpr int kRLOut = 2;      // output ring
@@ -62,147 +61,6 @@ struct SwzRow32 {
 };
 
 __device__ __forceinline__ int hidx(int n) { return n + (n >> 5); }  // padded h() copy
-
-// One row through R: U (registers, this thread's chunk) -> V (registers).
-// eL / eR: steady-state inputs left / right of the row; cf / cb: [C][K]
-// scratch; dx[2]: the row's border terms (added to V(0) / subtracted from
-// V(W-1)) -- published in smem by the caller before the first barrier.
-// Contains two block barriers.
-template <int K, int KIND>
-__device__ __forceinline__ void row_filter(const RowLapParams &p, const float (&U)[kRChunk],
-                                           float (&V)[kRChunk], float *cf, float *cb,
-                                           const float *e2, const float *dx2) {
-  const int c = threadIdx.x, C = p.C, lane = c & 31, warp = c >> 5;
-  // zero-state chunk carries: forward end state P + Q, backward start P - Q
-  {
-    float P[K], Q[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0f;
-#pragma unroll
-    for (int t = 0; t < kRChunk / 2; ++t) {
-      const float s = U[t] + U[kRChunk - 1 - t], d = U[t] - U[kRChunk - 1 - t];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        P[i] = fmaf(p.SP[i][t], s, P[i]);
-        Q[i] = fmaf(p.SQ[i][t], d, Q[i]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      cf[c * K + i] = P[i] + Q[i];
-      cb[c * K + i] = P[i] - Q[i];
-    }
-  }
-  __syncthreads();
-  // chunk scans: task 0 forward (chunks 0..C-1), task 1 backward
-  for (int task = warp; task < 2; task += (int)(blockDim.x >> 5)) {
-    float *cc = task == 0 ? cf : cb;
-    const int cpl = p.cpl;
-    const float e = e2[task];
-    float A[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) A[i] = 0.0f;
-    for (int q = 0; q < cpl; ++q) {
-      const int sp = lane * cpl + q;
-      if (sp >= C) break;
-      const int ch = task == 0 ? sp : C - 1 - sp;
-      float d[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) d[i] = cc[ch * K + i];
-      if (sp == 0) {  // + A^32 u_ss(e): the steady start enters with the first chunk
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-#pragma unroll
-          for (int m = 0; m < K; ++m) d[i] = fmaf(p.A32[i * K + m], p.Iss[m] * e, d[i]);
-      }
-      float An[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        float a = d[i];
-#pragma unroll
-        for (int m = 0; m < K; ++m) a = fmaf(p.A32[i * K + m], A[m], a);
-        An[i] = a;
-      }
-#pragma unroll
-      for (int i = 0; i < K; ++i) A[i] = An[i];
-    }
-#pragma unroll
-    for (int lv = 0; lv < 5; ++lv) {
-      const int o = 1 << lv;
-      float Bv[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) Bv[i] = __shfl_up_sync(0xffffffffu, A[i], o);
-      if (lane >= o) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          float a = A[i];
-#pragma unroll
-          for (int m = 0; m < K; ++m) a = fmaf(p.Apow[lv][i * K + m], Bv[m], a);
-          A[i] = a;
-        }
-      }
-    }
-    float E[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      const float v = __shfl_up_sync(0xffffffffu, A[i], 1);
-      E[i] = lane ? v : p.Iss[i] * e;
-    }
-    // each chunk's start state over its carry
-    for (int q = 0; q < cpl; ++q) {
-      const int sp = lane * cpl + q;
-      if (sp >= C) break;
-      const int ch = task == 0 ? sp : C - 1 - sp;
-      float d[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        d[i] = cc[ch * K + i];
-        cc[ch * K + i] = E[i];
-      }
-      if (sp == 0) {
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-#pragma unroll
-          for (int m = 0; m < K; ++m) d[i] = fmaf(p.A32[i * K + m], p.Iss[m] * e, d[i]);
-      }
-      float En[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        float a = d[i];
-#pragma unroll
-        for (int m = 0; m < K; ++m) a = fmaf(p.A32[i * K + m], E[m], a);
-        En[i] = a;
-      }
-#pragma unroll
-      for (int i = 0; i < K; ++i) E[i] = En[i];
-    }
-  }
-  __syncthreads();
-  // walks: backward parked (b0 U + s y-), forward adds y+
-  float park[kRChunk];
-  {
-    Rec32<K, KIND> rb;
-#pragma unroll
-    for (int i = 0; i < K; ++i) rb.u[i] = cb[c * K + i];
-#pragma unroll
-    for (int t = kRChunk - 1; t >= 0; --t) {
-      park[t] = rb.out_from(p.cs, p.b0 * U[t]);
-      rb.step(p, U[t]);
-    }
-  }
-  {
-    Rec32<K, KIND> rf;
-#pragma unroll
-    for (int i = 0; i < K; ++i) rf.u[i] = cf[c * K + i];
-#pragma unroll
-    for (int t = 0; t < kRChunk; ++t) {
-      V[t] = rf.out_from(p.c, park[t]);
-      rf.step(p, U[t]);
-    }
-  }
-  if (c == 0) V[0] += dx2[0];
-  if (c == C - 1) V[kRChunk - 1] -= dx2[1];
-}
 
 // Border-term partials of this thread's chunk: sum over its samples n >= 1
 // of h(n) G(n) (n <= Mh) and h(W - n) G(n) (W - n <= Mh), G(n) = X(n) - X(n-1),
@@ -572,9 +430,11 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
   static std::map<std::pair<int, size_t>, int> slot_cache;
   const int dev = current_device();
   int &slots = slot_cache[std::make_pair(dev, smem)];
-  if (!slots) {
+  static PerDevice attr;
+  if (attr.first())  // the largest footprint (C = 256), so every width may launch
     cudaFuncSetAttribute(rowlap_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+                         (int)rl_smem(kRLMaxC, K));
+  if (!slots) {
     int occ = 0, nsm = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, rl_block(p.C),
                                                   smem);
