@@ -3,6 +3,7 @@
 #pragma once
 #include "vmf_iir.cuh"
 #include "vmf_dfi.cuh"
+#include "vmf_rowlap.cuh"
 
 namespace vmf {
 
@@ -101,10 +102,10 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
 // instead of T; x = the frame (border partials), vt / vb = its virtual rows,
 // (rb, ra, rk, rb0, rsign) = the ROW stage (the border rows are row-filtered).
 struct Col32VMode {
-  const float *x;
-  int64_t ldx;
-  const float *vt, *vb;
-  const double *rb, *ra;
+  const float *vt, *vb;       // the row pass's virtual rows
+  const float *pt, *pb;       // its per-CTA border partials [grid][w]
+  RowLapGeom geom;            // its launch geometry
+  const double *rb, *ra;      // the row stage
   int rk;
   double rb0;
   int rsign;

@@ -98,13 +98,12 @@ __device__ __forceinline__ int64_t ridx(int b, int q, int K, int64_t W, int64_t 
 // two halves of the band's 32 sample pairs (t, 63 - t) of column j.  The tile
 // holds T rows r0-1 .. r1 (clamped), columns c0-4 .. c0+131 (clamped).
 // VM: the input is V = R(Lap5 X) of the fp32 row pass (U = V itself, no
-// horizontal neighbours); the border partials then come from the frame X.
+// horizontal neighbours); the border partials then come from the row pass.
 template <int K, bool VM>
 __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
     const float *__restrict__ T, int64_t ldt, Col32Params p, float *__restrict__ R,
     const __grid_constant__ Hm32 hm, const __grid_constant__ CUtensorMap tmap, int use_tma,
-    CandState *__restrict__ cs, const float *__restrict__ X, int64_t ldx,
-    const __grid_constant__ CUtensorMap xmap) {
+    CandState *__restrict__ cs) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
   float *tile = reinterpret_cast<float *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
@@ -122,6 +121,7 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
   // tile <- rows r0-1 .. r1, columns c0-4 .. c0+131 of src (TMA box, or
   // clamped loads: replicate edges, rows past H repeat H-1)
   auto stage = [&](const CUtensorMap *map, const float *src, int64_t ld, unsigned phase) {
+    (void)phase;
     if (tma) {
       if (threadIdx.x == 0) {
         if (phase == 0) mbar_init(&tbar, 1);
@@ -173,13 +173,10 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
   // boundary-correction partials (bands within Mh rows of the top / bottom):
   // top = sum h(r) G(r), bottom = sum h(H - r) G(r) over this band's rows
   // 1 <= r < H, G(r) = T(r) - T(r-1); each half takes 32 rows
+  // (V mode: the row pass accumulates the border partials of the frame)
   float pt = 0.0f, pb = 0.0f;
-  const bool top = r0 < p.Mh + 1, bot = r0 + kB32 > H - 1 - p.Mh;
+  const bool top = !VM && r0 < p.Mh + 1, bot = !VM && r0 + kB32 > H - 1 - p.Mh;
   if (top || bot) {  // (CTA-uniform)
-    if (VM) {  // G of the frame X: the same tile geometry, reloaded
-      __syncthreads();  // every V read done
-      stage(&xmap, X, ldx, 1);
-    }
     for (int t = half * (kB32 / 2); t < (half + 1) * (kB32 / 2); ++t) {
       const int64_t r = r0 + t;
       if (r < 1 || r >= H) continue;
@@ -221,6 +218,12 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
 //    one thread per (column, correction) sums the boundary partials in band
 //    order; the start states go back with coalesced stores.
 // ---------------------------------------------------------------------------
+// shared floats before the row-filter scratch: the records, or the staged row
+__host__ __device__ inline int scan32_scratch(int NB, int K, int64_t W) {
+  const int rec = NB * (2 * K + 2) * kScan32Cols, row = (int)(W + W / 32 + 1);
+  return rec > row ? rec : row;
+}
+
 // V mode: the CTA that finishes last (ticket in the CandState) also turns the
 // column sums of the border partials into Ky = R_ss(dy) with the ROW stage
 // (two single-row filters, vmf_rowlap.cuh), so no extra kernel sits on the
@@ -233,7 +236,10 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
                                                        const float *__restrict__ Vb,
                                                        const __grid_constant__ RowLapParams rp,
                                                        float *__restrict__ Ky,
-                                                       CandState *__restrict__ cs) {
+                                                       CandState *__restrict__ cs,
+                                                       const float *__restrict__ Pt,
+                                                       const float *__restrict__ Pb,
+                                                       RowLapGeom geom) {
   extern __shared__ __align__(16) float ss[];  // [NB][2K+2][32]
   constexpr int Q = 2 * K + 2;
   const int NB = p.NB;
@@ -241,6 +247,7 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
   const int64_t c0 = (int64_t)blockIdx.x * kScan32Cols;
   const int tid = threadIdx.x;
   __shared__ float es[2][kScan32Cols];
+  __shared__ double psum[6][kScan32Cols];
   pdl_wait();  // records come from the band carries
   const bool full = c0 + kScan32Cols <= W && (W & 3) == 0;
   if (full) {
@@ -300,43 +307,36 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
 #pragma unroll
       for (int i = 0; i < K; ++i) u[i] = un[i];
     }
-  } else if (tid < 4 * kScan32Cols) {  // boundary corrections, band order
+  } else if (!VM && tid < 4 * kScan32Cols) {  // boundary corrections, band order
     const int which = (tid - 2 * kScan32Cols) / kScan32Cols;
     const int c = tid - (2 + which) * kScan32Cols;
     double a = 0.0;
     for (int b = 0; b < NB; ++b) a += (double)ss[(b * Q + 2 * K + which) * kScan32Cols + c];
     if (c0 + c < W) Cc[(int64_t)which * W + c0 + c] = (float)a;
+  } else if (VM) {  // boundary corrections: the row-pass CTAs' partials, CTA order
+    // 6 groups of 32 threads: (top, bottom) x three contiguous CTA ranges
+    const int g = (tid - 2 * kScan32Cols) / kScan32Cols;
+    const int which = g / 3, part = g % 3;
+    const int c = tid & (kScan32Cols - 1);
+    const int64_t cc = c0 + c < W ? c0 + c : W - 1;
+    const float *P = which == 0 ? Pt : Pb;
+    const int b0 = geom.grid * part / 3, b1 = geom.grid * (part + 1) / 3;
+    double a = 0.0;
+#pragma unroll 4
+    for (int b = b0; b < b1; ++b) {
+      const int64_t rl = (int64_t)b * geom.rows_per;
+      const int64_t rh = rl + geom.rows_per < H ? rl + geom.rows_per : H;
+      const bool in = which == 0 ? rl <= geom.Mhc : rh - 1 >= H - geom.Mhc;
+      if (in) a += (double)__ldg(P + (int64_t)b * W + cc);
+    }
+    psum[g][c] = a;
   }
-  if (VM) {  // publish this CTA's column sums; the last CTA row-filters them
-    __shared__ int last;
-    __threadfence();
+  if (VM) {
     __syncthreads();
-    if (tid == 0) last = atomicAdd(&cs->ticket, 1) == (int)gridDim.x - 1;
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      float *cf = ss + NB * Q * kScan32Cols, *cb = cf + 256 * 4;  // past the records
-      __shared__ float e2[2], dx2[2];
-      const bool live = tid < rp.C;
-      for (int which = 0; which < 2; ++which) {
-        const float s = which == 0 ? p.sign : 1.0f;  // dyt carries the column stage's sign
-        const float *dy = Cc + (int64_t)which * W;
-        float U[kRChunk], V[kRChunk];
-#pragma unroll
-        for (int t = 0; t < kRChunk; ++t) U[t] = live ? s * __ldcg(dy + tid * kRChunk + t) : 0.0f;
-        if (tid == 0) {
-          e2[0] = s * __ldcg(dy);
-          e2[1] = s * __ldcg(dy + W - 1);
-          dx2[0] = dx2[1] = 0.0f;
-        }
-        __syncthreads();
-        row_filter<K, RKIND>(rp, U, V, cf, cb, e2, dx2);
-        if (live) {
-#pragma unroll
-          for (int t = 0; t < kRChunk; ++t) Ky[(int64_t)which * W + tid * kRChunk + t] = V[t];
-        }
-        __syncthreads();
-      }
+    if (tid < 2 * kScan32Cols) {
+      const int which = tid / kScan32Cols, c = tid & (kScan32Cols - 1);
+      const double a = (psum[3 * which][c] + psum[3 * which + 1][c]) + psum[3 * which + 2][c];
+      if (c0 + c < W) Cc[(int64_t)which * W + c0 + c] = (float)a;
     }
   }
   __syncthreads();
@@ -355,6 +355,45 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
       if (c0 + c < W) R[(int64_t)(b * Q + q) * W + c0 + c] = ss[(b * Q + q) * kScan32Cols + c];
     }
   }
+  if (VM) {  // publish this CTA's column sums; the last CTA row-filters them
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(&cs->ticket, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      // staging: the row (coalesced) at n + n/32 (conflict-free chunk reads)
+      float *rowp = ss;  // (the records are back in R: free)
+      float *cf = ss + scan32_scratch(NB, K, W), *cb = cf + 256 * 4;
+      __shared__ float e2[2], dx2[2];
+      const bool live = tid < rp.C;
+      for (int which = 0; which < 2; ++which) {
+        const float s = which == 0 ? p.sign : 1.0f;  // dyt carries the column stage's sign
+        const float *dy = Cc + (int64_t)which * W;
+        for (int n = tid; n < W; n += blockDim.x) rowp[n + (n >> 5)] = s * __ldcg(dy + n);
+        if (tid == 0) dx2[0] = dx2[1] = 0.0f;
+        __syncthreads();
+        if (tid == 0) {
+          e2[0] = rowp[0];
+          e2[1] = rowp[(W - 1) + ((W - 1) >> 5)];
+        }
+        float U[kRChunk], V[kRChunk];
+#pragma unroll
+        for (int t = 0; t < kRChunk; ++t) U[t] = live ? rowp[tid * (kRChunk + 1) + t] : 0.0f;
+        __syncthreads();
+        row_filter<K, RKIND>(rp, U, V, cf, cb, e2, dx2);
+        if (live) {
+#pragma unroll
+          for (int t = 0; t < kRChunk; ++t) rowp[tid * (kRChunk + 1) + t] = V[t];
+        }
+        __syncthreads();
+        for (int n = tid; n < W; n += blockDim.x) Ky[(int64_t)which * W + n] = rowp[n + (n >> 5)];
+        __syncthreads();
+      }
+    }
+  }
+
 }
 
 // ---------------------------------------------------------------------------
@@ -751,25 +790,20 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     if (attr.first())
       cudaFuncSetAttribute(colcarry32_kernel<K, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            csm);
-    CUtensorMap xmap;  // the frame, same box (V mode: border partials)
-    memset(&xmap, 0, sizeof(xmap));
-    const int xtma = !VM || make_tmap_2d_f32(&xmap, vm.x, h, w, vm.ldx, kCarryStride, kCarryRows);
-    cudaGetLastError();
     launch_pdl(colcarry32_kernel<K, VM>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
-               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma && xtma, cs, vm.x, vm.ldx,
-               xmap);
+               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs);
   }
   {
     Launch g(K_COL_SCAN, st);
     // records, then (V mode) the last CTA's row-filter scratch
-    const int ssm = p.NB * (2 * K + 2) * kScan32Cols * (int)sizeof(float) +
-                    (VM ? 2 * 256 * 4 * (int)sizeof(float) : 0);
+    const int ssm = (VM ? scan32_scratch(p.NB, K, w) + 2 * 256 * 4
+                        : p.NB * (2 * K + 2) * kScan32Cols) * (int)sizeof(float);
     static PerDevice attr;
     if (attr.first())
       cudaFuncSetAttribute(colscan32_kernel<K, VM, KIND>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     launch_pdl(colscan32_kernel<K, VM, KIND>, dim3((unsigned)cdiv(w, kScan32Cols)), dim3(256),
-               ssm, st, T, ldt, p, R, Cc, vm.vt, vm.vb, rp, Ky, cs);
+               ssm, st, T, ldt, p, R, Cc, vm.vt, vm.vb, rp, Ky, cs, vm.pt, vm.pb, vm.geom);
   }
   {
     Launch g(K_IIR_COLS_FUSED, st);

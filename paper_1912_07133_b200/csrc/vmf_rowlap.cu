@@ -98,13 +98,15 @@ template <int K, int KIND>
 __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
     const __grid_constant__ RowLapParams p, const __grid_constant__ HmRow hm,
-    float *__restrict__ Vt, float *__restrict__ Vb) {
+    float *__restrict__ Vt, float *__restrict__ Vb, const __grid_constant__ HmRow hmc, int Mhc,
+    float *__restrict__ Pt, float *__restrict__ Pb) {
   extern __shared__ __align__(1024) unsigned char smem_rl[];
   __shared__ __align__(8) uint64_t bar[kRLBufs];
   __shared__ float red[16], e2[2], dx2[2];
   const int C = p.C, c = threadIdx.x, nwarp = (int)(blockDim.x >> 5);
   const bool live = c < C;  // the block is whole warps; threads c >= C carry no chunk
-  const int rowb = C * 128;
+  const int rowbytes = C * 128;               // one row's TMA box
+  const int rowb = (rowbytes + 1023) & ~1023;  // buffer spacing: SWIZZLE_128B needs 1024-byte bases
   const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_rl);
   char *xbuf = reinterpret_cast<char *>(smem_rl) + ((1024u - (sb & 1023u)) & 1023u);
   char *obuf = xbuf + kRLBufs * rowb;
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     int64_t r = rlo - 1 + j;
     r = r < 0 ? 0 : (r >= H ? H - 1 : r);
     const int s = j % kRLBufs;
-    mbar_expect_tx(&bar[s], (unsigned)rowb);
+    mbar_expect_tx(&bar[s], (unsigned)rowbytes);
     tma_load_3d_hint(xbuf + s * rowb, &xmap, &bar[s], 0, 0, (int)r, l2_policy_evict_first());
   };
   if (c == 0) {
@@ -185,6 +187,13 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     __syncthreads();
   };
   if (rlo == 0) virtual_row(1, Vt);
+  // column-direction border partials over this CTA's rows (registers):
+  // top += h_C(r) G(r) for 1 <= r <= Mhc, bottom += h_C(H - r) G(r) for
+  // r >= H - Mhc; G(r) = X(r) - X(r-1); summed over CTAs by the column scan
+  const bool any_top = rlo <= Mhc, any_bot = rhi - 1 >= H - Mhc;
+  float acct[kRChunk], accb[kRChunk];
+#pragma unroll
+  for (int t = 0; t < kRChunk; ++t) acct[t] = accb[t] = 0.0f;
 
   for (int i = 0; i < nrows; ++i) {
     const int64_t r = rlo + i;
@@ -198,6 +207,16 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
       load_chunk(i, Xu);
 #pragma unroll
       for (int t = 0; t < kRChunk; ++t) U[t] = Xu[t] - X[t];
+      if (r >= 1 && r <= Mhc) {
+        const float w = hmc.h[r];
+#pragma unroll
+        for (int t = 0; t < kRChunk; ++t) acct[t] = fmaf(w, X[t] - Xu[t], acct[t]);
+      }
+      if (r >= 1 && r >= H - Mhc) {
+        const float w = hmc.h[H - r];
+#pragma unroll
+        for (int t = 0; t < kRChunk; ++t) accb[t] = fmaf(w, X[t] - Xu[t], accb[t]);
+      }
       load_chunk(i + 2, Xu);
 #pragma unroll
       for (int t = 0; t < kRChunk; ++t) {
@@ -243,41 +262,21 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     }
   }
   if (rhi == H) virtual_row(nrows, Vb);
+  if (live && (any_top || any_bot)) {
+    float *dt = Pt + (int64_t)blockIdx.x * W + c * kRChunk;
+    float *db = Pb + (int64_t)blockIdx.x * W + c * kRChunk;
+#pragma unroll
+    for (int q = 0; q < kRChunk / 4; ++q) {
+      if (any_top)
+        *reinterpret_cast<float4 *>(dt + 4 * q) =
+            make_float4(acct[4 * q], acct[4 * q + 1], acct[4 * q + 2], acct[4 * q + 3]);
+      if (any_bot)
+        *reinterpret_cast<float4 *>(db + 4 * q) =
+            make_float4(accb[4 * q], accb[4 * q + 1], accb[4 * q + 2], accb[4 * q + 3]);
+    }
+  }
   pdl_trigger();
   if (c == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-}
-
-// ---------------------------------------------------------------------------
-// rowfix: ky = R_ss(dy) for the top (CTA 0) and bottom (CTA 1) border terms
-// of the column direction: dy = s_C * (column sums of h_C(m) G(m)) from the
-// column scan; steady starts at the row's own end values (replicate).
-// ---------------------------------------------------------------------------
-template <int K, int KIND>
-__global__ void __launch_bounds__(kRLMaxC) rowfix_kernel(const __grid_constant__ RowLapParams p,
-                                                         const float *__restrict__ Cc, float sc,
-                                                         float *__restrict__ Ky) {
-  __shared__ float cf[kRLMaxC * 4], cb[kRLMaxC * 4];
-  __shared__ float e2[2], dx2[2];
-  const int c = threadIdx.x, W = (int)p.W;
-  pdl_wait();  // the column sums come from the column scan
-  const float *dy = Cc + (int64_t)blockIdx.x * W;
-  const float s = blockIdx.x == 0 ? sc : 1.0f;  // dyt carries the column stage's sign
-  const bool live = c < p.C;
-  float U[kRChunk], V[kRChunk];
-#pragma unroll
-  for (int t = 0; t < kRChunk; ++t) U[t] = live ? s * dy[c * kRChunk + t] : 0.0f;
-  if (c == 0) {
-    e2[0] = s * dy[0];
-    e2[1] = s * dy[W - 1];
-    dx2[0] = dx2[1] = 0.0f;
-  }
-  pdl_trigger();
-  __syncthreads();
-  row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
-  if (live) {
-#pragma unroll
-    for (int t = 0; t < kRChunk; ++t) Ky[(int64_t)blockIdx.x * W + c * kRChunk + t] = V[t];
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -410,13 +409,14 @@ bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, in
 static int rl_block(int C) { return (C + 31) / 32 * 32; }
 
 static size_t rl_smem(int C, int k) {
-  return 1024 + (size_t)(kRLBufs + kRLOut) * C * 128 + 2 * (size_t)rl_block(C) * k * sizeof(float) +
+  return 1024 + (size_t)(kRLBufs + kRLOut) * ((C * 128 + 1023) & ~1023) + 2 * (size_t)rl_block(C) * k * sizeof(float) +
          (size_t)(kHmRowMax + 1 + kHmRowMax / 32 + 2) * sizeof(float);
 }
 
 template <int K, int KIND>
 static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, float *Vt, float *Vb,
-                         RowLapPlan &P, cudaStream_t st) {
+                         RowLapPlan &P, const RowLapPlan &PC, float *Pt, float *Pb,
+                         RowLapGeom *geom, cudaStream_t st) {
   RowLapParams &p = P.p;
   CUtensorMap xm, vm;
   memset(&xm, 0, sizeof(xm));
@@ -444,49 +444,36 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
   }
   p.rows_per = (int)cdiv(p.H, slots);
   const int grid = (int)cdiv(p.H, p.rows_per);
+  if (grid > kRLMaxGrid) return fail(VMF_EVALUE, "row pass: too many CTAs");
+  geom->rows_per = p.rows_per;
+  geom->grid = grid;
+  geom->Mhc = PC.p.Mh;
   Launch g(K_IIR_ROWS_FUSED, st);
   launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(rl_block(p.C)), smem, st, xm, vm, p, P.hm,
-             Vt, Vb);
+             Vt, Vb, PC.hm, PC.p.Mh, Pt, Pb);
   return cuda_status("fp32 row pass");
 }
 
 int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *Vt, float *Vb,
                int64_t h, int64_t w, const double *b, const double *a, int k, double b0, int sign,
-               cudaStream_t st) {
-  static RowLapPlan P;  // (large: not on the stack)
+               const double *cb_, const double *ca, double cb0, int csign, float *Pt, float *Pb,
+               RowLapGeom *geom, cudaStream_t st) {
+  static RowLapPlan P, PC;  // (large: not on the stack)
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   int rc = rowlap_get_plan(h, w, b, a, k, b0, sign, &P);
   if (rc) return rc;
-  if (P.kind == M32_CPAIR) return launch_rowlap<2, M32_CPAIR>(x, ldx, V, ldv, Vt, Vb, P, st);
+  // the column stage's h along the columns (length h): its border weights
+  rc = rowlap_get_plan(w, h, cb_, ca, k, cb0, csign, &PC);
+  if (rc) return rc;
+  if (P.kind == M32_CPAIR)
+    return launch_rowlap<2, M32_CPAIR>(x, ldx, V, ldv, Vt, Vb, P, PC, Pt, Pb, geom, st);
   switch (k) {
-    case 2: return launch_rowlap<2, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, st);
-    case 3: return launch_rowlap<3, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, st);
-    case 4: return launch_rowlap<4, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, st);
+    case 2: return launch_rowlap<2, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, PC, Pt, Pb, geom, st);
+    case 3: return launch_rowlap<3, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, PC, Pt, Pb, geom, st);
+    case 4: return launch_rowlap<4, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, PC, Pt, Pb, geom, st);
   }
   return fail(VMF_EVALUE, "fp32 row pass supports K = 2..4, got %d", k);
-}
-
-int rowfix_run(const float *Cc, float *Ky, int64_t h, int64_t w, const double *b,
-               const double *a, int k, double b0, int sign, float col_sign, cudaStream_t st) {
-  static RowLapPlan P;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  int rc = rowlap_get_plan(h, w, b, a, k, b0, sign, &P);
-  if (rc) return rc;
-  Launch g(K_COL_SCAN, st);
-  auto go = [&](auto kern) {
-    launch_pdl(kern, dim3(2), dim3(rl_block(P.p.C)), 0, st, P.p, Cc, col_sign, Ky);
-  };
-  if (P.kind == M32_CPAIR)
-    go(rowfix_kernel<2, M32_CPAIR>);
-  else if (k == 2)
-    go(rowfix_kernel<2, M32_JORDAN>);
-  else if (k == 3)
-    go(rowfix_kernel<3, M32_JORDAN>);
-  else
-    go(rowfix_kernel<4, M32_JORDAN>);
-  return cuda_status("row fix");
 }
 
 }  // namespace vmf

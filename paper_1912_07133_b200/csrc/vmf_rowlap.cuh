@@ -171,14 +171,19 @@ int rowlap_get_plan(int64_t h, int64_t w, const double *b, const double *a, int 
                     int sign, RowLapPlan *out);
 bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
                       int sign);
+constexpr int kRLMaxGrid = 1024;  // row-pass CTAs (border partial rows)
+
+// launch geometry of a row pass, for the column scan's partial sums
+struct RowLapGeom {
+  int rows_per, grid, Mhc;
+};
 // X (fp32, pitch ldx; 16-byte aligned rows) -> V = R(Lap5 X) (pitch ldv) with
-// the left / right border terms folded in, and the virtual rows Vt / Vb [w]
+// the left / right border terms folded in, the virtual rows Vt / Vb [w], and
+// per CTA the column stage's border partials Pt / Pb [grid][w] (h_C weights;
+// (cb_, ca, cb0, csign) = the column stage, same order k)
 int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *Vt, float *Vb,
                int64_t h, int64_t w, const double *b, const double *a, int k, double b0, int sign,
-               cudaStream_t st);
-// Ky[2][w] = R_ss(s Cc[0]), R_ss(Cc[1]): the top / bottom border terms of the
-// column direction (Cc from the column scan; s = sign of the column stage)
-int rowfix_run(const float *Cc, float *Ky, int64_t h, int64_t w, const double *b,
-               const double *a, int k, double b0, int sign, float col_sign, cudaStream_t st);
+               const double *cb_, const double *ca, double cb0, int csign, float *Pt, float *Pb,
+               RowLapGeom *geom, cudaStream_t st);
 
 }  // namespace vmf
