@@ -45,6 +45,7 @@ struct CandState {
   // decoupled look-back of the finaliser's large-list path: per CTA
   // (status << 62) | count, status 1 = own count, 2 = inclusive prefix
   unsigned long long look[kFinCtas];
+  unsigned dyflag[128];      // the fp32 row pass's border CTAs (vmf_rowlap.cu)
 };
 
 // A candidate goes to the CTA's shared buffer, or straight to the global list
@@ -102,13 +103,8 @@ int colpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, double *b64,
 // instead of T; x = the frame (border partials), vt / vb = its virtual rows,
 // (rb, ra, rk, rb0, rsign) = the ROW stage (the border rows are row-filtered).
 struct Col32VMode {
-  const float *vt, *vb;       // the row pass's virtual rows
-  const float *pt, *pb;       // its per-CTA border partials [grid][w]
-  RowLapGeom geom;            // its launch geometry
-  const double *rb, *ra;      // the row stage
-  int rk;
-  double rb0;
-  int rsign;
+  const float *vt, *vb;       // the row pass's virtual rows (steady inputs, padded rows)
+  const float *ky;            // its border rows Ky[2][w] (added to L rows 0 / H-1)
 };
 bool colpass32_supported(int64_t h, int64_t w, const IirParams &ip);
 size_t colpass32_workspace_bytes(int64_t h, int64_t w, int k);

@@ -103,7 +103,7 @@ template <int K, bool VM>
 __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
     const float *__restrict__ T, int64_t ldt, Col32Params p, float *__restrict__ R,
     const __grid_constant__ Hm32 hm, const __grid_constant__ CUtensorMap tmap, int use_tma,
-    CandState *__restrict__ cs) {
+    CandState *__restrict__ cs, const float *__restrict__ Vb) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
   float *tile = reinterpret_cast<float *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
@@ -134,8 +134,12 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
       for (int e = threadIdx.x; e < kCarryRows * kCarryStride; e += blockDim.x) {
         const int tr = e / kCarryStride, tc = e - tr * kCarryStride;
         int64_t r = r0 - 1 + tr, c = c0 - 4 + tc;
-        r = r < 0 ? 0 : (r >= H ? H - 1 : r);
         c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+        if (VM && r >= H) {  // below the image the column input is the virtual row Vb
+          tile[e] = __ldg(Vb + c);
+          continue;
+        }
+        r = r < 0 ? 0 : (r >= H ? H - 1 : r);
         tile[e] = __ldg(src + r * ld + c);
       }
       __syncthreads();
@@ -218,28 +222,12 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32_kernel(
 //    one thread per (column, correction) sums the boundary partials in band
 //    order; the start states go back with coalesced stores.
 // ---------------------------------------------------------------------------
-// shared floats before the row-filter scratch: the records, or the staged row
-__host__ __device__ inline int scan32_scratch(int NB, int K, int64_t W) {
-  const int rec = NB * (2 * K + 2) * kScan32Cols, row = (int)(W + W / 32 + 1);
-  return rec > row ? rec : row;
-}
-
-// V mode: the CTA that finishes last (ticket in the CandState) also turns the
-// column sums of the border partials into Ky = R_ss(dy) with the ROW stage
-// (two single-row filters, vmf_rowlap.cuh), so no extra kernel sits on the
-// chain.
-template <int K, bool VM, int RKIND>
+template <int K, bool VM>
 __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict__ T, int64_t ldt,
                                                        Col32Params p, float *__restrict__ R,
                                                        float *__restrict__ Cc,
                                                        const float *__restrict__ Vt,
-                                                       const float *__restrict__ Vb,
-                                                       const __grid_constant__ RowLapParams rp,
-                                                       float *__restrict__ Ky,
-                                                       CandState *__restrict__ cs,
-                                                       const float *__restrict__ Pt,
-                                                       const float *__restrict__ Pb,
-                                                       RowLapGeom geom) {
+                                                       const float *__restrict__ Vb) {
   extern __shared__ __align__(16) float ss[];  // [NB][2K+2][32]
   constexpr int Q = 2 * K + 2;
   const int NB = p.NB;
@@ -247,7 +235,6 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
   const int64_t c0 = (int64_t)blockIdx.x * kScan32Cols;
   const int tid = threadIdx.x;
   __shared__ float es[2][kScan32Cols];
-  __shared__ double psum[6][kScan32Cols];
   pdl_wait();  // records come from the band carries
   const bool full = c0 + kScan32Cols <= W && (W & 3) == 0;
   if (full) {
@@ -308,36 +295,12 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
       for (int i = 0; i < K; ++i) u[i] = un[i];
     }
   } else if (!VM && tid < 4 * kScan32Cols) {  // boundary corrections, band order
+    // (V mode: the row pass computes the column direction's border rows)
     const int which = (tid - 2 * kScan32Cols) / kScan32Cols;
     const int c = tid - (2 + which) * kScan32Cols;
     double a = 0.0;
     for (int b = 0; b < NB; ++b) a += (double)ss[(b * Q + 2 * K + which) * kScan32Cols + c];
     if (c0 + c < W) Cc[(int64_t)which * W + c0 + c] = (float)a;
-  } else if (VM) {  // boundary corrections: the row-pass CTAs' partials, CTA order
-    // 6 groups of 32 threads: (top, bottom) x three contiguous CTA ranges
-    const int g = (tid - 2 * kScan32Cols) / kScan32Cols;
-    const int which = g / 3, part = g % 3;
-    const int c = tid & (kScan32Cols - 1);
-    const int64_t cc = c0 + c < W ? c0 + c : W - 1;
-    const float *P = which == 0 ? Pt : Pb;
-    const int b0 = geom.grid * part / 3, b1 = geom.grid * (part + 1) / 3;
-    double a = 0.0;
-#pragma unroll 4
-    for (int b = b0; b < b1; ++b) {
-      const int64_t rl = (int64_t)b * geom.rows_per;
-      const int64_t rh = rl + geom.rows_per < H ? rl + geom.rows_per : H;
-      const bool in = which == 0 ? rl <= geom.Mhc : rh - 1 >= H - geom.Mhc;
-      if (in) a += (double)__ldg(P + (int64_t)b * W + cc);
-    }
-    psum[g][c] = a;
-  }
-  if (VM) {
-    __syncthreads();
-    if (tid < 2 * kScan32Cols) {
-      const int which = tid / kScan32Cols, c = tid & (kScan32Cols - 1);
-      const double a = (psum[3 * which][c] + psum[3 * which + 1][c]) + psum[3 * which + 2][c];
-      if (c0 + c < W) Cc[(int64_t)which * W + c0 + c] = (float)a;
-    }
   }
   __syncthreads();
   // start states back over the carries (q < 2K), coalesced
@@ -353,44 +316,6 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
       const int r2 = e / kScan32Cols, c = e - r2 * kScan32Cols;
       const int b = r2 / (2 * K), q = r2 - b * 2 * K;
       if (c0 + c < W) R[(int64_t)(b * Q + q) * W + c0 + c] = ss[(b * Q + q) * kScan32Cols + c];
-    }
-  }
-  if (VM) {  // publish this CTA's column sums; the last CTA row-filters them
-    __shared__ int last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) last = atomicAdd(&cs->ticket, 1) == (int)gridDim.x - 1;
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      // staging: the row (coalesced) at n + n/32 (conflict-free chunk reads)
-      float *rowp = ss;  // (the records are back in R: free)
-      float *cf = ss + scan32_scratch(NB, K, W), *cb = cf + 256 * 4;
-      __shared__ float e2[2], dx2[2];
-      const bool live = tid < rp.C;
-      for (int which = 0; which < 2; ++which) {
-        const float s = which == 0 ? p.sign : 1.0f;  // dyt carries the column stage's sign
-        const float *dy = Cc + (int64_t)which * W;
-        for (int n = tid; n < W; n += blockDim.x) rowp[n + (n >> 5)] = s * __ldcg(dy + n);
-        if (tid == 0) dx2[0] = dx2[1] = 0.0f;
-        __syncthreads();
-        if (tid == 0) {
-          e2[0] = rowp[0];
-          e2[1] = rowp[(W - 1) + ((W - 1) >> 5)];
-        }
-        float U[kRChunk], V[kRChunk];
-#pragma unroll
-        for (int t = 0; t < kRChunk; ++t) U[t] = live ? rowp[tid * (kRChunk + 1) + t] : 0.0f;
-        __syncthreads();
-        row_filter<K, RKIND>(rp, U, V, cf, cb, e2, dx2);
-        if (live) {
-#pragma unroll
-          for (int t = 0; t < kRChunk; ++t) rowp[tid * (kRChunk + 1) + t] = V[t];
-        }
-        __syncthreads();
-        for (int n = tid; n < W; n += blockDim.x) Ky[(int64_t)which * W + n] = rowp[n + (n >> 5)];
-        __syncthreads();
-      }
     }
   }
 
@@ -416,7 +341,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     Col32Params p, const float *__restrict__ R, const float *__restrict__ Cc, float ctop_mul,
     CandState *__restrict__ st, int *__restrict__ gy, int *__restrict__ gx,
     float *__restrict__ gv, int gcap, const __grid_constant__ CUtensorMap tmap, int use_tma,
-    int vec_out) {
+    int vec_out, const float *__restrict__ Vb) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
   Col32Smem &S = *reinterpret_cast<Col32Smem *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
@@ -440,10 +365,11 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     for (int e = j; e < kT32Rows * kT32Stride; e += kC32) {
       const int tr = e / kT32Stride, tcn = e - tr * kT32Stride;
       int64_t r = r0 - 2 + tr, c = c0 - 4 + tcn;
-      r = r < 0 ? 0 : (r >= H ? H - 1 : r);
       c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+      const float *src = T + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldt + c;
+      if (VM && r >= H) src = Vb + c;  // below the image: the virtual row Vb
       const unsigned sa = (unsigned)__cvta_generic_to_shared(&S.tile[tr][tcn]);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(T + r * ldt + c));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src));
     }
     asm volatile("cp.async.commit_group;\n" ::);
   }
@@ -647,8 +573,8 @@ size_t colpass32_workspace_bytes(int64_t h, int64_t w, int k) {
   const int64_t NB = cdiv(h, kB32);
   const size_t rec = (size_t)NB * (2 * k + 2) * w * sizeof(float);
   const int64_t gcap = colpass_cand_capacity(h, w);
-  return 4096 + ((rec + 255) & ~(size_t)255) +
-         2 * ((2 * w * sizeof(float) + 255) & ~(size_t)255) + (size_t)gcap * 12 + 1024;
+  return 4096 + ((rec + 255) & ~(size_t)255) + ((2 * w * sizeof(float) + 255) & ~(size_t)255) +
+         (size_t)gcap * 12 + 1024;
 }
 
 static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
@@ -760,9 +686,8 @@ static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
 
 template <int K, int KIND, bool VM>
 static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Col32Plan &P,
-                    const Col32VMode &vm, const RowLapParams &rp, int32_t *det_yx,
-                    float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *ws,
-                    cudaStream_t st) {
+                    const Col32VMode &vm, int32_t *det_yx, float *det_val, int64_t cap,
+                    int64_t *n_det_dev, float *thr_dev, void *ws, cudaStream_t st) {
   const Col32Params &p = P.p;
   const int64_t h = p.H, w = p.W;
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
@@ -771,8 +696,6 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
   float *R = (float *)q;
   q += ((size_t)p.NB * (2 * K + 2) * w * sizeof(float) + 255) & ~(size_t)255;
   float *Cc = (float *)q;
-  q += (2 * w * sizeof(float) + 255) & ~(size_t)255;
-  float *Ky = (float *)q;
   q += (2 * w * sizeof(float) + 255) & ~(size_t)255;
   const int64_t gcap = colpass_cand_capacity(h, w);
   int *gy = (int *)q;
@@ -791,19 +714,18 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
       cudaFuncSetAttribute(colcarry32_kernel<K, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            csm);
     launch_pdl(colcarry32_kernel<K, VM>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
-               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs);
+               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs, vm.vb);
   }
   {
     Launch g(K_COL_SCAN, st);
     // records, then (V mode) the last CTA's row-filter scratch
-    const int ssm = (VM ? scan32_scratch(p.NB, K, w) + 2 * 256 * 4
-                        : p.NB * (2 * K + 2) * kScan32Cols) * (int)sizeof(float);
+    const int ssm = p.NB * (2 * K + 2) * kScan32Cols * (int)sizeof(float);
     static PerDevice attr;
     if (attr.first())
-      cudaFuncSetAttribute(colscan32_kernel<K, VM, KIND>,
+      cudaFuncSetAttribute(colscan32_kernel<K, VM>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    launch_pdl(colscan32_kernel<K, VM, KIND>, dim3((unsigned)cdiv(w, kScan32Cols)), dim3(256),
-               ssm, st, T, ldt, p, R, Cc, vm.vt, vm.vb, rp, Ky, cs, vm.pt, vm.pb, vm.geom);
+    launch_pdl(colscan32_kernel<K, VM>, dim3((unsigned)cdiv(w, kScan32Cols)), dim3(256), ssm, st,
+               T, ldt, p, R, Cc, vm.vt, vm.vb);
   }
   {
     Launch g(K_IIR_COLS_FUSED, st);
@@ -825,9 +747,9 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     // border terms of rows 0 / H-1: T mode adds sign * Cc (T is row-filtered
     // already); V mode adds the row-filtered Ky (sign inside)
     launch_pdl(kern, dim3((unsigned)cdiv(w, kC32Out), (unsigned)p.NB), dim3(kC32), sm, st, T, ldt,
-               L, ldl, p, (const float *)R, (const float *)(VM ? Ky : Cc), VM ? 1.0f : p.sign,
+               L, ldl, p, (const float *)R, (const float *)(VM ? vm.ky : Cc), VM ? 1.0f : p.sign,
                cs, gy, gx, gv, (int)gcap, tmap, use_tma,
-               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0));
+               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0), vm.vb);
   }
   if (p.frac > 0.0f)
     colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, h, w, p.frac, det_yx, det_val, cap, n_det_dev,
@@ -879,19 +801,11 @@ int colpass32_run(const float *T, int64_t ldt, float *L, int64_t ldl, const IirP
   run.p.frac = frac;
   const Col32VMode none = {};
   const Col32VMode &vm = vmode ? *vmode : none;
-  static RowLapPlan rplan;  // V mode: the row stage (border rows are row-filtered)
-  memset(&rplan.p, 0, sizeof(rplan.p));
-  if (vmode) {
-    const int rrc = rowlap_get_plan(h, w, vm.rb, vm.ra, vm.rk, vm.rb0, vm.rsign, &rplan);
-    if (rrc) return rrc;
-    if (rplan.kind != run.kind || vm.rk != ip.K)
-      return fail(VMF_EVALUE, "fp32 path: row and column stages need the same realisation");
-  }
-#define VMF_L32(KK, KD)                                                                         \
-  (vmode ? launch32<KK, KD, true>(T, ldt, L, ldl, run, vm, rplan.p, det_yx, det_val, cap,      \
-                                  n_det_dev, thr_dev, ws, st)                                   \
-         : launch32<KK, KD, false>(T, ldt, L, ldl, run, vm, rplan.p, det_yx, det_val, cap,     \
-                                   n_det_dev, thr_dev, ws, st))
+#define VMF_L32(KK, KD)                                                                       \
+  (vmode ? launch32<KK, KD, true>(T, ldt, L, ldl, run, vm, det_yx, det_val, cap, n_det_dev,  \
+                                  thr_dev, ws, st)                                            \
+         : launch32<KK, KD, false>(T, ldt, L, ldl, run, vm, det_yx, det_val, cap, n_det_dev, \
+                                   thr_dev, ws, st))
   if (run.kind == M32_CPAIR) return VMF_L32(2, M32_CPAIR);
   switch (ip.K) {
     case 2: return VMF_L32(2, M32_JORDAN);

@@ -92,14 +92,65 @@ __device__ __forceinline__ void dx_partials(const RowLapParams &p, const float *
 }
 
 // ---------------------------------------------------------------------------
+// border CTAs: the column direction's border sums, straight from the frame,
+// one thread per column (column stage pc, modal fp32):
+//   Dy[0][c] = s_C sum_{m>=1} h_C(m) G(m, c),  Dy[1][c] = sum h_C(m) G(H-m, c),
+//   G(m, c) = X(m, c) - X(m-1, c), as the zero-state recursion
+//   u <- A u + b G over m = Mh .. 1 (rows 1..Mh, resp. H-Mh..H-1), Dy = c . u.
+// Each CTA raises its flag (kDyDone) when its columns are written; the
+// column carry pass clears the flags again (cand_reset).
+// ---------------------------------------------------------------------------
+constexpr unsigned kDyDone = 0x600dc0deu;
+
+template <int K, int KIND>
+__device__ __forceinline__ void dy_cta(const RowLapParams &p, const RowLapParams &pc,
+                                       float *__restrict__ Dy, unsigned *__restrict__ dyflag,
+                                       int ndy) {
+  const int ncb = ndy / 2;
+  const int which = (int)blockIdx.x / ncb, cbk = (int)blockIdx.x % ncb;
+  const int64_t H = p.H, W = p.W;
+  const int64_t col = (int64_t)cbk * blockDim.x + threadIdx.x;
+  const int64_t cc = col < W ? col : W - 1;
+  const float *X = p.x + cc;  // (column cc of the frame)
+  const int64_t ld = p.ldx;
+  const int Mh = pc.Mh < H - 1 ? pc.Mh : (int)(H - 1);
+  Rec32<K, KIND> u;
+#pragma unroll
+  for (int i = 0; i < K; ++i) u.u[i] = 0.0f;
+  // top: rows m = Mh .. 1 (G(m) = X(m) - X(m-1)); bottom: rows H-Mh .. H-1
+  // (G(H-m), m = Mh .. 1)
+  const int64_t r_first = which == 0 ? Mh : H - Mh, step = which == 0 ? -1 : 1;
+  float xa = __ldg(X + r_first * ld), xb = __ldg(X + (r_first - 1) * ld);
+  int64_t r = r_first;
+#pragma unroll 4
+  for (int m = Mh; m >= 1; --m) {
+    // prefetch the next pair while this G is absorbed
+    const int64_t rn = r + step;
+    float na = 0.0f, nb = 0.0f;
+    if (m > 1) {
+      na = which == 0 ? xb : __ldg(X + rn * ld);
+      nb = which == 0 ? __ldg(X + (rn - 1) * ld) : xa;
+    }
+    u.step(pc, xa - xb);
+    xa = na;
+    xb = nb;
+    r = rn;
+  }
+  if (col < W) Dy[(int64_t)which * W + col] = (which == 0 ? pc.sign : 1.0f) * u.out(pc.c);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicExch(dyflag + which * 64 + cbk, kDyDone);
+}
+
+// ---------------------------------------------------------------------------
 // the row pass
 // ---------------------------------------------------------------------------
 template <int K, int KIND>
 __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
     const __grid_constant__ RowLapParams p, const __grid_constant__ HmRow hm,
-    float *__restrict__ Vt, float *__restrict__ Vb, const __grid_constant__ HmRow hmc, int Mhc,
-    float *__restrict__ Pt, float *__restrict__ Pb) {
+    float *__restrict__ Vt, float *__restrict__ Vb, const __grid_constant__ RowLapParams pc,
+    float *__restrict__ Dy, float *__restrict__ Ky, unsigned *__restrict__ dyflag, int ndy) {
   extern __shared__ __align__(1024) unsigned char smem_rl[];
   __shared__ __align__(8) uint64_t bar[kRLBufs];
   __shared__ float red[16], e2[2], dx2[2];
@@ -115,7 +166,11 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
   float *hs = cb + blockDim.x * K;  // h(0..Mh), padded one per 32
   const int64_t H = p.H;
   const int W = (int)p.W;
-  const int64_t rlo = (int64_t)blockIdx.x * p.rows_per;
+  if ((int)blockIdx.x < ndy) {  // a border CTA (dispatched first: the row CTAs may wait on it)
+    dy_cta<K, KIND>(p, pc, Dy, dyflag, ndy);
+    return;
+  }
+  const int64_t rlo = (int64_t)(blockIdx.x - ndy) * p.rows_per;
   const int64_t rhi = rlo + p.rows_per < H ? rlo + p.rows_per : H;
   if (rlo >= rhi) return;
   const int nrows = (int)(rhi - rlo);
@@ -187,14 +242,35 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     __syncthreads();
   };
   if (rlo == 0) virtual_row(1, Vt);
-  // column-direction border partials over this CTA's rows (registers):
-  // top += h_C(r) G(r) for 1 <= r <= Mhc, bottom += h_C(H - r) G(r) for
-  // r >= H - Mhc; G(r) = X(r) - X(r-1); summed over CTAs by the column scan
-  const bool any_top = rlo <= Mhc, any_bot = rhi - 1 >= H - Mhc;
-  float acct[kRChunk], accb[kRChunk];
+  auto border_row = [&](int which) {
+    const int ncb = ndy / 2;
+    if (c == 0) {
+      for (int q = 0; q < ncb; ++q)
+        while (*(volatile unsigned *)(dyflag + which * 64 + q) != kDyDone) __nanosleep(64);
+    }
+    __syncthreads();
+    __threadfence();
+    float *rowp = reinterpret_cast<float *>(xbuf);  // (the input ring is idle now)
+    const float *dy = Dy + (int64_t)which * W;
+    for (int n = c; n < W; n += blockDim.x) rowp[n + (n >> 5)] = __ldcg(dy + n);
+    if (c == 0) dx2[0] = dx2[1] = 0.0f;
+    __syncthreads();
+    if (c == 0) {
+      e2[0] = rowp[0];
+      e2[1] = rowp[(W - 1) + ((W - 1) >> 5)];
+    }
 #pragma unroll
-  for (int t = 0; t < kRChunk; ++t) acct[t] = accb[t] = 0.0f;
-
+    for (int t = 0; t < kRChunk; ++t) U[t] = live ? rowp[c * (kRChunk + 1) + t] : 0.0f;
+    __syncthreads();
+    row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
+    if (live) {
+#pragma unroll
+      for (int t = 0; t < kRChunk; ++t) rowp[c * (kRChunk + 1) + t] = V[t];
+    }
+    __syncthreads();
+    for (int n = c; n < W; n += blockDim.x) Ky[(int64_t)which * W + n] = rowp[n + (n >> 5)];
+    __syncthreads();
+  };
   for (int i = 0; i < nrows; ++i) {
     const int64_t r = rlo + i;
     // rows r-1, r, r+1 are logical rows i, i+1, i+2
@@ -207,16 +283,6 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
       load_chunk(i, Xu);
 #pragma unroll
       for (int t = 0; t < kRChunk; ++t) U[t] = Xu[t] - X[t];
-      if (r >= 1 && r <= Mhc) {
-        const float w = hmc.h[r];
-#pragma unroll
-        for (int t = 0; t < kRChunk; ++t) acct[t] = fmaf(w, X[t] - Xu[t], acct[t]);
-      }
-      if (r >= 1 && r >= H - Mhc) {
-        const float w = hmc.h[H - r];
-#pragma unroll
-        for (int t = 0; t < kRChunk; ++t) accb[t] = fmaf(w, X[t] - Xu[t], accb[t]);
-      }
       load_chunk(i + 2, Xu);
 #pragma unroll
       for (int t = 0; t < kRChunk; ++t) {
@@ -262,19 +328,10 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     }
   }
   if (rhi == H) virtual_row(nrows, Vb);
-  if (live && (any_top || any_bot)) {
-    float *dt = Pt + (int64_t)blockIdx.x * W + c * kRChunk;
-    float *db = Pb + (int64_t)blockIdx.x * W + c * kRChunk;
-#pragma unroll
-    for (int q = 0; q < kRChunk / 4; ++q) {
-      if (any_top)
-        *reinterpret_cast<float4 *>(dt + 4 * q) =
-            make_float4(acct[4 * q], acct[4 * q + 1], acct[4 * q + 2], acct[4 * q + 3]);
-      if (any_bot)
-        *reinterpret_cast<float4 *>(db + 4 * q) =
-            make_float4(accb[4 * q], accb[4 * q + 1], accb[4 * q + 2], accb[4 * q + 3]);
-    }
-  }
+  // the column direction's border rows: Ky = R_ss(Dy) once the border CTAs
+  // are done (they were dispatched before every row CTA)
+  if (rlo == 0) border_row(0);
+  if (rhi == H) border_row(1);
   pdl_trigger();
   if (c == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
@@ -414,10 +471,11 @@ static size_t rl_smem(int C, int k) {
 }
 
 template <int K, int KIND>
-static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, float *Vt, float *Vb,
-                         RowLapPlan &P, const RowLapPlan &PC, float *Pt, float *Pb,
-                         RowLapGeom *geom, cudaStream_t st) {
+static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows,
+                         RowLapPlan &P, const RowLapPlan &PC, unsigned *dyflag, cudaStream_t st) {
   RowLapParams &p = P.p;
+  p.x = x;
+  p.ldx = ldx;
   CUtensorMap xm, vm;
   memset(&xm, 0, sizeof(xm));
   memset(&vm, 0, sizeof(vm));
@@ -427,6 +485,7 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
     return fail(VMF_EVALUE, "row pass: TMA descriptors unavailable");
   }
   const size_t smem = rl_smem(p.C, K);
+  const int block = rl_block(p.C);
   static std::map<std::pair<int, size_t>, int> slot_cache;
   const int dev = current_device();
   int &slots = slot_cache[std::make_pair(dev, smem)];
@@ -436,42 +495,40 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
                          (int)rl_smem(kRLMaxC, K));
   if (!slots) {
     int occ = 0, nsm = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, rl_block(p.C),
-                                                  smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, block, smem);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
     slots = (occ > 0 ? occ : 1) * nsm;
   }
+  const int ndy = 2 * (int)cdiv(p.W, block);  // border CTAs: (top, bottom) x column blocks
   p.rows_per = (int)cdiv(p.H, slots);
-  const int grid = (int)cdiv(p.H, p.rows_per);
-  if (grid > kRLMaxGrid) return fail(VMF_EVALUE, "row pass: too many CTAs");
-  geom->rows_per = p.rows_per;
-  geom->grid = grid;
-  geom->Mhc = PC.p.Mh;
+  const int grid = ndy + (int)cdiv(p.H, p.rows_per);
+  float *Vt = vrows, *Vb = vrows + p.W, *Dy = vrows + 2 * p.W, *Ky = vrows + 4 * p.W;
   Launch g(K_IIR_ROWS_FUSED, st);
-  launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(rl_block(p.C)), smem, st, xm, vm, p, P.hm,
-             Vt, Vb, PC.hm, PC.p.Mh, Pt, Pb);
+  launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm, vm, p, P.hm, Vt, Vb,
+             PC.p, Dy, Ky, dyflag, ndy);
   return cuda_status("fp32 row pass");
 }
 
-int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *Vt, float *Vb,
-               int64_t h, int64_t w, const double *b, const double *a, int k, double b0, int sign,
-               const double *cb_, const double *ca, double cb0, int csign, float *Pt, float *Pb,
-               RowLapGeom *geom, cudaStream_t st) {
+int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows, int64_t h,
+               int64_t w, const double *b, const double *a, int k, double b0, int sign,
+               const double *cb_, const double *ca, double cb0, int csign, unsigned *dyflag,
+               cudaStream_t st) {
   static RowLapPlan P, PC;  // (large: not on the stack)
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   int rc = rowlap_get_plan(h, w, b, a, k, b0, sign, &P);
   if (rc) return rc;
-  // the column stage's h along the columns (length h): its border weights
+  // the column stage's modal form and border length along the columns
   rc = rowlap_get_plan(w, h, cb_, ca, k, cb0, csign, &PC);
   if (rc) return rc;
+  if (PC.kind != P.kind) return fail(VMF_EVALUE, "fp32 path: stages of different structure");
   if (P.kind == M32_CPAIR)
-    return launch_rowlap<2, M32_CPAIR>(x, ldx, V, ldv, Vt, Vb, P, PC, Pt, Pb, geom, st);
+    return launch_rowlap<2, M32_CPAIR>(x, ldx, V, ldv, vrows, P, PC, dyflag, st);
   switch (k) {
-    case 2: return launch_rowlap<2, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, PC, Pt, Pb, geom, st);
-    case 3: return launch_rowlap<3, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, PC, Pt, Pb, geom, st);
-    case 4: return launch_rowlap<4, M32_JORDAN>(x, ldx, V, ldv, Vt, Vb, P, PC, Pt, Pb, geom, st);
+    case 2: return launch_rowlap<2, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, dyflag, st);
+    case 3: return launch_rowlap<3, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, dyflag, st);
+    case 4: return launch_rowlap<4, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, dyflag, st);
   }
   return fail(VMF_EVALUE, "fp32 row pass supports K = 2..4, got %d", k);
 }

@@ -17,6 +17,8 @@ struct RowLapParams {
   float Iss[4];         // (I - A)^-1 b
   int64_t H, W;
   int C, cpl, rows_per, Mh, K;
+  const float *x;       // the frame (border CTAs), pitch ldx
+  int64_t ldx;
 };
 
 struct HmRow {
@@ -171,19 +173,15 @@ int rowlap_get_plan(int64_t h, int64_t w, const double *b, const double *a, int 
                     int sign, RowLapPlan *out);
 bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
                       int sign);
-constexpr int kRLMaxGrid = 1024;  // row-pass CTAs (border partial rows)
-
-// launch geometry of a row pass, for the column scan's partial sums
-struct RowLapGeom {
-  int rows_per, grid, Mhc;
-};
 // X (fp32, pitch ldx; 16-byte aligned rows) -> V = R(Lap5 X) (pitch ldv) with
-// the left / right border terms folded in, the virtual rows Vt / Vb [w], and
-// per CTA the column stage's border partials Pt / Pb [grid][w] (h_C weights;
-// (cb_, ca, cb0, csign) = the column stage, same order k)
-int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *Vt, float *Vb,
-               int64_t h, int64_t w, const double *b, const double *a, int k, double b0, int sign,
-               const double *cb_, const double *ca, double cb0, int csign, float *Pt, float *Pb,
-               RowLapGeom *geom, cudaStream_t st);
+// the left / right border terms folded in; vrows = [Vt | Vb | Dy(2) | Ky(2)]
+// x w floats: the virtual rows above / below the image and the column
+// direction's border rows Ky = R_ss(Dy) (column stage (cb_, ca, cb0, csign),
+// same order k); dyflag: 128 words of the pass's CandState (cleared by the
+// column carry pass).
+int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows, int64_t h,
+               int64_t w, const double *b, const double *a, int k, double b0, int sign,
+               const double *cb_, const double *ca, double cb0, int csign, unsigned *dyflag,
+               cudaStream_t st);
 
 }  // namespace vmf
