@@ -323,7 +323,7 @@ size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage
     if (c4 > carry) carry = c4;
   }
   return 3 * img + align256(carry) + align256(detect_workspace_bytes(1, h, w)) + 256 +
-         align256(6 * (size_t)w * sizeof(float));  // fp32 row pass: Vt, Vb, Dy, Ky
+         align256((size_t)kRowLapVrows * w * sizeof(float));  // fp32 row pass extras
 }
 
 // The all-fp32 "Laplacian-first" path (vmf_rowlap.cu + vmf_colpass32.cu V
@@ -375,7 +375,7 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   p += img;
   float *L = lap_out ? lap_out : (float *)p;
   p += img;
-  const size_t vrows_b = align256(6 * (size_t)w * sizeof(float));
+  const size_t vrows_b = align256((size_t)kRowLapVrows * w * sizeof(float));
   size_t carry_b = align256(vmf_blur_lap_detect_workspace_bytes(h, w, row_stage, col_stage) -
                             3 * img - align256(detect_workspace_bytes(1, h, w)) - 256 - vrows_b);
   void *carry = p;
@@ -387,13 +387,11 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   IirParams ipc;
   if (lapfirst_ok(x, x_dtype, h, w, ldx, row_stage, col_stage, &ipc)) {
     // V = R(Lap5 X) into T's slot, then the column pass in V mode
-    CandState *cs = (CandState *)(((uintptr_t)carry + 255) & ~(uintptr_t)255);
     rc = rowlap_run((const float *)x, ldx, T, w, vrows, h, w, row_stage->b_plus,
                     row_stage->a_plus, row_stage->n, row_stage->b_zero, row_stage->sign,
-                    col_stage->b_plus, col_stage->a_plus, col_stage->b_zero, col_stage->sign,
-                    cs->dyflag, st);
+                    col_stage->b_plus, col_stage->a_plus, col_stage->b_zero, col_stage->sign, st);
     if (rc) return rc;
-    const Col32VMode vm = {vrows, vrows + w, vrows + 4 * w};
+    const Col32VMode vm = {vrows, vrows + w, vrows + 2 * w};
     rc = colpass32_run(T, w, L, w, ipc, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
                        thr_dev, carry, carry_b, st, &vm);
     if (rc) return rc;

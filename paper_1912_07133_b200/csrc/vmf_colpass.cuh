@@ -45,7 +45,6 @@ struct CandState {
   // decoupled look-back of the finaliser's large-list path: per CTA
   // (status << 62) | count, status 1 = own count, 2 = inclusive prefix
   unsigned long long look[kFinCtas];
-  unsigned dyflag[128];      // the fp32 row pass's border CTAs (vmf_rowlap.cu)
 };
 
 // A candidate goes to the CTA's shared buffer, or straight to the global list

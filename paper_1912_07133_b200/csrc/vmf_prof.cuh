@@ -24,6 +24,7 @@ enum KernelId {
   K_FINALIZE,
   K_COL_CARRY,
   K_COL_SCAN,
+  K_ROW_BORDER,
   K_NUM_IDS
 };
 

@@ -92,54 +92,59 @@ __device__ __forceinline__ void dx_partials(const RowLapParams &p, const float *
 }
 
 // ---------------------------------------------------------------------------
-// border CTAs: the column direction's border sums, straight from the frame,
-// one thread per column (column stage pc, modal fp32):
-//   Dy[0][c] = s_C sum_{m>=1} h_C(m) G(m, c),  Dy[1][c] = sum h_C(m) G(H-m, c),
-//   G(m, c) = X(m, c) - X(m-1, c), as the zero-state recursion
-//   u <- A u + b G over m = Mh .. 1 (rows 1..Mh, resp. H-Mh..H-1), Dy = c . u.
-// Each CTA raises its flag (kDyDone) when its columns are written; the
-// column carry pass clears the flags again (cand_reset).
+// the border kernel: the column direction's border sums, straight from the
+// frame (column stage, modal fp32), in 64-row segments so the whole frame
+// edge is covered by ~1k short CTAs:
+//   Dy[0][c] = s_C sum_{m>=1} h_C(m) G(m, c),  Dy[1][c] = sum_{m>=1} h_C(m) G(H-m, c),
+//   G(m, c) = X(m, c) - X(m-1, c),  h_C(m) = c A^(m-1) b.
+// Segment k covers m = m0 .. m0+63 (m0 = 1 + 64 k): its share is
+// (c A^(m0-1)) . sum_t A^t b G(m0 + t), the inner sum a zero-state
+// recursion; S[which][k][c] holds the shares, summed in k order by the row
+// pass.  It reads only X, so it runs first and the row pass waits for it
+// (griddepcontrol) only before its first store.
 // ---------------------------------------------------------------------------
-constexpr unsigned kDyDone = 0x600dc0deu;
+constexpr int kSeg = 64;
 
 template <int K, int KIND>
-__device__ __forceinline__ void dy_cta(const RowLapParams &p, const RowLapParams &pc,
-                                       float *__restrict__ Dy, unsigned *__restrict__ dyflag,
-                                       int ndy) {
-  const int ncb = ndy / 2;
-  const int which = (int)blockIdx.x / ncb, cbk = (int)blockIdx.x % ncb;
-  const int64_t H = p.H, W = p.W;
-  const int64_t col = (int64_t)cbk * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(128) rowborder_kernel(const __grid_constant__ RowLapParams pc,
+                                                        const __grid_constant__ SegVec sv,
+                                                        const float *__restrict__ X, int64_t ldx,
+                                                        int64_t H, int64_t W,
+                                                        float *__restrict__ S) {
+  pdl_trigger();  // the row pass may launch now; it waits for this grid before its stores
+  const int nseg = sv.nseg;
+  const int which = (int)blockIdx.y / nseg, k = (int)blockIdx.y % nseg;
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t cc = col < W ? col : W - 1;
-  const float *X = p.x + cc;  // (column cc of the frame)
-  const int64_t ld = p.ldx;
-  const int Mh = pc.Mh < H - 1 ? pc.Mh : (int)(H - 1);
+  const int Mh = sv.Mh;
+  const int m0 = 1 + kSeg * k;
+  const int n = (Mh - m0 + 1) < kSeg ? (Mh - m0 + 1) : kSeg;  // m = m0 .. m0+n-1
+  // rows holding G(m) for m = m0 + t: top rows m (G = X(m) - X(m-1)); bottom
+  // rows H - m (G = X(H-m) - X(H-m-1)); the samples X(r) for the n+1 rows
+  // involved, all loaded before the recursion (independent loads)
+  float xs[kSeg + 1];
+  const float *Xc = X + cc;
+#pragma unroll
+  for (int t = 0; t <= kSeg; ++t) {
+    // top: xs[t] = X(m0 - 1 + t); bottom: xs[t] = X(H - m0 - t)
+    const int64_t r = which == 0 ? m0 - 1 + t : H - m0 - t;
+    xs[t] = t <= n ? __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx) : 0.0f;
+  }
   Rec32<K, KIND> u;
 #pragma unroll
   for (int i = 0; i < K; ++i) u.u[i] = 0.0f;
-  // top: rows m = Mh .. 1 (G(m) = X(m) - X(m-1)); bottom: rows H-Mh .. H-1
-  // (G(H-m), m = Mh .. 1)
-  const int64_t r_first = which == 0 ? Mh : H - Mh, step = which == 0 ? -1 : 1;
-  float xa = __ldg(X + r_first * ld), xb = __ldg(X + (r_first - 1) * ld);
-  int64_t r = r_first;
-#pragma unroll 4
-  for (int m = Mh; m >= 1; --m) {
-    // prefetch the next pair while this G is absorbed
-    const int64_t rn = r + step;
-    float na = 0.0f, nb = 0.0f;
-    if (m > 1) {
-      na = which == 0 ? xb : __ldg(X + rn * ld);
-      nb = which == 0 ? __ldg(X + (rn - 1) * ld) : xa;
+#pragma unroll
+  for (int t = kSeg - 1; t >= 0; --t) {
+    if (t < n) {
+      // G(m0 + t): top X(m0+t) - X(m0+t-1) = xs[t+1] - xs[t];
+      //            bottom X(H-m0-t) - X(H-m0-t-1) = xs[t] - xs[t+1]
+      const float g = which == 0 ? xs[t + 1] - xs[t] : xs[t] - xs[t + 1];
+      u.step(pc, g);
     }
-    u.step(pc, xa - xb);
-    xa = na;
-    xb = nb;
-    r = rn;
   }
-  if (col < W) Dy[(int64_t)which * W + col] = (which == 0 ? pc.sign : 1.0f) * u.out(pc.c);
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) atomicExch(dyflag + which * 64 + cbk, kDyDone);
+  float v = u.out(sv.v[k]);
+  if (which == 0) v *= pc.sign;
+  if (col < W) S[((int64_t)which * nseg + k) * W + col] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -149,8 +154,8 @@ template <int K, int KIND>
 __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
     const __grid_constant__ RowLapParams p, const __grid_constant__ HmRow hm,
-    float *__restrict__ Vt, float *__restrict__ Vb, const __grid_constant__ RowLapParams pc,
-    float *__restrict__ Dy, float *__restrict__ Ky, unsigned *__restrict__ dyflag, int ndy) {
+    float *__restrict__ Vt, float *__restrict__ Vb, const float *__restrict__ S, int nseg,
+    float *__restrict__ Ky) {
   extern __shared__ __align__(1024) unsigned char smem_rl[];
   __shared__ __align__(8) uint64_t bar[kRLBufs];
   __shared__ float red[16], e2[2], dx2[2];
@@ -166,11 +171,7 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
   float *hs = cb + blockDim.x * K;  // h(0..Mh), padded one per 32
   const int64_t H = p.H;
   const int W = (int)p.W;
-  if ((int)blockIdx.x < ndy) {  // a border CTA (dispatched first: the row CTAs may wait on it)
-    dy_cta<K, KIND>(p, pc, Dy, dyflag, ndy);
-    return;
-  }
-  const int64_t rlo = (int64_t)(blockIdx.x - ndy) * p.rows_per;
+  const int64_t rlo = (int64_t)blockIdx.x * p.rows_per;
   const int64_t rhi = rlo + p.rows_per < H ? rlo + p.rows_per : H;
   if (rlo >= rhi) return;
   const int nrows = (int)(rhi - rlo);
@@ -242,17 +243,17 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
     __syncthreads();
   };
   if (rlo == 0) virtual_row(1, Vt);
+  // the column direction's border rows Ky = R_ss(dy), dy = sum over the
+  // border kernel's segments (after this CTA's pdl_wait: the border kernel
+  // has completed)
   auto border_row = [&](int which) {
-    const int ncb = ndy / 2;
-    if (c == 0) {
-      for (int q = 0; q < ncb; ++q)
-        while (*(volatile unsigned *)(dyflag + which * 64 + q) != kDyDone) __nanosleep(64);
-    }
     __syncthreads();
-    __threadfence();
     float *rowp = reinterpret_cast<float *>(xbuf);  // (the input ring is idle now)
-    const float *dy = Dy + (int64_t)which * W;
-    for (int n = c; n < W; n += blockDim.x) rowp[n + (n >> 5)] = __ldcg(dy + n);
+    for (int n = c; n < W; n += blockDim.x) {
+      float a = 0.0f;
+      for (int k = 0; k < nseg; ++k) a += __ldg(S + ((int64_t)which * nseg + k) * W + n);
+      rowp[n + (n >> 5)] = a;
+    }
     if (c == 0) dx2[0] = dx2[1] = 0.0f;
     __syncthreads();
     if (c == 0) {
@@ -472,10 +473,8 @@ static size_t rl_smem(int C, int k) {
 
 template <int K, int KIND>
 static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows,
-                         RowLapPlan &P, const RowLapPlan &PC, unsigned *dyflag, cudaStream_t st) {
+                         RowLapPlan &P, const RowLapPlan &PC, const SegVec &sv, cudaStream_t st) {
   RowLapParams &p = P.p;
-  p.x = x;
-  p.ldx = ldx;
   CUtensorMap xm, vm;
   memset(&xm, 0, sizeof(xm));
   memset(&vm, 0, sizeof(vm));
@@ -483,6 +482,12 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
       !make_tmap_rows_swz_f32(&vm, V, p.H, p.W, ldv, 1)) {
     cudaGetLastError();
     return fail(VMF_EVALUE, "row pass: TMA descriptors unavailable");
+  }
+  float *Vt = vrows, *Vb = vrows + p.W, *Ky = vrows + 2 * p.W, *S = vrows + 4 * p.W;
+  {
+    Launch g(K_ROW_BORDER, st);  // the border kernel (reads X only)
+    launch_pdl(rowborder_kernel<K, KIND>, dim3((unsigned)cdiv(p.W, 128), (unsigned)(2 * sv.nseg)),
+               dim3(128), 0, st, PC.p, sv, x, ldx, p.H, p.W, S);
   }
   const size_t smem = rl_smem(p.C, K);
   const int block = rl_block(p.C);
@@ -500,21 +505,43 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
     cudaGetLastError();
     slots = (occ > 0 ? occ : 1) * nsm;
   }
-  const int ndy = 2 * (int)cdiv(p.W, block);  // border CTAs: (top, bottom) x column blocks
   p.rows_per = (int)cdiv(p.H, slots);
-  const int grid = ndy + (int)cdiv(p.H, p.rows_per);
-  float *Vt = vrows, *Vb = vrows + p.W, *Dy = vrows + 2 * p.W, *Ky = vrows + 4 * p.W;
+  const int grid = (int)cdiv(p.H, p.rows_per);
   Launch g(K_IIR_ROWS_FUSED, st);
   launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm, vm, p, P.hm, Vt, Vb,
-             PC.p, Dy, Ky, dyflag, ndy);
+             (const float *)S, sv.nseg, Ky);
   return cuda_status("fp32 row pass");
+}
+
+// segment vectors c A^(m0-1) of the column stage (m0 = 1 + 64 k)
+static int seg_vectors(const double *b, const double *a, int k, const RowLapPlan &PC, SegVec *sv) {
+  Modal M;
+  if (!modal_realise(b, a, k, &M)) return fail(VMF_EVALUE, "no modal realisation");
+  memset(sv, 0, sizeof(*sv));
+  sv->Mh = PC.p.Mh;
+  sv->nseg = (int)cdiv(sv->Mh, kSeg);
+  if (sv->nseg > kMaxSeg) return fail(VMF_EVALUE, "border too long");
+  ld v[4], t[4];
+  for (int i = 0; i < k; ++i) v[i] = M.c[i];  // c A^0
+  int m = 1;
+  for (int s = 0; s < sv->nseg; ++s) {
+    for (; m < 1 + kSeg * s; ++m) {  // v <- v A
+      for (int j = 0; j < k; ++j) {
+        t[j] = 0;
+        for (int i = 0; i < k; ++i) t[j] += v[i] * M.A[i * k + j];
+      }
+      memcpy(v, t, sizeof(ld) * k);
+    }
+    for (int i = 0; i < k; ++i) sv->v[s][i] = (float)v[i];
+  }
+  return VMF_OK;
 }
 
 int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows, int64_t h,
                int64_t w, const double *b, const double *a, int k, double b0, int sign,
-               const double *cb_, const double *ca, double cb0, int csign, unsigned *dyflag,
-               cudaStream_t st) {
+               const double *cb_, const double *ca, double cb0, int csign, cudaStream_t st) {
   static RowLapPlan P, PC;  // (large: not on the stack)
+  static SegVec sv;
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   int rc = rowlap_get_plan(h, w, b, a, k, b0, sign, &P);
@@ -523,12 +550,13 @@ int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows,
   rc = rowlap_get_plan(w, h, cb_, ca, k, cb0, csign, &PC);
   if (rc) return rc;
   if (PC.kind != P.kind) return fail(VMF_EVALUE, "fp32 path: stages of different structure");
-  if (P.kind == M32_CPAIR)
-    return launch_rowlap<2, M32_CPAIR>(x, ldx, V, ldv, vrows, P, PC, dyflag, st);
+  rc = seg_vectors(cb_, ca, k, PC, &sv);
+  if (rc) return rc;
+  if (P.kind == M32_CPAIR) return launch_rowlap<2, M32_CPAIR>(x, ldx, V, ldv, vrows, P, PC, sv, st);
   switch (k) {
-    case 2: return launch_rowlap<2, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, dyflag, st);
-    case 3: return launch_rowlap<3, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, dyflag, st);
-    case 4: return launch_rowlap<4, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, dyflag, st);
+    case 2: return launch_rowlap<2, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, sv, st);
+    case 3: return launch_rowlap<3, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, sv, st);
+    case 4: return launch_rowlap<4, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, sv, st);
   }
   return fail(VMF_EVALUE, "fp32 row pass supports K = 2..4, got %d", k);
 }

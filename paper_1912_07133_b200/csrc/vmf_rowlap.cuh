@@ -17,8 +17,12 @@ struct RowLapParams {
   float Iss[4];         // (I - A)^-1 b
   int64_t H, W;
   int C, cpl, rows_per, Mh, K;
-  const float *x;       // the frame (border CTAs), pitch ldx
-  int64_t ldx;
+};
+
+constexpr int kMaxSeg = 32;  // border segments of 64 rows (Mh <= 2048)
+struct SegVec {             // c A^(m0-1) per border segment (column stage)
+  float v[kMaxSeg][4];
+  int nseg, Mh;
 };
 
 struct HmRow {
@@ -174,14 +178,13 @@ int rowlap_get_plan(int64_t h, int64_t w, const double *b, const double *a, int 
 bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
                       int sign);
 // X (fp32, pitch ldx; 16-byte aligned rows) -> V = R(Lap5 X) (pitch ldv) with
-// the left / right border terms folded in; vrows = [Vt | Vb | Dy(2) | Ky(2)]
-// x w floats: the virtual rows above / below the image and the column
+// the left / right border terms folded in; vrows = [Vt | Vb | Ky(2) | S(2 x 32)]
+// x w floats: the virtual rows above / below the image, the column
 // direction's border rows Ky = R_ss(Dy) (column stage (cb_, ca, cb0, csign),
-// same order k); dyflag: 128 words of the pass's CandState (cleared by the
-// column carry pass).
+// same order k) and the border kernel's segment shares S.
 int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows, int64_t h,
                int64_t w, const double *b, const double *a, int k, double b0, int sign,
-               const double *cb_, const double *ca, double cb0, int csign, unsigned *dyflag,
-               cudaStream_t st);
+               const double *cb_, const double *ca, double cb0, int csign, cudaStream_t st);
+constexpr int kRowLapVrows = 4 + 2 * kMaxSeg;  // floats per column of vrows
 
 }  // namespace vmf
