@@ -71,6 +71,9 @@ struct Col32Params {
   float e1;                 // c A^-1 b
   float b0, sign, lsc, frac;
   float SP[4][kB32 / 2], SQ[4][kB32 / 2];  // folded band-carry weights
+  float Wh[kB32 / 2][4];    // A^t b, t < 32: the half-band carry (V-mode apply)
+  float A32[16];            // A^32 (fp32)
+  float cs[4];              // sign * c
   double AL[16];            // A^64, row-major K x K
   double Iss[4];            // (I - A)^-1 b: steady state per unit input
   int64_t H, W;
@@ -561,6 +564,304 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// V mode (the input V is the fp32 row pass's R(Lap5 X): no horizontal
+// neighbours needed, so the carry reads V straight from global memory)
+// ---------------------------------------------------------------------------
+// Carry: one CTA = 128 columns x one band, 256 threads; thread (j, half)
+// loads its 32 rows (16 folded pairs) with coalesced independent loads --
+// no staging, no shared tile, full occupancy -- rows past H read Vb.
+template <int K>
+__global__ void __launch_bounds__(2 * kC32) colcarry32v_kernel(const float *__restrict__ V,
+                                                             int64_t ldv, Col32Params p,
+                                                             float *__restrict__ R,
+                                                             CandState *__restrict__ cs,
+                                                             const float *__restrict__ Vb) {
+  __shared__ float part[2 * K][kC32];
+  const int j = threadIdx.x & (kC32 - 1), half = threadIdx.x >> 7;
+  const int b = blockIdx.y;
+  const int64_t H = p.H, W = p.W;
+  const int64_t col = (int64_t)blockIdx.x * kC32 + j;
+  const int64_t cc = col < W ? col : W - 1;
+  const int64_t r0 = (int64_t)b * kB32;
+  pdl_wait();  // V comes from the row pass
+  if (blockIdx.x == 0 && blockIdx.y == 0) cand_reset(cs);
+  float xa[kB32 / 4], xb[kB32 / 4];
+  const int t0 = half * (kB32 / 4);
+  auto ld = [&](int64_t r) { return r < H ? __ldg(V + r * ldv + cc) : __ldg(Vb + cc); };
+#pragma unroll
+  for (int t = 0; t < kB32 / 4; ++t) {
+    xa[t] = ld(r0 + t0 + t);
+    xb[t] = ld(r0 + kB32 - 1 - t0 - t);
+  }
+  pdl_trigger();
+  float P[K], Q[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0f;
+  auto run = [&](auto HALF) {  // warp-uniform halves: compile-time weight indices
+    constexpr int h0 = decltype(HALF)::value * (kB32 / 4);
+#pragma unroll
+    for (int t = 0; t < kB32 / 4; ++t) {
+      const float s = xa[t] + xb[t], d = xa[t] - xb[t];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        P[i] = fmaf(p.SP[i][h0 + t], s, P[i]);
+        Q[i] = fmaf(p.SQ[i][h0 + t], d, Q[i]);
+      }
+    }
+  };
+  if (half == 0)
+    run(std::integral_constant<int, 0>());
+  else
+    run(std::integral_constant<int, 1>());
+  if (half == 1) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      part[i][j] = P[i];
+      part[K + i][j] = Q[i];
+    }
+  }
+  __syncthreads();
+  if (half == 0 && col < W) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const float Pt = P[i] + part[i][j], Qt = Q[i] + part[K + i][j];
+      R[ridx(b, i, K, W, col)] = Pt + Qt;      // forward
+      R[ridx(b, K + i, K, W, col)] = Pt - Qt;  // backward
+    }
+  }
+}
+
+// Apply: one CTA = 128 columns x one band; the tile holds V rows r0-1 .. r1
+// (TMA box at column c0-4); L is written in place (each column is private to
+// its thread), then the owned 124 x 64 block leaves fused with the 3x3 NMS.
+// The band is walked in two 32-row halves so only 32 backward values are
+// parked in registers: the top half's backward start comes from a local
+// zero-state carry over the bottom half (ub(r0+32) = A^32 ub(r1) + sum A^t b V).
+struct Col32vSmem {
+  float tile[kB32 + 2][kT32Stride];  // V, then L: rows r0-1 .. r1, cols c0-4 .. c0+127
+  int cy[kCand32], cx[kCand32];
+  float cv[kCand32];
+  int ccount;
+  unsigned int cmax;
+  float thr_end;
+};
+
+template <int K, int KIND, bool LSC>
+__global__ void __launch_bounds__(kC32, 4) colapply32v_kernel(
+    const float *__restrict__ V, int64_t ldv, float *__restrict__ Lout, int64_t ldl,
+    Col32Params p, const float *__restrict__ R, const float *__restrict__ Ky,
+    CandState *__restrict__ st, int *__restrict__ gy, int *__restrict__ gx,
+    float *__restrict__ gv, int gcap, const __grid_constant__ CUtensorMap tmap, int use_tma,
+    int vec_out, const float *__restrict__ Vb) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
+  Col32vSmem &S = *reinterpret_cast<Col32vSmem *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t tbar;
+  const int j = threadIdx.x, lane = j & 31, wid = j >> 5;
+  const int64_t H = p.H, W = p.W;
+  const int64_t c0 = (int64_t)blockIdx.x * kC32Out;
+  const int64_t col = c0 - 2 + j;
+  const int64_t colc = col < 0 ? 0 : (col >= W ? W - 1 : col);
+  const int b = blockIdx.y;
+  const int64_t r0 = (int64_t)b * kB32, r1 = r0 + kB32;
+  const bool tma = use_tma && r0 >= 1 && r1 + 1 <= H && c0 >= 4 && c0 + kC32 <= W;
+  if (tma) {
+    if (j == 0) {
+      mbar_init(&tbar, 1);
+      mbar_expect_tx(&tbar, (unsigned)((kB32 + 2) * kT32Stride * sizeof(float)));
+      tma_load_2d_hint(&S.tile[0][0], &tmap, &tbar, (int)(c0 - 4), (int)(r0 - 1),
+                       l2_policy_evict_first());  // last use of V
+    }
+  } else {  // clamped 4-byte async copies; below the image the virtual row Vb
+    for (int e = j; e < (kB32 + 2) * kT32Stride; e += kC32) {
+      const int tr = e / kT32Stride, tcn = e - tr * kT32Stride;
+      int64_t r = r0 - 1 + tr, c = c0 - 4 + tcn;
+      c = c < 0 ? 0 : (c >= W ? W - 1 : c);
+      const float *src = r >= H ? Vb + c : V + (r < 0 ? 0 : r) * ldv + c;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(&S.tile[tr][tcn]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  if (j == 0) {
+    S.ccount = 0;
+    S.cmax = 0u;
+  }
+  pdl_wait();  // band start states, Ky and the CandState come from earlier kernels
+  const float gbound = __uint_as_float(st->absmax_bits);
+  Rec32<K, KIND> rf, rbt;
+  float ub1[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    rf.u[i] = R[ridx(b, i, K, W, colc)];
+    ub1[i] = R[ridx(b, K + i, K, W, colc)];
+  }
+  const float ctop = r0 == 0 ? Ky[colc] : 0.0f;
+  const float cbot = (H - 1 >= r0 - 1 && H - 1 <= r1) ? Ky[W + colc] : 0.0f;
+  if (tma) {
+    __syncthreads();
+    mbar_wait(&tbar, 0);
+  } else {
+    asm volatile("cp.async.wait_group 0;\n" ::);
+  }
+  __syncthreads();
+  float *tc = &S.tile[0][j + 2];  // tile row q <-> image row r0 - 1 + q
+#define TV(q) tc[(q) * kT32Stride]
+  const float b0 = p.b0, lsc = p.lsc;
+  float tmax = 0.0f;
+  auto fin = [&](float v, int64_t r) {  // corrections, scale, running max
+    if (r == 0) v += ctop;
+    if (r == H - 1) v -= cbot;
+    if (LSC) v *= lsc;
+    return v;
+  };
+  // top half's backward start: A^32 ub(r1) + sum_{t<32} A^t b V(r0 + 32 + t)
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    float a = 0.0f;
+#pragma unroll
+    for (int m = 0; m < K; ++m) a = fmaf(p.A32[i * K + m], ub1[m], a);
+    rbt.u[i] = a;
+  }
+#pragma unroll
+  for (int t = 0; t < kB32 / 2; ++t) {
+    const float v = TV(kB32 / 2 + 1 + t);
+#pragma unroll
+    for (int i = 0; i < K; ++i) rbt.u[i] = fmaf(p.Wh[t][i], v, rbt.u[i]);
+  }
+  float park[kB32 / 2];
+  // ---- top half: rows r0 .. r0+31 (and the halo row r0-1)
+#pragma unroll
+  for (int t = kB32 / 2 - 1; t >= 0; --t) {
+    const float v = TV(t + 1);
+    park[t] = rbt.out_from(p.cs, b0 * v);  // b0 V + s y-
+    rbt.step(p, v);
+  }
+  if (r0 > 0) {  // L(r0-1): y+(r0-1) = c A^-1 uf(r0-1) - e1 V(r0-1); y-(r0-1) = c ub(r0)
+    const float v = TV(0);
+    const float w = fmaf(-p.e1, v, rf.out_from(p.ci, rbt.out_from(p.cs, b0 * v)));
+    TV(0) = fin(w, r0 - 1);
+  }
+#pragma unroll
+  for (int t = 0; t < kB32 / 2; ++t) {
+    const float v = TV(t + 1);
+    const float w = fin(rf.out_from(p.c, park[t]), r0 + t);
+    rf.step(p, v);
+    TV(t + 1) = w;
+    if (r0 + t < H) tmax = fmaxf(tmax, fabsf(w));
+  }
+  // ---- bottom half: rows r0+32 .. r1-1 (and the halo row r1)
+  Rec32<K, KIND> rb;
+#pragma unroll
+  for (int i = 0; i < K; ++i) rb.u[i] = ub1[i];
+  float ym_below;
+  {
+    const float v = TV(kB32 + 1);  // y-(r1) = c A^-1 ub(r1) - e1 V(r1)
+    ym_below = fmaf(-p.e1, v, rb.out(p.ci));
+  }
+#pragma unroll
+  for (int t = kB32 / 2 - 1; t >= 0; --t) {
+    const float v = TV(kB32 / 2 + 1 + t);
+    park[t] = rb.out_from(p.cs, b0 * v);
+    rb.step(p, v);
+  }
+#pragma unroll
+  for (int t = 0; t < kB32 / 2; ++t) {
+    const float v = TV(kB32 / 2 + 1 + t);
+    const float w = fin(rf.out_from(p.c, park[t]), r0 + kB32 / 2 + t);
+    rf.step(p, v);
+    TV(kB32 / 2 + 1 + t) = w;
+    if (r0 + kB32 / 2 + t < H) tmax = fmaxf(tmax, fabsf(w));
+  }
+  {
+    const float v = TV(kB32 + 1);
+    const float w = rf.out_from(p.c, fmaf(b0, v, p.sign * ym_below));
+    TV(kB32 + 1) = fin(w, r1);
+  }
+#undef TV
+  pdl_trigger();
+  if (j < 2 || j >= kC32 - 2 || col >= W) tmax = 0.0f;
+  tmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+  if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
+  __syncthreads();
+  if (j == 0) atomicMax(&st->absmax_bits, S.cmax);
+  const float gnow = fmaxf(gbound, __uint_as_float(*(volatile unsigned *)&st->absmax_bits));
+  {
+    const int64_t rhi = r1 < H ? r1 : H;
+    const int nrow = (int)(rhi - r0);
+    const int ncol = (int)(W - c0 < kC32Out ? W - c0 : kC32Out);
+    const float th = p.frac > 0.0f ? p.frac * fmaxf(__uint_as_float(S.cmax), gnow)
+                                   : __int_as_float(0x7f800000);
+    auto test = [&](int q, int c, float v) {  // tile row q + 1, tile column 4 + c
+      const int64_t r = r0 + q, cc = c0 + c;
+      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return;
+      const int tr = q + 1, tcn = 4 + c;
+      bool gt = true, lt = true;
+#pragma unroll
+      for (int di = -1; di <= 1; ++di)
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj) {
+          if (!di && !dj) continue;
+          const float w = S.tile[tr + di][tcn + dj];
+          gt &= v > w;
+          lt &= v < w;
+        }
+      if ((gt && v >= th) || (lt && -v >= th))
+        cand_push(&S.ccount, S.cy, S.cx, S.cv, kCand32, st, gy, gx, gv, gcap, (int)r, (int)cc, v);
+    };
+    if (vec_out && ncol == kC32Out) {
+      const bool act = lane < kC32Out / 4;
+      const uint64_t lpol = l2_policy_evict_first();
+      float *dst = Lout + r0 * ldl + c0 + 4 * lane;
+#pragma unroll 4
+      for (int q = wid; q < nrow; q += kC32 / 32) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (act) {
+          v = *reinterpret_cast<const float4 *>(&S.tile[q + 1][4 + 4 * lane]);
+          st_v4_hint(dst + q * ldl, v, lpol);
+        }
+        const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+        if (m4 >= th) {
+          if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
+          if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
+          if (fabsf(v.z) >= th) test(q, 4 * lane + 2, v.z);
+          if (fabsf(v.w) >= th) test(q, 4 * lane + 3, v.w);
+        }
+      }
+    } else {
+      for (int q = wid; q < nrow; q += kC32 / 32)
+        for (int cl = 0; cl < ncol; cl += 32) {
+          const int c = cl + lane;
+          float v = 0.0f;
+          if (c < ncol) {
+            v = S.tile[q + 1][4 + c];
+            Lout[(r0 + q) * ldl + c0 + c] = v;
+          }
+          if (c < ncol && fabsf(v) >= th) test(q, c, v);
+        }
+    }
+  }
+  __syncthreads();
+  if (j == 0) {
+    const unsigned old = atomicMax(&st->absmax_bits, S.cmax);
+    S.thr_end = p.frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
+  }
+  __syncthreads();
+  const int n = S.ccount < kCand32 ? S.ccount : kCand32;
+  for (int q = j; q < n; q += kC32) {
+    if (!(fabsf(S.cv[q]) >= S.thr_end)) continue;
+    const int k = atomicAdd(&st->count, 1);
+    if (k < gcap) {
+      gy[k] = S.cy[q];
+      gx[k] = S.cx[q];
+      gv[k] = S.cv[q];
+    } else {
+      st->overflow = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host: modal realisation (long double), plan, launches
 // ---------------------------------------------------------------------------
 struct Col32Plan {
@@ -625,8 +926,15 @@ static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
   for (int i = 0; i < k; ++i)
     for (int t = 0; t < kB32 / 2; ++t) {
       p.SP[i][t] = (float)(0.5L * (Wt[t][i] + Wt[kB32 - 1 - t][i]));
+      p.Wh[t][i] = (float)Wt[t][i];
       p.SQ[i][t] = (float)(0.5L * (Wt[kB32 - 1 - t][i] - Wt[t][i]));
     }
+  {
+    ld A32[16];
+    matpow(M.A, kB32 / 2, A32, k);
+    for (int i = 0; i < k * k; ++i) p.A32[i] = (float)A32[i];
+    for (int i = 0; i < k; ++i) p.cs[i] = (float)(ip.sign * M.c[i]);
+  }
   ld AL[16];
   matpow(M.A, kB32, AL, k);
   for (int i = 0; i < k * k; ++i) p.AL[i] = (double)AL[i];
@@ -713,8 +1021,12 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     if (attr.first())
       cudaFuncSetAttribute(colcarry32_kernel<K, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            csm);
-    launch_pdl(colcarry32_kernel<K, VM>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
-               dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs, vm.vb);
+    if (VM)
+      launch_pdl(colcarry32v_kernel<K>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
+                 dim3(2 * kC32), 0, st, T, ldt, p, R, cs, vm.vb);
+    else
+      launch_pdl(colcarry32_kernel<K, VM>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
+                 dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs, vm.vb);
   }
   {
     Launch g(K_COL_SCAN, st);
@@ -727,7 +1039,26 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     launch_pdl(colscan32_kernel<K, VM>, dim3((unsigned)cdiv(w, kScan32Cols)), dim3(256), ssm, st,
                T, ldt, p, R, Cc, vm.vt, vm.vb);
   }
-  {
+  if (VM) {
+    Launch g(K_IIR_COLS_FUSED, st);
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    const int use_tma = make_tmap_2d_f32(&tmap, T, h, w, ldt, kT32Stride, kB32 + 2) &&
+                        !getenv("VMF_NO_TMA");
+    cudaGetLastError();
+    const int sm = (int)sizeof(Col32vSmem) + 128;
+    static PerDevice attr;
+    if (attr.first()) {
+      cudaFuncSetAttribute(colapply32v_kernel<K, KIND, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      cudaFuncSetAttribute(colapply32v_kernel<K, KIND, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    }
+    auto kern = p.lsc == 1.0f ? colapply32v_kernel<K, KIND, false> : colapply32v_kernel<K, KIND, true>;
+    launch_pdl(kern, dim3((unsigned)cdiv(w, kC32Out), (unsigned)p.NB), dim3(kC32), sm, st, T, ldt,
+               L, ldl, p, (const float *)R, vm.ky, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
+               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0), vm.vb);
+  } else {
     Launch g(K_IIR_COLS_FUSED, st);
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));

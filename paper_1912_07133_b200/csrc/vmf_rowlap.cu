@@ -43,7 +43,6 @@ namespace vmf {
 
 constexpr int kRLMaxC = 256;   // W <= 8192
 constexpr int kRLBufs = 4;     // input ring
-constexpr int kRLOut = 2;      // output ring
 
 // TMA SWIZZLE_128B layout of a [C][32] fp32 row (see vmf_rowpass.cu)
 struct SwzRow32 {
@@ -111,7 +110,8 @@ __global__ void __launch_bounds__(128) rowborder_kernel(const __grid_constant__ 
                                                         const float *__restrict__ X, int64_t ldx,
                                                         int64_t H, int64_t W,
                                                         float *__restrict__ S) {
-  pdl_trigger();  // the row pass may launch now; it waits for this grid before its stores
+  // (no early trigger: the row pass's CTAs would take the registers this
+  // grid needs and stretch it; it launches when this grid completes)
   const int nseg = sv.nseg;
   const int which = (int)blockIdx.y / nseg, k = (int)blockIdx.y % nseg;
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(128) rowborder_kernel(const __grid_constant__ 
 // the row pass
 // ---------------------------------------------------------------------------
 template <int K, int KIND>
-__global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
+__global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
     const __grid_constant__ RowLapParams p, const __grid_constant__ HmRow hm,
     float *__restrict__ Vt, float *__restrict__ Vb, const float *__restrict__ S, int nseg,
@@ -165,8 +165,8 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
   const int rowb = (rowbytes + 1023) & ~1023;  // buffer spacing: SWIZZLE_128B needs 1024-byte bases
   const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_rl);
   char *xbuf = reinterpret_cast<char *>(smem_rl) + ((1024u - (sb & 1023u)) & 1023u);
-  char *obuf = xbuf + kRLBufs * rowb;
-  float *cf = reinterpret_cast<float *>(obuf + kRLOut * rowb);
+  // (V(r) leaves from the slot of row r-1, dead once U(r) is formed)
+  float *cf = reinterpret_cast<float *>(xbuf + kRLBufs * rowb);
   float *cb = cf + blockDim.x * K;
   float *hs = cb + blockDim.x * K;  // h(0..Mh), padded one per 32
   const int64_t H = p.H;
@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
   // border kernel's segments (after this CTA's pdl_wait: the border kernel
   // has completed)
   auto border_row = [&](int which) {
+    if (c == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     __syncthreads();
     float *rowp = reinterpret_cast<float *>(xbuf);  // (the input ring is idle now)
     for (int n = c; n < W; n += blockDim.x) {
@@ -274,8 +275,13 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
   };
   for (int i = 0; i < nrows; ++i) {
     const int64_t r = rlo + i;
-    // rows r-1, r, r+1 are logical rows i, i+1, i+2
-    wait_row(i + 2 <= nrows + 1 ? i + 2 : nrows + 1);
+    // rows r-1, r, r+1 are logical rows i, i+1, i+2; the prefetch of row r+2
+    // goes to the slot of row r-2, which V(r-1) left from: drained?
+    if (c == 0 && i + 3 <= nrows + 1) {
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      issue(i + 3);
+    }
+    wait_row(i + 2);
     float xl, xr;
     load_chunk(i + 1, X);
     halos(i + 1, X, xl, xr);
@@ -298,13 +304,9 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
       const float xc = X[c == 0 ? 0 : kRChunk - 1];
       e2[c == 0 ? 0 : 1] = (ru.ld(n) - xc) + (rd.ld(n) - xc);
     }
+    row_carry32<K>(p, U, cf, cb);
+    __syncthreads();  // X of this row read; carries, e2, red published
     if (c == 0) {
-      // the output buffer this row fills was stored two rows ago: drained?
-      asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(kRLOut - 1) : "memory");
-    }
-    __syncthreads();  // X slots of this row read; e2 / red published; obuf free
-    if (c == 0) {
-      if (i + 3 <= nrows + 1) issue(i + 3);  // into the slot of row r-2 (free)
       float a = 0.0f, b = 0.0f;
       for (int w = 0; w < nwarp; ++w) {
         a += red[w];
@@ -313,18 +315,19 @@ __global__ void __launch_bounds__(kRLMaxC, 1) rowlap_kernel(
       dx2[0] = p.sign * a;
       dx2[1] = b;
     }
-    row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
-    const SwzRow32 ob{obuf + (i % kRLOut) * rowb};
+    row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2);
+    char *ob = xbuf + (i % kRLBufs) * rowb;  // the slot of row r-1
     if (live) {
+      const SwzRow32 o{ob};
 #pragma unroll
       for (int q = 0; q < kRChunk / 4; ++q)
-        ob.st4(c, q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]));
+        o.st4(c, q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]));
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
     __syncthreads();
     if (c == 0) {
       if (i == 0) pdl_wait();  // V may still be read by the previous scale's column pass
-      tma_store_3d_hint(&vmap, obuf + (i % kRLOut) * rowb, 0, 0, (int)r, l2_policy_evict_last());
+      tma_store_3d_hint(&vmap, ob, 0, 0, (int)r, l2_policy_evict_last());
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
   }
@@ -428,7 +431,9 @@ static int rl_plan(RowLapPlan *P, int64_t h, int64_t w, const double *b, const d
     }
     int64_t Mh = (int64_t)hv.size() - 1;
     ld tail = 0;
-    while (Mh > 1 && tail + fabsl(hv[Mh]) < 1e-9L * tot) tail += fabsl(hv[Mh--]);
+    // (border terms: a tail below 1e-8 of sum |h| is ~1e-8 of the edge
+    // gradients -- far below fp32 L)
+    while (Mh > 1 && tail + fabsl(hv[Mh]) < 1e-8L * tot) tail += fabsl(hv[Mh--]);
     p.Mh = (int)Mh;
     memset(&P->hm, 0, sizeof(P->hm));
     for (int64_t m = 1; m <= Mh; ++m) P->hm.h[m] = (float)hv[m];
@@ -466,9 +471,9 @@ bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, in
 
 static int rl_block(int C) { return (C + 31) / 32 * 32; }
 
-static size_t rl_smem(int C, int k) {
-  return 1024 + (size_t)(kRLBufs + kRLOut) * ((C * 128 + 1023) & ~1023) + 2 * (size_t)rl_block(C) * k * sizeof(float) +
-         (size_t)(kHmRowMax + 1 + kHmRowMax / 32 + 2) * sizeof(float);
+static size_t rl_smem(int C, int k, int Mh) {
+  return 1024 + (size_t)kRLBufs * ((C * 128 + 1023) & ~1023) +
+         2 * (size_t)rl_block(C) * k * sizeof(float) + (size_t)(Mh + 1 + Mh / 32 + 2) * sizeof(float);
 }
 
 template <int K, int KIND>
@@ -489,7 +494,7 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
     launch_pdl(rowborder_kernel<K, KIND>, dim3((unsigned)cdiv(p.W, 128), (unsigned)(2 * sv.nseg)),
                dim3(128), 0, st, PC.p, sv, x, ldx, p.H, p.W, S);
   }
-  const size_t smem = rl_smem(p.C, K);
+  const size_t smem = rl_smem(p.C, K, p.Mh);
   const int block = rl_block(p.C);
   static std::map<std::pair<int, size_t>, int> slot_cache;
   const int dev = current_device();
@@ -497,7 +502,7 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
   static PerDevice attr;
   if (attr.first())  // the largest footprint (C = 256), so every width may launch
     cudaFuncSetAttribute(rowlap_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)rl_smem(kRLMaxC, K));
+                         (int)rl_smem(kRLMaxC, K, kHmRowMax));
   if (!slots) {
     int occ = 0, nsm = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, block, smem);

@@ -37,16 +37,16 @@ struct RowLapPlan {
 
 constexpr int kRChunk = 32;
 
-// One row through R: U (registers, this thread's chunk) -> V (registers).
-// eL / eR: steady-state inputs left / right of the row; cf / cb: [C][K]
-// scratch; dx[2]: the row's border terms (added to V(0) / subtracted from
-// V(W-1)) -- published in smem by the caller before the first barrier.
-// Contains two block barriers.
-template <int K, int KIND>
-__device__ __forceinline__ void row_filter(const RowLapParams &p, const float (&U)[kRChunk],
-                                           float (&V)[kRChunk], float *cf, float *cb,
-                                           const float *e2, const float *dx2) {
-  const int c = threadIdx.x, C = p.C, lane = c & 31, warp = c >> 5;
+// One row through R, in two phases around a block barrier:
+//   row_carry32: this thread's chunk U -> its zero-state carries in cf / cb;
+//   row_scan_walk32: (after the barrier) chunk scans, then the walks -> V.
+// e2: steady-state inputs left / right of the row; cf / cb: [blockDim][K]
+// scratch; dx2: the row's border terms (added to V(0) / subtracted from
+// V(W-1)), read only after the scan's barrier.
+template <int K>
+__device__ __forceinline__ void row_carry32(const RowLapParams &p, const float (&U)[kRChunk],
+                                            float *cf, float *cb) {
+  const int c = threadIdx.x;
   // zero-state chunk carries: forward end state P + Q, backward start P - Q
   {
     float P[K], Q[K];
@@ -67,7 +67,13 @@ __device__ __forceinline__ void row_filter(const RowLapParams &p, const float (&
       cb[c * K + i] = P[i] - Q[i];
     }
   }
-  __syncthreads();
+}
+
+template <int K, int KIND>
+__device__ __forceinline__ void row_scan_walk32(const RowLapParams &p, const float (&U)[kRChunk],
+                                                float (&V)[kRChunk], float *cf, float *cb,
+                                                const float *e2, const float *dx2) {
+  const int c = threadIdx.x, C = p.C, lane = c & 31, warp = c >> 5;
   // chunk scans: task 0 forward (chunks 0..C-1), task 1 backward
   for (int task = warp; task < 2; task += (int)(blockDim.x >> 5)) {
     float *cc = task == 0 ? cf : cb;
@@ -175,6 +181,17 @@ __device__ __forceinline__ void row_filter(const RowLapParams &p, const float (&
 
 int rowlap_get_plan(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
                     int sign, RowLapPlan *out);
+
+// both phases (contains two block barriers)
+template <int K, int KIND>
+__device__ __forceinline__ void row_filter(const RowLapParams &p, const float (&U)[kRChunk],
+                                           float (&V)[kRChunk], float *cf, float *cb,
+                                           const float *e2, const float *dx2) {
+  row_carry32<K>(p, U, cf, cb);
+  __syncthreads();
+  row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2);
+}
+
 bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
                       int sign);
 // X (fp32, pitch ldx; 16-byte aligned rows) -> V = R(Lap5 X) (pitch ldv) with
