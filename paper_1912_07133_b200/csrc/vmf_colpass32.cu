@@ -587,11 +587,20 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32v_kernel(const float *__re
   if (blockIdx.x == 0 && blockIdx.y == 0) cand_reset(cs);
   float xa[kB32 / 4], xb[kB32 / 4];
   const int t0 = half * (kB32 / 4);
-  auto ld = [&](int64_t r) { return r < H ? __ldg(V + r * ldv + cc) : __ldg(Vb + cc); };
+  if (r0 + kB32 <= H) {  // (CTA-uniform) a full band: pointer steps, no row checks
+    const float *pa = V + (r0 + t0) * ldv + cc, *pb = V + (r0 + kB32 - 1 - t0) * ldv + cc;
 #pragma unroll
-  for (int t = 0; t < kB32 / 4; ++t) {
-    xa[t] = ld(r0 + t0 + t);
-    xb[t] = ld(r0 + kB32 - 1 - t0 - t);
+    for (int t = 0; t < kB32 / 4; ++t) {
+      xa[t] = __ldg(pa + t * ldv);
+      xb[t] = __ldg(pb - t * ldv);
+    }
+  } else {  // the last band: rows past H read the virtual row Vb
+    auto ld = [&](int64_t r) { return r < H ? __ldg(V + r * ldv + cc) : __ldg(Vb + cc); };
+#pragma unroll
+    for (int t = 0; t < kB32 / 4; ++t) {
+      xa[t] = ld(r0 + t0 + t);
+      xb[t] = ld(r0 + kB32 - 1 - t0 - t);
+    }
   }
   pdl_trigger();
   float P[K], Q[K];
@@ -709,12 +718,9 @@ __global__ void __launch_bounds__(kC32, 4) colapply32v_kernel(
 #define TV(q) tc[(q) * kT32Stride]
   const float b0 = p.b0, lsc = p.lsc;
   float tmax = 0.0f;
-  auto fin = [&](float v, int64_t r) {  // corrections, scale, running max
-    if (r == 0) v += ctop;
-    if (r == H - 1) v -= cbot;
-    if (LSC) v *= lsc;
-    return v;
-  };
+  auto fin = [&](float v) { return LSC ? v * lsc : v; };
+  // rows of this band (tile rows 1 .. nval) that lie inside the image
+  const int nval = (int)(H - r0 < kB32 ? H - r0 : kB32);
   // top half's backward start: A^32 ub(r1) + sum_{t<32} A^t b V(r0 + 32 + t)
 #pragma unroll
   for (int i = 0; i < K; ++i) {
@@ -740,15 +746,15 @@ __global__ void __launch_bounds__(kC32, 4) colapply32v_kernel(
   if (r0 > 0) {  // L(r0-1): y+(r0-1) = c A^-1 uf(r0-1) - e1 V(r0-1); y-(r0-1) = c ub(r0)
     const float v = TV(0);
     const float w = fmaf(-p.e1, v, rf.out_from(p.ci, rbt.out_from(p.cs, b0 * v)));
-    TV(0) = fin(w, r0 - 1);
+    TV(0) = fin(w);
   }
 #pragma unroll
   for (int t = 0; t < kB32 / 2; ++t) {
     const float v = TV(t + 1);
-    const float w = fin(rf.out_from(p.c, park[t]), r0 + t);
+    const float w = fin(rf.out_from(p.c, park[t]));
     rf.step(p, v);
     TV(t + 1) = w;
-    if (r0 + t < H) tmax = fmaxf(tmax, fabsf(w));
+    if (t < nval) tmax = fmaxf(tmax, fabsf(w));
   }
   // ---- bottom half: rows r0+32 .. r1-1 (and the halo row r1)
   Rec32<K, KIND> rb;
@@ -768,15 +774,27 @@ __global__ void __launch_bounds__(kC32, 4) colapply32v_kernel(
 #pragma unroll
   for (int t = 0; t < kB32 / 2; ++t) {
     const float v = TV(kB32 / 2 + 1 + t);
-    const float w = fin(rf.out_from(p.c, park[t]), r0 + kB32 / 2 + t);
+    const float w = fin(rf.out_from(p.c, park[t]));
     rf.step(p, v);
     TV(kB32 / 2 + 1 + t) = w;
-    if (r0 + kB32 / 2 + t < H) tmax = fmaxf(tmax, fabsf(w));
+    if (kB32 / 2 + t < nval) tmax = fmaxf(tmax, fabsf(w));
   }
   {
     const float v = TV(kB32 + 1);
     const float w = rf.out_from(p.c, fmaf(b0, v, p.sign * ym_below));
-    TV(kB32 + 1) = fin(w, r1);
+    TV(kB32 + 1) = fin(w);
+  }
+  // the border rows' terms: L(0) += Ky[0], L(H-1) -= Ky[1] (tile row r - r0 + 1)
+  if (r0 == 0) {
+    const float w = TV(1) + fin(ctop);
+    TV(1) = w;
+    tmax = fmaxf(tmax, fabsf(w));
+  }
+  if (H - 1 >= r0 - 1 && H - 1 <= r1) {
+    const int q = (int)(H - 1 - r0 + 1);
+    const float w = TV(q) - fin(cbot);
+    TV(q) = w;
+    if (q >= 1 && q <= nval) tmax = fmaxf(tmax, fabsf(w));
   }
 #undef TV
   pdl_trigger();

@@ -42,7 +42,7 @@
 namespace vmf {
 
 constexpr int kRLMaxC = 256;   // W <= 8192
-constexpr int kRLBufs = 4;     // input ring
+constexpr int kRLBufs = 3;     // input ring: rows r-1, r, r+1 (r+2 lands in r-1's slot)
 
 // TMA SWIZZLE_128B layout of a [C][32] fp32 row (see vmf_rowpass.cu)
 struct SwzRow32 {
@@ -60,35 +60,6 @@ struct SwzRow32 {
 };
 
 __device__ __forceinline__ int hidx(int n) { return n + (n >> 5); }  // padded h() copy
-
-// Border-term partials of this thread's chunk: sum over its samples n >= 1
-// of h(n) G(n) (n <= Mh) and h(W - n) G(n) (W - n <= Mh), G(n) = X(n) - X(n-1),
-// reduced over the CTA in a fixed order into red[0..nwarp) / red[8..).
-__device__ __forceinline__ void dx_partials(const RowLapParams &p, const float *hs,
-                                            const float (&X)[kRChunk], float xl, float *red) {
-  const int c = threadIdx.x, lane = c & 31, warp = c >> 5;
-  const int n0 = c * kRChunk;
-  const int W = (int)p.W, Mh = p.Mh;
-  float pl = 0.0f, pr = 0.0f;
-  if (n0 < W && (n0 <= Mh || n0 + kRChunk - 1 >= W - Mh)) {
-#pragma unroll
-    for (int t = 0; t < kRChunk; ++t) {
-      const int n = n0 + t;
-      const float g = X[t] - (t ? X[t - 1] : xl);
-      if (n >= 1 && n <= Mh) pl = fmaf(hs[hidx(n)], g, pl);
-      if (n >= 1 && W - n <= Mh) pr = fmaf(hs[hidx(W - n)], g, pr);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    pl += __shfl_xor_sync(0xffffffffu, pl, o);
-    pr += __shfl_xor_sync(0xffffffffu, pr, o);
-  }
-  if (lane == 0) {
-    red[warp] = pl;
-    red[8 + warp] = pr;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // the border kernel: the column direction's border sums, straight from the
@@ -150,10 +121,60 @@ __global__ void __launch_bounds__(128) rowborder_kernel(const __grid_constant__ 
 // ---------------------------------------------------------------------------
 // the row pass
 // ---------------------------------------------------------------------------
+// Left / right border terms of one row: dxl = s sum_{n>=1} h(n) G(n),
+// dxr = sum_{m>=1} h(m) G(W-m), G(n) = X(n) - X(n-1).  Per chunk (samples
+// n = n0+1 .. n0+32) the sums are modal: h(n0+1+t) = (c A^n0) A^t b and
+// h(W-n0-1-t) = (c A^(W-n0-33)) A^(31-t) b, so each chunk forms two zero-state
+// sums with the uniform weights A^t b and dots them with its own vectors
+// vl(c) = c A^n0, vr(c) = c A^(W-n0-33) (smem); chunks farther than Mh from
+// the edge contribute nothing measurable and skip.  Reduced over the CTA in
+// a fixed order into red[0..nwarp) / red[8..).
+template <int K>
+__device__ __forceinline__ void dx_partials(const RowLapParams &p, const float *vlr,
+                                            const float (&X)[kRChunk], float xr, float *red) {
+  const int c = threadIdx.x, lane = c & 31, warp = c >> 5;
+  const int n0 = c * kRChunk;
+  const int W = (int)p.W, Mh = p.Mh, C = p.C;
+  float pl = 0.0f, pr = 0.0f;
+  const bool L = c < C && n0 < Mh, Rr = c < C && n0 + kRChunk >= W - Mh;
+  if (L || Rr) {
+    float zl[K], zr[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) zl[i] = zr[i] = 0.0f;
+#pragma unroll
+    for (int t = 0; t < kRChunk; ++t) {
+      const float g = (t < kRChunk - 1 ? X[t + 1] : xr) - X[t];  // G(n0 + 1 + t)
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        zl[i] = fmaf(p.Wt[t][i], g, zl[i]);
+        zr[i] = fmaf(p.Wt[kRChunk - 1 - t][i], g, zr[i]);
+      }
+    }
+    if (L)
+#pragma unroll
+      for (int i = 0; i < K; ++i) pl = fmaf(vlr[c * 8 + i], zl[i], pl);
+    if (Rr)
+#pragma unroll
+      for (int i = 0; i < K; ++i) pr = fmaf(vlr[c * 8 + 4 + i], zr[i], pr);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pl += __shfl_xor_sync(0xffffffffu, pl, o);
+    pr += __shfl_xor_sync(0xffffffffu, pr, o);
+  }
+  if (lane == 0) {
+    red[warp] = pl;
+    red[8 + warp] = pr;
+  }
+}
+
+// Grid: row CTAs (contiguous rows each) + one edge CTA (the last) for the
+// four single-row filters: the virtual rows Vt / Vb and, once the border
+// kernel has completed, the column direction's border rows Ky = R_ss(Dy).
 template <int K, int KIND>
 __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
-    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap vmap,
-    const __grid_constant__ RowLapParams p, const __grid_constant__ HmRow hm,
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ RowLapParams p,
+    float *__restrict__ Vout, int64_t ldv, const __grid_constant__ VlrTab vtab,
     float *__restrict__ Vt, float *__restrict__ Vb, const float *__restrict__ S, int nseg,
     float *__restrict__ Ky) {
   extern __shared__ __align__(1024) unsigned char smem_rl[];
@@ -161,41 +182,40 @@ __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
   __shared__ float red[16], e2[2], dx2[2];
   const int C = p.C, c = threadIdx.x, nwarp = (int)(blockDim.x >> 5);
   const bool live = c < C;  // the block is whole warps; threads c >= C carry no chunk
-  const int rowbytes = C * 128;               // one row's TMA box
-  const int rowb = (rowbytes + 1023) & ~1023;  // buffer spacing: SWIZZLE_128B needs 1024-byte bases
+  const int rowbytes = C * 128;                // one row's TMA box
+  const int rowb = (rowbytes + 1023) & ~1023;  // slot spacing: SWIZZLE_128B needs 1024-byte bases
   const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_rl);
   char *xbuf = reinterpret_cast<char *>(smem_rl) + ((1024u - (sb & 1023u)) & 1023u);
-  // (V(r) leaves from the slot of row r-1, dead once U(r) is formed)
   float *cf = reinterpret_cast<float *>(xbuf + kRLBufs * rowb);
   float *cb = cf + blockDim.x * K;
-  float *hs = cb + blockDim.x * K;  // h(0..Mh), padded one per 32
+  float *vlr = cb + blockDim.x * K;  // [C][8]: vl (4), vr (4)
   const int64_t H = p.H;
   const int W = (int)p.W;
-  const int64_t rlo = (int64_t)blockIdx.x * p.rows_per;
-  const int64_t rhi = rlo + p.rows_per < H ? rlo + p.rows_per : H;
-  if (rlo >= rhi) return;
+  for (int e = c; e < C * 8; e += blockDim.x) vlr[e] = vtab.v[e];
+  const bool edge = blockIdx.x == gridDim.x - 1;
+  const int64_t rlo = edge ? 0 : (int64_t)blockIdx.x * p.rows_per;
+  const int64_t rhi = edge ? 0 : (rlo + p.rows_per < H ? rlo + p.rows_per : H);
   const int nrows = (int)(rhi - rlo);
-  // logical input row j = clamp(rlo - 1 + j), j = 0 .. nrows + 1, in slot j % 4
-  auto issue = [&](int j) {
-    int64_t r = rlo - 1 + j;
-    r = r < 0 ? 0 : (r >= H ? H - 1 : r);
-    const int s = j % kRLBufs;
+  auto issue_row = [&](int s, int64_t r) {
     mbar_expect_tx(&bar[s], (unsigned)rowbytes);
     tma_load_3d_hint(xbuf + s * rowb, &xmap, &bar[s], 0, 0, (int)r, l2_policy_evict_first());
   };
+  // row CTAs: logical input row j = clamp(rlo - 1 + j), j = 0 .. nrows + 1,
+  // in slot j % 3; the edge CTA: rows 0 and H-1 in slots 0 / 1
+  auto clampr = [&](int64_t r) { return r < 0 ? (int64_t)0 : (r >= H ? H - 1 : r); };
   if (c == 0) {
     for (int s = 0; s < kRLBufs; ++s) mbar_init(&bar[s], 1);
-    for (int j = 0; j < 3 && j <= nrows + 1; ++j) issue(j);
+    if (edge) {
+      issue_row(0, 0);
+      issue_row(1, H - 1);
+    } else {
+      for (int j = 0; j < kRLBufs && j <= nrows + 1; ++j) issue_row(j, clampr(rlo - 1 + j));
+    }
   }
-  for (int n = c; n <= p.Mh; n += blockDim.x) hs[hidx(n)] = hm.h[n];
   __syncthreads();
-  auto wait_row = [&](int j) { mbar_wait(&bar[j % kRLBufs], (unsigned)((j / kRLBufs) & 1)); };
-  wait_row(0);
-  wait_row(1);
-
   float U[kRChunk], V[kRChunk], X[kRChunk];
-  auto load_chunk = [&](int j, float (&o)[kRChunk]) {
-    const SwzRow32 r{xbuf + (j % kRLBufs) * rowb};
+  auto load_chunk = [&](int s, float (&o)[kRChunk]) {
+    const SwzRow32 r{xbuf + s * rowb};
 #pragma unroll
     for (int q = 0; q < kRChunk / 4; ++q) {
       const float4 v = live ? r.ld4(c, q) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -205,139 +225,131 @@ __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
       o[4 * q + 3] = v.w;
     }
   };
-  auto halos = [&](int j, const float (&x)[kRChunk], float &xl, float &xr) {
-    const SwzRow32 r{xbuf + (j % kRLBufs) * rowb};
+  auto halos = [&](int s, const float (&x)[kRChunk], float &xl, float &xr) {
+    const SwzRow32 r{xbuf + s * rowb};
     xl = c > 0 && live ? r.ld(c * kRChunk - 1) : x[0];
     xr = c < C - 1 ? r.ld(c * kRChunk + kRChunk) : x[kRChunk - 1];
   };
-  // a virtual row above / below the image: Vt / Vb = R0(D20 X) of row 0 /
-  // H-1 (zero starts), with that row's border terms
-  auto virtual_row = [&](int j, float *dst) {
-    float xl, xr;
-    load_chunk(j, X);
-    halos(j, X, xl, xr);
-#pragma unroll
-    for (int t = 0; t < kRChunk; ++t) {
-      const float l = t ? X[t - 1] : xl, r = t < kRChunk - 1 ? X[t + 1] : xr;
-      U[t] = (l - X[t]) + (r - X[t]);
+  auto reduce_dx = [&]() {  // (thread 0, after a barrier that follows dx_partials)
+    float a = 0.0f, b = 0.0f;
+    for (int w = 0; w < nwarp; ++w) {
+      a += red[w];
+      b += red[8 + w];
     }
-    dx_partials(p, hs, X, xl, red);
-    if (c == 0) e2[0] = e2[1] = 0.0f;
-    __syncthreads();
-    if (c == 0) {
-      float a = 0.0f, b = 0.0f;
-      for (int w = 0; w < nwarp; ++w) {
-        a += red[w];
-        b += red[8 + w];
+    dx2[0] = p.sign * a;
+    dx2[1] = b;
+  };
+
+  if (edge) {
+    // virtual rows: Vt / Vb = R0(D20 X) of row 0 / H-1 (zero starts), with
+    // that row's left / right border terms
+    for (int which = 0; which < 2; ++which) {
+      mbar_wait(&bar[which], 0);
+      float xl, xr;
+      load_chunk(which, X);
+      halos(which, X, xl, xr);
+#pragma unroll
+      for (int t = 0; t < kRChunk; ++t) {
+        const float l = t ? X[t - 1] : xl, r = t < kRChunk - 1 ? X[t + 1] : xr;
+        U[t] = (l - X[t]) + (r - X[t]);
       }
-      dx2[0] = p.sign * a;
-      dx2[1] = b;
-    }
-    row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
-    if (live) {
+      dx_partials<K>(p, vlr, X, xr, red);
+      if (c == 0) e2[0] = e2[1] = 0.0f;
+      row_carry32<K>(p, U, cf, cb);
+      __syncthreads();
+      if (c == 0) reduce_dx();
+      row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2);
+      float *dst = which == 0 ? Vt : Vb;
+      if (live) {
 #pragma unroll
-      for (int q = 0; q < kRChunk / 4; ++q)
-        *reinterpret_cast<float4 *>(dst + c * kRChunk + 4 * q) =
-            make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]);
+        for (int q = 0; q < kRChunk / 4; ++q)
+          *reinterpret_cast<float4 *>(dst + c * kRChunk + 4 * q) =
+              make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]);
+      }
+      __syncthreads();
     }
-    __syncthreads();
-  };
-  if (rlo == 0) virtual_row(1, Vt);
-  // the column direction's border rows Ky = R_ss(dy), dy = sum over the
-  // border kernel's segments (after this CTA's pdl_wait: the border kernel
-  // has completed)
-  auto border_row = [&](int which) {
-    if (c == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-    __syncthreads();
-    float *rowp = reinterpret_cast<float *>(xbuf);  // (the input ring is idle now)
-    for (int n = c; n < W; n += blockDim.x) {
-      float a = 0.0f;
-      for (int k = 0; k < nseg; ++k) a += __ldg(S + ((int64_t)which * nseg + k) * W + n);
-      rowp[n + (n >> 5)] = a;
-    }
-    if (c == 0) dx2[0] = dx2[1] = 0.0f;
-    __syncthreads();
-    if (c == 0) {
-      e2[0] = rowp[0];
-      e2[1] = rowp[(W - 1) + ((W - 1) >> 5)];
-    }
+    // border rows: Ky = R_ss(dy), dy = sum of the border kernel's segment
+    // shares (the border kernel is this grid's predecessor)
+    pdl_wait();
+    float *rowp = reinterpret_cast<float *>(xbuf);  // (the input slots are idle now)
+    for (int which = 0; which < 2; ++which) {
+      for (int n = c; n < W; n += blockDim.x) {
+        float a = 0.0f;
+        for (int k = 0; k < nseg; ++k) a += __ldg(S + ((int64_t)which * nseg + k) * W + n);
+        rowp[n + (n >> 5)] = a;
+      }
+      if (c == 0) dx2[0] = dx2[1] = 0.0f;
+      __syncthreads();
+      if (c == 0) {
+        e2[0] = rowp[0];
+        e2[1] = rowp[(W - 1) + ((W - 1) >> 5)];
+      }
 #pragma unroll
-    for (int t = 0; t < kRChunk; ++t) U[t] = live ? rowp[c * (kRChunk + 1) + t] : 0.0f;
-    __syncthreads();
-    row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
-    if (live) {
+      for (int t = 0; t < kRChunk; ++t) U[t] = live ? rowp[c * (kRChunk + 1) + t] : 0.0f;
+      __syncthreads();
+      row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
+      if (live) {
 #pragma unroll
-      for (int t = 0; t < kRChunk; ++t) rowp[c * (kRChunk + 1) + t] = V[t];
+        for (int t = 0; t < kRChunk; ++t) rowp[c * (kRChunk + 1) + t] = V[t];
+      }
+      __syncthreads();
+      for (int n = c; n < W; n += blockDim.x) Ky[(int64_t)which * W + n] = rowp[n + (n >> 5)];
+      __syncthreads();
     }
-    __syncthreads();
-    for (int n = c; n < W; n += blockDim.x) Ky[(int64_t)which * W + n] = rowp[n + (n >> 5)];
-    __syncthreads();
-  };
+    pdl_trigger();
+    return;
+  }
+  if (nrows <= 0) return;
+
   for (int i = 0; i < nrows; ++i) {
     const int64_t r = rlo + i;
-    // rows r-1, r, r+1 are logical rows i, i+1, i+2; the prefetch of row r+2
-    // goes to the slot of row r-2, which V(r-1) left from: drained?
-    if (c == 0 && i + 3 <= nrows + 1) {
-      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-      issue(i + 3);
+    // rows r-1, r, r+1 are logical rows i, i+1, i+2 (slots i%3, ...)
+    const int su = i % kRLBufs, sc = (i + 1) % kRLBufs, sd = (i + 2) % kRLBufs;
+    if (i == 0) {
+      mbar_wait(&bar[0], 0);
+      mbar_wait(&bar[1], 0);
     }
-    wait_row(i + 2);
+    mbar_wait(&bar[sd], (unsigned)(((i + 2) / kRLBufs) & 1));
     float xl, xr;
-    load_chunk(i + 1, X);
-    halos(i + 1, X, xl, xr);
+    load_chunk(sc, X);
+    halos(sc, X, xl, xr);
     {
       float Xu[kRChunk];
-      load_chunk(i, Xu);
+      load_chunk(su, Xu);
 #pragma unroll
       for (int t = 0; t < kRChunk; ++t) U[t] = Xu[t] - X[t];
-      load_chunk(i + 2, Xu);
+      load_chunk(sd, Xu);
 #pragma unroll
       for (int t = 0; t < kRChunk; ++t) {
         const float l = t ? X[t - 1] : xl, rr = t < kRChunk - 1 ? X[t + 1] : xr;
         U[t] = ((l - X[t]) + (rr - X[t])) + (U[t] + (Xu[t] - X[t]));
       }
     }
-    dx_partials(p, hs, X, xl, red);
+    dx_partials<K>(p, vlr, X, xr, red);
     if (c == 0 || c == C - 1) {  // D02 X of the end samples: the steady starts
-      const SwzRow32 ru{xbuf + (i % kRLBufs) * rowb}, rd{xbuf + ((i + 2) % kRLBufs) * rowb};
+      const SwzRow32 ru{xbuf + su * rowb}, rd{xbuf + sd * rowb};
       const int n = c == 0 ? 0 : W - 1;
       const float xc = X[c == 0 ? 0 : kRChunk - 1];
       e2[c == 0 ? 0 : 1] = (ru.ld(n) - xc) + (rd.ld(n) - xc);
     }
     row_carry32<K>(p, U, cf, cb);
-    __syncthreads();  // X of this row read; carries, e2, red published
+    __syncthreads();  // rows r-1 .. r+1 read; carries, e2, red published
     if (c == 0) {
-      float a = 0.0f, b = 0.0f;
-      for (int w = 0; w < nwarp; ++w) {
-        a += red[w];
-        b += red[8 + w];
-      }
-      dx2[0] = p.sign * a;
-      dx2[1] = b;
+      if (i + 3 <= nrows + 1) issue_row(su, clampr(rlo + 2 + i));  // row r+2 -> slot of r-1
+      reduce_dx();
     }
     row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2);
-    char *ob = xbuf + (i % kRLBufs) * rowb;  // the slot of row r-1
+    if (i == 0) pdl_wait();  // V may still be read by the previous scale's column pass
     if (live) {
-      const SwzRow32 o{ob};
+      float *dst = Vout + r * ldv + c * kRChunk;
+      const uint64_t pol = l2_policy_evict_last();  // V is read twice by the column pass
 #pragma unroll
       for (int q = 0; q < kRChunk / 4; ++q)
-        o.st4(c, q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]));
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
-    __syncthreads();
-    if (c == 0) {
-      if (i == 0) pdl_wait();  // V may still be read by the previous scale's column pass
-      tma_store_3d_hint(&vmap, ob, 0, 0, (int)r, l2_policy_evict_last());
-      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        st_v4_hint(dst + 4 * q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]),
+                   pol);
     }
   }
-  if (rhi == H) virtual_row(nrows, Vb);
-  // the column direction's border rows: Ky = R_ss(Dy) once the border CTAs
-  // are done (they were dispatched before every row CTA)
-  if (rlo == 0) border_row(0);
-  if (rhi == H) border_row(1);
   pdl_trigger();
-  if (c == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -381,6 +393,45 @@ static int rl_plan(RowLapPlan *P, int64_t h, int64_t w, const double *b, const d
       p.SP[i][t] = (float)(0.5L * (Wt[t][i] + Wt[kRChunk - 1 - t][i]));
       p.SQ[i][t] = (float)(0.5L * (Wt[kRChunk - 1 - t][i] - Wt[t][i]));
     }
+  for (int t = 0; t < kRChunk; ++t)
+    for (int i = 0; i < k; ++i) p.Wt[t][i] = (float)Wt[t][i];
+  // border-term chunk vectors vl(c) = c A^(32 c), vr(c) = c A^(W - 32 c - 33)
+  {
+    ld Ainv[16], IA[16];
+    for (int i = 0; i < k * k; ++i) IA[i] = M.A[i];
+    for (int col = 0; col < k; ++col) {  // A^-1 column by column
+      ld M2[16], y[4];
+      memcpy(M2, IA, sizeof(ld) * k * k);
+      for (int i = 0; i < k; ++i) y[i] = (i == col) ? 1 : 0;
+      if (!solve(M2, y, k)) return fail(VMF_EVALUE, "singular modal matrix");
+      for (int i = 0; i < k; ++i) Ainv[i * k + col] = y[i];
+    }
+    memset(&P->vlr, 0, sizeof(P->vlr));
+    ld A32[16];
+    matpow(M.A, kRChunk, A32, k);
+    ld v[4], t4[4];
+    for (int i = 0; i < k; ++i) v[i] = M.c[i];  // c A^0
+    for (int cc = 0; cc < p.C; ++cc) {          // vl(cc) = c A^(32 cc)
+      for (int i = 0; i < k; ++i) P->vlr.v[cc * 8 + i] = (float)v[i];
+      for (int jj = 0; jj < k; ++jj) {
+        t4[jj] = 0;
+        for (int i = 0; i < k; ++i) t4[jj] += v[i] * A32[i * k + jj];
+      }
+      memcpy(v, t4, sizeof(ld) * k);
+    }
+    for (int i = 0; i < k; ++i) {  // vr(C-1) = c A^-1, then x A^32 going left
+      v[i] = 0;
+      for (int jj = 0; jj < k; ++jj) v[i] += M.c[jj] * Ainv[jj * k + i];
+    }
+    for (int cc = p.C - 1; cc >= 0; --cc) {
+      for (int i = 0; i < k; ++i) P->vlr.v[cc * 8 + 4 + i] = (float)v[i];
+      for (int jj = 0; jj < k; ++jj) {
+        t4[jj] = 0;
+        for (int i = 0; i < k; ++i) t4[jj] += v[i] * A32[i * k + jj];
+      }
+      memcpy(v, t4, sizeof(ld) * k);
+    }
+  }
   ld A32[16];
   matpow(M.A, kRChunk, A32, k);
   for (int i = 0; i < k * k; ++i) p.A32[i] = (float)A32[i];
@@ -471,22 +522,20 @@ bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, in
 
 static int rl_block(int C) { return (C + 31) / 32 * 32; }
 
-static size_t rl_smem(int C, int k, int Mh) {
+static size_t rl_smem(int C, int k) {
   return 1024 + (size_t)kRLBufs * ((C * 128 + 1023) & ~1023) +
-         2 * (size_t)rl_block(C) * k * sizeof(float) + (size_t)(Mh + 1 + Mh / 32 + 2) * sizeof(float);
+         2 * (size_t)rl_block(C) * k * sizeof(float) + (size_t)C * 8 * sizeof(float);
 }
 
 template <int K, int KIND>
 static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows,
                          RowLapPlan &P, const RowLapPlan &PC, const SegVec &sv, cudaStream_t st) {
   RowLapParams &p = P.p;
-  CUtensorMap xm, vm;
+  CUtensorMap xm;
   memset(&xm, 0, sizeof(xm));
-  memset(&vm, 0, sizeof(vm));
-  if (!make_tmap_rows_swz_f32(&xm, x, p.H, p.W, ldx, 1) ||
-      !make_tmap_rows_swz_f32(&vm, V, p.H, p.W, ldv, 1)) {
+  if (!make_tmap_rows_swz_f32(&xm, x, p.H, p.W, ldx, 1)) {
     cudaGetLastError();
-    return fail(VMF_EVALUE, "row pass: TMA descriptors unavailable");
+    return fail(VMF_EVALUE, "row pass: TMA descriptor unavailable");
   }
   float *Vt = vrows, *Vb = vrows + p.W, *Ky = vrows + 2 * p.W, *S = vrows + 4 * p.W;
   {
@@ -494,7 +543,7 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
     launch_pdl(rowborder_kernel<K, KIND>, dim3((unsigned)cdiv(p.W, 128), (unsigned)(2 * sv.nseg)),
                dim3(128), 0, st, PC.p, sv, x, ldx, p.H, p.W, S);
   }
-  const size_t smem = rl_smem(p.C, K, p.Mh);
+  const size_t smem = rl_smem(p.C, K);
   const int block = rl_block(p.C);
   static std::map<std::pair<int, size_t>, int> slot_cache;
   const int dev = current_device();
@@ -502,7 +551,7 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
   static PerDevice attr;
   if (attr.first())  // the largest footprint (C = 256), so every width may launch
     cudaFuncSetAttribute(rowlap_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)rl_smem(kRLMaxC, K, kHmRowMax));
+                         (int)rl_smem(kRLMaxC, K));
   if (!slots) {
     int occ = 0, nsm = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, block, smem);
@@ -510,11 +559,12 @@ static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, flo
     cudaGetLastError();
     slots = (occ > 0 ? occ : 1) * nsm;
   }
-  p.rows_per = (int)cdiv(p.H, slots);
-  const int grid = (int)cdiv(p.H, p.rows_per);
+  // one slot is the edge CTA (virtual and border rows)
+  p.rows_per = (int)cdiv(p.H, slots > 1 ? slots - 1 : 1);
+  const int grid = (int)cdiv(p.H, p.rows_per) + 1;
   Launch g(K_IIR_ROWS_FUSED, st);
-  launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm, vm, p, P.hm, Vt, Vb,
-             (const float *)S, sv.nseg, Ky);
+  launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm, (const RowLapParams)p,
+             V, ldv, P.vlr, Vt, Vb, (const float *)S, sv.nseg, Ky);
   return cuda_status("fp32 row pass");
 }
 

@@ -1,5 +1,6 @@
 // vmf_rowlap.cuh -- the fp32 "Laplacian-first" row pass (vmf_rowlap.cu).
 #pragma once
+#include <vector>
 #include "vmf_common.cuh"
 #include "vmf_modal32.cuh"
 
@@ -12,6 +13,7 @@ struct RowLapParams {
   float c[4], cs[4];    // y+ = c . u(n-1); cs = sign * c (the anticausal part)
   float b0, sign;
   float SP[4][16], SQ[4][16];  // folded 32-sample chunk-carry weights
+  float Wt[32][4];      // A^t b, t < 32 (border-term chunk sums)
   float A32[16];        // A^32
   float Apow[5][16];    // A^(32 cpl 2^l): the chunk scan's Kogge-Stone steps
   float Iss[4];         // (I - A)^-1 b
@@ -29,9 +31,14 @@ struct HmRow {
   float h[kHmRowMax + 1];
 };
 
+struct VlrTab {  // [C][8]: the border-term chunk vectors vl(c) (4), vr(c) (4)
+  float v[256 * 8];
+};
+
 struct RowLapPlan {
   RowLapParams p;
   HmRow hm;
+  VlrTab vlr;
   int kind;
 };
 
