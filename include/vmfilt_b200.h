@@ -136,6 +136,30 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w,
                         float *thr_dev, int64_t *n_det_host, void *ws,
                         size_t ws_bytes, void *stream);
 
+/* Multi-scale sweep (config 3's scale sweep; engine.py:205-228 per scale):
+ * the same blur -> Laplacian -> threshold + NMS per scale as
+ * vmf_blur_lap_detect, with one row pass over x for every scale.
+ * vmf_sweep_supported: nonzero when the fp32 "Laplacian-first" path takes
+ * the sweep (fp32 x, w a multiple of 32 up to 8192, 16-byte aligned rows,
+ * IIR row and column stages of one order with an fp32 modal realisation,
+ * 1..8 scales).  vmf_sweep_rows: the row pass of every scale into
+ * sweep_ws (vmf_sweep_workspace_bytes).  vmf_sweep_detect: the column pass
+ * of one scale (any stream ordered after vmf_sweep_rows; scales are
+ * independent and may run concurrently, each with its own ws of
+ * vmf_sweep_detect_workspace_bytes); outputs as vmf_blur_lap_detect. */
+size_t vmf_sweep_workspace_bytes(int64_t h, int64_t w, int nscales);
+size_t vmf_sweep_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *col_stage);
+int vmf_sweep_supported(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                        int nscales, const vmf_stage *row_stages, const vmf_stage *col_stages);
+int vmf_sweep_rows(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx, int nscales,
+                   const vmf_stage *row_stages, const vmf_stage *col_stages, void *sweep_ws,
+                   size_t sweep_ws_bytes, void *stream);
+int vmf_sweep_detect(int scale, int64_t h, int64_t w, int nscales, const vmf_stage *col_stage,
+                     float lap_scale, float frac, float *lap_out, int32_t *det_yx,
+                     float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev,
+                     void *sweep_ws, size_t sweep_ws_bytes, void *ws, size_t ws_bytes,
+                     void *stream);
+
 /* Scale-space 3x3x3 NMS over a stack of ns normalised responses
  * N[s] (each h x w, pitch ldn, planes spaced plane_stride elements):
  * strict extremum against the 8 in-scale and the 9+9 adjacent-scale

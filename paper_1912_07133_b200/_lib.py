@@ -72,6 +72,15 @@ _PROTOS = {
     "vmf_blur_lap_detect": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, C.POINTER(VmfStage),
                                       C.POINTER(VmfStage), C.c_float, C.c_float, _vp, _vp, _vp,
                                       _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "vmf_sweep_workspace_bytes": (_sz, [_i64, _i64, C.c_int]),
+    "vmf_sweep_detect_workspace_bytes": (_sz, [_i64, _i64, C.POINTER(VmfStage)]),
+    "vmf_sweep_supported": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, C.c_int,
+                                      C.POINTER(VmfStage), C.POINTER(VmfStage)]),
+    "vmf_sweep_rows": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, C.c_int, C.POINTER(VmfStage),
+                                 C.POINTER(VmfStage), _vp, _sz, _vp]),
+    "vmf_sweep_detect": (C.c_int, [C.c_int, _i64, _i64, C.c_int, C.POINTER(VmfStage),
+                                   C.c_float, C.c_float, _vp, _vp, _vp, _i64, _vp, _vp, _vp,
+                                   _sz, _vp, _sz, _vp]),
     "vmf_hessian_detect_workspace_bytes": (_sz, [_i64, _i64, C.POINTER(VmfStage),
                                                  C.POINTER(VmfStage)]),
     "vmf_hessian_detect": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, C.POINTER(VmfStage),

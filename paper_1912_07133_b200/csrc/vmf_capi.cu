@@ -323,33 +323,79 @@ size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage
     if (c4 > carry) carry = c4;
   }
   return 3 * img + align256(carry) + align256(detect_workspace_bytes(1, h, w)) + 256 +
-         align256((size_t)kRowLapVrows * w * sizeof(float));  // fp32 row pass extras
+         align256((size_t)sweep_extras_floats(w) * sizeof(float));  // fp32 row pass extras
 }
 
 // The all-fp32 "Laplacian-first" path (vmf_rowlap.cu + vmf_colpass32.cu V
 // mode): fp32 frames with W = 32 C (C <= 256), 16-byte aligned rows, IIR row
 // and column stages with a modal fp32 realisation.
-static bool lapfirst_ok(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
-                        const vmf_stage *row, const vmf_stage *col, IirParams *ip) {
-  if (x_dtype != VMF_F32 || !row || !col || row->kind != VMF_STAGE_IIR ||
-      col->kind != VMF_STAGE_IIR || getenv("VMF_FORCE_GENERIC"))
-    return false;
-  if (((uintptr_t)x & 15) || ((ldx * 4) & 15)) return false;
-  if (row->n != col->n ||
-      !rowlap_supported(h, w, row->b_plus, row->a_plus, row->n, row->b_zero, row->sign))
-    return false;
-  if (iir_plan(ip, w, h, col->b_plus, col->a_plus, col->n, col->b_zero, col->sign)) {
-    cudaGetLastError();
-    return false;
+static SweepStage sweep_stage(const vmf_stage *row, const vmf_stage *col) {
+  SweepStage s;
+  s.rb = row->b_plus;
+  s.ra = row->a_plus;
+  s.rb0 = row->b_zero;
+  s.rsign = row->sign;
+  s.cb = col->b_plus;
+  s.ca = col->a_plus;
+  s.cb0 = col->b_zero;
+  s.csign = col->sign;
+  return s;
+}
+
+// The all-fp32 "Laplacian-first" path (vmf_rowlap.cu + vmf_colpass32.cu V
+// mode): fp32 frames with W = 32 C (C <= 256), 16-byte aligned rows, IIR row
+// and column stages of one order with a modal fp32 realisation.
+static bool lapfirst_ok(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx, int ns,
+                        const vmf_stage *rows, const vmf_stage *cols) {
+  if (x_dtype != VMF_F32 || getenv("VMF_FORCE_GENERIC") || ns < 1 || ns > kMaxScales) return false;
+  SweepStage st[kMaxScales];
+  for (int s = 0; s < ns; ++s) {
+    const vmf_stage *r = rows + s, *cl = cols + s;
+    if (r->kind != VMF_STAGE_IIR || cl->kind != VMF_STAGE_IIR || r->n != cl->n ||
+        r->n != rows[0].n)
+      return false;
+    IirParams ip;
+    if (iir_plan(&ip, w, h, cl->b_plus, cl->a_plus, cl->n, cl->b_zero, cl->sign)) {
+      cudaGetLastError();
+      return false;
+    }
+    if (!colpass32_supported(h, w, ip)) return false;
+    st[s] = sweep_stage(r, cl);
   }
-  if (!colpass32_supported(h, w, *ip)) return false;
-  // one realisation kind for both stages (the column scan row-filters the
-  // border rows with the row stage's plan)
-  RowLapPlan rpl;
-  Modal mc;
-  return rowlap_get_plan(h, w, row->b_plus, row->a_plus, row->n, row->b_zero, row->sign, &rpl) ==
-             VMF_OK &&
-         modal_realise(col->b_plus, col->a_plus, col->n, &mc) && mc.kind == rpl.kind;
+  return sweep_supported(x, h, w, ldx, rows[0].n, ns, st);
+}
+
+static size_t sweep_ws_bytes(int64_t h, int64_t w, int ns) {
+  return (size_t)ns * (align256((size_t)h * w * sizeof(float)) +
+                       align256((size_t)sweep_extras_floats(w) * sizeof(float))) + 256;
+}
+
+static SweepOut sweep_layout(void *sws, int64_t h, int64_t w, int ns) {
+  SweepOut o;
+  memset(&o, 0, sizeof(o));
+  char *p = (char *)(((uintptr_t)sws + 255) & ~(uintptr_t)255);
+  for (int s = 0; s < ns; ++s) {
+    o.V[s] = (float *)p;
+    p += align256((size_t)h * w * sizeof(float));
+    o.E[s] = (float *)p;
+    p += align256((size_t)sweep_extras_floats(w) * sizeof(float));
+  }
+  o.ldv = w;
+  return o;
+}
+
+// the column pass of scale s of a sweep (V mode) into L + detections
+static int sweep_cols(const SweepOut &o, int s, int64_t h, int64_t w, const vmf_stage *col,
+                      float lap_scale, float frac, float *L, int64_t ldl, int32_t *det_yx,
+                      float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev, void *cws,
+                      size_t cws_b, cudaStream_t st) {
+  IirParams ip;
+  int rc = iir_plan(&ip, w, h, col->b_plus, col->a_plus, col->n, col->b_zero, col->sign);
+  if (rc) return rc;
+  const float *E = o.E[s];
+  const Col32VMode vm = {E + kExVt * w, E + kExVb * w, E + kExKy * w};
+  return colpass32_run(o.V[s], o.ldv, L, ldl, ip, h, w, lap_scale, frac, det_yx, det_val, cap,
+                       n_det_dev, thr_dev, cws, cws_b, st, &vm);
 }
 
 int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
@@ -375,7 +421,7 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   p += img;
   float *L = lap_out ? lap_out : (float *)p;
   p += img;
-  const size_t vrows_b = align256((size_t)kRowLapVrows * w * sizeof(float));
+  const size_t vrows_b = align256((size_t)sweep_extras_floats(w) * sizeof(float));
   size_t carry_b = align256(vmf_blur_lap_detect_workspace_bytes(h, w, row_stage, col_stage) -
                             3 * img - align256(detect_workspace_bytes(1, h, w)) - 256 - vrows_b);
   void *carry = p;
@@ -384,16 +430,19 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   size_t dws_b = align256(detect_workspace_bytes(1, h, w));
   p += dws_b;
   float *vrows = (float *)p;
-  IirParams ipc;
-  if (lapfirst_ok(x, x_dtype, h, w, ldx, row_stage, col_stage, &ipc)) {
-    // V = R(Lap5 X) into T's slot, then the column pass in V mode
-    rc = rowlap_run((const float *)x, ldx, T, w, vrows, h, w, row_stage->b_plus,
-                    row_stage->a_plus, row_stage->n, row_stage->b_zero, row_stage->sign,
-                    col_stage->b_plus, col_stage->a_plus, col_stage->b_zero, col_stage->sign, st);
+  if (lapfirst_ok(x, x_dtype, h, w, ldx, 1, row_stage, col_stage)) {
+    // V = R(Lap5 X) into T's slot (a one-scale sweep), then the column pass
+    // in V mode
+    SweepOut o;
+    memset(&o, 0, sizeof(o));
+    o.V[0] = T;
+    o.E[0] = vrows;
+    o.ldv = w;
+    SweepStage sst = sweep_stage(row_stage, col_stage);
+    rc = sweep_rows((const float *)x, ldx, h, w, row_stage->n, 1, &sst, o, st);
     if (rc) return rc;
-    const Col32VMode vm = {vrows, vrows + w, vrows + 2 * w};
-    rc = colpass32_run(T, w, L, w, ipc, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
-                       thr_dev, carry, carry_b, st, &vm);
+    rc = sweep_cols(o, 0, h, w, col_stage, lap_scale, frac, L, w, det_yx, det_val, cap, n_det_dev,
+                    thr_dev, carry, carry_b, st);
     if (rc) return rc;
     if (blur_out) {  // B on request: T into the (unused) B slot, then the column leaf
       float *Tb = T + img / sizeof(float);
@@ -460,6 +509,68 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   if (frac <= 0.0f) return VMF_OK;
   return detect(L, w, h * w, 1, h, w, frac, true, det_yx, 2, det_val, cap, n_det_dev, thr_dev,
                 n_det_host, dws, dws_b, st);
+}
+
+// ---------------------------------------------------------------------------
+// multi-scale sweep: one fp32 row pass over X for every scale, then one
+// column pass per scale (any stream ordered after vmf_sweep_rows)
+// ---------------------------------------------------------------------------
+size_t vmf_sweep_workspace_bytes(int64_t h, int64_t w, int nscales) {
+  return sweep_ws_bytes(h, w, nscales);
+}
+
+size_t vmf_sweep_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *col_stage) {
+  return align256((size_t)h * w * sizeof(float)) +
+         align256(colpass32_workspace_bytes(h, w, col_stage ? col_stage->n : 4)) + 256;
+}
+
+int vmf_sweep_supported(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
+                        int nscales, const vmf_stage *row_stages, const vmf_stage *col_stages) {
+  if (!row_stages || !col_stages || h < 1 || w < 1 || ldx < w) return 0;
+  for (int s = 0; s < nscales; ++s)
+    if (check_stage(row_stages + s, w, "row") || check_stage(col_stages + s, h, "column")) {
+      set_error("%s", "");
+      return 0;
+    }
+  return lapfirst_ok(x, x_dtype, h, w, ldx, nscales, row_stages, col_stages) ? 1 : 0;
+}
+
+int vmf_sweep_rows(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx, int nscales,
+                   const vmf_stage *row_stages, const vmf_stage *col_stages, void *sweep_ws,
+                   size_t sweep_ws_bytes_, void *stream) {
+  if (!vmf_sweep_supported(x, x_dtype, h, w, ldx, nscales, row_stages, col_stages))
+    return fail(VMF_EVALUE, "sweep: frame / stages not supported by the fp32 path");
+  if (!sweep_ws || sweep_ws_bytes_ < sweep_ws_bytes(h, w, nscales))
+    return fail(VMF_EVALUE, "sweep workspace too small");
+  SweepStage st[kMaxScales];
+  for (int s = 0; s < nscales; ++s) st[s] = sweep_stage(row_stages + s, col_stages + s);
+  const SweepOut o = sweep_layout(sweep_ws, h, w, nscales);
+  return sweep_rows((const float *)x, ldx, h, w, row_stages[0].n, nscales, st, o,
+                    (cudaStream_t)stream);
+}
+
+int vmf_sweep_detect(int scale, int64_t h, int64_t w, int nscales, const vmf_stage *col_stage,
+                     float lap_scale, float frac, float *lap_out, int32_t *det_yx,
+                     float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev,
+                     void *sweep_ws, size_t sweep_ws_bytes_, void *ws, size_t ws_bytes,
+                     void *stream) {
+  if (scale < 0 || scale >= nscales) return fail(VMF_EVALUE, "scale index out of range");
+  int rc = check_stage(col_stage, h, "column");
+  if (rc) return rc;
+  if (!sweep_ws || sweep_ws_bytes_ < sweep_ws_bytes(h, w, nscales))
+    return fail(VMF_EVALUE, "sweep workspace too small");
+  const size_t need = vmf_sweep_detect_workspace_bytes(h, w, col_stage);
+  if (!ws || ws_bytes < need)
+    return fail(VMF_EVALUE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  if (frac > 0.0f && (!n_det_dev || !thr_dev || (cap > 0 && (!det_yx || !det_val))))
+    return fail(VMF_EVALUE, "detection outputs missing");
+  const SweepOut o = sweep_layout(sweep_ws, h, w, nscales);
+  char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float *L = lap_out ? lap_out : (float *)p;
+  p += align256((size_t)h * w * sizeof(float));
+  return sweep_cols(o, scale, h, w, col_stage, lap_scale, frac, L, w, det_yx, det_val, cap,
+                    n_det_dev, thr_dev, p, align256(colpass32_workspace_bytes(h, w, col_stage->n)),
+                    (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -62,42 +62,87 @@ struct SwzRow32 {
 __device__ __forceinline__ int hidx(int n) { return n + (n >> 5); }  // padded h() copy
 
 // ---------------------------------------------------------------------------
-// the border kernel: the column direction's border sums, straight from the
-// frame (column stage, modal fp32), in 64-row segments so the whole frame
-// edge is covered by ~1k short CTAs:
+// the border kernel (every scale): the column direction's border sums,
+// straight from the frame (column stage, modal fp32), in 64-row segments so
+// the frame edge is covered by ~1k short CTAs:
 //   Dy[0][c] = s_C sum_{m>=1} h_C(m) G(m, c),  Dy[1][c] = sum_{m>=1} h_C(m) G(H-m, c),
 //   G(m, c) = X(m, c) - X(m-1, c),  h_C(m) = c A^(m-1) b.
 // Segment k covers m = m0 .. m0+63 (m0 = 1 + 64 k): its share is
 // (c A^(m0-1)) . sum_t A^t b G(m0 + t), the inner sum a zero-state
-// recursion; S[which][k][c] holds the shares, summed in k order by the row
-// pass.  It reads only X, so it runs first and the row pass waits for it
-// (griddepcontrol) only before its first store.
+// recursion; S[which][k][c] holds the shares (summed in k order by the edge
+// CTAs).  The last ns CTA rows compute each scale's row-direction chunk
+// vectors vl(c) = c A^(32 c), vr(c) = c A^(W - 32 c - 33) (fp64 powers).
+// It reads only X, so it runs first; the row pass depends on it.
 // ---------------------------------------------------------------------------
 constexpr int kSeg = 64;
 
 template <int K, int KIND>
-__global__ void __launch_bounds__(128) rowborder_kernel(const __grid_constant__ RowLapParams pc,
-                                                        const __grid_constant__ SegVec sv,
-                                                        const float *__restrict__ X, int64_t ldx,
-                                                        int64_t H, int64_t W,
-                                                        float *__restrict__ S) {
-  // (no early trigger: the row pass's CTAs would take the registers this
-  // grid needs and stretch it; it launches when this grid completes)
-  const int nseg = sv.nseg;
-  const int which = (int)blockIdx.y / nseg, k = (int)blockIdx.y % nseg;
+__global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant__ BorderMulti bm,
+                                                           const float *__restrict__ X,
+                                                           int64_t ldx, int64_t H, int64_t W,
+                                                           SweepOut out) {
+  int y = blockIdx.y, s = 0;
+  while (s < bm.ns && y >= 2 * bm.s[s].sv.nseg) y -= 2 * bm.s[s++].sv.nseg;
+  if (s >= bm.ns) {  // chunk-vector rows: y = scale
+    const BorderScale &b = bm.s[y];
+    float *vlr = out.E[y] + kExVlr * W;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < b.C; c += gridDim.x * blockDim.x) {
+      // vl = c_r A32^c; vr = ci A32^(C-1-c): binary powers in fp64
+      double Pw[16], R[16], T[16];
+      auto power = [&](int e) {
+        for (int i = 0; i < K * K; ++i) {
+          Pw[i] = b.A32[i];
+          R[i] = (i % (K + 1) == 0) ? 1.0 : 0.0;
+        }
+        while (e > 0) {
+          if (e & 1) {
+            for (int i = 0; i < K; ++i)
+              for (int jj = 0; jj < K; ++jj) {
+                double a = 0.0;
+                for (int m = 0; m < K; ++m) a = fma(R[i * K + m], Pw[m * K + jj], a);
+                T[i * K + jj] = a;
+              }
+            for (int i = 0; i < K * K; ++i) R[i] = T[i];
+          }
+          for (int i = 0; i < K; ++i)
+            for (int jj = 0; jj < K; ++jj) {
+              double a = 0.0;
+              for (int m = 0; m < K; ++m) a = fma(Pw[i * K + m], Pw[m * K + jj], a);
+              T[i * K + jj] = a;
+            }
+          for (int i = 0; i < K * K; ++i) Pw[i] = T[i];
+          e >>= 1;
+        }
+      };
+      power(c);
+      for (int jj = 0; jj < K; ++jj) {
+        double a = 0.0;
+        for (int i = 0; i < K; ++i) a = fma((double)b.cr[i], R[i * K + jj], a);
+        vlr[c * 8 + jj] = (float)a;
+      }
+      power(b.C - 1 - c);
+      for (int jj = 0; jj < K; ++jj) {
+        double a = 0.0;
+        for (int i = 0; i < K; ++i) a = fma((double)b.ci[i], R[i * K + jj], a);
+        vlr[c * 8 + 4 + jj] = (float)a;
+      }
+    }
+    return;
+  }
+  const BorderScale &b = bm.s[s];
+  const int nseg = b.sv.nseg;
+  const int which = y / nseg, k = y % nseg;
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t cc = col < W ? col : W - 1;
-  const int Mh = sv.Mh;
+  const int Mh = b.sv.Mh;
   const int m0 = 1 + kSeg * k;
   const int n = (Mh - m0 + 1) < kSeg ? (Mh - m0 + 1) : kSeg;  // m = m0 .. m0+n-1
-  // rows holding G(m) for m = m0 + t: top rows m (G = X(m) - X(m-1)); bottom
-  // rows H - m (G = X(H-m) - X(H-m-1)); the samples X(r) for the n+1 rows
-  // involved, all loaded before the recursion (independent loads)
+  // top: xs[t] = X(m0 - 1 + t); bottom: xs[t] = X(H - m0 - t); all loaded
+  // before the recursion (independent loads)
   float xs[kSeg + 1];
   const float *Xc = X + cc;
 #pragma unroll
   for (int t = 0; t <= kSeg; ++t) {
-    // top: xs[t] = X(m0 - 1 + t); bottom: xs[t] = X(H - m0 - t)
     const int64_t r = which == 0 ? m0 - 1 + t : H - m0 - t;
     xs[t] = t <= n ? __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx) : 0.0f;
   }
@@ -110,98 +155,93 @@ __global__ void __launch_bounds__(128) rowborder_kernel(const __grid_constant__ 
       // G(m0 + t): top X(m0+t) - X(m0+t-1) = xs[t+1] - xs[t];
       //            bottom X(H-m0-t) - X(H-m0-t-1) = xs[t] - xs[t+1]
       const float g = which == 0 ? xs[t + 1] - xs[t] : xs[t] - xs[t + 1];
-      u.step(pc, g);
+      u.step(b, g);
     }
   }
-  float v = u.out(sv.v[k]);
-  if (which == 0) v *= pc.sign;
-  if (col < W) S[((int64_t)which * nseg + k) * W + col] = v;
+  float v = u.out(b.sv.v[k]);
+  if (which == 0) v *= b.sign;
+  if (col < W) out.E[s][kExS * W + ((int64_t)which * nseg + k) * W + col] = v;
 }
 
 // ---------------------------------------------------------------------------
-// the row pass
+// the row pass (every scale)
 // ---------------------------------------------------------------------------
-// Left / right border terms of one row: dxl = s sum_{n>=1} h(n) G(n),
-// dxr = sum_{m>=1} h(m) G(W-m), G(n) = X(n) - X(n-1).  Per chunk (samples
-// n = n0+1 .. n0+32) the sums are modal: h(n0+1+t) = (c A^n0) A^t b and
-// h(W-n0-1-t) = (c A^(W-n0-33)) A^(31-t) b, so each chunk forms two zero-state
-// sums with the uniform weights A^t b and dots them with its own vectors
-// vl(c) = c A^n0, vr(c) = c A^(W-n0-33) (smem); chunks farther than Mh from
-// the edge contribute nothing measurable and skip.  Reduced over the CTA in
-// a fixed order into red[0..nwarp) / red[8..).
+// Left / right border terms of one row for one scale: dxl = s sum_{n>=1}
+// h(n) G(n), dxr = sum_{m>=1} h(m) G(W-m), G(n) = X(n) - X(n-1).  Per chunk
+// (samples n = n0+1 .. n0+32) the sums are modal: h(n0+1+t) = (c A^n0) A^t b,
+// h(W-n0-1-t) = (c A^(W-n0-33)) A^(31-t) b, so a chunk forms two zero-state
+// sums with the uniform weights A^t b (g: its first differences) and dots
+// them with its vectors vl, vr (the border kernel's table); chunks farther
+// than Mh from an edge contribute nothing measurable and skip.
 template <int K>
-__device__ __forceinline__ void dx_partials(const RowLapParams &p, const float *vlr,
-                                            const float (&X)[kRChunk], float xr, float *red) {
-  const int c = threadIdx.x, lane = c & 31, warp = c >> 5;
+__device__ __forceinline__ void dx_chunk(const RowLapParams &p, const float *vlr,
+                                         const float (&g)[kRChunk], float &pl, float &pr) {
+  const int c = threadIdx.x;
   const int n0 = c * kRChunk;
   const int W = (int)p.W, Mh = p.Mh, C = p.C;
-  float pl = 0.0f, pr = 0.0f;
+  pl = pr = 0.0f;
   const bool L = c < C && n0 < Mh, Rr = c < C && n0 + kRChunk >= W - Mh;
   if (L || Rr) {
     float zl[K], zr[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) zl[i] = zr[i] = 0.0f;
 #pragma unroll
-    for (int t = 0; t < kRChunk; ++t) {
-      const float g = (t < kRChunk - 1 ? X[t + 1] : xr) - X[t];  // G(n0 + 1 + t)
+    for (int t = 0; t < kRChunk; ++t)
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        zl[i] = fmaf(p.Wt[t][i], g, zl[i]);
-        zr[i] = fmaf(p.Wt[kRChunk - 1 - t][i], g, zr[i]);
+        zl[i] = fmaf(p.Wt[t][i], g[t], zl[i]);
+        zr[i] = fmaf(p.Wt[kRChunk - 1 - t][i], g[t], zr[i]);
       }
-    }
     if (L)
 #pragma unroll
-      for (int i = 0; i < K; ++i) pl = fmaf(vlr[c * 8 + i], zl[i], pl);
+      for (int i = 0; i < K; ++i) pl = fmaf(__ldg(vlr + c * 8 + i), zl[i], pl);
     if (Rr)
 #pragma unroll
-      for (int i = 0; i < K; ++i) pr = fmaf(vlr[c * 8 + 4 + i], zr[i], pr);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    pl += __shfl_xor_sync(0xffffffffu, pl, o);
-    pr += __shfl_xor_sync(0xffffffffu, pr, o);
-  }
-  if (lane == 0) {
-    red[warp] = pl;
-    red[8 + warp] = pr;
+      for (int i = 0; i < K; ++i) pr = fmaf(__ldg(vlr + c * 8 + 4 + i), zr[i], pr);
   }
 }
 
-// Grid: row CTAs (contiguous rows each) + one edge CTA (the last) for the
-// four single-row filters: the virtual rows Vt / Vb and, once the border
-// kernel has completed, the column direction's border rows Ky = R_ss(Dy).
+__device__ __forceinline__ void warp_sum2(float &a, float &b) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+}
+
+// Grid: row CTAs (contiguous rows each) + one edge CTA per scale (the last
+// ns): the virtual rows Vt / Vb and the column direction's border rows
+// Ky = R_ss(Dy) of that scale (four single-row filters).  Per row, U = Lap5 X
+// is formed once and every scale's carries go before one barrier, the 2 ns
+// chunk scans share the warps, and each scale's walks write its V row.
 template <int K, int KIND>
-__global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
-    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ RowLapParams p,
-    float *__restrict__ Vout, int64_t ldv, const __grid_constant__ VlrTab vtab,
-    float *__restrict__ Vt, float *__restrict__ Vb, const float *__restrict__ S, int nseg,
-    float *__restrict__ Ky) {
+__global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ RowLapMulti rm,
+    SweepOut out) {
   extern __shared__ __align__(1024) unsigned char smem_rl[];
   __shared__ __align__(8) uint64_t bar[kRLBufs];
-  __shared__ float red[16], e2[2], dx2[2];
-  const int C = p.C, c = threadIdx.x, nwarp = (int)(blockDim.x >> 5);
+  __shared__ float red[kMaxScales][16], e2[2], dx2[kMaxScales][2];
+  const int C = rm.C, c = threadIdx.x, nwarp = (int)(blockDim.x >> 5), lane = c & 31;
+  const int ns = rm.ns;
   const bool live = c < C;  // the block is whole warps; threads c >= C carry no chunk
   const int rowbytes = C * 128;                // one row's TMA box
   const int rowb = (rowbytes + 1023) & ~1023;  // slot spacing: SWIZZLE_128B needs 1024-byte bases
   const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_rl);
   char *xbuf = reinterpret_cast<char *>(smem_rl) + ((1024u - (sb & 1023u)) & 1023u);
-  float *cf = reinterpret_cast<float *>(xbuf + kRLBufs * rowb);
-  float *cb = cf + blockDim.x * K;
-  float *vlr = cb + blockDim.x * K;  // [C][8]: vl (4), vr (4)
-  const int64_t H = p.H;
-  const int W = (int)p.W;
-  for (int e = c; e < C * 8; e += blockDim.x) vlr[e] = vtab.v[e];
-  const bool edge = blockIdx.x == gridDim.x - 1;
-  const int64_t rlo = edge ? 0 : (int64_t)blockIdx.x * p.rows_per;
-  const int64_t rhi = edge ? 0 : (rlo + p.rows_per < H ? rlo + p.rows_per : H);
+  float *cfb = reinterpret_cast<float *>(xbuf + kRLBufs * rowb);  // [ns][2][blockDim][K]
+  auto cfs = [&](int s) { return cfb + (size_t)s * 2 * blockDim.x * K; };
+  auto cbs = [&](int s) { return cfb + (size_t)(2 * s + 1) * blockDim.x * K; };
+  const int64_t H = rm.H;
+  const int W = (int)rm.W;
+  const int nrowctas = (int)gridDim.x - ns;
+  const bool edge = (int)blockIdx.x >= nrowctas;
+  const int64_t rlo = edge ? 0 : (int64_t)blockIdx.x * rm.rows_per;
+  const int64_t rhi = edge ? 0 : (rlo + rm.rows_per < H ? rlo + rm.rows_per : H);
   const int nrows = (int)(rhi - rlo);
   auto issue_row = [&](int s, int64_t r) {
     mbar_expect_tx(&bar[s], (unsigned)rowbytes);
     tma_load_3d_hint(xbuf + s * rowb, &xmap, &bar[s], 0, 0, (int)r, l2_policy_evict_first());
   };
-  // row CTAs: logical input row j = clamp(rlo - 1 + j), j = 0 .. nrows + 1,
-  // in slot j % 3; the edge CTA: rows 0 and H-1 in slots 0 / 1
   auto clampr = [&](int64_t r) { return r < 0 ? (int64_t)0 : (r >= H ? H - 1 : r); };
   if (c == 0) {
     for (int s = 0; s < kRLBufs; ++s) mbar_init(&bar[s], 1);
@@ -213,9 +253,12 @@ __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
     }
   }
   __syncthreads();
+  // the border kernel (this grid's predecessor) wrote the chunk vectors and
+  // segment shares; the previous scale's column pass may still read V
+  pdl_wait();
   float U[kRChunk], V[kRChunk], X[kRChunk];
-  auto load_chunk = [&](int s, float (&o)[kRChunk]) {
-    const SwzRow32 r{xbuf + s * rowb};
+  auto load_chunk = [&](int sl, float (&o)[kRChunk]) {
+    const SwzRow32 r{xbuf + sl * rowb};
 #pragma unroll
     for (int q = 0; q < kRChunk / 4; ++q) {
       const float4 v = live ? r.ld4(c, q) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -225,23 +268,45 @@ __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
       o[4 * q + 3] = v.w;
     }
   };
-  auto halos = [&](int s, const float (&x)[kRChunk], float &xl, float &xr) {
-    const SwzRow32 r{xbuf + s * rowb};
+  auto halos = [&](int sl, const float (&x)[kRChunk], float &xl, float &xr) {
+    const SwzRow32 r{xbuf + sl * rowb};
     xl = c > 0 && live ? r.ld(c * kRChunk - 1) : x[0];
     xr = c < C - 1 ? r.ld(c * kRChunk + kRChunk) : x[kRChunk - 1];
   };
-  auto reduce_dx = [&]() {  // (thread 0, after a barrier that follows dx_partials)
-    float a = 0.0f, b = 0.0f;
-    for (int w = 0; w < nwarp; ++w) {
-      a += red[w];
-      b += red[8 + w];
+  // border partials of all scales (first differences g of this thread's
+  // chunk), warp-reduced into red[s][warp] / red[s][8 + warp]
+  auto dx_all = [&](const float (&x)[kRChunk], float xr) {
+    float g[kRChunk];
+#pragma unroll
+    for (int t = 0; t < kRChunk; ++t) g[t] = (t < kRChunk - 1 ? x[t + 1] : xr) - x[t];
+    for (int s = 0; s < ns; ++s) {
+      float pl, pr;
+      dx_chunk<K>(rm.s[s], out.E[s] + kExVlr * W, g, pl, pr);
+      warp_sum2(pl, pr);
+      if (lane == 0) {
+        red[s][c >> 5] = pl;
+        red[s][8 + (c >> 5)] = pr;
+      }
     }
-    dx2[0] = p.sign * a;
-    dx2[1] = b;
+  };
+  auto reduce_dx = [&]() {  // (thread 0, after the barrier that follows dx_all)
+    for (int s = 0; s < ns; ++s) {
+      float a = 0.0f, b = 0.0f;
+      for (int w = 0; w < nwarp; ++w) {
+        a += red[s][w];
+        b += red[s][8 + w];
+      }
+      dx2[s][0] = rm.s[s].sign * a;
+      dx2[s][1] = b;
+    }
   };
 
   if (edge) {
-    // virtual rows: Vt / Vb = R0(D20 X) of row 0 / H-1 (zero starts), with
+    const int s = (int)blockIdx.x - nrowctas;
+    const RowLapParams &p = rm.s[s];
+    float *E = out.E[s];
+    float *cf = cfs(0), *cb = cbs(0);
+    // virtual rows: Vt / Vb = R0(D20 X) of row 0 / H-1 (zero starts) with
     // that row's left / right border terms
     for (int which = 0; which < 2; ++which) {
       mbar_wait(&bar[which], 0);
@@ -253,13 +318,32 @@ __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
         const float l = t ? X[t - 1] : xl, r = t < kRChunk - 1 ? X[t + 1] : xr;
         U[t] = (l - X[t]) + (r - X[t]);
       }
-      dx_partials<K>(p, vlr, X, xr, red);
+      {
+        float g[kRChunk];
+#pragma unroll
+        for (int t = 0; t < kRChunk; ++t) g[t] = (t < kRChunk - 1 ? X[t + 1] : xr) - X[t];
+        float pl, pr;
+        dx_chunk<K>(p, E + kExVlr * W, g, pl, pr);
+        warp_sum2(pl, pr);
+        if (lane == 0) {
+          red[0][c >> 5] = pl;
+          red[0][8 + (c >> 5)] = pr;
+        }
+      }
       if (c == 0) e2[0] = e2[1] = 0.0f;
       row_carry32<K>(p, U, cf, cb);
       __syncthreads();
-      if (c == 0) reduce_dx();
-      row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2);
-      float *dst = which == 0 ? Vt : Vb;
+      if (c == 0) {
+        float a = 0.0f, b = 0.0f;
+        for (int w = 0; w < nwarp; ++w) {
+          a += red[0][w];
+          b += red[0][8 + w];
+        }
+        dx2[0][0] = p.sign * a;
+        dx2[0][1] = b;
+      }
+      row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2[0]);
+      float *dst = E + (which == 0 ? kExVt : kExVb) * W;
       if (live) {
 #pragma unroll
         for (int q = 0; q < kRChunk / 4; ++q)
@@ -268,17 +352,16 @@ __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
       }
       __syncthreads();
     }
-    // border rows: Ky = R_ss(dy), dy = sum of the border kernel's segment
-    // shares (the border kernel is this grid's predecessor)
-    pdl_wait();
+    // border rows: Ky = R_ss(dy), dy = the border kernel's segment shares
     float *rowp = reinterpret_cast<float *>(xbuf);  // (the input slots are idle now)
+    const int nsg = p.nseg;
     for (int which = 0; which < 2; ++which) {
       for (int n = c; n < W; n += blockDim.x) {
         float a = 0.0f;
-        for (int k = 0; k < nseg; ++k) a += __ldg(S + ((int64_t)which * nseg + k) * W + n);
+        for (int k = 0; k < nsg; ++k) a += __ldg(E + kExS * W + ((int64_t)which * nsg + k) * W + n);
         rowp[n + (n >> 5)] = a;
       }
-      if (c == 0) dx2[0] = dx2[1] = 0.0f;
+      if (c == 0) dx2[0][0] = dx2[0][1] = 0.0f;
       __syncthreads();
       if (c == 0) {
         e2[0] = rowp[0];
@@ -287,13 +370,13 @@ __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
 #pragma unroll
       for (int t = 0; t < kRChunk; ++t) U[t] = live ? rowp[c * (kRChunk + 1) + t] : 0.0f;
       __syncthreads();
-      row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2);
+      row_filter<K, KIND>(p, U, V, cf, cb, e2, dx2[0]);
       if (live) {
 #pragma unroll
         for (int t = 0; t < kRChunk; ++t) rowp[c * (kRChunk + 1) + t] = V[t];
       }
       __syncthreads();
-      for (int n = c; n < W; n += blockDim.x) Ky[(int64_t)which * W + n] = rowp[n + (n >> 5)];
+      for (int n = c; n < W; n += blockDim.x) E[kExKy * W + (int64_t)which * W + n] = rowp[n + (n >> 5)];
       __syncthreads();
     }
     pdl_trigger();
@@ -325,28 +408,34 @@ __global__ void __launch_bounds__(kRLMaxC) rowlap_kernel(
         U[t] = ((l - X[t]) + (rr - X[t])) + (U[t] + (Xu[t] - X[t]));
       }
     }
-    dx_partials<K>(p, vlr, X, xr, red);
-    if (c == 0 || c == C - 1) {  // D02 X of the end samples: the steady starts
+    dx_all(X, xr);
+    if (c == 0 || c == C - 1) {  // D02 X of the end samples: the steady starts (every scale)
       const SwzRow32 ru{xbuf + su * rowb}, rd{xbuf + sd * rowb};
       const int n = c == 0 ? 0 : W - 1;
       const float xc = X[c == 0 ? 0 : kRChunk - 1];
       e2[c == 0 ? 0 : 1] = (ru.ld(n) - xc) + (rd.ld(n) - xc);
     }
-    row_carry32<K>(p, U, cf, cb);
+    for (int s = 0; s < ns; ++s) row_carry32<K>(rm.s[s], U, cfs(s), cbs(s));
     __syncthreads();  // rows r-1 .. r+1 read; carries, e2, red published
     if (c == 0) {
       if (i + 3 <= nrows + 1) issue_row(su, clampr(rlo + 2 + i));  // row r+2 -> slot of r-1
       reduce_dx();
     }
-    row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2);
-    if (i == 0) pdl_wait();  // V may still be read by the previous scale's column pass
-    if (live) {
-      float *dst = Vout + r * ldv + c * kRChunk;
-      const uint64_t pol = l2_policy_evict_last();  // V is read twice by the column pass
+    // the 2 ns chunk scans over the warps
+    for (int task = c >> 5; task < 2 * ns; task += nwarp)
+      chunk_scan32<K>(rm.s[task >> 1], (task & 1) ? cbs(task >> 1) : cfs(task >> 1), task & 1,
+                      e2[task & 1], lane);
+    __syncthreads();
+    for (int s = 0; s < ns; ++s) {
+      row_walks32<K, KIND>(rm.s[s], U, V, cfs(s), cbs(s), dx2[s]);
+      if (live) {
+        float *dst = out.V[s] + r * out.ldv + c * kRChunk;
+        const uint64_t pol = l2_policy_evict_last();  // V is read twice by the column pass
 #pragma unroll
-      for (int q = 0; q < kRChunk / 4; ++q)
-        st_v4_hint(dst + 4 * q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]),
-                   pol);
+        for (int q = 0; q < kRChunk / 4; ++q)
+          st_v4_hint(dst + 4 * q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]),
+                     pol);
+      }
     }
   }
   pdl_trigger();
@@ -395,42 +484,13 @@ static int rl_plan(RowLapPlan *P, int64_t h, int64_t w, const double *b, const d
     }
   for (int t = 0; t < kRChunk; ++t)
     for (int i = 0; i < k; ++i) p.Wt[t][i] = (float)Wt[t][i];
-  // border-term chunk vectors vl(c) = c A^(32 c), vr(c) = c A^(W - 32 c - 33)
-  {
-    ld Ainv[16], IA[16];
-    for (int i = 0; i < k * k; ++i) IA[i] = M.A[i];
-    for (int col = 0; col < k; ++col) {  // A^-1 column by column
-      ld M2[16], y[4];
-      memcpy(M2, IA, sizeof(ld) * k * k);
-      for (int i = 0; i < k; ++i) y[i] = (i == col) ? 1 : 0;
-      if (!solve(M2, y, k)) return fail(VMF_EVALUE, "singular modal matrix");
-      for (int i = 0; i < k; ++i) Ainv[i * k + col] = y[i];
-    }
-    memset(&P->vlr, 0, sizeof(P->vlr));
-    ld A32[16];
-    matpow(M.A, kRChunk, A32, k);
-    ld v[4], t4[4];
-    for (int i = 0; i < k; ++i) v[i] = M.c[i];  // c A^0
-    for (int cc = 0; cc < p.C; ++cc) {          // vl(cc) = c A^(32 cc)
-      for (int i = 0; i < k; ++i) P->vlr.v[cc * 8 + i] = (float)v[i];
-      for (int jj = 0; jj < k; ++jj) {
-        t4[jj] = 0;
-        for (int i = 0; i < k; ++i) t4[jj] += v[i] * A32[i * k + jj];
-      }
-      memcpy(v, t4, sizeof(ld) * k);
-    }
-    for (int i = 0; i < k; ++i) {  // vr(C-1) = c A^-1, then x A^32 going left
-      v[i] = 0;
-      for (int jj = 0; jj < k; ++jj) v[i] += M.c[jj] * Ainv[jj * k + i];
-    }
-    for (int cc = p.C - 1; cc >= 0; --cc) {
-      for (int i = 0; i < k; ++i) P->vlr.v[cc * 8 + 4 + i] = (float)v[i];
-      for (int jj = 0; jj < k; ++jj) {
-        t4[jj] = 0;
-        for (int i = 0; i < k; ++i) t4[jj] += v[i] * A32[i * k + jj];
-      }
-      memcpy(v, t4, sizeof(ld) * k);
-    }
+  {  // c A^-1: the right border's vector of the last chunk
+    ld At[16], x[4];
+    for (int i = 0; i < k; ++i)
+      for (int jj = 0; jj < k; ++jj) At[i * k + jj] = M.A[jj * k + i];
+    for (int i = 0; i < k; ++i) x[i] = M.c[i];
+    if (!solve(At, x, k)) return fail(VMF_EVALUE, "singular modal matrix");
+    for (int i = 0; i < k; ++i) P->ci[i] = (float)x[i];
   }
   ld A32[16];
   matpow(M.A, kRChunk, A32, k);
@@ -486,8 +546,6 @@ static int rl_plan(RowLapPlan *P, int64_t h, int64_t w, const double *b, const d
     // gradients -- far below fp32 L)
     while (Mh > 1 && tail + fabsl(hv[Mh]) < 1e-8L * tot) tail += fabsl(hv[Mh--]);
     p.Mh = (int)Mh;
-    memset(&P->hm, 0, sizeof(P->hm));
-    for (int64_t m = 1; m <= Mh; ++m) P->hm.h[m] = (float)hv[m];
   }
   return VMF_OK;
 }
@@ -522,58 +580,17 @@ bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, in
 
 static int rl_block(int C) { return (C + 31) / 32 * 32; }
 
-static size_t rl_smem(int C, int k) {
+static size_t rl_smem(int C, int k, int ns) {
   return 1024 + (size_t)kRLBufs * ((C * 128 + 1023) & ~1023) +
-         2 * (size_t)rl_block(C) * k * sizeof(float) + (size_t)C * 8 * sizeof(float);
+         (size_t)ns * 2 * rl_block(C) * k * sizeof(float);
 }
 
-template <int K, int KIND>
-static int launch_rowlap(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows,
-                         RowLapPlan &P, const RowLapPlan &PC, const SegVec &sv, cudaStream_t st) {
-  RowLapParams &p = P.p;
-  CUtensorMap xm;
-  memset(&xm, 0, sizeof(xm));
-  if (!make_tmap_rows_swz_f32(&xm, x, p.H, p.W, ldx, 1)) {
-    cudaGetLastError();
-    return fail(VMF_EVALUE, "row pass: TMA descriptor unavailable");
-  }
-  float *Vt = vrows, *Vb = vrows + p.W, *Ky = vrows + 2 * p.W, *S = vrows + 4 * p.W;
-  {
-    Launch g(K_ROW_BORDER, st);  // the border kernel (reads X only)
-    launch_pdl(rowborder_kernel<K, KIND>, dim3((unsigned)cdiv(p.W, 128), (unsigned)(2 * sv.nseg)),
-               dim3(128), 0, st, PC.p, sv, x, ldx, p.H, p.W, S);
-  }
-  const size_t smem = rl_smem(p.C, K);
-  const int block = rl_block(p.C);
-  static std::map<std::pair<int, size_t>, int> slot_cache;
-  const int dev = current_device();
-  int &slots = slot_cache[std::make_pair(dev, smem)];
-  static PerDevice attr;
-  if (attr.first())  // the largest footprint (C = 256), so every width may launch
-    cudaFuncSetAttribute(rowlap_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)rl_smem(kRLMaxC, K));
-  if (!slots) {
-    int occ = 0, nsm = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowlap_kernel<K, KIND>, block, smem);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
-    slots = (occ > 0 ? occ : 1) * nsm;
-  }
-  // one slot is the edge CTA (virtual and border rows)
-  p.rows_per = (int)cdiv(p.H, slots > 1 ? slots - 1 : 1);
-  const int grid = (int)cdiv(p.H, p.rows_per) + 1;
-  Launch g(K_IIR_ROWS_FUSED, st);
-  launch_pdl(rowlap_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm, (const RowLapParams)p,
-             V, ldv, P.vlr, Vt, Vb, (const float *)S, sv.nseg, Ky);
-  return cuda_status("fp32 row pass");
-}
-
-// segment vectors c A^(m0-1) of the column stage (m0 = 1 + 64 k)
-static int seg_vectors(const double *b, const double *a, int k, const RowLapPlan &PC, SegVec *sv) {
+// segment vectors c A^(m0-1) of a column stage (m0 = 1 + 64 k)
+static int seg_vectors(const double *b, const double *a, int k, int Mh, SegVec *sv) {
   Modal M;
   if (!modal_realise(b, a, k, &M)) return fail(VMF_EVALUE, "no modal realisation");
   memset(sv, 0, sizeof(*sv));
-  sv->Mh = PC.p.Mh;
+  sv->Mh = Mh;
   sv->nseg = (int)cdiv(sv->Mh, kSeg);
   if (sv->nseg > kMaxSeg) return fail(VMF_EVALUE, "border too long");
   ld v[4], t[4];
@@ -592,26 +609,117 @@ static int seg_vectors(const double *b, const double *a, int k, const RowLapPlan
   return VMF_OK;
 }
 
-int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows, int64_t h,
-               int64_t w, const double *b, const double *a, int k, double b0, int sign,
-               const double *cb_, const double *ca, double cb0, int csign, cudaStream_t st) {
-  static RowLapPlan P, PC;  // (large: not on the stack)
-  static SegVec sv;
+struct SweepPlan {
+  RowLapMulti rm;
+  BorderMulti bm;
+  int kind, nseg_total;
+};
+
+static int sweep_plan(int64_t h, int64_t w, int k, int ns, const SweepStage *st, SweepPlan *P) {
+  if (ns < 1 || ns > kMaxScales) return fail(VMF_EVALUE, "1..%d scales per sweep", kMaxScales);
+  memset(P, 0, sizeof(*P));
+  P->rm.ns = P->bm.ns = ns;
+  P->rm.H = h;
+  P->rm.W = w;
+  P->rm.C = (int)(w / kRChunk);
+  P->kind = -1;
+  for (int s = 0; s < ns; ++s) {
+    RowLapPlan R, Cp;
+    int rc = rowlap_get_plan(h, w, st[s].rb, st[s].ra, k, st[s].rb0, st[s].rsign, &R);
+    if (rc) return rc;
+    // the column stage along the columns (length h): modal form, border length
+    rc = rowlap_get_plan(w, h, st[s].cb, st[s].ca, k, st[s].cb0, st[s].csign, &Cp);
+    if (rc) return rc;
+    if (R.kind != Cp.kind || (P->kind >= 0 && R.kind != P->kind))
+      return fail(VMF_EVALUE, "sweep: every stage needs the same modal structure");
+    P->kind = R.kind;
+    P->rm.s[s] = R.p;
+    BorderScale &b = P->bm.s[s];
+    b.p = Cp.p.p;
+    b.q = Cp.p.q;
+    b.sign = Cp.p.sign;
+    for (int i = 0; i < 4; ++i) {
+      b.c[i] = Cp.p.c[i];
+      b.cr[i] = R.p.c[i];
+      b.ci[i] = R.ci[i];
+    }
+    for (int i = 0; i < 16; ++i) b.A32[i] = R.p.A32[i];
+    b.C = R.p.C;
+    b.Mh = R.p.Mh;
+    rc = seg_vectors(st[s].cb, st[s].ca, k, Cp.p.Mh, &b.sv);
+    if (rc) return rc;
+    P->rm.s[s].nseg = b.sv.nseg;
+    P->nseg_total += 2 * b.sv.nseg;
+  }
+  return VMF_OK;
+}
+
+bool sweep_supported(const void *x, int64_t h, int64_t w, int64_t ldx, int k, int ns,
+                     const SweepStage *st) {
+  if (getenv("VMF_NO_ROWLAP") || h < 2 || w < 64 || w % kRChunk || w / kRChunk > kRLMaxC)
+    return false;
+  if (((uintptr_t)x & 15) || ((ldx * 4) & 15)) return false;
+  static SweepPlan P;
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
-  int rc = rowlap_get_plan(h, w, b, a, k, b0, sign, &P);
+  return sweep_plan(h, w, k, ns, st, &P) == VMF_OK &&
+         rl_smem((int)(w / kRChunk), k, ns) <= 227 * 1024;
+}
+
+template <int K, int KIND>
+static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOut &out,
+                        cudaStream_t st) {
+  RowLapMulti &rm = P.rm;
+  CUtensorMap xm;
+  memset(&xm, 0, sizeof(xm));
+  if (!make_tmap_rows_swz_f32(&xm, x, rm.H, rm.W, ldx, 1)) {
+    cudaGetLastError();
+    return fail(VMF_EVALUE, "row pass: TMA descriptor unavailable");
+  }
+  {
+    Launch g(K_ROW_BORDER, st);  // the border kernel (reads X only)
+    launch_pdl(sweep_border_kernel<K, KIND>,
+               dim3((unsigned)cdiv(rm.W, 128), (unsigned)(P.nseg_total + rm.ns)), dim3(128), 0, st,
+               P.bm, x, ldx, rm.H, rm.W, out);
+  }
+  const size_t smem = rl_smem(rm.C, K, rm.ns);
+  const int block = rl_block(rm.C);
+  static std::map<std::pair<int, size_t>, int> slot_cache;
+  const int dev = current_device();
+  int &slots = slot_cache[std::make_pair(dev, smem)];
+  static PerDevice attr;
+  if (attr.first())
+    cudaFuncSetAttribute(sweep_rows_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+  if (!slots) {
+    int occ = 0, nsm = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_rows_kernel<K, KIND>, block, smem);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    slots = (occ > 0 ? occ : 1) * nsm;
+  }
+  // ns slots are the edge CTAs (virtual and border rows of each scale)
+  const int rslots = slots > rm.ns ? slots - rm.ns : 1;
+  rm.rows_per = (int)cdiv(rm.H, rslots);
+  const int grid = (int)cdiv(rm.H, rm.rows_per) + rm.ns;
+  Launch g(K_IIR_ROWS_FUSED, st);
+  launch_pdl(sweep_rows_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm,
+             (const RowLapMulti)rm, out);
+  return cuda_status("fp32 row pass");
+}
+
+int sweep_rows(const float *x, int64_t ldx, int64_t h, int64_t w, int k, int ns,
+               const SweepStage *st, const SweepOut &out, cudaStream_t stream) {
+  static SweepPlan P;  // (large: not on the stack)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  int rc = sweep_plan(h, w, k, ns, st, &P);
   if (rc) return rc;
-  // the column stage's modal form and border length along the columns
-  rc = rowlap_get_plan(w, h, cb_, ca, k, cb0, csign, &PC);
-  if (rc) return rc;
-  if (PC.kind != P.kind) return fail(VMF_EVALUE, "fp32 path: stages of different structure");
-  rc = seg_vectors(cb_, ca, k, PC, &sv);
-  if (rc) return rc;
-  if (P.kind == M32_CPAIR) return launch_rowlap<2, M32_CPAIR>(x, ldx, V, ldv, vrows, P, PC, sv, st);
+  if (P.kind == M32_CPAIR) return launch_sweep<2, M32_CPAIR>(x, ldx, P, out, stream);
   switch (k) {
-    case 2: return launch_rowlap<2, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, sv, st);
-    case 3: return launch_rowlap<3, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, sv, st);
-    case 4: return launch_rowlap<4, M32_JORDAN>(x, ldx, V, ldv, vrows, P, PC, sv, st);
+    case 2: return launch_sweep<2, M32_JORDAN>(x, ldx, P, out, stream);
+    case 3: return launch_sweep<3, M32_JORDAN>(x, ldx, P, out, stream);
+    case 4: return launch_sweep<4, M32_JORDAN>(x, ldx, P, out, stream);
   }
   return fail(VMF_EVALUE, "fp32 row pass supports K = 2..4, got %d", k);
 }

@@ -19,6 +19,7 @@ struct RowLapParams {
   float Iss[4];         // (I - A)^-1 b
   int64_t H, W;
   int C, cpl, rows_per, Mh, K;
+  int nseg;             // (sweep) the column stage's border segments of this scale
 };
 
 constexpr int kMaxSeg = 32;  // border segments of 64 rows (Mh <= 2048)
@@ -27,19 +28,46 @@ struct SegVec {             // c A^(m0-1) per border segment (column stage)
   int nseg, Mh;
 };
 
-struct HmRow {
-  float h[kHmRowMax + 1];
-};
-
-struct VlrTab {  // [C][8]: the border-term chunk vectors vl(c) (4), vr(c) (4)
-  float v[256 * 8];
-};
-
-struct RowLapPlan {
+struct RowLapPlan {  // (POD: cached by value)
   RowLapParams p;
-  HmRow hm;
-  VlrTab vlr;
+  float ci[4];        // c A^-1 (the right border's last-chunk vector)
   int kind;
+};
+
+// ---------------------------------------------------------------------------
+// multi-scale sweep (vmf_rowlap.cu): one pass over X feeds every scale's row
+// filter (U = Lap5 X, the X staging and the barriers are shared), then one
+// column pass per scale
+// ---------------------------------------------------------------------------
+constexpr int kMaxScales = 8;
+
+struct RowLapMulti {
+  RowLapParams s[kMaxScales];  // per scale: the row stage
+  int ns;
+  int64_t H, W;
+  int C, rows_per;
+};
+
+struct BorderScale {   // per scale, for the border kernel
+  float p, q, c[4], sign;   // the column stage (column-direction recursion)
+  SegVec sv;                // its segment vectors
+  float A32[16], cr[4], ci[4];  // the row stage: A^32, c, c A^-1 (chunk vectors)
+  int C, Mh;                // chunks; the row stage's border length
+};
+struct BorderMulti {
+  BorderScale s[kMaxScales];
+  int ns;
+};
+
+// Per-scale extras, floats, w = frame width: Vt [w] | Vb [w] | Ky [2w] |
+// S [2 x kMaxSeg x w] | vlr [C x 8]
+constexpr int64_t kExVt = 0, kExVb = 1, kExKy = 2, kExS = 4, kExVlr = 4 + 2 * kMaxSeg;
+inline int64_t sweep_extras_floats(int64_t w) { return (kExVlr + 1) * w; }
+
+struct SweepOut {
+  float *V[kMaxScales];   // V_s (pitch ldv)
+  float *E[kMaxScales];   // extras_s
+  int64_t ldv;
 };
 
 constexpr int kRChunk = 32;
@@ -76,23 +104,21 @@ __device__ __forceinline__ void row_carry32(const RowLapParams &p, const float (
   }
 }
 
-template <int K, int KIND>
-__device__ __forceinline__ void row_scan_walk32(const RowLapParams &p, const float (&U)[kRChunk],
-                                                float (&V)[kRChunk], float *cf, float *cb,
-                                                const float *e2, const float *dx2) {
-  const int c = threadIdx.x, C = p.C, lane = c & 31, warp = c >> 5;
-  // chunk scans: task 0 forward (chunks 0..C-1), task 1 backward
-  for (int task = warp; task < 2; task += (int)(blockDim.x >> 5)) {
-    float *cc = task == 0 ? cf : cb;
-    const int cpl = p.cpl;
-    const float e = e2[task];
+// One chunk scan (one warp): direction dir (0: chunks 0..C-1, 1: backward)
+// over the zero-state carries in cc, steady start e; leaves every chunk's
+// start state in cc.
+template <int K>
+__device__ __forceinline__ void chunk_scan32(const RowLapParams &p, float *cc, int dir, float e,
+                                             int lane) {
+
+    const int cpl = p.cpl, C = p.C;
     float A[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) A[i] = 0.0f;
     for (int q = 0; q < cpl; ++q) {
       const int sp = lane * cpl + q;
       if (sp >= C) break;
-      const int ch = task == 0 ? sp : C - 1 - sp;
+      const int ch = dir == 0 ? sp : C - 1 - sp;
       float d[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) d[i] = cc[ch * K + i];
@@ -139,7 +165,7 @@ __device__ __forceinline__ void row_scan_walk32(const RowLapParams &p, const flo
     for (int q = 0; q < cpl; ++q) {
       const int sp = lane * cpl + q;
       if (sp >= C) break;
-      const int ch = task == 0 ? sp : C - 1 - sp;
+      const int ch = dir == 0 ? sp : C - 1 - sp;
       float d[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
@@ -159,8 +185,14 @@ __device__ __forceinline__ void row_scan_walk32(const RowLapParams &p, const flo
       for (int i = 0; i < K; ++i) E[i] = En[i];
     }
   }
-  __syncthreads();
-  // walks: backward parked (b0 U + s y-), forward adds y+
+
+// The walks of one row (after the scans): backward parked (b0 U + s y-),
+// forward adds y+; the row's border terms on the end samples.
+template <int K, int KIND>
+__device__ __forceinline__ void row_walks32(const RowLapParams &p, const float (&U)[kRChunk],
+                                            float (&V)[kRChunk], const float *cf, const float *cb,
+                                            const float *dx2) {
+  const int c = threadIdx.x, C = p.C;
   float park[kRChunk];
   {
     Rec32<K, KIND> rb;
@@ -186,8 +218,17 @@ __device__ __forceinline__ void row_scan_walk32(const RowLapParams &p, const flo
   if (c == C - 1) V[kRChunk - 1] -= dx2[1];
 }
 
-int rowlap_get_plan(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
-                    int sign, RowLapPlan *out);
+
+template <int K, int KIND>
+__device__ __forceinline__ void row_scan_walk32(const RowLapParams &p, const float (&U)[kRChunk],
+                                                float (&V)[kRChunk], float *cf, float *cb,
+                                                const float *e2, const float *dx2) {
+  const int c = threadIdx.x, lane = c & 31, warp = c >> 5;
+  for (int task = warp; task < 2; task += (int)(blockDim.x >> 5))
+    chunk_scan32<K>(p, task == 0 ? cf : cb, task, e2[task], lane);
+  __syncthreads();
+  row_walks32<K, KIND>(p, U, V, cf, cb, dx2);
+}
 
 // both phases (contains two block barriers)
 template <int K, int KIND>
@@ -199,16 +240,22 @@ __device__ __forceinline__ void row_filter(const RowLapParams &p, const float (&
   row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2);
 }
 
+int rowlap_get_plan(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
+                    int sign, RowLapPlan *out);
 bool rowlap_supported(int64_t h, int64_t w, const double *b, const double *a, int k, double b0,
                       int sign);
-// X (fp32, pitch ldx; 16-byte aligned rows) -> V = R(Lap5 X) (pitch ldv) with
-// the left / right border terms folded in; vrows = [Vt | Vb | Ky(2) | S(2 x 32)]
-// x w floats: the virtual rows above / below the image, the column
-// direction's border rows Ky = R_ss(Dy) (column stage (cb_, ca, cb0, csign),
-// same order k) and the border kernel's segment shares S.
-int rowlap_run(const float *x, int64_t ldx, float *V, int64_t ldv, float *vrows, int64_t h,
-               int64_t w, const double *b, const double *a, int k, double b0, int sign,
-               const double *cb_, const double *ca, double cb0, int csign, cudaStream_t st);
-constexpr int kRowLapVrows = 4 + 2 * kMaxSeg;  // floats per column of vrows
+
+// One sweep's stage pair per scale (row stage, column stage), all of one
+// order k and one modal kind.  sweep_rows: the border kernel, then the
+// multi-scale row pass: V_s and the extras of every scale.
+struct SweepStage {
+  const double *rb, *ra, *cb, *ca;
+  double rb0, cb0;
+  int rsign, csign;
+};
+bool sweep_supported(const void *x, int64_t h, int64_t w, int64_t ldx, int k, int ns,
+                     const SweepStage *st);
+int sweep_rows(const float *x, int64_t ldx, int64_t h, int64_t w, int k, int ns,
+               const SweepStage *st, const SweepOut &out, cudaStream_t stream);
 
 }  // namespace vmf

@@ -131,15 +131,67 @@ def _side(n: int):
     return lst[:n]
 
 
+_SWEEP_SLOT = 1000  # workspace slot of the multi-scale row pass's outputs
+
+
+def _sweep_ok(x, code, stages) -> bool:
+    """The multi-scale fp32 path takes this sweep (vmf_sweep_supported)."""
+    if isinstance(x, (list, tuple)) or code != _lib.VMF_F32 or not stages:
+        return False
+    if os.environ.get("VMF_NO_SWEEP"):
+        return False
+    h, w = x.shape
+    arr = (_lib.VmfStage * len(stages))(*[st.s for st in stages])
+    return bool(_lib.lib().vmf_sweep_supported(_ptr(x), code, h, w, _pitch(x), len(stages), arr,
+                                               arr))
+
+
+def _sweep_launch_multi(x, code, stages, frac, lap_scales, cap, outs, laps, conc):
+    """One row pass for every scale (vmf_sweep_rows: the Laplacian of the
+    frame and its staging shared by all scales), then each scale's column
+    pass on `conc` side streams (vmf_sweep_detect)."""
+    L = _lib.lib()
+    h, w = x.shape
+    ns = len(stages)
+    arr = (_lib.VmfStage * ns)(*[st.s for st in stages])
+    sws = _workspace(L.vmf_sweep_workspace_bytes(h, w, ns), _SWEEP_SLOT)
+    _lib.check(L.vmf_sweep_rows(_ptr(x), code, h, w, _pitch(x), ns, arr, arr, _ptr(sws),
+                                sws.numel(), _stream()))
+    cur = torch.cuda.current_stream()
+    side = _side(conc) if conc > 1 else [cur]
+    if conc > 1:
+        for s in side:
+            s.wait_stream(cur)
+    for i in range(ns):
+        sc = 1.0 if lap_scales is None else float(lap_scales[i])
+        det_yx, det_val, scal = outs[i]
+        with torch.cuda.stream(side[i % len(side)]):
+            ws = _workspace(L.vmf_sweep_detect_workspace_bytes(h, w, C.byref(stages[i].s)),
+                            1 + i % len(side))
+            lap = None if laps is None else laps[i]
+            _lib.check(L.vmf_sweep_detect(
+                i, h, w, ns, C.byref(stages[i].s), sc, float(frac),
+                _ptr(lap) if lap is not None else None, _ptr(det_yx), _ptr(det_val), int(cap),
+                _ptr(scal), scal.data_ptr() + 8, _ptr(sws), sws.numel(), _ptr(ws), ws.numel(),
+                _stream()))
+    if conc > 1:
+        for s in side:
+            cur.wait_stream(s)
+
+
 def _sweep_launch(x, code, stages, frac, lap_scales, cap, outs, laps=None,
                   conc: int = SWEEP_STREAMS):
     """Queue one fused single-scale pass per stage.  The scales of a sweep
     are independent (same frame, own outputs), so with conc > 1 they run on
     `conc` side streams, each with its own workspace slot, forked from and
     joined back into the current stream: one scale's latency-bound phases
-    (band scan, finaliser, kernel tails) overlap another's row pass."""
+    (band scan, finaliser, kernel tails) overlap another's row pass.  When
+    the fp32 path takes the sweep, one row pass serves every scale."""
     ns = len(stages)
     conc = max(1, min(int(conc), ns))
+    if _sweep_ok(x, code, stages):
+        _sweep_launch_multi(x, code, stages, frac, lap_scales, cap, outs, laps, conc)
+        return
 
     def one(i, slot):  # x: one frame for every stage, or a list (one frame per stage)
         sc = 1.0 if lap_scales is None else float(lap_scales[i])
