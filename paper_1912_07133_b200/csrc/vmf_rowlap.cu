@@ -663,7 +663,7 @@ bool sweep_supported(const void *x, int64_t h, int64_t w, int64_t ldx, int k, in
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   return sweep_plan(h, w, k, ns, st, &P) == VMF_OK &&
-         rl_smem((int)(w / kRChunk), k, ns) <= 227 * 1024;
+         rl_smem((int)(w / kRChunk), k, ns) <= 220 * 1024;
 }
 
 template <int K, int KIND>
@@ -688,9 +688,14 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
   const int dev = current_device();
   int &slots = slot_cache[std::make_pair(dev, smem)];
   static PerDevice attr;
-  if (attr.first())
+  if (attr.first()) {  // the largest dynamic footprint next to the static shared memory
+    cudaFuncAttributes fa;
+    memset(&fa, 0, sizeof(fa));
+    cudaFuncGetAttributes(&fa, sweep_rows_kernel<K, KIND>);
     cudaFuncSetAttribute(sweep_rows_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
+                         227 * 1024 - (int)fa.sharedSizeBytes);
+    cudaGetLastError();
+  }
   if (!slots) {
     int occ = 0, nsm = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_rows_kernel<K, KIND>, block, smem);
