@@ -39,7 +39,7 @@ struct RowLapPlan {  // (POD: cached by value)
 // filter (U = Lap5 X, the X staging and the barriers are shared), then one
 // column pass per scale
 // ---------------------------------------------------------------------------
-constexpr int kMaxScales = 8;
+constexpr int kMaxScales = 5;  // (one row-pass instantiation per count)
 
 struct RowLapMulti {
   RowLapParams s[kMaxScales];  // per scale: the row stage
