@@ -173,31 +173,31 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
 // sums with the uniform weights A^t b (g: its first differences) and dots
 // them with its vectors vl, vr (the border kernel's table); chunks farther
 // than Mh from an edge contribute nothing measurable and skip.
-template <int K>
-__device__ __forceinline__ void dx_chunk(const RowLapParams &p, const float *vlr,
-                                         const float (&g)[kRChunk], float &pl, float &pr) {
+template <int K, int KIND>
+__device__ __forceinline__ void dx_chunk(const RowLapParams &p, const RC32<K> &rc,
+                                         const float *vlr, const float (&g)[kRChunk], float &pl,
+                                         float &pr) {
   const int c = threadIdx.x;
   const int n0 = c * kRChunk;
   const int W = (int)p.W, Mh = p.Mh, C = p.C;
   pl = pr = 0.0f;
   const bool L = c < C && n0 < Mh, Rr = c < C && n0 + kRChunk >= W - Mh;
   if (L || Rr) {
-    float zl[K], zr[K];
+    // zl = sum_t A^t b g_t (recursion from t = 31 down), zr = sum_t A^(31-t) b g_t
+    Rec32<K, KIND> zl, zr;
 #pragma unroll
-    for (int i = 0; i < K; ++i) zl[i] = zr[i] = 0.0f;
+    for (int i = 0; i < K; ++i) zl.u[i] = zr.u[i] = 0.0f;
 #pragma unroll
-    for (int t = 0; t < kRChunk; ++t)
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        zl[i] = fmaf(p.Wt[t][i], g[t], zl[i]);
-        zr[i] = fmaf(p.Wt[kRChunk - 1 - t][i], g[t], zr[i]);
-      }
+    for (int t = 0; t < kRChunk; ++t) {
+      zl.step(rc, g[kRChunk - 1 - t]);
+      zr.step(rc, g[t]);
+    }
     if (L)
 #pragma unroll
-      for (int i = 0; i < K; ++i) pl = fmaf(__ldg(vlr + c * 8 + i), zl[i], pl);
+      for (int i = 0; i < K; ++i) pl = fmaf(__ldg(vlr + c * 8 + i), zl.u[i], pl);
     if (Rr)
 #pragma unroll
-      for (int i = 0; i < K; ++i) pr = fmaf(__ldg(vlr + c * 8 + 4 + i), zr[i], pr);
+      for (int i = 0; i < K; ++i) pr = fmaf(__ldg(vlr + c * 8 + 4 + i), zr.u[i], pr);
   }
 }
 
@@ -214,7 +214,7 @@ __device__ __forceinline__ void warp_sum2(float &a, float &b) {
 // Ky = R_ss(Dy) of that scale (four single-row filters).  Per row, U = Lap5 X
 // is formed once and every scale's carries go before one barrier, the 2 ns
 // chunk scans share the warps, and each scale's walks write its V row.
-template <int K, int KIND, int NS>
+template <int K, int KIND>
 __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ RowLapMulti rm,
     SweepOut out) {
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
   __shared__ __align__(8) uint64_t bar[kRLBufs];
   __shared__ float red[kMaxScales][16], e2[2], dx2[kMaxScales][2];
   const int C = rm.C, c = threadIdx.x, nwarp = (int)(blockDim.x >> 5), lane = c & 31;
-  constexpr int ns = NS;  // (compile-time: every coefficient is a constant-bank operand)
+  const int ns = rm.ns;
   const bool live = c < C;  // the block is whole warps; threads c >= C carry no chunk
   const int rowbytes = C * 128;                // one row's TMA box
   const int rowb = (rowbytes + 1023) & ~1023;  // slot spacing: SWIZZLE_128B needs 1024-byte bases
@@ -279,10 +279,9 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     float g[kRChunk];
 #pragma unroll
     for (int t = 0; t < kRChunk; ++t) g[t] = (t < kRChunk - 1 ? x[t + 1] : xr) - x[t];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < ns; ++s) {
       float pl, pr;
-      dx_chunk<K>(rm.s[s], out.E[s] + kExVlr * W, g, pl, pr);
+      dx_chunk<K, KIND>(rm.s[s], RC32<K>(rm.s[s]), out.E[s] + kExVlr * W, g, pl, pr);
       warp_sum2(pl, pr);
       if (lane == 0) {
         red[s][c >> 5] = pl;
@@ -291,8 +290,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     }
   };
   auto reduce_dx = [&]() {  // (thread 0, after the barrier that follows dx_all)
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < ns; ++s) {
       float a = 0.0f, b = 0.0f;
       for (int w = 0; w < nwarp; ++w) {
         a += red[s][w];
@@ -325,7 +323,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
 #pragma unroll
         for (int t = 0; t < kRChunk; ++t) g[t] = (t < kRChunk - 1 ? X[t + 1] : xr) - X[t];
         float pl, pr;
-        dx_chunk<K>(p, E + kExVlr * W, g, pl, pr);
+        dx_chunk<K, KIND>(p, RC32<K>(p), E + kExVlr * W, g, pl, pr);
         warp_sum2(pl, pr);
         if (lane == 0) {
           red[0][c >> 5] = pl;
@@ -333,7 +331,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
         }
       }
       if (c == 0) e2[0] = e2[1] = 0.0f;
-      row_carry32<K>(p, U, cf, cb);
+      row_carry32<K, KIND>(RC32<K>(p), U, cf, cb);
       __syncthreads();
       if (c == 0) {
         float a = 0.0f, b = 0.0f;
@@ -417,24 +415,19 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
       const float xc = X[c == 0 ? 0 : kRChunk - 1];
       e2[c == 0 ? 0 : 1] = (ru.ld(n) - xc) + (rd.ld(n) - xc);
     }
-#pragma unroll
-    for (int s = 0; s < NS; ++s) row_carry32<K>(rm.s[s], U, cfs(s), cbs(s));
+    for (int s = 0; s < ns; ++s) row_carry32<K, KIND>(RC32<K>(rm.s[s]), U, cfs(s), cbs(s));
     __syncthreads();  // rows r-1 .. r+1 read; carries, e2, red published
     if (c == 0) {
       if (i + 3 <= nrows + 1) issue_row(su, clampr(rlo + 2 + i));  // row r+2 -> slot of r-1
       reduce_dx();
     }
     // the 2 ns chunk scans over the warps
-#pragma unroll
-    for (int s = 0; s < NS; ++s)
-#pragma unroll
-      for (int dir = 0; dir < 2; ++dir)
-        if ((2 * s + dir) % nwarp == (c >> 5))
-          chunk_scan32<K>(rm.s[s], dir ? cbs(s) : cfs(s), dir, e2[dir], lane);
+    for (int task = c >> 5; task < 2 * ns; task += nwarp)
+      chunk_scan32<K>(rm.s[task >> 1], (task & 1) ? cbs(task >> 1) : cfs(task >> 1), task & 1,
+                      e2[task & 1], lane);
     __syncthreads();
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      row_walks32<K, KIND>(rm.s[s], U, V, cfs(s), cbs(s), dx2[s]);
+    for (int s = 0; s < ns; ++s) {
+      row_walks32<K, KIND>(RC32<K>(rm.s[s]), C, U, V, cfs(s), cbs(s), dx2[s]);
       if (live) {
         float *dst = out.V[s] + r * out.ldv + c * kRChunk;
         const uint64_t pol = l2_policy_evict_last();  // V is read twice by the column pass
@@ -673,7 +666,7 @@ bool sweep_supported(const void *x, int64_t h, int64_t w, int64_t ldx, int k, in
          rl_smem((int)(w / kRChunk), k, ns) <= 220 * 1024;
 }
 
-template <int K, int KIND, int NS>
+template <int K, int KIND>
 static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOut &out,
                         cudaStream_t st) {
   RowLapMulti &rm = P.rm;
@@ -698,14 +691,14 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
   if (attr.first()) {  // the largest dynamic footprint next to the static shared memory
     cudaFuncAttributes fa;
     memset(&fa, 0, sizeof(fa));
-    cudaFuncGetAttributes(&fa, sweep_rows_kernel<K, KIND, NS>);
-    cudaFuncSetAttribute(sweep_rows_kernel<K, KIND, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncGetAttributes(&fa, sweep_rows_kernel<K, KIND>);
+    cudaFuncSetAttribute(sweep_rows_kernel<K, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024 - (int)fa.sharedSizeBytes);
     cudaGetLastError();
   }
   if (!slots) {
     int occ = 0, nsm = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_rows_kernel<K, KIND, NS>, block, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_rows_kernel<K, KIND>, block, smem);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
     slots = (occ > 0 ? occ : 1) * nsm;
@@ -715,22 +708,9 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
   rm.rows_per = (int)cdiv(rm.H, rslots);
   const int grid = (int)cdiv(rm.H, rm.rows_per) + rm.ns;
   Launch g(K_IIR_ROWS_FUSED, st);
-  launch_pdl(sweep_rows_kernel<K, KIND, NS>, dim3(grid), dim3(block), smem, st, xm,
+  launch_pdl(sweep_rows_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm,
              (const RowLapMulti)rm, out);
   return cuda_status("fp32 row pass");
-}
-
-template <int K, int KIND>
-static int launch_sweep_ns(const float *x, int64_t ldx, SweepPlan &P, const SweepOut &out,
-                           cudaStream_t st) {
-  switch (P.rm.ns) {
-    case 1: return launch_sweep<K, KIND, 1>(x, ldx, P, out, st);
-    case 2: return launch_sweep<K, KIND, 2>(x, ldx, P, out, st);
-    case 3: return launch_sweep<K, KIND, 3>(x, ldx, P, out, st);
-    case 4: return launch_sweep<K, KIND, 4>(x, ldx, P, out, st);
-    case 5: return launch_sweep<K, KIND, 5>(x, ldx, P, out, st);
-  }
-  return fail(VMF_EVALUE, "1..%d scales per sweep", kMaxScales);
 }
 
 int sweep_rows(const float *x, int64_t ldx, int64_t h, int64_t w, int k, int ns,
@@ -740,11 +720,11 @@ int sweep_rows(const float *x, int64_t ldx, int64_t h, int64_t w, int k, int ns,
   std::lock_guard<std::mutex> lk(mu);
   int rc = sweep_plan(h, w, k, ns, st, &P);
   if (rc) return rc;
-  if (P.kind == M32_CPAIR) return launch_sweep_ns<2, M32_CPAIR>(x, ldx, P, out, stream);
+  if (P.kind == M32_CPAIR) return launch_sweep<2, M32_CPAIR>(x, ldx, P, out, stream);
   switch (k) {
-    case 2: return launch_sweep_ns<2, M32_JORDAN>(x, ldx, P, out, stream);
-    case 3: return launch_sweep_ns<3, M32_JORDAN>(x, ldx, P, out, stream);
-    case 4: return launch_sweep_ns<4, M32_JORDAN>(x, ldx, P, out, stream);
+    case 2: return launch_sweep<2, M32_JORDAN>(x, ldx, P, out, stream);
+    case 3: return launch_sweep<3, M32_JORDAN>(x, ldx, P, out, stream);
+    case 4: return launch_sweep<4, M32_JORDAN>(x, ldx, P, out, stream);
   }
   return fail(VMF_EVALUE, "fp32 row pass supports K = 2..4, got %d", k);
 }

@@ -72,35 +72,48 @@ struct SweepOut {
 
 constexpr int kRChunk = 32;
 
+// The coefficients a chunk's recursions use, in registers (loaded once per
+// scale and row from the kernel parameters): pole, output vectors, b0.
+template <int K>
+struct RC32 {
+  float p, q, c[K], cs[K], b0;
+  __device__ __forceinline__ explicit RC32(const RowLapParams &P) {
+    p = P.p;
+    q = P.q;
+    b0 = P.b0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      c[i] = P.c[i];
+      cs[i] = P.cs[i];
+    }
+  }
+};
+
 // One row through R, in two phases around a block barrier:
-//   row_carry32: this thread's chunk U -> its zero-state carries in cf / cb;
+//   row_carry32: this thread's chunk U -> its zero-state carries in cf / cb
+//     (the forward end state and the backward start state of the chunk, by
+//     running the recursion from zero over the chunk: only the pole is
+//     needed, so nothing but registers is read);
 //   row_scan_walk32: (after the barrier) chunk scans, then the walks -> V.
 // e2: steady-state inputs left / right of the row; cf / cb: [blockDim][K]
 // scratch; dx2: the row's border terms (added to V(0) / subtracted from
 // V(W-1)), read only after the scan's barrier.
-template <int K>
-__device__ __forceinline__ void row_carry32(const RowLapParams &p, const float (&U)[kRChunk],
+template <int K, int KIND>
+__device__ __forceinline__ void row_carry32(const RC32<K> &rc, const float (&U)[kRChunk],
                                             float *cf, float *cb) {
   const int c = threadIdx.x;
-  // zero-state chunk carries: forward end state P + Q, backward start P - Q
-  {
-    float P[K], Q[K];
+  Rec32<K, KIND> f, b;
 #pragma unroll
-    for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0f;
+  for (int i = 0; i < K; ++i) f.u[i] = b.u[i] = 0.0f;
 #pragma unroll
-    for (int t = 0; t < kRChunk / 2; ++t) {
-      const float s = U[t] + U[kRChunk - 1 - t], d = U[t] - U[kRChunk - 1 - t];
+  for (int t = 0; t < kRChunk; ++t) {
+    f.step(rc, U[t]);
+    b.step(rc, U[kRChunk - 1 - t]);
+  }
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        P[i] = fmaf(p.SP[i][t], s, P[i]);
-        Q[i] = fmaf(p.SQ[i][t], d, Q[i]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      cf[c * K + i] = P[i] + Q[i];
-      cb[c * K + i] = P[i] - Q[i];
-    }
+  for (int i = 0; i < K; ++i) {
+    cf[c * K + i] = f.u[i];
+    cb[c * K + i] = b.u[i];
   }
 }
 
@@ -189,10 +202,10 @@ __device__ __forceinline__ void chunk_scan32(const RowLapParams &p, float *cc, i
 // The walks of one row (after the scans): backward parked (b0 U + s y-),
 // forward adds y+; the row's border terms on the end samples.
 template <int K, int KIND>
-__device__ __forceinline__ void row_walks32(const RowLapParams &p, const float (&U)[kRChunk],
+__device__ __forceinline__ void row_walks32(const RC32<K> &rc, int C, const float (&U)[kRChunk],
                                             float (&V)[kRChunk], const float *cf, const float *cb,
                                             const float *dx2) {
-  const int c = threadIdx.x, C = p.C;
+  const int c = threadIdx.x;
   float park[kRChunk];
   {
     Rec32<K, KIND> rb;
@@ -200,8 +213,8 @@ __device__ __forceinline__ void row_walks32(const RowLapParams &p, const float (
     for (int i = 0; i < K; ++i) rb.u[i] = cb[c * K + i];
 #pragma unroll
     for (int t = kRChunk - 1; t >= 0; --t) {
-      park[t] = rb.out_from(p.cs, p.b0 * U[t]);
-      rb.step(p, U[t]);
+      park[t] = rb.out_from(rc.cs, rc.b0 * U[t]);
+      rb.step(rc, U[t]);
     }
   }
   {
@@ -210,14 +223,13 @@ __device__ __forceinline__ void row_walks32(const RowLapParams &p, const float (
     for (int i = 0; i < K; ++i) rf.u[i] = cf[c * K + i];
 #pragma unroll
     for (int t = 0; t < kRChunk; ++t) {
-      V[t] = rf.out_from(p.c, park[t]);
-      rf.step(p, U[t]);
+      V[t] = rf.out_from(rc.c, park[t]);
+      rf.step(rc, U[t]);
     }
   }
   if (c == 0) V[0] += dx2[0];
   if (c == C - 1) V[kRChunk - 1] -= dx2[1];
 }
-
 
 template <int K, int KIND>
 __device__ __forceinline__ void row_scan_walk32(const RowLapParams &p, const float (&U)[kRChunk],
@@ -227,7 +239,7 @@ __device__ __forceinline__ void row_scan_walk32(const RowLapParams &p, const flo
   for (int task = warp; task < 2; task += (int)(blockDim.x >> 5))
     chunk_scan32<K>(p, task == 0 ? cf : cb, task, e2[task], lane);
   __syncthreads();
-  row_walks32<K, KIND>(p, U, V, cf, cb, dx2);
+  row_walks32<K, KIND>(RC32<K>(p), p.C, U, V, cf, cb, dx2);
 }
 
 // both phases (contains two block barriers)
@@ -235,7 +247,7 @@ template <int K, int KIND>
 __device__ __forceinline__ void row_filter(const RowLapParams &p, const float (&U)[kRChunk],
                                            float (&V)[kRChunk], float *cf, float *cb,
                                            const float *e2, const float *dx2) {
-  row_carry32<K>(p, U, cf, cb);
+  row_carry32<K, KIND>(RC32<K>(p), U, cf, cb);
   __syncthreads();
   row_scan_walk32<K, KIND>(p, U, V, cf, cb, e2, dx2);
 }
