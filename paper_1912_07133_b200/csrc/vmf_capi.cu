@@ -371,15 +371,15 @@ static size_t sweep_ws_bytes(int64_t h, int64_t w, int ns) {
 }
 
 static SweepOut sweep_layout(void *sws, int64_t h, int64_t w, int ns) {
+  (void)ns;
   SweepOut o;
   memset(&o, 0, sizeof(o));
   char *p = (char *)(((uintptr_t)sws + 255) & ~(uintptr_t)255);
-  for (int s = 0; s < ns; ++s) {
-    o.V[s] = (float *)p;
-    p += align256((size_t)h * w * sizeof(float));
-    o.E[s] = (float *)p;
-    p += align256((size_t)sweep_extras_floats(w) * sizeof(float));
-  }
+  const size_t vb = align256((size_t)h * w * sizeof(float));
+  const size_t eb = align256((size_t)sweep_extras_floats(w) * sizeof(float));
+  o.V0 = (float *)p;
+  o.E0 = (float *)(p + vb);
+  o.vstride = o.estride = (int64_t)((vb + eb) / sizeof(float));
   o.ldv = w;
   return o;
 }
@@ -392,9 +392,9 @@ static int sweep_cols(const SweepOut &o, int s, int64_t h, int64_t w, const vmf_
   IirParams ip;
   int rc = iir_plan(&ip, w, h, col->b_plus, col->a_plus, col->n, col->b_zero, col->sign);
   if (rc) return rc;
-  const float *E = o.E[s];
+  const float *E = o.E(s);
   const Col32VMode vm = {E + kExVt * w, E + kExVb * w, E + kExKy * w};
-  return colpass32_run(o.V[s], o.ldv, L, ldl, ip, h, w, lap_scale, frac, det_yx, det_val, cap,
+  return colpass32_run(o.V(s), o.ldv, L, ldl, ip, h, w, lap_scale, frac, det_yx, det_val, cap,
                        n_det_dev, thr_dev, cws, cws_b, st, &vm);
 }
 
@@ -435,8 +435,8 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
     // in V mode
     SweepOut o;
     memset(&o, 0, sizeof(o));
-    o.V[0] = T;
-    o.E[0] = vrows;
+    o.V0 = T;
+    o.E0 = vrows;
     o.ldv = w;
     SweepStage sst = sweep_stage(row_stage, col_stage);
     rc = sweep_rows((const float *)x, ldx, h, w, row_stage->n, 1, &sst, o, st);

@@ -656,7 +656,7 @@ struct Col32vSmem {
 };
 
 template <int K, int KIND, bool LSC>
-__global__ void __launch_bounds__(kC32, 4) colapply32v_kernel(
+__global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
     const float *__restrict__ V, int64_t ldv, float *__restrict__ Lout, int64_t ldl,
     Col32Params p, const float *__restrict__ R, const float *__restrict__ Ky,
     CandState *__restrict__ st, int *__restrict__ gy, int *__restrict__ gx,

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
   while (s < bm.ns && y >= 2 * bm.s[s].sv.nseg) y -= 2 * bm.s[s++].sv.nseg;
   if (s >= bm.ns) {  // chunk-vector rows: y = scale
     const BorderScale &b = bm.s[y];
-    float *vlr = out.E[y] + kExVlr * W;
+    float *vlr = out.E(y) + kExVlr * W;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < b.C; c += gridDim.x * blockDim.x) {
       // vl = c_r A32^c; vr = ci A32^(C-1-c): binary powers in fp64
       double Pw[16], R[16], T[16];
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
   }
   float v = u.out(b.sv.v[k]);
   if (which == 0) v *= b.sign;
-  if (col < W) out.E[s][kExS * W + ((int64_t)which * nseg + k) * W + col] = v;
+  if (col < W) out.E(s)[kExS * W + ((int64_t)which * nseg + k) * W + col] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -217,7 +217,7 @@ __device__ __forceinline__ void warp_sum2(float &a, float &b) {
 template <int K, int KIND>
 __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ RowLapMulti rm,
-    SweepOut out) {
+    const SweepOut out) {
   extern __shared__ __align__(1024) unsigned char smem_rl[];
   __shared__ __align__(8) uint64_t bar[kRLBufs];
   __shared__ float red[kMaxScales][16], e2[2], dx2[kMaxScales][2];
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     for (int t = 0; t < kRChunk; ++t) g[t] = (t < kRChunk - 1 ? x[t + 1] : xr) - x[t];
     for (int s = 0; s < ns; ++s) {
       float pl, pr;
-      dx_chunk<K, KIND>(rm.s[s], RC32<K>(rm.s[s]), out.E[s] + kExVlr * W, g, pl, pr);
+      dx_chunk<K, KIND>(rm.s[s], RC32<K>(rm.s[s]), out.E(s) + kExVlr * W, g, pl, pr);
       warp_sum2(pl, pr);
       if (lane == 0) {
         red[s][c >> 5] = pl;
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
   if (edge) {
     const int s = (int)blockIdx.x - nrowctas;
     const RowLapParams &p = rm.s[s];
-    float *E = out.E[s];
+    float *E = out.E(s);
     float *cf = cfs(0), *cb = cbs(0);
     // virtual rows: Vt / Vb = R0(D20 X) of row 0 / H-1 (zero starts) with
     // that row's left / right border terms
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     for (int s = 0; s < ns; ++s) {
       row_walks32<K, KIND>(RC32<K>(rm.s[s]), C, U, V, cfs(s), cbs(s), dx2[s]);
       if (live) {
-        float *dst = out.V[s] + r * out.ldv + c * kRChunk;
+        float *dst = out.V(s) + r * out.ldv + c * kRChunk;
         const uint64_t pol = l2_policy_evict_last();  // V is read twice by the column pass
 #pragma unroll
         for (int q = 0; q < kRChunk / 4; ++q)

@@ -64,10 +64,12 @@ struct BorderMulti {
 constexpr int64_t kExVt = 0, kExVb = 1, kExKy = 2, kExS = 4, kExVlr = 4 + 2 * kMaxSeg;
 inline int64_t sweep_extras_floats(int64_t w) { return (kExVlr + 1) * w; }
 
-struct SweepOut {
-  float *V[kMaxScales];   // V_s (pitch ldv)
-  float *E[kMaxScales];   // extras_s
+struct SweepOut {          // scale s: V_s = V0 + s vstride, extras_s = E0 + s estride
+  float *V0, *E0;
+  int64_t vstride, estride;  // floats
   int64_t ldv;
+  __host__ __device__ float *V(int s) const { return V0 + s * vstride; }
+  __host__ __device__ float *E(int s) const { return E0 + s * estride; }
 };
 
 constexpr int kRChunk = 32;
