@@ -183,21 +183,32 @@ __device__ __forceinline__ void dx_chunk(const RowLapParams &p, const RC32<K> &r
   pl = pr = 0.0f;
   const bool L = c < C && n0 < Mh, Rr = c < C && n0 + kRChunk >= W - Mh;
   if (L || Rr) {
-    // zl = sum_t A^t b g_t (recursion from t = 31 down), zr = sum_t A^(31-t) b g_t
-    Rec32<K, KIND> zl, zr;
+    // zl = sum_t A^t b g_t (recursion from t = 31 down), zr = sum_t A^(31-t) b g_t;
+    // a chunk near one edge only forms that side's sum
+    if (L) {
+      float v[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) zl.u[i] = zr.u[i] = 0.0f;
+      for (int i = 0; i < K; ++i) v[i] = __ldg(vlr + c * 8 + i);  // (issued before the recursion)
+      Rec32<K, KIND> z;
 #pragma unroll
-    for (int t = 0; t < kRChunk; ++t) {
-      zl.step(rc, g[kRChunk - 1 - t]);
-      zr.step(rc, g[t]);
+      for (int i = 0; i < K; ++i) z.u[i] = 0.0f;
+#pragma unroll
+      for (int t = 0; t < kRChunk; ++t) z.step(rc, g[kRChunk - 1 - t]);
+#pragma unroll
+      for (int i = 0; i < K; ++i) pl = fmaf(v[i], z.u[i], pl);
     }
-    if (L)
+    if (Rr) {
+      float v[K];
 #pragma unroll
-      for (int i = 0; i < K; ++i) pl = fmaf(__ldg(vlr + c * 8 + i), zl.u[i], pl);
-    if (Rr)
+      for (int i = 0; i < K; ++i) v[i] = __ldg(vlr + c * 8 + 4 + i);
+      Rec32<K, KIND> z;
 #pragma unroll
-      for (int i = 0; i < K; ++i) pr = fmaf(__ldg(vlr + c * 8 + 4 + i), zr.u[i], pr);
+      for (int i = 0; i < K; ++i) z.u[i] = 0.0f;
+#pragma unroll
+      for (int t = 0; t < kRChunk; ++t) z.step(rc, g[t]);
+#pragma unroll
+      for (int i = 0; i < K; ++i) pr = fmaf(v[i], z.u[i], pr);
+    }
   }
 }
 
@@ -229,6 +240,15 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
   const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_rl);
   char *xbuf = reinterpret_cast<char *>(smem_rl) + ((1024u - (sb & 1023u)) & 1023u);
   float *cfb = reinterpret_cast<float *>(xbuf + kRLBufs * rowb);  // [ns][2][blockDim][K]
+  // every scale's parameters in shared memory: the scale loops index them at
+  // run time (broadcast LDS instead of constant-cache misses)
+  RowLapParams *sp = reinterpret_cast<RowLapParams *>(cfb + (size_t)rm.ns * 2 * blockDim.x * K);
+  {
+    const int nw = (int)(rm.ns * sizeof(RowLapParams) / sizeof(int));
+    const int *src = reinterpret_cast<const int *>(&rm.s[0]);
+    int *dst = reinterpret_cast<int *>(sp);
+    for (int e = threadIdx.x; e < nw; e += blockDim.x) dst[e] = src[e];
+  }
   auto cfs = [&](int s) { return cfb + (size_t)s * 2 * blockDim.x * K; };
   auto cbs = [&](int s) { return cfb + (size_t)(2 * s + 1) * blockDim.x * K; };
   const int64_t H = rm.H;
@@ -281,7 +301,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     for (int t = 0; t < kRChunk; ++t) g[t] = (t < kRChunk - 1 ? x[t + 1] : xr) - x[t];
     for (int s = 0; s < ns; ++s) {
       float pl, pr;
-      dx_chunk<K, KIND>(rm.s[s], RC32<K>(rm.s[s]), out.E(s) + kExVlr * W, g, pl, pr);
+      dx_chunk<K, KIND>(sp[s], RC32<K>(sp[s]), out.E(s) + kExVlr * W, g, pl, pr);
       warp_sum2(pl, pr);
       if (lane == 0) {
         red[s][c >> 5] = pl;
@@ -296,14 +316,14 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
         a += red[s][w];
         b += red[s][8 + w];
       }
-      dx2[s][0] = rm.s[s].sign * a;
+      dx2[s][0] = sp[s].sign * a;
       dx2[s][1] = b;
     }
   };
 
   if (edge) {
     const int s = (int)blockIdx.x - nrowctas;
-    const RowLapParams &p = rm.s[s];
+    const RowLapParams &p = sp[s];
     float *E = out.E(s);
     float *cf = cfs(0), *cb = cbs(0);
     // virtual rows: Vt / Vb = R0(D20 X) of row 0 / H-1 (zero starts) with
@@ -415,7 +435,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
       const float xc = X[c == 0 ? 0 : kRChunk - 1];
       e2[c == 0 ? 0 : 1] = (ru.ld(n) - xc) + (rd.ld(n) - xc);
     }
-    for (int s = 0; s < ns; ++s) row_carry32<K, KIND>(RC32<K>(rm.s[s]), U, cfs(s), cbs(s));
+    for (int s = 0; s < ns; ++s) row_carry32<K, KIND>(RC32<K>(sp[s]), U, cfs(s), cbs(s));
     __syncthreads();  // rows r-1 .. r+1 read; carries, e2, red published
     if (c == 0) {
       if (i + 3 <= nrows + 1) issue_row(su, clampr(rlo + 2 + i));  // row r+2 -> slot of r-1
@@ -423,11 +443,11 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     }
     // the 2 ns chunk scans over the warps
     for (int task = c >> 5; task < 2 * ns; task += nwarp)
-      chunk_scan32<K>(rm.s[task >> 1], (task & 1) ? cbs(task >> 1) : cfs(task >> 1), task & 1,
+      chunk_scan32<K>(sp[task >> 1], (task & 1) ? cbs(task >> 1) : cfs(task >> 1), task & 1,
                       e2[task & 1], lane);
     __syncthreads();
     for (int s = 0; s < ns; ++s) {
-      row_walks32<K, KIND>(RC32<K>(rm.s[s]), C, U, V, cfs(s), cbs(s), dx2[s]);
+      row_walks32<K, KIND>(RC32<K>(sp[s]), C, U, V, cfs(s), cbs(s), dx2[s]);
       if (live) {
         float *dst = out.V(s) + r * out.ldv + c * kRChunk;
         const uint64_t pol = l2_policy_evict_last();  // V is read twice by the column pass
@@ -582,7 +602,7 @@ static int rl_block(int C) { return (C + 31) / 32 * 32; }
 
 static size_t rl_smem(int C, int k, int ns) {
   return 1024 + (size_t)kRLBufs * ((C * 128 + 1023) & ~1023) +
-         (size_t)ns * 2 * rl_block(C) * k * sizeof(float);
+         (size_t)ns * 2 * rl_block(C) * k * sizeof(float) + (size_t)ns * sizeof(RowLapParams) + 16;
 }
 
 // segment vectors c A^(m0-1) of a column stage (m0 = 1 + 64 k)
