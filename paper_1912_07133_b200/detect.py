@@ -146,34 +146,48 @@ def _sweep_ok(x, code, stages) -> bool:
                                                arr))
 
 
+# scales per row pass of a sweep: the column passes of one group overlap the
+# next group's row pass (VMF_SWEEP_GROUP overrides it for experiments)
+SWEEP_GROUP = int(os.environ.get("VMF_SWEEP_GROUP", "5"))
+
+
 def _sweep_launch_multi(x, code, stages, frac, lap_scales, cap, outs, laps, conc):
-    """One row pass for every scale (vmf_sweep_rows: the Laplacian of the
-    frame and its staging shared by all scales), then each scale's column
-    pass on `conc` side streams (vmf_sweep_detect)."""
+    """Row passes for groups of scales (vmf_sweep_rows: the Laplacian of the
+    frame and its staging shared by a group's scales), each followed by its
+    scales' column passes on `conc` side streams (vmf_sweep_detect) that
+    overlap the next group's row pass."""
     L = _lib.lib()
     h, w = x.shape
     ns = len(stages)
-    arr = (_lib.VmfStage * ns)(*[st.s for st in stages])
-    sws = _workspace(L.vmf_sweep_workspace_bytes(h, w, ns), _SWEEP_SLOT)
-    _lib.check(L.vmf_sweep_rows(_ptr(x), code, h, w, _pitch(x), ns, arr, arr, _ptr(sws),
-                                sws.numel(), _stream()))
+    grp = max(1, min(SWEEP_GROUP, 5))
     cur = torch.cuda.current_stream()
     side = _side(conc) if conc > 1 else [cur]
-    if conc > 1:
-        for s in side:
-            s.wait_stream(cur)
-    for i in range(ns):
-        sc = 1.0 if lap_scales is None else float(lap_scales[i])
-        det_yx, det_val, scal = outs[i]
-        with torch.cuda.stream(side[i % len(side)]):
-            ws = _workspace(L.vmf_sweep_detect_workspace_bytes(h, w, C.byref(stages[i].s)),
-                            1 + i % len(side))
-            lap = None if laps is None else laps[i]
-            _lib.check(L.vmf_sweep_detect(
-                i, h, w, ns, C.byref(stages[i].s), sc, float(frac),
-                _ptr(lap) if lap is not None else None, _ptr(det_yx), _ptr(det_val), int(cap),
-                _ptr(scal), scal.data_ptr() + 8, _ptr(sws), sws.numel(), _ptr(ws), ws.numel(),
-                _stream()))
+    k = 0
+    for g0 in range(0, ns, grp):
+        sub = stages[g0:g0 + grp]
+        ng = len(sub)
+        arr = (_lib.VmfStage * ng)(*[st.s for st in sub])
+        sws = _workspace(L.vmf_sweep_workspace_bytes(h, w, ng), _SWEEP_SLOT + g0)
+        _lib.check(L.vmf_sweep_rows(_ptr(x), code, h, w, _pitch(x), ng, arr, arr, _ptr(sws),
+                                    sws.numel(), _stream()))
+        if conc > 1:
+            for s in side:
+                s.wait_stream(cur)
+        for j in range(ng):
+            i = g0 + j
+            sc = 1.0 if lap_scales is None else float(lap_scales[i])
+            det_yx, det_val, scal = outs[i]
+            st_ = side[k % len(side)]
+            k += 1
+            with torch.cuda.stream(st_):
+                ws = _workspace(L.vmf_sweep_detect_workspace_bytes(h, w, C.byref(stages[i].s)),
+                                1 + (k - 1) % len(side))
+                lap = None if laps is None else laps[i]
+                _lib.check(L.vmf_sweep_detect(
+                    j, h, w, ng, C.byref(stages[i].s), sc, float(frac),
+                    _ptr(lap) if lap is not None else None, _ptr(det_yx), _ptr(det_val), int(cap),
+                    _ptr(scal), scal.data_ptr() + 8, _ptr(sws), sws.numel(), _ptr(ws), ws.numel(),
+                    _stream()))
     if conc > 1:
         for s in side:
             cur.wait_stream(s)
