@@ -141,10 +141,21 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
   // before the recursion (independent loads)
   float xs[kSeg + 1];
   const float *Xc = X + cc;
+  // rows r(t) = r0 + dir t, t = 0..n; the common segment (whole, inside the
+  // frame) walks one pointer by a 32-bit stride, the rest clamps per row
+  const int64_t r0 = which == 0 ? m0 - 1 : H - m0;
+  const int64_t rend = which == 0 ? r0 + n : r0 - n;
+  if (n == kSeg && r0 >= 0 && r0 < H && rend >= 0 && rend < H && (int64_t)kSeg * ldx < (1 << 29)) {
+    const float *p = Xc + r0 * ldx;
+    const int step = which == 0 ? (int)ldx : -(int)ldx;
 #pragma unroll
-  for (int t = 0; t <= kSeg; ++t) {
-    const int64_t r = which == 0 ? m0 - 1 + t : H - m0 - t;
-    xs[t] = t <= n ? __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx) : 0.0f;
+    for (int t = 0; t <= kSeg; ++t) xs[t] = __ldg(p + t * step);
+  } else {
+#pragma unroll
+    for (int t = 0; t <= kSeg; ++t) {
+      const int64_t r = which == 0 ? m0 - 1 + t : H - m0 - t;
+      xs[t] = t <= n ? __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx) : 0.0f;
+    }
   }
   Rec32<K, KIND> u;
 #pragma unroll
