@@ -42,12 +42,18 @@ METRIC = "Mpixel/s per scale (IIR vs FIR) and achieved HBM GB/s vs B200 peak, 1 
 UNIT = "Mpixel/s"
 FLUSH_BYTES = 256 << 20
 # algorithmic bytes per pixel per launch: fp32 read + write
+# (the sweep's row pass reads X once and writes V of every scale: 4 + 4 ns;
+# its column apply reads V and writes L in place: 8; the column carry reads V)
 ALGO_BYTES_PER_PX = {
     "iir_apply": 8, "iir_carry": 4, "iir_rows_fused": 8, "iir_cols_fused": 8,
     "fir_rows": 8, "fir_cols": 8, "laplacian": 8, "nms_count": 4, "nms_write": 4,
-    "absmax": 4,
+    "absmax": 4, "sweep_rows": 4 + 4 * 5, "col_apply": 8, "col_carry": 4,
 }
-PATH_BYTES_PER_PX = 16  # fused path: read x, write T, read T, write L
+PATH_BYTES_PER_PX = 16  # per scale: read x, write V, read V, write L
+# fp32 FMAs per pixel per scale of the modal K = 3 recursions (SURVEY §8(d)
+# restated for the Laplacian-first path): per pass, chunk / band carries
+# 2 directions x K, walks 2 directions x 2K (state + output), combine 2
+FMA_PER_PX_PASS = {3: 6 * 3 + 2}
 
 
 def parse():
@@ -190,21 +196,30 @@ def max_over_ranks(v, ws, device):
 # CPU side: the oracle port (test infrastructure) as baseline / reference arm
 # ---------------------------------------------------------------------------
 DFMA_PEAK_T = 16.44  # T fp64 FMA/s: profiles/r1_pipes.txt (tools/microbench/pipes.cu on this pool)
+N_SM = 148
 
 
-def compute_roofline(per_scale):
-    """Per scale, the algorithmic fp64 FMA rate against the measured DFMA
-    peak (SURVEY.md §8(d): IIR 4K+1 = 13 FMA per pixel per pass for K = 3;
-    FIR one FMA per tap per pass; both passes)."""
-    out = {"peak_tfma_s": DFMA_PEAK_T, "peak_source": "profiles/r1_pipes.txt", "iir": {},
-           "fir": {}}
+def compute_roofline(per_scale, sweep_value, sm_mhz):
+    """The arithmetic rooflines.  IIR (fp32 modal path): algorithmic fp32
+    FMAs (FMA_PER_PX_PASS, both passes) against 148 SMs x 128 FMA/clk at the
+    sampled SM clock, per single scale and for the 5-scale sweep.  FIR (fp64
+    accumulation): one DFMA per tap per pass against the measured DFMA peak."""
+    f32 = N_SM * 128 * (sm_mhz or 1965.0) * 1e6 / 1e12
+    fma = 2 * FMA_PER_PX_PASS[3]
+    out = {"iir_fp32": {"peak_tfma_s": round(f32, 2), "fma_per_px_scale": fma,
+                        "sweep": {"tfma_s": round(sweep_value * 1e6 * fma / 1e12, 2),
+                                  "frac": round(sweep_value * 1e6 * fma / 1e12 / f32, 3)},
+                        "per_scale": {}},
+           "fir_fp64": {"peak_tfma_s": DFMA_PEAK_T, "peak_source": "profiles/r1_pipes.txt",
+                        "per_scale": {}}}
     for sg, v in per_scale["iir"].items():
-        a = v * 1e6 * 2 * 13 / 1e12
-        out["iir"][sg] = {"tfma_s": round(a, 2), "frac": round(a / DFMA_PEAK_T, 3)}
+        a = v * 1e6 * fma / 1e12
+        out["iir_fp32"]["per_scale"][sg] = {"tfma_s": round(a, 2), "frac": round(a / f32, 3)}
     for sg, v in per_scale["fir"].items():
         taps = 2 * int(4 * float(sg)) + 1  # gaussian_fir(sigma, 0, 4 sigma)
         a = v * 1e6 * 2 * taps / 1e12
-        out["fir"][sg] = {"taps": taps, "tfma_s": round(a, 2), "frac": round(a / DFMA_PEAK_T, 3)}
+        out["fir_fp64"]["per_scale"][sg] = {"taps": taps, "tfma_s": round(a, 2),
+                                            "frac": round(a / DFMA_PEAK_T, 3)}
     return out
 
 
@@ -279,7 +294,7 @@ def workload_config(h, w, n_gpus):
             "frame": [h, w], "scales": len(IIR), "parallelism": f"replicas x{n_gpus}"}
 
 
-DTYPE = "fp32 I/O, f64 recursion state"
+DTYPE = "f32"  # the IIR sweep: fp32 I/O, fp32 modal recursion state
 
 
 def run_reference(args):
@@ -455,7 +470,7 @@ def run_ours(args):
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dom_name, (dom_ms, dom_n) = dom
     per_launch_ms = dom_ms / dom_n
-    algo = ALGO_BYTES_PER_PX.get(dom_name, 8) * h * w
+    algo = ALGO_BYTES_PER_PX.get(dom_name, 8) * h * w  # (sweep_rows: 5 scales per launch)
     achieved = algo / (per_launch_ms / 1e3) / 1e9
     traffic = None
     try:
@@ -545,7 +560,7 @@ def run_ours(args):
                          "algo_bytes_per_launch": algo, "avg_launch_ms": round(per_launch_ms, 5)},
             "path_roofline": {"bytes_per_px": PATH_BYTES_PER_PX, "achieved": round(path_gbs, 1),
                               "peak": hbm, "frac": round(path_gbs / hbm, 4), "unit": "GB/s"},
-            "compute_roofline": compute_roofline(per_scale),
+            "compute_roofline": compute_roofline(per_scale, value / ws, clk.get("sm_mhz")),
             "kernels": {k: {"avg_ms": round(v[0] / v[1], 5), "launches": v[1]}
                         for k, v in prof.items()},
             "e2e": {"value": round(e2e, 1), "unit": UNIT,

@@ -1058,7 +1058,7 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
                T, ldt, p, R, Cc, vm.vt, vm.vb);
   }
   if (VM) {
-    Launch g(K_IIR_COLS_FUSED, st);
+    Launch g(K_COL_APPLY, st);
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
     const int use_tma = make_tmap_2d_f32(&tmap, T, h, w, ldt, kT32Stride, kB32 + 2) &&

@@ -11,7 +11,8 @@ namespace vmf {
 const char *const kKernelNames[K_NUM_IDS] = {
     "iir_carry", "iir_scan", "iir_apply", "iir_scale", "fir_rows", "fir_cols",
     "laplacian", "absmax", "nms_count", "nms_scan", "nms_write", "iir_rows_fused",
-    "iir_cols_fused", "finalize", "col_carry", "col_scan", "row_border"};
+    "iir_cols_fused", "finalize", "col_carry", "col_scan", "sweep_border", "sweep_rows",
+    "col_apply"};
 
 namespace {
 std::atomic<long long> g_launches{0};

@@ -25,6 +25,8 @@ enum KernelId {
   K_COL_CARRY,
   K_COL_SCAN,
   K_ROW_BORDER,
+  K_SWEEP_ROWS,
+  K_COL_APPLY,
   K_NUM_IDS
 };
 

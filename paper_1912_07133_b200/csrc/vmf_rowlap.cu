@@ -152,25 +152,22 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
     for (int t = 0; t <= kSeg; ++t) xs[t] = __ldg(p + t * step);
   } else {
 #pragma unroll
-    for (int t = 0; t <= kSeg; ++t) {
-      const int64_t r = which == 0 ? m0 - 1 + t : H - m0 - t;
-      xs[t] = t <= n ? __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx) : 0.0f;
+    for (int t = 0; t <= kSeg; ++t) {  // t > n repeats row n: G = 0 there
+      const int tt = t < n ? t : n;
+      const int64_t r = which == 0 ? m0 - 1 + tt : H - m0 - tt;
+      xs[t] = __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx);
     }
   }
   Rec32<K, KIND> u;
 #pragma unroll
   for (int i = 0; i < K; ++i) u.u[i] = 0.0f;
+  // G(m0 + t): top X(m0+t) - X(m0+t-1) = xs[t+1] - xs[t]; bottom
+  // X(H-m0-t) - X(H-m0-t-1) = -(xs[t+1] - xs[t]): the sign goes on the share.
+  // Steps t >= n see G = 0 on a zero state (rows repeated above).
 #pragma unroll
-  for (int t = kSeg - 1; t >= 0; --t) {
-    if (t < n) {
-      // G(m0 + t): top X(m0+t) - X(m0+t-1) = xs[t+1] - xs[t];
-      //            bottom X(H-m0-t) - X(H-m0-t-1) = xs[t] - xs[t+1]
-      const float g = which == 0 ? xs[t + 1] - xs[t] : xs[t] - xs[t + 1];
-      u.step(b, g);
-    }
-  }
+  for (int t = kSeg - 1; t >= 0; --t) u.step(b, xs[t + 1] - xs[t]);
   float v = u.out(b.sv.v[k]);
-  if (which == 0) v *= b.sign;
+  v *= which == 0 ? b.sign : -1.0f;
   if (col < W) out.E(s)[kExS * W + ((int64_t)which * nseg + k) * W + col] = v;
 }
 
@@ -738,7 +735,7 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
   const int rslots = slots > rm.ns ? slots - rm.ns : 1;
   rm.rows_per = (int)cdiv(rm.H, rslots);
   const int grid = (int)cdiv(rm.H, rm.rows_per) + rm.ns;
-  Launch g(K_IIR_ROWS_FUSED, st);
+  Launch g(K_SWEEP_ROWS, st);
   launch_pdl(sweep_rows_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm,
              (const RowLapMulti)rm, out);
   return cuda_status("fp32 row pass");
