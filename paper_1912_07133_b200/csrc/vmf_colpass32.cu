@@ -334,7 +334,6 @@ struct Col32Smem {
   float cv[kCand32];
   int ccount;
   unsigned int cmax;
-  float thr_end;
 };
 
 // LSC: multiply by lap_scale (sigma^2 normalisation of the scale-space stack)
@@ -542,16 +541,11 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
         }
     }
   }
-  __syncthreads();
-  // ---- flush candidates that survive the best threshold known now ---------
-  if (j == 0) {
-    const unsigned old = atomicMax(&st->absmax_bits, S.cmax);
-    S.thr_end = p.frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
-  }
+  // ---- flush the shared candidates (they passed th; the finaliser applies
+  // the final threshold) ----------------------------------------------------
   __syncthreads();
   const int n = S.ccount < kCand32 ? S.ccount : kCand32;
   for (int q = j; q < n; q += kC32) {
-    if (!(fabsf(S.cv[q]) >= S.thr_end)) continue;
     const int k = atomicAdd(&st->count, 1);
     if (k < gcap) {
       gy[k] = S.cy[q];
@@ -652,7 +646,6 @@ struct Col32vSmem {
   float cv[kCand32];
   int ccount;
   unsigned int cmax;
-  float thr_end;
 };
 
 template <int K, int KIND, bool LSC>
@@ -859,15 +852,11 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
         }
     }
   }
-  __syncthreads();
-  if (j == 0) {
-    const unsigned old = atomicMax(&st->absmax_bits, S.cmax);
-    S.thr_end = p.frac * fmaxf(__uint_as_float(old), __uint_as_float(S.cmax));
-  }
+  // (the shared candidates already passed th; the finaliser applies the final
+  // threshold, so no second, fresher read of the global maximum is needed)
   __syncthreads();
   const int n = S.ccount < kCand32 ? S.ccount : kCand32;
   for (int q = j; q < n; q += kC32) {
-    if (!(fabsf(S.cv[q]) >= S.thr_end)) continue;
     const int k = atomicAdd(&st->count, 1);
     if (k < gcap) {
       gy[k] = S.cy[q];

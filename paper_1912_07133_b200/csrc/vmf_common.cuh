@@ -129,6 +129,13 @@ __device__ __forceinline__ void st_v4_hint(float *addr, float4 v, uint64_t polic
                "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(policy)
                : "memory");
 }
+// 256-bit store (sm_100: STG.256, one full 32-byte sector per lane)
+__device__ __forceinline__ void st_v8_hint(float *addr, const float *v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;\n" ::"l"(addr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]),
+               "f"(v[7]), "l"(policy)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async16_hint(void *smem_dst, const void *src, uint64_t policy) {
   unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),

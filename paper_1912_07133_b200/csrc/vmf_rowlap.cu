@@ -41,6 +41,35 @@
 
 namespace vmf {
 
+#ifndef VMF_ABL
+#define VMF_ABL 0
+#endif
+#ifndef VMF_TIMELINE
+#define VMF_TIMELINE 0
+#endif
+#if VMF_TIMELINE  // per-CTA / per-row globaltimer stamps (tools/row_ablation.py)
+__device__ unsigned long long g_tl[4096];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL(idx) \
+  do {          \
+    if (threadIdx.x == 0) g_tl[(idx)] = gtime(); \
+  } while (0)
+#define TLROW(i, ph) \
+  do {               \
+    if (blockIdx.x < 8 && (i) < 16) TL(2560 + (blockIdx.x * 16 + (i)) * 4 + (ph)); \
+  } while (0)
+#else
+#define TL(idx) \
+  do {          \
+  } while (0)
+#define TLROW(i, ph) \
+  do {               \
+  } while (0)
+#endif
 constexpr int kRLMaxC = 256;   // W <= 8192
 constexpr int kRLBufs = 3;     // input ring: rows r-1, r, r+1 (r+2 lands in r-1's slot)
 
@@ -234,7 +263,7 @@ __device__ __forceinline__ void warp_sum2(float &a, float &b) {
 // is formed once and every scale's carries go before one barrier, the 2 ns
 // chunk scans share the warps, and each scale's walks write its V row.
 template <int K, int KIND>
-__global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
+__global__ void __maxnreg__(168) sweep_rows_kernel(  // (3 CTAs of 128 threads per SM)
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ RowLapMulti rm,
     const SweepOut out) {
   extern __shared__ __align__(1024) unsigned char smem_rl[];
@@ -283,7 +312,9 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
   __syncthreads();
   // the border kernel (this grid's predecessor) wrote the chunk vectors and
   // segment shares; the previous scale's column pass may still read V
+  TL(2048 + (blockIdx.x & 511));
   pdl_wait();
+  TL(blockIdx.x & 1023);
   float U[kRChunk], V[kRChunk], X[kRChunk];
   auto load_chunk = [&](int sl, float (&o)[kRChunk]) {
     const SwzRow32 r{xbuf + sl * rowb};
@@ -384,10 +415,25 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     float *rowp = reinterpret_cast<float *>(xbuf);  // (the input slots are idle now)
     const int nsg = p.nseg;
     for (int which = 0; which < 2; ++which) {
-      for (int n = c; n < W; n += blockDim.x) {
-        float a = 0.0f;
-        for (int k = 0; k < nsg; ++k) a += __ldg(E + kExS * W + ((int64_t)which * nsg + k) * W + n);
-        rowp[n + (n >> 5)] = a;
+      // W <= 32 blockDim columns per thread, in groups of 8, each summed in k
+      // order; a segment's 8 loads are in flight together
+      for (int j0 = 0; j0 < kRChunk; j0 += 8) {
+        float a[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = 0.0f;
+        for (int k = 0; k < nsg; ++k) {
+          const float *S = E + kExS * W + ((int64_t)which * nsg + k) * W + c;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int n = c + (j0 + j) * (int)blockDim.x;
+            if (n < W) a[j] += __ldg(S + (j0 + j) * blockDim.x);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n = c + (j0 + j) * (int)blockDim.x;
+          if (n < W) rowp[n + (n >> 5)] = a[j];
+        }
       }
       if (c == 0) dx2[0][0] = dx2[0][1] = 0.0f;
       __syncthreads();
@@ -407,6 +453,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
       for (int n = c; n < W; n += blockDim.x) E[kExKy * W + (int64_t)which * W + n] = rowp[n + (n >> 5)];
       __syncthreads();
     }
+    TL(1024 + (blockIdx.x & 1023));
     pdl_trigger();
     return;
   }
@@ -421,6 +468,7 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
       mbar_wait(&bar[1], 0);
     }
     mbar_wait(&bar[sd], (unsigned)(((i + 2) / kRLBufs) & 1));
+    TLROW(i, 0);
     float xl, xr;
     load_chunk(sc, X);
     halos(sc, X, xl, xr);
@@ -440,32 +488,56 @@ __global__ void __launch_bounds__(kRLMaxC) sweep_rows_kernel(
     if (c == 0 || c == C - 1) {  // D02 X of the end samples: the steady starts (every scale)
       const SwzRow32 ru{xbuf + su * rowb}, rd{xbuf + sd * rowb};
       const int n = c == 0 ? 0 : W - 1;
-      const float xc = X[c == 0 ? 0 : kRChunk - 1];
+      const float xc = c == 0 ? X[0] : X[kRChunk - 1];
       e2[c == 0 ? 0 : 1] = (ru.ld(n) - xc) + (rd.ld(n) - xc);
     }
+#if VMF_ABL != 3 && VMF_ABL != 6 && VMF_ABL != 7  // (VMF_ABL: timing ablations, tools/row_ablation.sh; results invalid)
     for (int s = 0; s < ns; ++s) row_carry32<K, KIND>(RC32<K>(sp[s]), U, cfs(s), cbs(s));
+#endif
     __syncthreads();  // rows r-1 .. r+1 read; carries, e2, red published
+    TLROW(i, 1);
     if (c == 0) {
       if (i + 3 <= nrows + 1) issue_row(su, clampr(rlo + 2 + i));  // row r+2 -> slot of r-1
       reduce_dx();
     }
     // the 2 ns chunk scans over the warps
+#if VMF_ABL != 1 && VMF_ABL != 6 && VMF_ABL != 7
     for (int task = c >> 5; task < 2 * ns; task += nwarp)
       chunk_scan32<K>(sp[task >> 1], (task & 1) ? cbs(task >> 1) : cfs(task >> 1), task & 1,
                       e2[task & 1], lane);
+#endif
     __syncthreads();
+    TLROW(i, 2);
     for (int s = 0; s < ns; ++s) {
+#if VMF_ABL != 2 && VMF_ABL != 6 && VMF_ABL != 7
       row_walks32<K, KIND>(RC32<K>(sp[s]), C, U, V, cfs(s), cbs(s), dx2[s]);
+#else
+      for (int t = 0; t < kRChunk; ++t) V[t] = U[t] * (float)s;
+#endif
+#if VMF_ABL == 4 || VMF_ABL == 7
+      if (live && V[0] == 12345.678f && V[31] == -1.5f) {
+#else
       if (live) {
+#endif
         float *dst = out.V(s) + r * out.ldv + c * kRChunk;
-        const uint64_t pol = l2_policy_evict_last();  // V is read twice by the column pass
+#if VMF_ABL == 5
 #pragma unroll
         for (int q = 0; q < kRChunk / 4; ++q)
-          st_v4_hint(dst + 4 * q, make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]),
-                     pol);
+          *reinterpret_cast<float4 *>(dst + 4 * q) =
+              make_float4(V[4 * q], V[4 * q + 1], V[4 * q + 2], V[4 * q + 3]);
+#else
+        // V is read twice by the column pass; 256-bit stores: each lane fills
+        // whole 32-byte sectors (the 128-byte lane stride of a chunk row
+        // leaves 16-byte stores at half a sector each)
+        const uint64_t pol = l2_policy_evict_last();
+#pragma unroll
+        for (int q = 0; q < kRChunk / 8; ++q) st_v8_hint(dst + 8 * q, V + 8 * q, pol);
+#endif
       }
     }
+    TLROW(i, 3);
   }
+  TL(1024 + (blockIdx.x & 1023));
   pdl_trigger();
 }
 
@@ -741,6 +813,17 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
   return cuda_status("fp32 row pass");
 }
 
+#if VMF_TIMELINE
+}  // namespace vmf
+extern "C" int vmf_debug_timeline(unsigned long long *host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, vmf::g_tl, sizeof(unsigned long long) * (n < 4096 ? n : 4096));
+}
+extern "C" int vmf_debug_timeline_reset(void) {
+  static unsigned long long z[4096];
+  return (int)cudaMemcpyToSymbol(vmf::g_tl, z, sizeof(z));
+}
+namespace vmf {
+#endif
 int sweep_rows(const float *x, int64_t ldx, int64_t h, int64_t w, int k, int ns,
                const SweepStage *st, const SweepOut &out, cudaStream_t stream) {
   static SweepPlan P;  // (large: not on the stack)
