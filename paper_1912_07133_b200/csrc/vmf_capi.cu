@@ -10,6 +10,7 @@
 #include "vmf_rowlap.cuh"
 #include "vmf_modal32.cuh"
 #include "vmf_firpass.cuh"
+#include "vmf_firtc.cuh"
 
 namespace vmf {
 size_t greedy_nms_workspace_bytes(int64_t n, int64_t h, int64_t w, double r2);
@@ -322,6 +323,11 @@ size_t vmf_blur_lap_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage
     size_t c4 = firpass_workspace_bytes(h, w);
     if (c4 > carry) carry = c4;
   }
+  if (row_stage && col_stage && row_stage->kind == VMF_STAGE_FIR &&
+      col_stage->kind == VMF_STAGE_FIR) {
+    size_t c5 = firtc_workspace_bytes(h, w, row_stage->n, col_stage->n);
+    if (c5 > carry) carry = c5;
+  }
   return 3 * img + align256(carry) + align256(detect_workspace_bytes(1, h, w)) + 256 +
          align256((size_t)sweep_extras_floats(w) * sizeof(float));  // fp32 row pass extras
 }
@@ -449,6 +455,32 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
       rc = run_stage<ROWS>(row_stage, x, x_dtype, Tb, h, w, ldx, w, carry, carry_b, st);
       if (rc) return rc;
       rc = run_stage<COLS>(col_stage, Tb, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);
+      if (rc) return rc;
+    }
+    if (n_det_host && frac > 0.0f) {
+      cudaMemcpyAsync(n_det_host, n_det_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      return cuda_status("detect readback");
+    }
+    return VMF_OK;
+  }
+  // the tensor-core FIR path beats the fp64 CUDA-core one from ~65 taps
+  // (profiles/README.md); VMF_FORCE_FIRTC takes it for any length (tests)
+  static const bool force_tc = getenv("VMF_FORCE_FIRTC") != nullptr;
+  if (x_dtype == VMF_F32 && row_stage->kind == VMF_STAGE_FIR && col_stage->kind == VMF_STAGE_FIR &&
+      !getenv("VMF_FORCE_GENERIC") && firtc_supported(h, w, ldx, row_stage->n, col_stage->n) &&
+      ((uintptr_t)x & 15) == 0 &&
+      (force_tc || (row_stage->n > col_stage->n ? row_stage->n : col_stage->n) >= kFirTcMinTaps)) {
+    // both FIR passes on the tensor cores, Laplacian first, then stage 4
+    // (vmf_firtc.cu)
+    rc = firtc_detect((const float *)x, ldx, h, w, row_stage->taps, row_stage->n, col_stage->taps,
+                      col_stage->n, lap_scale, frac, L, w, det_yx, det_val, cap, n_det_dev, thr_dev,
+                      carry, carry_b, st);
+    if (rc) return rc;
+    if (blur_out) {  // B on request: the two FIR leaves (T in T's slot)
+      rc = run_stage<ROWS>(row_stage, x, x_dtype, T, h, w, ldx, w, carry, carry_b, st);
+      if (rc) return rc;
+      rc = run_stage<COLS>(col_stage, T, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);
       if (rc) return rc;
     }
     if (n_det_host && frac > 0.0f) {

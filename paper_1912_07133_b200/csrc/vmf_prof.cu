@@ -12,7 +12,7 @@ const char *const kKernelNames[K_NUM_IDS] = {
     "iir_carry", "iir_scan", "iir_apply", "iir_scale", "fir_rows", "fir_cols",
     "laplacian", "absmax", "nms_count", "nms_scan", "nms_write", "iir_rows_fused",
     "iir_cols_fused", "finalize", "col_carry", "col_scan", "sweep_border", "sweep_rows",
-    "col_apply"};
+    "col_apply", "firtc_prep", "firtc_rows", "firtc_cols"};
 
 namespace {
 std::atomic<long long> g_launches{0};

@@ -27,6 +27,9 @@ enum KernelId {
   K_ROW_BORDER,
   K_SWEEP_ROWS,
   K_COL_APPLY,
+  K_FIRTC_PREP,
+  K_FIRTC_ROWS,
+  K_FIRTC_COLS,
   K_NUM_IDS
 };
 

@@ -52,4 +52,19 @@ bool make_tmap_rows_swz_f32(CUtensorMap *map, const float *base, int64_t rows, i
   return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_2d_f32_sw128(CUtensorMap *map, const float *base, int64_t rows, int64_t cols,
+                            int64_t ld, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  if (((uintptr_t)base & 15) || ((ld * 4) & 15) || box_rows > 256) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace vmf

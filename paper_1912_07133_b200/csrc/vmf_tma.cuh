@@ -19,6 +19,12 @@ bool make_tmap_2d_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t
 bool make_tmap_rows_swz_f32(CUtensorMap *map, const float *base, int64_t rows, int64_t w,
                             int64_t ld, int nrows);
 
+// 2-D fp32 [rows][cols] map with 128-byte swizzle and box {32 cols, box_rows}:
+// the K-major SWIZZLE_128B operand layout of tcgen05.mma (8-row x 128-byte
+// atoms, 1024 bytes apart).  OOB elements read as zero.
+bool make_tmap_2d_f32_sw128(CUtensorMap *map, const float *base, int64_t rows, int64_t cols,
+                            int64_t ld, int box_rows);
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
@@ -76,6 +82,11 @@ __device__ __forceinline__ void tma_store_3d_hint(const CUtensorMap *map, const 
       " [%0, {%1, %2, %3}], [%4], %5;\n" ::"l"(reinterpret_cast<uint64_t>(map)),
       "r"(c0), "r"(c1), "r"(c2), "r"(s), "l"(policy)
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
