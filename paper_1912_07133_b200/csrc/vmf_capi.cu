@@ -466,7 +466,7 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   }
   // the tensor-core FIR path beats the fp64 CUDA-core one from ~65 taps
   // (profiles/README.md); VMF_FORCE_FIRTC takes it for any length (tests)
-  static const bool force_tc = getenv("VMF_FORCE_FIRTC") != nullptr;
+  const bool force_tc = getenv("VMF_FORCE_FIRTC") != nullptr;
   if (x_dtype == VMF_F32 && row_stage->kind == VMF_STAGE_FIR && col_stage->kind == VMF_STAGE_FIR &&
       !getenv("VMF_FORCE_GENERIC") && firtc_supported(h, w, ldx, row_stage->n, col_stage->n) &&
       ((uintptr_t)x & 15) == 0 &&

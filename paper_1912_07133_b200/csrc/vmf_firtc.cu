@@ -650,7 +650,10 @@ __global__ void __launch_bounds__(256) firtc_nms_kernel(const float *__restrict_
         gt &= v > w;
         lt &= v < w;
       }
-    if (gt || lt) cand_push(&ccount, cy, cx, cv, kNmsCand, st, gy, gx, gv, gcap, r, cc, v);
+    // a maximum counts when positive, a minimum when negative (|v| >= thr alone
+    // would admit a positive local minimum)
+    if ((gt && v >= thr) || (lt && -v >= thr))
+      cand_push(&ccount, cy, cx, cv, kNmsCand, st, gy, gx, gv, gcap, r, cc, v);
   }
   __syncthreads();
   const int n = ccount < kNmsCand ? ccount : kNmsCand;
