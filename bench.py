@@ -199,27 +199,47 @@ DFMA_PEAK_T = 16.44  # T fp64 FMA/s: profiles/r1_pipes.txt (tools/microbench/pip
 N_SM = 148
 
 
+FIRTC_MIN_TAPS = 65  # vmf_firtc.cuh kFirTcMinTaps: from here the FIR runs on the tensor cores
+
+
 def compute_roofline(per_scale, sweep_value, sm_mhz):
     """The arithmetic rooflines.  IIR (fp32 modal path): algorithmic fp32
     FMAs (FMA_PER_PX_PASS, both passes) against 148 SMs x 128 FMA/clk at the
-    sampled SM clock, per single scale and for the 5-scale sweep.  FIR (fp64
-    accumulation): one DFMA per tap per pass against the measured DFMA peak."""
+    sampled SM clock, per single scale and for the 5-scale sweep.  FIR: below
+    FIRTC_MIN_TAPS one DFMA per tap per pass against the measured DFMA peak;
+    from there the tensor-core path, whose MMA work per pixel and pass is
+    3 (3xTF32) x 2 x KW (the 128 + 2k window rounded up to 32) FLOP, against
+    the TF32 dense peak taken as half the measured bf16 peak."""
     f32 = N_SM * 128 * (sm_mhz or 1965.0) * 1e6 / 1e12
     fma = 2 * FMA_PER_PX_PASS[3]
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            tf32 = float(json.load(fh)["bf16_tflops"]) / 2
+        tf32_src = "MEASURED_PEAKS.json bf16_tflops / 2"
+    except Exception:
+        tf32, tf32_src = 1100.0, "B200_PROFILING.md nominal TF32 dense"
     out = {"iir_fp32": {"peak_tfma_s": round(f32, 2), "fma_per_px_scale": fma,
                         "sweep": {"tfma_s": round(sweep_value * 1e6 * fma / 1e12, 2),
                                   "frac": round(sweep_value * 1e6 * fma / 1e12 / f32, 3)},
                         "per_scale": {}},
-           "fir_fp64": {"peak_tfma_s": DFMA_PEAK_T, "peak_source": "profiles/r1_pipes.txt",
-                        "per_scale": {}}}
+           "fir": {"fp64_peak_tfma_s": DFMA_PEAK_T, "fp64_peak_source": "profiles/r1_pipes.txt",
+                   "tf32_peak_tflop_s": round(tf32, 1), "tf32_peak_source": tf32_src,
+                   "per_scale": {}}}
     for sg, v in per_scale["iir"].items():
         a = v * 1e6 * fma / 1e12
         out["iir_fp32"]["per_scale"][sg] = {"tfma_s": round(a, 2), "frac": round(a / f32, 3)}
     for sg, v in per_scale["fir"].items():
         taps = 2 * int(4 * float(sg)) + 1  # gaussian_fir(sigma, 0, 4 sigma)
-        a = v * 1e6 * 2 * taps / 1e12
-        out["fir_fp64"]["per_scale"][sg] = {"taps": taps, "tfma_s": round(a, 2),
-                                            "frac": round(a / DFMA_PEAK_T, 3)}
+        if taps >= FIRTC_MIN_TAPS:
+            kw = -(-(128 + taps - 1) // 32) * 32
+            a = v * 1e6 * 2 * 3 * 2 * kw / 1e12
+            out["fir"]["per_scale"][sg] = {"taps": taps, "path": "tensor cores (3xTF32)",
+                                           "mma_tflop_s": round(a, 1), "frac": round(a / tf32, 3),
+                                           "useful_tflop_s": round(v * 1e6 * 4 * taps / 1e12, 1)}
+        else:
+            a = v * 1e6 * 2 * taps / 1e12
+            out["fir"]["per_scale"][sg] = {"taps": taps, "path": "fp64 CUDA cores",
+                                           "tfma_s": round(a, 2), "frac": round(a / DFMA_PEAK_T, 3)}
     return out
 
 
