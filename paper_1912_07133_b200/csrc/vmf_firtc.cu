@@ -26,7 +26,8 @@
 #include "vmf_prof.cuh"
 #include "vmf_tma.cuh"
 
-#ifndef VMF_TC_ABL  // timing ablations (tools/gpu): 1 no split, 2 no stores, 3 one MMA step
+#ifndef VMF_TC_ABL  // timing ablations (tools/gpu): 1 no split, 2 no stores, 3 one MMA step,
+                    // 4 no MMA, 5 every tile loads tile 0's lines
 #define VMF_TC_ABL 0
 #endif
 
@@ -42,9 +43,20 @@ __device__ unsigned long long g_tctl[1024];
       g_tctl[(i) * 8 + (ph)] = t_;                                              \
     }                                                                           \
   } while (0)
+#define TCS(g, ph)                                                             \
+  do {                                                                          \
+    if (blockIdx.x == 0 && (g) < 96) {                                          \
+      unsigned long long t_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+      g_tctl[512 + (g) * 5 + (ph)] = t_;                                        \
+    }                                                                           \
+  } while (0)
 #else
 #define TCTL(i, ph) \
   do {              \
+  } while (0)
+#define TCS(g, ph) \
+  do {             \
   } while (0)
 #endif
 
@@ -420,9 +432,11 @@ __global__ void __launch_bounds__(kThreads, 1) firtc_mma_kernel(
           if (g >= nst) mbar_wait(&empty[st], (unsigned)(((g / nst) - 1) & 1));
           if (sl == 0) TCTL((t - (int)blockIdx.x) / (int)gridDim.x, 0);
           if (sl == ns - 1) TCTL((t - (int)blockIdx.x) / (int)gridDim.x, 1);
+          TCS(g, 0);
           mbar_expect_tx(&full[st], kOpBytes);
-          tma_load_2d_hint(ring + st * kStageBytes, &ta, &full[st], n0 - P.k + kSlice * sl, m0,
-                           pol_a);
+          tma_load_2d_hint(ring + st * kStageBytes, &ta, &full[st],
+                           VMF_TC_ABL == 5 ? kSlice * sl : n0 - P.k + kSlice * sl,
+                           VMF_TC_ABL == 5 ? 0 : m0, pol_a);
         }
       }
     }
@@ -439,19 +453,21 @@ __global__ void __launch_bounds__(kThreads, 1) firtc_mma_kernel(
         for (int sl = 0; sl < ns; ++sl, ++g) {
           const int st = g % nst;
           mbar_wait(&conv[st], (unsigned)((g / nst) & 1));
+          TCS(g, 3);
           asm volatile("tcgen05.fence::after_thread_sync;\n");
           const uint32_t ga = band_s + (uint32_t)(ns - 1 - sl) * 4096u;
           const uint64_t ah = sw128_desc(ga), al = sw128_desc(ga + gbytes);
           const uint32_t b = ring_s + st * kStageBytes;
           const uint64_t bh = sw128_desc(b), bl = sw128_desc(b + kOpBytes);
 #pragma unroll
-          for (int kk = 0; kk < (VMF_TC_ABL == 3 ? 1 : kSlice / 8); ++kk) {  // K = 8 (32 bytes) per instruction
+          for (int kk = 0; kk < (VMF_TC_ABL == 3 ? 1 : VMF_TC_ABL == 4 ? 0 : kSlice / 8); ++kk) {  // K = 8 (32 bytes) per instruction
             const uint64_t o = 2 * kk;
             mma_tf32(d, ah + o, bh + o, (sl > 0 || kk > 0) ? 1u : 0u);
             mma_tf32(d, ah + o, bl + o, 1u);
             mma_tf32(d, al + o, bh + o, 1u);
           }
           mma_commit(&empty[st]);  // the slot is free once these MMAs have read it
+          TCS(g, 4);
         }
         TCTL(i, 3);
         mma_commit(&tfull[buf]);
@@ -466,6 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1) firtc_mma_kernel(
       for (int sl = 0; sl < ns; ++sl, ++g) {
         const int st = g % nst;
         mbar_wait(&full[st], (unsigned)((g / nst) & 1));
+        if (ct == 0) TCS(g, 1);
         float4 *raw = reinterpret_cast<float4 *>(ring + st * kStageBytes);
         float4 *lo = reinterpret_cast<float4 *>(ring + st * kStageBytes + kOpBytes);
 #pragma unroll
@@ -487,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1) firtc_mma_kernel(
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // visible to the MMA
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[st]);
+        if (ct == 0) TCS(g, 2);
       }
     }
   } else {

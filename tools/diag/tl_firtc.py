@@ -31,3 +31,9 @@ for name in sys.argv[1:] or ["g2_k8", "g32_k128"]:
     for i in range(n):
         print("  tile %2d: issue %7.2f..%7.2f  mma %7.2f..%7.2f  epi %7.2f..%7.2f us" %
               tuple([i] + [(v - t0) / 1e3 for v in t[i, :6]]))
+    sl = buf.astype(np.int64)[512:512 + 96 * 5].reshape(96, 5)
+    print("  slice: tma issue -> full -> converted -> mma sees -> mma committed (us from tile 0)")
+    for g in range(0, 40):
+        if sl[g, 0] == 0:
+            break
+        print("   %2d: %s" % (g, "  ".join("%7.2f" % ((v - t0) / 1e3) for v in sl[g])))
