@@ -110,6 +110,9 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
                                                            const float *__restrict__ X,
                                                            int64_t ldx, int64_t H, int64_t W,
                                                            SweepOut out) {
+  // the frame may come from the kernel just before this one (the row pass
+  // after this kernel then reads it with no wait of its own: this wait covers it)
+  pdl_wait();
   int y = blockIdx.y, s = 0;
   while (s < bm.ns && y >= 2 * bm.s[s].sv.nseg) y -= 2 * bm.s[s++].sv.nseg;
   if (s >= bm.ns) {  // chunk-vector rows: y = scale

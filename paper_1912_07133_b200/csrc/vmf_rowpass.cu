@@ -421,6 +421,9 @@ __global__ void __launch_bounds__(kRowThreads, NR == 1 ? (NBUF == 2 ? 5 : 4) : 3
   const int64_t rlo = (int64_t)blockIdx.x * per;
   const int64_t rhi = rlo + per < H ? rlo + per : H;
   if (rlo >= rhi) return;
+  // x may come from the kernel just before this one on the stream (a dtype
+  // conversion, say): wait for it before the prologue reads it
+  pdl_wait();
   if (c == 0) {
     for (int q = 0; q < NBUF; ++q) mbar_init(&bar[q], 1);
     // prologue: the first NBUF-1 steps in flight
