@@ -959,31 +959,32 @@ __global__ void __launch_bounds__(kFinThreads) colfinal_kernel(
   }
   __syncthreads();
   const int T = m;
-  if (threadIdx.x == 0) {
+  {
+    // every CTA publishes its own count; CTA b then reads the counts of all
+    // CTAs j < b at once (one thread each, spinning only on a CTA that has
+    // not counted yet -- it was dispatched earlier) and sums them: no serial
+    // chain of inclusive prefixes from CTA to CTA
     volatile unsigned long long *look = st->look;
-    if (b == 0) {
-      prefix = 0;
-    } else {
-      look[b] = kLookAgg | (unsigned long long)T;  // own count, before the look-back
-      long long acc = 0;
-      for (int j = b - 1; j >= 0;) {
-        const unsigned long long f = look[j];
-        if (f & kLookPre) {
-          acc += (long long)(f & kLookMask);
-          break;
-        }
-        if (f & kLookAgg) {
-          acc += (long long)(f & kLookMask);
-          --j;
-        }
-        // else: CTA j has not counted yet (spin; it was dispatched earlier)
-      }
-      prefix = acc;
+    __shared__ long long wsum[kFinThreads / 32];
+    if (threadIdx.x == 0) look[b] = kLookAgg | (unsigned long long)T;
+    long long v = 0;
+    for (int j = threadIdx.x; j < b; j += blockDim.x) {
+      unsigned long long f;
+      do {
+        f = look[j];
+      } while (!(f & kLookAgg));
+      v += (long long)(f & kLookMask);
     }
-    if (b < G - 1)
-      look[b] = kLookPre | (unsigned long long)(prefix + T);
-    else
-      *n_det = prefix + T;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long acc = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += wsum[w];
+      prefix = acc;
+      if (b == G - 1) *n_det = acc + T;
+    }
   }
   __syncthreads();
   const long long base = prefix;

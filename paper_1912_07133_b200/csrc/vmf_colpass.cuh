@@ -70,6 +70,30 @@ __device__ __forceinline__ void cand_push(int *ccount, int *cy, int *cx, float *
   }
 }
 
+// Flush a CTA's n shared candidates (n uniform over the CTA, read after a
+// barrier) to the global list with ONE reservation per CTA: a per-candidate
+// atomicAdd on the single global counter serialises in L2 when thresholds
+// are low and thousands of candidates arrive (frac = 0.05).  All threads of
+// the CTA must call it; sbase is a __shared__ int.
+__device__ __forceinline__ void cand_flush(int n, const int *cy, const int *cx, const float *cv,
+                                           CandState *st, int *gy, int *gx, float *gv, int gcap,
+                                           int *sbase) {
+  if (n <= 0) return;
+  if (threadIdx.x == 0) *sbase = atomicAdd(&st->count, n);
+  __syncthreads();
+  const int base = *sbase;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    const int k = base + q;
+    if (k < gcap) {
+      gy[k] = cy[q];
+      gx[k] = cx[q];
+      gv[k] = cv[q];
+    } else {
+      st->overflow = 1;
+    }
+  }
+}
+
 // Zero the CandState (one CTA's threads; after the pass's pdl_wait).
 __device__ __forceinline__ void cand_reset(CandState *st) {
   unsigned *w = reinterpret_cast<unsigned *>(st);

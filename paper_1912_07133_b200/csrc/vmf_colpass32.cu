@@ -544,17 +544,9 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
   // ---- flush the shared candidates (they passed th; the finaliser applies
   // the final threshold) ----------------------------------------------------
   __syncthreads();
-  const int n = S.ccount < kCand32 ? S.ccount : kCand32;
-  for (int q = j; q < n; q += kC32) {
-    const int k = atomicAdd(&st->count, 1);
-    if (k < gcap) {
-      gy[k] = S.cy[q];
-      gx[k] = S.cx[q];
-      gv[k] = S.cv[q];
-    } else {
-      st->overflow = 1;
-    }
-  }
+  __shared__ int flush_base;
+  cand_flush(S.ccount < kCand32 ? S.ccount : kCand32, S.cy, S.cx, S.cv, st, gy, gx, gv, gcap,
+             &flush_base);
 }
 
 // ---------------------------------------------------------------------------
@@ -855,17 +847,9 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
   // (the shared candidates already passed th; the finaliser applies the final
   // threshold, so no second, fresher read of the global maximum is needed)
   __syncthreads();
-  const int n = S.ccount < kCand32 ? S.ccount : kCand32;
-  for (int q = j; q < n; q += kC32) {
-    const int k = atomicAdd(&st->count, 1);
-    if (k < gcap) {
-      gy[k] = S.cy[q];
-      gx[k] = S.cx[q];
-      gv[k] = S.cv[q];
-    } else {
-      st->overflow = 1;
-    }
-  }
+  __shared__ int flush_base;
+  cand_flush(S.ccount < kCand32 ? S.ccount : kCand32, S.cy, S.cx, S.cv, st, gy, gx, gv, gcap,
+             &flush_base);
 }
 
 // ---------------------------------------------------------------------------

@@ -674,17 +674,8 @@ __global__ void __launch_bounds__(256) firtc_nms_kernel(const float *__restrict_
       cand_push(&ccount, cy, cx, cv, kNmsCand, st, gy, gx, gv, gcap, r, cc, v);
   }
   __syncthreads();
-  const int n = ccount < kNmsCand ? ccount : kNmsCand;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) {
-    const int k = atomicAdd(&st->count, 1);
-    if (k < gcap) {
-      gy[k] = cy[q];
-      gx[k] = cx[q];
-      gv[k] = cv[q];
-    } else {
-      st->overflow = 1;
-    }
-  }
+  __shared__ int flush_base;
+  cand_flush(ccount < kNmsCand ? ccount : kNmsCand, cy, cx, cv, st, gy, gx, gv, gcap, &flush_base);
   pdl_trigger();
 }
 
