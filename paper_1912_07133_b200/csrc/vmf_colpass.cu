@@ -698,9 +698,9 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
     // frac <= 0: L only (scale-space stacks), no candidates
     const float th = p.frac > 0.0f ? p.frac * fmaxf(__uint_as_float(S.cmax), gnow)
                                    : __int_as_float(0x7f800000);
-    auto test = [&](int q, int c, float v) {  // tile row q + K, tile column 4 + c
+    auto test = [&](int q, int c, float v) -> bool {  // tile row q + K, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
-      if (r < 1 || r > H - 2 || cc < 1 || cc > p.W - 2) return;
+      if (r < 1 || r > H - 2 || cc < 1 || cc > p.W - 2) return false;
       const int tr = q + K, tc = 4 + c;
       bool gt = true, lt = true;
 #pragma unroll
@@ -714,8 +714,7 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
         }
       // a maximum counts when L >= t, a minimum when -L >= t (|L| >= t alone
       // would admit a maximum of a negative region)
-      if ((gt && v >= th) || (lt && -v >= th))
-        cand_push(&S.ccount, S.cy, S.cx, S.cv, kCandSmem, st, gy, gx, gv, gcap, (int)r, (int)cc, v);
+      return (gt && v >= th) || (lt && -v >= th);
     };
     if (vec_out && ncol == kColOut) {  // 31 float4 per row, one row per warp
       const bool act = lane < kColOut / 4;
@@ -729,11 +728,15 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
           st_v4_hint(dst + q * ldl, v, lpol);
         }
         const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-        if (m4 >= th) {
-          if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
-          if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
-          if (fabsf(v.z) >= th) test(q, 4 * lane + 2, v.z);
-          if (fabsf(v.w) >= th) test(q, 4 * lane + 3, v.w);
+        if (__any_sync(0xffffffffu, act && m4 >= th)) {  // (warp-uniform) rare
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+          unsigned m = 0u;
+          if (act && m4 >= th) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (fabsf(vv[i]) >= th && test(q, 4 * lane + i, vv[i])) m |= 1u << i;
+          }
+          cand_push_warp(&S.ccount, S.cy, S.cx, S.cv, kCandSmem, st, gy, gx, gv, gcap, m, (int)(r0 + q), (int)(c0 + 4 * lane), vv);
         }
       }
     } else {
@@ -745,7 +748,9 @@ __global__ void __launch_bounds__(kColThreads, 4) colapply_kernel(
             v = S.tile[q + K][4 + c];
             Lout[(r0 + q) * ldl + c0 + c] = v;
           }
-          if (c < ncol && fabsf(v) >= th) test(q, c, v);
+          const unsigned m = c < ncol && fabsf(v) >= th && test(q, c, v) ? 1u : 0u;
+          const float vv[4] = {v, 0.f, 0.f, 0.f};
+          cand_push_warp(&S.ccount, S.cy, S.cx, S.cv, kCandSmem, st, gy, gx, gv, gcap, m, (int)(r0 + q), (int)(c0 + c), vv);
         }
     }
   }

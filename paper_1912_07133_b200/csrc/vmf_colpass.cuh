@@ -70,6 +70,51 @@ __device__ __forceinline__ void cand_push(int *ccount, int *cy, int *cx, float *
   }
 }
 
+// Warp-ballot compaction: the lanes of `mem` (the converged lanes calling
+// together; the whole warp by default) append up to 4 candidates each,
+// (y, x0 + i, v[i]) for the set bits i of `mask`.  One ballot per candidate
+// slot ranks every lane's candidates among the warp's, and the lowest lane
+// reserves the warp's block in the CTA's shared buffer with ONE atomicAdd
+// (past the buffer, the global list, as cand_push).
+__device__ __forceinline__ void cand_push_warp(int *ccount, int *cy, int *cx, float *cv,
+                                               int smem_cap, CandState *st, int *gy, int *gx,
+                                               float *gv, int gcap, unsigned mask, int y, int x0,
+                                               const float (&v)[4], unsigned mem = 0xffffffffu) {
+  if (!__ballot_sync(mem, mask != 0u)) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int before = 0, tot = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned bal = __ballot_sync(mem, (mask >> i) & 1u);
+    before += __popc(bal & lt);
+    tot += __popc(bal);
+  }
+  const int leader = __ffs(mem) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(ccount, tot);
+  int k = __shfl_sync(mem, base, leader) + before;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (!((mask >> i) & 1u)) continue;
+    if (k < smem_cap) {
+      cy[k] = y;
+      cx[k] = x0 + i;
+      cv[k] = v[i];
+    } else {
+      const int g = atomicAdd(&st->count, 1);
+      if (g < gcap) {
+        gy[g] = y;
+        gx[g] = x0 + i;
+        gv[g] = v[i];
+      } else {
+        st->overflow = 1;
+      }
+    }
+    ++k;
+  }
+}
+
 // Flush a CTA's n shared candidates (n uniform over the CTA, read after a
 // barrier) to the global list with ONE reservation per CTA: a per-candidate
 // atomicAdd on the single global counter serialises in L2 when thresholds

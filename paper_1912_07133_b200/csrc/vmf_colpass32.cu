@@ -491,9 +491,9 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
     const int ncol = (int)(W - c0 < kC32Out ? W - c0 : kC32Out);
     const float th = p.frac > 0.0f ? p.frac * fmaxf(__uint_as_float(S.cmax), gnow)
                                    : __int_as_float(0x7f800000);
-    auto test = [&](int q, int c, float v) {  // lt row q + 1, lt column 4 + c
+    auto test = [&](int q, int c, float v) -> bool {  // lt row q + 1, lt column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
-      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return;
+      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return false;
       const int tr = q + 1, tcn = 4 + c;
       bool gt = true, lt = true;
 #pragma unroll
@@ -506,8 +506,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
           lt &= v < w;
         }
       // a maximum counts when L >= t, a minimum when -L >= t
-      if ((gt && v >= th) || (lt && -v >= th))
-        cand_push(&S.ccount, S.cy, S.cx, S.cv, kCand32, st, gy, gx, gv, gcap, (int)r, (int)cc, v);
+      return (gt && v >= th) || (lt && -v >= th);
     };
     if (vec_out && ncol == kC32Out) {  // 31 float4 per row, one row per warp
       const bool act = lane < kC32Out / 4;
@@ -521,11 +520,15 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
           st_v4_hint(dst + q * ldl, v, lpol);
         }
         const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-        if (m4 >= th) {
-          if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
-          if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
-          if (fabsf(v.z) >= th) test(q, 4 * lane + 2, v.z);
-          if (fabsf(v.w) >= th) test(q, 4 * lane + 3, v.w);
+        if (__any_sync(0xffffffffu, act && m4 >= th)) {  // (warp-uniform) rare
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+          unsigned m = 0u;
+          if (act && m4 >= th) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (fabsf(vv[i]) >= th && test(q, 4 * lane + i, vv[i])) m |= 1u << i;
+          }
+          cand_push_warp(&S.ccount, S.cy, S.cx, S.cv, kCand32, st, gy, gx, gv, gcap, m, (int)(r0 + q), (int)(c0 + 4 * lane), vv);
         }
       }
     } else {
@@ -537,7 +540,9 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
             v = S.lt[q + 1][4 + c];
             Lout[(r0 + q) * ldl + c0 + c] = v;
           }
-          if (c < ncol && fabsf(v) >= th) test(q, c, v);
+          const unsigned m = c < ncol && fabsf(v) >= th && test(q, c, v) ? 1u : 0u;
+          const float vv[4] = {v, 0.f, 0.f, 0.f};
+          cand_push_warp(&S.ccount, S.cy, S.cx, S.cv, kCand32, st, gy, gx, gv, gcap, m, (int)(r0 + q), (int)(c0 + c), vv);
         }
     }
   }
@@ -560,9 +565,10 @@ template <int K>
 __global__ void __launch_bounds__(2 * kC32) colcarry32v_kernel(const float *__restrict__ V,
                                                              int64_t ldv, Col32Params p,
                                                              float *__restrict__ R,
+                                                             float *__restrict__ Mid,
                                                              CandState *__restrict__ cs,
                                                              const float *__restrict__ Vb) {
-  __shared__ float part[2 * K][kC32];
+  __shared__ float part[3 * K][kC32];
   const int j = threadIdx.x & (kC32 - 1), half = threadIdx.x >> 7;
   const int b = blockIdx.y;
   const int64_t H = p.H, W = p.W;
@@ -589,9 +595,9 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32v_kernel(const float *__re
     }
   }
   pdl_trigger();
-  float P[K], Q[K];
+  float P[K], Q[K], Mh[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) P[i] = Q[i] = 0.0f;
+  for (int i = 0; i < K; ++i) P[i] = Q[i] = Mh[i] = 0.0f;
   auto run = [&](auto HALF) {  // warp-uniform halves: compile-time weight indices
     constexpr int h0 = decltype(HALF)::value * (kB32 / 4);
 #pragma unroll
@@ -601,6 +607,9 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32v_kernel(const float *__re
       for (int i = 0; i < K; ++i) {
         P[i] = fmaf(p.SP[i][h0 + t], s, P[i]);
         Q[i] = fmaf(p.SQ[i][h0 + t], d, Q[i]);
+        // the bottom half-band's backward zero-state carry (the apply's
+        // top-half start): xb[t] is row r0 + 63 - h0 - t = r0 + 32 + (31 - h0 - t)
+        Mh[i] = fmaf(p.Wh[kB32 / 2 - 1 - h0 - t][i], xb[t], Mh[i]);
       }
     }
   };
@@ -613,6 +622,7 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32v_kernel(const float *__re
     for (int i = 0; i < K; ++i) {
       part[i][j] = P[i];
       part[K + i][j] = Q[i];
+      part[2 * K + i][j] = Mh[i];
     }
   }
   __syncthreads();
@@ -622,6 +632,7 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32v_kernel(const float *__re
       const float Pt = P[i] + part[i][j], Qt = Q[i] + part[K + i][j];
       R[ridx(b, i, K, W, col)] = Pt + Qt;      // forward
       R[ridx(b, K + i, K, W, col)] = Pt - Qt;  // backward
+      Mid[((int64_t)b * K + i) * W + col] = Mh[i] + part[2 * K + i][j];
     }
   }
 }
@@ -643,10 +654,11 @@ struct Col32vSmem {
 template <int K, int KIND, bool LSC>
 __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
     const float *__restrict__ V, int64_t ldv, float *__restrict__ Lout, int64_t ldl,
-    Col32Params p, const float *__restrict__ R, const float *__restrict__ Ky,
-    CandState *__restrict__ st, int *__restrict__ gy, int *__restrict__ gx,
-    float *__restrict__ gv, int gcap, const __grid_constant__ CUtensorMap tmap, int use_tma,
-    int vec_out, const float *__restrict__ Vb) {
+    Col32Params p, const float *__restrict__ R, const float *__restrict__ Mid,
+    const float *__restrict__ Ky, CandState *__restrict__ st, int *__restrict__ gy,
+    int *__restrict__ gx, float *__restrict__ gv, int gcap,
+    const __grid_constant__ CUtensorMap tmap, int use_tma, int vec_out,
+    const float *__restrict__ Vb) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);
   Col32vSmem &S = *reinterpret_cast<Col32vSmem *>(smem_raw + ((128u - (sbase & 127u)) & 127u));
@@ -658,7 +670,11 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
   const int64_t colc = col < 0 ? 0 : (col >= W ? W - 1 : col);
   const int b = blockIdx.y;
   const int64_t r0 = (int64_t)b * kB32, r1 = r0 + kB32;
-  const bool tma = use_tma && r0 >= 1 && r1 + 1 <= H && c0 >= 4 && c0 + kC32 <= W;
+  // every full band goes by TMA: the box's out-of-frame parts (the row above
+  // band 0, the row below the last band, the columns left of column 0 and
+  // right of W-1) arrive zero-filled and only feed outputs that are never
+  // stored or tested (the halo rows / columns outside the frame)
+  const bool tma = use_tma && r1 <= H;
   if (tma) {
     if (j == 0) {
       mbar_init(&tbar, 1);
@@ -684,11 +700,12 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
   pdl_wait();  // band start states, Ky and the CandState come from earlier kernels
   const float gbound = __uint_as_float(st->absmax_bits);
   Rec32<K, KIND> rf, rbt;
-  float ub1[K];
+  float ub1[K], mid[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     rf.u[i] = R[ridx(b, i, K, W, colc)];
     ub1[i] = R[ridx(b, K + i, K, W, colc)];
+    mid[i] = Mid[((int64_t)b * K + i) * W + colc];
   }
   const float ctop = r0 == 0 ? Ky[colc] : 0.0f;
   const float cbot = (H - 1 >= r0 - 1 && H - 1 <= r1) ? Ky[W + colc] : 0.0f;
@@ -707,19 +724,17 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
   // rows of this band (tile rows 1 .. nval) that lie inside the image
   const int nval = (int)(H - r0 < kB32 ? H - r0 : kB32);
   // top half's backward start: A^32 ub(r1) + sum_{t<32} A^t b V(r0 + 32 + t)
+  // (the sum is the carry pass's half-band record)
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    float a = 0.0f;
+    float a = mid[i];
 #pragma unroll
     for (int m = 0; m < K; ++m) a = fmaf(p.A32[i * K + m], ub1[m], a);
     rbt.u[i] = a;
   }
-#pragma unroll
-  for (int t = 0; t < kB32 / 2; ++t) {
-    const float v = TV(kB32 / 2 + 1 + t);
-#pragma unroll
-    for (int i = 0; i < K; ++i) rbt.u[i] = fmaf(p.Wh[t][i], v, rbt.u[i]);
-  }
+  // a fresher global maximum for the NMS threshold below, loaded now so its
+  // latency hides behind the walks
+  const unsigned gmid = *(volatile unsigned *)&st->absmax_bits;
   float park[kB32 / 2];
   // ---- top half: rows r0 .. r0+31 (and the halo row r0-1)
 #pragma unroll
@@ -739,7 +754,7 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
     const float w = fin(rf.out_from(p.c, park[t]));
     rf.step(p, v);
     TV(t + 1) = w;
-    if (t < nval) tmax = fmaxf(tmax, fabsf(w));
+    tmax = fmaxf(tmax, fabsf(w));  // (a partial band re-takes it below)
   }
   // ---- bottom half: rows r0+32 .. r1-1 (and the halo row r1)
   Rec32<K, KIND> rb;
@@ -762,7 +777,7 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
     const float w = fin(rf.out_from(p.c, park[t]));
     rf.step(p, v);
     TV(kB32 / 2 + 1 + t) = w;
-    if (kB32 / 2 + t < nval) tmax = fmaxf(tmax, fabsf(w));
+    tmax = fmaxf(tmax, fabsf(w));
   }
   {
     const float v = TV(kB32 + 1);
@@ -770,16 +785,17 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
     TV(kB32 + 1) = fin(w);
   }
   // the border rows' terms: L(0) += Ky[0], L(H-1) -= Ky[1] (tile row r - r0 + 1)
-  if (r0 == 0) {
-    const float w = TV(1) + fin(ctop);
-    TV(1) = w;
-    tmax = fmaxf(tmax, fabsf(w));
-  }
-  if (H - 1 >= r0 - 1 && H - 1 <= r1) {
+  const bool bot = H - 1 >= r0 - 1 && H - 1 <= r1;
+  if (r0 == 0) TV(1) = TV(1) + fin(ctop);
+  if (bot) {
     const int q = (int)(H - 1 - r0 + 1);
-    const float w = TV(q) - fin(cbot);
-    TV(q) = w;
-    if (q >= 1 && q <= nval) tmax = fmaxf(tmax, fabsf(w));
+    TV(q) = TV(q) - fin(cbot);
+  }
+  // (CTA-uniform) bands with a corrected border row or rows past H: the
+  // maximum is re-taken over the final values of the band's own rows
+  if (nval < kB32 || r0 == 0 || bot) {
+    tmax = 0.0f;
+    for (int t = 0; t < nval; ++t) tmax = fmaxf(tmax, fabsf(TV(t + 1)));
   }
 #undef TV
   pdl_trigger();
@@ -788,16 +804,16 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
   if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
   __syncthreads();
   if (j == 0) atomicMax(&st->absmax_bits, S.cmax);
-  const float gnow = fmaxf(gbound, __uint_as_float(*(volatile unsigned *)&st->absmax_bits));
+  const float gnow = fmaxf(gbound, __uint_as_float(gmid));
   {
     const int64_t rhi = r1 < H ? r1 : H;
     const int nrow = (int)(rhi - r0);
     const int ncol = (int)(W - c0 < kC32Out ? W - c0 : kC32Out);
     const float th = p.frac > 0.0f ? p.frac * fmaxf(__uint_as_float(S.cmax), gnow)
                                    : __int_as_float(0x7f800000);
-    auto test = [&](int q, int c, float v) {  // tile row q + 1, tile column 4 + c
+    auto test = [&](int q, int c, float v) -> bool {  // tile row q + 1, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
-      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return;
+      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return false;
       const int tr = q + 1, tcn = 4 + c;
       bool gt = true, lt = true;
 #pragma unroll
@@ -809,8 +825,7 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
           gt &= v > w;
           lt &= v < w;
         }
-      if ((gt && v >= th) || (lt && -v >= th))
-        cand_push(&S.ccount, S.cy, S.cx, S.cv, kCand32, st, gy, gx, gv, gcap, (int)r, (int)cc, v);
+      return (gt && v >= th) || (lt && -v >= th);
     };
     if (vec_out && ncol == kC32Out) {
       const bool act = lane < kC32Out / 4;
@@ -824,11 +839,15 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
           st_v4_hint(dst + q * ldl, v, lpol);
         }
         const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-        if (m4 >= th) {
-          if (fabsf(v.x) >= th) test(q, 4 * lane, v.x);
-          if (fabsf(v.y) >= th) test(q, 4 * lane + 1, v.y);
-          if (fabsf(v.z) >= th) test(q, 4 * lane + 2, v.z);
-          if (fabsf(v.w) >= th) test(q, 4 * lane + 3, v.w);
+        if (__any_sync(0xffffffffu, act && m4 >= th)) {  // (warp-uniform) rare
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+          unsigned m = 0u;
+          if (act && m4 >= th) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (fabsf(vv[i]) >= th && test(q, 4 * lane + i, vv[i])) m |= 1u << i;
+          }
+          cand_push_warp(&S.ccount, S.cy, S.cx, S.cv, kCand32, st, gy, gx, gv, gcap, m, (int)(r0 + q), (int)(c0 + 4 * lane), vv);
         }
       }
     } else {
@@ -840,7 +859,9 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
             v = S.tile[q + 1][4 + c];
             Lout[(r0 + q) * ldl + c0 + c] = v;
           }
-          if (c < ncol && fabsf(v) >= th) test(q, c, v);
+          const unsigned m = c < ncol && fabsf(v) >= th && test(q, c, v) ? 1u : 0u;
+          const float vv[4] = {v, 0.f, 0.f, 0.f};
+          cand_push_warp(&S.ccount, S.cy, S.cx, S.cv, kCand32, st, gy, gx, gv, gcap, m, (int)(r0 + q), (int)(c0 + c), vv);
         }
     }
   }
@@ -864,9 +885,10 @@ struct Col32Plan {
 size_t colpass32_workspace_bytes(int64_t h, int64_t w, int k) {
   const int64_t NB = cdiv(h, kB32);
   const size_t rec = (size_t)NB * (2 * k + 2) * w * sizeof(float);
+  const size_t mid = (size_t)NB * k * w * sizeof(float);  // half-band carries (V mode)
   const int64_t gcap = colpass_cand_capacity(h, w);
-  return 4096 + ((rec + 255) & ~(size_t)255) + ((2 * w * sizeof(float) + 255) & ~(size_t)255) +
-         (size_t)gcap * 12 + 1024;
+  return 4096 + ((rec + 255) & ~(size_t)255) + ((mid + 255) & ~(size_t)255) +
+         ((2 * w * sizeof(float) + 255) & ~(size_t)255) + (size_t)gcap * 12 + 1024;
 }
 
 static int plan32(Col32Plan *P, int64_t h, int64_t w, const IirParams &ip) {
@@ -994,6 +1016,8 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
   char *q = base + 4096;
   float *R = (float *)q;
   q += ((size_t)p.NB * (2 * K + 2) * w * sizeof(float) + 255) & ~(size_t)255;
+  float *Mid = (float *)q;
+  q += ((size_t)p.NB * K * w * sizeof(float) + 255) & ~(size_t)255;
   float *Cc = (float *)q;
   q += (2 * w * sizeof(float) + 255) & ~(size_t)255;
   const int64_t gcap = colpass_cand_capacity(h, w);
@@ -1014,7 +1038,7 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
                            csm);
     if (VM)
       launch_pdl(colcarry32v_kernel<K>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
-                 dim3(2 * kC32), 0, st, T, ldt, p, R, cs, vm.vb);
+                 dim3(2 * kC32), 0, st, T, ldt, p, R, Mid, cs, vm.vb);
     else
       launch_pdl(colcarry32_kernel<K, VM>, dim3((unsigned)cdiv(w, kC32), (unsigned)p.NB),
                  dim3(2 * kC32), csm, st, T, ldt, p, R, P.hm, cmap, ctma, cs, vm.vb);
@@ -1047,8 +1071,8 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     }
     auto kern = p.lsc == 1.0f ? colapply32v_kernel<K, KIND, false> : colapply32v_kernel<K, KIND, true>;
     launch_pdl(kern, dim3((unsigned)cdiv(w, kC32Out), (unsigned)p.NB), dim3(kC32), sm, st, T, ldt,
-               L, ldl, p, (const float *)R, vm.ky, cs, gy, gx, gv, (int)gcap, tmap, use_tma,
-               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0), vm.vb);
+               L, ldl, p, (const float *)R, (const float *)Mid, vm.ky, cs, gy, gx, gv, (int)gcap,
+               tmap, use_tma, (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0), vm.vb);
   } else {
     Launch g(K_IIR_COLS_FUSED, st);
     CUtensorMap tmap;

@@ -445,9 +445,9 @@ __device__ __forceinline__ void fc_tile(
     // frac <= 0: L only (scale-space stacks), no candidates
     const float th = frac > 0.0f ? frac * fmaxf(__uint_as_float(S.cmax), gbound)
                                  : __int_as_float(0x7f800000);
-    auto test = [&](int q, int c, float v) {  // L tile row q + 1, tile column 4 + c
+    auto test = [&](int q, int c, float v) -> bool {  // L tile row q + 1, tile column 4 + c
       const int64_t r = r0 + q, cc = c0 + c;
-      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return;
+      if (r < 1 || r > H - 2 || cc < 1 || cc > W - 2) return false;
       const float *lp = Ls + (q + 1) * SH::kStride + 4 + c;
       bool gt = true, lt = true;
 #pragma unroll
@@ -461,8 +461,13 @@ __device__ __forceinline__ void fc_tile(
         }
       // a maximum counts when L >= t, a minimum when -L >= t (|L| >= t alone
       // would admit a maximum of a negative region)
-      if ((gt && v >= th) || (lt && -v >= th))
-        cand_push(&S.ccount, S.cy, S.cx, S.cv, kFcCand, st, gy, gx, gv, gcap, (int)r, (int)cc, v);
+      return (gt && v >= th) || (lt && -v >= th);
+    };
+    // warp-ballot compaction over the lanes that reach it together
+    auto push = [&](unsigned m, int q, int c, const float (&vv)[4]) {
+      const unsigned mem = __activemask();
+      cand_push_warp(&S.ccount, S.cy, S.cx, S.cv, kFcCand, st, gy, gx, gv, gcap, m,
+                     (int)(r0 + q), (int)(c0 + c), vv, mem);
     };
     if (vec_out && ncol == SH::kOut) {
       // a row is kOut / 4 float4 (15 for the 64-column tile): with <= 16 a
@@ -476,12 +481,14 @@ __device__ __forceinline__ void fc_tile(
           const float4 v = *reinterpret_cast<const float4 *>(Ls + (q + 1) * SH::kStride + 4 + 4 * u);
           *reinterpret_cast<float4 *>(dst + q * ldl) = v;
           const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+          unsigned m = 0u;
           if (m4 >= th) {
-            if (fabsf(v.x) >= th) test(q, 4 * u, v.x);
-            if (fabsf(v.y) >= th) test(q, 4 * u + 1, v.y);
-            if (fabsf(v.z) >= th) test(q, 4 * u + 2, v.z);
-            if (fabsf(v.w) >= th) test(q, 4 * u + 3, v.w);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (fabsf(vv[i]) >= th && test(q, 4 * u + i, vv[i])) m |= 1u << i;
           }
+          push(m, q, 4 * u, vv);
         }
       }
     } else {
@@ -489,7 +496,8 @@ __device__ __forceinline__ void fc_tile(
         for (int cl = lane; cl < ncol; cl += 32) {
           const float v = Ls[(q + 1) * SH::kStride + 4 + cl];
           Lout[(r0 + q) * ldl + c0 + cl] = v;
-          if (fabsf(v) >= th) test(q, cl, v);
+          const float vv[4] = {v, 0.f, 0.f, 0.f};
+          push(fabsf(v) >= th && test(q, cl, v) ? 1u : 0u, q, cl, vv);
         }
     }
   }

@@ -657,21 +657,24 @@ __global__ void __launch_bounds__(256) firtc_nms_kernel(const float *__restrict_
   for (int q = threadIdx.x >> 7; q < kNmsR; q += 2) {
     const int r = r0 + q;
     const float v = t[q + 1][j + 1];
-    if (!(fabsf(v) >= thr) || r < 1 || r > H - 2 || cc < 1 || cc > W - 2) continue;
-    bool gt = true, lt = true;
+    unsigned m = 0u;
+    if (fabsf(v) >= thr && r >= 1 && r <= H - 2 && cc >= 1 && cc <= W - 2) {
+      bool gt = true, lt = true;
 #pragma unroll
-    for (int di = 0; di < 3; ++di)
+      for (int di = 0; di < 3; ++di)
 #pragma unroll
-      for (int dj = 0; dj < 3; ++dj) {
-        if (di == 1 && dj == 1) continue;
-        const float w = t[q + di][j + dj];
-        gt &= v > w;
-        lt &= v < w;
-      }
-    // a maximum counts when positive, a minimum when negative (|v| >= thr alone
-    // would admit a positive local minimum)
-    if ((gt && v >= thr) || (lt && -v >= thr))
-      cand_push(&ccount, cy, cx, cv, kNmsCand, st, gy, gx, gv, gcap, r, cc, v);
+        for (int dj = 0; dj < 3; ++dj) {
+          if (di == 1 && dj == 1) continue;
+          const float w = t[q + di][j + dj];
+          gt &= v > w;
+          lt &= v < w;
+        }
+      // a maximum counts when positive, a minimum when negative (|v| >= thr
+      // alone would admit a positive local minimum)
+      m = (gt && v >= thr) || (lt && -v >= thr) ? 1u : 0u;
+    }
+    const float vv[4] = {v, 0.f, 0.f, 0.f};  // (q is warp-uniform: the whole warp calls)
+    cand_push_warp(&ccount, cy, cx, cv, kNmsCand, st, gy, gx, gv, gcap, m, r, cc, vv);
   }
   __syncthreads();
   __shared__ int flush_base;

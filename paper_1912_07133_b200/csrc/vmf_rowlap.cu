@@ -804,6 +804,10 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_rows_kernel<K, KIND>, block, smem);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
+    if (const char *e = getenv("VMF_ROW_OCC")) {  // experiment: fewer resident CTAs per SM
+      const int o = atoi(e);
+      if (o > 0 && o < occ) occ = o;
+    }
     slots = (occ > 0 ? occ : 1) * nsm;
   }
   // ns slots are the edge CTAs (virtual and border rows of each scale)
