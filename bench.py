@@ -408,7 +408,7 @@ def run_ours(args):
              torch.empty(1 << 18, dtype=torch.float32, device=dev),
              torch.empty(2, dtype=torch.int64, device=dev)) for _ in IIR]
 
-    def step(stages, conc=detect.SWEEP_STREAMS):
+    def step(stages, conc=None):
         # the product sweep (detect_sweep's device part): scales on
         # concurrent streams, L of every scale written to its workspace
         detect._sweep_launch(x, _lib.VMF_F32, stages, 0.5, None, 1 << 18, outs, conc=conc)
@@ -616,7 +616,7 @@ def run_ours(args):
                                 "Mpixel/s per scale that upload rate alone allows"},
             "gpu_launches": int(launches),
             "graph": "each timed step is one CUDA-graph replay of the 5-scale sweep "
-                     f"({detect.SWEEP_STREAMS} scales in flight on concurrent streams); "
+                     f"(row pass for all scales, then each scale's column pass on its own stream); "
                      "`kernels` and `roofline` come from a serialised replay",
             "clocks": clk,
             "cpu_baseline": cpu,

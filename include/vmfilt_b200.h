@@ -232,6 +232,9 @@ void vmf_profile_begin(void);
 void vmf_profile_stop(void);
 int vmf_profile_read(double *ms, long long *counts, int n);
 int vmf_profile_end(double *ms, long long *counts, int n);
+/* The recorded launches in order: kernel id, start / end in ms after the
+ * first recorded start (a concurrent replay's timeline); returns the count. */
+int vmf_profile_timeline(int *ids, float *t0, float *t1, int n);
 
 #ifdef __cplusplus
 }

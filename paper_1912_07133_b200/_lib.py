@@ -67,6 +67,8 @@ _PROTOS = {
     "vmf_profile_stop": (None, []),
     "vmf_profile_read": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int]),
     "vmf_profile_end": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int]),
+    "vmf_profile_timeline": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_float),
+                                       C.POINTER(C.c_float), C.c_int]),
     "vmf_blur_lap_detect_workspace_bytes": (_sz, [_i64, _i64, C.POINTER(VmfStage),
                                                   C.POINTER(VmfStage)]),
     "vmf_blur_lap_detect": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, C.POINTER(VmfStage),
@@ -152,6 +154,17 @@ def profile_read() -> dict:
     cnt = (C.c_longlong * n)()
     L.vmf_profile_read(ms, cnt, n)
     return {L.vmf_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(n) if cnt[i]}
+
+
+def profile_timeline(n: int = 4096) -> list:
+    """-> [(kernel name, start_ms, end_ms)] of the recorded launches, times
+    after the first recorded start."""
+    L = lib()
+    ids = (C.c_int * n)()
+    t0 = (C.c_float * n)()
+    t1 = (C.c_float * n)()
+    m = L.vmf_profile_timeline(ids, t0, t1, n)
+    return [(L.vmf_kernel_name(ids[i]).decode(), t0[i], t1[i]) for i in range(m)]
 
 
 def profile_end() -> dict:

@@ -112,6 +112,30 @@ int vmf_profile_read(double *ms, long long *counts, int n) {
   return vmf::K_NUM_IDS;
 }
 
+// The recorded launches in order: id, start and end in ms after the first
+// recorded start (a concurrent replay's timeline).  Returns the count.
+int vmf_profile_timeline(int *ids, float *t0, float *t1, int n) {
+  std::lock_guard<std::mutex> lk(vmf::g_mu);
+  int m = 0;
+  if (vmf::g_recs.empty()) return 0;
+  cudaEvent_t ref = vmf::g_recs[0].a;
+  for (auto &r : vmf::g_recs) {
+    if (m >= n) break;
+    cudaEventSynchronize(r.b);
+    float a = 0.0f, b = 0.0f;
+    if (cudaEventElapsedTime(&a, ref, r.a) != cudaSuccess ||
+        cudaEventElapsedTime(&b, ref, r.b) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    ids[m] = r.id;
+    t0[m] = a;
+    t1[m] = b;
+    ++m;
+  }
+  return m;
+}
+
 int vmf_profile_end(double *ms, long long *counts, int n) {
   vmf_profile_stop();
   return vmf_profile_read(ms, counts, n);

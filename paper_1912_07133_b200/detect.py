@@ -118,9 +118,15 @@ def _fused(x, code, row: _Stage, col: _Stage, lap_scale, frac, blur_out, lap_out
     return det_yx, det_val, scal, n_host.value
 
 
-# scales in flight in a sweep (measured on B200: 1 -> 0.617 ms, 3 -> 0.532 ms);
-# VMF_SWEEP_STREAMS overrides it for experiments
+# scales (or frames) in flight on the per-scale fused path (measured on B200:
+# 1 -> 0.617 ms, 3 -> 0.532 ms per 5-scale sweep); VMF_SWEEP_STREAMS overrides
+# it for experiments
 SWEEP_STREAMS = int(os.environ.get("VMF_SWEEP_STREAMS", "3"))
+# the multi-scale sweep's column passes: one stream per scale, up to this many
+# (5 scales: 3 streams 0.433 ms, 4: 0.435, 5: 0.416 -- with fewer streams a
+# stream's second scale waits behind the first's latency-bound finaliser);
+# VMF_SWEEP_SCALE_STREAMS overrides it
+SWEEP_SCALE_STREAMS = int(os.environ.get("VMF_SWEEP_SCALE_STREAMS", "8"))
 _side_streams: dict = {}
 
 
@@ -193,8 +199,7 @@ def _sweep_launch_multi(x, code, stages, frac, lap_scales, cap, outs, laps, conc
             cur.wait_stream(s)
 
 
-def _sweep_launch(x, code, stages, frac, lap_scales, cap, outs, laps=None,
-                  conc: int = SWEEP_STREAMS):
+def _sweep_launch(x, code, stages, frac, lap_scales, cap, outs, laps=None, conc=None):
     """Queue one fused single-scale pass per stage.  The scales of a sweep
     are independent (same frame, own outputs), so with conc > 1 they run on
     `conc` side streams, each with its own workspace slot, forked from and
@@ -202,10 +207,11 @@ def _sweep_launch(x, code, stages, frac, lap_scales, cap, outs, laps=None,
     (band scan, finaliser, kernel tails) overlap another's row pass.  When
     the fp32 path takes the sweep, one row pass serves every scale."""
     ns = len(stages)
-    conc = max(1, min(int(conc), ns))
     if _sweep_ok(x, code, stages):
+        conc = max(1, min(int(SWEEP_SCALE_STREAMS if conc is None else conc), ns))
         _sweep_launch_multi(x, code, stages, frac, lap_scales, cap, outs, laps, conc)
         return
+    conc = max(1, min(int(SWEEP_STREAMS if conc is None else conc), ns))
 
     def one(i, slot):  # x: one frame for every stage, or a list (one frame per stage)
         sc = 1.0 if lap_scales is None else float(lap_scales[i])

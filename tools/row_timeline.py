@@ -30,7 +30,7 @@ for it in range(4):
     flush.zero_()
     torch.cuda.synchronize()
     L.vmf_debug_timeline_reset()
-    detect._sweep_launch(x, _lib.VMF_F32, stg, 0.5, None, 1 << 18, outs, conc=3)
+    detect._sweep_launch(x, _lib.VMF_F32, stg, 0.5, None, 1 << 18, outs)
     torch.cuda.synchronize()
     L.vmf_debug_timeline(buf.ctypes.data, 4096)
     t = buf.astype(np.int64)
