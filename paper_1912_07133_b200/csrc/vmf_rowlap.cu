@@ -113,9 +113,9 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
   // the frame may come from the kernel just before this one (the row pass
   // after this kernel then reads it with no wait of its own: this wait covers it)
   pdl_wait();
-  int y = blockIdx.y, s = 0;
-  while (s < bm.ns && y >= 2 * bm.s[s].sv.nseg) y -= 2 * bm.s[s++].sv.nseg;
-  if (s >= bm.ns) {  // chunk-vector rows: y = scale
+  int y = blockIdx.y;
+  if (y >= 2 * bm.maxseg) {  // chunk-vector rows: y = scale
+    y -= 2 * bm.maxseg;
     const BorderScale &b = bm.s[y];
     float *vlr = out.E(y) + kExVlr * W;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < b.C; c += gridDim.x * blockDim.x) {
@@ -161,16 +161,15 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
     }
     return;
   }
-  const BorderScale &b = bm.s[s];
-  const int nseg = b.sv.nseg;
-  const int which = y / nseg, k = y % nseg;
+  // segment k of side `which` for EVERY scale whose border reaches it: the
+  // rows are loaded once, each scale runs its own recursion over them
+  const int which = y / bm.maxseg, k = y % bm.maxseg;
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t cc = col < W ? col : W - 1;
-  const int Mh = b.sv.Mh;
   const int m0 = 1 + kSeg * k;
-  const int n = (Mh - m0 + 1) < kSeg ? (Mh - m0 + 1) : kSeg;  // m = m0 .. m0+n-1
+  const int n = (bm.maxMh - m0 + 1) < kSeg ? (bm.maxMh - m0 + 1) : kSeg;  // m = m0 .. m0+n-1
   // top: xs[t] = X(m0 - 1 + t); bottom: xs[t] = X(H - m0 - t); all loaded
-  // before the recursion (independent loads)
+  // before the recursions (independent loads)
   float xs[kSeg + 1];
   const float *Xc = X + cc;
   // rows r(t) = r0 + dir t, t = 0..n; the common segment (whole, inside the
@@ -190,17 +189,28 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
       xs[t] = __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx);
     }
   }
-  Rec32<K, KIND> u;
+  for (int s = 0; s < bm.ns; ++s) {
+    const BorderScale &b = bm.s[s];
+    const int nseg = b.sv.nseg;
+    if (k >= nseg) continue;
+    const int ns_ = (b.sv.Mh - m0 + 1) < kSeg ? (b.sv.Mh - m0 + 1) : kSeg;  // this scale's rows
+    Rec32<K, KIND> u;
 #pragma unroll
-  for (int i = 0; i < K; ++i) u.u[i] = 0.0f;
-  // G(m0 + t): top X(m0+t) - X(m0+t-1) = xs[t+1] - xs[t]; bottom
-  // X(H-m0-t) - X(H-m0-t-1) = -(xs[t+1] - xs[t]): the sign goes on the share.
-  // Steps t >= n see G = 0 on a zero state (rows repeated above).
+    for (int i = 0; i < K; ++i) u.u[i] = 0.0f;
+    // G(m0 + t): top X(m0+t) - X(m0+t-1) = xs[t+1] - xs[t]; bottom
+    // X(H-m0-t) - X(H-m0-t-1) = -(xs[t+1] - xs[t]): the sign goes on the share.
+    // Steps t >= ns_ see G = 0 on a zero state.
+    if (ns_ == kSeg) {
 #pragma unroll
-  for (int t = kSeg - 1; t >= 0; --t) u.step(b, xs[t + 1] - xs[t]);
-  float v = u.out(b.sv.v[k]);
-  v *= which == 0 ? b.sign : -1.0f;
-  if (col < W) out.E(s)[kExS * W + ((int64_t)which * nseg + k) * W + col] = v;
+      for (int t = kSeg - 1; t >= 0; --t) u.step(b, xs[t + 1] - xs[t]);
+    } else {
+#pragma unroll
+      for (int t = kSeg - 1; t >= 0; --t) u.step(b, t < ns_ ? xs[t + 1] - xs[t] : 0.0f);
+    }
+    float v = u.out(b.sv.v[k]);
+    v *= which == 0 ? b.sign : -1.0f;
+    if (col < W) out.E(s)[kExS * W + ((int64_t)which * nseg + k) * W + col] = v;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -341,10 +351,15 @@ __global__ void __maxnreg__(168) sweep_rows_kernel(  // (3 CTAs of 128 threads p
     float g[kRChunk];
 #pragma unroll
     for (int t = 0; t < kRChunk; ++t) g[t] = (t < kRChunk - 1 ? x[t + 1] : xr) - x[t];
+    const int cw0 = c & ~31;  // the warp's first chunk
     for (int s = 0; s < ns; ++s) {
-      float pl, pr;
-      dx_chunk<K, KIND>(sp[s], RC32<K>(sp[s]), out.E(s) + kExVlr * W, g, pl, pr);
-      warp_sum2(pl, pr);
+      float pl = 0.0f, pr = 0.0f;
+      const int Mh = sp[s].Mh;
+      // (warp-uniform) only warps with a chunk within Mh of an edge contribute
+      if (kRChunk * cw0 < Mh || kRChunk * (cw0 + 32) >= W - Mh) {
+        dx_chunk<K, KIND>(sp[s], RC32<K>(sp[s]), out.E(s) + kExVlr * W, g, pl, pr);
+        warp_sum2(pl, pr);
+      }
       if (lane == 0) {
         red[s][c >> 5] = pl;
         red[s][8 + (c >> 5)] = pr;
@@ -753,6 +768,8 @@ static int sweep_plan(int64_t h, int64_t w, int k, int ns, const SweepStage *st,
     if (rc) return rc;
     P->rm.s[s].nseg = b.sv.nseg;
     P->nseg_total += 2 * b.sv.nseg;
+    if (b.sv.nseg > P->bm.maxseg) P->bm.maxseg = b.sv.nseg;
+    if (b.sv.Mh > P->bm.maxMh) P->bm.maxMh = b.sv.Mh;
   }
   return VMF_OK;
 }
@@ -782,7 +799,7 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
   {
     Launch g(K_ROW_BORDER, st);  // the border kernel (reads X only)
     launch_pdl(sweep_border_kernel<K, KIND>,
-               dim3((unsigned)cdiv(rm.W, 128), (unsigned)(P.nseg_total + rm.ns)), dim3(128), 0, st,
+               dim3((unsigned)cdiv(rm.W, 128), (unsigned)(2 * P.bm.maxseg + rm.ns)), dim3(128), 0, st,
                P.bm, x, ldx, rm.H, rm.W, out);
   }
   const size_t smem = rl_smem(rm.C, K, rm.ns);

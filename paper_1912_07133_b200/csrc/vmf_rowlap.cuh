@@ -57,6 +57,7 @@ struct BorderScale {   // per scale, for the border kernel
 struct BorderMulti {
   BorderScale s[kMaxScales];
   int ns;
+  int maxseg, maxMh;  // the longest scale's segments / border length
 };
 
 // Per-scale extras, floats, w = frame width: Vt [w] | Vb [w] | Ky [2w] |
