@@ -146,7 +146,10 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w,
  * sweep_ws (vmf_sweep_workspace_bytes).  vmf_sweep_detect: the column pass
  * of one scale (any stream ordered after vmf_sweep_rows; scales are
  * independent and may run concurrently, each with its own ws of
- * vmf_sweep_detect_workspace_bytes); outputs as vmf_blur_lap_detect. */
+ * vmf_sweep_detect_workspace_bytes); outputs as vmf_blur_lap_detect.
+ * lap_out may be NULL: the detections are then made from the column pass's
+ * tiles and L is never written (the candidate list is sized for every
+ * strict 3x3 extremum of the frame, so no fallback needs L). */
 size_t vmf_sweep_workspace_bytes(int64_t h, int64_t w, int nscales);
 size_t vmf_sweep_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *col_stage);
 int vmf_sweep_supported(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,

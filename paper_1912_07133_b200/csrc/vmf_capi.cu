@@ -447,8 +447,8 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
     SweepStage sst = sweep_stage(row_stage, col_stage);
     rc = sweep_rows((const float *)x, ldx, h, w, row_stage->n, 1, &sst, o, st);
     if (rc) return rc;
-    rc = sweep_cols(o, 0, h, w, col_stage, lap_scale, frac, L, w, det_yx, det_val, cap, n_det_dev,
-                    thr_dev, carry, carry_b, st);
+    rc = sweep_cols(o, 0, h, w, col_stage, lap_scale, frac, lap_out, w, det_yx, det_val, cap,
+                    n_det_dev, thr_dev, carry, carry_b, st);
     if (rc) return rc;
     if (blur_out) {  // B on request: T into the (unused) B slot, then the column leaf
       float *Tb = T + img / sizeof(float);
@@ -499,8 +499,8 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
                   col_stage->b_zero, col_stage->sign);
     if (rc) return rc;
     if (colpass32_supported(h, w, ip))  // fp32 "Laplacian first" (vmf_colpass32.cu)
-      rc = colpass32_run(T, w, L, w, ip, h, w, lap_scale, frac, det_yx, det_val, cap, n_det_dev,
-                         thr_dev, carry, carry_b, st);
+      rc = colpass32_run(T, w, lap_out, w, ip, h, w, lap_scale, frac, det_yx, det_val, cap,
+                         n_det_dev, thr_dev, carry, carry_b, st);
     else
       rc = colpass_run(T, w, L, w, nullptr, ip, h, w, lap_scale, frac, det_yx, det_val, cap,
                        n_det_dev, thr_dev, carry, carry_b, st);
@@ -552,8 +552,7 @@ size_t vmf_sweep_workspace_bytes(int64_t h, int64_t w, int nscales) {
 }
 
 size_t vmf_sweep_detect_workspace_bytes(int64_t h, int64_t w, const vmf_stage *col_stage) {
-  return align256((size_t)h * w * sizeof(float)) +
-         align256(colpass32_workspace_bytes(h, w, col_stage ? col_stage->n : 4)) + 256;
+  return align256(colpass32_workspace_bytes(h, w, col_stage ? col_stage->n : 4)) + 256;
 }
 
 int vmf_sweep_supported(const void *x, int x_dtype, int64_t h, int64_t w, int64_t ldx,
@@ -598,9 +597,8 @@ int vmf_sweep_detect(int scale, int64_t h, int64_t w, int nscales, const vmf_sta
     return fail(VMF_EVALUE, "detection outputs missing");
   const SweepOut o = sweep_layout(sweep_ws, h, w, nscales);
   char *p = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  float *L = lap_out ? lap_out : (float *)p;
-  p += align256((size_t)h * w * sizeof(float));
-  return sweep_cols(o, scale, h, w, col_stage, lap_scale, frac, L, w, det_yx, det_val, cap,
+  // lap_out null: detections only, L stays in the column pass's tiles
+  return sweep_cols(o, scale, h, w, col_stage, lap_scale, frac, lap_out, w, det_yx, det_val, cap,
                     n_det_dev, thr_dev, p, align256(colpass32_workspace_bytes(h, w, col_stage->n)),
                     (cudaStream_t)stream);
 }

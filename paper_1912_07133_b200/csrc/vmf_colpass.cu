@@ -908,7 +908,9 @@ __global__ void __launch_bounds__(kFinThreads) colfinal_kernel(
   const int n = count < gcap ? count : gcap;
   const bool big = n > kSortCap;
   if (blockIdx.x == 0 && threadIdx.x == 0 && thr_out) *thr_out = thr;
-  if (force_full || overflow) {  // global list overflow: exact, slow path
+  // global list overflow: exact, slow path over L (a pass that keeps L in
+  // its tiles -- L null -- sizes its list for every possible candidate)
+  if ((force_full || overflow) && L) {
     if (blockIdx.x == 0) final_fullscan(L, ldl, H, W, thr, det_yx, det_val, cap, n_det);
     return;
   }

@@ -508,16 +508,16 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
       // a maximum counts when L >= t, a minimum when -L >= t
       return (gt && v >= th) || (lt && -v >= th);
     };
-    if (vec_out && ncol == kC32Out) {  // 31 float4 per row, one row per warp
+    if ((vec_out || !Lout) && ncol == kC32Out) {  // 31 float4 per row, one row per warp
       const bool act = lane < kC32Out / 4;
-      const uint64_t lpol = l2_policy_evict_first();  // L streams out
-      float *dst = Lout + r0 * ldl + c0 + 4 * lane;
+      const uint64_t lpol = l2_policy_evict_first();  // L streams out (if stored)
+      float *dst = Lout ? Lout + r0 * ldl + c0 + 4 * lane : nullptr;
 #pragma unroll 4
       for (int q = wid; q < nrow; q += kC32 / 32) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (act) {
           v = *reinterpret_cast<const float4 *>(&S.lt[q + 1][4 + 4 * lane]);
-          st_v4_hint(dst + q * ldl, v, lpol);
+          if (dst) st_v4_hint(dst + q * ldl, v, lpol);
         }
         const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
         if (__any_sync(0xffffffffu, act && m4 >= th)) {  // (warp-uniform) rare
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kC32, 3) colapply32_kernel(
           float v = 0.0f;
           if (c < ncol) {
             v = S.lt[q + 1][4 + c];
-            Lout[(r0 + q) * ldl + c0 + c] = v;
+            if (Lout) Lout[(r0 + q) * ldl + c0 + c] = v;
           }
           const unsigned m = c < ncol && fabsf(v) >= th && test(q, c, v) ? 1u : 0u;
           const float vv[4] = {v, 0.f, 0.f, 0.f};
@@ -827,16 +827,17 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
         }
       return (gt && v >= th) || (lt && -v >= th);
     };
-    if (vec_out && ncol == kC32Out) {
+    if ((vec_out || !Lout) && ncol == kC32Out) {
+      // (Lout null: detections only -- L never leaves the tile)
       const bool act = lane < kC32Out / 4;
       const uint64_t lpol = l2_policy_evict_first();
-      float *dst = Lout + r0 * ldl + c0 + 4 * lane;
+      float *dst = Lout ? Lout + r0 * ldl + c0 + 4 * lane : nullptr;
 #pragma unroll 4
       for (int q = wid; q < nrow; q += kC32 / 32) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (act) {
           v = *reinterpret_cast<const float4 *>(&S.tile[q + 1][4 + 4 * lane]);
-          st_v4_hint(dst + q * ldl, v, lpol);
+          if (dst) st_v4_hint(dst + q * ldl, v, lpol);
         }
         const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
         if (__any_sync(0xffffffffu, act && m4 >= th)) {  // (warp-uniform) rare
@@ -857,7 +858,7 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
           float v = 0.0f;
           if (c < ncol) {
             v = S.tile[q + 1][4 + c];
-            Lout[(r0 + q) * ldl + c0 + c] = v;
+            if (Lout) Lout[(r0 + q) * ldl + c0 + c] = v;
           }
           const unsigned m = c < ncol && fabsf(v) >= th && test(q, c, v) ? 1u : 0u;
           const float vv[4] = {v, 0.f, 0.f, 0.f};
@@ -882,11 +883,19 @@ struct Col32Plan {
   int kind;
 };
 
+// Candidate capacity of the fp32 column pass: every candidate is a strict
+// 3x3 extremum of L (maxima pairwise apart, minima too: at most
+// ceil(h/2) ceil(w/2) of each), so the list cannot overflow and the
+// finaliser never needs L itself -- L is stored only on request.
+static int64_t cand32_capacity(int64_t h, int64_t w) {
+  return 2 * cdiv(h, 2) * cdiv(w, 2) + 64;
+}
+
 size_t colpass32_workspace_bytes(int64_t h, int64_t w, int k) {
   const int64_t NB = cdiv(h, kB32);
   const size_t rec = (size_t)NB * (2 * k + 2) * w * sizeof(float);
   const size_t mid = (size_t)NB * k * w * sizeof(float);  // half-band carries (V mode)
-  const int64_t gcap = colpass_cand_capacity(h, w);
+  const int64_t gcap = cand32_capacity(h, w);
   return 4096 + ((rec + 255) & ~(size_t)255) + ((mid + 255) & ~(size_t)255) +
          ((2 * w * sizeof(float) + 255) & ~(size_t)255) + (size_t)gcap * 12 + 1024;
 }
@@ -1020,7 +1029,7 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
   q += ((size_t)p.NB * K * w * sizeof(float) + 255) & ~(size_t)255;
   float *Cc = (float *)q;
   q += (2 * w * sizeof(float) + 255) & ~(size_t)255;
-  const int64_t gcap = colpass_cand_capacity(h, w);
+  const int64_t gcap = cand32_capacity(h, w);
   int *gy = (int *)q;
   int *gx = gy + gcap;
   float *gv = (float *)(gx + gcap);
@@ -1072,7 +1081,7 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     auto kern = p.lsc == 1.0f ? colapply32v_kernel<K, KIND, false> : colapply32v_kernel<K, KIND, true>;
     launch_pdl(kern, dim3((unsigned)cdiv(w, kC32Out), (unsigned)p.NB), dim3(kC32), sm, st, T, ldt,
                L, ldl, p, (const float *)R, (const float *)Mid, vm.ky, cs, gy, gx, gv, (int)gcap,
-               tmap, use_tma, (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0), vm.vb);
+               tmap, use_tma, (int)(L && ldl % 4 == 0 && (uintptr_t)L % 16 == 0), vm.vb);
   } else {
     Launch g(K_IIR_COLS_FUSED, st);
     CUtensorMap tmap;
@@ -1095,7 +1104,7 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
     launch_pdl(kern, dim3((unsigned)cdiv(w, kC32Out), (unsigned)p.NB), dim3(kC32), sm, st, T, ldt,
                L, ldl, p, (const float *)R, (const float *)(VM ? vm.ky : Cc), VM ? 1.0f : p.sign,
                cs, gy, gx, gv, (int)gcap, tmap, use_tma,
-               (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0), vm.vb);
+               (int)(L && ldl % 4 == 0 && (uintptr_t)L % 16 == 0), vm.vb);
   }
   if (p.frac > 0.0f)
     colfinal_launch(cs, gy, gx, gv, gcap, L, ldl, h, w, p.frac, det_yx, det_val, cap, n_det_dev,

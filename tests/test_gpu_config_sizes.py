@@ -136,3 +136,24 @@ def test_config3_low_threshold_large_list(cat, frame3, name):
     assert np.all(np.diff(key) > 0)  # strictly (y, x) ordered
     exempt, bad = compare_blobs(dets.as_set(), want, L, thr)
     assert not bad, (name, len(bad), bad[:10])
+
+
+def test_detections_only_sweep_extreme_candidate_count(cat):
+    """detect_sweep keeps L in the column pass's tiles (no L in HBM); its
+    candidate list is sized for every strict 3x3 extremum, so a threshold
+    near zero on a pure-noise frame (~4 % of the pixels are extrema after the
+    sigma 2 blur: far more than the h w / 64 a list sized for a normal
+    threshold would hold) still returns the oracle's exact list, with no
+    fallback that would need L."""
+    from paper_1912_07133_b200 import detect
+
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((2048, 2048)).astype(np.float32)
+    frac = 1e-4
+    got = detect.detect_sweep(x, [cat["rp2"]], frac=frac, cap=1 << 20)
+    for name, dets in zip(["rp2"], got):
+        L, want, thr = _oracle_scale(x, cat[name], frac=frac)
+        assert dets.count > x.size // 64, (name, dets.count)
+        assert not dets.overflow
+        exempt, bad = compare_blobs(dets.as_set(), want, L, thr)
+        assert not bad, (name, len(bad), bad[:10])

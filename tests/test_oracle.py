@@ -109,3 +109,28 @@ def test_catalog_filters_are_valid_blurs(cat):
             assert abs(g - 1.0) < 1e-9, name
         elif not name.startswith("vm_bank"):
             assert abs(sum(f.taps) - 1.0) < 1e-12, name
+
+
+def test_strict_extrema_bound_sizes_the_candidate_list():
+    """The fp32 column pass sizes its candidate list for 2 ceil(h/2) ceil(w/2)
+    entries (vmf_colpass32.cu cand32_capacity) so that, with L kept in its
+    tiles, no overflow can occur: strict 3x3 maxima are pairwise more than
+    one pixel apart (a 2x2 block holds at most one), and so are the minima.
+    Checked at threshold 0 on the densest patterns and on noise."""
+    rng = np.random.default_rng(7)
+    for h, w in [(8, 8), (9, 7), (64, 64), (33, 65)]:
+        bound = 2 * (-(-h // 2)) * (-(-w // 2))
+        yy, xx = np.mgrid[0:h, 0:w]
+        pats = [
+            rng.standard_normal((h, w)),
+            ((yy % 2 == 0) & (xx % 2 == 0)).astype(float) - ((yy % 2 == 1) & (xx % 2 == 1)),
+            np.cos(np.pi * yy) * np.cos(np.pi * xx),
+        ]
+        for a in pats:
+            ys, xs, vs, thr = O.detect3x3_np(a, thr=0.0)
+            assert len(ys) <= bound, (h, w, len(ys), bound)
+            # maxima alone and minima alone each fit a quarter
+            mx = [(y, x) for y, x in zip(ys, xs) if all(
+                a[y, x] > a[min(max(y + i, 0), h - 1), min(max(x + j, 0), w - 1)]
+                for i in (-1, 0, 1) for j in (-1, 0, 1) if i or j)]
+            assert len(mx) <= (-(-h // 2)) * (-(-w // 2))
