@@ -518,8 +518,8 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   }
   if (fused_fir_col(col_stage, h, w)) {
     // column FIR + Laplacian + NMS in one pass over T (vmf_firpass.cu)
-    rc = firpass_run(T, w, L, w, col_stage->taps, col_stage->n, h, w, lap_scale, frac, det_yx,
-                     det_val, cap, n_det_dev, thr_dev, carry, carry_b, st);
+    rc = firpass_run(T, w, lap_out, w, col_stage->taps, col_stage->n, h, w, lap_scale, frac,
+                     det_yx, det_val, cap, n_det_dev, thr_dev, carry, carry_b, st);
     if (rc) return rc;
     if (blur_out) {
       rc = run_stage<COLS>(col_stage, T, VMF_F32, blur_out, h, w, w, w, carry, carry_b, st);

@@ -469,17 +469,18 @@ __device__ __forceinline__ void fc_tile(
       cand_push_warp(&S.ccount, S.cy, S.cx, S.cv, kFcCand, st, gy, gx, gv, gcap, m,
                      (int)(r0 + q), (int)(c0 + c), vv, mem);
     };
-    if (vec_out && ncol == SH::kOut) {
+    if ((vec_out || !Lout) && ncol == SH::kOut) {
       // a row is kOut / 4 float4 (15 for the 64-column tile): with <= 16 a
-      // warp takes two rows per step (half-warps), else one
+      // warp takes two rows per step (half-warps), else one.  (Lout null:
+      // detections only, L never leaves the tile)
       constexpr int kRpw = SH::kOut / 4 <= 16 ? 2 : 1;
       const int u = kRpw == 2 ? (lane & 15) : lane;
       if (u < SH::kOut / 4) {
-        float *dst = Lout + r0 * ldl + c0 + 4 * u;
+        float *dst = Lout ? Lout + r0 * ldl + c0 + 4 * u : nullptr;
         for (int q = kRpw * wid + (kRpw == 2 ? lane >> 4 : 0); q < nrow;
              q += kRpw * (SH::kThreads / 32)) {
           const float4 v = *reinterpret_cast<const float4 *>(Ls + (q + 1) * SH::kStride + 4 + 4 * u);
-          *reinterpret_cast<float4 *>(dst + q * ldl) = v;
+          if (dst) *reinterpret_cast<float4 *>(dst + q * ldl) = v;
           const float m4 = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
           const float vv[4] = {v.x, v.y, v.z, v.w};
           unsigned m = 0u;
@@ -495,7 +496,7 @@ __device__ __forceinline__ void fc_tile(
       for (int q = wid; q < nrow; q += SH::kThreads / 32)
         for (int cl = lane; cl < ncol; cl += 32) {
           const float v = Ls[(q + 1) * SH::kStride + 4 + cl];
-          Lout[(r0 + q) * ldl + c0 + cl] = v;
+          if (Lout) Lout[(r0 + q) * ldl + c0 + cl] = v;
           const float vv[4] = {v, 0.f, 0.f, 0.f};
           push(fabsf(v) >= th && test(q, cl, v) ? 1u : 0u, q, cl, vv);
         }
@@ -604,8 +605,15 @@ bool firpass_supported(int64_t h, int64_t w, int ntaps) {
   return fc_smem_any(np) + sizeof(FcSmall) + 1024 <= 227 * 1024;
 }
 
+// every candidate is a strict 3x3 extremum of L (at most ceil(h/2) ceil(w/2)
+// maxima and as many minima): the list cannot overflow, so L is stored only
+// on request (the finaliser's full-scan fallback is never needed)
+static int64_t fir_cand_capacity(int64_t h, int64_t w) {
+  return 2 * cdiv(h, 2) * cdiv(w, 2) + 64;
+}
+
 size_t firpass_workspace_bytes(int64_t h, int64_t w) {
-  return 4096 + (size_t)colpass_cand_capacity(h, w) * 12 + 256;
+  return 4096 + (size_t)fir_cand_capacity(h, w) * 12 + 256;
 }
 
 // window rows staged by TMA: nbox boxes of `rows` (<= 256, a multiple of 8)
@@ -664,14 +672,14 @@ int firpass_run(const float *T, int64_t ldt, float *L, int64_t ldl, const double
   fir_plan(&tp, taps, ntaps);
   char *base = (char *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   CandState *cs = (CandState *)base;
-  const int64_t gcap = colpass_cand_capacity(h, w);
+  const int64_t gcap = fir_cand_capacity(h, w);
   int *gy = (int *)(base + 4096);
   int *gx = gy + gcap;
   float *gv = (float *)(gx + gcap);
   cudaMemsetAsync(cs, 0, sizeof(CandState), st);
   {
     Launch g(K_FIR_COLS, st);
-    const int vec = (int)(ldl % 4 == 0 && (uintptr_t)L % 16 == 0);
+    const int vec = (int)(L && ldl % 4 == 0 && (uintptr_t)L % 16 == 0);
     launch_firapply<FcLong>(T, ldt, L, ldl, h, w, tp, lap_scale, frac, cs, gy, gx, gv, gcap, vec,
                             st);
   }
