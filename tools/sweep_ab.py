@@ -32,4 +32,12 @@ for grp in [int(v) for v in os.environ.get("GROUPS", "5,3,2,1").split(",")]:
             tot += a.elapsed_time(b)
         res[f"grp{grp}_conc{conc}"] = round(tot / 20, 4)
         del g
+        if os.environ.get("EAGER"):  # the same step launched eagerly (no graph)
+            tot = 0.0
+            for _ in range(20):
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+                a.record(); step(); b.record(); b.synchronize()
+                tot += a.elapsed_time(b)
+            res[f"eager_grp{grp}_conc{conc}"] = round(tot / 20, 4)
 print(json.dumps(res))
