@@ -510,7 +510,15 @@ __global__ void __maxnreg__(168) sweep_rows_kernel(  // (3 CTAs of 128 threads p
       e2[c == 0 ? 0 : 1] = (ru.ld(n) - xc) + (rd.ld(n) - xc);
     }
 #if VMF_ABL != 3 && VMF_ABL != 6 && VMF_ABL != 7  // (VMF_ABL: timing ablations, tools/row_ablation.sh; results invalid)
-    for (int s = 0; s < ns; ++s) row_carry32<K, KIND>(RC32<K>(sp[s]), U, cfs(s), cbs(s));
+    if (rm.carry_fold) {
+      float2 sd[16];  // the folded sample pairs, shared by every scale's carries
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        sd[t] = make_float2(U[t] + U[kRChunk - 1 - t], U[t] - U[kRChunk - 1 - t]);
+      for (int s = 0; s < ns; ++s) row_carry32_fold<K>(sp[s], sd, cfs(s), cbs(s));
+    } else {
+      for (int s = 0; s < ns; ++s) row_carry32<K, KIND>(RC32<K>(sp[s]), U, cfs(s), cbs(s));
+    }
 #endif
     __syncthreads();  // rows r-1 .. r+1 read; carries, e2, red published
     TLROW(i, 1);
@@ -597,8 +605,8 @@ static int rl_plan(RowLapPlan *P, int64_t h, int64_t w, const double *b, const d
   }
   for (int i = 0; i < k; ++i)
     for (int t = 0; t < kRChunk / 2; ++t) {
-      p.SP[i][t] = (float)(0.5L * (Wt[t][i] + Wt[kRChunk - 1 - t][i]));
-      p.SQ[i][t] = (float)(0.5L * (Wt[kRChunk - 1 - t][i] - Wt[t][i]));
+      p.SPQ[i][t][0] = (float)(0.5L * (Wt[t][i] + Wt[kRChunk - 1 - t][i]));
+      p.SPQ[i][t][1] = (float)(0.5L * (Wt[kRChunk - 1 - t][i] - Wt[t][i]));
     }
   for (int t = 0; t < kRChunk; ++t)
     for (int i = 0; i < k; ++i) p.Wt[t][i] = (float)Wt[t][i];
@@ -830,6 +838,7 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
   // ns slots are the edge CTAs (virtual and border rows of each scale)
   const int rslots = slots > rm.ns ? slots - rm.ns : 1;
   rm.rows_per = (int)cdiv(rm.H, rslots);
+  rm.carry_fold = getenv("VMF_CARRY_REC") ? 0 : 1;
   const int grid = (int)cdiv(rm.H, rm.rows_per) + rm.ns;
   Launch g(K_SWEEP_ROWS, st);
   launch_pdl(sweep_rows_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm,

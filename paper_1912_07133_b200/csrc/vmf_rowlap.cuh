@@ -12,7 +12,9 @@ struct RowLapParams {
   float p, q;           // modal pole (JORDAN: p; CPAIR: p + i q)
   float c[4], cs[4];    // y+ = c . u(n-1); cs = sign * c (the anticausal part)
   float b0, sign;
-  float SP[4][16], SQ[4][16];  // folded 32-sample chunk-carry weights
+  alignas(16) float SPQ[4][16][2];  // folded 32-sample chunk-carry weights (SP, SQ) pairs:
+                       // fwd = sum SP s + SQ d, bwd = sum SP s - SQ d over the
+                       // pairs s = U(t) + U(31-t), d = U(t) - U(31-t)
   float Wt[32][4];      // A^t b, t < 32 (border-term chunk sums)
   float A32[16];        // A^32
   float Apow[5][16];    // A^(32 cpl 2^l): the chunk scan's Kogge-Stone steps
@@ -46,6 +48,7 @@ struct RowLapMulti {
   int ns;
   int64_t H, W;
   int C, rows_per;
+  int carry_fold;              // chunk carries as folded packed-FMA sums (else recursions)
 };
 
 struct BorderScale {   // per scale, for the border kernel
@@ -117,6 +120,47 @@ __device__ __forceinline__ void row_carry32(const RC32<K> &rc, const float (&U)[
   for (int i = 0; i < K; ++i) {
     cf[c * K + i] = f.u[i];
     cb[c * K + i] = b.u[i];
+  }
+}
+
+// Packed fp32 FMA (sm_100 FFMA2: two lanes' worth of FMAs per issue slot):
+// (a.x b.x + c.x, a.y b.y + c.y).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+// The zero-state chunk carries of one scale from the row's folded sample
+// pairs sd[t] = (U(t) + U(31-t), U(t) - U(31-t)) (formed once per row for
+// every scale): (P_i, Q_i) = sum_t (SP_it, SQ_it) * sd[t] as packed FMAs
+// with the (SP, SQ) pairs read two at a time from shared memory;
+// forward carry P + Q, backward P - Q (the recursion's end states, as
+// independent sums instead of a chain).
+template <int K>
+__device__ __forceinline__ void row_carry32_fold(const RowLapParams &p, const float2 (&sd)[16],
+                                                 float *cf, float *cb) {
+  const int c = threadIdx.x;
+  float2 pq[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) pq[i] = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int t = 0; t < 16; t += 2) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const float4 w = *reinterpret_cast<const float4 *>(&p.SPQ[i][t][0]);
+      pq[i] = ffma2(make_float2(w.x, w.y), sd[t], pq[i]);
+      pq[i] = ffma2(make_float2(w.z, w.w), sd[t + 1], pq[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    cf[c * K + i] = pq[i].x + pq[i].y;
+    cb[c * K + i] = pq[i].x - pq[i].y;
   }
 }
 
