@@ -42,6 +42,8 @@ struct CandState {
   int count;                 // candidates appended
   int overflow;              // the global candidate list overflowed
   int ticket;                // CTAs done (the fp32 column scan's last-CTA step)
+  unsigned int bound_bits;   // a lower bound of max |L| known before the apply
+                             // (the fp32 band scan: |L| on the band-boundary rows)
   // decoupled look-back of the finaliser's large-list path: per CTA
   // (status << 62) | count, status 1 = own count, 2 = inclusive prefix
   unsigned long long look[kFinCtas];

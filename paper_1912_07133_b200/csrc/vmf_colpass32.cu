@@ -230,7 +230,8 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
                                                        Col32Params p, float *__restrict__ R,
                                                        float *__restrict__ Cc,
                                                        const float *__restrict__ Vt,
-                                                       const float *__restrict__ Vb) {
+                                                       const float *__restrict__ Vb,
+                                                       CandState *__restrict__ cst) {
   extern __shared__ __align__(16) float ss[];  // [NB][2K+2][32]
   constexpr int Q = 2 * K + 2;
   const int NB = p.NB;
@@ -306,6 +307,31 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
     if (c0 + c < W) Cc[(int64_t)which * W + c0 + c] = (float)a;
   }
   __syncthreads();
+  // V mode: L on the band-boundary rows r1 = 64 b (b >= 1, r1 < H - 1) from the
+  // start states just formed -- the apply's bottom-halo formula,
+  //   L(r1) = c uf(b) + b0 V(r1) + s (c A^-1 ub(b-1) - e1 V(r1)),
+  // exact L values, so their max (a hair below, for the rounding differences
+  // to the apply's own walk) is a lower bound of max |L| that the apply's
+  // candidate threshold can use from its first CTA on
+  if (VM && p.frac > 0.0f) {
+    float bmax = 0.0f;
+    for (int e = tid; e < (NB - 1) * kScan32Cols; e += blockDim.x) {
+      const int b = 1 + e / kScan32Cols, c = e - (b - 1) * kScan32Cols;
+      const int64_t r1 = (int64_t)b * kB32, col = c0 + c;
+      if (r1 >= H - 1 || col >= W) continue;
+      const float v = __ldg(T + r1 * ldt + col);
+      float yp = 0.0f, ym = 0.0f;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        yp = fmaf(p.c[i], ss[(b * Q + i) * kScan32Cols + c], yp);
+        ym = fmaf(p.ci[i], ss[((b - 1) * Q + K + i) * kScan32Cols + c], ym);
+      }
+      const float l = (yp + p.b0 * v + p.sign * fmaf(-p.e1, v, ym)) * p.lsc;
+      bmax = fmaxf(bmax, fabsf(l));
+    }
+    bmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(bmax)));
+    if ((tid & 31) == 0) atomicMax(&cst->bound_bits, __float_as_uint(bmax * 0.999f));
+  }
   // start states back over the carries (q < 2K), coalesced
   if (full) {
     for (int e = tid; e < NB * 2 * K * (kScan32Cols / 4); e += blockDim.x) {
@@ -698,7 +724,8 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
     S.cmax = 0u;
   }
   pdl_wait();  // band start states, Ky and the CandState come from earlier kernels
-  const float gbound = __uint_as_float(st->absmax_bits);
+  // lower bounds of max |L|: the band scan's boundary rows, the earlier CTAs
+  const float gbound = fmaxf(__uint_as_float(st->bound_bits), __uint_as_float(st->absmax_bits));
   Rec32<K, KIND> rf, rbt;
   float ub1[K], mid[K];
 #pragma unroll
@@ -1061,7 +1088,7 @@ static int launch32(const float *T, int64_t ldt, float *L, int64_t ldl, const Co
       cudaFuncSetAttribute(colscan32_kernel<K, VM>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     launch_pdl(colscan32_kernel<K, VM>, dim3((unsigned)cdiv(w, kScan32Cols)), dim3(256), ssm, st,
-               T, ldt, p, R, Cc, vm.vt, vm.vb);
+               T, ldt, p, R, Cc, vm.vt, vm.vb, cs);
   }
   if (VM) {
     Launch g(K_COL_APPLY, st);
