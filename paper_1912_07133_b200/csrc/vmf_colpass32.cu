@@ -239,6 +239,19 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
   const int64_t c0 = (int64_t)blockIdx.x * kScan32Cols;
   const int tid = threadIdx.x;
   __shared__ float es[2][kScan32Cols];
+  // V on the band-boundary rows (the bound below): the row pass wrote it long
+  // before, so the loads go out ahead of the wait for the carries
+  constexpr int kBnd = 16;  // boundary values per thread ((NB - 1) x 32 <= 16 x 256)
+  float vb[kBnd];
+  if (VM && p.frac > 0.0f) {
+#pragma unroll
+    for (int k = 0; k < kBnd; ++k) {
+      const int e = tid + k * (int)blockDim.x;
+      const int b = 1 + e / kScan32Cols, c = e - (b - 1) * kScan32Cols;
+      const int64_t r1 = (int64_t)b * kB32, col = c0 + c;
+      vb[k] = (b < NB && r1 < H - 1 && col < W) ? __ldg(T + r1 * ldt + col) : 0.0f;
+    }
+  }
   pdl_wait();  // records come from the band carries
   const bool full = c0 + kScan32Cols <= W && (W & 3) == 0;
   if (full) {
@@ -315,11 +328,13 @@ __global__ void __launch_bounds__(256) colscan32_kernel(const float *__restrict_
   // candidate threshold can use from its first CTA on
   if (VM && p.frac > 0.0f) {
     float bmax = 0.0f;
-    for (int e = tid; e < (NB - 1) * kScan32Cols; e += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < kBnd; ++k) {
+      const int e = tid + k * (int)blockDim.x;
       const int b = 1 + e / kScan32Cols, c = e - (b - 1) * kScan32Cols;
       const int64_t r1 = (int64_t)b * kB32, col = c0 + c;
-      if (r1 >= H - 1 || col >= W) continue;
-      const float v = __ldg(T + r1 * ldt + col);
+      if (b >= NB || r1 >= H - 1 || col >= W) continue;
+      const float v = vb[k];
       float yp = 0.0f, ym = 0.0f;
 #pragma unroll
       for (int i = 0; i < K; ++i) {
