@@ -49,6 +49,7 @@ struct RowLapMulti {
   int64_t H, W;
   int C, rows_per;
   int carry_fold;              // chunk carries as folded packed-FMA sums (else recursions)
+  int store_inline;            // V stored in 8-sample groups during the forward walk
 };
 
 struct BorderScale {   // per scale, for the border kernel
@@ -276,6 +277,43 @@ __device__ __forceinline__ void row_walks32(const RC32<K> &rc, int C, const floa
   }
   if (c == 0) V[0] += dx2[0];
   if (c == C - 1) V[kRChunk - 1] -= dx2[1];
+}
+
+// row_walks32 with V leaving as it is produced: each group of 8 outputs goes
+// out as one 256-bit store, so the stores spread over the forward walk and
+// release their registers long before the next scale reuses them
+template <int K, int KIND>
+__device__ __forceinline__ void row_walks32_store(const RC32<K> &rc, int C,
+                                                  const float (&U)[kRChunk], const float *cf,
+                                                  const float *cb, const float *dx2, float *dst,
+                                                  bool live, uint64_t pol) {
+  const int c = threadIdx.x;
+  float park[kRChunk];
+  {
+    Rec32<K, KIND> rb;
+#pragma unroll
+    for (int i = 0; i < K; ++i) rb.u[i] = cb[c * K + i];
+#pragma unroll
+    for (int t = kRChunk - 1; t >= 0; --t) {
+      park[t] = rb.out_from(rc.cs, rc.b0 * U[t]);
+      rb.step(rc, U[t]);
+    }
+  }
+  Rec32<K, KIND> rf;
+#pragma unroll
+  for (int i = 0; i < K; ++i) rf.u[i] = cf[c * K + i];
+#pragma unroll
+  for (int q = 0; q < kRChunk / 8; ++q) {
+    float v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      v[t] = rf.out_from(rc.c, park[8 * q + t]);
+      rf.step(rc, U[8 * q + t]);
+    }
+    if (q == 0 && c == 0) v[0] += dx2[0];
+    if (q == kRChunk / 8 - 1 && c == C - 1) v[7] -= dx2[1];
+    if (live) st_v8_hint(dst + 8 * q, v, pol);
+  }
 }
 
 template <int K, int KIND>
