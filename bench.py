@@ -400,12 +400,13 @@ def run_ours(args):
     x = torch.from_numpy(frame).to(dev)
     iir = [detect.make_stage(cat[n]) for n in IIR]
     fir = [detect.make_stage(cat[n]) for n in FIR]
-    lap = torch.empty((h, w), dtype=torch.float32, device=dev)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
     def one_scale(stg, frac=0.5):
-        detect._fused(x, _lib.VMF_F32, stg, stg, 1.0, frac, None, lap, 1 << 18, False)
+        # the detect path of one scale (blur_laplacian_detect's device part):
+        # detections only, L is not asked for
+        detect._fused(x, _lib.VMF_F32, stg, stg, 1.0, frac, None, None, 1 << 18, False)
 
     # detection buffers of every scale, allocated up front (nothing is
     # allocated on the side streams inside a graph capture)
