@@ -294,9 +294,12 @@ __global__ void __maxnreg__(168) sweep_rows_kernel(  // (3 CTAs of 128 threads p
   // run time (broadcast LDS instead of constant-cache misses)
   RowLapParams *sp = reinterpret_cast<RowLapParams *>(cfb + (size_t)rm.ns * 2 * blockDim.x * K);
   {
-    const int nw = (int)(rm.ns * sizeof(RowLapParams) / sizeof(int));
-    const int *src = reinterpret_cast<const int *>(&rm.s[0]);
-    int *dst = reinterpret_cast<int *>(sp);
+    // 16-byte words: a divergent constant-bank read costs one transaction per
+    // distinct address, so wide words mean fewer of them
+    static_assert(sizeof(RowLapParams) % 16 == 0, "RowLapParams: whole 16-byte words");
+    const int nw = (int)(rm.ns * sizeof(RowLapParams) / sizeof(int4));
+    const int4 *src = reinterpret_cast<const int4 *>(&rm.s[0]);
+    int4 *dst = reinterpret_cast<int4 *>(sp);
     for (int e = threadIdx.x; e < nw; e += blockDim.x) dst[e] = src[e];
   }
   auto cfs = [&](int s) { return cfb + (size_t)s * 2 * blockDim.x * K; };
@@ -616,8 +619,6 @@ static int rl_plan(RowLapPlan *P, int64_t h, int64_t w, const double *b, const d
       p.SPQ[i][t][0] = (float)(0.5L * (Wt[t][i] + Wt[kRChunk - 1 - t][i]));
       p.SPQ[i][t][1] = (float)(0.5L * (Wt[kRChunk - 1 - t][i] - Wt[t][i]));
     }
-  for (int t = 0; t < kRChunk; ++t)
-    for (int i = 0; i < k; ++i) p.Wt[t][i] = (float)Wt[t][i];
   {  // c A^-1: the right border's vector of the last chunk
     ld At[16], x[4];
     for (int i = 0; i < k; ++i)

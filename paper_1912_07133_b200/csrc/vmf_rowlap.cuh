@@ -15,7 +15,6 @@ struct RowLapParams {
   alignas(16) float SPQ[4][16][2];  // folded 32-sample chunk-carry weights (SP, SQ) pairs:
                        // fwd = sum SP s + SQ d, bwd = sum SP s - SQ d over the
                        // pairs s = U(t) + U(31-t), d = U(t) - U(31-t)
-  float Wt[32][4];      // A^t b, t < 32 (border-term chunk sums)
   float A32[16];        // A^32
   float Apow[5][16];    // A^(32 cpl 2^l): the chunk scan's Kogge-Stone steps
   float Iss[4];         // (I - A)^-1 b
