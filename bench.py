@@ -535,13 +535,18 @@ def run_ours(args):
     ne2e = max(args.steps, 64)
     detect.stream_sweep([host] * ne2e, stages_obj)
     torch.cuda.synchronize()
+    # median of 3 timed streams (a single 64-frame stream varied by ~4 % run
+    # to run on the host side)
+    e2e_runs = []
+    for _ in range(3):
+        barrier(ws)
+        t0 = time.perf_counter()
+        res = detect.stream_sweep([host] * ne2e, stages_obj)
+        torch.cuda.synchronize()
+        e2e_runs.append(max_over_ranks(time.perf_counter() - t0, ws, dev))
+        assert len(res) == ne2e
     barrier(ws)
-    t0 = time.perf_counter()
-    res = detect.stream_sweep([host] * ne2e, stages_obj)
-    torch.cuda.synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - t0, ws, dev)
-    barrier(ws)
-    assert len(res) == ne2e
+    e2e_s = sorted(e2e_runs)[1]
     d2h = len(iir) * (16 + 12 * 4096)  # per frame: header + first 4096 detections per scale
     e2e = mpx * len(iir) * ws * ne2e / e2e_s
     # the same without overlap: one detect_sweep call per frame (upload,
@@ -619,7 +624,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(frame.nbytes),
                     "d2h_bytes_per_step": int(d2h),
                     "api": "detect.stream_sweep over K pinned frames (uploads overlapped)",
-                    "frames": ne2e,
+                    "frames": ne2e, "timed_streams": "median of 3",
                     "single_frame_value": round(e2e_single, 1),
                     "single_frame_api": "detect.detect_sweep per frame (no overlap)",
                     "h2d_gbs": round(h2d_gbs, 1),
