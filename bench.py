@@ -794,52 +794,44 @@ def other_configs(cat, flush, stream):
     # config 3 with the scale-space rule: sigma^2-normalised L of the 5 IIR
     # scales into one stack, 3x3x3 NMS over it (detect.scale_space_detect's
     # device part; the per-scale passes on concurrent streams)
-    from paper_1912_07133_b200.engine import _ptr
 
     f3 = synth.config3_frame(4096)
     x3 = torch.from_numpy(f3).cuda()
     sig3 = (2, 4, 8, 16, 32)
     st3 = [detect.make_stage(cat[f"rp{s}"]) for s in sig3]
     stack = torch.empty((5, 4096, 4096), dtype=torch.float32, device=x3.device)
-    dummy = [(torch.empty((1, 2), dtype=torch.int32, device=x3.device),
-              torch.empty(1, dtype=torch.float32, device=x3.device),
-              torch.empty(2, dtype=torch.int64, device=x3.device)) for _ in sig3]
-    L3 = _lib.lib()
-    ws3 = torch.empty(L3.vmf_detect3x3x3_workspace_bytes(5, 4096, 4096), dtype=torch.uint8,
-                      device=x3.device)
+    cands3 = (torch.empty((5, detect.SS_CAND_CAP, 2), dtype=torch.int32, device=x3.device),
+              torch.empty((5, detect.SS_CAND_CAP), dtype=torch.float32, device=x3.device),
+              torch.empty((5, 2), dtype=torch.int64, device=x3.device))
     det3 = torch.empty((1 << 18, 3), dtype=torch.int32, device=x3.device)
     val3 = torch.empty(1 << 18, dtype=torch.float32, device=x3.device)
     scal3 = torch.zeros(2, dtype=torch.int64, device=x3.device)
 
-    def ss_step():
-        detect._sweep_launch(x3, _lib.VMF_F32, st3, 0.0, [float(s) ** 2 for s in sig3], 0, dummy,
-                             laps=[stack[i] for i in range(5)])
-        _lib.check(L3.vmf_detect3x3x3(_ptr(stack), 5, 4096, 4096, 4096, 4096 * 4096, 0.5,
-                                      _ptr(det3), _ptr(val3), 1 << 18, _ptr(scal3),
-                                      scal3.data_ptr() + 8, None, _ptr(ws3), ws3.numel(),
-                                      torch.cuda.current_stream().cuda_stream))
+    def ss_step():  # the stack planes + per-scale candidates, then the 3x3x3 rule on them
+        detect._scale_space_launch(x3, _lib.VMF_F32, st3, sig3, 0.5, stack, cands3, det3, val3,
+                                   scal3)
 
     ms3 = graph_ms(ss_step)
+    assert int(scal3[0].item()) >= 0, "a scale's candidate list overflowed"
     out["config3_scale_space"] = {
         "workload": "4096x4096 fp32, 5 repeated-pole scales, sigma^2-normalised L stack, "
                     "3x3x3 NMS at 0.5 max|stack|",
         "mpx_s_per_scale": round(5 * 4096 * 4096 / 1e6 / (ms3 / 1e3), 1),
         "ms_per_sweep": round(ms3, 4)}
-    del x3, stack, ws3
+    del x3, stack, cands3
 
     # config 5: 8192^2 fp32, Butterworth sigma 48 (K=2) vs colored SG 385 taps
     f5 = synth.config5_frame(8192)
     x5 = torch.from_numpy(f5).cuda()
-    lap5 = torch.empty_like(x5)
     c5 = {"workload": "8192x8192 fp32, bw48 IIR vs sg38.4 (385-tap) FIR, fused blur + "
                       "Laplacian + 3x3 NMS"}
     for name in ("bw48", "sg38.4"):
         stg = detect.make_stage(cat[name])
-        ms = graph_ms(lambda: detect._fused(x5, _lib.VMF_F32, stg, stg, 1.0, 0.5, None, lap5,
+        ms = graph_ms(lambda: detect._fused(x5, _lib.VMF_F32, stg, stg, 1.0, 0.5, None, None,
                                             1 << 18, False))
         c5[name + "_mpx_s"] = round(8192 * 8192 / 1e6 / (ms / 1e3), 1)
     out["config5"] = c5
-    del x5, lap5
+    del x5
     return out
 
 

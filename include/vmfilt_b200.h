@@ -178,6 +178,20 @@ int vmf_detect3x3x3_absmax(const float *n, int64_t ns, int64_t h, int64_t w, int
                            int32_t *det_syx, float *det_val, int64_t cap, int64_t *n_det_dev,
                            float *thr_dev, int64_t *n_det_host, void *ws, size_t ws_bytes,
                            void *stream);
+/* The same rule from the candidate lists of the stack's fused column passes
+ * (vmf_sweep_detect with lap_out = plane s and frac > 0: plane s's strict
+ * 3x3 extrema above frac * max|N_s|, sorted by (y, x); cand_yx[s][i][2],
+ * cand_val[s][i] with cand_stride entries per scale, cand_scal[s] = {count,
+ * threshold bits}): the stack threshold is the largest scale threshold and a
+ * candidate is kept when it also clears the 9 + 9 adjacent-scale neighbours
+ * -- the exact result of vmf_detect3x3x3 without a pass over the stack.
+ * *n_det_dev = -1 when a scale's list was cut short (count > cand_stride):
+ * run vmf_detect3x3x3 then. */
+int vmf_detect3x3x3_cands(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ldn,
+                          int64_t plane_stride, const int32_t *cand_yx, const float *cand_val,
+                          int64_t cand_stride, const int64_t *cand_scal, int32_t *det_syx,
+                          float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev,
+                          void *stream);
 int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w,
                     int64_t ldn, int64_t plane_stride, float frac,
                     int32_t *det_syx, float *det_val, int64_t cap,

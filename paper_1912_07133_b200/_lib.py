@@ -58,6 +58,8 @@ _PROTOS = {
     "vmf_detect3x3x3_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "vmf_detect3x3x3": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, C.c_float, _vp, _vp,
                                   _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "vmf_detect3x3x3_cands": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
+                                        _vp, _vp, _i64, _vp, _vp, _vp]),
     "vmf_detect3x3x3_absmax": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, C.c_float, _vp,
                                          _vp, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "vmf_launch_count": (C.c_longlong, []),

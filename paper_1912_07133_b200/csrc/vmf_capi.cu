@@ -157,6 +157,21 @@ int vmf_detect3x3x3(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ld
                 thr_dev, n_det_host, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int vmf_detect3x3x3_cands(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ldn,
+                          int64_t plane_stride, const int32_t *cand_yx, const float *cand_val,
+                          int64_t cand_stride, const int64_t *cand_scal, int32_t *det_syx,
+                          float *det_val, int64_t cap, int64_t *n_det_dev, float *thr_dev,
+                          void *stream) {
+  if (ns < 1 || ns > 64 || h < 1 || w < 1) return fail(VMF_EVALUE, "stack must be 3-D and non-empty");
+  if (ldn < w || plane_stride < h * ldn) return fail(VMF_EVALUE, "bad stack strides");
+  if (!cand_yx || !cand_val || !cand_scal || cand_stride < 1 || !n_det_dev)
+    return fail(VMF_EVALUE, "candidate lists missing");
+  if (cap > 0 && (!det_syx || !det_val)) return fail(VMF_EVALUE, "detection buffers are NULL");
+  return detect3x3x3_cands(n, ldn, plane_stride, (int)ns, h, w, cand_yx, cand_val, cand_stride,
+                           cand_scal, det_syx, det_val, cap, n_det_dev, thr_dev,
+                           (cudaStream_t)stream);
+}
+
 int vmf_detect3x3x3_absmax(const float *n, int64_t ns, int64_t h, int64_t w, int64_t ldn,
                            int64_t plane_stride, float frac, const float *absmax_dev,
                            int32_t *det_syx, float *det_val, int64_t cap, int64_t *n_det_dev,

@@ -276,6 +276,115 @@ __global__ void absmax_kernel(const float *__restrict__ l, int64_t ld, int64_t p
 }
 
 // ---------------------------------------------------------------------------
+// the scale-space rule from per-scale candidates: each scale's fused column
+// pass wrote its plane of the stack and listed its strict 3x3 extrema above
+// frac * its own max (sorted by (y, x)); the stack threshold is the largest
+// of those thresholds, and a 3x3x3 detection is one of those candidates that
+// also clears the adjacent planes' 9 + 9 neighbours and the stack threshold
+// -- so only the candidates are tested, in (s, y, x) order, by one CTA
+// (block-wide ordered compaction); no pass over the whole stack.
+// ---------------------------------------------------------------------------
+constexpr int kCandThreads = 1024;
+__global__ void __launch_bounds__(kCandThreads) detect3x3x3_cands_kernel(
+    const float *__restrict__ l, int64_t ld, int64_t plane, int ns, int64_t h, int64_t w,
+    const int32_t *__restrict__ cyx, const float *__restrict__ cval, int64_t cstride,
+    const int64_t *__restrict__ cscal, int32_t *__restrict__ det, float *__restrict__ dval,
+    int64_t cap, int64_t *__restrict__ n_det, float *__restrict__ thr_out) {
+  __shared__ int wsum[kCandThreads / 32];
+  __shared__ float sthr;
+  __shared__ int overflow;
+  pdl_wait();  // the column passes' candidate lists and the stack
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    float t = 0.0f;
+    int ov = 0;
+    for (int s = 0; s < ns; ++s) {
+      t = fmaxf(t, __int_as_float((int)(cscal[2 * s + 1] & 0xffffffffll)));
+      ov |= cscal[2 * s] > cstride;
+    }
+    sthr = t;
+    overflow = ov;
+    if (thr_out) *thr_out = t;
+  }
+  __syncthreads();
+  if (overflow) {  // a list was cut short: the caller runs the full-stack rule
+    if (tid == 0) *n_det = -1;
+    return;
+  }
+  const float thr = sthr;
+  int64_t base = 0;
+  for (int s = 0; s < ns; ++s) {
+    const int64_t n = cscal[2 * s];
+    for (int64_t q0 = 0; q0 < n; q0 += kCandThreads) {
+      const int64_t q = q0 + tid;
+      int keep = 0;
+      int32_t y = 0, x = 0;
+      float v = 0.0f;
+      if (q < n) {
+        y = cyx[(s * cstride + q) * 2];
+        x = cyx[(s * cstride + q) * 2 + 1];
+        v = cval[s * cstride + q];
+        if (fabsf(v) >= thr) {
+          bool gt = v > 0.0f, lt = v < 0.0f;  // (the in-plane test already passed)
+          for (int t = s - 1; t <= s + 1; t += 2) {
+            if (t < 0 || t >= ns) continue;
+            const float *Q = l + (int64_t)t * plane;
+#pragma unroll
+            for (int di = -1; di <= 1; ++di)
+#pragma unroll
+              for (int dj = -1; dj <= 1; ++dj) {
+                const float u = Q[(int64_t)(y + di) * ld + x + dj];
+                gt &= v > u;
+                lt &= v < u;
+              }
+          }
+          keep = (gt && v >= thr) || (lt && -v >= thr);
+        }
+      }
+      // ordered block compaction
+      int inc = keep;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (lane == 31) wsum[wid] = inc;
+      __syncthreads();
+      if (wid == 0) {
+        int v2 = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, v2, o);
+          if (lane >= o) v2 += t;
+        }
+        wsum[lane] = v2;
+      }
+      __syncthreads();
+      const int64_t pos = base + (wid ? wsum[wid - 1] : 0) + inc - keep;
+      if (keep && pos < cap) {
+        det[3 * pos] = s;
+        det[3 * pos + 1] = y;
+        det[3 * pos + 2] = x;
+        dval[pos] = v;
+      }
+      base += wsum[kCandThreads / 32 - 1];
+      __syncthreads();
+    }
+  }
+  if (tid == 0) *n_det = base;
+}
+
+int detect3x3x3_cands(const float *l, int64_t ld, int64_t plane, int ns, int64_t h, int64_t w,
+                      const int32_t *cyx, const float *cval, int64_t cstride,
+                      const int64_t *cscal, int32_t *det, float *dval, int64_t cap,
+                      int64_t *n_det, float *thr_out, cudaStream_t st) {
+  Launch g(K_NMS_WRITE, st);
+  launch_pdl(detect3x3x3_cands_kernel, dim3(1), dim3(kCandThreads), 0, st, l, ld, plane, ns, h, w,
+             cyx, cval, cstride, cscal, det, dval, cap, n_det, thr_out);
+  return cuda_status("scale-space detect (candidates)");
+}
+
+// ---------------------------------------------------------------------------
 // host
 // ---------------------------------------------------------------------------
 static int sm_count() {

@@ -15,6 +15,12 @@ float *detect_absmax_slot(void *ws);
 int detect_if(const float *l, int64_t ld, int64_t h, int64_t w, float frac, float *absmax,
               const int *gate, int32_t *det_yx, float *det_val, int64_t cap, int64_t *n_det_dev,
               float *thr_dev, void *ws, size_t ws_bytes, cudaStream_t st);
+// the scale-space rule from the per-scale candidate lists of the fused
+// column passes (see vmf_detect3x3x3_cands); *n_det = -1 when a list was cut
+int detect3x3x3_cands(const float *l, int64_t ld, int64_t plane, int ns, int64_t h, int64_t w,
+                      const int32_t *cyx, const float *cval, int64_t cstride,
+                      const int64_t *cscal, int32_t *det, float *dval, int64_t cap,
+                      int64_t *n_det, float *thr_out, cudaStream_t st);
 int detect(const float *l, int64_t ld, int64_t plane, int64_t ns, int64_t h, int64_t w,
            float frac, bool have_absmax, int32_t *det_idx, int idx_stride, float *det_val,
            int64_t cap, int64_t *n_det_dev, float *thr_dev, int64_t *n_det_host, void *ws,

@@ -296,33 +296,66 @@ def detect_sweep(img, stages, frac: float = 0.5, lap_scales=None, cap: int = 1 <
     return out
 
 
+SS_CAND_CAP = 1 << 16  # per-scale candidate list of the scale-space rule
+
+
+def _scale_space_launch(x, code, stages, sigmas, frac, stack, cands, det, val, scal):
+    """Device part of scale_space_detect (frac > 0): the sweep writes each
+    scale's plane of the sigma^2-normalised stack and lists its strict 3x3
+    extrema above frac * that plane's max (the fused column pass's own
+    detection), then vmf_detect3x3x3_cands keeps the candidates that clear
+    the adjacent planes and the stack threshold.  scal[0] = -1 means a list
+    was cut short (the caller runs the full-stack rule)."""
+    ns = len(stages)
+    h, w = x.shape
+    cyx, cval, cscal = cands
+    _sweep_launch(x, code, stages, frac, [float(sg) ** 2 for sg in sigmas], cyx.shape[1],
+                  [(cyx[s], cval[s], cscal[s]) for s in range(ns)],
+                  laps=[stack[s] for s in range(ns)])
+    _lib.check(_lib.lib().vmf_detect3x3x3_cands(
+        _ptr(stack), ns, h, w, w, h * w, _ptr(cyx), _ptr(cval), cyx.shape[1], _ptr(cscal),
+        _ptr(det), _ptr(val), det.shape[0], _ptr(scal), scal.data_ptr() + 8, _stream()))
+
+
 def scale_space_detect(img, stages, sigmas, frac: float = 0.5, cap: int = 1 << 18,
                        return_stack: bool = False):
     """Config-3 scale sweep: per scale the fused blur + Laplacian with
-    lap_scale = sigma^2 into one stack, then 3x3x3 NMS over the stack."""
+    lap_scale = sigma^2 into one stack, then 3x3x3 NMS over the stack
+    (frac > 0: from the column passes' own candidate lists; else, and when a
+    list overflows, over the whole stack)."""
     if len(stages) != len(sigmas) or not stages:
         raise ValueError("need one stage per sigma")
     x, kind, code = _as_image(img)
     h, w = x.shape
     ns = len(stages)
+    stg = [_Stage(st) for st in stages]
     stack = torch.empty((ns, h, w), dtype=torch.float32, device=x.device)
-    dummy = [(torch.empty((1, 2), dtype=torch.int32, device=x.device),
-              torch.empty(1, dtype=torch.float32, device=x.device),
-              torch.empty(2, dtype=torch.int64, device=x.device)) for _ in range(ns)]
-    _sweep_launch(x, code, [_Stage(st) for st in stages], 0.0, [float(sg) ** 2 for sg in sigmas],
-                  0, dummy, laps=[stack[s] for s in range(ns)])
-    L = _lib.lib()
-    nbytes = L.vmf_detect3x3x3_workspace_bytes(ns, h, w)
-    ws = _workspace(nbytes)
     cap = int(cap)
     det = torch.empty((max(cap, 1), 3), dtype=torch.int32, device=x.device)
     val = torch.empty((max(cap, 1),), dtype=torch.float32, device=x.device)
     scal = torch.zeros(2, dtype=torch.int64, device=x.device)
-    n_host = C.c_int64(0)
-    _lib.check(L.vmf_detect3x3x3(_ptr(stack), ns, h, w, w, h * w, float(frac), _ptr(det),
-                                 _ptr(val), cap, _ptr(scal), scal.data_ptr() + 8,
-                                 C.byref(n_host), _ptr(ws), ws.numel(), _stream()))
-    n = n_host.value
+    L = _lib.lib()
+    n = -1
+    if frac > 0:
+        cands = (torch.empty((ns, SS_CAND_CAP, 2), dtype=torch.int32, device=x.device),
+                 torch.empty((ns, SS_CAND_CAP), dtype=torch.float32, device=x.device),
+                 torch.empty((ns, 2), dtype=torch.int64, device=x.device))
+        _scale_space_launch(x, code, stg, sigmas, float(frac), stack, cands, det, val, scal)
+        n = int(scal[0].item())
+    if n < 0:  # the full-stack rule
+        if frac <= 0:
+            dummy = [(torch.empty((1, 2), dtype=torch.int32, device=x.device),
+                      torch.empty(1, dtype=torch.float32, device=x.device),
+                      torch.empty(2, dtype=torch.int64, device=x.device)) for _ in range(ns)]
+            _sweep_launch(x, code, stg, 0.0, [float(sg) ** 2 for sg in sigmas], 0, dummy,
+                          laps=[stack[s] for s in range(ns)])
+        nbytes = L.vmf_detect3x3x3_workspace_bytes(ns, h, w)
+        ws = _workspace(nbytes)
+        n_host = C.c_int64(0)
+        _lib.check(L.vmf_detect3x3x3(_ptr(stack), ns, h, w, w, h * w, float(frac), _ptr(det),
+                                     _ptr(val), cap, _ptr(scal), scal.data_ptr() + 8,
+                                     C.byref(n_host), _ptr(ws), ws.numel(), _stream()))
+        n = n_host.value
     thr = float(scal[1:2].view(torch.float32)[0].item())
     m = min(n, cap)
     d, v = det[:m], val[:m]

@@ -214,22 +214,67 @@ def test_config2_fir(cat):
     assert r["sg3.2"]["n_gpu"] > 0 and r["g4_k16"]["n_gpu"] > 0
 
 
+@pytest.mark.parametrize("frac", [0.5, 0.01])
 @pytest.mark.parametrize("family", ["iir", "fir"])
-def test_config3_scale_space(cat, family):
+def test_config3_scale_space(cat, family, frac):
+    """(At frac 0.5 the sigma 32 plane's edge values, which set the stack
+    maximum, leave no 3x3x3 extremum in this frame; 0.01 keeps hundreds.)"""
     D = _D()
     x = synth.config3_frame(2048)  # quarter-area instance; the 4096^2 run is in bench
     spec = synth.CONFIG_STAGES[3]
     stages = [cat[n] for n in spec[family]]
     sig = spec["sigmas"]
-    dets, stack = D.scale_space_detect(x, stages, sig, frac=0.5, return_stack=True)
+    dets, stack = D.scale_space_detect(x, stages, sig, frac=frac, return_stack=True)
     N = np.stack([O.laplacian(O.blur(x, s)) * (g * g) for s, g in zip(stages, sig)])
     for i in range(len(sig)):
         e = max_rel_err(stack[i], N[i])
         assert e < TOL_REL, (family, sig[i], e)
-    ss, ys, xs, vs, thr = O.detect3x3x3(N, 0.5)
+    ss, ys, xs, vs, thr = O.detect3x3x3(N, frac)
+    if frac < 0.1:
+        assert len(ss) > 100 and dets.count > 100, (len(ss), dets.count)
     exempt, bad = compare_blobs(dets.as_set(), set(zip(ss.tolist(), ys.tolist(), xs.tolist())),
                                 N, thr, stack=True)
     assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("family", ["iir", "fir"])
+def test_scale_space_candidates_equal_full_stack_rule(cat, family, monkeypatch):
+    """The scale-space rule from the column passes' candidate lists
+    (vmf_detect3x3x3_cands) returns exactly what the full-stack rule
+    (vmf_detect3x3x3 over the whole stack) returns -- same detections, values,
+    order and threshold -- and a list cut short falls back to the full rule."""
+    D = _D()
+    x = synth.config3_frame(2048)
+    spec = synth.CONFIG_STAGES[3]
+    stages = [cat[n] for n in spec[family]]
+    sig = spec["sigmas"]
+    frac = 0.01  # (the sigma 32 plane's edge values set the stack max: none clear 0.1 of it)
+    fast, stack = D.scale_space_detect(x, stages, sig, frac=frac, return_stack=True)
+    from paper_1912_07133_b200 import _lib, detect
+    import ctypes as C
+    ns, (h, w) = len(sig), x.shape
+    st = torch.from_numpy(stack).cuda()
+    L = _lib.lib()
+    ws = torch.empty(L.vmf_detect3x3x3_workspace_bytes(ns, h, w), dtype=torch.uint8, device="cuda")
+    det = torch.empty((1 << 18, 3), dtype=torch.int32, device="cuda")
+    val = torch.empty(1 << 18, dtype=torch.float32, device="cuda")
+    scal = torch.zeros(2, dtype=torch.int64, device="cuda")
+    n_host = C.c_int64(0)
+    _lib.check(L.vmf_detect3x3x3(st.data_ptr(), ns, h, w, w, h * w, frac, det.data_ptr(),
+                                 val.data_ptr(), 1 << 18, scal.data_ptr(), scal.data_ptr() + 8,
+                                 C.byref(n_host), ws.data_ptr(), ws.numel(),
+                                 torch.cuda.current_stream().cuda_stream))
+    n = n_host.value
+    assert fast.count == n > 0
+    assert fast.threshold == float(scal[1:2].view(torch.float32)[0].item())
+    d = det[:n].cpu().numpy()
+    np.testing.assert_array_equal(np.asarray(fast.s), d[:, 0])
+    np.testing.assert_array_equal(np.asarray(fast.y), d[:, 1])
+    np.testing.assert_array_equal(np.asarray(fast.x), d[:, 2])
+    np.testing.assert_array_equal(np.asarray(fast.value), val[:n].cpu().numpy())
+    monkeypatch.setattr(detect, "SS_CAND_CAP", 4)  # every list overflows: the full rule
+    slow = D.scale_space_detect(x, stages, sig, frac=frac)
+    assert slow.as_set() == fast.as_set() and slow.count == fast.count
 
 
 def test_config4_u16_stream(cat):
