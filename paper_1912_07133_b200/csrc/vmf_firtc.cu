@@ -608,73 +608,84 @@ __global__ void __launch_bounds__(kThreads, 1) firtc_mma_kernel(
 // machinery (per-CTA buffer, global list) to the sorting finaliser.
 // ---------------------------------------------------------------------------
 constexpr int kNmsR = 32, kNmsC = 128, kNmsCand = 256;
+constexpr int kNmsP = kNmsC + 8;  // tile pitch: halo column 3, interior 4 .. 131, halo 132
 __global__ void __launch_bounds__(256) firtc_nms_kernel(const float *__restrict__ L, int64_t ldl,
                                                         int H, int W, float frac,
                                                         CandState *__restrict__ st,
                                                         int *__restrict__ gy, int *__restrict__ gx,
                                                         float *__restrict__ gv, int gcap, int vec) {
-  __shared__ float t[kNmsR + 2][kNmsC + 3];
+  __shared__ __align__(16) float t[kNmsR + 2][kNmsP];
   __shared__ int cy[kNmsCand], cx[kNmsCand];
   __shared__ float cv[kNmsCand];
   __shared__ int ccount;
   const int r0 = blockIdx.y * kNmsR, c0 = blockIdx.x * kNmsC;
-  if (threadIdx.x == 0) ccount = 0;
+  const int tid = threadIdx.x;
+  if (tid == 0) ccount = 0;
   pdl_wait();  // L and its max come from the column pass
   const float thr = frac * __uint_as_float(st->absmax_bits);
-  // tile rows r0-1 .. r0+32 (clamped), columns c0-1 .. c0+128: the 128
-  // interior columns as float4 when the rows allow, the two halo columns apart
+  // tile rows r0-1 .. r0+32 (clamped): the 128 interior columns by 16-byte
+  // asynchronous copies (all in flight together), the two halo columns apart
   const bool v4 = vec && c0 + kNmsC <= W;
-  for (int e = threadIdx.x; e < (kNmsR + 2) * (kNmsC / 4); e += blockDim.x) {
+  for (int e = tid; e < (kNmsR + 2) * (kNmsC / 4); e += blockDim.x) {
     const int tr = e >> 5, q = e & 31;
     int r = r0 - 1 + tr;
     r = r < 0 ? 0 : (r >= H ? H - 1 : r);
     const float *row = L + (int64_t)r * ldl;
     if (v4) {
-      const float4 x = __ldg(reinterpret_cast<const float4 *>(row + c0) + q);
-      t[tr][1 + 4 * q] = x.x;
-      t[tr][2 + 4 * q] = x.y;
-      t[tr][3 + 4 * q] = x.z;
-      t[tr][4 + 4 * q] = x.w;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(&t[tr][4 + 4 * q]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(row + c0 + 4 * q));
     } else {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = c0 + 4 * q + u;
-        t[tr][1 + 4 * q + u] = __ldg(row + (c < W ? c : W - 1));
+        t[tr][4 + 4 * q + u] = __ldg(row + (c < W ? c : W - 1));
       }
     }
   }
-  if (threadIdx.x < 2 * (kNmsR + 2)) {
-    const int tr = threadIdx.x >> 1, side = threadIdx.x & 1;
+  if (v4) asm volatile("cp.async.commit_group;\n" ::);
+  if (tid < 2 * (kNmsR + 2)) {
+    const int tr = tid >> 1, side = tid & 1;
     int r = r0 - 1 + tr;
     r = r < 0 ? 0 : (r >= H ? H - 1 : r);
     int c = side ? c0 + kNmsC : c0 - 1;
     c = c < 0 ? 0 : (c >= W ? W - 1 : c);
-    t[tr][side ? kNmsC + 1 : 0] = __ldg(L + (int64_t)r * ldl + c);
+    t[tr][side ? 4 + kNmsC : 3] = __ldg(L + (int64_t)r * ldl + c);
   }
+  if (v4) asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
-  const int j = threadIdx.x & (kNmsC - 1);
-  const int cc = c0 + j;
-  for (int q = threadIdx.x >> 7; q < kNmsR; q += 2) {
+  // warp w takes rows w, w+8, w+16, w+24; a lane 4 adjacent columns: the
+  // warp votes on each row's 128 values before any neighbour is read
+  const int w = tid >> 5, lane = tid & 31;
+  for (int q = w; q < kNmsR; q += 8) {
     const int r = r0 + q;
-    const float v = t[q + 1][j + 1];
+    const float4 x = *reinterpret_cast<const float4 *>(&t[q + 1][4 + 4 * lane]);
+    const float vv[4] = {x.x, x.y, x.z, x.w};
+    const float m4 = fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w)));
+    const bool live = r >= 1 && r <= H - 2 && m4 >= thr;
+    if (!__any_sync(0xffffffffu, live)) continue;  // (warp-uniform)
     unsigned m = 0u;
-    if (fabsf(v) >= thr && r >= 1 && r <= H - 2 && cc >= 1 && cc <= W - 2) {
-      bool gt = true, lt = true;
+    if (live) {
 #pragma unroll
-      for (int di = 0; di < 3; ++di)
+      for (int i = 0; i < 4; ++i) {
+        const int cc = c0 + 4 * lane + i, tc = 4 + 4 * lane + i;
+        const float v = vv[i];
+        if (!(fabsf(v) >= thr) || cc < 1 || cc > W - 2) continue;
+        bool gt = true, lt = true;
 #pragma unroll
-        for (int dj = 0; dj < 3; ++dj) {
-          if (di == 1 && dj == 1) continue;
-          const float w = t[q + di][j + dj];
-          gt &= v > w;
-          lt &= v < w;
-        }
-      // a maximum counts when positive, a minimum when negative (|v| >= thr
-      // alone would admit a positive local minimum)
-      m = (gt && v >= thr) || (lt && -v >= thr) ? 1u : 0u;
+        for (int di = 0; di < 3; ++di)
+#pragma unroll
+          for (int dj = -1; dj <= 1; ++dj) {
+            if (di == 1 && dj == 0) continue;
+            const float u = t[q + di][tc + dj];
+            gt &= v > u;
+            lt &= v < u;
+          }
+        // a maximum counts when positive, a minimum when negative (|v| >= thr
+        // alone would admit a positive local minimum)
+        if ((gt && v >= thr) || (lt && -v >= thr)) m |= 1u << i;
+      }
     }
-    const float vv[4] = {v, 0.f, 0.f, 0.f};  // (q is warp-uniform: the whole warp calls)
-    cand_push_warp(&ccount, cy, cx, cv, kNmsCand, st, gy, gx, gv, gcap, m, r, cc, vv);
+    cand_push_warp(&ccount, cy, cx, cv, kNmsCand, st, gy, gx, gv, gcap, m, r, c0 + 4 * lane, vv);
   }
   __syncthreads();
   __shared__ int flush_base;
