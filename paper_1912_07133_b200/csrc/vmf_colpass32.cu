@@ -740,7 +740,9 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
   }
   pdl_wait();  // band start states, Ky and the CandState come from earlier kernels
   // lower bounds of max |L|: the band scan's boundary rows, the earlier CTAs
-  const float gbound = fmaxf(__uint_as_float(st->bound_bits), __uint_as_float(st->absmax_bits));
+  // (combined only where the threshold is formed: the loads' latency hides
+  // behind the walks)
+  const unsigned gb_scan = st->bound_bits, gb_max = st->absmax_bits;
   Rec32<K, KIND> rf, rbt;
   float ub1[K], mid[K];
 #pragma unroll
@@ -846,7 +848,8 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
   if (lane == 0) atomicMax(&S.cmax, __float_as_uint(tmax));
   __syncthreads();
   if (j == 0) atomicMax(&st->absmax_bits, S.cmax);
-  const float gnow = fmaxf(gbound, __uint_as_float(gmid));
+  const float gnow = fmaxf(fmaxf(__uint_as_float(gb_scan), __uint_as_float(gb_max)),
+                           __uint_as_float(gmid));
   {
     const int64_t rhi = r1 < H ? r1 : H;
     const int nrow = (int)(rhi - r0);
@@ -874,8 +877,20 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
       const bool act = lane < kC32Out / 4;
       const uint64_t lpol = l2_policy_evict_first();
       float *dst = Lout ? Lout + r0 * ldl + c0 + 4 * lane : nullptr;
+      bool any = true;
+      if (!dst) {  // detections only: one vote over the warp's rows first
+        float mx = 0.0f;
+        if (act) {
 #pragma unroll 4
-      for (int q = wid; q < nrow; q += kC32 / 32) {
+          for (int q = wid; q < nrow; q += kC32 / 32) {
+            const float4 v = *reinterpret_cast<const float4 *>(&S.tile[q + 1][4 + 4 * lane]);
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          }
+        }
+        any = __any_sync(0xffffffffu, mx >= th);
+      }
+#pragma unroll 4
+      for (int q = wid; any && q < nrow; q += kC32 / 32) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (act) {
           v = *reinterpret_cast<const float4 *>(&S.tile[q + 1][4 + 4 * lane]);
