@@ -485,6 +485,7 @@ int vmf_blur_lap_detect(const void *x, int x_dtype, int64_t h, int64_t w, int64_
   if (x_dtype == VMF_F32 && row_stage->kind == VMF_STAGE_FIR && col_stage->kind == VMF_STAGE_FIR &&
       !getenv("VMF_FORCE_GENERIC") && firtc_supported(h, w, ldx, row_stage->n, col_stage->n) &&
       ((uintptr_t)x & 15) == 0 &&
+      !getenv("VMF_NO_FIRTC") &&  // (tests: the fp64 fused FIR pass at any length)
       (force_tc || (row_stage->n > col_stage->n ? row_stage->n : col_stage->n) >= kFirTcMinTaps)) {
     // both FIR passes on the tensor cores, Laplacian first, then stage 4
     // (vmf_firtc.cu)

@@ -33,7 +33,9 @@
 namespace vmf {
 
 constexpr int kTcMaxK = 192;       // FIR half-length (taps <= 385)
-constexpr int kFirTcMinTaps = 65;  // below, the fp64 CUDA-core FIR (vmf_firpass.cu) is faster
+// below, the fp64 CUDA-core FIR (vmf_firpass.cu) is faster: at 4096^2, 17 taps
+// 124.9k vs 117.0k Mpixel/s on the tensor cores; 33 taps 104.6k vs 117.4k
+constexpr int kFirTcMinTaps = 33;
 
 // true if the tensor-core FIR path takes this frame and these stages
 bool firtc_supported(int64_t h, int64_t w, int64_t ldx, int row_taps, int col_taps);

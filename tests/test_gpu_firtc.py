@@ -108,7 +108,7 @@ def test_firtc_default_dispatch(cat, monkeypatch):
 
     monkeypatch.delenv("VMF_FORCE_FIRTC")
     x = _frame(256, 256, 8)
-    for name, tc in (("g2_k8", False), ("g16_k64", True)):
+    for name, tc in (("g2_k8", False), ("g4_k16", True), ("g16_k64", True)):
         _lib.profile_begin()
         detect.blur_laplacian_detect(x, cat[name])
         torch.cuda.synchronize()

@@ -341,7 +341,7 @@ def test_stream_detect_matches_per_frame(cat):
 
 
 @pytest.mark.parametrize("ntaps", [1, 3, 5, 7, 9, 11, 13, 15, 19, 23, 29, 41, 63, 71, 101])
-def test_fir_every_tap_remainder(ntaps):
+def test_fir_every_tap_remainder(ntaps, monkeypatch):
     """The register-blocked FIR runs taps in blocks of 8 and the last n % 8
     taps separately (1: from the samples already in the window; 2..4: a half
     block; 5..7: a full block over zero-padded taps), with the row window
@@ -361,7 +361,9 @@ def test_fir_every_tap_remainder(ntaps):
     yy, xx = np.ogrid[:301, :517]
     for cy, cx in ((40, 60), (150, 300), (280, 500)):
         y += np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / 18.0).astype(np.float32)
-    _check_pipeline(y, f, label=f"fir {ntaps} taps")
+    _check_pipeline(y, f, label=f"fir {ntaps} taps")  # (tensor cores from 33 taps)
+    monkeypatch.setenv("VMF_NO_FIRTC", "1")  # the fp64 fused FIR column pass at every length
+    _check_pipeline(y, f, label=f"fir {ntaps} taps (fp64 fused pass)")
 
 
 def test_fir_fused_long_taps(cat):
