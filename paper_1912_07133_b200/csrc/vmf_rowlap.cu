@@ -539,6 +539,17 @@ __global__ void __maxnreg__(168) sweep_rows_kernel(  // (3 CTAs of 128 threads p
     TLROW(i, 2);
     for (int s = 0; s < ns; ++s) {
 #if VMF_ABL == 0
+      if (rm.store_inline == 2) {
+        if (sp[s].sign > 0.f)
+          row_walks32_pair<K, KIND, true>(sp[s], C, U, cfs(s), cbs(s), dx2[s],
+                                          out.V(s) + r * out.ldv + c * kRChunk, live,
+                                          l2_policy_evict_last());
+        else
+          row_walks32_pair<K, KIND, false>(sp[s], C, U, cfs(s), cbs(s), dx2[s],
+                                           out.V(s) + r * out.ldv + c * kRChunk, live,
+                                           l2_policy_evict_last());
+        continue;
+      }
       if (rm.store_inline) {
         row_walks32_store<K, KIND>(RC32<K>(sp[s]), C, U, cfs(s), cbs(s), dx2[s],
                                    out.V(s) + r * out.ldv + c * kRChunk, live,
@@ -848,7 +859,7 @@ static int launch_sweep(const float *x, int64_t ldx, SweepPlan &P, const SweepOu
   const int rslots = slots > rm.ns ? slots - rm.ns : 1;
   rm.rows_per = (int)cdiv(rm.H, rslots);
   rm.carry_fold = getenv("VMF_CARRY_REC") ? 0 : 1;
-  rm.store_inline = getenv("VMF_STORE_AFTER") ? 0 : 1;
+  rm.store_inline = getenv("VMF_STORE_AFTER") ? 0 : getenv("VMF_WALK_SEQ") ? 1 : 2;
   const int grid = (int)cdiv(rm.H, rm.rows_per) + rm.ns;
   Launch g(K_SWEEP_ROWS, st);
   launch_pdl(sweep_rows_kernel<K, KIND>, dim3(grid), dim3(block), smem, st, xm,

@@ -48,7 +48,8 @@ struct RowLapMulti {
   int64_t H, W;
   int C, rows_per;
   int carry_fold;              // chunk carries as folded packed-FMA sums (else recursions)
-  int store_inline;            // V stored in 8-sample groups during the forward walk
+  int store_inline;            // V stored in 8-sample groups during the walk (2: the two
+                               // directions paired on packed FMAs, 1: walked in turn)
 };
 
 struct BorderScale {   // per scale, for the border kernel
@@ -132,6 +133,15 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
       "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
       : "=f"(d.x), "=f"(d.y)
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
 
@@ -312,6 +322,80 @@ __device__ __forceinline__ void row_walks32_store(const RC32<K> &rc, int C,
     if (q == 0 && c == 0) v[0] += dx2[0];
     if (q == kRChunk / 8 - 1 && c == C - 1) v[7] -= dx2[1];
     if (live) st_v8_hint(dst + 8 * q, v, pol);
+  }
+}
+
+// row_walks32_store with the two directions as the lanes of packed FMAs:
+// step j runs the forward recursion at sample j and the backward one at
+// 31 - j on the same pole (a broadcast operand), so each step is 2K + 1
+// FFMA2 for both walks (4K + 1 FFMA per sample when walked one after the
+// other).  Steps 0..15 park the pairs (fwd(j), bwd(31-j)) -- outputs without
+// the b0 U term; at step 16 the state pairs swap halves, and steps 16..31
+// start from the parked halves plus b0 U (both lanes, broadcast b0), so the
+// pair of step j is (V(31-j), V(j)) and V completes from the middle out (two
+// 8-sample groups after step 23, the last two after step 31).  The park
+// stays 32 registers.  Per lane the terms are the single-walk ones; only the
+// order in which b0 U and the two directions' sums are added differs.
+// SYM (sign +1, every blur): cs = c, so the output vectors broadcast too.
+template <int K, int KIND, bool SYM>
+__device__ __forceinline__ void row_walks32_pair(const RowLapParams &P, int C,
+                                                 const float (&U)[kRChunk], const float *cf,
+                                                 const float *cb, const float *dx2, float *dst,
+                                                 bool live, uint64_t pol) {
+  const int c = threadIdx.x;
+  float2 u[K], cc[K], cx[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    u[i] = make_float2(cf[c * K + i], cb[c * K + i]);
+    cc[i] = SYM ? make_float2(P.c[i], P.c[i]) : make_float2(P.c[i], P.cs[i]);
+    cx[i] = SYM ? cc[i] : make_float2(P.cs[i], P.c[i]);
+  }
+  const float2 p2 = make_float2(P.p, P.p), q2 = make_float2(P.q, P.q),
+               nq2 = make_float2(-P.q, -P.q), b02 = make_float2(P.b0, P.b0);
+  auto step = [&](float2 x2) {
+    if (KIND == M32_JORDAN) {
+      u[0] = ffma2(p2, u[0], x2);
+#pragma unroll
+      for (int i = 1; i < K; ++i) u[i] = ffma2(p2, u[i], u[i - 1]);
+    } else {
+      const float2 ur = u[0], ui = u[1];
+      u[0] = ffma2(p2, ur, ffma2(nq2, ui, x2));
+      u[1] = ffma2(q2, ur, fmul2(p2, ui));
+    }
+  };
+  float2 pk[kRChunk / 2];
+#pragma unroll
+  for (int j = 0; j < kRChunk / 2; ++j) {
+    const float2 x2 = make_float2(U[j], U[kRChunk - 1 - j]);
+    float2 o = fmul2(cc[0], u[0]);
+#pragma unroll
+    for (int i = 1; i < K; ++i) o = ffma2(cc[i], u[i], o);
+    pk[j] = o;  // (fwd(j), bwd(31-j)) without b0 U
+    step(x2);
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) u[i] = make_float2(u[i].y, u[i].x);  // (bwd, fwd)
+  float lo[8], hi[8];
+#pragma unroll
+  for (int j = kRChunk / 2; j < kRChunk; ++j) {
+    const int m = kRChunk - 1 - j;
+    const float2 x2 = make_float2(U[m], U[j]);
+    float2 o = ffma2(b02, x2, pk[m]);  // (fwd(m) + b0 U(m), bwd(j) + b0 U(j))
+#pragma unroll
+    for (int i = 0; i < K; ++i) o = ffma2(cx[i], u[i], o);  // (V(m), V(j))
+    step(x2);
+    const int g = (j - kRChunk / 2) & 7;
+    lo[7 - g] = o.x;  // V(m): m = 15 - g (first group) or 7 - g (second)
+    hi[g] = o.y;      // V(j): j = 16 + g or 24 + g
+    if (g == 7) {
+      const bool last = j == kRChunk - 1;
+      if (last && c == 0) lo[0] += dx2[0];
+      if (last && c == C - 1) hi[7] -= dx2[1];
+      if (live) {
+        st_v8_hint(dst + (last ? 0 : 8), lo, pol);
+        st_v8_hint(dst + (last ? 24 : 16), hi, pol);
+      }
+    }
   }
 }
 
