@@ -678,6 +678,73 @@ __global__ void __launch_bounds__(2 * kC32) colcarry32v_kernel(const float *__re
   }
 }
 
+// One 32-row half of the apply with the two directions as the lanes of
+// packed FMAs (the row pass's row_walks32_pair on a tile column): step j runs
+// the forward recursion at half row j and the backward one at 31 - j; steps
+// 0..15 park (fwd(j), bwd(31-j)) without the b0 V term, the state pairs swap
+// halves, and steps 16..31 finish (L(31-j), L(j)) from the parked halves and
+// write them over V in the tile (rows still to be read lie outside the
+// written middle).  In: uf / ub the half's start states; out: the end states
+// (uf after the half's last row, ub = ub(first row)).
+template <int K, int KIND, bool SYM, bool LSC>
+__device__ __forceinline__ void col_half_pair(float *tc, int base, const Col32Params &p,
+                                              float (&uf)[K], float (&ub)[K], float &tmax) {
+#define TVH(q) tc[(base + (q)) * kT32Stride]
+  float2 u[K], cc[K], cx[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    u[i] = make_float2(uf[i], ub[i]);
+    cc[i] = SYM ? make_float2(p.c[i], p.c[i]) : make_float2(p.c[i], p.cs[i]);
+    cx[i] = SYM ? cc[i] : make_float2(p.cs[i], p.c[i]);
+  }
+  const float2 p2 = make_float2(p.p, p.p), q2 = make_float2(p.q, p.q),
+               nq2 = make_float2(-p.q, -p.q), b02 = make_float2(p.b0, p.b0),
+               l2 = make_float2(p.lsc, p.lsc);
+  auto step = [&](float2 x2) {
+    if (KIND == M32_JORDAN) {
+      u[0] = ffma2(p2, u[0], x2);
+#pragma unroll
+      for (int i = 1; i < K; ++i) u[i] = ffma2(p2, u[i], u[i - 1]);
+    } else {
+      const float2 ur = u[0], ui = u[1];
+      u[0] = ffma2(p2, ur, ffma2(nq2, ui, x2));
+      u[1] = ffma2(q2, ur, fmul2(p2, ui));
+    }
+  };
+  constexpr int N = kB32 / 2;
+  float2 pk[N / 2];
+#pragma unroll
+  for (int j = 0; j < N / 2; ++j) {
+    const float2 x2 = make_float2(TVH(j), TVH(N - 1 - j));
+    float2 o = fmul2(cc[0], u[0]);
+#pragma unroll
+    for (int i = 1; i < K; ++i) o = ffma2(cc[i], u[i], o);
+    pk[j] = o;
+    step(x2);
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) u[i] = make_float2(u[i].y, u[i].x);  // (bwd, fwd)
+#pragma unroll
+  for (int j = N / 2; j < N; ++j) {
+    const int m = N - 1 - j;
+    const float2 x2 = make_float2(TVH(m), TVH(j));
+    float2 o = ffma2(b02, x2, pk[m]);
+#pragma unroll
+    for (int i = 0; i < K; ++i) o = ffma2(cx[i], u[i], o);  // (L(m), L(j))
+    step(x2);
+    if (LSC) o = fmul2(l2, o);
+    TVH(m) = o.x;
+    TVH(j) = o.y;
+    tmax = fmaxf(tmax, fmaxf(fabsf(o.x), fabsf(o.y)));
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    ub[i] = u[i].x;
+    uf[i] = u[i].y;
+  }
+#undef TVH
+}
+
 // Apply: one CTA = 128 columns x one band; the tile holds V rows r0-1 .. r1
 // (TMA box at column c0-4); L is written in place (each column is private to
 // its thread), then the owned 124 x 64 block leaves fused with the 3x3 NMS.
@@ -779,54 +846,47 @@ __global__ void __launch_bounds__(kC32, 5) colapply32v_kernel(
   // a fresher global maximum for the NMS threshold below, loaded now so its
   // latency hides behind the walks
   const unsigned gmid = *(volatile unsigned *)&st->absmax_bits;
-  float park[kB32 / 2];
   // ---- top half: rows r0 .. r0+31 (and the halo row r0-1)
+  float uf[K], ub[K], hf = 0.0f;
 #pragma unroll
-  for (int t = kB32 / 2 - 1; t >= 0; --t) {
-    const float v = TV(t + 1);
-    park[t] = rbt.out_from(p.cs, b0 * v);  // b0 V + s y-
-    rbt.step(p, v);
+  for (int i = 0; i < K; ++i) {
+    uf[i] = rf.u[i];
+    ub[i] = rbt.u[i];
+    hf = fmaf(p.ci[i], uf[i], hf);  // c A^-1 uf(r0-1): the halo row's forward part
   }
+  auto walk_half = [&](int base) {
+    if (p.sign > 0.0f)
+      col_half_pair<K, KIND, true, LSC>(tc, base, p, uf, ub, tmax);
+    else
+      col_half_pair<K, KIND, false, LSC>(tc, base, p, uf, ub, tmax);
+  };
+  walk_half(1);
   if (r0 > 0) {  // L(r0-1): y+(r0-1) = c A^-1 uf(r0-1) - e1 V(r0-1); y-(r0-1) = c ub(r0)
     const float v = TV(0);
-    const float w = fmaf(-p.e1, v, rf.out_from(p.ci, rbt.out_from(p.cs, b0 * v)));
-    TV(0) = fin(w);
-  }
+    float a = fmaf(b0, v, hf);
 #pragma unroll
-  for (int t = 0; t < kB32 / 2; ++t) {
-    const float v = TV(t + 1);
-    const float w = fin(rf.out_from(p.c, park[t]));
-    rf.step(p, v);
-    TV(t + 1) = w;
-    tmax = fmaxf(tmax, fabsf(w));  // (a partial band re-takes it below)
+    for (int i = 0; i < K; ++i) a = fmaf(p.cs[i], ub[i], a);
+    TV(0) = fin(fmaf(-p.e1, v, a));
   }
   // ---- bottom half: rows r0+32 .. r1-1 (and the halo row r1)
-  Rec32<K, KIND> rb;
-#pragma unroll
-  for (int i = 0; i < K; ++i) rb.u[i] = ub1[i];
   float ym_below;
   {
     const float v = TV(kB32 + 1);  // y-(r1) = c A^-1 ub(r1) - e1 V(r1)
-    ym_below = fmaf(-p.e1, v, rb.out(p.ci));
-  }
+    float a = 0.0f;
 #pragma unroll
-  for (int t = kB32 / 2 - 1; t >= 0; --t) {
-    const float v = TV(kB32 / 2 + 1 + t);
-    park[t] = rb.out_from(p.cs, b0 * v);
-    rb.step(p, v);
+    for (int i = 0; i < K; ++i) {
+      ub[i] = ub1[i];
+      a = fmaf(p.ci[i], ub1[i], a);
+    }
+    ym_below = fmaf(-p.e1, v, a);
   }
-#pragma unroll
-  for (int t = 0; t < kB32 / 2; ++t) {
-    const float v = TV(kB32 / 2 + 1 + t);
-    const float w = fin(rf.out_from(p.c, park[t]));
-    rf.step(p, v);
-    TV(kB32 / 2 + 1 + t) = w;
-    tmax = fmaxf(tmax, fabsf(w));
-  }
+  walk_half(kB32 / 2 + 1);
   {
     const float v = TV(kB32 + 1);
-    const float w = rf.out_from(p.c, fmaf(b0, v, p.sign * ym_below));
-    TV(kB32 + 1) = fin(w);
+    float a = fmaf(b0, v, p.sign * ym_below);
+#pragma unroll
+    for (int i = 0; i < K; ++i) a = fmaf(p.c[i], uf[i], a);
+    TV(kB32 + 1) = fin(a);
   }
   // the border rows' terms: L(0) += Ky[0], L(H-1) -= Ky[1] (tile row r - r0 + 1)
   const bool bot = H - 1 >= r0 - 1 && H - 1 <= r1;

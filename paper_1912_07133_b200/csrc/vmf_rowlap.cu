@@ -106,7 +106,7 @@ __device__ __forceinline__ int hidx(int n) { return n + (n >> 5); }  // padded h
 constexpr int kSeg = 64;
 
 template <int K, int KIND>
-__global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant__ BorderMulti bm,
+__global__ void __launch_bounds__(128, 7) sweep_border_kernel(const __grid_constant__ BorderMulti bm,
                                                            const float *__restrict__ X,
                                                            int64_t ldx, int64_t H, int64_t W,
                                                            SweepOut out) {
@@ -168,46 +168,67 @@ __global__ void __launch_bounds__(128) sweep_border_kernel(const __grid_constant
   const int64_t cc = col < W ? col : W - 1;
   const int m0 = 1 + kSeg * k;
   const int n = (bm.maxMh - m0 + 1) < kSeg ? (bm.maxMh - m0 + 1) : kSeg;  // m = m0 .. m0+n-1
-  // top: xs[t] = X(m0 - 1 + t); bottom: xs[t] = X(H - m0 - t); all loaded
-  // before the recursions (independent loads)
-  float xs[kSeg + 1];
+  // top: xs[t] = X(m0 - 1 + t); bottom: xs[t] = X(H - m0 - t).  The segment
+  // goes in two 32-row halves (t = 32..64, then 0..32), each loaded whole
+  // before the recursions (independent loads), every scale's state carried
+  // across: 33 staged rows keep the kernel at 72 registers, so the ~1k CTAs
+  // are one wave (the whole segment staged took 96 registers: 1.25 waves)
+  constexpr int kH = kSeg / 2;
+  float xs[kH + 1];
   const float *Xc = X + cc;
   // rows r(t) = r0 + dir t, t = 0..n; the common segment (whole, inside the
   // frame) walks one pointer by a 32-bit stride, the rest clamps per row
   const int64_t r0 = which == 0 ? m0 - 1 : H - m0;
   const int64_t rend = which == 0 ? r0 + n : r0 - n;
-  if (n == kSeg && r0 >= 0 && r0 < H && rend >= 0 && rend < H && (int64_t)kSeg * ldx < (1 << 29)) {
-    const float *p = Xc + r0 * ldx;
-    const int step = which == 0 ? (int)ldx : -(int)ldx;
+  const bool fast =
+      n == kSeg && r0 >= 0 && r0 < H && rend >= 0 && rend < H && (int64_t)kSeg * ldx < (1 << 29);
+  Rec32<K, KIND> u[kMaxScales];
 #pragma unroll
-    for (int t = 0; t <= kSeg; ++t) xs[t] = __ldg(p + t * step);
-  } else {
+  for (int s = 0; s < kMaxScales; ++s)
 #pragma unroll
-    for (int t = 0; t <= kSeg; ++t) {  // t > n repeats row n: G = 0 there
-      const int tt = t < n ? t : n;
-      const int64_t r = which == 0 ? m0 - 1 + tt : H - m0 - tt;
-      xs[t] = __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx);
+    for (int i = 0; i < K; ++i) u[s].u[i] = 0.0f;
+#pragma unroll
+  for (int hh = 1; hh >= 0; --hh) {
+    const int t0 = kH * hh;
+    if (fast) {
+      const int step = which == 0 ? (int)ldx : -(int)ldx;
+      const float *p = Xc + r0 * ldx + (int64_t)t0 * step;
+#pragma unroll
+      for (int t = 0; t <= kH; ++t) xs[t] = __ldg(p + t * step);
+    } else {
+#pragma unroll
+      for (int t = 0; t <= kH; ++t) {  // t > n repeats row n: G = 0 there
+        const int tt = t0 + t < n ? t0 + t : n;
+        const int64_t r = which == 0 ? m0 - 1 + tt : H - m0 - tt;
+        xs[t] = __ldg(Xc + (r < 0 ? 0 : (r >= H ? H - 1 : r)) * ldx);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kMaxScales; ++s) {
+      if (s >= bm.ns) break;
+      const BorderScale &b = bm.s[s];
+      if (k >= b.sv.nseg) continue;
+      const int ns_ = (b.sv.Mh - m0 + 1) < kSeg ? (b.sv.Mh - m0 + 1) : kSeg;  // this scale's rows
+      // G(m0 + t): top X(m0+t) - X(m0+t-1) = xs[t+1] - xs[t]; bottom
+      // X(H-m0-t) - X(H-m0-t-1) = -(xs[t+1] - xs[t]): the sign goes on the share.
+      // Steps t >= ns_ see G = 0 on a zero state.
+      if (ns_ == kSeg) {
+#pragma unroll
+        for (int t = kH - 1; t >= 0; --t) u[s].step(b, xs[t + 1] - xs[t]);
+      } else {
+#pragma unroll
+        for (int t = kH - 1; t >= 0; --t)
+          u[s].step(b, t0 + t < ns_ ? xs[t + 1] - xs[t] : 0.0f);
+      }
     }
   }
-  for (int s = 0; s < bm.ns; ++s) {
+#pragma unroll
+  for (int s = 0; s < kMaxScales; ++s) {
+    if (s >= bm.ns) break;
     const BorderScale &b = bm.s[s];
     const int nseg = b.sv.nseg;
     if (k >= nseg) continue;
-    const int ns_ = (b.sv.Mh - m0 + 1) < kSeg ? (b.sv.Mh - m0 + 1) : kSeg;  // this scale's rows
-    Rec32<K, KIND> u;
-#pragma unroll
-    for (int i = 0; i < K; ++i) u.u[i] = 0.0f;
-    // G(m0 + t): top X(m0+t) - X(m0+t-1) = xs[t+1] - xs[t]; bottom
-    // X(H-m0-t) - X(H-m0-t-1) = -(xs[t+1] - xs[t]): the sign goes on the share.
-    // Steps t >= ns_ see G = 0 on a zero state.
-    if (ns_ == kSeg) {
-#pragma unroll
-      for (int t = kSeg - 1; t >= 0; --t) u.step(b, xs[t + 1] - xs[t]);
-    } else {
-#pragma unroll
-      for (int t = kSeg - 1; t >= 0; --t) u.step(b, t < ns_ ? xs[t + 1] - xs[t] : 0.0f);
-    }
-    float v = u.out(b.sv.v[k]);
+    float v = u[s].out(b.sv.v[k]);
     v *= which == 0 ? b.sign : -1.0f;
     if (col < W) out.E(s)[kExS * W + ((int64_t)which * nseg + k) * W + col] = v;
   }

@@ -124,27 +124,6 @@ __device__ __forceinline__ void row_carry32(const RC32<K> &rc, const float (&U)[
   }
 }
 
-// Packed fp32 FMA (sm_100 FFMA2: two lanes' worth of FMAs per issue slot):
-// (a.x b.x + c.x, a.y b.y + c.y).
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
-__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
-  float2 d;
-  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-
 // The zero-state chunk carries of one scale from the row's folded sample
 // pairs sd[t] = (U(t) + U(31-t), U(t) - U(31-t)) (formed once per row for
 // every scale): (P_i, Q_i) = sum_t (SP_it, SQ_it) * sd[t] as packed FMAs
