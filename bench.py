@@ -204,7 +204,7 @@ DFMA_PEAK_T = 16.44  # T fp64 FMA/s: profiles/r1_pipes.txt (tools/microbench/pip
 N_SM = 148
 
 
-FIRTC_MIN_TAPS = 65  # vmf_firtc.cuh kFirTcMinTaps: from here the FIR runs on the tensor cores
+FIRTC_MIN_TAPS = 33  # vmf_firtc.cuh kFirTcMinTaps: from here the FIR runs on the tensor cores
 
 
 def compute_roofline(per_scale, sweep_value, sm_mhz):
